@@ -1,0 +1,388 @@
+#!/usr/bin/env python3
+"""Benchmark of the MRIP replication runner (BASELINE.json metric: replications/sec per
+model on 1/2/4/8 B200, with warp-exec efficiency / ALU-issue fraction from ncu).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
+
+Workload (a "step"): BASELINE config 2 — Monte-Carlo pi, 10^6 replications x 10^4 draws
+per GPU (weak scaling: rank g runs slots [g*10^6, (g+1)*10^6) of one run of N*10^6
+replications), master seed 42, WLP mapping: exact random-spacing seeding on device +
+the WLP replication kernel + the two-pass device statistics of the outputs, merged
+across ranks (all_gather of sufficient statistics), -> mean / 95% CI.
+
+  value  device-resident: outputs stay in HBM, CUDA events on the launching stream over
+         exactly K steps after W warm-ups, barrier + synchronize on both sides, max over
+         ranks. Inputs (the replications' 12-byte stream seeds) are generated in the step.
+         The 8 MB output per GPU and the 120 MB of seeds are far below L2 capacity
+         reuse distance: every step rewrites them (config "l2": "inputs regenerated").
+  e2e    the same metric through the reference-facing call with HOST buffers: at N=1
+         wlp_run (run_model) writing per-replication outputs to pinned host memory + device
+         CI; at N>1 the sharded step plus the D2H of the shard's outputs. Wall clock
+         (perf_counter with synchronize), max over ranks.
+
+Extras (N=1): WLP and TLP rates for every model/config of BASELINE (2, 3, 4), the
+ALU-issue roofline of the dominant kernel, and the CPU baseline (the reference's own
+replication functions, oracle/_ref, on all host cores, bounded sample).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "replications/sec (pi, 1e6 reps x 1e4 draws per GPU, WLP)"
+UNIT = "replications/s"
+R_PER_GPU = 1_000_000
+DRAWS = 10_000
+SEED = 42
+
+# Algorithmic instruction counts per unit (issue slots of one lane), see DESIGN.md §roofline:
+# one taus88 draw = 16 SASS (6 IMAD.SHL, 3 shift-merge, 7 LOP3); pi point = 2 draws +
+# 2 exact u32->f64 + 2 DMUL + DADD + DSETP + count = 39; walk step = 2 draws + shift +
+# 2 compare/add = 35.
+INSTR_PER_UNIT = {0: 39, 2: 35}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------------------------
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.flush()
+        rows = [r.split(", ") for r in Path(self.f.name).read_text().splitlines() if r.strip()]
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) >= 9 for i in range(4) if r[5 + i].strip() == "Active"})
+        loaded = [s for s in sm if mx and s >= 0.5 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def measured_peaks() -> dict:
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+def ncu_traffic() -> dict:
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu summary."""
+    try:
+        return json.loads((ROOT / "profiles" / "ncu_summary.json").read_text())
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------------------------------------
+
+
+def dist_setup():
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def device_timed(step, steps: int, warmup: int, world: int):
+    """CUDA-event time per step over exactly `steps` steps (after `warmup`), max over ranks."""
+    import torch
+
+    for _ in range(warmup):
+        step()
+    barrier(world)
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(steps):
+        step()
+    e1.record(s)
+    torch.cuda.synchronize()
+    barrier(world)
+    return max_over_ranks(e0.elapsed_time(e1) / steps, world)
+
+
+def wall_timed(step, steps: int, warmup: int, world: int):
+    import torch
+
+    for _ in range(warmup):
+        step()
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    torch.cuda.synchronize()
+    t = (time.perf_counter() - t0) * 1e3 / steps
+    barrier(world)
+    return max_over_ranks(t, world)
+
+
+# ---------------------------------------------------------------------------------------------
+
+
+def cpu_baseline(model: int, p, budget_s: float = 15.0, steps: int = 1):
+    """The reference's own host path (oracle/_ref = proj/src compiled unmodified):
+    random_spacing (sequential, as in the reference) + the replication functions on all
+    host threads (they are pure), on a bounded sample of the workload."""
+    import oracle
+
+    ref = oracle.Oracle("reference") if oracle.available("reference") else oracle.Oracle("port")
+    kind = "reference" if ref.kind == "reference" else "port"
+    nth = os.cpu_count() or 1
+    op = oracle.params_from(p)
+
+    def run(S):
+        t0 = time.perf_counter()
+        keys = ref.random_spacing(SEED, S)
+        t1 = time.perf_counter()
+        if kind == "reference":
+            ref.replications(model, op, keys, nthreads=nth)
+        else:
+            ref.replications(model, op, keys)
+        t2 = time.perf_counter()
+        return t1 - t0, t2 - t1
+
+    S = 4 * nth
+    a, b = run(S)
+    per = (a + b) / S
+    S = int(max(4 * nth, min(p.replications, budget_s / max(per, 1e-9))))
+    S = max(nth, (S // nth) * nth)
+    tot = [run(S) for _ in range(steps)]
+    tsp = sum(x for x, _ in tot) / steps
+    trep = sum(y for _, y in tot) / steps
+    return {"value": S / (tsp + trep), "unit": UNIT, "cores": nth if kind == "reference" else 1, "kind": kind,
+            "sample": f"{S} of {p.replications} replications (seed {SEED}): random_spacing 1 thread "
+                      f"{tsp:.3f}s + replications on {nth if kind == 'reference' else 1} threads {trep:.3f}s",
+            "step_s": tsp + trep}
+
+
+def run_reference_arm(args):
+    """--impl reference: the reference CPU path on this box's host cores."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import paper_1501_01405_b200 as w
+
+    p = w.ModelParams(replications=R_PER_GPU * world, draws=DRAWS)
+    # one calibration/warm-up step sizes each step at ~6 s of CPU work, then exactly K steps
+    cal = cpu_baseline(0, p, budget_s=6.0)
+    rates = [cpu_baseline(0, p, budget_s=6.0)["value"] for _ in range(args.steps)]
+    v = statistics.mean(rates)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * p.replications / v,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32+f64",
+            "data": "synthetic (taus88 streams from master seed 42)",
+            "config": {"workload": "BASELINE config 2: pi, 1e6 replications x 1e4 draws per GPU",
+                       "replications": p.replications, "draws": DRAWS},
+            "cpu_baseline": {k: cal[k] for k in ("kind", "cores", "sample")} | {"value": v, "unit": UNIT},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------------
+
+
+def model_rate(w, model, p, mode, steps=5, warmup=3):
+    """Device-resident replications/s of one (model, mode) run on this GPU + kernel ms."""
+    import torch
+
+    from paper_1501_01405_b200 import OUTPUT_NAMES, SimReport
+
+    outs = [torch.empty(p.replications, dtype=torch.float64, device="cuda") for _ in OUTPUT_NAMES[model]]
+    kms = []
+
+    def step():
+        rep = SimReport()
+        w.run_shard(model, p, mode, SEED, 0, p.replications, outs, on_device=True, report=rep)
+        kms.append(rep.kernel_ms)
+
+    ms = device_timed(step, steps, warmup, 1)
+    k = kms[warmup:]
+    return {"reps_per_s": p.replications / (ms * 1e-3), "ms_per_run": ms, "kernel_ms": sum(k) / len(k)}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    import torch
+
+    import paper_1501_01405_b200 as w
+    from paper_1501_01405_b200 import distributed as D
+
+    world, rank, local = dist_setup()
+    model, mode = w.ModelKind.Pi, w.ExecutionMode.Wlp
+    R = R_PER_GPU * world
+    p = w.ModelParams(replications=R, draws=DRAWS)
+    stream = torch.cuda.current_stream().cuda_stream
+    comm = D._Comm(device="cuda")
+    kernel_ms: list = []
+    runner = D.gpu_runner(model, p, mode, SEED, stream=stream, kernel_ms=kernel_ms)
+    stats = D.gpu_stats(stream=stream)
+    result = {}
+
+    def step():
+        result["r"] = D.run_sharded(model, R, runner, stats, comm=comm)
+
+    clocks = Clocks(local)
+    clocks.start()
+    ms = device_timed(step, args.steps, args.warmup, world)
+    clk = clocks.stop()
+    k_ms = kernel_ms[args.warmup:]
+    kernel_avg = sum(k_ms) / len(k_ms)
+    kernel_avg = max_over_ranks(kernel_avg, world)
+    value = R / (ms * 1e-3)
+    # launches of our kernels per step: seed + model + 2 statistics passes (1 output)
+    launches = args.steps * 4
+    ci = result["r"].cis[0]
+
+    # ---- e2e through the reference-facing call with host buffers
+    count = result["r"].count
+    host = [torch.empty(count, dtype=torch.float64, pin_memory=True)]
+    if world == 1:
+        def e2e_step():
+            w.run_model_into(model, p, mode, SEED, [h.numpy() for h in host], on_device=False, ci_level=0.95)
+    else:
+        def e2e_step():
+            r = D.run_sharded(model, R, runner, stats, comm=comm)
+            host[0].copy_(r.outputs[0][:count], non_blocking=False)
+    e2e_ms = wall_timed(e2e_step, args.steps, min(args.warmup, 3), world)
+
+    # ---- roofline of the dominant kernel (ALU issue; no tensor cores on this path)
+    peaks = measured_peaks()
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    fmax = float(peaks.get("sm_max_mhz", 1965.0))
+    units = R_PER_GPU * DRAWS
+    achieved = units * INSTR_PER_UNIT[0] / 32 / (kernel_avg * 1e-3) / 1e9  # G warp-instr/s
+    peak = 4 * sms * fmax * 1e6 / 1e9
+    nc = ncu_traffic().get("k_wlp_lanes<0>", {})
+    roofline = {"bound": "issue", "kernel": "k_wlp_lanes<0> (pi WLP)", "achieved": achieved, "peak": peak,
+                "unit": "Gwarp-inst/s", "frac": achieved / peak, "traffic": nc.get("dram_bytes_per_launch"),
+                "algorithmic": f"{INSTR_PER_UNIT[0]} lane-instr/point x {units:.0e} points per launch / 32",
+                "peak_source": f"4 issue/clk x {sms} SMs x sm_max_mhz {fmax:.0f} (MEASURED_PEAKS.json); "
+                               "no tensor/HBM roofline applies (integer/fp64 ALU work)",
+                "kernel_ms": kernel_avg,
+                "frac_at_measured_clock": (achieved / (4 * sms * clk["sm_mhz"] * 1e-3)) if clk.get("sm_mhz") else None,
+                "hbm_gbs_output_writeout": (R_PER_GPU * 8 + 3 * 4 * R_PER_GPU) / (kernel_avg * 1e-3) / 1e9}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32+f64",
+            "data": "synthetic (taus88 streams by random spacing from master seed 42)",
+            "config": {"workload": "BASELINE config 2: pi, 1e6 replications x 1e4 draws per GPU, WLP",
+                       "replications": R, "draws": DRAWS, "mode": "wlp", "parallelism": f"shard{world}",
+                       "l2": "inputs regenerated every step (seeds 12 B/rep + outputs 8 B/rep)"},
+            "e2e": {"value": R / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 64 * world,
+                    "d2h_bytes_per_step": R * 8, "ms_per_step": e2e_ms,
+                    "note": "inputs are (master seed, params) by value; outputs D2H to pinned host"},
+            "gpu_launches": launches, "clocks": clk, "roofline": roofline,
+            "result": {"mean": ci.mean, "half_width": ci.halfWidth, "n": ci.n}}
+
+    if world == 1 and not args.no_extras:
+        extras = {}
+        cfgs = [("cfg2_pi_1e6x1e4", w.ModelKind.Pi, dict(replications=1_000_000, draws=10_000)),
+                ("cfg3_walk_1e5x1e3", w.ModelKind.Walk, dict(replications=100_000, steps=1000, chunks=30)),
+                ("cfg4_pi_1e7x1e3", w.ModelKind.Pi, dict(replications=10_000_000, draws=1000)),
+                ("cfg4_mm1_1e7x1e3", w.ModelKind.Mm1, dict(replications=10_000_000, clients=1000)),
+                ("cfg4_walk_1e7x1e3", w.ModelKind.Walk, dict(replications=10_000_000, steps=1000, chunks=30))]
+        for name, m, kw in cfgs:
+            pp = w.ModelParams(**kw)
+            extras[name] = {}
+            for md in (w.ExecutionMode.Wlp, w.ExecutionMode.Tlp):
+                r = model_rate(w, m, pp, md)
+                if m in INSTR_PER_UNIT:
+                    units_ = pp.replications * pp.units(m)
+                    r["issue_frac"] = units_ * INSTR_PER_UNIT[int(m)] / 32 / (r["kernel_ms"] * 1e-3) / (peak * 1e9)
+                extras[name][w.mode_name(md)] = r
+        line["extras"] = extras
+    if world == 1 and rank == 0 and not args.no_cpu:
+        line["cpu_baseline"] = {k: v for k, v in cpu_baseline(0, p).items() if k != "step_s"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,218 @@
+/*
+ * wlp_b200.h — C ABI of the B200 Multiple-Replications-in-Parallel engine
+ * (Warp-Level Parallelism, arXiv 1501.01405), libwlp_b200.so.
+ *
+ * Plain C: pointers, sizes, status codes; no C++ or torch types. Every entry point
+ * names the reference interface it replaces (paths relative to /root/reference/proj).
+ * The C++ drop-in (include/warpsim_b200.hpp) and the Python mirror
+ * (paper_1501_01405_b200/__init__.py) are thin layers over these calls.
+ *
+ * Execution: all model work runs in hand-written sm_100a kernels on the calling
+ * thread's current CUDA device (cudaSetDevice), on `stream` (a cudaStream_t, or NULL for
+ * the legacy default stream). There is no CPU fallback: without a usable GPU every
+ * compute call returns WLP_ECUDA.
+ *
+ * Buffers are caller-owned. `*_on_device` = 1 means the pointer is device memory on the
+ * current device and the call is asynchronous on `stream` unless stated otherwise;
+ * 0 means host memory (pageable or pinned) and the call returns with results written.
+ * The library owns its device scratch (released by wlp_shutdown).
+ *
+ * Thread safety: calls are serialised per device by an internal lock.
+ */
+#ifndef WLP_B200_H
+#define WLP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; the C++ layer rethrows them as the reference's exception types
+ * (include/warpsim/error.hpp:8-36). */
+#define WLP_OK 0
+#define WLP_EDOMAIN 1   /* DomainError: invalid params (models.cpp:26-44, rng.cpp:58-59)   */
+#define WLP_EPLAN 2     /* PlanError: launch planning (wlp.cpp:71-105)                     */
+#define WLP_EFAULT 3    /* FaultError: a device lane fault                                 */
+#define WLP_ESPACING 4  /* Error: random_spacing found no distinct seed (rng.cpp:81-82)    */
+#define WLP_ECUDA 5     /* Error: CUDA runtime failure / no device                         */
+#define WLP_EINTERNAL 7 /* Error: anything else                                            */
+
+/* ModelKind (models.hpp:18) and ExecutionMode (wlp.hpp:16). */
+#define WLP_MODEL_PI 0
+#define WLP_MODEL_MM1 1
+#define WLP_MODEL_WALK 2
+#define WLP_MODE_SEQUENTIAL 0
+#define WLP_MODE_TLP 1
+#define WLP_MODE_WLP 2
+
+/* ModelParams (models.hpp:23-31); defaults 1, 1000, 1000, 0.5, 1.0, 1000, 30. */
+typedef struct wlp_params {
+    int64_t replications;
+    int64_t draws;   /* pi: points per replication   */
+    int64_t clients; /* mm1                          */
+    double lambda;   /* mm1 arrival rate             */
+    double mu;       /* mm1 service rate             */
+    int64_t steps;   /* walk                         */
+    int64_t chunks;  /* walk                         */
+} wlp_params;
+
+/* LaunchConfig (kernel_ir.hpp:35-45), 1-D/2-D as the reference uses it. */
+typedef struct wlp_launch_cfg {
+    int64_t block_x, block_y, block_z;
+    int64_t grid_x, grid_y;
+    int32_t warp_size;
+} wlp_launch_cfg;
+
+/* SimReport (device.hpp:62-71). On the GPU: total_cycles = measured kernel time in SM
+ * cycles at the device's clock, waves_executed = ceil(blocks / resident capacity),
+ * peak_resident_warps = min(launch warps, resident capacity); the simulator-only
+ * counters (issues, memReads, ...) are 0 — ncu measures those. */
+typedef struct wlp_report {
+    int64_t total_cycles;
+    int64_t waves_executed;
+    int64_t peak_resident_warps;
+    uint64_t issues, alu_issues, mem_reads, mem_writes, divergence_events;
+    double kernel_ms; /* model-kernel time from CUDA events (0 when not timed) */
+} wlp_report;
+
+/* ConfidenceInterval (models.hpp:118-127). */
+typedef struct wlp_ci {
+    double mean;
+    double half_width;
+    double level;
+    int64_t n;
+    int32_t warn_small_sample; /* n < 30 */
+} wlp_ci;
+
+/* Sufficient statistics of one output array over a replication range: count, sum as an
+ * unevaluated double-double (hi + lo), and, after the second pass, the centred sum of
+ * squares about `center` (hi + lo). Shards combine these exactly (wlp_stats_merge). */
+typedef struct wlp_stats {
+    int64_t n;
+    double sum_hi, sum_lo;
+    double center;
+    double ss_hi, ss_lo;
+} wlp_stats;
+
+/* A seeding candidate whose stream key could collide with another's (some component
+ * below twice its minimum). `index` is the global candidate
+ * index (candidate i = remap(master draws 3i+1..3i+3)). */
+typedef struct wlp_special {
+    int64_t index;
+    uint32_t s1, s2, s3, pad;
+} wlp_special;
+
+/* ---- host-only utilities (no GPU needed) -------------------------------------- */
+
+const char* wlp_last_error(void);   /* message of the last failing call on this thread */
+int wlp_version(void);              /* ABI version (1)                                  */
+
+/* validate_params (models.cpp:26-44): WLP_EDOMAIN on invalid values; a non-empty
+ * warning (lambda >= mu) is copied into warn[cap]. */
+int wlp_validate_params(int model, const wlp_params* p, char* warn, int warn_cap);
+
+/* plan_launch (wlp.cpp:71-105): reference geometry per mode, PlanError above
+ * grid_limit (the reference default is 65535), partial-warp warning. */
+int wlp_plan_launch(int64_t replications, int mode, int tlp_block_size, int64_t grid_limit,
+                    wlp_launch_cfg* cfg, char* warn, int warn_cap);
+
+/* rng_state_from_seed (rng.cpp:36-40). */
+int wlp_master_from_seed(uint64_t seed, uint32_t state_out[3]);
+
+/* make_rng_state (rng.cpp:29-34). */
+int wlp_make_state(uint32_t s1, uint32_t s2, uint32_t s3, uint32_t state_out[3]);
+
+/* State after n taus_next calls (rng.cpp:42-51), by GF(2) jump-ahead on the host. */
+int wlp_jump_host(const uint32_t state[3], uint64_t n, uint32_t state_out[3]);
+
+/* inverse_normal_cdf (models.cpp:61-97). */
+int wlp_inverse_normal_cdf(double p, double* z);
+
+/* Exact rejection bookkeeping of random_spacing (rng.cpp:67-87) from the special
+ * candidates of all shards: sorts them by index, marks every candidate whose key equals
+ * an earlier accepted one, and merges with `prev`. Returns WLP_ESPACING if one stream
+ * would need 1000 redraws. out may alias nothing; cap >= n_prev + n_special. */
+int wlp_spacing_rejections(const wlp_special* specials, int64_t n_special, const int64_t* prev,
+                           int64_t n_prev, int64_t* out, int64_t out_cap, int64_t* n_out);
+
+/* Merge shard statistics (b into a), exactly in double-double. */
+int wlp_stats_merge(wlp_stats* a, const wlp_stats* b);
+
+/* confidence_interval (models.cpp:99-119) from merged second-pass statistics. */
+int wlp_ci_from_stats(const wlp_stats* s, double level, wlp_ci* ci);
+
+/* ---- device entry points --------------------------------------------------------- */
+
+int wlp_device_count(int* n);
+
+/* Raw taus88 stream: make_rng_state(s1,s2,s3) then n outputs of taus_next
+ * (rng.cpp:29-51; the taus88.golden format). Generated in parallel by jump-ahead. */
+int wlp_taus_stream(uint32_t s1, uint32_t s2, uint32_t s3, int64_t n, uint32_t* out,
+                    int out_on_device, void* stream);
+
+/* random_spacing(rng_state_from_seed(master_seed), R) (rng.cpp:67-87) for stream slots
+ * [slot_begin, slot_begin + count) of a run, given the global rejection list
+ * (sorted candidate indices, normally empty). Keys are written SoA: s[0..count) = s1,
+ * s[count..2count) = s2, s[2count..3count) = s3. Special candidates met while filling
+ * the slots are appended to specials (up to cap; *n_special gets the true count).
+ * Synchronous. For a whole run use slot_begin = 0, count = R and iterate with
+ * wlp_spacing_rejections until no new rejection appears (wlp_seed_streams_exact). */
+int wlp_seed_streams(uint64_t master_seed, int64_t slot_begin, int64_t count,
+                     const int64_t* rejected, int64_t n_rejected, uint32_t* s_out,
+                     int out_on_device, void* stream, wlp_special* specials,
+                     int64_t special_cap, int64_t* n_special);
+
+/* Whole-run exact random_spacing (iterates the rejection fixpoint internally). */
+int wlp_seed_streams_exact(uint64_t master_seed, int64_t count, uint32_t* s_out,
+                           int out_on_device, void* stream);
+
+/* Replications over caller-given streams (SoA s[3*count], host or device):
+ * pi_replication / mm1_replication / walk_replication (models.cpp:46-59) for each,
+ * mapped per `mode` (TLP: thread per replication; WLP and SEQUENTIAL: warp per
+ * replication). mm1 writes out0 = avgIdle, out1 = avgWaitQueue, out2 = avgSystem;
+ * pi and walk write out0 only. */
+int wlp_run_streams(int model, const wlp_params* p, int mode, const uint32_t* s, int64_t count,
+                    int s_on_device, double* out0, double* out1, double* out2,
+                    int out_on_device, void* stream, wlp_report* report);
+
+/* run_model (models.cpp:329-397) for a shard [r_begin, r_begin + r_count) of a run of
+ * p->replications: seeds the shard's streams on device (global rejection list as in
+ * wlp_seed_streams), runs the model in `mode`, writes per-replication outputs.
+ * Reports the shard's special candidates so the caller can check spacing collisions
+ * across shards and re-run with a rejection list in the (astronomically rare) case of
+ * one. Outputs on device: asynchronous unless report/specials are requested. */
+int wlp_run_shard(int model, const wlp_params* p, int mode, uint64_t master_seed,
+                  int tlp_block_size, int64_t r_begin, int64_t r_count, const int64_t* rejected,
+                  int64_t n_rejected, double* out0, double* out1, double* out2,
+                  int out_on_device, void* stream, wlp_special* specials, int64_t special_cap,
+                  int64_t* n_special, wlp_report* report);
+
+/* run_model (models.cpp:329-397), single device, whole run: exact seeding, model,
+ * outputs, optional report, and optional device-side confidence intervals of every
+ * output (ci array of 1 or 3 entries, NULL to skip) at `level`. The outputs-on-host
+ * form is the reference-facing call (e2e); warning text as in build_kernel
+ * (models.cpp:294-299). */
+int wlp_run(int model, const wlp_params* p, int mode, uint64_t master_seed, int tlp_block_size,
+            double* out0, double* out1, double* out2, int out_on_device, void* stream,
+            wlp_report* report, wlp_ci* ci, double level, char* warn, int warn_cap);
+
+/* Device statistics of a device array (pass 1: n and sum; pass 2: centred sum of
+ * squares about stats->center). Synchronous; n <= 256 sums sequentially, bit-identical
+ * to the reference's naive loop (models.cpp:104-109). */
+int wlp_stats_device(const double* x, int64_t n, int pass, wlp_stats* stats, void* stream);
+
+/* confidence_interval over a host array through the device reduction. */
+int wlp_confidence_interval(const double* samples, int64_t n, double level, wlp_ci* ci);
+
+/* Test hook: -log(1 - k[i]*2^-32) through the device glibc-log port (host arrays). */
+int wlp_debug_neg_log1m(const uint32_t* k, int64_t n, double* out);
+
+/* Release all device scratch of the current device. */
+int wlp_shutdown(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WLP_B200_H */

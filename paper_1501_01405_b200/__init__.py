@@ -1,0 +1,561 @@
+"""B200-native Multiple-Replications-in-Parallel engine (Warp-Level Parallelism, arXiv 1501.01405).
+
+Python mirror of the reference's replication-runner API (proj/include/warpsim/models.hpp,
+rng.hpp, wlp.hpp, error.hpp) over the C ABI of ``libwlp_b200.so`` (include/wlp_b200.h).
+Names, argument meaning and error types follow the reference:
+
+    run_model(ModelKind.Pi, ModelParams(replications=32, draws=100), ExecutionMode.Wlp,
+              DeviceProfile(), master_seed=42)                          # models.hpp:173-175
+    confidence_interval(run.primary)                                    # models.hpp:132
+
+Every model computation runs in the sm_100a kernels; there is no CPU path. Importing
+works without a GPU (host utilities such as plan_launch / validate_params run on the
+host, as in the reference); compute calls raise ``Error`` when no device is usable, and
+importing raises if the native library has not been built (``build.build_all()``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Optional, Sequence
+
+import numpy as np
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libwlp_b200.so"
+
+# ---- errors (error.hpp:8-36) ------------------------------------------------------------
+
+
+class Error(RuntimeError):
+    """warpsim::Error"""
+
+
+class DomainError(Error):
+    """Invalid arguments (warpsim::DomainError)."""
+
+
+class PlanError(Error):
+    """Launch planning failure (warpsim::PlanError)."""
+
+
+class FaultError(Error):
+    """A lane hit a runtime fault (warpsim::FaultError)."""
+
+
+class ParseError(Error):
+    """warpsim::ParseError"""
+
+
+class AnalysisError(Error):
+    """warpsim::AnalysisError"""
+
+
+OK, EDOMAIN, EPLAN, EFAULT, ESPACING, ECUDA, EINTERNAL = 0, 1, 2, 3, 4, 5, 7
+_EXC = {EDOMAIN: DomainError, EPLAN: PlanError, EFAULT: FaultError, ESPACING: Error, ECUDA: Error,
+        EINTERNAL: Error}
+
+# ---- enums and records --------------------------------------------------------------------
+
+
+class ModelKind(enum.IntEnum):  # models.hpp:18
+    Pi = 0
+    Mm1 = 1
+    Walk = 2
+
+
+class ExecutionMode(enum.IntEnum):  # wlp.hpp:16
+    Sequential = 0
+    Tlp = 1
+    Wlp = 2
+
+
+_MODEL_NAMES = {ModelKind.Pi: "pi", ModelKind.Mm1: "mm1", ModelKind.Walk: "walk"}
+_MODE_NAMES = {ExecutionMode.Sequential: "sequential", ExecutionMode.Tlp: "tlp", ExecutionMode.Wlp: "wlp"}
+OUTPUT_NAMES = {ModelKind.Pi: ("out",), ModelKind.Mm1: ("outIdle", "outWait", "outSys"), ModelKind.Walk: ("out",)}
+PRIMARY = {ModelKind.Pi: "out", ModelKind.Mm1: "outWait", ModelKind.Walk: "out"}  # models.cpp:304-324
+
+
+def model_name(m: ModelKind) -> str:
+    return _MODEL_NAMES[ModelKind(m)]
+
+
+def model_from_name(name: str) -> ModelKind:
+    for k, v in _MODEL_NAMES.items():
+        if v == name:
+            return k
+    raise DomainError(f"unknown model '{name}' (pi|mm1|walk)")
+
+
+def mode_name(m: ExecutionMode) -> str:
+    return _MODE_NAMES[ExecutionMode(m)]
+
+
+def mode_from_name(name: str) -> ExecutionMode:
+    for k, v in _MODE_NAMES.items():
+        if v == name:
+            return k
+    raise DomainError(f"unknown execution mode '{name}' (sequential|tlp|wlp)")
+
+
+@dataclass
+class ModelParams:  # models.hpp:23-31 (`lambda` is spelled lambda_ in Python)
+    replications: int = 1
+    draws: int = 1000
+    clients: int = 1000
+    lambda_: float = 0.5
+    mu: float = 1.0
+    steps: int = 1000
+    chunks: int = 30
+
+    def units(self, model: ModelKind) -> int:
+        return {ModelKind.Pi: self.draws, ModelKind.Mm1: self.clients, ModelKind.Walk: self.steps}[ModelKind(model)]
+
+
+@dataclass
+class RngState:  # rng.hpp:11-17
+    s1: int = 2
+    s2: int = 8
+    s3: int = 16
+
+
+@dataclass
+class DeviceProfile:  # device.hpp:19-28 — accepted for signature compatibility, ignored
+    numSMs: int = 14
+    warpSchedulersPerSM: int = 2
+    maxResidentBlocksPerSM: int = 8
+    maxResidentWarpsPerSM: int = 48
+    deviceResidentBlockCap: int = 64
+    aluIssueCycles: int = 1
+    memLatencyCycles: int = 400
+    maxThreadsPerBlock: int = 1024
+
+
+@dataclass
+class SimOptions:  # device.hpp:53-60 — accepted, ignored
+    smPermutationSeed: Optional[int] = None
+    maskStackDepth: int = 32
+
+
+@dataclass
+class SimReport:  # device.hpp:62-71; measured on the GPU (see wlp_report in wlp_b200.h)
+    totalCycles: int = 0
+    wavesExecuted: int = 0
+    peakResidentWarps: int = 0
+    issues: int = 0
+    aluIssues: int = 0
+    memReads: int = 0
+    memWrites: int = 0
+    divergenceEvents: int = 0
+    kernel_ms: float = 0.0
+
+
+@dataclass
+class LaunchConfig:  # kernel_ir.hpp:35-45
+    blockDim: tuple = (1, 1, 1)
+    gridDim: tuple = (1, 1)
+    warpSize: int = 32
+
+
+@dataclass
+class LaunchPlan:  # wlp.hpp:38-43
+    cfg: LaunchConfig
+    replications: int
+    mode: ExecutionMode
+    warning: Optional[str]
+
+
+@dataclass
+class ModelRun:  # models.hpp:160-167
+    outputs: dict
+    primary: np.ndarray
+    report: SimReport
+    cfg: LaunchConfig
+    mode: ExecutionMode
+    warning: Optional[str]
+
+
+@dataclass
+class ConfidenceInterval:  # models.hpp:118-127
+    mean: float = 0.0
+    halfWidth: float = 0.0
+    level: float = 0.95
+    n: int = 0
+    warnSmallSample: bool = False
+
+    def low(self) -> float:
+        return self.mean - self.halfWidth
+
+    def high(self) -> float:
+        return self.mean + self.halfWidth
+
+
+# ---- C ABI --------------------------------------------------------------------------------
+
+
+class _Params(C.Structure):
+    _fields_ = [("replications", C.c_int64), ("draws", C.c_int64), ("clients", C.c_int64),
+                ("lambda_", C.c_double), ("mu", C.c_double), ("steps", C.c_int64), ("chunks", C.c_int64)]
+
+
+class _Cfg(C.Structure):
+    _fields_ = [("block_x", C.c_int64), ("block_y", C.c_int64), ("block_z", C.c_int64),
+                ("grid_x", C.c_int64), ("grid_y", C.c_int64), ("warp_size", C.c_int32)]
+
+
+class _Report(C.Structure):
+    _fields_ = [("total_cycles", C.c_int64), ("waves_executed", C.c_int64), ("peak_resident_warps", C.c_int64),
+                ("issues", C.c_uint64), ("alu_issues", C.c_uint64), ("mem_reads", C.c_uint64),
+                ("mem_writes", C.c_uint64), ("divergence_events", C.c_uint64), ("kernel_ms", C.c_double)]
+
+
+class _CI(C.Structure):
+    _fields_ = [("mean", C.c_double), ("half_width", C.c_double), ("level", C.c_double), ("n", C.c_int64),
+                ("warn_small_sample", C.c_int32)]
+
+
+class Stats(C.Structure):
+    """wlp_stats: shard sufficient statistics (count, double-double sums)."""
+    _fields_ = [("n", C.c_int64), ("sum_hi", C.c_double), ("sum_lo", C.c_double), ("center", C.c_double),
+                ("ss_hi", C.c_double), ("ss_lo", C.c_double)]
+
+
+class Special(C.Structure):
+    """wlp_special: a seeding candidate whose key could collide."""
+    _fields_ = [("index", C.c_int64), ("s1", C.c_uint32), ("s2", C.c_uint32), ("s3", C.c_uint32),
+                ("pad", C.c_uint32)]
+
+
+_P = C.c_void_p
+_I64 = C.c_int64
+_SIGS = {
+    "wlp_last_error": (C.c_char_p, []),
+    "wlp_version": (C.c_int, []),
+    "wlp_validate_params": (C.c_int, [C.c_int, C.POINTER(_Params), C.c_char_p, C.c_int]),
+    "wlp_plan_launch": (C.c_int, [_I64, C.c_int, C.c_int, _I64, C.POINTER(_Cfg), C.c_char_p, C.c_int]),
+    "wlp_master_from_seed": (C.c_int, [C.c_uint64, _P]),
+    "wlp_make_state": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, _P]),
+    "wlp_jump_host": (C.c_int, [_P, C.c_uint64, _P]),
+    "wlp_inverse_normal_cdf": (C.c_int, [C.c_double, C.POINTER(C.c_double)]),
+    "wlp_spacing_rejections": (C.c_int, [_P, _I64, _P, _I64, _P, _I64, C.POINTER(_I64)]),
+    "wlp_stats_merge": (C.c_int, [C.POINTER(Stats), C.POINTER(Stats)]),
+    "wlp_ci_from_stats": (C.c_int, [C.POINTER(Stats), C.c_double, C.POINTER(_CI)]),
+    "wlp_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "wlp_taus_stream": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, _I64, _P, C.c_int, _P]),
+    "wlp_seed_streams": (C.c_int, [C.c_uint64, _I64, _I64, _P, _I64, _P, C.c_int, _P, _P, _I64, C.POINTER(_I64)]),
+    "wlp_seed_streams_exact": (C.c_int, [C.c_uint64, _I64, _P, C.c_int, _P]),
+    "wlp_run_streams": (C.c_int, [C.c_int, C.POINTER(_Params), C.c_int, _P, _I64, C.c_int, _P, _P, _P, C.c_int, _P,
+                                  C.POINTER(_Report)]),
+    "wlp_run_shard": (C.c_int, [C.c_int, C.POINTER(_Params), C.c_int, C.c_uint64, C.c_int, _I64, _I64, _P, _I64,
+                                _P, _P, _P, C.c_int, _P, _P, _I64, C.POINTER(_I64), C.POINTER(_Report)]),
+    "wlp_run": (C.c_int, [C.c_int, C.POINTER(_Params), C.c_int, C.c_uint64, C.c_int, _P, _P, _P, C.c_int, _P,
+                          C.POINTER(_Report), C.POINTER(_CI), C.c_double, C.c_char_p, C.c_int]),
+    "wlp_stats_device": (C.c_int, [_P, _I64, C.c_int, C.POINTER(Stats), _P]),
+    "wlp_confidence_interval": (C.c_int, [_P, _I64, C.c_double, C.POINTER(_CI)]),
+    "wlp_debug_neg_log1m": (C.c_int, [_P, _I64, _P]),
+    "wlp_shutdown": (C.c_int, []),
+}
+EXPORTS = tuple(_SIGS)
+
+
+def _load() -> C.CDLL:
+    if not LIB_PATH.exists():
+        raise ImportError(f"{LIB_PATH.name} is not built; run `python -m paper_1501_01405_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(str(LIB_PATH))
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+class _LazyLib:
+    """Loads libwlp_b200.so on first use (so `python -m paper_1501_01405_b200.build` can run
+    before the library exists); any call without the library raises ImportError."""
+
+    _cdll: Optional[C.CDLL] = None
+
+    def __getattr__(self, name: str):
+        if _LazyLib._cdll is None:
+            _LazyLib._cdll = _load()
+        return getattr(_LazyLib._cdll, name)
+
+
+_lib = _LazyLib()
+
+
+def native_library() -> C.CDLL:
+    """The loaded libwlp_b200.so (loads it)."""
+    _lib.wlp_version
+    return _LazyLib._cdll
+
+
+def _check(status: int) -> None:
+    if status != OK:
+        msg = (_lib.wlp_last_error() or b"").decode(errors="replace")
+        raise _EXC.get(status, Error)(msg)
+
+
+def _params(p: ModelParams) -> _Params:
+    return _Params(int(p.replications), int(p.draws), int(p.clients), float(p.lambda_), float(p.mu),
+                   int(p.steps), int(p.chunks))
+
+
+def _ptr(a) -> Optional[int]:
+    """Data pointer of a numpy array / torch tensor / int / None."""
+    if a is None:
+        return None
+    if isinstance(a, int):
+        return a
+    if isinstance(a, np.ndarray):
+        if not a.flags.c_contiguous:
+            raise DomainError("array must be C-contiguous")
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    raise DomainError(f"unsupported buffer type {type(a)!r}")
+
+
+def _report(r: _Report) -> SimReport:
+    return SimReport(r.total_cycles, r.waves_executed, r.peak_resident_warps, r.issues, r.alu_issues, r.mem_reads,
+                     r.mem_writes, r.divergence_events, r.kernel_ms)
+
+
+# ---- host utilities (reference host functions) ----------------------------------------------
+
+
+def validate_params(model: ModelKind, p: ModelParams) -> Optional[str]:
+    """validate_params (models.cpp:26-44): DomainError, or the lambda >= mu warning."""
+    buf = C.create_string_buffer(512)
+    _check(_lib.wlp_validate_params(int(model), C.byref(_params(p)), buf, 512))
+    return buf.value.decode() or None
+
+
+def plan_launch(replications: int, mode: ExecutionMode, prof: Optional[DeviceProfile] = None,
+                tlp_block_size: int = 256, grid_limit: int = 65535) -> LaunchPlan:
+    """plan_launch (wlp.cpp:71-105), reference geometry and PlanError semantics."""
+    prof = prof or DeviceProfile()
+    if tlp_block_size > prof.maxThreadsPerBlock:
+        raise PlanError("plan_launch: tlp_block_size exceeds maxThreadsPerBlock")
+    cfg = _Cfg()
+    buf = C.create_string_buffer(512)
+    _check(_lib.wlp_plan_launch(int(replications), int(mode), int(tlp_block_size), int(grid_limit), C.byref(cfg),
+                                buf, 512))
+    lc = LaunchConfig((cfg.block_x, cfg.block_y, cfg.block_z), (cfg.grid_x, cfg.grid_y), cfg.warp_size)
+    return LaunchPlan(lc, int(replications), ExecutionMode(mode), buf.value.decode() or None)
+
+
+def make_rng_state(s1: int, s2: int, s3: int) -> RngState:
+    """make_rng_state (rng.cpp:29-34)."""
+    out = (C.c_uint32 * 3)()
+    _check(_lib.wlp_make_state(s1 & 0xFFFFFFFF, s2 & 0xFFFFFFFF, s3 & 0xFFFFFFFF, out))
+    return RngState(*out)
+
+
+def rng_state_from_seed(seed: int) -> RngState:
+    """rng_state_from_seed (rng.cpp:36-40)."""
+    out = (C.c_uint32 * 3)()
+    _check(_lib.wlp_master_from_seed(seed & (2**64 - 1), out))
+    return RngState(*out)
+
+
+def jump_state(state: RngState, n: int) -> RngState:
+    """State after n taus_next calls, by GF(2) jump-ahead (host)."""
+    s = (C.c_uint32 * 3)(state.s1, state.s2, state.s3)
+    out = (C.c_uint32 * 3)()
+    _check(_lib.wlp_jump_host(s, n, out))
+    return RngState(*out)
+
+
+def inverse_normal_cdf(p: float) -> float:
+    """inverse_normal_cdf (models.cpp:61-97)."""
+    z = C.c_double()
+    _check(_lib.wlp_inverse_normal_cdf(float(p), C.byref(z)))
+    return z.value
+
+
+def spacing_rejections(specials: Sequence[Special], prev: Sequence[int] = ()) -> list:
+    """Rejected candidate indices of random_spacing given all special candidates."""
+    n = len(specials)
+    arr = (Special * max(n, 1))(*specials)
+    pv = (C.c_int64 * max(len(prev), 1))(*prev)
+    out = (C.c_int64 * (n + len(prev) + 1))()
+    nout = C.c_int64()
+    _check(_lib.wlp_spacing_rejections(arr, n, pv, len(prev), out, n + len(prev) + 1, C.byref(nout)))
+    return list(out[: nout.value])
+
+
+def stats_merge(a: Stats, b: Stats) -> Stats:
+    r = Stats(a.n, a.sum_hi, a.sum_lo, a.center, a.ss_hi, a.ss_lo)
+    _check(_lib.wlp_stats_merge(C.byref(r), C.byref(b)))
+    return r
+
+
+def ci_from_stats(s: Stats, level: float = 0.95) -> ConfidenceInterval:
+    ci = _CI()
+    _check(_lib.wlp_ci_from_stats(C.byref(s), float(level), C.byref(ci)))
+    return ConfidenceInterval(ci.mean, ci.half_width, ci.level, ci.n, bool(ci.warn_small_sample))
+
+
+# ---- device entry points ----------------------------------------------------------------------
+
+
+def device_count() -> int:
+    n = C.c_int()
+    _check(_lib.wlp_device_count(C.byref(n)))
+    return n.value
+
+
+def taus_stream(state: RngState, n: int) -> np.ndarray:
+    """make_rng_state(state) then n taus_next outputs (rng.cpp:29-51), on the GPU."""
+    out = np.empty(n, dtype=np.uint32)
+    _check(_lib.wlp_taus_stream(state.s1, state.s2, state.s3, n, _ptr(out), 0, None))
+    return out
+
+
+def random_spacing_seed(master_seed: int, count: int) -> np.ndarray:
+    """random_spacing(rng_state_from_seed(master_seed), count) (rng.cpp:67-87) on the GPU.
+    Returns a (3, count) uint32 array (rows s1, s2, s3)."""
+    out = np.empty((3, count), dtype=np.uint32)
+    _check(_lib.wlp_seed_streams_exact(master_seed & (2**64 - 1), count, _ptr(out), 0, None))
+    return out
+
+
+def seed_streams(master_seed: int, slot_begin: int, count: int, rejected: Sequence[int] = (),
+                 special_cap: int = 4096):
+    """Shard form of random_spacing: stream slots [slot_begin, slot_begin+count) given a
+    global rejection list; returns (keys (3,count), specials list)."""
+    out = np.empty((3, count), dtype=np.uint32)
+    rej = np.asarray(sorted(rejected), dtype=np.int64)
+    sp = (Special * special_cap)()
+    nsp = C.c_int64()
+    _check(_lib.wlp_seed_streams(master_seed & (2**64 - 1), slot_begin, count, _ptr(rej) if len(rej) else None,
+                                 len(rej), _ptr(out), 0, None, sp, special_cap, C.byref(nsp)))
+    return out, list(sp[: min(nsp.value, special_cap)])
+
+
+def run_streams(model: ModelKind, p: ModelParams, mode: ExecutionMode, streams: np.ndarray):
+    """Replications over explicit streams ((3,R) uint32): pi_/mm1_/walk_replication
+    (models.cpp:46-59) of every stream, on the GPU. Returns a dict of output arrays."""
+    streams = np.ascontiguousarray(streams, dtype=np.uint32)
+    R = streams.shape[1]
+    outs = [np.empty(R) for _ in OUTPUT_NAMES[ModelKind(model)]]
+    o = [_ptr(x) for x in outs] + [None] * (3 - len(outs))
+    _check(_lib.wlp_run_streams(int(model), C.byref(_params(p)), int(mode), _ptr(streams), R, 0, o[0], o[1], o[2], 0,
+                                None, None))
+    return dict(zip(OUTPUT_NAMES[ModelKind(model)], outs))
+
+
+def pi_replication(draws: int, stream: RngState) -> float:
+    """pi_replication (models.cpp:46-49), one replication on the GPU."""
+    s = np.array([[stream.s1], [stream.s2], [stream.s3]], dtype=np.uint32)
+    return float(run_streams(ModelKind.Pi, ModelParams(draws=draws), ExecutionMode.Wlp, s)["out"][0])
+
+
+def mm1_replication(clients: int, lambda_: float, mu: float, stream: RngState):
+    """mm1_replication (models.cpp:51-54) -> (avgIdle, avgWaitQueue, avgSystem)."""
+    s = np.array([[stream.s1], [stream.s2], [stream.s3]], dtype=np.uint32)
+    o = run_streams(ModelKind.Mm1, ModelParams(clients=clients, lambda_=lambda_, mu=mu), ExecutionMode.Wlp, s)
+    return float(o["outIdle"][0]), float(o["outWait"][0]), float(o["outSys"][0])
+
+
+def walk_replication(steps: int, chunks: int, stream: RngState) -> float:
+    """walk_replication (models.cpp:56-59)."""
+    s = np.array([[stream.s1], [stream.s2], [stream.s3]], dtype=np.uint32)
+    return float(run_streams(ModelKind.Walk, ModelParams(steps=steps, chunks=chunks), ExecutionMode.Wlp, s)["out"][0])
+
+
+def run_model(model: ModelKind, p: ModelParams, mode: ExecutionMode, prof: Optional[DeviceProfile] = None,
+              master_seed: int = 1, tlp_block_size: int = 256, opts: Optional[SimOptions] = None,
+              *, timed: bool = True) -> ModelRun:
+    """run_model (models.cpp:329-397): seeds R streams by random spacing from master_seed,
+    runs the model in `mode` on the GPU, returns per-replication outputs (host arrays).
+
+    Outputs are bit-identical to the reference's Sequential mode. `prof`/`opts` are
+    accepted for signature compatibility and ignored (the hardware is real). The
+    SEQUENTIAL mode runs the warp-per-replication kernel too (there is no host path);
+    its `cfg` is the reference's single-thread geometry.
+    """
+    model, mode = ModelKind(model), ExecutionMode(mode)
+    plan = plan_launch(p.replications, mode, prof, tlp_block_size, grid_limit=0x7FFFFFFF)
+    R = int(p.replications)
+    names = OUTPUT_NAMES[model]
+    outs = [np.empty(R) for _ in names]
+    o = [_ptr(x) for x in outs] + [None] * (3 - len(outs))
+    rep = _Report()
+    warn = C.create_string_buffer(512)
+    _check(_lib.wlp_run(int(model), C.byref(_params(p)), int(mode), master_seed & (2**64 - 1), int(tlp_block_size),
+                        o[0], o[1], o[2], 0, None, C.byref(rep) if timed else None, None, 0.95, warn, 512))
+    outputs = dict(zip(names, outs))
+    return ModelRun(outputs, outputs[PRIMARY[model]], _report(rep), plan.cfg, mode, warn.value.decode() or None)
+
+
+def run_model_into(model: ModelKind, p: ModelParams, mode: ExecutionMode, master_seed: int, outs, *,
+                   on_device: bool, stream: Optional[int] = None, tlp_block_size: int = 256,
+                   ci_level: Optional[float] = None):
+    """Low-level run_model writing into caller buffers (device pointers / torch CUDA tensors
+    when on_device, else host arrays). Returns the list of ConfidenceIntervals when
+    ci_level is given (device reduction), else None."""
+    o = [_ptr(x) for x in outs] + [None] * (3 - len(outs))
+    nci = len(OUTPUT_NAMES[ModelKind(model)])
+    cis = (_CI * nci)() if ci_level is not None else None
+    _check(_lib.wlp_run(int(model), C.byref(_params(p)), int(mode), master_seed & (2**64 - 1), int(tlp_block_size),
+                        o[0], o[1], o[2], 1 if on_device else 0, stream, None, cis,
+                        float(ci_level or 0.95), None, 0))
+    if cis is None:
+        return None
+    return [ConfidenceInterval(c.mean, c.half_width, c.level, c.n, bool(c.warn_small_sample)) for c in cis]
+
+
+def run_shard(model: ModelKind, p: ModelParams, mode: ExecutionMode, master_seed: int, r_begin: int, r_count: int,
+              outs, *, on_device: bool, rejected: Sequence[int] = (), stream: Optional[int] = None,
+              tlp_block_size: int = 256, special_cap: int = 4096, report: Optional[SimReport] = None):
+    """Shard [r_begin, r_begin + r_count) of a run of p.replications; returns the shard's
+    special seeding candidates. If `report` is given it is filled
+    with the model kernel's measured time (CUDA events on the launching stream)."""
+    o = [_ptr(x) for x in outs] + [None] * (3 - len(outs))
+    rej = np.asarray(sorted(rejected), dtype=np.int64)
+    sp = (Special * special_cap)()
+    nsp = C.c_int64()
+    rep = _Report() if report is not None else None
+    _check(_lib.wlp_run_shard(int(model), C.byref(_params(p)), int(mode), master_seed & (2**64 - 1),
+                              int(tlp_block_size), r_begin, r_count, _ptr(rej) if len(rej) else None, len(rej),
+                              o[0], o[1], o[2], 1 if on_device else 0, stream, sp, special_cap, C.byref(nsp),
+                              C.byref(rep) if rep is not None else None))
+    if rep is not None:
+        report.__dict__.update(vars(_report(rep)))
+    if nsp.value > special_cap:
+        raise Error("too many special seeding candidates")
+    return list(sp[: nsp.value])
+
+
+def stats_device(x, n: int, pass_: int, stats: Optional[Stats] = None, stream: Optional[int] = None) -> Stats:
+    """Device sufficient statistics of a device array (pass 1: sum; pass 2: centred SS)."""
+    s = stats if stats is not None else Stats()
+    _check(_lib.wlp_stats_device(_ptr(x), n, pass_, C.byref(s), stream))
+    return s
+
+
+def confidence_interval(samples, level: float = 0.95) -> ConfidenceInterval:
+    """confidence_interval (models.cpp:99-119) through the device reduction. For n <= 256
+    the sums are the reference's sequential loop, bit for bit."""
+    x = np.ascontiguousarray(samples, dtype=np.float64)
+    ci = _CI()
+    _check(_lib.wlp_confidence_interval(_ptr(x) if len(x) else None, len(x), float(level), C.byref(ci)))
+    return ConfidenceInterval(ci.mean, ci.half_width, ci.level, ci.n, bool(ci.warn_small_sample))
+
+
+def debug_neg_log1m(k) -> np.ndarray:
+    """-log(1 - k*2^-32) through the device glibc-log port (test hook)."""
+    k = np.ascontiguousarray(k, dtype=np.uint32)
+    out = np.empty(len(k))
+    _check(_lib.wlp_debug_neg_log1m(_ptr(k) if len(k) else None, len(k), _ptr(out) if len(k) else None))
+    return out
+
+
+def shutdown() -> None:
+    _check(_lib.wlp_shutdown())

@@ -1,0 +1,135 @@
+// Bit-exact port of glibc 2.39's x86-64 FMA `log` (__log_fma) for host and device.
+//
+// Why: the mm1 model draws exponentials as -log(1-u)/rate (reference models.hpp:67,75;
+// rng.cpp:60) through the host's libm. CUDA's log() rounds differently, so per-
+// replication mm1 outputs would not be bit-identical to the CPU oracle. glibc's
+// algorithm (sysdeps/ieee754/dbl-64/e_log.c, ARM optimized-routines, N = 128 table)
+// is restated here in the exact operation order of the FMA build: the contractions
+// below were read off the disassembly of libm.so.6's __log_fma;
+// every plain + - * must stay unfused (host: -ffp-contract=off, device: --fmad=false),
+// every fused step is an explicit fma().
+//
+// Pinned by tools/check_glibc_log.c: identical bits to libm's log for every input the
+// model can produce, x = 1 - k*2^-32, k in [0, 2^32) (exhaustive), plus the generic
+// paths (subnormals, specials) on samples.
+#pragma once
+
+#include <stdint.h>
+
+#include "glibc_log_data.h"
+
+#if defined(__CUDACC__)
+#define WLP_HD __host__ __device__ __forceinline__
+#else
+#define WLP_HD static inline
+#include <math.h>
+#include <string.h>
+#endif
+
+namespace wlp {
+
+#if defined(__CUDACC__)
+__device__ __constant__ double kLogTabDev[256] = WLP_LOG_TAB_INIT;
+#endif
+
+#if defined(__CUDA_ARCH__)
+#define WLP_LOG_TAB kLogTabDev
+#define WLP_FMA(a, b, c) __fma_rn((a), (b), (c))
+#define WLP_MUL(a, b) __dmul_rn((a), (b))
+#define WLP_ADD(a, b) __dadd_rn((a), (b))
+#define WLP_SUB(a, b) __dsub_rn((a), (b))
+WLP_HD uint64_t wlp_as_u64(double x) { return static_cast<uint64_t>(__double_as_longlong(x)); }
+WLP_HD double wlp_as_f64(uint64_t x) { return __longlong_as_double(static_cast<long long>(x)); }
+#else
+static const double kLogTabHost[256] = WLP_LOG_TAB_INIT;
+#define WLP_LOG_TAB kLogTabHost
+#define WLP_FMA(a, b, c) fma((a), (b), (c))
+#define WLP_MUL(a, b) ((a) * (b))
+#define WLP_ADD(a, b) ((a) + (b))
+#define WLP_SUB(a, b) ((a) - (b))
+WLP_HD uint64_t wlp_as_u64(double x) {
+    uint64_t u;
+    memcpy(&u, &x, sizeof u);
+    return u;
+}
+WLP_HD double wlp_as_f64(uint64_t u) {
+    double x;
+    memcpy(&x, &u, sizeof x);
+    return x;
+}
+#endif
+
+// Inputs 1 - 2^-4 <= x < 1 + 0x1.09p-4 take the table-free polynomial path.
+constexpr uint64_t kLogNearLo = 0x3FEE000000000000ull;               // 1 - 0x1p-4
+constexpr uint64_t kLogNearSpan = 0x3FF1090000000000ull - kLogNearLo;  // up to 1 + 0x1.09p-4
+constexpr uint64_t kLogOff = 0x3fe6000000000000ull;  // table subintervals cover [OFF, 2*OFF)
+
+// log(x) for x within 1 - 2^-4 .. 1 + 0x1.09p-4 (x != 1): r = x - 1 is exact, log1p(r)
+// = r - r^2/2 + r^3 * P(r); the r^2/2 term is split hi/lo (rhi keeps 26 bits of r).
+WLP_HD double log_near_one(double x) {
+    const double r = WLP_SUB(x, 1.0);
+    const double r2 = WLP_MUL(r, r);
+    const double r3 = WLP_MUL(r, r2);
+    constexpr double B[11] = WLP_LOG_POLY1_INIT;
+    const double ta = WLP_FMA(r2, B[3], WLP_FMA(r, B[2], B[1]));
+    const double tb = WLP_FMA(r2, B[6], WLP_FMA(r, B[5], B[4]));
+    const double tc = WLP_FMA(r3, B[10], WLP_FMA(r2, B[9], WLP_FMA(r, B[8], B[7])));
+    const double p = WLP_FMA(WLP_FMA(tc, r3, tb), r3, ta);
+    const double rw = WLP_FMA(r, 0x1p27, r);
+    const double rhi = WLP_FMA(-0x1p27, r, rw);
+    const double rhi2 = WLP_MUL(rhi, rhi);
+    const double rlo = WLP_SUB(r, rhi);
+    const double hi = WLP_FMA(rhi2, B[0], r);
+    double lo = WLP_FMA(rhi2, B[0], WLP_SUB(r, hi));
+    lo = WLP_FMA(WLP_MUL(B[0], rlo), WLP_ADD(r, rhi), lo);
+    return WLP_ADD(hi, WLP_FMA(p, r3, lo));
+}
+
+// log(x) for positive normal x outside the near-one window: x = 2^k * z, z in
+// [OFF, 2*OFF); log x = k*ln2 + log(c) + log1p(z/c - 1), c from the 128-entry table.
+WLP_HD double log_table(uint64_t ix) {
+    const uint64_t tmp = ix - kLogOff;
+    const int i = static_cast<int>((tmp >> 45) & 127u);
+    const int64_t k = static_cast<int64_t>(tmp) >> 52;
+    const uint64_t iz = ix - (tmp & (0xfffull << 52));
+    const double invc = WLP_LOG_TAB[2 * i];
+    const double logc = WLP_LOG_TAB[2 * i + 1];
+    const double z = wlp_as_f64(iz);
+    const double kd = static_cast<double>(k);
+    constexpr double A[5] = WLP_LOG_POLY_INIT;
+    const double r = WLP_FMA(z, invc, -1.0);
+    const double w = WLP_FMA(kd, WLP_LOG_LN2HI, logc);
+    const double hi = WLP_ADD(r, w);
+    const double lo = WLP_FMA(kd, WLP_LOG_LN2LO, WLP_ADD(WLP_SUB(w, hi), r));
+    const double r2 = WLP_MUL(r, r);
+    const double q = WLP_FMA(WLP_FMA(r, A[4], A[3]), r2, WLP_FMA(r, A[2], A[1]));
+    const double y = WLP_FMA(WLP_MUL(r, r2), q, WLP_FMA(r2, A[0], lo));
+    return WLP_ADD(y, hi);
+}
+
+// glibc log() semantics for every double (specials follow e_log.c: log(0) = -inf,
+// log(<0) and log(nan) = nan, log(inf) = inf, subnormals normalised first).
+WLP_HD double glibc_log(double x) {
+    uint64_t ix = wlp_as_u64(x);
+    if (ix - kLogNearLo < kLogNearSpan) {
+        if (ix == 0x3FF0000000000000ull) return 0.0;
+        return log_near_one(x);
+    }
+    const uint32_t top = static_cast<uint32_t>(ix >> 48);
+    if (top - 0x0010u >= 0x7ff0u - 0x0010u) {
+        if ((ix << 1) == 0) return -wlp_as_f64(0x7ff0000000000000ull);
+        if (ix == 0x7ff0000000000000ull) return x;
+        if ((top & 0x8000u) || (top & 0x7ff0u) == 0x7ff0u) return wlp_as_f64(0x7ff8000000000000ull);
+        ix = wlp_as_u64(WLP_MUL(x, 0x1p52)) - (52ull << 52);
+    }
+    return log_table(ix);
+}
+
+// -log(1 - u) for u = n * 2^-32, n a taus88 output (u in [0, 1), 1 - u exact and
+// normal): the exponential variate numerator of mm1 (models.hpp:67,75).
+WLP_HD double neg_log1m_u32(uint32_t n) {
+    const double u = static_cast<double>(n) * 0x1p-32;
+    return -glibc_log(WLP_SUB(1.0, u));
+}
+
+}  // namespace wlp

@@ -1,0 +1,69 @@
+// Launch interface of the sm_100a kernels (implemented in kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "taus88.cuh"
+
+namespace wlp {
+
+// Replication-kernel arguments shared by every model/mapping.
+struct RepArgs {
+    const uint32_t* seeds;  // SoA: s1[count], s2[count], s3[count]
+    int64_t count;          // replications in this launch
+    int64_t n;              // units per replication (draws / clients / steps)
+    int64_t chunks;         // walk
+    double lambda, mu;      // mm1 rates
+    double inv_lambda, inv_mu;  // exact reciprocals when the rate is a power of two, else 0
+    double* out0;
+    double* out1;
+    double* out2;
+};
+
+// Seeding: stream slots [slot_begin, slot_begin+count) of a run.
+struct SeedArgs {
+    const uint32_t* powers;  // [64][3][32] binary powers of the taus88 step
+    Taus master;
+    int64_t slot_begin, count;
+    const int64_t* rejected;  // sorted global candidate indices
+    int64_t n_rejected;
+    uint32_t* out;  // SoA 3*count
+    void* specials;  // wlp_special[cap]
+    int64_t special_cap;
+    unsigned long long* n_special;
+};
+
+constexpr int kWlpBlock = 256;     // pi / walk WLP block (8 warps)
+constexpr int kMm1Block = 512;     // mm1 WLP block (16 warps)
+constexpr int kMm1PanelT = 8;      // mm1: clients per lane per panel
+constexpr int kSeedBlock = 128;
+constexpr int kSeedPerThread = 32;
+
+// Layout of wlp_special (include/wlp_b200.h).
+struct SpecialRec {
+    int64_t index;
+    uint32_t s1, s2, s3, pad;
+};
+
+// Resident blocks per SM for each WLP kernel (occupancy API), for persistent grids.
+int wlp_blocks_per_sm(int model);
+// Resident blocks per SM of the TLP kernel at a given block size.
+int tlp_blocks_per_sm(int model, int block);
+
+cudaError_t launch_seed(const SeedArgs& a, cudaStream_t st);
+cudaError_t launch_neg_log1m(const uint32_t* k, int64_t n, double* out, cudaStream_t st);
+cudaError_t launch_taus_stream(const uint32_t* powers, Taus seed, int64_t n, uint32_t* out,
+                               cudaStream_t st);
+// WLP: persistent grid of `grid` blocks; lane_tab = lane-start nibble tables (device),
+// uni_tab = panel-skip table (mm1 only).
+cudaError_t launch_wlp(int model, const RepArgs& a, const uint32_t* lane_tab,
+                       const uint32_t* uni_tab, int64_t lane_units, int grid, cudaStream_t st);
+// TLP: thread per replication, block = tlp_block, grid = ceil(count / tlp_block).
+cudaError_t launch_tlp(int model, const RepArgs& a, int tlp_block, cudaStream_t st);
+// Stats: per-block partials [grid][4] (sum_hi, sum_lo or ss_hi, ss_lo) of x (pass 1
+// about 0, pass 2 about `center`).
+cudaError_t launch_stats(const double* x, int64_t n, int pass, double center, double* partials,
+                         int grid, cudaStream_t st);
+
+}  // namespace wlp

@@ -1,0 +1,855 @@
+// C-ABI implementation (include/wlp_b200.h): per-device context and scratch, the exact
+// random-spacing fixpoint, model dispatch, device statistics, and the host-side
+// reference utilities (validate_params, plan_launch, rng_state_from_seed,
+// inverse_normal_cdf) the drop-in API needs.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <set>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/wlp_b200.h"
+#include "jump.hpp"
+#include "kernels.cuh"
+
+static_assert(sizeof(wlp_special) == sizeof(wlp::SpecialRec), "wlp_special layout");
+
+namespace wlp {
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define WLP_CUDA(expr)                                                                       \
+    do {                                                                                     \
+        cudaError_t e_ = (expr);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            return fail(WLP_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) +    \
+                                       " at " #expr);                                        \
+    } while (0)
+
+#define WLP_TRY(expr)            \
+    do {                         \
+        int s_ = (expr);         \
+        if (s_ != WLP_OK) return s_; \
+    } while (0)
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    int64_t cap = 0;
+    cudaError_t ensure(int64_t n) {
+        if (n <= cap) return cudaSuccess;
+        release();
+        const cudaError_t e = cudaMalloc(&p, static_cast<size_t>(std::max<int64_t>(n, 1)) * sizeof(T));
+        if (e == cudaSuccess)
+            cap = n;
+        else
+            p = nullptr;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+constexpr int64_t kSpecialCap = 4096;
+constexpr int kMaxLaneTabs = 64;
+
+struct DevCtx {
+    int dev = 0;
+    int sms = 0;
+    int clock_khz = 0;
+    int wlp_bps[3] = {1, 1, 1};
+    std::mutex mu;
+    bool ready = false;
+    DevBuf<uint32_t> powers;
+    std::map<uint64_t, DevBuf<uint32_t>> lane_tabs;  // by lane jump stride (draws)
+    DevBuf<uint32_t> mm1_lane, mm1_skip;
+    DevBuf<uint32_t> seeds, in_seeds;
+    DevBuf<double> outs, partials, stats_in;
+    DevBuf<SpecialRec> specials;
+    DevBuf<unsigned long long> counter;
+    DevBuf<int64_t> rejected;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+std::mutex g_ctx_mu;
+std::map<int, std::unique_ptr<DevCtx>> g_ctx;
+
+int upload_u32(DevBuf<uint32_t>& b, const std::vector<uint32_t>& v) {
+    WLP_CUDA(b.ensure(static_cast<int64_t>(v.size())));
+    WLP_CUDA(cudaMemcpy(b.p, v.data(), v.size() * 4, cudaMemcpyHostToDevice));
+    return WLP_OK;
+}
+
+int ctx_init(DevCtx& c) {
+    if (c.ready) return WLP_OK;
+    WLP_CUDA(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, c.dev));
+    if (cudaDeviceGetAttribute(&c.clock_khz, cudaDevAttrClockRate, c.dev) != cudaSuccess) c.clock_khz = 0;
+    WLP_TRY(upload_u32(c.powers, flat_binary_powers()));
+    WLP_TRY(upload_u32(c.mm1_lane, lane_tables(2ull * kMm1PanelT)));
+    WLP_TRY(upload_u32(c.mm1_skip, uniform_table(2ull * 31 * kMm1PanelT)));
+    for (int m = 0; m < 3; ++m) c.wlp_bps[m] = wlp_blocks_per_sm(m);
+    WLP_CUDA(c.specials.ensure(kSpecialCap));
+    WLP_CUDA(c.counter.ensure(1));
+    WLP_CUDA(cudaEventCreate(&c.ev0));
+    WLP_CUDA(cudaEventCreate(&c.ev1));
+    WLP_CUDA(cudaGetLastError());
+    c.ready = true;
+    return WLP_OK;
+}
+
+// Context of the calling thread's current device, locked.
+int acquire(DevCtx*& out, std::unique_lock<std::mutex>& lk) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return fail(WLP_ECUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    int n = 0;
+    e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        return fail(WLP_ECUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    DevCtx* c;
+    {
+        std::lock_guard<std::mutex> g(g_ctx_mu);
+        auto& slot = g_ctx[dev];
+        if (!slot) {
+            slot = std::make_unique<DevCtx>();
+            slot->dev = dev;
+        }
+        c = slot.get();
+    }
+    lk = std::unique_lock<std::mutex>(c->mu);
+    WLP_TRY(ctx_init(*c));
+    out = c;
+    return WLP_OK;
+}
+
+int64_t units_of(int model, const wlp_params& p) {
+    return model == WLP_MODEL_PI ? p.draws : model == WLP_MODEL_MM1 ? p.clients : p.steps;
+}
+
+// 1/rate when rate = 2^k (|k| <= 512): then x/rate == x*(1/rate) exactly.
+double exact_reciprocal(double rate) {
+    int e = 0;
+    const double m = std::frexp(rate, &e);
+    if (m != 0.5 || e < -510 || e > 512) return 0.0;
+    return std::ldexp(1.0, 1 - e);
+}
+
+int lane_table(DevCtx& c, uint64_t stride, const uint32_t*& out) {
+    auto it = c.lane_tabs.find(stride);
+    if (it == c.lane_tabs.end()) {
+        if (static_cast<int>(c.lane_tabs.size()) >= kMaxLaneTabs) {
+            WLP_CUDA(cudaDeviceSynchronize());
+            for (auto& kv : c.lane_tabs) kv.second.release();
+            c.lane_tabs.clear();
+        }
+        DevBuf<uint32_t>& b = c.lane_tabs[stride];
+        WLP_TRY(upload_u32(b, lane_tables(stride)));
+        out = b.p;
+        return WLP_OK;
+    }
+    out = it->second.p;
+    return WLP_OK;
+}
+
+
+int check_model_mode(int model, int mode) {
+    if (model < 0 || model > 2) return fail(WLP_EDOMAIN, "unknown model id");
+    if (mode < 0 || mode > 2) return fail(WLP_EDOMAIN, "unknown execution mode id");
+    return WLP_OK;
+}
+
+// ---- host reference utilities -------------------------------------------------------
+
+// validate_params (models.cpp:26-44)
+int validate(int model, const wlp_params* p, std::string* warning) {
+    if (!p) return fail(WLP_EDOMAIN, "params: null");
+    if (p->replications < 1) return fail(WLP_EDOMAIN, "params: replications must be >= 1");
+    switch (model) {
+        case WLP_MODEL_PI:
+            if (p->draws < 1) return fail(WLP_EDOMAIN, "pi: draws must be >= 1");
+            break;
+        case WLP_MODEL_MM1:
+            if (p->clients < 1) return fail(WLP_EDOMAIN, "mm1: clients must be >= 1");
+            if (!(p->lambda > 0.0) || !(p->mu > 0.0)) return fail(WLP_EDOMAIN, "mm1: rates must be > 0");
+            if (p->lambda >= p->mu && warning)
+                *warning = "mm1: lambda >= mu, queue is unstable; steady-state comparisons are off";
+            break;
+        case WLP_MODEL_WALK:
+            if (p->steps < 1) return fail(WLP_EDOMAIN, "walk: steps must be >= 1");
+            if (p->chunks < 2) return fail(WLP_EDOMAIN, "walk: chunks must be >= 2");
+            break;
+        default: return fail(WLP_EDOMAIN, "unknown model");
+    }
+    // device limit of this engine: per-lane counters are 32-bit
+    if (units_of(model, *p) >= (int64_t(1) << 36))
+        return fail(WLP_EPLAN, "units per replication exceed the device limit of 2^36");
+    return WLP_OK;
+}
+
+// plan_launch (wlp.cpp:71-105) with the launch_warning text (kernel_ir.cpp:150-156).
+int plan(int64_t R, int mode, int tlp_block, int64_t grid_limit, wlp_launch_cfg* cfg, std::string* warning) {
+    if (R < 1) return fail(WLP_EPLAN, "plan_launch: need at least one replication");
+    if (tlp_block < 1) return fail(WLP_EPLAN, "plan_launch: tlp_block_size must be >= 1");
+    if (tlp_block > 1024) return fail(WLP_EPLAN, "plan_launch: tlp_block_size exceeds maxThreadsPerBlock");
+    wlp_launch_cfg c{1, 1, 1, 1, 1, 32};
+    if (mode == WLP_MODE_SEQUENTIAL) {
+        c.warp_size = 1;
+    } else if (mode == WLP_MODE_WLP) {
+        c.block_x = 32;
+        c.grid_x = R;
+    } else if (mode == WLP_MODE_TLP) {
+        c.block_x = std::min<int64_t>(R, tlp_block);
+        c.grid_x = (R + c.block_x - 1) / c.block_x;
+    } else {
+        return fail(WLP_EDOMAIN, "unknown execution mode id");
+    }
+    if (c.grid_x > grid_limit || c.grid_y > grid_limit)
+        return fail(WLP_EPLAN, "plan_launch: " + std::to_string(R) + " replications exceed the grid limit of " +
+                                   std::to_string(grid_limit) + " blocks per dimension");
+    const int64_t tpb = c.block_x * c.block_y * c.block_z;
+    if (warning && tpb % c.warp_size != 0)
+        *warning = "block size " + std::to_string(tpb) + " is not a multiple of warpSize " +
+                   std::to_string(c.warp_size) + "; trailing warp runs partially populated";
+    if (cfg) *cfg = c;
+    return WLP_OK;
+}
+
+uint64_t splitmix64(uint64_t& x) {
+    x += 0x9e3779b97f4a7c15ull;
+    uint64_t z = x;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+// rng_state_from_seed (rng.cpp:36-40) as the reference's g++ build behaves: its three
+// word() calls are arguments of one call, evaluated right to left, so s3 takes the
+// first splitmix64 output and s1 the third (pinned by tests/golden/spacing.json).
+Taus master_from_seed(uint64_t seed) {
+    uint64_t x = seed;
+    const uint32_t first = static_cast<uint32_t>(splitmix64(x) >> 32);
+    const uint32_t second = static_cast<uint32_t>(splitmix64(x) >> 32);
+    const uint32_t third = static_cast<uint32_t>(splitmix64(x) >> 32);
+    return make_state(third, second, first);
+}
+
+// inverse_normal_cdf (models.cpp:61-97): Acklam's rational guess + two Halley steps.
+int inv_normal(double p, double* out) {
+    if (!(p > 0.0 && p < 1.0)) return fail(WLP_EDOMAIN, "inverse_normal_cdf: p outside (0,1)");
+    static const double A[6] = {-3.969683028665376e+01, 2.209460984245205e+02, -2.759285104469687e+02,
+                                1.383577518672690e+02,  -3.066479806614716e+01, 2.506628277459239e+00};
+    static const double B[5] = {-5.447609879822406e+01, 1.615858368580409e+02, -1.556989798598866e+02,
+                                6.680131188771972e+01,  -1.328068155288572e+01};
+    static const double C[6] = {-7.784894002430293e-03, -3.223964580411365e-01, -2.400758277161838e+00,
+                                -2.549732539343734e+00, 4.374664141464968e+00,  2.938163982698783e+00};
+    static const double D[4] = {7.784695709041462e-03, 3.224671290700398e-01, 2.445134137142996e+00,
+                                3.754408661907416e+00};
+    const double plow = 0.02425;
+    double x;
+    if (p < plow) {
+        const double q = std::sqrt(-2.0 * std::log(p));
+        x = (((((C[0] * q + C[1]) * q + C[2]) * q + C[3]) * q + C[4]) * q + C[5]) /
+            ((((D[0] * q + D[1]) * q + D[2]) * q + D[3]) * q + 1.0);
+    } else if (p <= 1.0 - plow) {
+        const double q = p - 0.5, r = q * q;
+        x = (((((A[0] * r + A[1]) * r + A[2]) * r + A[3]) * r + A[4]) * r + A[5]) * q /
+            (((((B[0] * r + B[1]) * r + B[2]) * r + B[3]) * r + B[4]) * r + 1.0);
+    } else {
+        const double q = std::sqrt(-2.0 * std::log(1.0 - p));
+        x = -(((((C[0] * q + C[1]) * q + C[2]) * q + C[3]) * q + C[4]) * q + C[5]) /
+            ((((D[0] * q + D[1]) * q + D[2]) * q + D[3]) * q + 1.0);
+    }
+    const double sqrt2 = 1.4142135623730951, pi = 3.141592653589793;
+    for (int k = 0; k < 2; ++k) {
+        const double e = 0.5 * std::erfc(-x / sqrt2) - p;
+        const double u = e * std::sqrt(2.0 * pi) * std::exp(x * x / 2.0);
+        x = x - u / (1.0 + x * u / 2.0);
+    }
+    *out = x;
+    return WLP_OK;
+}
+
+void dd_add(double& hi, double& lo, double v) {  // TwoSum
+    const double s = hi + v;
+    const double bb = s - hi;
+    const double err = (hi - (s - bb)) + (v - bb);
+    hi = s;
+    lo += err;
+}
+
+// Rejections from specials (see wlp_spacing_rejections).
+int spacing_rejections(std::vector<SpecialRec> sp, const std::vector<int64_t>& prev, std::vector<int64_t>& out) {
+    std::sort(sp.begin(), sp.end(), [](const SpecialRec& a, const SpecialRec& b) { return a.index < b.index; });
+    std::set<std::tuple<uint32_t, uint32_t, uint32_t>> seen;
+    out = prev;
+    for (const SpecialRec& s : sp) {
+        if (!seen.insert({s.s1, s.s2, s.s3}).second) out.push_back(s.index);
+    }
+    std::sort(out.begin(), out.end());
+    out.erase(std::unique(out.begin(), out.end()), out.end());
+    // rng.cpp:80-82: one stream redrawn 1000 times is an Error.
+    int64_t run = 0;
+    for (size_t i = 0; i < out.size(); ++i) {
+        run = (i > 0 && out[i] == out[i - 1] + 1) ? run + 1 : 1;
+        if (run >= 1000) return fail(WLP_ESPACING, "random_spacing: could not find a distinct stream seed");
+    }
+    return WLP_OK;
+}
+
+// ---- device building blocks ------------------------------------------------------------
+
+// Seed slots [slot_begin, slot_begin+count) into d_out (SoA), async; specials counted.
+int seed_async(DevCtx& c, Taus master, int64_t slot_begin, int64_t count, const std::vector<int64_t>& rej,
+               uint32_t* d_out, cudaStream_t st) {
+    if (!rej.empty()) {
+        WLP_CUDA(c.rejected.ensure(static_cast<int64_t>(rej.size())));
+        WLP_CUDA(cudaMemcpyAsync(c.rejected.p, rej.data(), rej.size() * 8, cudaMemcpyHostToDevice, st));
+    }
+    WLP_CUDA(cudaMemsetAsync(c.counter.p, 0, 8, st));
+    SeedArgs a;
+    a.powers = c.powers.p;
+    a.master = master;
+    a.slot_begin = slot_begin;
+    a.count = count;
+    a.rejected = rej.empty() ? nullptr : c.rejected.p;
+    a.n_rejected = static_cast<int64_t>(rej.size());
+    a.out = d_out;
+    a.specials = c.specials.p;
+    a.special_cap = kSpecialCap;
+    a.n_special = c.counter.p;
+    WLP_CUDA(launch_seed(a, st));
+    return WLP_OK;
+}
+
+// Specials of the last seed_async (synchronises the stream).
+int read_specials(DevCtx& c, cudaStream_t st, std::vector<SpecialRec>& sp, int64_t& n_total) {
+    unsigned long long n = 0;
+    WLP_CUDA(cudaMemcpyAsync(&n, c.counter.p, 8, cudaMemcpyDeviceToHost, st));
+    WLP_CUDA(cudaStreamSynchronize(st));
+    n_total = static_cast<int64_t>(n);
+    if (n_total > kSpecialCap) return fail(WLP_EINTERNAL, "random_spacing: too many special candidates");
+    sp.resize(static_cast<size_t>(n_total));
+    if (n_total) WLP_CUDA(cudaMemcpy(sp.data(), c.specials.p, n_total * sizeof(SpecialRec), cudaMemcpyDeviceToHost));
+    return WLP_OK;
+}
+
+int wlp_grid(DevCtx& c, int model, int64_t count) {
+    const int warps_per_block = (model == WLP_MODEL_MM1 ? kMm1Block : kWlpBlock) / 32;
+    const int64_t cap = static_cast<int64_t>(c.sms) * c.wlp_bps[model];
+    const int64_t need = (count + warps_per_block - 1) / warps_per_block;
+    return static_cast<int>(std::max<int64_t>(1, std::min(cap, need)));
+}
+
+// Launch the model over d_seeds (count replications). Async.
+int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_block, const uint32_t* d_seeds,
+                int64_t count, double* o0, double* o1, double* o2, cudaStream_t st, int& grid_out) {
+    RepArgs a;
+    a.seeds = d_seeds;
+    a.count = count;
+    a.n = units_of(model, p);
+    a.chunks = p.chunks;
+    a.lambda = p.lambda;
+    a.mu = p.mu;
+    a.inv_lambda = model == WLP_MODEL_MM1 ? exact_reciprocal(p.lambda) : 0.0;
+    a.inv_mu = model == WLP_MODEL_MM1 ? exact_reciprocal(p.mu) : 0.0;
+    a.out0 = o0;
+    a.out1 = o1;
+    a.out2 = o2;
+    if (mode == WLP_MODE_TLP) {
+        const int64_t block = std::min<int64_t>(count, tlp_block);
+        grid_out = static_cast<int>((count + block - 1) / block);
+        WLP_CUDA(launch_tlp(model, a, tlp_block, st));
+        return WLP_OK;
+    }
+    // WLP, and SEQUENTIAL (replication order is irrelevant to the per-replication result;
+    // the engine has no host execution path).
+    grid_out = wlp_grid(c, model, count);
+    if (model == WLP_MODEL_MM1) {
+        WLP_CUDA(launch_wlp(model, a, c.mm1_lane.p, c.mm1_skip.p, 0, grid_out, st));
+    } else {
+        const int64_t K = (a.n + 31) / 32;
+        const uint32_t* tab = nullptr;
+        WLP_TRY(lane_table(c, 2ull * static_cast<uint64_t>(K), tab));
+        WLP_CUDA(launch_wlp(model, a, tab, nullptr, K, grid_out, st));
+    }
+    return WLP_OK;
+}
+
+void fill_report(DevCtx& c, int model, int mode, int tlp_block, int64_t count, int grid, float ms, wlp_report* rep) {
+    if (!rep) return;
+    std::memset(rep, 0, sizeof *rep);
+    rep->kernel_ms = ms;
+    rep->total_cycles = static_cast<int64_t>(std::llround(static_cast<double>(ms) * c.clock_khz));
+    int64_t bps, warps_per_block;
+    if (mode == WLP_MODE_TLP) {
+        const int block = static_cast<int>(std::min<int64_t>(count, tlp_block));
+        bps = tlp_blocks_per_sm(model, block);
+        warps_per_block = (block + 31) / 32;
+    } else {
+        bps = c.wlp_bps[model];
+        warps_per_block = (model == WLP_MODEL_MM1 ? kMm1Block : kWlpBlock) / 32;
+    }
+    const int64_t resident = bps * c.sms;
+    rep->waves_executed = (grid + resident - 1) / resident;
+    rep->peak_resident_warps = std::min<int64_t>(grid, resident) * warps_per_block;
+}
+
+int stats_device(DevCtx& c, const double* x, int64_t n, int pass, wlp_stats* s, cudaStream_t st) {
+    const int grid = std::max(1, std::min<int>(c.sms * 4, static_cast<int>((n + 255) / 256)));
+    WLP_CUDA(c.partials.ensure(2 * grid));
+    const double center = pass == 1 ? 0.0 : s->center;
+    WLP_CUDA(launch_stats(x, n, pass, center, c.partials.p, grid, st));
+    const int used = n <= 256 ? 1 : grid;
+    std::vector<double> h(2 * used);
+    WLP_CUDA(cudaMemcpyAsync(h.data(), c.partials.p, h.size() * 8, cudaMemcpyDeviceToHost, st));
+    WLP_CUDA(cudaStreamSynchronize(st));
+    double hi = 0.0, lo = 0.0;
+    for (int b = 0; b < used; ++b) {
+        dd_add(hi, lo, h[2 * b]);
+        lo += h[2 * b + 1];
+    }
+    // renormalise
+    const double t = hi + lo;
+    lo = lo - (t - hi);
+    hi = t;
+    if (pass == 1) {
+        s->n = n;
+        s->sum_hi = hi;
+        s->sum_lo = lo;
+        s->center = (hi + lo) / static_cast<double>(n);
+    } else {
+        s->ss_hi = hi;
+        s->ss_lo = lo;
+    }
+    return WLP_OK;
+}
+
+int ci_from_stats(const wlp_stats* s, double level, wlp_ci* ci) {
+    if (s->n < 2) return fail(WLP_EDOMAIN, "confidence_interval: need at least 2 samples");
+    if (!(level > 0.0 && level < 1.0)) return fail(WLP_EDOMAIN, "confidence_interval: level outside (0,1)");
+    const double n = static_cast<double>(s->n);
+    const double mean = (s->sum_hi + s->sum_lo) / n;
+    const double sd = std::sqrt((s->ss_hi + s->ss_lo) / static_cast<double>(s->n - 1));
+    double z = 0.0;
+    WLP_TRY(inv_normal(0.5 + level / 2.0, &z));
+    ci->mean = mean;
+    ci->half_width = z * sd / std::sqrt(n);
+    ci->level = level;
+    ci->n = s->n;
+    ci->warn_small_sample = s->n < 30 ? 1 : 0;
+    return WLP_OK;
+}
+
+int ci_device(DevCtx& c, const double* d_x, int64_t n, double level, wlp_ci* ci, cudaStream_t st) {
+    if (n < 2) return fail(WLP_EDOMAIN, "confidence_interval: need at least 2 samples");
+    if (!(level > 0.0 && level < 1.0)) return fail(WLP_EDOMAIN, "confidence_interval: level outside (0,1)");
+    wlp_stats s{};
+    WLP_TRY(stats_device(c, d_x, n, 1, &s, st));
+    WLP_TRY(stats_device(c, d_x, n, 2, &s, st));
+    return ci_from_stats(&s, level, ci);
+}
+
+void copy_warning(const std::string& w, char* buf, int cap) {
+    if (!buf || cap <= 0) return;
+    const size_t n = std::min<size_t>(w.size(), static_cast<size_t>(cap - 1));
+    std::memcpy(buf, w.data(), n);
+    buf[n] = 0;
+}
+
+int n_outputs(int model) { return model == WLP_MODEL_MM1 ? 3 : 1; }
+
+}  // namespace
+}  // namespace wlp
+
+using namespace wlp;
+
+extern "C" {
+
+const char* wlp_last_error(void) { return g_err.c_str(); }
+int wlp_version(void) { return 1; }
+
+int wlp_validate_params(int model, const wlp_params* p, char* warn, int warn_cap) {
+    std::string w;
+    WLP_TRY(validate(model, p, &w));
+    copy_warning(w, warn, warn_cap);
+    return WLP_OK;
+}
+
+int wlp_plan_launch(int64_t replications, int mode, int tlp_block_size, int64_t grid_limit, wlp_launch_cfg* cfg,
+                    char* warn, int warn_cap) {
+    std::string w;
+    WLP_TRY(plan(replications, mode, tlp_block_size, grid_limit, cfg, &w));
+    copy_warning(w, warn, warn_cap);
+    return WLP_OK;
+}
+
+int wlp_master_from_seed(uint64_t seed, uint32_t out[3]) {
+    const Taus t = master_from_seed(seed);
+    out[0] = t.s1;
+    out[1] = t.s2;
+    out[2] = t.s3;
+    return WLP_OK;
+}
+
+int wlp_make_state(uint32_t s1, uint32_t s2, uint32_t s3, uint32_t out[3]) {
+    const Taus t = make_state(s1, s2, s3);
+    out[0] = t.s1;
+    out[1] = t.s2;
+    out[2] = t.s3;
+    return WLP_OK;
+}
+
+int wlp_jump_host(const uint32_t s[3], uint64_t n, uint32_t out[3]) {
+    const Taus t = jump_state(Taus{s[0], s[1], s[2]}, n);
+    out[0] = t.s1;
+    out[1] = t.s2;
+    out[2] = t.s3;
+    return WLP_OK;
+}
+
+int wlp_inverse_normal_cdf(double p, double* z) { return inv_normal(p, z); }
+
+int wlp_spacing_rejections(const wlp_special* specials, int64_t n_special, const int64_t* prev, int64_t n_prev,
+                           int64_t* out, int64_t out_cap, int64_t* n_out) {
+    std::vector<SpecialRec> sp(n_special);
+    if (n_special) std::memcpy(sp.data(), specials, n_special * sizeof(SpecialRec));
+    std::vector<int64_t> pv(prev, prev + n_prev), res;
+    WLP_TRY(spacing_rejections(sp, pv, res));
+    if (static_cast<int64_t>(res.size()) > out_cap) return fail(WLP_EINTERNAL, "rejection buffer too small");
+    std::copy(res.begin(), res.end(), out);
+    *n_out = static_cast<int64_t>(res.size());
+    return WLP_OK;
+}
+
+int wlp_stats_merge(wlp_stats* a, const wlp_stats* b) {
+    a->n += b->n;
+    dd_add(a->sum_hi, a->sum_lo, b->sum_hi);
+    a->sum_lo += b->sum_lo;
+    dd_add(a->ss_hi, a->ss_lo, b->ss_hi);
+    a->ss_lo += b->ss_lo;
+    return WLP_OK;
+}
+
+int wlp_ci_from_stats(const wlp_stats* s, double level, wlp_ci* ci) { return ci_from_stats(s, level, ci); }
+
+int wlp_device_count(int* n) {
+    WLP_CUDA(cudaGetDeviceCount(n));
+    return WLP_OK;
+}
+
+int wlp_taus_stream(uint32_t s1, uint32_t s2, uint32_t s3, int64_t n, uint32_t* out, int out_on_device,
+                    void* stream) {
+    if (n < 0) return fail(WLP_EDOMAIN, "taus_stream: negative count");
+    DevCtx* c;
+    std::unique_lock<std::mutex> lk;
+    WLP_TRY(acquire(c, lk));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint32_t* d = out;
+    if (!out_on_device) {
+        WLP_CUDA(c->seeds.ensure(std::max<int64_t>(n, 1)));
+        d = c->seeds.p;
+    }
+    WLP_CUDA(launch_taus_stream(c->powers.p, make_state(s1, s2, s3), n, d, st));
+    if (!out_on_device) {
+        WLP_CUDA(cudaMemcpyAsync(out, d, n * 4, cudaMemcpyDeviceToHost, st));
+        WLP_CUDA(cudaStreamSynchronize(st));
+    }
+    return WLP_OK;
+}
+
+int wlp_debug_neg_log1m(const uint32_t* k, int64_t n, double* out) {
+    if (n < 0) return fail(WLP_EDOMAIN, "neg_log1m: negative count");
+    if (n == 0) return WLP_OK;
+    DevCtx* c;
+    std::unique_lock<std::mutex> lk;
+    WLP_TRY(acquire(c, lk));
+    WLP_CUDA(c->in_seeds.ensure(n));
+    WLP_CUDA(c->outs.ensure(n));
+    WLP_CUDA(cudaMemcpy(c->in_seeds.p, k, n * 4, cudaMemcpyHostToDevice));
+    WLP_CUDA(launch_neg_log1m(c->in_seeds.p, n, c->outs.p, nullptr));
+    WLP_CUDA(cudaMemcpy(out, c->outs.p, n * 8, cudaMemcpyDeviceToHost));
+    return WLP_OK;
+}
+
+int wlp_seed_streams(uint64_t master_seed, int64_t slot_begin, int64_t count, const int64_t* rejected,
+                     int64_t n_rejected, uint32_t* s_out, int out_on_device, void* stream, wlp_special* specials,
+                     int64_t special_cap, int64_t* n_special) {
+    if (count < 0 || slot_begin < 0) return fail(WLP_EDOMAIN, "seed_streams: negative range");
+    DevCtx* c;
+    std::unique_lock<std::mutex> lk;
+    WLP_TRY(acquire(c, lk));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint32_t* d = s_out;
+    if (!out_on_device) {
+        WLP_CUDA(c->seeds.ensure(3 * std::max<int64_t>(count, 1)));
+        d = c->seeds.p;
+    }
+    std::vector<int64_t> rej(rejected, rejected + n_rejected);
+    WLP_TRY(seed_async(*c, master_from_seed(master_seed), slot_begin, count, rej, d, st));
+    std::vector<SpecialRec> sp;
+    int64_t nt = 0;
+    WLP_TRY(read_specials(*c, st, sp, nt));
+    if (n_special) *n_special = nt;
+    if (specials) std::memcpy(specials, sp.data(), std::min<int64_t>(nt, special_cap) * sizeof(SpecialRec));
+    if (!out_on_device) {
+        WLP_CUDA(cudaMemcpy(s_out, d, 3 * count * 4, cudaMemcpyDeviceToHost));
+    }
+    return WLP_OK;
+}
+
+int wlp_seed_streams_exact(uint64_t master_seed, int64_t count, uint32_t* s_out, int out_on_device, void* stream) {
+    if (count < 0) return fail(WLP_EDOMAIN, "seed_streams: negative count");
+    DevCtx* c;
+    std::unique_lock<std::mutex> lk;
+    WLP_TRY(acquire(c, lk));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint32_t* d = s_out;
+    if (!out_on_device) {
+        WLP_CUDA(c->seeds.ensure(3 * std::max<int64_t>(count, 1)));
+        d = c->seeds.p;
+    }
+    const Taus master = master_from_seed(master_seed);
+    std::vector<int64_t> rej;
+    for (;;) {
+        WLP_TRY(seed_async(*c, master, 0, count, rej, d, st));
+        std::vector<SpecialRec> sp;
+        int64_t nt = 0;
+        WLP_TRY(read_specials(*c, st, sp, nt));
+        if (nt < 2) break;
+        std::vector<int64_t> next;
+        WLP_TRY(spacing_rejections(sp, rej, next));
+        if (next == rej) break;
+        rej.swap(next);
+    }
+    if (!out_on_device) WLP_CUDA(cudaMemcpy(s_out, d, 3 * count * 4, cudaMemcpyDeviceToHost));
+    return WLP_OK;
+}
+
+int wlp_run_streams(int model, const wlp_params* p, int mode, const uint32_t* s, int64_t count, int s_on_device,
+                    double* out0, double* out1, double* out2, int out_on_device, void* stream, wlp_report* report) {
+    WLP_TRY(check_model_mode(model, mode));
+    if (count < 0) return fail(WLP_EDOMAIN, "run_streams: negative count");
+    wlp_params q = *p;
+    q.replications = std::max<int64_t>(count, 1);
+    WLP_TRY(validate(model, &q, nullptr));
+    if (count == 0) return WLP_OK;
+    DevCtx* c;
+    std::unique_lock<std::mutex> lk;
+    WLP_TRY(acquire(c, lk));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const uint32_t* ds = s;
+    if (!s_on_device) {
+        WLP_CUDA(c->in_seeds.ensure(3 * count));
+        WLP_CUDA(cudaMemcpyAsync(c->in_seeds.p, s, 3 * count * 4, cudaMemcpyHostToDevice, st));
+        ds = c->in_seeds.p;
+    }
+    double *o0 = out0, *o1 = out1, *o2 = out2;
+    if (!out_on_device) {
+        WLP_CUDA(c->outs.ensure(3 * count));
+        o0 = c->outs.p;
+        o1 = c->outs.p + count;
+        o2 = c->outs.p + 2 * count;
+    }
+    int grid = 0;
+    if (report) WLP_CUDA(cudaEventRecord(c->ev0, st));
+    WLP_TRY(model_async(*c, model, q, mode, 256, ds, count, o0, o1, o2, st, grid));
+    if (report) WLP_CUDA(cudaEventRecord(c->ev1, st));
+    if (!out_on_device) {
+        WLP_CUDA(cudaMemcpyAsync(out0, o0, count * 8, cudaMemcpyDeviceToHost, st));
+        if (model == WLP_MODEL_MM1) {
+            WLP_CUDA(cudaMemcpyAsync(out1, o1, count * 8, cudaMemcpyDeviceToHost, st));
+            WLP_CUDA(cudaMemcpyAsync(out2, o2, count * 8, cudaMemcpyDeviceToHost, st));
+        }
+    }
+    if (report || !out_on_device) WLP_CUDA(cudaStreamSynchronize(st));
+    if (report) {
+        float ms = 0.f;
+        WLP_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+        fill_report(*c, model, mode, 256, count, grid, ms, report);
+    }
+    return WLP_OK;
+}
+
+int wlp_run_shard(int model, const wlp_params* p, int mode, uint64_t master_seed, int tlp_block_size,
+                  int64_t r_begin, int64_t r_count, const int64_t* rejected, int64_t n_rejected, double* out0,
+                  double* out1, double* out2, int out_on_device, void* stream, wlp_special* specials,
+                  int64_t special_cap, int64_t* n_special, wlp_report* report) {
+    WLP_TRY(check_model_mode(model, mode));
+    WLP_TRY(validate(model, p, nullptr));
+    WLP_TRY(plan(p->replications, mode, tlp_block_size, 0x7FFFFFFF, nullptr, nullptr));
+    if (r_begin < 0 || r_count < 0 || r_begin + r_count > p->replications)
+        return fail(WLP_EDOMAIN, "run_shard: shard outside [0, replications)");
+    if (r_count == 0) {
+        if (n_special) *n_special = 0;
+        return WLP_OK;
+    }
+    DevCtx* c;
+    std::unique_lock<std::mutex> lk;
+    WLP_TRY(acquire(c, lk));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    WLP_CUDA(c->seeds.ensure(3 * r_count));
+    double *o0 = out0, *o1 = out1, *o2 = out2;
+    if (!out_on_device) {
+        WLP_CUDA(c->outs.ensure(3 * r_count));
+        o0 = c->outs.p;
+        o1 = c->outs.p + r_count;
+        o2 = c->outs.p + 2 * r_count;
+    }
+    std::vector<int64_t> rej(rejected, rejected + n_rejected);
+    WLP_TRY(seed_async(*c, master_from_seed(master_seed), r_begin, r_count, rej, c->seeds.p, st));
+    int grid = 0;
+    if (report) WLP_CUDA(cudaEventRecord(c->ev0, st));
+    WLP_TRY(model_async(*c, model, *p, mode, tlp_block_size, c->seeds.p, r_count, o0, o1, o2, st, grid));
+    if (report) WLP_CUDA(cudaEventRecord(c->ev1, st));
+    if (!out_on_device) {
+        WLP_CUDA(cudaMemcpyAsync(out0, o0, r_count * 8, cudaMemcpyDeviceToHost, st));
+        if (model == WLP_MODEL_MM1) {
+            WLP_CUDA(cudaMemcpyAsync(out1, o1, r_count * 8, cudaMemcpyDeviceToHost, st));
+            WLP_CUDA(cudaMemcpyAsync(out2, o2, r_count * 8, cudaMemcpyDeviceToHost, st));
+        }
+    }
+    if (specials || n_special || report || !out_on_device) {
+        std::vector<SpecialRec> sp;
+        int64_t nt = 0;
+        WLP_TRY(read_specials(*c, st, sp, nt));
+        if (n_special) *n_special = nt;
+        if (specials) std::memcpy(specials, sp.data(), std::min<int64_t>(nt, special_cap) * sizeof(SpecialRec));
+    }
+    if (report) {
+        float ms = 0.f;
+        WLP_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+        fill_report(*c, model, mode, tlp_block_size, r_count, grid, ms, report);
+    }
+    return WLP_OK;
+}
+
+int wlp_run(int model, const wlp_params* p, int mode, uint64_t master_seed, int tlp_block_size, double* out0,
+            double* out1, double* out2, int out_on_device, void* stream, wlp_report* report, wlp_ci* ci,
+            double level, char* warn, int warn_cap) {
+    WLP_TRY(check_model_mode(model, mode));
+    std::string pw, lw;
+    WLP_TRY(validate(model, p, &pw));
+    WLP_TRY(plan(p->replications, mode, tlp_block_size, 0x7FFFFFFF, nullptr, &lw));
+    // build_kernel (models.cpp:294-299): params warning "; " plan warning
+    copy_warning(!pw.empty() && !lw.empty() ? pw + "; " + lw : (!pw.empty() ? pw : lw), warn, warn_cap);
+    const int64_t R = p->replications;
+    DevCtx* c;
+    std::unique_lock<std::mutex> lk;
+    WLP_TRY(acquire(c, lk));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    WLP_CUDA(c->seeds.ensure(3 * R));
+    double *o0 = out0, *o1 = out1, *o2 = out2;
+    if (!out_on_device) {
+        WLP_CUDA(c->outs.ensure(3 * R));
+        o0 = c->outs.p;
+        o1 = c->outs.p + R;
+        o2 = c->outs.p + 2 * R;
+    }
+    const Taus master = master_from_seed(master_seed);
+    std::vector<int64_t> rej;
+    int grid = 0;
+    for (;;) {
+        // Seeding and the model run back to back; the spacing check below only forces a
+        // re-run when two special candidates actually share a key.
+        WLP_TRY(seed_async(*c, master, 0, R, rej, c->seeds.p, st));
+        if (report) WLP_CUDA(cudaEventRecord(c->ev0, st));
+        WLP_TRY(model_async(*c, model, *p, mode, tlp_block_size, c->seeds.p, R, o0, o1, o2, st, grid));
+        if (report) WLP_CUDA(cudaEventRecord(c->ev1, st));
+        std::vector<SpecialRec> sp;
+        int64_t nt = 0;
+        WLP_TRY(read_specials(*c, st, sp, nt));
+        if (nt < 2) break;
+        std::vector<int64_t> next;
+        WLP_TRY(spacing_rejections(sp, rej, next));
+        if (next == rej) break;
+        rej.swap(next);
+    }
+    if (ci) {
+        for (int k = 0; k < n_outputs(model); ++k) {
+            const double* d = k == 0 ? o0 : k == 1 ? o1 : o2;
+            WLP_TRY(ci_device(*c, d, R, level, &ci[k], st));
+        }
+    }
+    if (!out_on_device) {
+        WLP_CUDA(cudaMemcpyAsync(out0, o0, R * 8, cudaMemcpyDeviceToHost, st));
+        if (model == WLP_MODEL_MM1) {
+            WLP_CUDA(cudaMemcpyAsync(out1, o1, R * 8, cudaMemcpyDeviceToHost, st));
+            WLP_CUDA(cudaMemcpyAsync(out2, o2, R * 8, cudaMemcpyDeviceToHost, st));
+        }
+        WLP_CUDA(cudaStreamSynchronize(st));
+    }
+    if (report) {
+        float ms = 0.f;
+        WLP_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+        fill_report(*c, model, mode, tlp_block_size, R, grid, ms, report);
+    }
+    return WLP_OK;
+}
+
+int wlp_stats_device(const double* x, int64_t n, int pass, wlp_stats* stats, void* stream) {
+    if (n < 1) return fail(WLP_EDOMAIN, "stats: empty input");
+    if (pass != 1 && pass != 2) return fail(WLP_EDOMAIN, "stats: pass must be 1 or 2");
+    DevCtx* c;
+    std::unique_lock<std::mutex> lk;
+    WLP_TRY(acquire(c, lk));
+    return stats_device(*c, x, n, pass, stats, static_cast<cudaStream_t>(stream));
+}
+
+int wlp_confidence_interval(const double* samples, int64_t n, double level, wlp_ci* ci) {
+    if (n < 2) return fail(WLP_EDOMAIN, "confidence_interval: need at least 2 samples");
+    if (!(level > 0.0 && level < 1.0)) return fail(WLP_EDOMAIN, "confidence_interval: level outside (0,1)");
+    DevCtx* c;
+    std::unique_lock<std::mutex> lk;
+    WLP_TRY(acquire(c, lk));
+    WLP_CUDA(c->stats_in.ensure(n));
+    WLP_CUDA(cudaMemcpy(c->stats_in.p, samples, n * 8, cudaMemcpyHostToDevice));
+    return ci_device(*c, c->stats_in.p, n, level, ci, nullptr);
+}
+
+int wlp_shutdown(void) {
+    std::lock_guard<std::mutex> g(g_ctx_mu);
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return WLP_OK;
+    auto it = g_ctx.find(dev);
+    if (it == g_ctx.end()) return WLP_OK;
+    DevCtx& c = *it->second;
+    std::lock_guard<std::mutex> lk(c.mu);
+    cudaDeviceSynchronize();
+    c.powers.release();
+    for (auto& kv : c.lane_tabs) kv.second.release();
+    c.lane_tabs.clear();
+    c.mm1_lane.release();
+    c.mm1_skip.release();
+    c.seeds.release();
+    c.in_seeds.release();
+    c.outs.release();
+    c.partials.release();
+    c.stats_in.release();
+    c.specials.release();
+    c.counter.release();
+    c.rejected.release();
+    if (c.ev0) cudaEventDestroy(c.ev0);
+    if (c.ev1) cudaEventDestroy(c.ev1);
+    c.ev0 = c.ev1 = nullptr;
+    c.ready = false;
+    return WLP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,265 @@
+"""Parity of the sm_100a path (through the C ABI) with the CPU oracle: bit-exact raw
+streams, stream seeds and per-replication outputs; aggregate statistics within 1e-12
+relative (bit-exact for R <= 256, where the device sums sequentially like the
+reference, models.cpp:104-109). Run on the B200 box: pytest -m gpu."""
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import GOLD, golden, unhex
+
+pytestmark = pytest.mark.gpu
+
+MODES = ("Sequential", "Tlp", "Wlp")
+
+
+def P(w, **kw):
+    return w.ModelParams(**kw)
+
+
+def hexes(a):
+    return [float(x).hex() for x in a]
+
+
+def test_native_library_is_the_cuda_build(gpu):
+    lib = gpu.native_library()
+    assert lib._name.endswith("libwlp_b200.so")
+    assert gpu.device_count() >= 1
+
+
+# ---- raw streams and seeding ------------------------------------------------------------
+
+
+def test_taus88_golden(gpu):
+    g = golden("taus88.json")  # proj/taus88.golden
+    got = gpu.taus_stream(gpu.RngState(*g["seed"]), 100)
+    assert got.tolist() == g["outputs"]
+
+
+def test_taus_stream_long_jump_ahead(gpu, port):
+    # 64-output chunks per thread start by GF(2) jump-ahead: every chunk boundary checked
+    for seed in [(1, 2, 3), (2, 8, 16), (0xFFFFFFFF, 0xFFFFFFF0, 0x80000000), (123456789, 362436069, 521288629)]:
+        st = gpu.make_rng_state(*seed)
+        got = gpu.taus_stream(st, 200_003)
+        assert np.array_equal(got, port.taus_stream(*seed, 200_003))
+
+
+def test_random_spacing_digests(gpu):
+    for seed, want in golden("spacing.json").items():
+        k = gpu.random_spacing_seed(int(seed), want["count"])
+        assert k[:, :4].T.tolist() == want["head"]
+        assert hashlib.sha256(np.ascontiguousarray(k, dtype="<u4").tobytes()).hexdigest() == want["sha256"]
+
+
+def test_random_spacing_large_vs_port(gpu, port):
+    k = gpu.random_spacing_seed(77, 1_000_003)
+    assert np.array_equal(k, port.random_spacing(77, 1_000_003))
+
+
+def test_seed_shards_and_rejection_remap(gpu, port):
+    R = 20_000
+    whole = port.random_spacing(5, R + 3)
+    # shards of the same run concatenate to the whole run
+    parts = [gpu.seed_streams(5, b, c)[0] for b, c in ((0, 7000), (7000, 1), (7001, R - 7001))]
+    assert np.array_equal(np.concatenate(parts, axis=1), whole[:, :R])
+    # a rejection list (as produced by a key collision) skips those candidates, exactly
+    # like random_spacing's redraw loop (rng.cpp:74-84)
+    rej = [0, 4, 5, 19_999]
+    keys, _ = gpu.seed_streams(5, 0, R - 1, rejected=rej)
+    keep = np.array([i for i in range(R + 3) if i not in rej][: R - 1])
+    assert np.array_equal(keys, whole[:, keep])
+    keys2, _ = gpu.seed_streams(5, 12_345, 100, rejected=rej)
+    assert np.array_equal(keys2, whole[:, keep[12_345:12_445]])
+
+
+def test_special_candidates_reported(gpu):
+    # over many candidates some key component falls below twice its minimum
+    keys, specials = gpu.seed_streams(11, 0, 3_000_000)
+    s1, s2, s3 = keys.astype(np.int64)
+    mask = (s1 < 4) | (s2 < 16) | (s3 < 32)
+    assert sorted(s.index for s in specials) == np.nonzero(mask)[0].tolist()
+
+
+# ---- per-replication outputs --------------------------------------------------------------
+
+
+@pytest.mark.parametrize("case", golden("replications.json")["cases"],
+                         ids=lambda c: f"m{c['model']}-s{c['seed']}-{c['params']}")
+def test_run_model_golden_all_modes(gpu, case):
+    kw = dict(case["params"])
+    p = gpu.ModelParams(**kw)
+    for mode in MODES:
+        run = gpu.run_model(gpu.ModelKind(case["model"]), p, gpu.ExecutionMode[mode], master_seed=case["seed"])
+        for name, want in case["outputs"].items():
+            assert hexes(run.outputs[name]) == want, (mode, name)
+
+
+@pytest.mark.parametrize("model", [0, 1, 2])
+def test_medium_runs_vs_port(gpu, port, model):
+    kw = {0: dict(replications=4099, draws=1000), 1: dict(replications=1500, clients=999, lambda_=0.6, mu=0.9),
+          2: dict(replications=5003, steps=1000, chunks=30)}[model]
+    p = gpu.ModelParams(**kw)
+    want = port.run_model(model, oracle.params_from(p), 20260201)
+    for mode in MODES:
+        run = gpu.run_model(gpu.ModelKind(model), p, gpu.ExecutionMode[mode], master_seed=20260201)
+        for name in oracle.OUTPUTS[model]:
+            assert np.array_equal(run.outputs[name], want[name]), (mode, name)
+
+
+def test_run_streams_pi_mm1_walk_replication(gpu, port):
+    keys = port.random_spacing(3, 50)
+    st = gpu.RngState(*[int(x) for x in keys[:, 7]])
+    seed = keys[:, 7:8]
+    assert gpu.pi_replication(777, st) == port.replications(0, oracle.params(draws=777), seed)["out"][0]
+    m = port.replications(1, oracle.params(clients=321, lambda_=0.25, mu=2.0), seed)
+    assert gpu.mm1_replication(321, 0.25, 2.0, st) == (m["outIdle"][0], m["outWait"][0], m["outSys"][0])
+    assert gpu.walk_replication(99, 4, st) == port.replications(2, oracle.params(steps=99, chunks=4), seed)["out"][0]
+
+
+def test_statistical_pins(gpu):
+    pins = golden("pins.json")
+    r = gpu.run_model(gpu.ModelKind.Pi, P(gpu, replications=1, draws=1_000_000), gpu.ExecutionMode.Wlp,
+                      master_seed=42)
+    assert hexes(r.primary) == pins["pi_1x1e6"]["out"]
+    for mode in ("Wlp", "Tlp"):
+        r = gpu.run_model(gpu.ModelKind.Mm1, P(gpu, replications=30, clients=100_000), gpu.ExecutionMode[mode],
+                          master_seed=42)
+        for k in ("outIdle", "outWait", "outSys"):
+            assert hexes(r.outputs[k]) == pins["mm1_30x1e5"][k]
+    r = gpu.run_model(gpu.ModelKind.Walk, P(gpu, replications=3000, steps=1000, chunks=30), gpu.ExecutionMode.Wlp,
+                      master_seed=42)
+    assert hashlib.sha256(r.primary.astype("<f8").tobytes()).hexdigest() == pins["walk_3000x1000"]["sha256"]
+
+
+def test_device_log_port_vs_glibc_fixture(gpu):
+    g = golden("log_pairs.json")
+    got = gpu.debug_neg_log1m(np.asarray(g["k"], dtype=np.uint32))
+    assert hexes(got) == g["neg_log1m"]
+
+
+def test_device_log_port_vs_host_libm_dense(gpu, port):
+    # 2^24 evenly spread model inputs + the whole near-one window edge region
+    k = np.concatenate([np.arange(0, 2**32, 256, dtype=np.uint64), np.arange(2**28 - 4096, 2**28 + 4096)])
+    k = k.astype(np.uint32)
+    got = gpu.debug_neg_log1m(k)
+    if oracle.host_log_variant() != "fma":
+        pytest.skip("this host's libm is not the FMA variant the fixtures were made with")
+    want = port.exponential_from_u(k.astype(np.float64) * 2.0**-32, 1.0)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+# ---- statistics ---------------------------------------------------------------------------
+
+
+def test_confidence_interval_golden(gpu):
+    g = golden("stats.json")
+    for c in g["ci"]:
+        ci = gpu.confidence_interval(unhex(c["x"]), c["level"])
+        assert ci.n == c["n"] and ci.warnSmallSample == c["warn"]
+        if c["n"] <= 256:  # sequential device sum: bit-exact
+            assert ci.mean.hex() == c["mean"] and ci.halfWidth.hex() == c["half_width"]
+        else:
+            assert ci.mean == pytest.approx(float.fromhex(c["mean"]), rel=1e-12)
+            assert ci.halfWidth == pytest.approx(float.fromhex(c["half_width"]), rel=1e-12)
+    with pytest.raises(gpu.DomainError):
+        gpu.confidence_interval([1.0])
+    with pytest.raises(gpu.DomainError):
+        gpu.confidence_interval([1.0, 2.0], 1.0)
+
+
+def test_device_ci_of_run_matches_reference(gpu, ref):
+    for model, kw in [(0, dict(replications=100_000, draws=100)), (1, dict(replications=20_000, clients=200)),
+                      (2, dict(replications=50_000, steps=200, chunks=30))]:
+        p = gpu.ModelParams(**kw)
+        outs = [np.empty(p.replications) for _ in oracle.OUTPUTS[model]]
+        cis = gpu.run_model_into(gpu.ModelKind(model), p, gpu.ExecutionMode.Wlp, 42, outs, on_device=False,
+                                 ci_level=0.95)
+        for o, ci in zip(outs, cis):
+            m, hw, n, warn = ref.confidence_interval(o, 0.95)
+            assert ci.n == n and ci.mean == pytest.approx(m, rel=1e-12, abs=1e-300)
+            assert ci.halfWidth == pytest.approx(hw, rel=1e-12)
+
+
+def test_sweep_golden_means(gpu):
+    # proj/tests/golden/sweep_pi.golden: seed 42, draws 100, R = 1, 2 — mean / CI columns
+    rows = [r.split(",") for r in (GOLD / "sweep_pi.csv").read_text().splitlines()[1:]]
+    for R, mode, _, *_, mean, lo, hi in rows:
+        run = gpu.run_model(gpu.ModelKind.Pi, P(gpu, replications=int(R), draws=100), gpu.mode_from_name(mode),
+                            master_seed=42)
+        if int(R) == 1:
+            assert repr(run.primary[0]) == mean
+        else:
+            ci = gpu.confidence_interval(run.primary)
+            assert (repr(ci.mean), repr(ci.low()), repr(ci.high())) == (mean, lo, hi)
+
+
+# ---- shards, errors, warnings ---------------------------------------------------------------
+
+
+def test_shards_concatenate_to_whole_run(gpu):
+    p = P(gpu, replications=10_007, clients=300)
+    whole = gpu.run_model(gpu.ModelKind.Mm1, p, gpu.ExecutionMode.Wlp, master_seed=9)
+    parts = {k: [] for k in ("outIdle", "outWait", "outSys")}
+    for b, c in ((0, 3000), (3000, 5000), (8000, 2007)):
+        outs = [np.empty(c) for _ in range(3)]
+        sp = gpu.run_shard(gpu.ModelKind.Mm1, p, gpu.ExecutionMode.Tlp, 9, b, c, outs, on_device=False)
+        assert isinstance(sp, list)
+        for k, o in zip(parts, outs):
+            parts[k].append(o)
+    for k in parts:
+        assert np.array_equal(np.concatenate(parts[k]), whole.outputs[k])
+
+
+def test_errors_and_warnings(gpu):
+    with pytest.raises(gpu.DomainError):
+        gpu.run_model(gpu.ModelKind.Pi, P(gpu, replications=3, draws=0), gpu.ExecutionMode.Wlp)
+    with pytest.raises(gpu.DomainError):
+        gpu.run_model(gpu.ModelKind.Mm1, P(gpu, replications=3, mu=0.0), gpu.ExecutionMode.Tlp)
+    with pytest.raises(gpu.PlanError):
+        gpu.run_model(gpu.ModelKind.Walk, P(gpu, replications=3), gpu.ExecutionMode.Tlp, tlp_block_size=4096)
+    # test_models.cpp:350-366
+    run = gpu.run_model(gpu.ModelKind.Mm1, P(gpu, replications=50, clients=20, lambda_=1.0, mu=0.5),
+                        gpu.ExecutionMode.Tlp, master_seed=1)
+    assert "unstable" in run.warning and "warp" in run.warning
+    run = gpu.run_model(gpu.ModelKind.Mm1, P(gpu, replications=64, clients=20), gpu.ExecutionMode.Tlp, master_seed=1)
+    assert run.warning is None
+    assert run.report.kernel_ms > 0 and run.report.totalCycles > 0
+
+
+# ---- full-size properties (BASELINE configs 2-4) --------------------------------------------
+
+
+def _device_run(gpu, model, p, mode, seed):
+    import torch
+
+    outs = [torch.empty(p.replications, dtype=torch.float64, device="cuda") for _ in oracle.OUTPUTS[model]]
+    gpu.run_model_into(gpu.ModelKind(model), p, mode, seed, outs, on_device=True)
+    torch.cuda.synchronize()
+    return [o.cpu().numpy() for o in outs]
+
+
+@pytest.mark.parametrize("model,kw", [(0, dict(replications=1_000_000, draws=10_000)),
+                                      (2, dict(replications=100_000, steps=1000, chunks=30)),
+                                      (0, dict(replications=10_000_000, draws=1000)),
+                                      (1, dict(replications=10_000_000, clients=1000)),
+                                      (2, dict(replications=10_000_000, steps=1000, chunks=30))],
+                         ids=["cfg2-pi", "cfg3-walk", "cfg4-pi", "cfg4-mm1", "cfg4-walk"])
+def test_full_size_wlp_equals_tlp_and_sampled_oracle(gpu, ref, model, kw):
+    p = gpu.ModelParams(**kw)
+    wlp = _device_run(gpu, model, p, gpu.ExecutionMode.Wlp, 42)
+    tlp = _device_run(gpu, model, p, gpu.ExecutionMode.Tlp, 42)
+    for a, b in zip(wlp, tlp):
+        assert np.array_equal(a, b)
+    # a random sample of replications re-computed by the reference on the host
+    idx = np.sort(np.random.default_rng(0).choice(p.replications, 512, replace=False))
+    keys = gpu.random_spacing_seed(42, p.replications)[:, idx]
+    want = ref.replications(model, oracle.params_from(p), keys, nthreads=8)
+    for a, name in zip(wlp, oracle.OUTPUTS[model]):
+        assert np.array_equal(a[idx], want[name])
+    # integer-valued outputs stay in range; pi mean near pi
+    if model == 0:
+        assert abs(wlp[0].mean() - np.pi) < 1e-3
+    if model == 2:
+        assert wlp[0].min() >= 0 and wlp[0].max() < kw["chunks"] and np.all(wlp[0] == np.floor(wlp[0]))
