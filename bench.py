@@ -334,7 +334,8 @@ def main():
     units = R_PER_GPU * DRAWS
     achieved = units * INSTR_PER_UNIT[0] / 32 / (kernel_avg * 1e-3) / 1e9  # G warp-instr/s
     peak = 4 * sms * fmax * 1e6 / 1e9
-    nc = ncu_traffic().get("k_wlp_lanes<0>", {})
+    nc_all = ncu_traffic().get("k_wlp_lanes<0>", {})
+    nc = nc_all[sorted(nc_all)[-1]] if nc_all else {}  # latest committed capture
     roofline = {"bound": "issue", "kernel": "k_wlp_lanes<0> (pi WLP)", "achieved": achieved, "peak": peak,
                 "unit": "Gwarp-inst/s", "frac": achieved / peak, "traffic": nc.get("dram_bytes_per_launch"),
                 "algorithmic": f"{INSTR_PER_UNIT[0]} lane-instr/point x {units:.0e} points per launch / 32",

@@ -9,9 +9,12 @@
 // every plain + - * must stay unfused (host: -ffp-contract=off, device: --fmad=false),
 // every fused step is an explicit fma().
 //
-// Pinned by tools/check_glibc_log.c: identical bits to libm's log for every input the
+// Pinned by tools/check_glibc_log.cpp: identical bits to libm's log for every input the
 // model can produce, x = 1 - k*2^-32, k in [0, 2^32) (exhaustive), plus the generic
 // paths (subnormals, specials) on samples.
+//
+// Device code passes the {invc, logc} table as a pointer (a shared-memory copy: the
+// table index is data dependent, and a divergent __constant__ read serialises).
 #pragma once
 
 #include <stdint.h>
@@ -29,20 +32,19 @@
 namespace wlp {
 
 #if defined(__CUDACC__)
-__device__ __constant__ double kLogTabDev[256] = WLP_LOG_TAB_INIT;
+__device__ const double kLogTabDev[256] = WLP_LOG_TAB_INIT;  // global; kernels stage it in smem
 #endif
+static const double kLogTabHost[256] = WLP_LOG_TAB_INIT;
 
 #if defined(__CUDA_ARCH__)
-#define WLP_LOG_TAB kLogTabDev
 #define WLP_FMA(a, b, c) __fma_rn((a), (b), (c))
 #define WLP_MUL(a, b) __dmul_rn((a), (b))
 #define WLP_ADD(a, b) __dadd_rn((a), (b))
 #define WLP_SUB(a, b) __dsub_rn((a), (b))
 WLP_HD uint64_t wlp_as_u64(double x) { return static_cast<uint64_t>(__double_as_longlong(x)); }
 WLP_HD double wlp_as_f64(uint64_t x) { return __longlong_as_double(static_cast<long long>(x)); }
+WLP_HD int wlp_clz32(uint32_t x) { return __clz(static_cast<int>(x)); }
 #else
-static const double kLogTabHost[256] = WLP_LOG_TAB_INIT;
-#define WLP_LOG_TAB kLogTabHost
 #define WLP_FMA(a, b, c) fma((a), (b), (c))
 #define WLP_MUL(a, b) ((a) * (b))
 #define WLP_ADD(a, b) ((a) + (b))
@@ -57,12 +59,16 @@ WLP_HD double wlp_as_f64(uint64_t u) {
     memcpy(&x, &u, sizeof x);
     return x;
 }
+WLP_HD int wlp_clz32(uint32_t x) { return x ? __builtin_clz(x) : 32; }
 #endif
 
 // Inputs 1 - 2^-4 <= x < 1 + 0x1.09p-4 take the table-free polynomial path.
 constexpr uint64_t kLogNearLo = 0x3FEE000000000000ull;               // 1 - 0x1p-4
 constexpr uint64_t kLogNearSpan = 0x3FF1090000000000ull - kLogNearLo;  // up to 1 + 0x1.09p-4
 constexpr uint64_t kLogOff = 0x3fe6000000000000ull;  // table subintervals cover [OFF, 2*OFF)
+constexpr uint64_t kOneBits = 0x3FF0000000000000ull;
+
+WLP_HD bool log_is_near_one(uint64_t ix) { return ix - kLogNearLo < kLogNearSpan; }
 
 // log(x) for x within 1 - 2^-4 .. 1 + 0x1.09p-4 (x != 1): r = x - 1 is exact, log1p(r)
 // = r - r^2/2 + r^3 * P(r); the r^2/2 term is split hi/lo (rhi keeps 26 bits of r).
@@ -86,14 +92,15 @@ WLP_HD double log_near_one(double x) {
 }
 
 // log(x) for positive normal x outside the near-one window: x = 2^k * z, z in
-// [OFF, 2*OFF); log x = k*ln2 + log(c) + log1p(z/c - 1), c from the 128-entry table.
-WLP_HD double log_table(uint64_t ix) {
+// [OFF, 2*OFF); log x = k*ln2 + log(c) + log1p(z/c - 1), c from the 128-entry table
+// `tab` = {invc, logc} pairs.
+WLP_HD double log_table(uint64_t ix, const double* tab) {
     const uint64_t tmp = ix - kLogOff;
     const int i = static_cast<int>((tmp >> 45) & 127u);
     const int64_t k = static_cast<int64_t>(tmp) >> 52;
     const uint64_t iz = ix - (tmp & (0xfffull << 52));
-    const double invc = WLP_LOG_TAB[2 * i];
-    const double logc = WLP_LOG_TAB[2 * i + 1];
+    const double invc = tab[2 * i];
+    const double logc = tab[2 * i + 1];
     const double z = wlp_as_f64(iz);
     const double kd = static_cast<double>(k);
     constexpr double A[5] = WLP_LOG_POLY_INIT;
@@ -109,10 +116,10 @@ WLP_HD double log_table(uint64_t ix) {
 
 // glibc log() semantics for every double (specials follow e_log.c: log(0) = -inf,
 // log(<0) and log(nan) = nan, log(inf) = inf, subnormals normalised first).
-WLP_HD double glibc_log(double x) {
+WLP_HD double glibc_log_tab(double x, const double* tab) {
     uint64_t ix = wlp_as_u64(x);
-    if (ix - kLogNearLo < kLogNearSpan) {
-        if (ix == 0x3FF0000000000000ull) return 0.0;
+    if (log_is_near_one(ix)) {
+        if (ix == kOneBits) return 0.0;
         return log_near_one(x);
     }
     const uint32_t top = static_cast<uint32_t>(ix >> 48);
@@ -122,14 +129,30 @@ WLP_HD double glibc_log(double x) {
         if ((top & 0x8000u) || (top & 0x7ff0u) == 0x7ff0u) return wlp_as_f64(0x7ff8000000000000ull);
         ix = wlp_as_u64(WLP_MUL(x, 0x1p52)) - (52ull << 52);
     }
-    return log_table(ix);
+    return log_table(ix, tab);
 }
 
-// -log(1 - u) for u = n * 2^-32, n a taus88 output (u in [0, 1), 1 - u exact and
-// normal): the exponential variate numerator of mm1 (models.hpp:67,75).
-WLP_HD double neg_log1m_u32(uint32_t n) {
-    const double u = static_cast<double>(n) * 0x1p-32;
-    return -glibc_log(WLP_SUB(1.0, u));
+#if !defined(__CUDA_ARCH__)
+static inline double glibc_log(double x) { return glibc_log_tab(x, kLogTabHost); }
+#endif
+
+// Bits of x = 1 - n*2^-32 (the reference's `1.0 - next()`, exact) built with integer
+// ops: m = 2^32 - n, x = m*2^-32 = 2^(-1-lz) * 1.f with lz = clz(m). n = 0 gives 1.0.
+WLP_HD uint64_t one_minus_u32_bits(uint32_t n) {
+    const uint32_t m = 0u - n;
+    if (m == 0u) return kOneBits;
+    const int lz = wlp_clz32(m);
+    const uint32_t frac = (m << lz) << 1;  // mantissa bits below the leading one
+    const uint32_t hi = (static_cast<uint32_t>(1022 - lz) << 20) | (frac >> 12);
+    return (static_cast<uint64_t>(hi) << 32) | static_cast<uint64_t>(frac << 20);
+}
+
+// -log(1 - n*2^-32) for a taus88 output n: the exponential numerator of mm1
+// (models.hpp:67,75). Scalar form (host reference of the batched device routine).
+WLP_HD double neg_log1m_u32_tab(uint32_t n, const double* tab) {
+    const uint64_t ix = one_minus_u32_bits(n);
+    if (log_is_near_one(ix)) return ix == kOneBits ? -0.0 : -log_near_one(wlp_as_f64(ix));
+    return -log_table(ix, tab);
 }
 
 }  // namespace wlp

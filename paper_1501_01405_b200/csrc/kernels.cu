@@ -1,5 +1,6 @@
 // sm_100a kernels of the WLP replication engine. No tensor cores: every kernel here is
-// integer / FP64 ALU work bounded by instruction issue.
+// integer / FP64 ALU work bounded by instruction issue and the ALU / FP64 pipes (see
+// DESIGN.md §roofline).
 //
 //   k_seed       random_spacing (rng.cpp:67-87) by jump-ahead: thread t fills 32 stream
 //                slots from master draw 3*c(t) on, flags "special" candidates.
@@ -11,7 +12,7 @@
 //                32*T-client panel into shared memory, lane 0 runs the order-preserving
 //                Lindley recursion (models.hpp:61-84) on them.
 //   k_tlp        the thread-per-replication comparison mapping (plan_launch TLP
-//                geometry, wlp.cpp:88-92).
+//                geometry, wlp.cpp:88-92); mm1 shares the batched exponential routine.
 //   k_stats      sums / centred sums of squares for the confidence interval.
 //
 // Compiled with --fmad=false: the reference is built with -ffp-contract=off
@@ -80,6 +81,17 @@ __device__ __forceinline__ Taus load_seed(const RepArgs& a, int64_t r) {
     return Taus{__ldg(a.seeds + r), __ldg(a.seeds + a.count + r), __ldg(a.seeds + 2 * a.count + r)};
 }
 
+template <int WORDS>
+__device__ __forceinline__ void stage_u32(uint32_t* dst, const uint32_t* __restrict__ src) {
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    for (int i = threadIdx.x; i < WORDS / 4; i += blockDim.x) d[i] = __ldg(s + i);
+}
+
+__device__ __forceinline__ void stage_log_table(double* dst) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) dst[i] = kLogTabDev[i];
+}
+
 // Inside test of one pi point, x*x + y*y <= 1.0 in unfused fp64 (models.hpp:54-56),
 // evaluated on the unscaled draws: with x = a*2^-32 every product and sum is the
 // reference's value times 2^64 exactly (power-of-two scaling commutes with rounding
@@ -127,13 +139,6 @@ __device__ __forceinline__ int walk_dx(Taus& st, uint32_t units) {
     return dx;
 }
 
-// -log(1-u)/rate (models.hpp:67,75); exact reciprocal product when rate = 2^k.
-template <bool INV>
-__device__ __forceinline__ double expo(uint32_t n, double rate, double inv) {
-    const double e = neg_log1m_u32(n);
-    return INV ? __dmul_rn(e, inv) : __ddiv_rn(e, rate);
-}
-
 __device__ __forceinline__ int64_t warp_sum_i64(int64_t v) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
@@ -145,6 +150,80 @@ __device__ __forceinline__ int64_t warp_sum_i64(int64_t v) {
 __device__ __forceinline__ double walk_fold(int64_t px, int64_t c) {
     return static_cast<double>(((px % c) + c) % c);
 }
+
+// ---------------------------------------------------------------------------------
+// mm1 exponentials: -log(1 - u)/rate for a batch of draws per lane, warp-cooperative.
+//
+// glibc's log has two algorithms: the table path and, for 1 - 2^-4 <= x < 1 + ..., a
+// longer polynomial (1 in 16 model draws). Per lane the branch is data dependent, so a
+// warp that evaluates draws lane by lane runs both paths almost always (1-(15/16)^32 =
+// 87%). Instead every input goes through the table path (branch-free), and the
+// near-one inputs of the whole warp are compacted (ballot/popc) and evaluated once, spread
+// over the lanes; their results replace the table-path values.
+// ---------------------------------------------------------------------------------
+
+constexpr int kExpoB = 8;  // log inputs per lane per batch
+
+struct NearList {  // per-warp compaction scratch
+    uint32_t n[32 * kExpoB];
+    uint16_t dst[32 * kExpoB];
+};
+
+// -log(1 - n*2^-32) for every lane's B inputs. Near-one results are written by the lane
+// that evaluates them into out[dst] when `direct` (the WLP panel buffer), else returned
+// through res[] and picked up by the owner.
+template <int B>
+__device__ __forceinline__ void neg_log1m_batch(const uint32_t (&n)[B], double (&e)[B], const double* tab,
+                                                NearList& nl, double* res, unsigned mask, int lane) {
+    int pos[B];
+    int total = 0;
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+        const uint64_t ix = one_minus_u32_bits(n[j]);
+        const bool near = log_is_near_one(ix);
+        e[j] = -log_table(ix, tab);
+        const unsigned b = __ballot_sync(mask, near);
+        pos[j] = near ? total + __popc(b & lt) : -1;
+        if (near) nl.n[pos[j]] = n[j];
+        total += __popc(b);
+    }
+    if (total == 0) return;  // warp-uniform
+    __syncwarp(mask);
+    const int width = __popc(mask);
+    for (int p = lane; p < total; p += width) {
+        const uint64_t ix = one_minus_u32_bits(nl.n[p]);
+        res[p] = ix == kOneBits ? -0.0 : -log_near_one(wlp_as_f64(ix));
+    }
+    __syncwarp(mask);
+#pragma unroll
+    for (int j = 0; j < B; ++j)
+        if (pos[j] >= 0) e[j] = res[pos[j]];
+    __syncwarp(mask);
+}
+
+template <bool INV>
+__device__ __forceinline__ double scale(double e, double rate, double inv) {
+    return INV ? __dmul_rn(e, inv) : __ddiv_rn(e, rate);
+}
+
+// One step of the Lindley recursion with the reference's operation order
+// (models.hpp:67-77): t = (w + s) - a; idle/w update; s = next service; sums.
+struct Queue {
+    double w = 0.0, s = 0.0, idle = 0.0, sumw = 0.0, sums = 0.0;
+    __device__ __forceinline__ void client(double a, double s_next) {
+        const double t = __dsub_rn(__dadd_rn(w, s), a);
+        if (t < 0.0) {  // the server ran dry before this arrival
+            idle = __dsub_rn(idle, t);
+            w = 0.0;
+        } else {
+            w = t;
+        }
+        s = s_next;
+        sumw = __dadd_rn(sumw, w);
+        sums = __dadd_rn(sums, __dadd_rn(w, s));
+    }
+};
 
 // ---------------------------------------------------------------------------------
 // Seeding
@@ -207,12 +286,6 @@ __global__ void __launch_bounds__(kSeedBlock) k_seed(SeedArgs a) {
     }
 }
 
-// -log(1 - k*2^-32) for a batch of k (pins the device glibc-log port directly).
-__global__ void k_neg_log1m(const uint32_t* __restrict__ k, int64_t n, double* __restrict__ out) {
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = neg_log1m_u32(k[i]);
-}
-
 constexpr int kTausPerThread = 64;
 
 __global__ void k_taus(const uint32_t* __restrict__ pw, Taus seed, int64_t n, uint32_t* out) {
@@ -224,6 +297,27 @@ __global__ void k_taus(const uint32_t* __restrict__ pw, Taus seed, int64_t n, ui
     for (int64_t i = i0; i < i1; ++i) out[i] = taus_next(s);
 }
 
+// -log(1 - k*2^-32) through the production batch routine (pins the device log port).
+constexpr int kLogHookBlock = 256;
+__global__ void __launch_bounds__(kLogHookBlock) k_neg_log1m(const uint32_t* __restrict__ k, int64_t n,
+                                                             double* __restrict__ out) {
+    __shared__ double tab[256];
+    __shared__ NearList nl[kLogHookBlock / 32];
+    __shared__ double res[kLogHookBlock / 32][32 * kExpoB];
+    stage_log_table(tab);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t base = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kExpoB;
+    uint32_t in[kExpoB];
+    double e[kExpoB];
+#pragma unroll
+    for (int j = 0; j < kExpoB; ++j) in[j] = base + j < n ? k[base + j] : 0u;
+    neg_log1m_batch<kExpoB>(in, e, tab, nl[w], res[w], kFull, lane);
+#pragma unroll
+    for (int j = 0; j < kExpoB; ++j)
+        if (base + j < n) out[base + j] = e[j];
+}
+
 // ---------------------------------------------------------------------------------
 // WLP: one replication per warp
 // ---------------------------------------------------------------------------------
@@ -232,14 +326,10 @@ __global__ void k_taus(const uint32_t* __restrict__ pw, Taus seed, int64_t n, ui
 // costs the same, so a static split is balanced). Results are parked in lane
 // (r - lo) % 32 and stored 32 at a time (coalesced 256 B).
 template <int MODEL>
-__global__ void __launch_bounds__(kWlpBlock) k_wlp_lanes(RepArgs a, const uint32_t* __restrict__ gtab,
-                                                          int64_t K) {
+__global__ void __launch_bounds__(kWlpBlock, 3) k_wlp_lanes(RepArgs a, const uint32_t* __restrict__ gtab,
+                                                             int64_t K) {
     extern __shared__ uint32_t tab[];  // kLaneTabWords
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(gtab);
-        uint4* dst = reinterpret_cast<uint4*>(tab);
-        for (int i = threadIdx.x; i < kLaneTabWords / 4; i += blockDim.x) dst[i] = __ldg(src + i);
-    }
+    stage_u32<kLaneTabWords>(tab, gtab);
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -271,6 +361,17 @@ __global__ void __launch_bounds__(kWlpBlock) k_wlp_lanes(RepArgs a, const uint32
     }
 }
 
+// mm1 WLP shared memory: lane-start tables, panel-skip table, log table, then per warp
+// the panel buffer (a and s of 32*T clients) and the near-one compaction list.
+constexpr int kMm1P = 32 * kMm1PanelT;
+struct Mm1Warp {
+    double a[kMm1P];
+    double s[kMm1P];
+    NearList nl;
+};
+constexpr size_t kMm1Smem =
+    (kLaneTabWords + kUniTabWords) * 4 + 256 * 8 + (kMm1Block / 32) * sizeof(Mm1Warp);
+
 // mm1: lanes generate, lane 0 recurses. Panel p covers clients [p*32T, (p+1)*32T); lane l
 // produces clients p*32T + l*T + j (j < T) from draws 2*(that index) and 2*(...)+1, so
 // each lane steps its own contiguous draw range and hops 62T draws between panels.
@@ -278,33 +379,46 @@ template <bool INV>
 __global__ void __launch_bounds__(kMm1Block) k_wlp_mm1(RepArgs a, const uint32_t* __restrict__ gtab,
                                                         const uint32_t* __restrict__ gskip) {
     constexpr int T = kMm1PanelT;
-    constexpr int P = 32 * T;
-    extern __shared__ uint32_t sm[];
-    uint32_t* tab = sm;
-    uint32_t* skip = sm + kLaneTabWords;
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(gtab);
-        uint4* dst = reinterpret_cast<uint4*>(tab);
-        for (int i = threadIdx.x; i < kLaneTabWords / 4; i += blockDim.x) dst[i] = __ldg(src + i);
-        for (int i = threadIdx.x; i < kUniTabWords; i += blockDim.x) skip[i] = __ldg(gskip + i);
-    }
+    constexpr int P = kMm1P;
+    static_assert(2 * T % kExpoB == 0, "panel draws per lane must be whole batches");
+    extern __shared__ __align__(16) unsigned char smraw[];
+    uint32_t* tab = reinterpret_cast<uint32_t*>(smraw);
+    uint32_t* skip = tab + kLaneTabWords;
+    double* logtab = reinterpret_cast<double*>(skip + kUniTabWords);
+    Mm1Warp& W = reinterpret_cast<Mm1Warp*>(logtab + 256)[threadIdx.x >> 5];
+    stage_u32<kLaneTabWords>(tab, gtab);
+    for (int i = threadIdx.x; i < kUniTabWords; i += blockDim.x) skip[i] = __ldg(gskip + i);
+    stage_log_table(logtab);
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    double* buf = reinterpret_cast<double*>(sm + kLaneTabWords + kUniTabWords) + (threadIdx.x >> 5) * (2 * P);
     const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     const int64_t lo = warp * a.count / nwarps, hi = (warp + 1) * a.count / nwarps;
     double k0 = 0.0, k1 = 0.0, k2 = 0.0;
     for (int64_t r = lo; r < hi; ++r) {
         Taus st = lane_jump(tab, lane, load_seed(a, r));
-        double w = 0.0, s = 0.0, idle = 0.0, sumw = 0.0, sums = 0.0;
+        Queue q;
         for (int64_t base = 0; base < a.n; base += P) {
+            // draws of my T clients: a_c = draw 2c, s_c = draw 2c+1, in batches of kExpoB;
+            // the panel buffer doubles as the batches' near-one scratch until it is written
+            double ea[T], es[T];
 #pragma unroll
-            for (int j = 0; j < T; ++j) {
-                const uint32_t ua = taus_next(st);
-                const uint32_t us = taus_next(st);
-                buf[j * 32 + lane] = expo<INV>(ua, a.lambda, a.inv_lambda);
-                buf[P + j * 32 + lane] = expo<INV>(us, a.mu, a.inv_mu);
+            for (int h = 0; h < 2 * T; h += kExpoB) {
+                uint32_t n[kExpoB];
+                double e[kExpoB];
+#pragma unroll
+                for (int j = 0; j < kExpoB; ++j) n[j] = taus_next(st);
+                neg_log1m_batch<kExpoB>(n, e, logtab, W.nl, W.a, kFull, lane);
+#pragma unroll
+                for (int j = 0; j < kExpoB; j += 2) {
+                    ea[(h + j) / 2] = scale<INV>(e[j], a.lambda, a.inv_lambda);
+                    es[(h + j) / 2] = scale<INV>(e[j + 1], a.mu, a.inv_mu);
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < T; ++c) {
+                W.a[c * 32 + lane] = ea[c];
+                W.s[c * 32 + lane] = es[c];
             }
             __syncwarp();
             if (lane == 0) {
@@ -312,26 +426,16 @@ __global__ void __launch_bounds__(kMm1Block) k_wlp_mm1(RepArgs a, const uint32_t
                 const int cnt = left < P ? static_cast<int>(left) : P;
                 for (int c = 0; c < cnt; ++c) {
                     const int idx = (c % T) * 32 + c / T;
-                    const double av = buf[idx];
-                    const double t = __dsub_rn(__dadd_rn(w, s), av);
-                    if (t < 0.0) {  // server idle before this arrival
-                        idle = __dsub_rn(idle, t);
-                        w = 0.0;
-                    } else {
-                        w = t;
-                    }
-                    s = buf[P + idx];
-                    sumw = __dadd_rn(sumw, w);
-                    sums = __dadd_rn(sums, __dadd_rn(w, s));
+                    q.client(W.a[idx], W.s[idx]);
                 }
             }
             __syncwarp();
             st = uni_jump(skip, st);
         }
         const double nd = static_cast<double>(a.n);
-        const double v0 = __shfl_sync(kFull, __ddiv_rn(idle, nd), 0);
-        const double v1 = __shfl_sync(kFull, __ddiv_rn(sumw, nd), 0);
-        const double v2 = __shfl_sync(kFull, __ddiv_rn(sums, nd), 0);
+        const double v0 = __shfl_sync(kFull, __ddiv_rn(q.idle, nd), 0);
+        const double v1 = __shfl_sync(kFull, __ddiv_rn(q.sumw, nd), 0);
+        const double v2 = __shfl_sync(kFull, __ddiv_rn(q.sums, nd), 0);
         const int slot = static_cast<int>((r - lo) & 31);
         if (lane == slot) {
             k0 = v0;
@@ -352,7 +456,7 @@ __global__ void __launch_bounds__(kMm1Block) k_wlp_mm1(RepArgs a, const uint32_t
 // TLP: one replication per thread (the comparison mapping)
 // ---------------------------------------------------------------------------------
 
-template <int MODEL, bool INV>
+template <int MODEL>
 __global__ void k_tlp(RepArgs a) {
     const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (r >= a.count) return;  // tail threads of the last block stay inert (wlp.cpp:125-138)
@@ -367,25 +471,6 @@ __global__ void k_tlp(RepArgs a) {
             done += part;
         }
         a.out0[r] = __ddiv_rn(__dmul_rn(4.0, static_cast<double>(c)), static_cast<double>(a.n));
-    } else if (MODEL == 1) {
-        double w = 0.0, s = 0.0, idle = 0.0, sumw = 0.0, sums = 0.0;
-        for (int64_t i = 0; i < a.n; ++i) {
-            const double av = expo<INV>(taus_next(st), a.lambda, a.inv_lambda);
-            const double t = __dsub_rn(__dadd_rn(w, s), av);
-            if (t < 0.0) {
-                idle = __dsub_rn(idle, t);
-                w = 0.0;
-            } else {
-                w = t;
-            }
-            s = expo<INV>(taus_next(st), a.mu, a.inv_mu);
-            sumw = __dadd_rn(sumw, w);
-            sums = __dadd_rn(sums, __dadd_rn(w, s));
-        }
-        const double nd = static_cast<double>(a.n);
-        a.out0[r] = __ddiv_rn(idle, nd);
-        a.out1[r] = __ddiv_rn(sumw, nd);
-        a.out2[r] = __ddiv_rn(sums, nd);
     } else {
         // models.hpp:92-105 as written: a 4-way branch per step on d = floor(4u).
         double px = 0.0, py = 0.0;
@@ -403,6 +488,48 @@ __global__ void k_tlp(RepArgs a) {
         }
         a.out0[r] = walk_fold(static_cast<int64_t>(px), a.chunks);
     }
+}
+
+// mm1 thread per replication: each lane runs its own queue; the exponentials of 4
+// clients (8 draws) per lane go through the warp-cooperative batch log.
+struct TlpMm1Warp {
+    NearList nl;
+    double res[32 * kExpoB];
+};
+
+template <bool INV>
+__global__ void k_tlp_mm1(RepArgs a) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double* logtab = reinterpret_cast<double*>(smraw);
+    TlpMm1Warp& W = reinterpret_cast<TlpMm1Warp*>(logtab + 256)[threadIdx.x >> 5];
+    stage_log_table(logtab);
+    __syncthreads();
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    // every thread of a warp takes part in the batch (tail threads on a dummy stream);
+    // blocks that are not a multiple of 32 have a partial last warp
+    const int lane = threadIdx.x & 31;
+    const int in_warp = static_cast<int>(blockDim.x) - (static_cast<int>(threadIdx.x) & ~31);
+    const unsigned mask = in_warp >= 32 ? kFull : ((1u << in_warp) - 1u);
+    const bool live = r < a.count;
+    Taus st = live ? load_seed(a, r) : Taus{2u, 8u, 16u};
+    Queue q;
+    for (int64_t done = 0; done < a.n; done += kExpoB / 2) {
+        uint32_t n[kExpoB];
+        double e[kExpoB];
+#pragma unroll
+        for (int j = 0; j < kExpoB; ++j) n[j] = taus_next(st);
+        neg_log1m_batch<kExpoB>(n, e, logtab, W.nl, W.res, mask, lane);
+        const int64_t left = a.n - done;
+        const int cnt = left < kExpoB / 2 ? static_cast<int>(left) : kExpoB / 2;
+#pragma unroll
+        for (int c = 0; c < kExpoB / 2; ++c)
+            if (c < cnt) q.client(scale<INV>(e[2 * c], a.lambda, a.inv_lambda), scale<INV>(e[2 * c + 1], a.mu, a.inv_mu));
+    }
+    if (!live) return;
+    const double nd = static_cast<double>(a.n);
+    a.out0[r] = __ddiv_rn(q.idle, nd);
+    a.out1[r] = __ddiv_rn(q.sumw, nd);
+    a.out2[r] = __ddiv_rn(q.sums, nd);
 }
 
 // ---------------------------------------------------------------------------------
@@ -465,6 +592,13 @@ __global__ void __launch_bounds__(kStatsBlock) k_stats(const double* __restrict_
     }
 }
 
+size_t tlp_mm1_smem(int block) { return 256 * 8 + static_cast<size_t>((block + 31) / 32) * sizeof(TlpMm1Warp); }
+
+template <class K>
+void allow_smem(K kernel, size_t bytes) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------------
@@ -474,17 +608,16 @@ __global__ void __launch_bounds__(kStatsBlock) k_stats(const double* __restrict_
 int wlp_blocks_per_sm(int model) {
     int nb = 0;
     if (model == 1) {
-        const size_t smem = (kLaneTabWords + kUniTabWords) * 4 + (kMm1Block / 32) * 2 * 32 * kMm1PanelT * 8;
-        cudaFuncSetAttribute(k_wlp_mm1<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        cudaFuncSetAttribute(k_wlp_mm1<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_mm1<false>, kMm1Block, smem);
+        allow_smem(k_wlp_mm1<false>, kMm1Smem);
+        allow_smem(k_wlp_mm1<true>, kMm1Smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_mm1<false>, kMm1Block, kMm1Smem);
     } else {
         const size_t smem = kLaneTabWords * 4;
         if (model == 0) {
-            cudaFuncSetAttribute(k_wlp_lanes<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            allow_smem(k_wlp_lanes<0>, smem);
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_lanes<0>, kWlpBlock, smem);
         } else {
-            cudaFuncSetAttribute(k_wlp_lanes<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            allow_smem(k_wlp_lanes<2>, smem);
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_lanes<2>, kWlpBlock, smem);
         }
     }
@@ -494,9 +627,14 @@ int wlp_blocks_per_sm(int model) {
 int tlp_blocks_per_sm(int model, int block) {
     int nb = 0;
     switch (model) {
-        case 0: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tlp<0, false>, block, 0); break;
-        case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tlp<1, false>, block, 0); break;
-        default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tlp<2, false>, block, 0); break;
+        case 0: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tlp<0>, block, 0); break;
+        case 1: {
+            const size_t smem = tlp_mm1_smem(block);
+            allow_smem(k_tlp_mm1<false>, smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tlp_mm1<false>, block, smem);
+            break;
+        }
+        default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tlp<2>, block, 0); break;
     }
     return nb < 1 ? 1 : nb;
 }
@@ -508,7 +646,7 @@ cudaError_t launch_seed(const SeedArgs& a, cudaStream_t st) {
     const size_t smem = 3 * kSeedBlock * (kSeedPerThread + 1) * 4;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_seed, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        allow_smem(k_seed, smem);
         attr = true;
     }
     k_seed<<<static_cast<unsigned>(grid), kSeedBlock, smem, st>>>(a);
@@ -517,7 +655,8 @@ cudaError_t launch_seed(const SeedArgs& a, cudaStream_t st) {
 
 cudaError_t launch_neg_log1m(const uint32_t* k, int64_t n, double* out, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
-    k_neg_log1m<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(k, n, out);
+    const int64_t per_block = static_cast<int64_t>(kLogHookBlock) * kExpoB;
+    k_neg_log1m<<<static_cast<unsigned>((n + per_block - 1) / per_block), kLogHookBlock, 0, st>>>(k, n, out);
     return cudaGetLastError();
 }
 
@@ -533,11 +672,10 @@ cudaError_t launch_wlp(int model, const RepArgs& a, const uint32_t* lane_tab, co
                        int64_t lane_units, int grid, cudaStream_t st) {
     if (a.count <= 0) return cudaSuccess;
     if (model == 1) {
-        const size_t smem = (kLaneTabWords + kUniTabWords) * 4 + (kMm1Block / 32) * 2 * 32 * kMm1PanelT * 8;
         if (a.inv_lambda != 0.0 && a.inv_mu != 0.0)
-            k_wlp_mm1<true><<<grid, kMm1Block, smem, st>>>(a, lane_tab, uni_tab);
+            k_wlp_mm1<true><<<grid, kMm1Block, kMm1Smem, st>>>(a, lane_tab, uni_tab);
         else
-            k_wlp_mm1<false><<<grid, kMm1Block, smem, st>>>(a, lane_tab, uni_tab);
+            k_wlp_mm1<false><<<grid, kMm1Block, kMm1Smem, st>>>(a, lane_tab, uni_tab);
     } else if (model == 0) {
         k_wlp_lanes<0><<<grid, kWlpBlock, kLaneTabWords * 4, st>>>(a, lane_tab, lane_units);
     } else {
@@ -553,14 +691,19 @@ cudaError_t launch_tlp(int model, const RepArgs& a, int tlp_block, cudaStream_t 
     const bool inv = a.inv_lambda != 0.0 && a.inv_mu != 0.0;
     const dim3 g(static_cast<unsigned>(grid)), b(static_cast<unsigned>(block));
     switch (model) {
-        case 0: k_tlp<0, false><<<g, b, 0, st>>>(a); break;
-        case 1:
-            if (inv)
-                k_tlp<1, true><<<g, b, 0, st>>>(a);
-            else
-                k_tlp<1, false><<<g, b, 0, st>>>(a);
+        case 0: k_tlp<0><<<g, b, 0, st>>>(a); break;
+        case 1: {
+            const size_t smem = tlp_mm1_smem(static_cast<int>(block));
+            if (inv) {
+                allow_smem(k_tlp_mm1<true>, smem);
+                k_tlp_mm1<true><<<g, b, smem, st>>>(a);
+            } else {
+                allow_smem(k_tlp_mm1<false>, smem);
+                k_tlp_mm1<false><<<g, b, smem, st>>>(a);
+            }
             break;
-        default: k_tlp<2, false><<<g, b, 0, st>>>(a); break;
+        }
+        default: k_tlp<2><<<g, b, 0, st>>>(a); break;
     }
     return cudaGetLastError();
 }

@@ -34,8 +34,8 @@ struct SeedArgs {
     unsigned long long* n_special;
 };
 
-constexpr int kWlpBlock = 256;     // pi / walk WLP block (8 warps)
-constexpr int kMm1Block = 512;     // mm1 WLP block (16 warps)
+constexpr int kWlpBlock = 512;     // pi / walk WLP block (16 warps; 3 blocks = 48 warps per SM)
+constexpr int kMm1Block = 256;     // mm1 WLP block (8 warps)
 constexpr int kMm1PanelT = 8;      // mm1: clients per lane per panel
 constexpr int kSeedBlock = 128;
 constexpr int kSeedPerThread = 32;

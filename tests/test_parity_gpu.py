@@ -189,10 +189,10 @@ def test_sweep_golden_means(gpu):
         run = gpu.run_model(gpu.ModelKind.Pi, P(gpu, replications=int(R), draws=100), gpu.mode_from_name(mode),
                             master_seed=42)
         if int(R) == 1:
-            assert repr(run.primary[0]) == mean
+            assert repr(float(run.primary[0])) == mean
         else:
             ci = gpu.confidence_interval(run.primary)
-            assert (repr(ci.mean), repr(ci.low()), repr(ci.high())) == (mean, lo, hi)
+            assert (repr(float(ci.mean)), repr(float(ci.low())), repr(float(ci.high()))) == (mean, lo, hi)
 
 
 # ---- shards, errors, warnings ---------------------------------------------------------------

@@ -39,8 +39,11 @@ int main(int argc, char** argv) {
                 const double u = static_cast<double>(static_cast<std::uint32_t>(k)) * 0x1p-32;
                 const double x = 1.0 - u;
                 const double a = wlp::glibc_log(x), b = std::log(x);
+                // the integer construction of 1-u and the split near-one/table paths the
+                // device kernels use
+                const double c = wlp::neg_log1m_u32_tab(static_cast<std::uint32_t>(k), wlp::kLogTabHost);
                 if (x >= 1.0 - 0x1p-4) ++near[t];
-                if (bits(a) != bits(b)) {
+                if (bits(a) != bits(b) || bits(c) != bits(-b) || wlp::one_minus_u32_bits(static_cast<std::uint32_t>(k)) != bits(x)) {
                     if (!bad[t]) first_bad[t] = k;
                     ++bad[t];
                 }

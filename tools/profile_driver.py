@@ -1,0 +1,31 @@
+#!/usr/bin/env python3
+"""Launch one configuration of the replication kernels for ncu (run on the GPU box).
+
+    python tools/profile_driver.py MODEL MODE R N [--repeat K]
+    ncu --set full --clock-control none --import-source on -k regex:k_wlp -s 1 -c 1 \
+        -o gpurun_out/prof_pi_wlp python tools/profile_driver.py pi wlp 1000000 10000 --repeat 2
+"""
+import argparse
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import torch  # noqa: E402
+
+import paper_1501_01405_b200 as w  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("model", choices=["pi", "mm1", "walk"])
+ap.add_argument("mode", choices=["sequential", "tlp", "wlp"])
+ap.add_argument("R", type=int)
+ap.add_argument("N", type=int)
+ap.add_argument("--repeat", type=int, default=2)
+a = ap.parse_args()
+m = w.model_from_name(a.model)
+p = w.ModelParams(replications=a.R, draws=a.N, clients=a.N, steps=a.N)
+outs = [torch.empty(a.R, dtype=torch.float64, device="cuda") for _ in w.OUTPUT_NAMES[m]]
+for _ in range(a.repeat):
+    w.run_shard(m, p, w.mode_from_name(a.mode), 42, 0, a.R, outs, on_device=True)
+torch.cuda.synchronize()
+print(a.model, a.mode, a.R, a.N, "mean", float(outs[0].mean()))
