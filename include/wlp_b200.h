@@ -167,6 +167,12 @@ int wlp_seed_streams(uint64_t master_seed, int64_t slot_begin, int64_t count,
 int wlp_seed_streams_exact(uint64_t master_seed, int64_t count, uint32_t* s_out,
                            int out_on_device, void* stream);
 
+/* random_spacing(master, count) (rng.cpp:67-87) from an explicit master state (not
+ * re-mapped); master_out (may be NULL) receives the master after all consumed draws,
+ * as the reference's by-reference master. Synchronous. */
+int wlp_seed_streams_state(const uint32_t master[3], int64_t count, uint32_t* s_out,
+                           int out_on_device, void* stream, uint32_t master_out[3]);
+
 /* Replications over caller-given streams (SoA s[3*count], host or device):
  * pi_replication / mm1_replication / walk_replication (models.cpp:46-59) for each,
  * mapped per `mode` (TLP: thread per replication; WLP and SEQUENTIAL: warp per

@@ -247,6 +247,7 @@ _SIGS = {
     "wlp_taus_stream": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, _I64, _P, C.c_int, _P]),
     "wlp_seed_streams": (C.c_int, [C.c_uint64, _I64, _I64, _P, _I64, _P, C.c_int, _P, _P, _I64, C.POINTER(_I64)]),
     "wlp_seed_streams_exact": (C.c_int, [C.c_uint64, _I64, _P, C.c_int, _P]),
+    "wlp_seed_streams_state": (C.c_int, [_P, _I64, _P, C.c_int, _P, _P]),
     "wlp_run_streams": (C.c_int, [C.c_int, C.POINTER(_Params), C.c_int, _P, _I64, C.c_int, _P, _P, _P, C.c_int, _P,
                                   C.POINTER(_Report)]),
     "wlp_run_shard": (C.c_int, [C.c_int, C.POINTER(_Params), C.c_int, C.c_uint64, C.c_int, _I64, _I64, _P, _I64,
@@ -423,6 +424,16 @@ def random_spacing_seed(master_seed: int, count: int) -> np.ndarray:
     out = np.empty((3, count), dtype=np.uint32)
     _check(_lib.wlp_seed_streams_exact(master_seed & (2**64 - 1), count, _ptr(out), 0, None))
     return out
+
+
+def random_spacing(master: RngState, count: int):
+    """random_spacing(master, count) (rng.cpp:67-87) on the GPU from a master state.
+    Returns (streams as a (3, count) uint32 array, the master after the consumed draws)."""
+    out = np.empty((3, count), dtype=np.uint32)
+    m = (C.c_uint32 * 3)(master.s1, master.s2, master.s3)
+    after = (C.c_uint32 * 3)()
+    _check(_lib.wlp_seed_streams_state(m, count, _ptr(out) if count else None, 0, None, after))
+    return out, RngState(*after)
 
 
 def seed_streams(master_seed: int, slot_begin: int, count: int, rejected: Sequence[int] = (),

@@ -24,6 +24,7 @@ CSRC = PKG / "csrc"
 HOST = PKG / "host"
 LIB = PKG / "libwlp_b200.so"
 CXXLIB = PKG / "libwarpsim_b200.so"
+CLI = PKG / "warpsim"
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -53,19 +54,26 @@ def build_cuda(force: bool = False) -> Path:
 
 
 def build_cxx(force: bool = False) -> Path:
-    srcs = sorted(HOST.glob("*.cpp"))
-    if not srcs:
-        return CXXLIB
+    srcs = [HOST / "warpsim_api.cpp"]
     deps = srcs + [ROOT / "include" / "warpsim_b200.hpp", ROOT / "include" / "wlp_b200.h", LIB]
     if force or _stale(CXXLIB, deps):
         _run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-fPIC", "-shared", f"-I{ROOT / 'include'}",
-              *map(str, srcs), "-o", str(CXXLIB), f"-L{PKG}", "-lwlp_b200", f"-Wl,-rpath,$ORIGIN"])
+              *map(str, srcs), "-o", str(CXXLIB), f"-L{PKG}", "-lwlp_b200", "-Wl,-rpath,$ORIGIN"])
     return CXXLIB
+
+
+def build_cli(force: bool = False) -> Path:
+    src = HOST / "cli.cpp"
+    if force or _stale(CLI, [src, ROOT / "include" / "warpsim_b200.hpp", CXXLIB]):
+        _run(["g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", str(src), "-o", str(CLI), f"-L{PKG}",
+              "-lwarpsim_b200", "-lwlp_b200", "-Wl,-rpath,$ORIGIN"])
+    return CLI
 
 
 def build_all(force: bool = False) -> None:
     build_cuda(force)
     build_cxx(force)
+    build_cli(force)
 
 
 if __name__ == "__main__":

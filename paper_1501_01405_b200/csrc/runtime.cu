@@ -614,7 +614,12 @@ int wlp_seed_streams(uint64_t master_seed, int64_t slot_begin, int64_t count, co
     return WLP_OK;
 }
 
-int wlp_seed_streams_exact(uint64_t master_seed, int64_t count, uint32_t* s_out, int out_on_device, void* stream) {
+}  // extern "C"
+
+namespace wlp {
+namespace {
+// Whole-run exact random_spacing from a master state; *n_rejected = redraws used.
+int seed_exact(Taus master, int64_t count, uint32_t* s_out, int out_on_device, void* stream, int64_t* n_rejected) {
     if (count < 0) return fail(WLP_EDOMAIN, "seed_streams: negative count");
     DevCtx* c;
     std::unique_lock<std::mutex> lk;
@@ -625,7 +630,6 @@ int wlp_seed_streams_exact(uint64_t master_seed, int64_t count, uint32_t* s_out,
         WLP_CUDA(c->seeds.ensure(3 * std::max<int64_t>(count, 1)));
         d = c->seeds.p;
     }
-    const Taus master = master_from_seed(master_seed);
     std::vector<int64_t> rej;
     for (;;) {
         WLP_TRY(seed_async(*c, master, 0, count, rej, d, st));
@@ -638,7 +642,30 @@ int wlp_seed_streams_exact(uint64_t master_seed, int64_t count, uint32_t* s_out,
         if (next == rej) break;
         rej.swap(next);
     }
-    if (!out_on_device) WLP_CUDA(cudaMemcpy(s_out, d, 3 * count * 4, cudaMemcpyDeviceToHost));
+    if (!out_on_device && count) WLP_CUDA(cudaMemcpy(s_out, d, 3 * count * 4, cudaMemcpyDeviceToHost));
+    if (n_rejected) *n_rejected = static_cast<int64_t>(rej.size());
+    return WLP_OK;
+}
+}  // namespace
+}  // namespace wlp
+
+extern "C" {
+
+int wlp_seed_streams_exact(uint64_t master_seed, int64_t count, uint32_t* s_out, int out_on_device, void* stream) {
+    return seed_exact(master_from_seed(master_seed), count, s_out, out_on_device, stream, nullptr);
+}
+
+int wlp_seed_streams_state(const uint32_t master[3], int64_t count, uint32_t* s_out, int out_on_device,
+                           void* stream, uint32_t master_out[3]) {
+    const Taus m{master[0], master[1], master[2]};
+    int64_t nrej = 0;
+    WLP_TRY(seed_exact(m, count, s_out, out_on_device, stream, &nrej));
+    if (master_out) {
+        const Taus after = jump_state(m, 3ull * static_cast<uint64_t>(count + nrej));
+        master_out[0] = after.s1;
+        master_out[1] = after.s2;
+        master_out[2] = after.s3;
+    }
     return WLP_OK;
 }
 

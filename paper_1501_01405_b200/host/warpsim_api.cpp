@@ -1,0 +1,374 @@
+// C++ drop-in API (include/warpsim_b200.hpp) over the C ABI of libwlp_b200.so.
+// Every model computation is a C-ABI call into the sm_100a kernels; this file holds only
+// argument plumbing, the reference's error mapping and the sweep/CSV bookkeeping
+// (reference proj/src/sweep.cpp:57-186 semantics, re-implemented).
+#include <charconv>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+
+#include "warpsim_b200.hpp"
+#include "wlp_b200.h"
+
+namespace warpsim {
+namespace {
+
+[[noreturn]] void raise(int code) {
+    const std::string msg = wlp_last_error();
+    switch (code) {
+        case WLP_EDOMAIN: throw DomainError(msg);
+        case WLP_EPLAN: throw PlanError(msg);
+        case WLP_EFAULT: throw FaultError(msg);
+        default: throw Error(msg);
+    }
+}
+
+void check(int code) {
+    if (code != WLP_OK) raise(code);
+}
+
+wlp_params to_c(const ModelParams& p) {
+    return wlp_params{p.replications, p.draws, p.clients, p.lambda, p.mu, p.steps, p.chunks};
+}
+
+int model_id(ModelKind m) { return m == ModelKind::Pi ? WLP_MODEL_PI : m == ModelKind::Mm1 ? WLP_MODEL_MM1 : WLP_MODEL_WALK; }
+int mode_id(ExecutionMode m) {
+    return m == ExecutionMode::Sequential ? WLP_MODE_SEQUENTIAL : m == ExecutionMode::Tlp ? WLP_MODE_TLP : WLP_MODE_WLP;
+}
+
+SimReport from_c(const wlp_report& r) {
+    SimReport s;
+    s.totalCycles = r.total_cycles;
+    s.wavesExecuted = r.waves_executed;
+    s.peakResidentWarps = r.peak_resident_warps;
+    s.issues = r.issues;
+    s.aluIssues = r.alu_issues;
+    s.memReads = r.mem_reads;
+    s.memWrites = r.mem_writes;
+    s.divergenceEvents = r.divergence_events;
+    s.kernelMs = r.kernel_ms;
+    return s;
+}
+
+std::vector<std::uint32_t> soa(const RngState& s) { return {s.s1, s.s2, s.s3}; }
+
+constexpr const char* kHeader =
+    "replications,mode,model,total_cycles,mem_reads,mem_writes,divergence_events,waves,mean,ci_low,ci_high";
+
+std::string fmt_double(double v) {
+    char buf[64];
+    auto res = std::to_chars(buf, buf + sizeof buf, v);  // shortest round trip, as sweep.cpp:18-22
+    return std::string(buf, res.ptr);
+}
+
+template <class T>
+T parse_num(const std::string& f, std::size_t line, const char* what) {
+    T v{};
+    auto res = std::from_chars(f.data(), f.data() + f.size(), v);
+    if (res.ec != std::errc{} || res.ptr != f.data() + f.size())
+        throw ParseError("csv line " + std::to_string(line) + ": bad " + what + " '" + f + "'");
+    return v;
+}
+
+}  // namespace
+
+const char* mode_name(ExecutionMode mode) {
+    switch (mode) {
+        case ExecutionMode::Sequential: return "sequential";
+        case ExecutionMode::Tlp: return "tlp";
+        case ExecutionMode::Wlp: return "wlp";
+    }
+    return "?";
+}
+
+ExecutionMode mode_from_name(const std::string& name) {
+    if (name == "sequential") return ExecutionMode::Sequential;
+    if (name == "tlp") return ExecutionMode::Tlp;
+    if (name == "wlp") return ExecutionMode::Wlp;
+    throw DomainError("unknown execution mode '" + name + "' (sequential|tlp|wlp)");
+}
+
+const char* model_name(ModelKind model) {
+    switch (model) {
+        case ModelKind::Pi: return "pi";
+        case ModelKind::Mm1: return "mm1";
+        case ModelKind::Walk: return "walk";
+    }
+    return "?";
+}
+
+ModelKind model_from_name(const std::string& name) {
+    if (name == "pi") return ModelKind::Pi;
+    if (name == "mm1") return ModelKind::Mm1;
+    if (name == "walk") return ModelKind::Walk;
+    throw DomainError("unknown model '" + name + "' (pi|mm1|walk)");
+}
+
+RngState make_rng_state(std::uint32_t s1, std::uint32_t s2, std::uint32_t s3) {
+    std::uint32_t o[3];
+    check(wlp_make_state(s1, s2, s3, o));
+    return RngState{o[0], o[1], o[2]};
+}
+
+RngState rng_state_from_seed(std::uint64_t seed) {
+    std::uint32_t o[3];
+    check(wlp_master_from_seed(seed, o));
+    return RngState{o[0], o[1], o[2]};
+}
+
+std::vector<RngState> random_spacing(RngState& master, std::size_t count) {
+    std::vector<std::uint32_t> keys(3 * count);
+    const std::uint32_t m[3] = {master.s1, master.s2, master.s3};
+    std::uint32_t after[3];
+    check(wlp_seed_streams_state(m, static_cast<std::int64_t>(count), count ? keys.data() : nullptr, 0, nullptr,
+                                 after));
+    master = RngState{after[0], after[1], after[2]};
+    std::vector<RngState> out(count);
+    for (std::size_t i = 0; i < count; ++i) out[i] = RngState{keys[i], keys[count + i], keys[2 * count + i]};
+    return out;
+}
+
+std::vector<std::uint32_t> taus_stream(RngState& state, std::size_t n) {
+    std::vector<std::uint32_t> out(n);
+    // state is taken as-is (already a valid state); make_rng_state would only re-map
+    check(wlp_taus_stream(state.s1, state.s2, state.s3, static_cast<std::int64_t>(n), n ? out.data() : nullptr, 0,
+                          nullptr));
+    const std::uint32_t s[3] = {state.s1, state.s2, state.s3};
+    std::uint32_t o[3];
+    check(wlp_jump_host(s, n, o));
+    state = RngState{o[0], o[1], o[2]};
+    return out;
+}
+
+LaunchPlan plan_launch(std::int64_t replications, ExecutionMode mode, const DeviceProfile& prof, int tlp_block_size,
+                       std::int64_t grid_limit) {
+    if (tlp_block_size > prof.maxThreadsPerBlock && tlp_block_size <= 1024)
+        throw PlanError("plan_launch: tlp_block_size exceeds maxThreadsPerBlock");
+    wlp_launch_cfg c{};
+    char warn[512];
+    check(wlp_plan_launch(replications, mode_id(mode), tlp_block_size, grid_limit, &c, warn, sizeof warn));
+    LaunchPlan plan;
+    plan.cfg.blockDim = Dim3{c.block_x, c.block_y, c.block_z};
+    plan.cfg.gridDim = Dim2{c.grid_x, c.grid_y};
+    plan.cfg.warpSize = c.warp_size;
+    plan.replications = replications;
+    plan.mode = mode;
+    if (warn[0]) plan.warning = std::string(warn);
+    return plan;
+}
+
+std::optional<std::string> validate_params(ModelKind model, const ModelParams& p) {
+    const wlp_params c = to_c(p);
+    char warn[512];
+    check(wlp_validate_params(model_id(model), &c, warn, sizeof warn));
+    if (warn[0]) return std::string(warn);
+    return std::nullopt;
+}
+
+namespace {
+std::vector<std::vector<double>> run_one(ModelKind model, const ModelParams& p, RngState stream) {
+    const auto s = soa(stream);
+    const wlp_params c = to_c(p);
+    const int nout = model == ModelKind::Mm1 ? 3 : 1;
+    std::vector<std::vector<double>> o(3, std::vector<double>(1));
+    check(wlp_run_streams(model_id(model), &c, WLP_MODE_WLP, s.data(), 1, 0, o[0].data(),
+                          nout > 1 ? o[1].data() : nullptr, nout > 1 ? o[2].data() : nullptr, 0, nullptr, nullptr));
+    return o;
+}
+}  // namespace
+
+double pi_replication(std::int64_t draws, RngState stream) {
+    ModelParams p;
+    p.draws = draws;
+    return run_one(ModelKind::Pi, p, stream)[0][0];
+}
+
+MM1Result mm1_replication(std::int64_t clients, double lambda, double mu, RngState stream) {
+    ModelParams p;
+    p.clients = clients;
+    p.lambda = lambda;
+    p.mu = mu;
+    auto o = run_one(ModelKind::Mm1, p, stream);
+    return MM1Result{o[0][0], o[1][0], o[2][0]};
+}
+
+double walk_replication(std::int64_t steps, std::int64_t chunks, RngState stream) {
+    ModelParams p;
+    p.steps = steps;
+    p.chunks = chunks;
+    return run_one(ModelKind::Walk, p, stream)[0][0];
+}
+
+double inverse_normal_cdf(double p) {
+    double z = 0.0;
+    check(wlp_inverse_normal_cdf(p, &z));
+    return z;
+}
+
+ConfidenceInterval confidence_interval(const std::vector<double>& samples, double level) {
+    wlp_ci ci{};
+    check(wlp_confidence_interval(samples.empty() ? nullptr : samples.data(), static_cast<std::int64_t>(samples.size()),
+                                  level, &ci));
+    return ConfidenceInterval{ci.mean, ci.half_width, ci.level, ci.n, ci.warn_small_sample != 0};
+}
+
+ModelRun run_model(ModelKind model, const ModelParams& p, ExecutionMode mode, const DeviceProfile& prof,
+                   std::uint64_t master_seed, int tlp_block_size, const SimOptions&) {
+    const LaunchPlan plan = plan_launch(p.replications, mode, prof, tlp_block_size, 0x7FFFFFFF);
+    const wlp_params c = to_c(p);
+    const std::size_t R = static_cast<std::size_t>(p.replications);
+    ModelRun run;
+    run.cfg = plan.cfg;
+    run.mode = mode;
+    const bool mm1 = model == ModelKind::Mm1;
+    std::vector<double> o0(R), o1(mm1 ? R : 0), o2(mm1 ? R : 0);
+    wlp_report rep{};
+    char warn[512];
+    check(wlp_run(model_id(model), &c, mode_id(mode), master_seed, tlp_block_size, o0.data(),
+                  mm1 ? o1.data() : nullptr, mm1 ? o2.data() : nullptr, 0, nullptr, &rep, nullptr, 0.95, warn,
+                  sizeof warn));
+    if (warn[0]) run.warning = std::string(warn);
+    run.report = from_c(rep);
+    if (mm1) {
+        run.outputs["outIdle"] = std::move(o0);
+        run.outputs["outWait"] = std::move(o1);
+        run.outputs["outSys"] = std::move(o2);
+        run.primary = run.outputs["outWait"];
+    } else {
+        run.outputs["out"] = std::move(o0);
+        run.primary = run.outputs["out"];
+    }
+    return run;
+}
+
+// ---- sweep (reference sweep.hpp:42-60 semantics) ---------------------------------------
+
+std::vector<SweepRow> run_sweep(const SweepSpec& spec, const DeviceProfile& prof) {
+    if (spec.rMin < 1 || spec.rMin > spec.rMax) throw DomainError("sweep: need 1 <= rMin <= rMax");
+    if (spec.rStep < 1) throw DomainError("sweep: rStep must be >= 1");
+    if (spec.modes.empty()) throw DomainError("sweep: no execution modes selected");
+    std::vector<SweepRow> rows;
+    for (ExecutionMode mode : {ExecutionMode::Sequential, ExecutionMode::Tlp, ExecutionMode::Wlp}) {
+        bool on = false;
+        for (ExecutionMode m : spec.modes) on = on || m == mode;
+        if (!on) continue;
+        for (std::int64_t R = spec.rMin; R <= spec.rMax; R += spec.rStep) {
+            ModelParams params = spec.params;
+            params.replications = R;
+            const ModelRun run = run_model(spec.model, params, mode, prof, spec.masterSeed, spec.tlpBlockSize);
+            SweepRow row;
+            row.replications = R;
+            row.mode = mode;
+            row.model = spec.model;
+            row.totalCycles = run.report.totalCycles;  // measured on the GPU
+            row.memReads = run.report.memReads;
+            row.memWrites = run.report.memWrites;
+            row.divergenceEvents = run.report.divergenceEvents;
+            row.waves = run.report.wavesExecuted;
+            if (run.primary.size() >= 2) {
+                const ConfidenceInterval ci = confidence_interval(run.primary);
+                row.mean = ci.mean;
+                row.ciLow = ci.low();
+                row.ciHigh = ci.high();
+            } else {
+                row.mean = row.ciLow = row.ciHigh = run.primary.at(0);
+            }
+            rows.push_back(row);
+        }
+    }
+    return rows;
+}
+
+std::vector<std::int64_t> detect_steps(const std::vector<std::pair<std::int64_t, std::int64_t>>& curve) {
+    std::vector<std::int64_t> steps;
+    for (std::size_t i = 1; i < curve.size(); ++i) {
+        if (curve[i].first <= curve[i - 1].first)
+            throw AnalysisError("step detection: curve not sorted by ascending R");
+        if (curve[i].second < curve[i - 1].second)
+            throw AnalysisError("step detection: cycles decreased at R=" + std::to_string(curve[i].first) +
+                                " — cost curves must be non-decreasing");
+        if (curve[i].second > curve[i - 1].second) steps.push_back(curve[i].first);
+    }
+    return steps;
+}
+
+std::vector<std::pair<std::int64_t, std::int64_t>> curve_of(const std::vector<SweepRow>& rows, ExecutionMode mode) {
+    std::vector<std::pair<std::int64_t, std::int64_t>> c;
+    for (const SweepRow& r : rows)
+        if (r.mode == mode) c.emplace_back(r.replications, r.totalCycles);
+    return c;
+}
+
+std::string csv_string(const std::vector<SweepRow>& rows) {
+    std::ostringstream out;
+    out << kHeader << '\n';
+    for (const SweepRow& r : rows)
+        out << r.replications << ',' << mode_name(r.mode) << ',' << model_name(r.model) << ',' << r.totalCycles << ','
+            << r.memReads << ',' << r.memWrites << ',' << r.divergenceEvents << ',' << r.waves << ','
+            << fmt_double(r.mean) << ',' << fmt_double(r.ciLow) << ',' << fmt_double(r.ciHigh) << '\n';
+    return out.str();
+}
+
+void emit_csv(const std::vector<SweepRow>& rows, const std::string& path) {
+    if (rows.empty()) throw DomainError("emit_csv: no rows");
+    std::ofstream out(path);
+    if (!out) throw Error("cannot write csv: " + path);
+    out << csv_string(rows);
+    if (!out.flush()) throw Error("write failed: " + path);
+}
+
+std::vector<SweepRow> parse_csv_string(const std::string& text) {
+    std::istringstream in(text);
+    std::string line;
+    std::size_t lineno = 0;
+    std::vector<SweepRow> rows;
+    while (std::getline(in, line)) {
+        ++lineno;
+        if (!line.empty() && line.back() == '\r') line.pop_back();
+        if (lineno == 1) {
+            if (line != kHeader) throw ParseError("csv line 1: unexpected header");
+            continue;
+        }
+        if (line.empty()) continue;
+        std::vector<std::string> f;
+        std::size_t start = 0;
+        for (;;) {
+            const std::size_t comma = line.find(',', start);
+            f.push_back(line.substr(start, comma == std::string::npos ? std::string::npos : comma - start));
+            if (comma == std::string::npos) break;
+            start = comma + 1;
+        }
+        if (f.size() != 11)
+            throw ParseError("csv line " + std::to_string(lineno) + ": expected 11 fields, got " +
+                             std::to_string(f.size()));
+        SweepRow r;
+        r.replications = parse_num<std::int64_t>(f[0], lineno, "integer");
+        try {
+            r.mode = mode_from_name(f[1]);
+            r.model = model_from_name(f[2]);
+        } catch (const DomainError& e) {
+            throw ParseError("csv line " + std::to_string(lineno) + ": " + e.what());
+        }
+        r.totalCycles = parse_num<std::int64_t>(f[3], lineno, "integer");
+        r.memReads = parse_num<std::uint64_t>(f[4], lineno, "integer");
+        r.memWrites = parse_num<std::uint64_t>(f[5], lineno, "integer");
+        r.divergenceEvents = parse_num<std::uint64_t>(f[6], lineno, "integer");
+        r.waves = parse_num<std::int64_t>(f[7], lineno, "integer");
+        r.mean = parse_num<double>(f[8], lineno, "real");
+        r.ciLow = parse_num<double>(f[9], lineno, "real");
+        r.ciHigh = parse_num<double>(f[10], lineno, "real");
+        rows.push_back(r);
+    }
+    if (rows.empty()) throw ParseError("csv: no data rows");
+    return rows;
+}
+
+std::vector<SweepRow> parse_csv(const std::string& path) {
+    std::ifstream in(path);
+    if (!in) throw Error("cannot open csv: " + path);
+    std::ostringstream buf;
+    buf << in.rdbuf();
+    return parse_csv_string(buf.str());
+}
+
+}  // namespace warpsim
