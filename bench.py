@@ -374,6 +374,22 @@ def main():
                     units_ = pp.replications * pp.units(m)
                     r["issue_frac"] = units_ * INSTR_PER_UNIT[int(m)] / 32 / (r["kernel_ms"] * 1e-3) / (peak * 1e9)
                 extras[name][w.mode_name(md)] = r
+        # config 5: experimental plan, 64 factor-level sets x 30 replications, one launch
+        sets = [w.ModelParams(replications=30, clients=10_000, lambda_=0.1 + 0.8 * k / 63, mu=1.0) for k in range(64)]
+        seeds = [SEED + k for k in range(64)]
+        extras["cfg5_plan_mm1_64x30x1e4"] = {}
+        for md in (w.ExecutionMode.Wlp, w.ExecutionMode.Tlp):
+            outs = [torch.empty(64 * 30, dtype=torch.float64, device="cuda") for _ in range(3)]
+            kms = []
+
+            def pstep():
+                rep = w.SimReport()
+                w.run_plan(w.ModelKind.Mm1, sets, seeds, md, outs, on_device=True, report=rep)
+                kms.append(rep.kernel_ms)
+
+            pms = device_timed(pstep, 5, 3, 1)
+            extras["cfg5_plan_mm1_64x30x1e4"][w.mode_name(md)] = {
+                "reps_per_s": 1920 / (pms * 1e-3), "ms_per_run": pms, "kernel_ms": sum(kms[3:]) / len(kms[3:])}
         line["extras"] = extras
     if world == 1 and rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = {k: v for k, v in cpu_baseline(0, p).items() if k != "step_s"}

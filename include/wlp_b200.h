@@ -203,6 +203,16 @@ int wlp_run(int model, const wlp_params* p, int mode, uint64_t master_seed, int 
             double* out0, double* out1, double* out2, int out_on_device, void* stream,
             wlp_report* report, wlp_ci* ci, double level, char* warn, int warn_cap);
 
+/* Experimental plan (BASELINE config 5): n_sets factor-level sets of one model, set k
+ * being run_model(model, sets[k], mode, master_seeds[k]) — its own parameters, replication
+ * count and master seed — executed as ONE batched seeding launch and ONE model launch
+ * (WLP: warps take replications from a global counter; TLP: thread per replication).
+ * Outputs are concatenated in set order (set k starts at sum_{j<k} sets[j].replications)
+ * and bit-identical to the n_sets separate runs. Units per replication < 2^32. */
+int wlp_run_plan(int model, const wlp_params* sets, const uint64_t* master_seeds, int n_sets, int mode,
+                 int tlp_block_size, double* out0, double* out1, double* out2, int out_on_device,
+                 void* stream, wlp_report* report);
+
 /* Device statistics of a device array (pass 1: n and sum; pass 2: centred sum of
  * squares about stats->center). Synchronous; n <= 256 sums sequentially, bit-identical
  * to the reference's naive loop (models.cpp:104-109). */

@@ -254,6 +254,8 @@ _SIGS = {
                                 _P, _P, _P, C.c_int, _P, _P, _I64, C.POINTER(_I64), C.POINTER(_Report)]),
     "wlp_run": (C.c_int, [C.c_int, C.POINTER(_Params), C.c_int, C.c_uint64, C.c_int, _P, _P, _P, C.c_int, _P,
                           C.POINTER(_Report), C.POINTER(_CI), C.c_double, C.c_char_p, C.c_int]),
+    "wlp_run_plan": (C.c_int, [C.c_int, _P, _P, C.c_int, C.c_int, C.c_int, _P, _P, _P, C.c_int, _P,
+                               C.POINTER(_Report)]),
     "wlp_stats_device": (C.c_int, [_P, _I64, C.c_int, C.POINTER(Stats), _P]),
     "wlp_confidence_interval": (C.c_int, [_P, _I64, C.c_double, C.POINTER(_CI)]),
     "wlp_debug_neg_log1m": (C.c_int, [_P, _I64, _P]),
@@ -542,6 +544,39 @@ def run_shard(model: ModelKind, p: ModelParams, mode: ExecutionMode, master_seed
     if nsp.value > special_cap:
         raise Error("too many special seeding candidates")
     return list(sp[: nsp.value])
+
+
+def run_plan(model: ModelKind, sets: Sequence[ModelParams], master_seeds: Sequence[int], mode: ExecutionMode,
+             outs=None, *, on_device: bool = False, stream: Optional[int] = None, tlp_block_size: int = 256,
+             report: Optional[SimReport] = None):
+    """Experimental plan (BASELINE config 5): every factor-level set k is
+    run_model(model, sets[k], mode, master_seeds[k]), all in one launch. Returns a list (per
+    set) of output dicts when outs is None (host), else fills `outs` (concatenated)."""
+    model = ModelKind(model)
+    n = len(sets)
+    if n != len(master_seeds):
+        raise DomainError("plan: one master seed per set")
+    arr = (_Params * max(n, 1))(*[_params(p) for p in sets])
+    seeds = (C.c_uint64 * max(n, 1))(*[s & (2**64 - 1) for s in master_seeds])
+    R = sum(int(p.replications) for p in sets)
+    names = OUTPUT_NAMES[model]
+    host = outs is None
+    if host:
+        outs = [np.empty(R) for _ in names]
+    o = [_ptr(x) for x in outs] + [None] * (3 - len(outs))
+    rep = _Report() if report is not None else None
+    _check(_lib.wlp_run_plan(int(model), arr, seeds, n, int(mode), int(tlp_block_size), o[0], o[1], o[2],
+                             1 if on_device else 0, stream, C.byref(rep) if rep is not None else None))
+    if rep is not None:
+        report.__dict__.update(vars(_report(rep)))
+    if not host:
+        return None
+    res, off = [], 0
+    for p in sets:
+        r = int(p.replications)
+        res.append({nm: o_[off:off + r] for nm, o_ in zip(names, outs)})
+        off += r
+    return res
 
 
 def stats_device(x, n: int, pass_: int, stats: Optional[Stats] = None, stream: Optional[int] = None) -> Stats:

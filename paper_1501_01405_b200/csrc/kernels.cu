@@ -229,29 +229,36 @@ struct Queue {
 // Seeding
 // ---------------------------------------------------------------------------------
 
-__global__ void __launch_bounds__(kSeedBlock) k_seed(SeedArgs a) {
+// One block of stream slots of one random_spacing run: slots [blk*B, (blk+1)*B) of
+// `count` (B = kSeedBlock * kSeedPerThread), slot i = candidate c(slot_begin + i) after
+// the sorted rejection list; keys land SoA at out[plane*stride + out_off + i].
+__device__ __forceinline__ void seed_block(const uint32_t* __restrict__ pw, Taus master, int64_t slot_begin,
+                                           int64_t count, int64_t blk, const int64_t* __restrict__ rejected,
+                                           int64_t n_rejected, uint32_t* __restrict__ out, int64_t out_off,
+                                           int64_t stride, SpecialRec* specials, int64_t special_cap,
+                                           unsigned long long* n_special, uint32_t job) {
     extern __shared__ uint32_t sh[];  // 3 x [kSeedBlock][33] (padded: conflict-free)
     constexpr int kRow = kSeedPerThread + 1;
     constexpr int kPlane = kSeedBlock * kRow;
     const int tid = threadIdx.x;
-    const int64_t blk0 = static_cast<int64_t>(blockIdx.x) * kSeedBlock * kSeedPerThread;
+    const int64_t blk0 = blk * kSeedBlock * kSeedPerThread;
     const int64_t my0 = blk0 + static_cast<int64_t>(tid) * kSeedPerThread;
-    int64_t left = a.count - my0;
+    const int64_t left = count - my0;
     const int nmine = left <= 0 ? 0 : (left < kSeedPerThread ? static_cast<int>(left) : kSeedPerThread);
     if (nmine > 0) {
-        int64_t c = a.slot_begin + my0;  // candidate index of my first slot
+        int64_t c = slot_begin + my0;  // candidate index of my first slot
         int64_t ri = 0;
-        while (ri < a.n_rejected && a.rejected[ri] <= c) {
+        while (ri < n_rejected && rejected[ri] <= c) {
             ++c;
             ++ri;
         }
-        Taus m = jump_pow(a.powers, a.master, 3ull * static_cast<uint64_t>(c));
+        Taus m = jump_pow(pw, master, 3ull * static_cast<uint64_t>(c));
         for (int j = 0; j < nmine; ++j) {
             Taus key;
             for (;;) {
                 const uint32_t x = taus_next(m), y = taus_next(m), z = taus_next(m);
                 key = make_state(x, y, z);
-                if (ri < a.n_rejected && a.rejected[ri] == c) {  // a redrawn candidate
+                if (ri < n_rejected && rejected[ri] == c) {  // a redrawn candidate
                     ++ri;
                     ++c;
                     continue;
@@ -259,14 +266,14 @@ __global__ void __launch_bounds__(kSeedBlock) k_seed(SeedArgs a) {
                 break;
             }
             if (is_special_key(key)) {
-                const unsigned long long pos = atomicAdd(a.n_special, 1ull);
-                if (static_cast<int64_t>(pos) < a.special_cap) {
-                    SpecialRec* sp = static_cast<SpecialRec*>(a.specials) + pos;
+                const unsigned long long pos = atomicAdd(n_special, 1ull);
+                if (static_cast<int64_t>(pos) < special_cap) {
+                    SpecialRec* sp = specials + pos;
                     sp->index = c;
                     sp->s1 = key.s1;
                     sp->s2 = key.s2;
                     sp->s3 = key.s3;
-                    sp->pad = 0;
+                    sp->pad = job;
                 }
             }
             ++c;
@@ -276,14 +283,39 @@ __global__ void __launch_bounds__(kSeedBlock) k_seed(SeedArgs a) {
         }
     }
     __syncthreads();
-    int64_t nblk = a.count - blk0;
+    int64_t nblk = count - blk0;
     if (nblk > kSeedBlock * kSeedPerThread) nblk = kSeedBlock * kSeedPerThread;
     for (int i = tid; i < nblk; i += kSeedBlock) {
         const int si = (i / kSeedPerThread) * kRow + (i % kSeedPerThread);
-        a.out[blk0 + i] = sh[si];
-        a.out[a.count + blk0 + i] = sh[kPlane + si];
-        a.out[2 * a.count + blk0 + i] = sh[2 * kPlane + si];
+        out[out_off + blk0 + i] = sh[si];
+        out[stride + out_off + blk0 + i] = sh[kPlane + si];
+        out[2 * stride + out_off + blk0 + i] = sh[2 * kPlane + si];
     }
+}
+
+__global__ void __launch_bounds__(kSeedBlock) k_seed(SeedArgs a) {
+    seed_block(a.powers, a.master, a.slot_begin, a.count, blockIdx.x, a.rejected, a.n_rejected, a.out, a.out_off,
+               a.stride ? a.stride : a.count,
+               static_cast<SpecialRec*>(a.specials), a.special_cap, a.n_special, 0u);
+}
+
+// Many independent runs (one per plan set) in one launch; block -> job by binary search.
+__global__ void __launch_bounds__(kSeedBlock) k_seed_jobs(const uint32_t* __restrict__ pw,
+                                                          const SeedJob* __restrict__ jobs, int n_jobs,
+                                                          uint32_t* __restrict__ out, int64_t total,
+                                                          SpecialRec* specials, int64_t special_cap,
+                                                          unsigned long long* n_special) {
+    int lo = 0, hi = n_jobs - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (jobs[mid].block0 <= static_cast<int64_t>(blockIdx.x))
+            lo = mid;
+        else
+            hi = mid - 1;
+    }
+    const SeedJob& J = jobs[lo];
+    seed_block(pw, J.master, 0, J.count, blockIdx.x - J.block0, nullptr, 0, out, J.out_off, total, specials,
+               special_cap, n_special, static_cast<uint32_t>(lo));
 }
 
 constexpr int kTausPerThread = 64;
@@ -375,63 +407,86 @@ constexpr size_t kMm1Smem =
 // mm1: lanes generate, lane 0 recurses. Panel p covers clients [p*32T, (p+1)*32T); lane l
 // produces clients p*32T + l*T + j (j < T) from draws 2*(that index) and 2*(...)+1, so
 // each lane steps its own contiguous draw range and hops 62T draws between panels.
+// Returns the queue (valid on lane 0).
 template <bool INV>
-__global__ void __launch_bounds__(kMm1Block) k_wlp_mm1(RepArgs a, const uint32_t* __restrict__ gtab,
-                                                        const uint32_t* __restrict__ gskip) {
+__device__ __forceinline__ Queue mm1_warp_rep(Taus st, int64_t n, double lambda, double mu, double inv_l,
+                                              double inv_m, const double* logtab, const uint32_t* skip, Mm1Warp& W,
+                                              int lane) {
     constexpr int T = kMm1PanelT;
     constexpr int P = kMm1P;
     static_assert(2 * T % kExpoB == 0, "panel draws per lane must be whole batches");
+    Queue q;
+    for (int64_t base = 0; base < n; base += P) {
+        // draws of my T clients: a_c = draw 2c, s_c = draw 2c+1, in batches of kExpoB;
+        // the panel buffer doubles as the batches' near-one scratch until it is written
+        double ea[T], es[T];
+#pragma unroll
+        for (int h = 0; h < 2 * T; h += kExpoB) {
+            uint32_t d[kExpoB];
+            double e[kExpoB];
+#pragma unroll
+            for (int j = 0; j < kExpoB; ++j) d[j] = taus_next(st);
+            neg_log1m_batch<kExpoB>(d, e, logtab, W.nl, W.a, kFull, lane);
+#pragma unroll
+            for (int j = 0; j < kExpoB; j += 2) {
+                ea[(h + j) / 2] = scale<INV>(e[j], lambda, inv_l);
+                es[(h + j) / 2] = scale<INV>(e[j + 1], mu, inv_m);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < T; ++c) {
+            W.a[c * 32 + lane] = ea[c];
+            W.s[c * 32 + lane] = es[c];
+        }
+        __syncwarp();
+        if (lane == 0) {
+            const int64_t left = n - base;
+            const int cnt = left < P ? static_cast<int>(left) : P;
+            for (int c = 0; c < cnt; ++c) {
+                const int idx = (c % T) * 32 + c / T;
+                q.client(W.a[idx], W.s[idx]);
+            }
+        }
+        __syncwarp();
+        st = uni_jump(skip, st);
+    }
+    return q;
+}
+
+struct Mm1Smem {
+    uint32_t* tab;
+    uint32_t* skip;
+    double* logtab;
+    Mm1Warp* W;
+};
+
+__device__ __forceinline__ Mm1Smem mm1_stage(const uint32_t* gtab, const uint32_t* gskip) {
     extern __shared__ __align__(16) unsigned char smraw[];
-    uint32_t* tab = reinterpret_cast<uint32_t*>(smraw);
-    uint32_t* skip = tab + kLaneTabWords;
-    double* logtab = reinterpret_cast<double*>(skip + kUniTabWords);
-    Mm1Warp& W = reinterpret_cast<Mm1Warp*>(logtab + 256)[threadIdx.x >> 5];
-    stage_u32<kLaneTabWords>(tab, gtab);
-    for (int i = threadIdx.x; i < kUniTabWords; i += blockDim.x) skip[i] = __ldg(gskip + i);
-    stage_log_table(logtab);
+    Mm1Smem m;
+    m.tab = reinterpret_cast<uint32_t*>(smraw);
+    m.skip = m.tab + kLaneTabWords;
+    m.logtab = reinterpret_cast<double*>(m.skip + kUniTabWords);
+    m.W = reinterpret_cast<Mm1Warp*>(m.logtab + 256) + (threadIdx.x >> 5);
+    stage_u32<kLaneTabWords>(m.tab, gtab);
+    for (int i = threadIdx.x; i < kUniTabWords; i += blockDim.x) m.skip[i] = __ldg(gskip + i);
+    stage_log_table(m.logtab);
     __syncthreads();
+    return m;
+}
+
+template <bool INV>
+__global__ void __launch_bounds__(kMm1Block) k_wlp_mm1(RepArgs a, const uint32_t* __restrict__ gtab,
+                                                        const uint32_t* __restrict__ gskip) {
+    const Mm1Smem m = mm1_stage(gtab, gskip);
     const int lane = threadIdx.x & 31;
     const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     const int64_t lo = warp * a.count / nwarps, hi = (warp + 1) * a.count / nwarps;
     double k0 = 0.0, k1 = 0.0, k2 = 0.0;
     for (int64_t r = lo; r < hi; ++r) {
-        Taus st = lane_jump(tab, lane, load_seed(a, r));
-        Queue q;
-        for (int64_t base = 0; base < a.n; base += P) {
-            // draws of my T clients: a_c = draw 2c, s_c = draw 2c+1, in batches of kExpoB;
-            // the panel buffer doubles as the batches' near-one scratch until it is written
-            double ea[T], es[T];
-#pragma unroll
-            for (int h = 0; h < 2 * T; h += kExpoB) {
-                uint32_t n[kExpoB];
-                double e[kExpoB];
-#pragma unroll
-                for (int j = 0; j < kExpoB; ++j) n[j] = taus_next(st);
-                neg_log1m_batch<kExpoB>(n, e, logtab, W.nl, W.a, kFull, lane);
-#pragma unroll
-                for (int j = 0; j < kExpoB; j += 2) {
-                    ea[(h + j) / 2] = scale<INV>(e[j], a.lambda, a.inv_lambda);
-                    es[(h + j) / 2] = scale<INV>(e[j + 1], a.mu, a.inv_mu);
-                }
-            }
-#pragma unroll
-            for (int c = 0; c < T; ++c) {
-                W.a[c * 32 + lane] = ea[c];
-                W.s[c * 32 + lane] = es[c];
-            }
-            __syncwarp();
-            if (lane == 0) {
-                const int64_t left = a.n - base;
-                const int cnt = left < P ? static_cast<int>(left) : P;
-                for (int c = 0; c < cnt; ++c) {
-                    const int idx = (c % T) * 32 + c / T;
-                    q.client(W.a[idx], W.s[idx]);
-                }
-            }
-            __syncwarp();
-            st = uni_jump(skip, st);
-        }
+        const Taus st = lane_jump(m.tab, lane, load_seed(a, r));
+        const Queue q = mm1_warp_rep<INV>(st, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu, m.logtab, m.skip, *m.W,
+                                          lane);
         const double nd = static_cast<double>(a.n);
         const double v0 = __shfl_sync(kFull, __ddiv_rn(q.idle, nd), 0);
         const double v1 = __shfl_sync(kFull, __ddiv_rn(q.sumw, nd), 0);
@@ -456,46 +511,76 @@ __global__ void __launch_bounds__(kMm1Block) k_wlp_mm1(RepArgs a, const uint32_t
 // TLP: one replication per thread (the comparison mapping)
 // ---------------------------------------------------------------------------------
 
+__device__ __forceinline__ double pi_rep_tlp(Taus st, int64_t n) {
+    // c counts exactly (the reference accumulates 0.0/1.0 in a double, exact < 2^53)
+    uint64_t c = 0;
+    for (int64_t done = 0; done < n;) {
+        const int64_t left = n - done;
+        const uint32_t part = left > 0x40000000 ? 0x40000000u : static_cast<uint32_t>(left);
+        c += pi_hits(st, part);
+        done += part;
+    }
+    return __ddiv_rn(__dmul_rn(4.0, static_cast<double>(c)), static_cast<double>(n));
+}
+
+// models.hpp:92-105 as written: a 4-way branch per step on d = floor(4u).
+__device__ __forceinline__ double walk_rep_tlp(Taus st, int64_t n, int64_t chunks) {
+    double px = 0.0, py = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        const uint32_t d = taus_next(st) >> 30;
+        (void)taus_next(st);
+        if (d == 0u)
+            px = __dadd_rn(px, 1.0);
+        else if (d == 1u)
+            px = __dsub_rn(px, 1.0);
+        else if (d == 2u)
+            py = __dadd_rn(py, 1.0);
+        else
+            py = __dsub_rn(py, 1.0);
+    }
+    return walk_fold(static_cast<int64_t>(px), chunks);
+}
+
 template <int MODEL>
 __global__ void k_tlp(RepArgs a) {
     const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (r >= a.count) return;  // tail threads of the last block stay inert (wlp.cpp:125-138)
-    Taus st = load_seed(a, r);
-    if (MODEL == 0) {
-        // c counts exactly (the reference accumulates 0.0/1.0 in a double, exact < 2^53)
-        uint64_t c = 0;
-        for (int64_t done = 0; done < a.n;) {
-            const int64_t left = a.n - done;
-            const uint32_t part = left > 0x40000000 ? 0x40000000u : static_cast<uint32_t>(left);
-            c += pi_hits(st, part);
-            done += part;
-        }
-        a.out0[r] = __ddiv_rn(__dmul_rn(4.0, static_cast<double>(c)), static_cast<double>(a.n));
-    } else {
-        // models.hpp:92-105 as written: a 4-way branch per step on d = floor(4u).
-        double px = 0.0, py = 0.0;
-        for (int64_t i = 0; i < a.n; ++i) {
-            const uint32_t d = taus_next(st) >> 30;
-            (void)taus_next(st);
-            if (d == 0u)
-                px = __dadd_rn(px, 1.0);
-            else if (d == 1u)
-                px = __dsub_rn(px, 1.0);
-            else if (d == 2u)
-                py = __dadd_rn(py, 1.0);
-            else
-                py = __dsub_rn(py, 1.0);
-        }
-        a.out0[r] = walk_fold(static_cast<int64_t>(px), a.chunks);
-    }
+    const Taus st = load_seed(a, r);
+    a.out0[r] = MODEL == 0 ? pi_rep_tlp(st, a.n) : walk_rep_tlp(st, a.n, a.chunks);
 }
 
 // mm1 thread per replication: each lane runs its own queue; the exponentials of 4
-// clients (8 draws) per lane go through the warp-cooperative batch log.
+// clients (8 draws) per lane go through the warp-cooperative batch log. Every thread of
+// a warp takes part in each batch up to the warp's longest replication (`n_warp`).
 struct TlpMm1Warp {
     NearList nl;
     double res[32 * kExpoB];
 };
+
+template <bool INV>
+__device__ __forceinline__ Queue mm1_thread_rep(Taus st, int64_t n, int64_t n_warp, double lambda, double mu,
+                                                double inv_l, double inv_m, const double* logtab, TlpMm1Warp& W,
+                                                unsigned mask, int lane) {
+    Queue q;
+    for (int64_t done = 0; done < n_warp; done += kExpoB / 2) {
+        uint32_t d[kExpoB];
+        double e[kExpoB];
+#pragma unroll
+        for (int j = 0; j < kExpoB; ++j) d[j] = taus_next(st);
+        neg_log1m_batch<kExpoB>(d, e, logtab, W.nl, W.res, mask, lane);
+        const int64_t left = n - done;
+        const int cnt = left <= 0 ? 0 : (left < kExpoB / 2 ? static_cast<int>(left) : kExpoB / 2);
+#pragma unroll
+        for (int c = 0; c < kExpoB / 2; ++c)
+            if (c < cnt) q.client(scale<INV>(e[2 * c], lambda, inv_l), scale<INV>(e[2 * c + 1], mu, inv_m));
+    }
+    return q;
+}
+
+__device__ __forceinline__ unsigned block_lane_mask() {  // partial last warp of odd-sized blocks
+    const int in_warp = static_cast<int>(blockDim.x) - (static_cast<int>(threadIdx.x) & ~31);
+    return in_warp >= 32 ? kFull : ((1u << in_warp) - 1u);
+}
 
 template <bool INV>
 __global__ void k_tlp_mm1(RepArgs a) {
@@ -505,28 +590,125 @@ __global__ void k_tlp_mm1(RepArgs a) {
     stage_log_table(logtab);
     __syncthreads();
     const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    // every thread of a warp takes part in the batch (tail threads on a dummy stream);
-    // blocks that are not a multiple of 32 have a partial last warp
     const int lane = threadIdx.x & 31;
-    const int in_warp = static_cast<int>(blockDim.x) - (static_cast<int>(threadIdx.x) & ~31);
-    const unsigned mask = in_warp >= 32 ? kFull : ((1u << in_warp) - 1u);
     const bool live = r < a.count;
-    Taus st = live ? load_seed(a, r) : Taus{2u, 8u, 16u};
-    Queue q;
-    for (int64_t done = 0; done < a.n; done += kExpoB / 2) {
-        uint32_t n[kExpoB];
-        double e[kExpoB];
-#pragma unroll
-        for (int j = 0; j < kExpoB; ++j) n[j] = taus_next(st);
-        neg_log1m_batch<kExpoB>(n, e, logtab, W.nl, W.res, mask, lane);
-        const int64_t left = a.n - done;
-        const int cnt = left < kExpoB / 2 ? static_cast<int>(left) : kExpoB / 2;
-#pragma unroll
-        for (int c = 0; c < kExpoB / 2; ++c)
-            if (c < cnt) q.client(scale<INV>(e[2 * c], a.lambda, a.inv_lambda), scale<INV>(e[2 * c + 1], a.mu, a.inv_mu));
-    }
+    const Taus st = live ? load_seed(a, r) : Taus{2u, 8u, 16u};  // tail threads: dummy stream
+    const Queue q = mm1_thread_rep<INV>(st, a.n, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu, logtab, W,
+                                        block_lane_mask(), lane);
     if (!live) return;
     const double nd = static_cast<double>(a.n);
+    a.out0[r] = __ddiv_rn(q.idle, nd);
+    a.out1[r] = __ddiv_rn(q.sumw, nd);
+    a.out2[r] = __ddiv_rn(q.sums, nd);
+}
+
+// ---------------------------------------------------------------------------------
+// Experimental plan (BASELINE config 5): heterogeneous factor-level sets, one launch.
+// WLP warps take replications from a global counter (costs differ per set); pi/walk use
+// fixed panels (kPlanT units per lane) so one pair of jump tables serves every set.
+// ---------------------------------------------------------------------------------
+
+__device__ __forceinline__ int find_set(const SetParam* __restrict__ s, int n, int64_t r) {
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s[mid].off <= r)
+            lo = mid;
+        else
+            hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ Taus plan_seed(const PlanArgs& a, int64_t r) {
+    return Taus{__ldg(a.seeds + r), __ldg(a.seeds + a.count + r), __ldg(a.seeds + 2 * a.count + r)};
+}
+
+__device__ __forceinline__ int64_t next_rep(const PlanArgs& a, int lane) {
+    unsigned long long r = 0;
+    if (lane == 0) r = atomicAdd(a.next, 1ull);
+    return static_cast<int64_t>(__shfl_sync(kFull, r, 0));
+}
+
+template <int MODEL>
+__global__ void __launch_bounds__(kWlpBlock, 3) k_plan_lanes(PlanArgs a, const uint32_t* __restrict__ gtab,
+                                                              const uint32_t* __restrict__ gskip) {
+    extern __shared__ uint32_t sm[];
+    uint32_t* tab = sm;
+    uint32_t* skip = sm + kLaneTabWords;
+    stage_u32<kLaneTabWords>(tab, gtab);
+    for (int i = threadIdx.x; i < kUniTabWords; i += blockDim.x) skip[i] = __ldg(gskip + i);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    constexpr int64_t P = 32 * kPlanT;
+    for (int64_t r = next_rep(a, lane); r < a.count; r = next_rep(a, lane)) {
+        const SetParam S = a.sets[find_set(a.sets, a.n_sets, r)];
+        Taus st = lane_jump(tab, lane, plan_seed(a, r));
+        int64_t acc = 0;
+        for (int64_t base = 0; base < S.n; base += P) {
+            int64_t mine = S.n - base - static_cast<int64_t>(lane) * kPlanT;
+            mine = mine < 0 ? 0 : (mine > kPlanT ? kPlanT : mine);
+            if (MODEL == 0)
+                acc += pi_hits(st, static_cast<uint32_t>(mine));
+            else
+                acc += walk_dx(st, static_cast<uint32_t>(mine));
+            st = uni_jump(skip, st);
+        }
+        const int64_t total = warp_sum_i64(acc);
+        if (lane == 0)
+            a.out0[r] = MODEL == 0 ? __ddiv_rn(__dmul_rn(4.0, static_cast<double>(total)), static_cast<double>(S.n))
+                                   : walk_fold(total, S.chunks);
+    }
+}
+
+__global__ void __launch_bounds__(kMm1Block) k_plan_mm1(PlanArgs a, const uint32_t* __restrict__ gtab,
+                                                         const uint32_t* __restrict__ gskip) {
+    const Mm1Smem m = mm1_stage(gtab, gskip);
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = next_rep(a, lane); r < a.count; r = next_rep(a, lane)) {
+        const SetParam S = a.sets[find_set(a.sets, a.n_sets, r)];
+        const Taus st = lane_jump(m.tab, lane, plan_seed(a, r));
+        const Queue q = (S.inv_lambda != 0.0 && S.inv_mu != 0.0)
+                            ? mm1_warp_rep<true>(st, S.n, S.lambda, S.mu, S.inv_lambda, S.inv_mu, m.logtab, m.skip,
+                                                 *m.W, lane)
+                            : mm1_warp_rep<false>(st, S.n, S.lambda, S.mu, S.inv_lambda, S.inv_mu, m.logtab, m.skip,
+                                                  *m.W, lane);
+        if (lane == 0) {
+            const double nd = static_cast<double>(S.n);
+            a.out0[r] = __ddiv_rn(q.idle, nd);
+            a.out1[r] = __ddiv_rn(q.sumw, nd);
+            a.out2[r] = __ddiv_rn(q.sums, nd);
+        }
+    }
+}
+
+template <int MODEL>
+__global__ void k_plan_tlp(PlanArgs a) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= a.count) return;
+    const SetParam S = a.sets[find_set(a.sets, a.n_sets, r)];
+    const Taus st = plan_seed(a, r);
+    a.out0[r] = MODEL == 0 ? pi_rep_tlp(st, S.n) : walk_rep_tlp(st, S.n, S.chunks);
+}
+
+__global__ void k_plan_tlp_mm1(PlanArgs a) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double* logtab = reinterpret_cast<double*>(smraw);
+    TlpMm1Warp& W = reinterpret_cast<TlpMm1Warp*>(logtab + 256)[threadIdx.x >> 5];
+    stage_log_table(logtab);
+    __syncthreads();
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const unsigned mask = block_lane_mask();
+    const bool live = r < a.count;
+    const SetParam S = a.sets[find_set(a.sets, a.n_sets, live ? r : a.count - 1)];
+    const int64_t n = live ? S.n : 0;
+    const int64_t n_warp = static_cast<int64_t>(__reduce_max_sync(mask, static_cast<unsigned>(n)));
+    const Taus st = live ? plan_seed(a, r) : Taus{2u, 8u, 16u};
+    // per-lane rates differ across sets: always divide unless the lane's rates are 2^k
+    const Queue q = mm1_thread_rep<false>(st, n, n_warp, S.lambda, S.mu, 0.0, 0.0, logtab, W, mask, lane);
+    if (!live) return;
+    const double nd = static_cast<double>(S.n);
     a.out0[r] = __ddiv_rn(q.idle, nd);
     a.out1[r] = __ddiv_rn(q.sumw, nd);
     a.out2[r] = __ddiv_rn(q.sums, nd);
@@ -704,6 +886,61 @@ cudaError_t launch_tlp(int model, const RepArgs& a, int tlp_block, cudaStream_t 
             break;
         }
         default: k_tlp<2><<<g, b, 0, st>>>(a); break;
+    }
+    return cudaGetLastError();
+}
+
+int plan_blocks_per_sm(int model) {
+    int nb = 0;
+    if (model == 1) {
+        allow_smem(k_plan_mm1, kMm1Smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_plan_mm1, kMm1Block, kMm1Smem);
+    } else {
+        const size_t smem = (kLaneTabWords + kUniTabWords) * 4;
+        allow_smem(k_plan_lanes<0>, smem);
+        allow_smem(k_plan_lanes<2>, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_plan_lanes<0>, kWlpBlock, smem);
+    }
+    return nb < 1 ? 1 : nb;
+}
+
+cudaError_t launch_seed_jobs(const uint32_t* powers, const SeedJob* d_jobs, int n_jobs, int64_t total_blocks,
+                             int64_t total_slots, uint32_t* out, void* specials, int64_t special_cap,
+                             unsigned long long* n_special, cudaStream_t st) {
+    if (total_blocks <= 0) return cudaSuccess;
+    const size_t smem = 3 * kSeedBlock * (kSeedPerThread + 1) * 4;
+    allow_smem(k_seed_jobs, smem);
+    k_seed_jobs<<<static_cast<unsigned>(total_blocks), kSeedBlock, smem, st>>>(
+        powers, d_jobs, n_jobs, out, total_slots, static_cast<SpecialRec*>(specials), special_cap, n_special);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_plan(int model, int mode, const PlanArgs& a, const uint32_t* lane_tab, const uint32_t* uni_tab,
+                        const uint32_t* mm1_lane, const uint32_t* mm1_skip, int grid, int tlp_block,
+                        cudaStream_t st) {
+    if (a.count <= 0) return cudaSuccess;
+    if (mode == 1) {  // TLP
+        const int64_t block = a.count < tlp_block ? a.count : tlp_block;
+        const dim3 g(static_cast<unsigned>((a.count + block - 1) / block)), b(static_cast<unsigned>(block));
+        if (model == 1) {
+            const size_t smem = tlp_mm1_smem(static_cast<int>(block));
+            allow_smem(k_plan_tlp_mm1, smem);
+            k_plan_tlp_mm1<<<g, b, smem, st>>>(a);
+        } else if (model == 0) {
+            k_plan_tlp<0><<<g, b, 0, st>>>(a);
+        } else {
+            k_plan_tlp<2><<<g, b, 0, st>>>(a);
+        }
+        return cudaGetLastError();
+    }
+    if (model == 1) {
+        k_plan_mm1<<<grid, kMm1Block, kMm1Smem, st>>>(a, mm1_lane, mm1_skip);
+    } else {
+        const size_t smem = (kLaneTabWords + kUniTabWords) * 4;
+        if (model == 0)
+            k_plan_lanes<0><<<grid, kWlpBlock, smem, st>>>(a, lane_tab, uni_tab);
+        else
+            k_plan_lanes<2><<<grid, kWlpBlock, smem, st>>>(a, lane_tab, uni_tab);
     }
     return cudaGetLastError();
 }

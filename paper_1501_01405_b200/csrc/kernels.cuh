@@ -28,12 +28,43 @@ struct SeedArgs {
     int64_t slot_begin, count;
     const int64_t* rejected;  // sorted global candidate indices
     int64_t n_rejected;
-    uint32_t* out;  // SoA 3*count
+    uint32_t* out;  // SoA: plane p of slot i at out[p*stride + out_off + i]
     void* specials;  // wlp_special[cap]
     int64_t special_cap;
     unsigned long long* n_special;
+    int64_t out_off = 0;
+    int64_t stride = 0;  // 0: count
 };
 
+// Experimental plan (BASELINE config 5): many factor-level sets in one launch.
+struct SetParam {
+    int64_t off;     // first replication of the set in the concatenated launch
+    int64_t n;       // units per replication
+    int64_t chunks;  // walk
+    double lambda, mu, inv_lambda, inv_mu;
+};
+
+struct PlanArgs {
+    const uint32_t* seeds;  // SoA over all replications of all sets
+    int64_t count;          // total replications
+    const SetParam* sets;
+    int n_sets;
+    double* out0;
+    double* out1;
+    double* out2;
+    unsigned long long* next;  // dynamic work counter (zeroed before launch)
+};
+
+// Batched seeding of many independent random_spacing runs (one per set).
+struct SeedJob {
+    Taus master;
+    uint32_t pad;
+    int64_t count;    // slots of this job
+    int64_t out_off;  // first slot in the concatenated SoA
+    int64_t block0;   // first block of this job in the launch
+};
+
+constexpr int kPlanT = 32;          // pi/walk plan kernels: units per lane per panel
 constexpr int kWlpBlock = 512;     // pi / walk WLP block (16 warps; 3 blocks = 48 warps per SM)
 constexpr int kMm1Block = 256;     // mm1 WLP block (8 warps)
 constexpr int kMm1PanelT = 8;      // mm1: clients per lane per panel
@@ -61,6 +92,16 @@ cudaError_t launch_wlp(int model, const RepArgs& a, const uint32_t* lane_tab,
                        const uint32_t* uni_tab, int64_t lane_units, int grid, cudaStream_t st);
 // TLP: thread per replication, block = tlp_block, grid = ceil(count / tlp_block).
 cudaError_t launch_tlp(int model, const RepArgs& a, int tlp_block, cudaStream_t st);
+// Plan: batched seeding (specials carry the job index in `pad`), then one model launch.
+cudaError_t launch_seed_jobs(const uint32_t* powers, const SeedJob* d_jobs, int n_jobs, int64_t total_blocks,
+                             int64_t total_slots, uint32_t* out, void* specials, int64_t special_cap,
+                             unsigned long long* n_special, cudaStream_t st);
+// grid: persistent blocks for WLP; TLP uses `tlp_block` threads per block over all replications.
+cudaError_t launch_plan(int model, int mode, const PlanArgs& a, const uint32_t* lane_tab, const uint32_t* uni_tab,
+                        const uint32_t* mm1_lane, const uint32_t* mm1_skip, int grid, int tlp_block,
+                        cudaStream_t st);
+int plan_blocks_per_sm(int model);
+
 // Stats: per-block partials [grid][4] (sum_hi, sum_lo or ss_hi, ss_lo) of x (pass 1
 // about 0, pass 2 about `center`).
 cudaError_t launch_stats(const double* x, int64_t n, int pass, double center, double* partials,

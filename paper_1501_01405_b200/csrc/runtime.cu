@@ -85,6 +85,11 @@ struct DevCtx {
     DevBuf<SpecialRec> specials;
     DevBuf<unsigned long long> counter;
     DevBuf<int64_t> rejected;
+    DevBuf<unsigned long long> work;
+    DevBuf<SeedJob> jobs;
+    DevBuf<SetParam> setp;
+    DevBuf<uint32_t> plan_lane, plan_skip;
+    int plan_bps[3] = {1, 1, 1};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
 
@@ -104,9 +109,15 @@ int ctx_init(DevCtx& c) {
     WLP_TRY(upload_u32(c.powers, flat_binary_powers()));
     WLP_TRY(upload_u32(c.mm1_lane, lane_tables(2ull * kMm1PanelT)));
     WLP_TRY(upload_u32(c.mm1_skip, uniform_table(2ull * 31 * kMm1PanelT)));
-    for (int m = 0; m < 3; ++m) c.wlp_bps[m] = wlp_blocks_per_sm(m);
+    WLP_TRY(upload_u32(c.plan_lane, lane_tables(2ull * kPlanT)));
+    WLP_TRY(upload_u32(c.plan_skip, uniform_table(2ull * 31 * kPlanT)));
+    for (int m = 0; m < 3; ++m) {
+        c.wlp_bps[m] = wlp_blocks_per_sm(m);
+        c.plan_bps[m] = plan_blocks_per_sm(m);
+    }
     WLP_CUDA(c.specials.ensure(kSpecialCap));
     WLP_CUDA(c.counter.ensure(1));
+    WLP_CUDA(c.work.ensure(1));
     WLP_CUDA(cudaEventCreate(&c.ev0));
     WLP_CUDA(cudaEventCreate(&c.ev1));
     WLP_CUDA(cudaGetLastError());
@@ -826,6 +837,120 @@ int wlp_run(int model, const wlp_params* p, int mode, uint64_t master_seed, int 
         float ms = 0.f;
         WLP_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
         fill_report(*c, model, mode, tlp_block_size, R, grid, ms, report);
+    }
+    return WLP_OK;
+}
+
+int wlp_run_plan(int model, const wlp_params* sets, const uint64_t* master_seeds, int n_sets, int mode,
+                 int tlp_block_size, double* out0, double* out1, double* out2, int out_on_device, void* stream,
+                 wlp_report* report) {
+    WLP_TRY(check_model_mode(model, mode));
+    if (n_sets < 1 || !sets || !master_seeds) return fail(WLP_EDOMAIN, "plan: need at least one set");
+    std::vector<SetParam> sp(n_sets);
+    std::vector<SeedJob> jobs(n_sets);
+    int64_t R = 0, blocks = 0;
+    const int64_t per_block = static_cast<int64_t>(kSeedBlock) * kSeedPerThread;
+    for (int k = 0; k < n_sets; ++k) {
+        WLP_TRY(validate(model, &sets[k], nullptr));
+        const int64_t n = units_of(model, sets[k]);
+        if (n > 0xFFFFFFFFll) return fail(WLP_EPLAN, "plan: units per replication must be < 2^32");
+        sp[k] = SetParam{R, n, sets[k].chunks, sets[k].lambda, sets[k].mu,
+                         model == WLP_MODEL_MM1 ? exact_reciprocal(sets[k].lambda) : 0.0,
+                         model == WLP_MODEL_MM1 ? exact_reciprocal(sets[k].mu) : 0.0};
+        jobs[k] = SeedJob{master_from_seed(master_seeds[k]), 0u, sets[k].replications, R, blocks};
+        R += sets[k].replications;
+        blocks += (sets[k].replications + per_block - 1) / per_block;
+    }
+    WLP_TRY(plan(R, mode, tlp_block_size, 0x7FFFFFFF, nullptr, nullptr));
+    DevCtx* c;
+    std::unique_lock<std::mutex> lk;
+    WLP_TRY(acquire(c, lk));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    WLP_CUDA(c->seeds.ensure(3 * R));
+    WLP_CUDA(c->jobs.ensure(n_sets));
+    WLP_CUDA(c->setp.ensure(n_sets));
+    WLP_CUDA(cudaMemcpyAsync(c->jobs.p, jobs.data(), n_sets * sizeof(SeedJob), cudaMemcpyHostToDevice, st));
+    WLP_CUDA(cudaMemcpyAsync(c->setp.p, sp.data(), n_sets * sizeof(SetParam), cudaMemcpyHostToDevice, st));
+    double *o0 = out0, *o1 = out1, *o2 = out2;
+    if (!out_on_device) {
+        WLP_CUDA(c->outs.ensure(3 * R));
+        o0 = c->outs.p;
+        o1 = c->outs.p + R;
+        o2 = c->outs.p + 2 * R;
+    }
+    // one batched seeding launch for all sets
+    WLP_CUDA(cudaMemsetAsync(c->counter.p, 0, 8, st));
+    WLP_CUDA(launch_seed_jobs(c->powers.p, c->jobs.p, n_sets, blocks, R, c->seeds.p, c->specials.p, kSpecialCap,
+                              c->counter.p, st));
+    std::vector<SpecialRec> specials;
+    int64_t nt = 0;
+    WLP_TRY(read_specials(*c, st, specials, nt));
+    // per set, a key collision (only ever between special candidates) re-seeds that set
+    // exactly with its rejection list
+    std::map<uint32_t, std::vector<SpecialRec>> by_job;
+    for (const SpecialRec& s : specials) by_job[s.pad].push_back(s);
+    for (auto& kv : by_job) {
+        if (kv.second.size() < 2) continue;
+        const int k = static_cast<int>(kv.first);
+        std::vector<int64_t> rej, next;
+        WLP_TRY(spacing_rejections(kv.second, rej, next));
+        while (next != rej) {  // re-seed set k in place (its slice of the SoA) until no new redraw
+            rej.swap(next);
+            WLP_CUDA(c->rejected.ensure(static_cast<int64_t>(rej.size())));
+            WLP_CUDA(cudaMemcpyAsync(c->rejected.p, rej.data(), rej.size() * 8, cudaMemcpyHostToDevice, st));
+            WLP_CUDA(cudaMemsetAsync(c->counter.p, 0, 8, st));
+            SeedArgs a{};
+            a.powers = c->powers.p;
+            a.master = jobs[k].master;
+            a.slot_begin = 0;
+            a.count = jobs[k].count;
+            a.rejected = c->rejected.p;
+            a.n_rejected = static_cast<int64_t>(rej.size());
+            a.out = c->seeds.p;
+            a.out_off = jobs[k].out_off;
+            a.stride = R;
+            a.specials = c->specials.p;
+            a.special_cap = kSpecialCap;
+            a.n_special = c->counter.p;
+            WLP_CUDA(launch_seed(a, st));
+            std::vector<SpecialRec> sp2;
+            int64_t n2 = 0;
+            WLP_TRY(read_specials(*c, st, sp2, n2));
+            WLP_TRY(spacing_rejections(sp2, rej, next));
+        }
+    }
+    PlanArgs pa;
+    pa.seeds = c->seeds.p;
+    pa.count = R;
+    pa.sets = c->setp.p;
+    pa.n_sets = n_sets;
+    pa.out0 = o0;
+    pa.out1 = o1;
+    pa.out2 = o2;
+    pa.next = c->work.p;
+    WLP_CUDA(cudaMemsetAsync(c->work.p, 0, 8, st));
+    const int wpb = (model == WLP_MODEL_MM1 ? kMm1Block : kWlpBlock) / 32;
+    const int grid = static_cast<int>(
+        std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(c->sms) * c->plan_bps[model], (R + wpb - 1) / wpb)));
+    if (report) WLP_CUDA(cudaEventRecord(c->ev0, st));
+    WLP_CUDA(launch_plan(model, mode, pa, c->plan_lane.p, c->plan_skip.p, c->mm1_lane.p, c->mm1_skip.p, grid,
+                         tlp_block_size, st));
+    if (report) WLP_CUDA(cudaEventRecord(c->ev1, st));
+    if (!out_on_device) {
+        WLP_CUDA(cudaMemcpyAsync(out0, o0, R * 8, cudaMemcpyDeviceToHost, st));
+        if (model == WLP_MODEL_MM1) {
+            WLP_CUDA(cudaMemcpyAsync(out1, o1, R * 8, cudaMemcpyDeviceToHost, st));
+            WLP_CUDA(cudaMemcpyAsync(out2, o2, R * 8, cudaMemcpyDeviceToHost, st));
+        }
+    }
+    if (report || !out_on_device) WLP_CUDA(cudaStreamSynchronize(st));
+    if (report) {
+        float ms = 0.f;
+        WLP_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+        const int g = mode == WLP_MODE_TLP ? static_cast<int>((R + std::min<int64_t>(R, tlp_block_size) - 1) /
+                                                              std::min<int64_t>(R, tlp_block_size))
+                                           : grid;
+        fill_report(*c, model, mode, tlp_block_size, R, g, ms, report);
     }
     return WLP_OK;
 }
