@@ -131,7 +131,7 @@ def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or "LOCAL_RANK" in os.environ:  # under torchrun: always the NCCL path
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
@@ -395,9 +395,9 @@ def main():
         line["cpu_baseline"] = {k: v for k, v in cpu_baseline(0, p).items() if k != "step_s"}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
-        import torch.distributed as dist
+    import torch.distributed as dist
 
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

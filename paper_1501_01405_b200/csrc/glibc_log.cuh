@@ -147,6 +147,42 @@ WLP_HD uint64_t one_minus_u32_bits(uint32_t n) {
     return (static_cast<uint64_t>(hi) << 32) | static_cast<uint64_t>(frac << 20);
 }
 
+#if defined(__CUDACC__)
+// Device fast forms (same values, fewer instructions):
+// x = 1 - n*2^-32 exactly as (2^20 + m*2^-32) - 2^20 with m = 2^32 - n: in [2^20, 2^21) the
+// ulp is 2^-32, so the bit pattern (0x413 exponent, mantissa m) is built directly and one
+// exact subtraction normalises it.
+__device__ __forceinline__ double one_minus_u32_dev(uint32_t n) {
+    const int hi = 0x41300000 + (n == 0u ? 1 : 0);
+    return __dsub_rn(__hiloint2double(hi, static_cast<int>(0u - n)), 0x1p20);
+}
+
+// The near-one window and OFF have zero low words, so the tests and the table-path
+// decomposition only touch the high word of x.
+__device__ __forceinline__ bool near_one_dev(double x) {
+    return static_cast<uint32_t>(__double2hiint(x)) - 0x3FEE0000u < 0x00030900u;
+}
+
+__device__ __forceinline__ double log_table_dev(double x, const double* tab) {
+    const uint32_t hx = static_cast<uint32_t>(__double2hiint(x));
+    const uint32_t thi = hx - 0x3fe60000u;  // high word of ix - OFF
+    const int i = static_cast<int>((thi >> 13) & 127u);
+    const int k = static_cast<int>(thi) >> 20;
+    const double z = __hiloint2double(static_cast<int>(hx - (thi & 0xfff00000u)), __double2loint(x));
+    const double2 c = reinterpret_cast<const double2*>(tab)[i];  // {invc, logc}
+    const double kd = static_cast<double>(k);
+    constexpr double A[5] = WLP_LOG_POLY_INIT;
+    const double r = __fma_rn(z, c.x, -1.0);
+    const double w = __fma_rn(kd, WLP_LOG_LN2HI, c.y);
+    const double hi = __dadd_rn(r, w);
+    const double lo = __fma_rn(kd, WLP_LOG_LN2LO, __dadd_rn(__dsub_rn(w, hi), r));
+    const double r2 = __dmul_rn(r, r);
+    const double q = __fma_rn(__fma_rn(r, A[4], A[3]), r2, __fma_rn(r, A[2], A[1]));
+    const double y = __fma_rn(__dmul_rn(r, r2), q, __fma_rn(r2, A[0], lo));
+    return __dadd_rn(y, hi);
+}
+#endif
+
 // -log(1 - n*2^-32) for a taus88 output n: the exponential numerator of mm1
 // (models.hpp:67,75). Scalar form (host reference of the batched device routine).
 WLP_HD double neg_log1m_u32_tab(uint32_t n, const double* tab) {

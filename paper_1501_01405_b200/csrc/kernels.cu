@@ -166,23 +166,23 @@ constexpr int kExpoB = 8;  // log inputs per lane per batch
 
 struct NearList {  // per-warp compaction scratch
     uint32_t n[32 * kExpoB];
-    uint16_t dst[32 * kExpoB];
 };
 
-// -log(1 - n*2^-32) for every lane's B inputs. Near-one results are written by the lane
-// that evaluates them into out[dst] when `direct` (the WLP panel buffer), else returned
-// through res[] and picked up by the owner.
-template <int B>
+// -log(1 - n*2^-32) for every lane's B inputs. The near-one inputs are listed in nl, each
+// evaluated by one lane into res[pos], and picked up by their owner. FULL: all 32 lanes
+// take part (no divergence checks); else `mask_` names the lanes of a partial warp.
+template <int B, bool FULL>
 __device__ __forceinline__ void neg_log1m_batch(const uint32_t (&n)[B], double (&e)[B], const double* tab,
-                                                NearList& nl, double* res, unsigned mask, int lane) {
+                                                NearList& nl, double* res, unsigned mask_, int lane) {
+    const unsigned mask = FULL ? kFull : mask_;
     int pos[B];
     int total = 0;
     const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
     for (int j = 0; j < B; ++j) {
-        const uint64_t ix = one_minus_u32_bits(n[j]);
-        const bool near = log_is_near_one(ix);
-        e[j] = -log_table(ix, tab);
+        const double x = one_minus_u32_dev(n[j]);
+        const bool near = near_one_dev(x);
+        e[j] = -log_table_dev(x, tab);
         const unsigned b = __ballot_sync(mask, near);
         pos[j] = near ? total + __popc(b & lt) : -1;
         if (near) nl.n[pos[j]] = n[j];
@@ -190,10 +190,10 @@ __device__ __forceinline__ void neg_log1m_batch(const uint32_t (&n)[B], double (
     }
     if (total == 0) return;  // warp-uniform
     __syncwarp(mask);
-    const int width = __popc(mask);
+    const int width = FULL ? 32 : __popc(mask);
     for (int p = lane; p < total; p += width) {
-        const uint64_t ix = one_minus_u32_bits(nl.n[p]);
-        res[p] = ix == kOneBits ? -0.0 : -log_near_one(wlp_as_f64(ix));
+        const uint32_t v = nl.n[p];
+        res[p] = v == 0u ? -0.0 : -log_near_one(one_minus_u32_dev(v));
     }
     __syncwarp(mask);
 #pragma unroll
@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(kLogHookBlock) k_neg_log1m(const uint32_t* __r
     double e[kExpoB];
 #pragma unroll
     for (int j = 0; j < kExpoB; ++j) in[j] = base + j < n ? k[base + j] : 0u;
-    neg_log1m_batch<kExpoB>(in, e, tab, nl[w], res[w], kFull, lane);
+    neg_log1m_batch<kExpoB, true>(in, e, tab, nl[w], res[w], kFull, lane);
 #pragma unroll
     for (int j = 0; j < kExpoB; ++j)
         if (base + j < n) out[base + j] = e[j];
@@ -397,8 +397,9 @@ __global__ void __launch_bounds__(kWlpBlock, 3) k_wlp_lanes(RepArgs a, const uin
 // the panel buffer (a and s of 32*T clients) and the near-one compaction list.
 constexpr int kMm1P = 32 * kMm1PanelT;
 struct Mm1Warp {
-    double a[kMm1P];
-    double s[kMm1P];
+    // client-ordered {a, s} pairs, lane l's T clients at [l*(T+1), l*(T+1)+T) (one pad
+    // slot per lane segment spreads the lanes' STS.128 over the banks)
+    double2 pair[32 * (kMm1PanelT + 1)];
     NearList nl;
 };
 constexpr size_t kMm1Smem =
@@ -426,7 +427,7 @@ __device__ __forceinline__ Queue mm1_warp_rep(Taus st, int64_t n, double lambda,
             double e[kExpoB];
 #pragma unroll
             for (int j = 0; j < kExpoB; ++j) d[j] = taus_next(st);
-            neg_log1m_batch<kExpoB>(d, e, logtab, W.nl, W.a, kFull, lane);
+            neg_log1m_batch<kExpoB, true>(d, e, logtab, W.nl, reinterpret_cast<double*>(W.pair), kFull, lane);
 #pragma unroll
             for (int j = 0; j < kExpoB; j += 2) {
                 ea[(h + j) / 2] = scale<INV>(e[j], lambda, inv_l);
@@ -434,17 +435,24 @@ __device__ __forceinline__ Queue mm1_warp_rep(Taus st, int64_t n, double lambda,
             }
         }
 #pragma unroll
-        for (int c = 0; c < T; ++c) {
-            W.a[c * 32 + lane] = ea[c];
-            W.s[c * 32 + lane] = es[c];
-        }
+        for (int c = 0; c < T; ++c) W.pair[lane * (T + 1) + c] = make_double2(ea[c], es[c]);
         __syncwarp();
-        if (lane == 0) {
+        if (lane == 0) {  // the order-preserving recursion, 8 clients per unrolled step
             const int64_t left = n - base;
-            const int cnt = left < P ? static_cast<int>(left) : P;
-            for (int c = 0; c < cnt; ++c) {
-                const int idx = (c % T) * 32 + c / T;
-                q.client(W.a[idx], W.s[idx]);
+            if (left >= P) {
+                const double2* p = W.pair;
+                for (int seg = 0; seg < 32; ++seg, p += T + 1) {
+                    double2 v[T];
+#pragma unroll
+                    for (int j = 0; j < T; ++j) v[j] = p[j];
+#pragma unroll
+                    for (int j = 0; j < T; ++j) q.client(v[j].x, v[j].y);
+                }
+            } else {
+                for (int c = 0; c < static_cast<int>(left); ++c) {
+                    const double2 v = W.pair[(c / T) * (T + 1) + c % T];
+                    q.client(v.x, v.y);
+                }
             }
         }
         __syncwarp();
@@ -557,7 +565,7 @@ struct TlpMm1Warp {
     double res[32 * kExpoB];
 };
 
-template <bool INV>
+template <bool INV, bool FULL>
 __device__ __forceinline__ Queue mm1_thread_rep(Taus st, int64_t n, int64_t n_warp, double lambda, double mu,
                                                 double inv_l, double inv_m, const double* logtab, TlpMm1Warp& W,
                                                 unsigned mask, int lane) {
@@ -567,7 +575,7 @@ __device__ __forceinline__ Queue mm1_thread_rep(Taus st, int64_t n, int64_t n_wa
         double e[kExpoB];
 #pragma unroll
         for (int j = 0; j < kExpoB; ++j) d[j] = taus_next(st);
-        neg_log1m_batch<kExpoB>(d, e, logtab, W.nl, W.res, mask, lane);
+        neg_log1m_batch<kExpoB, FULL>(d, e, logtab, W.nl, W.res, mask, lane);
         const int64_t left = n - done;
         const int cnt = left <= 0 ? 0 : (left < kExpoB / 2 ? static_cast<int>(left) : kExpoB / 2);
 #pragma unroll
@@ -593,8 +601,11 @@ __global__ void k_tlp_mm1(RepArgs a) {
     const int lane = threadIdx.x & 31;
     const bool live = r < a.count;
     const Taus st = live ? load_seed(a, r) : Taus{2u, 8u, 16u};  // tail threads: dummy stream
-    const Queue q = mm1_thread_rep<INV>(st, a.n, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu, logtab, W,
-                                        block_lane_mask(), lane);
+    const unsigned mask = block_lane_mask();
+    const Queue q = mask == kFull ? mm1_thread_rep<INV, true>(st, a.n, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu,
+                                                              logtab, W, mask, lane)
+                                  : mm1_thread_rep<INV, false>(st, a.n, a.n, a.lambda, a.mu, a.inv_lambda,
+                                                               a.inv_mu, logtab, W, mask, lane);
     if (!live) return;
     const double nd = static_cast<double>(a.n);
     a.out0[r] = __ddiv_rn(q.idle, nd);
@@ -706,7 +717,9 @@ __global__ void k_plan_tlp_mm1(PlanArgs a) {
     const int64_t n_warp = static_cast<int64_t>(__reduce_max_sync(mask, static_cast<unsigned>(n)));
     const Taus st = live ? plan_seed(a, r) : Taus{2u, 8u, 16u};
     // per-lane rates differ across sets: always divide unless the lane's rates are 2^k
-    const Queue q = mm1_thread_rep<false>(st, n, n_warp, S.lambda, S.mu, 0.0, 0.0, logtab, W, mask, lane);
+    const Queue q = mask == kFull
+                        ? mm1_thread_rep<false, true>(st, n, n_warp, S.lambda, S.mu, 0.0, 0.0, logtab, W, mask, lane)
+                        : mm1_thread_rep<false, false>(st, n, n_warp, S.lambda, S.mu, 0.0, 0.0, logtab, W, mask, lane);
     if (!live) return;
     const double nd = static_cast<double>(S.n);
     a.out0[r] = __ddiv_rn(q.idle, nd);

@@ -57,17 +57,18 @@ class _Comm:
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.device = device or ("cuda" if dist.is_initialized() and dist.get_backend(group) == "nccl" else "cpu")
+        self.active = dist.is_initialized()  # collectives run even at world size 1 (exercises NCCL)
 
     def gather_f64(self, vals: Sequence[float]) -> np.ndarray:
         t = self.torch.tensor(list(vals), dtype=self.torch.float64, device=self.device)
-        if self.world == 1:
+        if not self.active:
             return t.cpu().numpy()[None, :]
         out = [self.torch.empty_like(t) for _ in range(self.world)]
         self.dist.all_gather(out, t, group=self.group)
         return self.torch.stack(out).cpu().numpy()
 
     def gather_specials(self, sp: Sequence[Special]) -> List[Special]:
-        if self.world == 1:
+        if not self.active:
             return list(sp)
         n = len(sp)
         flags = self.gather_i64([n])
@@ -89,7 +90,7 @@ class _Comm:
 
     def gather_i64(self, vals) -> np.ndarray:
         t = self.torch.tensor(np.asarray(vals, dtype=np.int64), device=self.device)
-        if self.world == 1:
+        if not self.active:
             return t.cpu().numpy()[None, :]
         out = [self.torch.empty_like(t) for _ in range(self.world)]
         self.dist.all_gather(out, t, group=self.group)
