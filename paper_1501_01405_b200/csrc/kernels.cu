@@ -354,9 +354,19 @@ __global__ void __launch_bounds__(kLogHookBlock) k_neg_log1m(const uint32_t* __r
 // WLP: one replication per warp
 // ---------------------------------------------------------------------------------
 
-// Warp w of the persistent grid owns replications [w*R/W, (w+1)*R/W) (every replication
-// costs the same, so a static split is balanced). Results are parked in lane
-// (r - lo) % 32 and stored 32 at a time (coalesced 256 B).
+// Work distribution of the persistent WLP grids: a warp takes a.grab consecutive
+// replications from a global counter (lane 0's atomic is issued one group ahead, so its
+// latency hides behind the current group). Static splits left a tail: the issue arbiter
+// favours some warps, which then finish long before the others. Results of a group are
+// parked in lanes 0..grab-1 and stored together (coalesced).
+__device__ __forceinline__ unsigned long long grab_issue(const RepArgs& a, int lane) {
+    return lane == 0 ? atomicAdd(a.next, static_cast<unsigned long long>(a.grab)) : 0ull;
+}
+
+__device__ __forceinline__ int64_t grab_take(unsigned long long ticket) {
+    return static_cast<int64_t>(__shfl_sync(kFull, ticket, 0));
+}
+
 template <int MODEL>
 __global__ void __launch_bounds__(kWlpBlock, 3) k_wlp_lanes(RepArgs a, const uint32_t* __restrict__ gtab,
                                                              int64_t K) {
@@ -364,32 +374,32 @@ __global__ void __launch_bounds__(kWlpBlock, 3) k_wlp_lanes(RepArgs a, const uin
     stage_u32<kLaneTabWords>(tab, gtab);
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    const int64_t lo = warp * a.count / nwarps, hi = (warp + 1) * a.count / nwarps;
     int64_t mine = a.n - static_cast<int64_t>(lane) * K;
     mine = mine < 0 ? 0 : (mine > K ? K : mine);
     const uint32_t units = static_cast<uint32_t>(mine);
     const bool wide = a.n >= (int64_t(1) << 31);
-    double keep = 0.0;
-    for (int64_t r = lo; r < hi; ++r) {
-        Taus st = lane_jump(tab, lane, load_seed(a, r));
-        double val;
-        if (MODEL == 0) {  // pi: count points inside the quarter circle
-            const uint32_t hits = pi_hits(st, units);
-            const int64_t total = wide ? warp_sum_i64(hits) : static_cast<int64_t>(__reduce_add_sync(kFull, hits));
-            // c counts exactly in a double, so (4.0*c)/draws is the reference's value.
-            val = __ddiv_rn(__dmul_rn(4.0, static_cast<double>(total)), static_cast<double>(a.n));
-        } else {  // walk: only the x displacement reaches the output
-            const int dx = walk_dx(st, units);
-            const int64_t total = wide ? warp_sum_i64(dx) : static_cast<int64_t>(__reduce_add_sync(kFull, dx));
-            val = walk_fold(total, a.chunks);
+    for (int64_t base = grab_take(grab_issue(a, lane)); base < a.count;) {
+        const unsigned long long ticket = grab_issue(a, lane);  // next group, in flight
+        const int64_t end = base + a.grab < a.count ? base + a.grab : a.count;
+        double keep = 0.0;
+        for (int64_t r = base; r < end; ++r) {
+            Taus st = lane_jump(tab, lane, load_seed(a, r));
+            double val;
+            if (MODEL == 0) {  // pi: count points inside the quarter circle
+                const uint32_t hits = pi_hits(st, units);
+                const int64_t total =
+                    wide ? warp_sum_i64(hits) : static_cast<int64_t>(__reduce_add_sync(kFull, hits));
+                // c counts exactly in a double, so (4.0*c)/draws is the reference's value.
+                val = __ddiv_rn(__dmul_rn(4.0, static_cast<double>(total)), static_cast<double>(a.n));
+            } else {  // walk: only the x displacement reaches the output
+                const int dx = walk_dx(st, units);
+                const int64_t total = wide ? warp_sum_i64(dx) : static_cast<int64_t>(__reduce_add_sync(kFull, dx));
+                val = walk_fold(total, a.chunks);
+            }
+            if (lane == static_cast<int>(r - base)) keep = val;
         }
-        const int slot = static_cast<int>((r - lo) & 31);
-        if (lane == slot) keep = val;
-        if (slot == 31 || r == hi - 1) {
-            if (lane <= slot) a.out0[r - slot + lane] = keep;
-        }
+        if (lane < end - base) a.out0[base + lane] = keep;
+        base = grab_take(ticket);
     }
 }
 
@@ -487,31 +497,30 @@ __global__ void __launch_bounds__(kMm1Block) k_wlp_mm1(RepArgs a, const uint32_t
                                                         const uint32_t* __restrict__ gskip) {
     const Mm1Smem m = mm1_stage(gtab, gskip);
     const int lane = threadIdx.x & 31;
-    const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    const int64_t lo = warp * a.count / nwarps, hi = (warp + 1) * a.count / nwarps;
-    double k0 = 0.0, k1 = 0.0, k2 = 0.0;
-    for (int64_t r = lo; r < hi; ++r) {
-        const Taus st = lane_jump(m.tab, lane, load_seed(a, r));
-        const Queue q = mm1_warp_rep<INV>(st, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu, m.logtab, m.skip, *m.W,
-                                          lane);
-        const double nd = static_cast<double>(a.n);
-        const double v0 = __shfl_sync(kFull, __ddiv_rn(q.idle, nd), 0);
-        const double v1 = __shfl_sync(kFull, __ddiv_rn(q.sumw, nd), 0);
-        const double v2 = __shfl_sync(kFull, __ddiv_rn(q.sums, nd), 0);
-        const int slot = static_cast<int>((r - lo) & 31);
-        if (lane == slot) {
-            k0 = v0;
-            k1 = v1;
-            k2 = v2;
-        }
-        if (slot == 31 || r == hi - 1) {
-            if (lane <= slot) {
-                a.out0[r - slot + lane] = k0;
-                a.out1[r - slot + lane] = k1;
-                a.out2[r - slot + lane] = k2;
+    for (int64_t base = grab_take(grab_issue(a, lane)); base < a.count;) {
+        const unsigned long long ticket = grab_issue(a, lane);
+        const int64_t end = base + a.grab < a.count ? base + a.grab : a.count;
+        double k0 = 0.0, k1 = 0.0, k2 = 0.0;
+        for (int64_t r = base; r < end; ++r) {
+            const Taus st = lane_jump(m.tab, lane, load_seed(a, r));
+            const Queue q = mm1_warp_rep<INV>(st, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu, m.logtab, m.skip,
+                                              *m.W, lane);
+            const double nd = static_cast<double>(a.n);
+            const double v0 = __shfl_sync(kFull, __ddiv_rn(q.idle, nd), 0);
+            const double v1 = __shfl_sync(kFull, __ddiv_rn(q.sumw, nd), 0);
+            const double v2 = __shfl_sync(kFull, __ddiv_rn(q.sums, nd), 0);
+            if (lane == static_cast<int>(r - base)) {
+                k0 = v0;
+                k1 = v1;
+                k2 = v2;
             }
         }
+        if (lane < end - base) {
+            a.out0[base + lane] = k0;
+            a.out1[base + lane] = k1;
+            a.out2[base + lane] = k2;
+        }
+        base = grab_take(ticket);
     }
 }
 
@@ -792,6 +801,9 @@ size_t tlp_mm1_smem(int block) { return 256 * 8 + static_cast<size_t>((block + 3
 template <class K>
 void allow_smem(K kernel, size_t bytes) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+    // the persistent grids are sized by the occupancy API, which assumes the largest
+    // shared-memory carveout; ask for it so every planned block is resident at once
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 
 }  // namespace

@@ -19,6 +19,10 @@ struct RepArgs {
     double* out0;
     double* out1;
     double* out2;
+    // WLP: warps take `grab` consecutive replications at a time from *next (zeroed
+    // before launch), so warps the arbiter favours do not leave a tail behind them
+    unsigned long long* next = nullptr;
+    int grab = 1;
 };
 
 // Seeding: stream slots [slot_begin, slot_begin+count) of a run.

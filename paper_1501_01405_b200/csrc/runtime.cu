@@ -91,6 +91,9 @@ struct DevCtx {
     DevBuf<uint32_t> plan_lane, plan_skip;
     int plan_bps[3] = {1, 1, 1};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t done = nullptr;  // end of the last library work (cross-stream ordering)
+    cudaStream_t last_stream = nullptr;
+    bool last_used = false;
 };
 
 std::mutex g_ctx_mu;
@@ -120,6 +123,7 @@ int ctx_init(DevCtx& c) {
     WLP_CUDA(c.work.ensure(1));
     WLP_CUDA(cudaEventCreate(&c.ev0));
     WLP_CUDA(cudaEventCreate(&c.ev1));
+    WLP_CUDA(cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming));
     WLP_CUDA(cudaGetLastError());
     c.ready = true;
     return WLP_OK;
@@ -149,6 +153,22 @@ int acquire(DevCtx*& out, std::unique_lock<std::mutex>& lk) {
     out = c;
     return WLP_OK;
 }
+
+// The device scratch (seed keys, work counter, specials) is shared by every call on a
+// device. Calls on one stream are ordered by the stream; a call on a different stream
+// first waits for the last library work, and every call records its end.
+struct StreamOrder {
+    DevCtx& c;
+    cudaStream_t st;
+    StreamOrder(DevCtx& ctx, cudaStream_t s) : c(ctx), st(s) {
+        if (c.last_used && c.last_stream != st) cudaStreamWaitEvent(st, c.done, 0);
+    }
+    ~StreamOrder() {
+        cudaEventRecord(c.done, st);
+        c.last_stream = st;
+        c.last_used = true;
+    }
+};
 
 int64_t units_of(int model, const wlp_params& p) {
     return model == WLP_MODEL_PI ? p.draws : model == WLP_MODEL_MM1 ? p.clients : p.steps;
@@ -392,6 +412,10 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
     // WLP, and SEQUENTIAL (replication order is irrelevant to the per-replication result;
     // the engine has no host execution path).
     grid_out = wlp_grid(c, model, count);
+    const int64_t warps = static_cast<int64_t>(grid_out) * ((model == WLP_MODEL_MM1 ? kMm1Block : kWlpBlock) / 32);
+    a.grab = static_cast<int>(std::clamp<int64_t>(count / (warps * 32), 1, 32));  // ~32 grabs per warp
+    a.next = c.work.p;
+    WLP_CUDA(cudaMemsetAsync(c.work.p, 0, sizeof(unsigned long long), st));
     if (model == WLP_MODEL_MM1) {
         WLP_CUDA(launch_wlp(model, a, c.mm1_lane.p, c.mm1_skip.p, 0, grid_out, st));
     } else {
@@ -572,6 +596,7 @@ int wlp_taus_stream(uint32_t s1, uint32_t s2, uint32_t s3, int64_t n, uint32_t* 
     std::unique_lock<std::mutex> lk;
     WLP_TRY(acquire(c, lk));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamOrder so(*c, st);
     uint32_t* d = out;
     if (!out_on_device) {
         WLP_CUDA(c->seeds.ensure(std::max<int64_t>(n, 1)));
@@ -591,6 +616,7 @@ int wlp_debug_neg_log1m(const uint32_t* k, int64_t n, double* out) {
     DevCtx* c;
     std::unique_lock<std::mutex> lk;
     WLP_TRY(acquire(c, lk));
+    StreamOrder so(*c, nullptr);
     WLP_CUDA(c->in_seeds.ensure(n));
     WLP_CUDA(c->outs.ensure(n));
     WLP_CUDA(cudaMemcpy(c->in_seeds.p, k, n * 4, cudaMemcpyHostToDevice));
@@ -607,6 +633,7 @@ int wlp_seed_streams(uint64_t master_seed, int64_t slot_begin, int64_t count, co
     std::unique_lock<std::mutex> lk;
     WLP_TRY(acquire(c, lk));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamOrder so(*c, st);
     uint32_t* d = s_out;
     if (!out_on_device) {
         WLP_CUDA(c->seeds.ensure(3 * std::max<int64_t>(count, 1)));
@@ -636,6 +663,7 @@ int seed_exact(Taus master, int64_t count, uint32_t* s_out, int out_on_device, v
     std::unique_lock<std::mutex> lk;
     WLP_TRY(acquire(c, lk));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamOrder so(*c, st);
     uint32_t* d = s_out;
     if (!out_on_device) {
         WLP_CUDA(c->seeds.ensure(3 * std::max<int64_t>(count, 1)));
@@ -692,6 +720,7 @@ int wlp_run_streams(int model, const wlp_params* p, int mode, const uint32_t* s,
     std::unique_lock<std::mutex> lk;
     WLP_TRY(acquire(c, lk));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamOrder so(*c, st);
     const uint32_t* ds = s;
     if (!s_on_device) {
         WLP_CUDA(c->in_seeds.ensure(3 * count));
@@ -742,6 +771,7 @@ int wlp_run_shard(int model, const wlp_params* p, int mode, uint64_t master_seed
     std::unique_lock<std::mutex> lk;
     WLP_TRY(acquire(c, lk));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamOrder so(*c, st);
     WLP_CUDA(c->seeds.ensure(3 * r_count));
     double *o0 = out0, *o1 = out1, *o2 = out2;
     if (!out_on_device) {
@@ -792,6 +822,7 @@ int wlp_run(int model, const wlp_params* p, int mode, uint64_t master_seed, int 
     std::unique_lock<std::mutex> lk;
     WLP_TRY(acquire(c, lk));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamOrder so(*c, st);
     WLP_CUDA(c->seeds.ensure(3 * R));
     double *o0 = out0, *o1 = out1, *o2 = out2;
     if (!out_on_device) {
@@ -866,6 +897,7 @@ int wlp_run_plan(int model, const wlp_params* sets, const uint64_t* master_seeds
     std::unique_lock<std::mutex> lk;
     WLP_TRY(acquire(c, lk));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamOrder so(*c, st);
     WLP_CUDA(c->seeds.ensure(3 * R));
     WLP_CUDA(c->jobs.ensure(n_sets));
     WLP_CUDA(c->setp.ensure(n_sets));
@@ -961,6 +993,7 @@ int wlp_stats_device(const double* x, int64_t n, int pass, wlp_stats* stats, voi
     DevCtx* c;
     std::unique_lock<std::mutex> lk;
     WLP_TRY(acquire(c, lk));
+    StreamOrder so(*c, static_cast<cudaStream_t>(stream));
     return stats_device(*c, x, n, pass, stats, static_cast<cudaStream_t>(stream));
 }
 
@@ -970,6 +1003,7 @@ int wlp_confidence_interval(const double* samples, int64_t n, double level, wlp_
     DevCtx* c;
     std::unique_lock<std::mutex> lk;
     WLP_TRY(acquire(c, lk));
+    StreamOrder so(*c, nullptr);
     WLP_CUDA(c->stats_in.ensure(n));
     WLP_CUDA(cudaMemcpy(c->stats_in.p, samples, n * 8, cudaMemcpyHostToDevice));
     return ci_device(*c, c->stats_in.p, n, level, ci, nullptr);
@@ -999,7 +1033,14 @@ int wlp_shutdown(void) {
     c.rejected.release();
     if (c.ev0) cudaEventDestroy(c.ev0);
     if (c.ev1) cudaEventDestroy(c.ev1);
-    c.ev0 = c.ev1 = nullptr;
+    if (c.done) cudaEventDestroy(c.done);
+    c.ev0 = c.ev1 = c.done = nullptr;
+    c.last_used = false;
+    c.work.release();
+    c.jobs.release();
+    c.setp.release();
+    c.plan_lane.release();
+    c.plan_skip.release();
     c.ready = false;
     return WLP_OK;
 }
