@@ -107,14 +107,14 @@ __device__ __forceinline__ uint32_t pi_hits(Taus& st, uint32_t units) {
     for (; u + 4 <= units; u += 4) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const uint32_t x = taus_next(st);
-            const uint32_t y = taus_next(st);
+            uint32_t x, y;
+            taus_next2(st, x, y);
             if (pi_inside(x, y)) ++hits;
         }
     }
     for (; u < units; ++u) {
-        const uint32_t x = taus_next(st);
-        const uint32_t y = taus_next(st);
+        uint32_t x, y;
+        taus_next2(st, x, y);
         if (pi_inside(x, y)) ++hits;
     }
     return hits;

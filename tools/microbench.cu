@@ -52,6 +52,50 @@ __global__ void k_mixed_taus(uint32_t* out, uint32_t seed) {  // the real taus88
     if (acc == 0x12345) out[0] = acc;
 }
 
+// taus88 with some components rebalanced onto the FMA pipe: the right shift as
+// mul.hi by 2^(32-r) and the final merge as mad (operands from kernel params so ptxas
+// cannot turn them back into SHF/LEA). variant bit c set = component c rebalanced.
+struct Mul {
+    uint32_t hi[3], sh[3];
+};
+__device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t mad(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+template <int V>
+__global__ void k_taus_rebal(uint32_t* out, uint32_t seed, Mul mm) {
+    uint32_t s1[4], s2[4], s3[4], acc = 0;
+    for (int i = 0; i < 4; ++i) {
+        s1[i] = seed * (i + 3) + threadIdx.x;
+        s2[i] = seed * (i + 7) ^ threadIdx.x;
+        s3[i] = seed + i * 977 + threadIdx.x * 31;
+    }
+    for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (V & 1)
+                s1[i] = mad(s1[i] & 0xFFFFFFFEu, mm.sh[0], mulhi((s1[i] << 13) ^ s1[i], mm.hi[0]));
+            else
+                s1[i] = ((s1[i] & 0xFFFFFFFEu) << 12) ^ (((s1[i] << 13) ^ s1[i]) >> 19);
+            if (V & 2)
+                s2[i] = mad(s2[i] & 0xFFFFFFF8u, mm.sh[1], mulhi((s2[i] << 2) ^ s2[i], mm.hi[1]));
+            else
+                s2[i] = ((s2[i] & 0xFFFFFFF8u) << 4) ^ (((s2[i] << 2) ^ s2[i]) >> 25);
+            if (V & 4)
+                s3[i] = mad(s3[i] & 0xFFFFFFF0u, mm.sh[2], mulhi((s3[i] << 3) ^ s3[i], mm.hi[2]));
+            else
+                s3[i] = ((s3[i] & 0xFFFFFFF0u) << 17) ^ (((s3[i] << 3) ^ s3[i]) >> 11);
+            acc += s1[i] ^ s2[i] ^ s3[i];
+        }
+    if (acc == 0x12345) out[0] = acc;
+}
+
 __global__ void k_dadd(double* out, double seed) {
     double a[8];
     for (int i = 0; i < 8; ++i) a[i] = seed + threadIdx.x + i;
@@ -159,6 +203,16 @@ int main() {
     report("I2F.F64.U32", time_it([&] { k_i2f64<<<blocks, threads>>>(dd, 1); }), 8);
     // taus88: 4 streams x (16 SASS per draw) + acc add per draw
     report("taus88 draw (16 SASS+1)", time_it([&] { k_mixed_taus<<<blocks, threads>>>(du, 7); }), 4 * 17);
+    Mul mm{{1u << 13, 1u << 7, 1u << 21}, {1u << 12, 1u << 4, 1u << 17}};
+    // same draws per launch as above: report as draws/clk relative (warp-instr count of the
+    // reference form, 17 per draw, so the numbers compare directly)
+    report("taus rebal comp1", time_it([&] { k_taus_rebal<1><<<blocks, threads>>>(du, 7, mm); }), 4 * 17);
+    report("taus rebal comp2", time_it([&] { k_taus_rebal<2><<<blocks, threads>>>(du, 7, mm); }), 4 * 17);
+    report("taus rebal comp3", time_it([&] { k_taus_rebal<4><<<blocks, threads>>>(du, 7, mm); }), 4 * 17);
+    report("taus rebal comp2+3", time_it([&] { k_taus_rebal<6><<<blocks, threads>>>(du, 7, mm); }), 4 * 17);
+    report("taus rebal comp1+2", time_it([&] { k_taus_rebal<3><<<blocks, threads>>>(du, 7, mm); }), 4 * 17);
+    report("taus rebal all", time_it([&] { k_taus_rebal<7><<<blocks, threads>>>(du, 7, mm); }), 4 * 17);
+    report("taus rebal none", time_it([&] { k_taus_rebal<0><<<blocks, threads>>>(du, 7, mm); }), 4 * 17);
     (void)warp_instr;
     return 0;
 }
