@@ -101,6 +101,7 @@ __device__ __forceinline__ bool pi_inside(uint32_t a, uint32_t b) {
     return __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)) <= 0x1p64;
 }
 
+
 // Hits among `units` consecutive points of a stream (main loop unrolled by 4).
 __device__ __forceinline__ uint32_t pi_hits(Taus& st, uint32_t units) {
     uint32_t hits = 0, u = 0;
@@ -120,23 +121,35 @@ __device__ __forceinline__ uint32_t pi_hits(Taus& st, uint32_t units) {
     return hits;
 }
 
-// x displacement of `units` consecutive walk steps (direction = floor(4u) = out >> 30,
-// second draw of each step discarded, models.hpp:93-104).
-__device__ __forceinline__ int walk_dx(Taus& st, uint32_t units) {
-    int dx = 0;
+// x displacement of `units` consecutive walk steps (direction d = floor(4u) = out >> 30,
+// second draw of each step discarded, models.hpp:93-104): dx = #(d==0) - #(d==1). Per
+// step we add the cubic q(d) = -4d^3 + 21d^2 - 29d (= 6*([d==0]-[d==1]) - 6 on {0..3}) by
+// Horner in three IMADs (FMA pipe) instead of compares and selects (ALU pipe); then
+// dx = (sum q + 6*units) / 6 exactly. |sum| <= 12*units < 2^31 for units < 2^27.
+__device__ __forceinline__ int walk_dx_block(Taus& st, uint32_t units) {
+    int acc = 0;
     uint32_t u = 0;
     for (; u + 4 <= units; u += 4) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const uint32_t d = taus_next_skip1(st) >> 30;
-            dx += static_cast<int>(d == 0u) - static_cast<int>(d == 1u);
+            const int d = static_cast<int>(taus_next_skip1(st) >> 30);
+            acc += (((21 - 4 * d) * d) - 29) * d;
         }
     }
     for (; u < units; ++u) {
-        const uint32_t d = taus_next_skip1(st) >> 30;
-        dx += static_cast<int>(d == 0u) - static_cast<int>(d == 1u);
+        const int d = static_cast<int>(taus_next_skip1(st) >> 30);
+        acc += (((21 - 4 * d) * d) - 29) * d;
     }
-    return dx;
+    return (acc + 6 * static_cast<int>(units)) / 6;
+}
+
+__device__ __forceinline__ int walk_dx(Taus& st, uint32_t units) {
+    int dx = 0;
+    while (units > (1u << 24)) {
+        dx += walk_dx_block(st, 1u << 24);
+        units -= 1u << 24;
+    }
+    return dx + walk_dx_block(st, units);
 }
 
 __device__ __forceinline__ int64_t warp_sum_i64(int64_t v) {
