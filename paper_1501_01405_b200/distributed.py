@@ -120,24 +120,49 @@ def run_sharded(model: ModelKind, R: int, runner: Callable, stats: Callable, *, 
     """
     comm = comm or _Comm()
     begin, count = shard_range(R, comm.world, comm.rank)
+    nout = len(OUTPUT_NAMES[ModelKind(model)])
     rejected: List[int] = []
     rounds = 0
+    # Exchange 1 carries the shard's special candidates AND its pass-1 statistics (one
+    # all_gather); a rejection (astronomically rare) discards the round and re-runs.
     while True:
         rounds += 1
         outputs, specials = runner(begin, count, rejected)
-        allsp = comm.gather_specials(specials)
+        firsts = [stats(out, 1, 0.0) for out in outputs[:nout]]
+        if len(specials) > SPECIAL_SLOTS:
+            allsp = comm.gather_specials(specials)
+            rows = comm.gather_f64([v for s in firsts for v in (s.n, s.sum_hi, s.sum_lo)])
+        else:
+            buf = [float(len(specials))] + [0.0] * (4 * SPECIAL_SLOTS)
+            for j, s in enumerate(specials):
+                buf[1 + 4 * j: 5 + 4 * j] = (float(s.index), float(s.s1), float(s.s2), float(s.s3))
+            buf += [v for s in firsts for v in (s.n, s.sum_hi, s.sum_lo)]
+            g = comm.gather_f64(buf)
+            if comm.active and int(g[:, 0].max()) > SPECIAL_SLOTS:  # another rank overflowed
+                allsp = comm.gather_specials(specials)
+            else:
+                allsp = [Special(int(row[1 + 4 * j]), int(row[2 + 4 * j]), int(row[3 + 4 * j]),
+                                 int(row[4 + 4 * j]), 0) for row in g for j in range(int(row[0]))]
+            rows = g[:, 1 + 4 * SPECIAL_SLOTS:]
         nxt = spacing_rejections(allsp, rejected) if len(allsp) >= 2 else list(rejected)
         if nxt == rejected:
             break
         rejected = nxt
+    totals, centers, seconds = [], [], []
+    for k in range(nout):
+        tot = merge_stats(rows[:, 3 * k: 3 * k + 3], 1)
+        totals.append(tot)
+        centers.append((tot.sum_hi + tot.sum_lo) / tot.n)
+    # Exchange 2: centred sums of squares about the global means.
+    for k, out in enumerate(outputs[:nout]):
+        s2 = stats(out, 2, centers[k])
+        seconds += [0.0, s2.ss_hi, s2.ss_lo]
+    g2 = comm.gather_f64(seconds)
     cis = []
-    for out in outputs[: len(OUTPUT_NAMES[ModelKind(model)])]:
-        s1 = stats(out, 1, 0.0)
-        tot = merge_stats(comm.gather_f64([s1.n, s1.sum_hi, s1.sum_lo]), 1)
-        center = (tot.sum_hi + tot.sum_lo) / tot.n
-        s2 = stats(out, 2, center)
-        ss = merge_stats(comm.gather_f64([0, s2.ss_hi, s2.ss_lo]), 2)
-        tot.center = center
+    for k in range(nout):
+        ss = merge_stats(g2[:, 3 * k: 3 * k + 3], 2)
+        tot = totals[k]
+        tot.center = centers[k]
         tot.ss_hi, tot.ss_lo = ss.ss_hi, ss.ss_lo
         cis.append(ci_from_stats(tot, level))
     return ShardResult(outputs, begin, count, cis, rejected, rounds)
@@ -168,7 +193,7 @@ def gpu_runner(model: ModelKind, p, mode, master_seed: int, stream: Optional[int
                              stream=stream, report=rep)
         if rep is not None:
             kernel_ms.append(rep.kernel_ms)
-        return outs, specials
+        return [o[:count] for o in outs], specials
 
     return run
 
@@ -179,6 +204,8 @@ def gpu_stats(stream: Optional[int] = None):
     def st(out, pass_: int, center: float) -> Stats:
         n = out.numel()
         s = Stats(n, 0.0, 0.0, center, 0.0, 0.0)
+        if n == 0:  # an empty shard (more ranks than replications)
+            return s
         return stats_device(out, n, pass_, s, stream)
 
     return st

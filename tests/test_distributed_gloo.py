@@ -27,8 +27,8 @@ def _free_port() -> int:
     return port
 
 
-def _oracle_runner(port, inject_collision: bool):
-    p = oracle.params(**PARAMS)
+def _oracle_runner(port, inject_collision: bool, R: int = R):
+    p = oracle.params(**dict(PARAMS, replications=R))
     cands = port.random_spacing(SEED, R + 16)  # raw candidates (no natural collisions here)
 
     def run(begin, count, rejected):
@@ -56,23 +56,23 @@ def _np_stats(x, pass_, center):
     return w.Stats(len(x), 0.0, 0.0, center, math.fsum((x - center) ** 2), 0.0)
 
 
-def _worker(rank, world, port_no, inject, q):
+def _worker(rank, world, port_no, inject, R_, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         port = oracle.Oracle("port")
-        res = D.run_sharded(MODEL, R, _oracle_runner(port, inject), _np_stats)
+        res = D.run_sharded(MODEL, R_, _oracle_runner(port, inject, R_), _np_stats)
         q.put((rank, res.begin, res.count, [o.tolist() for o in res.outputs],
                [(c.mean, c.halfWidth, c.n) for c in res.cis], res.rejected, res.rounds))
     finally:
         dist.destroy_process_group()
 
 
-def _run(world, inject):
+def _run(world, inject, R_=R):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port_no = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port_no, inject, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port_no, inject, R_, q)) for r in range(world)]
     for p in procs:
         p.start()
     got = sorted(q.get(timeout=120) for _ in procs)
@@ -110,3 +110,15 @@ def test_two_rank_sharded_run(inject):
         assert n == nn and mean == pytest.approx(m, rel=1e-12) and hw == pytest.approx(h, rel=1e-12)
     assert all(g[5] == rejected for g in got)
     assert all(g[6] == (2 if inject else 1) for g in got)
+
+
+def test_more_ranks_than_replications():
+    # 3 ranks, 2 replications: rank 2 holds an empty shard and still joins every exchange
+    got = _run(3, False, R_=2)
+    assert [g[2] for g in got] == [0, 1, 1]
+    port = oracle.Oracle("port")
+    want = port.replications(MODEL, oracle.params(**dict(PARAMS, replications=2)), port.random_spacing(SEED, 2))
+    outs = np.concatenate([np.asarray(g[3][1]) for g in got])
+    assert np.array_equal(outs, want["outWait"])
+    m, h, n, _ = port.confidence_interval(want["outWait"])
+    assert got[0][4][1][2] == n == 2 and got[0][4][1][0] == pytest.approx(m, rel=1e-12)
