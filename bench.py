@@ -54,6 +54,10 @@ SEED = 42
 # 2 exact u32->f64 + 2 DMUL + DADD + DSETP + count = 39; walk step = 2 draws + shift +
 # 2 compare/add = 35.
 INSTR_PER_UNIT = {0: 39, 2: 35}
+# mm1 is FP64-pipe work: per client two exponentials, each 1-u (1) + glibc log (15 fp ops
+# on the table path as compiled in __log_fma, 26 on the near-one path taken 1 time in 16:
+# 15.7 average) + negate/scale (1), plus the Lindley step (6 DADD + 1 compare) = 42.
+FP64_PER_CLIENT = 42
 
 
 def parse():
@@ -370,9 +374,11 @@ def main():
             extras[name] = {}
             for md in (w.ExecutionMode.Wlp, w.ExecutionMode.Tlp):
                 r = model_rate(w, m, pp, md)
+                units_ = pp.replications * pp.units(m)
                 if m in INSTR_PER_UNIT:
-                    units_ = pp.replications * pp.units(m)
                     r["issue_frac"] = units_ * INSTR_PER_UNIT[int(m)] / 32 / (r["kernel_ms"] * 1e-3) / (peak * 1e9)
+                else:  # FP64 pipe: 64 lanes/clk/SM (measured, profiles/round1_microbench.txt)
+                    r["fp64_frac"] = units_ * FP64_PER_CLIENT / (r["kernel_ms"] * 1e-3) / (64 * sms * fmax * 1e6)
                 extras[name][w.mode_name(md)] = r
         # config 5: experimental plan, 64 factor-level sets x 30 replications, one launch
         sets = [w.ModelParams(replications=30, clients=10_000, lambda_=0.1 + 0.8 * k / 63, mu=1.0) for k in range(64)]
