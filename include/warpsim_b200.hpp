@@ -92,8 +92,11 @@ struct DeviceProfile {
     int maxThreadsPerBlock = 1024;
 };
 struct SimOptions {
-    std::optional<std::uint64_t> smPermutationSeed;
-    int maskStackDepth = 32;
+    std::optional<std::uint64_t> smPermutationSeed;  // accepted, ignored (real hardware)
+    int maskStackDepth = 32;                         // accepted, ignored
+    // B200 extension: fill SimReport::divergenceEvents / memReads / memWrites from
+    // instrumented kernels (wlp_set_hw_counters). Off by default: costs some speed.
+    bool hardwareCounters = false;
 };
 struct SimReport {
     std::int64_t totalCycles = 0;

@@ -108,6 +108,17 @@ typedef struct wlp_special {
 const char* wlp_last_error(void);   /* message of the last failing call on this thread */
 int wlp_version(void);              /* ABI version (1)                                  */
 
+/* Hardware counters for the SimReport of later calls on this thread (enable != 0): the
+ * replication kernels run instrumented variants and wlp_report gets
+ *   divergence_events — warp-level splits of the model's data-dependent `if`s, counted
+ *                       with the reference's event definition (warp_exec.cpp:272-284):
+ *                       the TLP walk's 3 nested direction ifs, the TLP mm1 `t < 0`;
+ *                       WLP has none (no lane runs a model branch against another);
+ *   mem_reads / mem_writes — global load / store warp-instructions of the model kernel
+ *                       (the analogue of the paper's Table 1 counts; atomics excluded).
+ * Costs some speed; off by default. */
+int wlp_set_hw_counters(int enable);
+
 /* validate_params (models.cpp:26-44): WLP_EDOMAIN on invalid values; a non-empty
  * warning (lambda >= mu) is copied into warn[cap]. */
 int wlp_validate_params(int model, const wlp_params* p, char* warn, int warn_cap);

@@ -172,6 +172,16 @@ class Oracle:
         return out
 
     # reference-only helpers
+    def run_model_report(self, model: int, p: _Params, seed: int, mode: int, tlp_block: int = 256) -> dict:
+        """The reference's SimReport (simulated Fermi counters) of run_model."""
+        out = (C.c_int64 * 8)()
+        f = self.lib.ref_run_model_report
+        f.argtypes = [C.c_int, C.POINTER(_Params), C.c_int, C.c_uint64, C.c_int, C.c_void_p]
+        self._check(f(model, C.byref(p), mode, seed, tlp_block, out))
+        keys = ("totalCycles", "wavesExecuted", "peakResidentWarps", "issues", "aluIssues", "memReads", "memWrites",
+                "divergenceEvents")
+        return dict(zip(keys, list(out)))
+
     def plan_launch(self, R: int, mode: int, tlp_block: int = 256):
         dims = (C.c_int64 * 3)()
         warn = C.create_string_buffer(512)

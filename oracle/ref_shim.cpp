@@ -166,6 +166,27 @@ int ref_run_model(int model, const RefParams* p, int mode, std::uint64_t seed, i
     });
 }
 
+// SimReport of run_model (device.hpp:62-71): [totalCycles, wavesExecuted,
+// peakResidentWarps, issues, aluIssues, memReads, memWrites, divergenceEvents].
+int ref_run_model_report(int model, const RefParams* p, int mode, std::uint64_t seed, int tlp_block,
+                         std::int64_t* out8) {
+    return guarded([&] {
+        warpsim::DeviceProfile prof;
+        warpsim::ModelRun run = warpsim::run_model(to_model(model), to_params(p), to_mode(mode), prof, seed,
+                                                   tlp_block);
+        const warpsim::SimReport& r = run.report;
+        const std::int64_t v[8] = {r.totalCycles,
+                                   r.wavesExecuted,
+                                   r.peakResidentWarps,
+                                   static_cast<std::int64_t>(r.issues),
+                                   static_cast<std::int64_t>(r.aluIssues),
+                                   static_cast<std::int64_t>(r.memReads),
+                                   static_cast<std::int64_t>(r.memWrites),
+                                   static_cast<std::int64_t>(r.divergenceEvents)};
+        std::memcpy(out8, v, sizeof v);
+    });
+}
+
 // The reference's host replication loop (models.cpp:345-376) over caller-given streams,
 // split into contiguous slices over `nthreads` host threads. The per-replication
 // functions are pure, so slicing changes nothing but wall time. This is the

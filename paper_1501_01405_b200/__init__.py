@@ -234,6 +234,7 @@ _I64 = C.c_int64
 _SIGS = {
     "wlp_last_error": (C.c_char_p, []),
     "wlp_version": (C.c_int, []),
+    "wlp_set_hw_counters": (C.c_int, [C.c_int]),
     "wlp_validate_params": (C.c_int, [C.c_int, C.POINTER(_Params), C.c_char_p, C.c_int]),
     "wlp_plan_launch": (C.c_int, [_I64, C.c_int, C.c_int, _I64, C.POINTER(_Cfg), C.c_char_p, C.c_int]),
     "wlp_master_from_seed": (C.c_int, [C.c_uint64, _P]),
@@ -480,6 +481,20 @@ def walk_replication(steps: int, chunks: int, stream: RngState) -> float:
     """walk_replication (models.cpp:56-59)."""
     s = np.array([[stream.s1], [stream.s2], [stream.s3]], dtype=np.uint32)
     return float(run_streams(ModelKind.Walk, ModelParams(steps=steps, chunks=chunks), ExecutionMode.Wlp, s)["out"][0])
+
+
+class hw_counters:
+    """Context manager: SimReports of run_model inside carry hardware counters
+    (divergenceEvents with the reference's definition, memReads/memWrites as global
+    load/store warp-instructions) from instrumented kernels. See wlp_set_hw_counters."""
+
+    def __enter__(self):
+        _check(_lib.wlp_set_hw_counters(1))
+        return self
+
+    def __exit__(self, *exc):
+        _check(_lib.wlp_set_hw_counters(0))
+        return False
 
 
 def run_model(model: ModelKind, p: ModelParams, mode: ExecutionMode, prof: Optional[DeviceProfile] = None,

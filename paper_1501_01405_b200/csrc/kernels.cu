@@ -92,6 +92,22 @@ __device__ __forceinline__ void stage_log_table(double* dst) {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) dst[i] = kLogTabDev[i];
 }
 
+// Warp-level load instructions of a `for (i = tid; i < total; i += blockDim)` staging
+// loop: the iterations of the warp's first lane.
+__device__ __forceinline__ unsigned staged_loads(int total) {
+    const int first = static_cast<int>(threadIdx.x) & ~31;
+    return first < total ? static_cast<unsigned>((total - first + blockDim.x - 1) / blockDim.x) : 0u;
+}
+
+__device__ __forceinline__ void flush_tally(const HwTally& h, unsigned long long* hw) {
+    const unsigned act = __activemask();
+    if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(act) - 1)) {
+        if (h.div) atomicAdd(hw, static_cast<unsigned long long>(h.div));
+        if (h.ld) atomicAdd(hw + 1, static_cast<unsigned long long>(h.ld));
+        if (h.st) atomicAdd(hw + 2, static_cast<unsigned long long>(h.st));
+    }
+}
+
 // Inside test of one pi point, x*x + y*y <= 1.0 in unfused fp64 (models.hpp:54-56),
 // evaluated on the unscaled draws: with x = a*2^-32 every product and sum is the
 // reference's value times 2^64 exactly (power-of-two scaling commutes with rounding
@@ -224,9 +240,11 @@ __device__ __forceinline__ double scale(double e, double rate, double inv) {
 // (models.hpp:67-77): t = (w + s) - a; idle/w update; s = next service; sums.
 struct Queue {
     double w = 0.0, s = 0.0, idle = 0.0, sumw = 0.0, sums = 0.0;
-    __device__ __forceinline__ void client(double a, double s_next) {
+    // returns whether the `t < 0` branch (server idle) was taken
+    __device__ __forceinline__ bool client(double a, double s_next) {
         const double t = __dsub_rn(__dadd_rn(w, s), a);
-        if (t < 0.0) {  // the server ran dry before this arrival
+        const bool dry = t < 0.0;
+        if (dry) {  // the server ran dry before this arrival
             idle = __dsub_rn(idle, t);
             w = 0.0;
         } else {
@@ -235,6 +253,7 @@ struct Queue {
         s = s_next;
         sumw = __dadd_rn(sumw, w);
         sums = __dadd_rn(sums, __dadd_rn(w, s));
+        return dry;
     }
 };
 
@@ -380,13 +399,15 @@ __device__ __forceinline__ int64_t grab_take(unsigned long long ticket) {
     return static_cast<int64_t>(__shfl_sync(kFull, ticket, 0));
 }
 
-template <int MODEL>
+template <int MODEL, bool COUNT>
 __global__ void __launch_bounds__(kWlpBlock, 3) k_wlp_lanes(RepArgs a, const uint32_t* __restrict__ gtab,
                                                              int64_t K) {
     extern __shared__ uint32_t tab[];  // kLaneTabWords
     stage_u32<kLaneTabWords>(tab, gtab);
     __syncthreads();
     const int lane = threadIdx.x & 31;
+    HwTally hw;  // WLP: no lane runs a model branch against another, so hw.div stays 0
+    if (COUNT) hw.ld = staged_loads(kLaneTabWords / 4);
     int64_t mine = a.n - static_cast<int64_t>(lane) * K;
     mine = mine < 0 ? 0 : (mine > K ? K : mine);
     const uint32_t units = static_cast<uint32_t>(mine);
@@ -412,8 +433,13 @@ __global__ void __launch_bounds__(kWlpBlock, 3) k_wlp_lanes(RepArgs a, const uin
             if (lane == static_cast<int>(r - base)) keep = val;
         }
         if (lane < end - base) a.out0[base + lane] = keep;
+        if (COUNT) {
+            hw.ld += 3 * static_cast<unsigned>(end - base);
+            hw.st += 1;
+        }
         base = grab_take(ticket);
     }
+    if (COUNT) flush_tally(hw, a.hw);
 }
 
 // mm1 WLP shared memory: lane-start tables, panel-skip table, log table, then per warp
@@ -505,11 +531,13 @@ __device__ __forceinline__ Mm1Smem mm1_stage(const uint32_t* gtab, const uint32_
     return m;
 }
 
-template <bool INV>
+template <bool INV, bool COUNT>
 __global__ void __launch_bounds__(kMm1Block) k_wlp_mm1(RepArgs a, const uint32_t* __restrict__ gtab,
                                                         const uint32_t* __restrict__ gskip) {
     const Mm1Smem m = mm1_stage(gtab, gskip);
     const int lane = threadIdx.x & 31;
+    HwTally hw;  // the `t < 0` branch runs on lane 0 alone: no split, hw.div stays 0
+    if (COUNT) hw.ld = staged_loads(kLaneTabWords / 4) + staged_loads(kUniTabWords) + staged_loads(256);
     for (int64_t base = grab_take(grab_issue(a, lane)); base < a.count;) {
         const unsigned long long ticket = grab_issue(a, lane);
         const int64_t end = base + a.grab < a.count ? base + a.grab : a.count;
@@ -533,8 +561,13 @@ __global__ void __launch_bounds__(kMm1Block) k_wlp_mm1(RepArgs a, const uint32_t
             a.out1[base + lane] = k1;
             a.out2[base + lane] = k2;
         }
+        if (COUNT) {
+            hw.ld += 3 * static_cast<unsigned>(end - base);
+            hw.st += 3;
+        }
         base = grab_take(ticket);
     }
+    if (COUNT) flush_tally(hw, a.hw);
 }
 
 // ---------------------------------------------------------------------------------
@@ -571,12 +604,55 @@ __device__ __forceinline__ double walk_rep_tlp(Taus st, int64_t n, int64_t chunk
     return walk_fold(static_cast<int64_t>(px), chunks);
 }
 
-template <int MODEL>
+// One warp-level `if` of the reference's event definition (warp_exec.cpp:272-284): with
+// active lanes `act`, the branch diverges when some take it and some do not. Returns the
+// lanes that did not take it (the else side's active mask).
+__device__ __forceinline__ unsigned split_if(unsigned act, bool cond, unsigned& events, unsigned sync = 0u) {
+    const unsigned taken = __ballot_sync(sync ? sync : act, cond) & act;
+    if (taken != 0u && taken != act) ++events;
+    return act & ~taken;
+}
+
+// The walk with its 4-way branch (models.cpp:216-253 nests three ifs) and event counting.
+__device__ __forceinline__ double walk_rep_tlp_counted(Taus st, int64_t n, int64_t chunks, unsigned& events) {
+    const unsigned act = __activemask();
+    double px = 0.0, py = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        const uint32_t d = taus_next(st) >> 30;
+        (void)taus_next(st);
+        const unsigned a1 = split_if(act, d == 0u, events);
+        const unsigned a2 = a1 ? split_if(a1, d == 1u, events) : 0u;
+        if (a2) split_if(a2, d == 2u, events);
+        if (d == 0u)
+            px = __dadd_rn(px, 1.0);
+        else if (d == 1u)
+            px = __dsub_rn(px, 1.0);
+        else if (d == 2u)
+            py = __dadd_rn(py, 1.0);
+        else
+            py = __dsub_rn(py, 1.0);
+    }
+    return walk_fold(static_cast<int64_t>(px), chunks);
+}
+
+template <int MODEL, bool COUNT>
 __global__ void k_tlp(RepArgs a) {
     const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (r >= a.count) return;  // tail threads of the last block stay inert (wlp.cpp:125-138)
     const Taus st = load_seed(a, r);
-    a.out0[r] = MODEL == 0 ? pi_rep_tlp(st, a.n) : walk_rep_tlp(st, a.n, a.chunks);
+    HwTally hw;
+    if (MODEL == 0) {
+        a.out0[r] = pi_rep_tlp(st, a.n);  // no data-dependent branch: no events
+    } else if (COUNT) {
+        a.out0[r] = walk_rep_tlp_counted(st, a.n, a.chunks, hw.div);
+    } else {
+        a.out0[r] = walk_rep_tlp(st, a.n, a.chunks);
+    }
+    if (COUNT) {
+        hw.ld = 3;  // the seed words
+        hw.st = 1;
+        flush_tally(hw, a.hw);
+    }
 }
 
 // mm1 thread per replication: each lane runs its own queue; the exponentials of 4
@@ -587,11 +663,13 @@ struct TlpMm1Warp {
     double res[32 * kExpoB];
 };
 
-template <bool INV, bool FULL>
+template <bool INV, bool FULL, bool COUNT = false>
 __device__ __forceinline__ Queue mm1_thread_rep(Taus st, int64_t n, int64_t n_warp, double lambda, double mu,
                                                 double inv_l, double inv_m, const double* logtab, TlpMm1Warp& W,
-                                                unsigned mask, int lane) {
+                                                unsigned mask, int lane, bool live = true,
+                                                unsigned* events = nullptr) {
     Queue q;
+    const unsigned act = COUNT ? __ballot_sync(mask, live) : 0u;  // lanes of real replications
     for (int64_t done = 0; done < n_warp; done += kExpoB / 2) {
         uint32_t d[kExpoB];
         double e[kExpoB];
@@ -602,7 +680,11 @@ __device__ __forceinline__ Queue mm1_thread_rep(Taus st, int64_t n, int64_t n_wa
         const int cnt = left <= 0 ? 0 : (left < kExpoB / 2 ? static_cast<int>(left) : kExpoB / 2);
 #pragma unroll
         for (int c = 0; c < kExpoB / 2; ++c)
-            if (c < cnt) q.client(scale<INV>(e[2 * c], lambda, inv_l), scale<INV>(e[2 * c + 1], mu, inv_m));
+            if (c < cnt) {
+                const bool dry =
+                    q.client(scale<INV>(e[2 * c], lambda, inv_l), scale<INV>(e[2 * c + 1], mu, inv_m));
+                if (COUNT && act) split_if(act, dry, *events, mask);  // models.cpp:199-201's if
+            }
     }
     return q;
 }
@@ -612,7 +694,7 @@ __device__ __forceinline__ unsigned block_lane_mask() {  // partial last warp of
     return in_warp >= 32 ? kFull : ((1u << in_warp) - 1u);
 }
 
-template <bool INV>
+template <bool INV, bool COUNT>
 __global__ void k_tlp_mm1(RepArgs a) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double* logtab = reinterpret_cast<double*>(smraw);
@@ -624,10 +706,20 @@ __global__ void k_tlp_mm1(RepArgs a) {
     const bool live = r < a.count;
     const Taus st = live ? load_seed(a, r) : Taus{2u, 8u, 16u};  // tail threads: dummy stream
     const unsigned mask = block_lane_mask();
-    const Queue q = mask == kFull ? mm1_thread_rep<INV, true>(st, a.n, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu,
-                                                              logtab, W, mask, lane)
-                                  : mm1_thread_rep<INV, false>(st, a.n, a.n, a.lambda, a.mu, a.inv_lambda,
-                                                               a.inv_mu, logtab, W, mask, lane);
+    unsigned events = 0;
+    const Queue q = mask == kFull
+                        ? mm1_thread_rep<INV, true, COUNT>(st, a.n, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu,
+                                                           logtab, W, mask, lane, live, &events)
+                        : mm1_thread_rep<INV, false, COUNT>(st, a.n, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu,
+                                                            logtab, W, mask, lane, live, &events);
+    if (COUNT) {
+        HwTally hw;
+        hw.div = events;
+        const bool any_live = __any_sync(mask, live);
+        hw.ld = staged_loads(256) + (any_live ? 3u : 0u);
+        hw.st = any_live ? 3u : 0u;
+        flush_tally(hw, a.hw);
+    }
     if (!live) return;
     const double nd = static_cast<double>(a.n);
     a.out0[r] = __ddiv_rn(q.idle, nd);
@@ -828,18 +920,21 @@ void allow_smem(K kernel, size_t bytes) {
 int wlp_blocks_per_sm(int model) {
     int nb = 0;
     if (model == 1) {
-        allow_smem(k_wlp_mm1<false>, kMm1Smem);
-        allow_smem(k_wlp_mm1<true>, kMm1Smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_mm1<false>, kMm1Block, kMm1Smem);
+        allow_smem(k_wlp_mm1<false, false>, kMm1Smem);
+        allow_smem(k_wlp_mm1<true, false>, kMm1Smem);
+        allow_smem(k_wlp_mm1<false, true>, kMm1Smem);
+        allow_smem(k_wlp_mm1<true, true>, kMm1Smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_mm1<false, false>, kMm1Block, kMm1Smem);
     } else {
         const size_t smem = kLaneTabWords * 4;
-        if (model == 0) {
-            allow_smem(k_wlp_lanes<0>, smem);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_lanes<0>, kWlpBlock, smem);
-        } else {
-            allow_smem(k_wlp_lanes<2>, smem);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_lanes<2>, kWlpBlock, smem);
-        }
+        allow_smem(k_wlp_lanes<0, false>, smem);
+        allow_smem(k_wlp_lanes<0, true>, smem);
+        allow_smem(k_wlp_lanes<2, false>, smem);
+        allow_smem(k_wlp_lanes<2, true>, smem);
+        if (model == 0)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_lanes<0, false>, kWlpBlock, smem);
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_lanes<2, false>, kWlpBlock, smem);
     }
     return nb < 1 ? 1 : nb;
 }
@@ -847,14 +942,14 @@ int wlp_blocks_per_sm(int model) {
 int tlp_blocks_per_sm(int model, int block) {
     int nb = 0;
     switch (model) {
-        case 0: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tlp<0>, block, 0); break;
+        case 0: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tlp<0, false>, block, 0); break;
         case 1: {
             const size_t smem = tlp_mm1_smem(block);
-            allow_smem(k_tlp_mm1<false>, smem);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tlp_mm1<false>, block, smem);
+            allow_smem(k_tlp_mm1<false, false>, smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tlp_mm1<false, false>, block, smem);
             break;
         }
-        default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tlp<2>, block, 0); break;
+        default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tlp<2, false>, block, 0); break;
     }
     return nb < 1 ? 1 : nb;
 }
@@ -891,15 +986,19 @@ cudaError_t launch_taus_stream(const uint32_t* powers, Taus seed, int64_t n, uin
 cudaError_t launch_wlp(int model, const RepArgs& a, const uint32_t* lane_tab, const uint32_t* uni_tab,
                        int64_t lane_units, int grid, cudaStream_t st) {
     if (a.count <= 0) return cudaSuccess;
+    const bool count = a.hw != nullptr;
     if (model == 1) {
+        auto go = [&](auto kernel) { kernel<<<grid, kMm1Block, kMm1Smem, st>>>(a, lane_tab, uni_tab); };
         if (a.inv_lambda != 0.0 && a.inv_mu != 0.0)
-            k_wlp_mm1<true><<<grid, kMm1Block, kMm1Smem, st>>>(a, lane_tab, uni_tab);
+            count ? go(k_wlp_mm1<true, true>) : go(k_wlp_mm1<true, false>);
         else
-            k_wlp_mm1<false><<<grid, kMm1Block, kMm1Smem, st>>>(a, lane_tab, uni_tab);
-    } else if (model == 0) {
-        k_wlp_lanes<0><<<grid, kWlpBlock, kLaneTabWords * 4, st>>>(a, lane_tab, lane_units);
+            count ? go(k_wlp_mm1<false, true>) : go(k_wlp_mm1<false, false>);
     } else {
-        k_wlp_lanes<2><<<grid, kWlpBlock, kLaneTabWords * 4, st>>>(a, lane_tab, lane_units);
+        auto go = [&](auto kernel) { kernel<<<grid, kWlpBlock, kLaneTabWords * 4, st>>>(a, lane_tab, lane_units); };
+        if (model == 0)
+            count ? go(k_wlp_lanes<0, true>) : go(k_wlp_lanes<0, false>);
+        else
+            count ? go(k_wlp_lanes<2, true>) : go(k_wlp_lanes<2, false>);
     }
     return cudaGetLastError();
 }
@@ -910,20 +1009,32 @@ cudaError_t launch_tlp(int model, const RepArgs& a, int tlp_block, cudaStream_t 
     const int64_t grid = (a.count + block - 1) / block;
     const bool inv = a.inv_lambda != 0.0 && a.inv_mu != 0.0;
     const dim3 g(static_cast<unsigned>(grid)), b(static_cast<unsigned>(block));
+    const bool count = a.hw != nullptr;
     switch (model) {
-        case 0: k_tlp<0><<<g, b, 0, st>>>(a); break;
+        case 0:
+            if (count)
+                k_tlp<0, true><<<g, b, 0, st>>>(a);
+            else
+                k_tlp<0, false><<<g, b, 0, st>>>(a);
+            break;
         case 1: {
             const size_t smem = tlp_mm1_smem(static_cast<int>(block));
-            if (inv) {
-                allow_smem(k_tlp_mm1<true>, smem);
-                k_tlp_mm1<true><<<g, b, smem, st>>>(a);
-            } else {
-                allow_smem(k_tlp_mm1<false>, smem);
-                k_tlp_mm1<false><<<g, b, smem, st>>>(a);
-            }
+            auto go = [&](auto kernel) {
+                allow_smem(kernel, smem);
+                kernel<<<g, b, smem, st>>>(a);
+            };
+            if (inv)
+                count ? go(k_tlp_mm1<true, true>) : go(k_tlp_mm1<true, false>);
+            else
+                count ? go(k_tlp_mm1<false, true>) : go(k_tlp_mm1<false, false>);
             break;
         }
-        default: k_tlp<2><<<g, b, 0, st>>>(a); break;
+        default:
+            if (count)
+                k_tlp<2, true><<<g, b, 0, st>>>(a);
+            else
+                k_tlp<2, false><<<g, b, 0, st>>>(a);
+            break;
     }
     return cudaGetLastError();
 }

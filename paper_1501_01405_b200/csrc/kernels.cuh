@@ -23,6 +23,16 @@ struct RepArgs {
     // before launch), so warps the arbiter favours do not leave a tail behind them
     unsigned long long* next = nullptr;
     int grab = 1;
+    // Hardware counters (SimReport, device.hpp:62-71): when non-null, the kernels run an
+    // instrumented variant that adds, per warp, [0] the warp-level branch splits of the
+    // model's data-dependent `if`s (the reference's event definition,
+    // warp_exec.cpp:272-284), [1] global load and [2] global store warp-instructions.
+    unsigned long long* hw = nullptr;
+};
+
+// Per-warp instrumentation tally (identical in every lane; the leader flushes it).
+struct HwTally {
+    unsigned div = 0, ld = 0, st = 0;
 };
 
 // Seeding: stream slots [slot_begin, slot_begin+count) of a run.

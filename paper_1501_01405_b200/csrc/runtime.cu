@@ -26,6 +26,7 @@ namespace wlp {
 namespace {
 
 thread_local std::string g_err;
+thread_local bool g_hw_counters = false;  // wlp_set_hw_counters
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
@@ -86,6 +87,7 @@ struct DevCtx {
     DevBuf<unsigned long long> counter;
     DevBuf<int64_t> rejected;
     DevBuf<unsigned long long> work;
+    DevBuf<unsigned long long> hw;  // instrumentation tallies [div, ld, st]
     DevBuf<SeedJob> jobs;
     DevBuf<SetParam> setp;
     DevBuf<uint32_t> plan_lane, plan_skip;
@@ -121,6 +123,7 @@ int ctx_init(DevCtx& c) {
     WLP_CUDA(c.specials.ensure(kSpecialCap));
     WLP_CUDA(c.counter.ensure(1));
     WLP_CUDA(c.work.ensure(1));
+    WLP_CUDA(c.hw.ensure(3));
     WLP_CUDA(cudaEventCreate(&c.ev0));
     WLP_CUDA(cudaEventCreate(&c.ev1));
     WLP_CUDA(cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming));
@@ -403,6 +406,10 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
     a.out0 = o0;
     a.out1 = o1;
     a.out2 = o2;
+    if (g_hw_counters) {
+        WLP_CUDA(cudaMemsetAsync(c.hw.p, 0, 3 * sizeof(unsigned long long), st));
+        a.hw = c.hw.p;
+    }
     if (mode == WLP_MODE_TLP) {
         const int64_t block = std::min<int64_t>(count, tlp_block);
         grid_out = static_cast<int>((count + block - 1) / block);
@@ -444,6 +451,14 @@ void fill_report(DevCtx& c, int model, int mode, int tlp_block, int64_t count, i
     const int64_t resident = bps * c.sms;
     rep->waves_executed = (grid + resident - 1) / resident;
     rep->peak_resident_warps = std::min<int64_t>(grid, resident) * warps_per_block;
+    if (g_hw_counters) {  // tallies of the instrumented kernels (the stream is synchronised)
+        unsigned long long h[3] = {0, 0, 0};
+        if (cudaMemcpy(h, c.hw.p, sizeof h, cudaMemcpyDeviceToHost) == cudaSuccess) {
+            rep->divergence_events = h[0];
+            rep->mem_reads = h[1];
+            rep->mem_writes = h[2];
+        }
+    }
 }
 
 int stats_device(DevCtx& c, const double* x, int64_t n, int pass, wlp_stats* s, cudaStream_t st) {
@@ -519,6 +534,11 @@ extern "C" {
 
 const char* wlp_last_error(void) { return g_err.c_str(); }
 int wlp_version(void) { return 1; }
+
+int wlp_set_hw_counters(int enable) {
+    g_hw_counters = enable != 0;
+    return WLP_OK;
+}
 
 int wlp_validate_params(int model, const wlp_params* p, char* warn, int warn_cap) {
     std::string w;
@@ -1037,6 +1057,7 @@ int wlp_shutdown(void) {
     c.ev0 = c.ev1 = c.done = nullptr;
     c.last_used = false;
     c.work.release();
+    c.hw.release();
     c.jobs.release();
     c.setp.release();
     c.plan_lane.release();

@@ -213,7 +213,16 @@ ConfidenceInterval confidence_interval(const std::vector<double>& samples, doubl
 }
 
 ModelRun run_model(ModelKind model, const ModelParams& p, ExecutionMode mode, const DeviceProfile& prof,
-                   std::uint64_t master_seed, int tlp_block_size, const SimOptions&) {
+                   std::uint64_t master_seed, int tlp_block_size, const SimOptions& opts) {
+    struct Counters {  // scoped wlp_set_hw_counters
+        bool on;
+        explicit Counters(bool o) : on(o) {
+            if (on) wlp_set_hw_counters(1);
+        }
+        ~Counters() {
+            if (on) wlp_set_hw_counters(0);
+        }
+    } counters(opts.hardwareCounters);
     const LaunchPlan plan = plan_launch(p.replications, mode, prof, tlp_block_size, 0x7FFFFFFF);
     const wlp_params c = to_c(p);
     const std::size_t R = static_cast<std::size_t>(p.replications);

@@ -290,6 +290,18 @@ static void gpu_tests() {
         }
         CHECK_THROWS_AS(run_sweep(SweepSpec{}, prof), DomainError);  // no modes
     });
+    test_case("SimReport hardware counters via SimOptions (TLP walk diverges, WLP does not)", [&] {
+        ModelParams p;
+        p.replications = 64;
+        p.steps = 100;
+        SimOptions opts;
+        opts.hardwareCounters = true;
+        ModelRun tlp = run_model(ModelKind::Walk, p, ExecutionMode::Tlp, prof, 42, 256, opts);
+        ModelRun wlp = run_model(ModelKind::Walk, p, ExecutionMode::Wlp, prof, 42, 256, opts);
+        CHECK(tlp.report.divergenceEvents > 0 && tlp.report.memReads == 6 && tlp.report.memWrites == 2);
+        CHECK(wlp.report.divergenceEvents == 0 && wlp.report.memReads > 0);
+        CHECK(run_model(ModelKind::Walk, p, ExecutionMode::Tlp, prof, 42).report.divergenceEvents == 0);  // off
+    });
     test_case("errors map onto the reference's exception types", [&] {
         ModelParams p;
         p.draws = 0;
