@@ -380,6 +380,17 @@ def main():
                 else:  # FP64 pipe: 64 lanes/clk/SM (measured, profiles/round1_microbench.txt)
                     r["fp64_frac"] = units_ * FP64_PER_CLIENT / (r["kernel_ms"] * 1e-3) / (64 * sms * fmax * 1e6)
                 extras[name][w.mode_name(md)] = r
+        # config 3's warp-execution evidence (paper Table 1 / Fig. 7 analogue): divergence
+        # events with the reference's definition and global memory warp-instructions, from
+        # the instrumented kernels (outputs identical; counters cost a little speed)
+        pw = w.ModelParams(replications=100_000, steps=1000, chunks=30)
+        table1 = {}
+        with w.hw_counters():
+            for md in (w.ExecutionMode.Wlp, w.ExecutionMode.Tlp):
+                rr = w.run_model(w.ModelKind.Walk, pw, md, master_seed=SEED).report
+                table1[w.mode_name(md)] = {"divergence_events": rr.divergenceEvents, "mem_reads": rr.memReads,
+                                           "mem_writes": rr.memWrites}
+        extras["cfg3_walk_1e5x1e3"]["counters"] = table1
         # config 5: experimental plan, 64 factor-level sets x 30 replications, one launch
         sets = [w.ModelParams(replications=30, clients=10_000, lambda_=0.1 + 0.8 * k / 63, mu=1.0) for k in range(64)]
         seeds = [SEED + k for k in range(64)]
