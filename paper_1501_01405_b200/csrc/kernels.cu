@@ -716,7 +716,8 @@ __global__ void k_tlp_mm1(RepArgs a) {
         HwTally hw;
         hw.div = events;
         const bool any_live = __any_sync(mask, live);
-        hw.ld = staged_loads(256) + (any_live ? 3u : 0u);
+        // the seed loads are predicated, so a warp of dummy lanes still issues them
+        hw.ld = staged_loads(256) + 3u;
         hw.st = any_live ? 3u : 0u;
         flush_tally(hw, a.hw);
     }

@@ -21,11 +21,18 @@ ap.add_argument("mode", choices=["sequential", "tlp", "wlp"])
 ap.add_argument("R", type=int)
 ap.add_argument("N", type=int)
 ap.add_argument("--repeat", type=int, default=2)
+ap.add_argument("--counters", action="store_true", help="instrumented kernels; print the SimReport tallies")
 a = ap.parse_args()
 m = w.model_from_name(a.model)
 p = w.ModelParams(replications=a.R, draws=a.N, clients=a.N, steps=a.N)
 outs = [torch.empty(a.R, dtype=torch.float64, device="cuda") for _ in w.OUTPUT_NAMES[m]]
+rep = w.SimReport()
+ctx = w.hw_counters() if a.counters else None
+if ctx:
+    ctx.__enter__()
 for _ in range(a.repeat):
-    w.run_shard(m, p, w.mode_from_name(a.mode), 42, 0, a.R, outs, on_device=True)
+    w.run_shard(m, p, w.mode_from_name(a.mode), 42, 0, a.R, outs, on_device=True, report=rep)
+if ctx:
+    ctx.__exit__(None, None, None)
 torch.cuda.synchronize()
-print(a.model, a.mode, a.R, a.N, "mean", float(outs[0].mean()))
+print(a.model, a.mode, a.R, a.N, "mean", float(outs[0].mean()), "report", rep)
