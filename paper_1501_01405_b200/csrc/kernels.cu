@@ -174,10 +174,12 @@ __device__ __forceinline__ int64_t warp_sum_i64(int64_t v) {
     return v;
 }
 
-// fold of the walk's final x (models.hpp:106-107): fmod(fmod(px,c)+c,c) on an integral
-// px is exact and equals ((px % c) + c) % c (C remainder, sign of the dividend).
-__device__ __forceinline__ double walk_fold(int64_t px, int64_t c) {
-    return static_cast<double>(((px % c) + c) % c);
+// fold of the walk's final x (models.hpp:106-107), in the reference's own arithmetic:
+// c = (double)chunks (rounded above 2^53, as there), fmod(fmod(px, c) + c, c). fmod is
+// exact in IEEE arithmetic on both sides; px is an exact integer (|px| <= steps).
+__device__ __forceinline__ double walk_fold(int64_t px, int64_t chunks) {
+    const double c = static_cast<double>(chunks);
+    return fmod(__dadd_rn(fmod(static_cast<double>(px), c), c), c);
 }
 
 // ---------------------------------------------------------------------------------

@@ -77,7 +77,15 @@ def main() -> None:
             (0, dict(replications=3, draws=33)), (2, dict(replications=4, steps=1, chunks=2)),
             (2, dict(replications=4, steps=63, chunks=2)), (1, dict(replications=3, clients=1)),
             (1, dict(replications=3, clients=257, lambda_=1.0, mu=0.5)),
-            (1, dict(replications=2, clients=300, lambda_=0.3, mu=0.7))]
+            (1, dict(replications=2, clients=300, lambda_=0.3, mu=0.7)),
+            # extreme rates: overflow to inf / underflow, non power-of-two and 2^k rates
+            (1, dict(replications=3, clients=50, lambda_=1e-300, mu=1e300)),
+            (1, dict(replications=3, clients=50, lambda_=2.0**-600, mu=2.0**700)),
+            (1, dict(replications=3, clients=50, lambda_=3.0, mu=0.1)),
+            # chunks beyond 2^53: the reference folds in double with c rounded
+            (2, dict(replications=3, steps=101, chunks=2**60 + 1)),
+            (2, dict(replications=3, steps=101, chunks=2**53 + 1)),
+            (0, dict(replications=2, draws=2**20 + 3))]
     for model, kw in edge:
         res = ref.run_model(model, oracle.params(**kw), 7)
         cases.append({"seed": 7, "model": model, "params": kw,
