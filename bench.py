@@ -231,9 +231,19 @@ def cpu_baseline(model: int, p, budget_s: float = 15.0, steps: int = 1):
     tot = [run(S) for _ in range(steps)]
     tsp = sum(x for x, _ in tot) / steps
     trep = sum(y for _, y in tot) / steps
+    # single-core rate of the same functions on a small slice
+    s1 = max(4, min(S, int(2.0 / max(per * nth, 1e-9))))
+    keys = ref.random_spacing(SEED, s1)
+    t0 = time.perf_counter()
+    if kind == "reference":
+        ref.replications(model, op, keys, nthreads=1)
+    else:
+        ref.replications(model, op, keys)
+    t1 = time.perf_counter()
     return {"value": S / (tsp + trep), "unit": UNIT, "cores": nth if kind == "reference" else 1, "kind": kind,
             "sample": f"{S} of {p.replications} replications (seed {SEED}): random_spacing 1 thread "
                       f"{tsp:.3f}s + replications on {nth if kind == 'reference' else 1} threads {trep:.3f}s",
+            "single_core_value": s1 / (t1 - t0 + tsp / S * s1), "single_core_sample": f"{s1} replications",
             "step_s": tsp + trep}
 
 
