@@ -9,8 +9,9 @@
 //                units [l*K, (l+1)*K) after one nibble-table jump; exact integer
 //                warp reduction (__reduce_add_sync) of hits / x-displacement.
 //   k_wlp_mm1    mm1, one replication per warp; lanes produce the exponentials of a
-//                32*T-client panel into shared memory, lane 0 runs the order-preserving
-//                Lindley recursion (models.hpp:61-84) on them.
+//                32*T-client panel, chain the Lindley recursion (models.hpp:61-84) across
+//                their segments by exact fixed-point rounds, and lanes 0-2 run the three
+//                order-dependent sums.
 //   k_tlp        the thread-per-replication comparison mapping (plan_launch TLP
 //                geometry, wlp.cpp:88-92); mm1 shares the batched exponential routine.
 //   k_stats      sums / centred sums of squares for the confidence interval.
@@ -445,75 +446,155 @@ __global__ void __launch_bounds__(kWlpBlock, 3) k_wlp_lanes(RepArgs a, const uin
 }
 
 // mm1 WLP shared memory: lane-start tables, panel-skip table, log table, then per warp
-// the panel buffer (a and s of 32*T clients) and the near-one compaction list.
+// the panel's per-client terms of the three ordered sums and the near-one compaction list.
 constexpr int kMm1P = 32 * kMm1PanelT;
+constexpr int kMm1Seg = kMm1PanelT + 2;  // lane segment stride (doubles): STS.128 rows spread over banks
+constexpr int kMm1Arr = 32 * kMm1Seg + 2;  // array stride: the three sum lanes read different banks
 struct Mm1Warp {
-    // client-ordered {a, s} pairs, lane l's T clients at [l*(T+1), l*(T+1)+T) (one pad
-    // slot per lane segment spreads the lanes' STS.128 over the banks)
-    double2 pair[32 * (kMm1PanelT + 1)];
+    // [k][l*kMm1Seg + c] = term k of client l*T + c of the panel: k = 0 w (-> sumw),
+    // 1 w + s (-> sums), 2 the idle increment -t or +0 (-> idle). Also the near-one
+    // scratch of the exponential batches before the terms are written.
+    double term[3 * kMm1Arr];
     NearList nl;
 };
-constexpr size_t kMm1Smem =
-    (kLaneTabWords + kUniTabWords) * 4 + 256 * 8 + (kMm1Block / 32) * sizeof(Mm1Warp);
+static_assert(kMm1Arr >= 32 * kExpoB, "near-one results alias the term arrays");
+constexpr size_t kMm1Smem = kUniTabWords * 4 + 256 * 8 + (kMm1Block / 32) * sizeof(Mm1Warp);
 
-// mm1: lanes generate, lane 0 recurses. Panel p covers clients [p*32T, (p+1)*32T); lane l
-// produces clients p*32T + l*T + j (j < T) from draws 2*(that index) and 2*(...)+1, so
-// each lane steps its own contiguous draw range and hops 62T draws between panels.
-// Returns the queue (valid on lane 0).
+// One client of the Lindley recursion, models.hpp:67-78 in the reference's rounding:
+// t = (w + s_prev) - a with u = fl(w + s_prev) carried from the previous client (it is
+// the previous client's sums term, the same fl(w + s)); w = t < 0 ? 0 : t; u = fl(w + s).
+// * w = fmax(t, +0) is the branch: t is never -0 or NaN here (u >= +0, a finite), so
+//   both give +0 for t < 0 and t otherwise.
+// * d is the idle increment, d = fl(w - t): -t when dry, +0 otherwise, exactly. idle - t
+//   == idle + (-t), and idle + (+0) == idle (idle >= +0), so the reference's conditional
+//   `idle = idle - t` becomes a plain ordered sum of d like the other two.
+__device__ __forceinline__ void lindley(double& w, double& u, double a, double s, double& d) {
+    const double t = __dsub_rn(u, a);
+    w = fmax(t, 0.0);
+    d = __dsub_rn(w, t);
+    u = __dadd_rn(w, s);
+}
+
+// mm1, one replication per warp. Panel p covers clients [p*32T, (p+1)*32T); lane l owns
+// clients p*32T + l*T + c (c < T), drawn from draws 2*(that index) and 2*(...)+1, so each
+// lane steps its own contiguous draw range and hops 62T draws between panels.
+//
+// Per panel: (1) lanes compute their clients' exponentials (a, s). (2) The Lindley
+// recursion is chained across the 32 lane segments. Round 1: every lane runs its segment
+// from an input waiting time (lane 0 the true carry, the others 0) and stores its clients'
+// sum terms. Then, while some lane's input (its predecessor's segment end) changed, those
+// lanes re-run from the new input, storing terms, until their waiting time is 0: there
+// the new trajectory has met the old one (the recursion is monotone in w and inputs only
+// grow from round to round, so new w = 0 forces old w = 0) and everything after is
+// unchanged; a lane that never meets it passes a new end on. Lane 0 is exact in round 1
+// and lane l by round l+1, so the fixed point is the sequential trajectory bit for bit;
+// at rho = 1/2 the server runs dry at about every other arrival, so the re-runs are
+// short. (3) Lanes 0-2 run the three ordered sums over the panel's terms: sumw, sums and
+// idle are order-dependent fp64 and stay sequential, one lane each, in one instruction.
 template <bool INV>
-__device__ __forceinline__ Queue mm1_warp_rep(Taus st, int64_t n, double lambda, double mu, double inv_l,
-                                              double inv_m, const double* logtab, const uint32_t* skip, Mm1Warp& W,
-                                              int lane) {
+__device__ __forceinline__ double mm1_warp_rep(Taus st, int64_t n, double lambda, double mu, double inv_l,
+                                               double inv_m, const double* logtab, const uint32_t* skip, Mm1Warp& W,
+                                               int lane) {
     constexpr int T = kMm1PanelT;
     constexpr int P = kMm1P;
-    static_assert(2 * T % kExpoB == 0, "panel draws per lane must be whole batches");
-    Queue q;
+    static_assert(2 * T % kExpoB == 0 && T % 2 == 0, "panel draws per lane must be whole batches");
+    double wc = 0.0, sc = 0.0;  // carry (warp-uniform): w and s of the panel's predecessor client
+    double acc = 0.0;           // lane k < 3: ordered sum of term k
+    double* const term = W.term + lane * kMm1Seg;
     for (int64_t base = 0; base < n; base += P) {
-        // draws of my T clients: a_c = draw 2c, s_c = draw 2c+1, in batches of kExpoB;
-        // the panel buffer doubles as the batches' near-one scratch until it is written
         double ea[T], es[T];
 #pragma unroll
         for (int h = 0; h < 2 * T; h += kExpoB) {
             uint32_t d[kExpoB];
             double e[kExpoB];
 #pragma unroll
-            for (int j = 0; j < kExpoB; ++j) d[j] = taus_next(st);
-            neg_log1m_batch<kExpoB, true>(d, e, logtab, W.nl, reinterpret_cast<double*>(W.pair), kFull, lane);
+            for (int j = 0; j < kExpoB; j += 2) taus_next2(st, d[j], d[j + 1]);
+            neg_log1m_batch<kExpoB, true>(d, e, logtab, W.nl, W.term, kFull, lane);
 #pragma unroll
             for (int j = 0; j < kExpoB; j += 2) {
                 ea[(h + j) / 2] = scale<INV>(e[j], lambda, inv_l);
                 es[(h + j) / 2] = scale<INV>(e[j + 1], mu, inv_m);
             }
         }
+        const int64_t left = n - base;
+        const bool has = left > static_cast<int64_t>(lane) * T;  // my segment holds clients
+        double sp = __shfl_up_sync(kFull, es[T - 1], 1);       // s of my segment's predecessor
+        if (lane == 0) sp = sc;
+        double in = lane == 0 ? wc : 0.0;
+        double end;
+        {  // round 1: the whole segment (clients past n are computed too, never summed)
+            double w = in, u = __dadd_rn(in, sp);
 #pragma unroll
-        for (int c = 0; c < T; ++c) W.pair[lane * (T + 1) + c] = make_double2(ea[c], es[c]);
-        __syncwarp();
-        if (lane == 0) {  // the order-preserving recursion, 8 clients per unrolled step
-            const int64_t left = n - base;
-            if (left >= P) {
-                const double2* p = W.pair;
-                for (int seg = 0; seg < 32; ++seg, p += T + 1) {
-                    double2 v[T];
+            for (int c = 0; c < T; c += 2) {
+                double w0, d0, w1, d1;
+                lindley(w0, u, ea[c], es[c], d0);
+                const double u0 = u;
+                lindley(w1, u, ea[c + 1], es[c + 1], d1);
+                *reinterpret_cast<double2*>(term + c) = make_double2(w0, w1);
+                *reinterpret_cast<double2*>(term + kMm1Arr + c) = make_double2(u0, u);
+                *reinterpret_cast<double2*>(term + 2 * kMm1Arr + c) = make_double2(d0, d1);
+                w = w1;
+            }
+            end = w;
+        }
+        for (;;) {  // ripple rounds (warp-uniform loop)
+            double nin = __shfl_up_sync(kFull, end, 1);
+            if (lane == 0) nin = wc;
+            bool run = has && __double_as_longlong(nin) != __double_as_longlong(in);
+            if (!__any_sync(kFull, run)) break;
+            if (run) in = nin;
+            double w = in, u = __dadd_rn(in, sp);
 #pragma unroll
-                    for (int j = 0; j < T; ++j) v[j] = p[j];
-#pragma unroll
-                    for (int j = 0; j < T; ++j) q.client(v[j].x, v[j].y);
-                }
-            } else {
-                for (int c = 0; c < static_cast<int>(left); ++c) {
-                    const double2 v = W.pair[(c / T) * (T + 1) + c % T];
-                    q.client(v.x, v.y);
+            for (int c = 0; c < T; ++c) {
+                if (c % 2 == 0 && !__any_sync(kFull, run)) break;  // (checked every other client)
+                if (run) {
+                    double d;
+                    lindley(w, u, ea[c], es[c], d);
+                    term[c] = w;
+                    term[kMm1Arr + c] = u;
+                    term[2 * kMm1Arr + c] = d;
+                    run = w != 0.0;  // met the previous trajectory: the rest is unchanged
+                    if (c == T - 1 && run) end = w;
                 }
             }
+        }
+        wc = __shfl_sync(kFull, end, 31);
+        sc = __shfl_sync(kFull, es[T - 1], 31);
+        __syncwarp();
+        if (lane < 3) {  // the ordered sums, one lane per sum
+            const double* x = W.term + lane * kMm1Arr;
+            const int cnt = left >= P ? P : static_cast<int>(left);
+            const int nseg = cnt / T;
+            // segment loads run one segment ahead of the adds (the last prefetch reads past
+            // the array into the next one or the near-one list: in bounds, unused)
+            double2 v[T / 2];
+#pragma unroll
+            for (int j = 0; j < T / 2; ++j) v[j] = reinterpret_cast<const double2*>(x)[j];
+            for (int seg = 0; seg < nseg; ++seg) {
+                x += kMm1Seg;
+                double2 nv[T / 2];
+#pragma unroll
+                for (int j = 0; j < T / 2; ++j) nv[j] = reinterpret_cast<const double2*>(x)[j];
+#pragma unroll
+                for (int j = 0; j < T / 2; ++j) {
+                    acc = __dadd_rn(acc, v[j].x);
+                    acc = __dadd_rn(acc, v[j].y);
+                }
+#pragma unroll
+                for (int j = 0; j < T / 2; ++j) v[j] = nv[j];
+            }
+            for (int c = 0; c < cnt - nseg * T; ++c) acc = __dadd_rn(acc, x[c]);
         }
         __syncwarp();
         st = uni_jump(skip, st);
     }
-    return q;
+    return acc;
 }
 
+// The lane-start tables stay in global memory (L1/L2 resident): one 24-load jump per
+// replication of ~10^3 clients is noise, and the 48 KB are better spent on term arrays.
 struct Mm1Smem {
-    uint32_t* tab;
+    const uint32_t* tab;
     uint32_t* skip;
     double* logtab;
     Mm1Warp* W;
@@ -522,11 +603,10 @@ struct Mm1Smem {
 __device__ __forceinline__ Mm1Smem mm1_stage(const uint32_t* gtab, const uint32_t* gskip) {
     extern __shared__ __align__(16) unsigned char smraw[];
     Mm1Smem m;
-    m.tab = reinterpret_cast<uint32_t*>(smraw);
-    m.skip = m.tab + kLaneTabWords;
+    m.tab = gtab;
+    m.skip = reinterpret_cast<uint32_t*>(smraw);
     m.logtab = reinterpret_cast<double*>(m.skip + kUniTabWords);
     m.W = reinterpret_cast<Mm1Warp*>(m.logtab + 256) + (threadIdx.x >> 5);
-    stage_u32<kLaneTabWords>(m.tab, gtab);
     for (int i = threadIdx.x; i < kUniTabWords; i += blockDim.x) m.skip[i] = __ldg(gskip + i);
     stage_log_table(m.logtab);
     __syncthreads();
@@ -534,24 +614,24 @@ __device__ __forceinline__ Mm1Smem mm1_stage(const uint32_t* gtab, const uint32_
 }
 
 template <bool INV, bool COUNT>
-__global__ void __launch_bounds__(kMm1Block) k_wlp_mm1(RepArgs a, const uint32_t* __restrict__ gtab,
+__global__ void __launch_bounds__(kMm1Block, 3) k_wlp_mm1(RepArgs a, const uint32_t* __restrict__ gtab,
                                                         const uint32_t* __restrict__ gskip) {
     const Mm1Smem m = mm1_stage(gtab, gskip);
     const int lane = threadIdx.x & 31;
-    HwTally hw;  // the `t < 0` branch runs on lane 0 alone: no split, hw.div stays 0
-    if (COUNT) hw.ld = staged_loads(kLaneTabWords / 4) + staged_loads(kUniTabWords) + staged_loads(256);
+    HwTally hw;  // the `t < 0` decision is a per-lane select, never a warp branch: hw.div stays 0
+    if (COUNT) hw.ld = staged_loads(kUniTabWords) + staged_loads(256);
     for (int64_t base = grab_take(grab_issue(a, lane)); base < a.count;) {
         const unsigned long long ticket = grab_issue(a, lane);
         const int64_t end = base + a.grab < a.count ? base + a.grab : a.count;
         double k0 = 0.0, k1 = 0.0, k2 = 0.0;
         for (int64_t r = base; r < end; ++r) {
             const Taus st = lane_jump(m.tab, lane, load_seed(a, r));
-            const Queue q = mm1_warp_rep<INV>(st, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu, m.logtab, m.skip,
-                                              *m.W, lane);
-            const double nd = static_cast<double>(a.n);
-            const double v0 = __shfl_sync(kFull, __ddiv_rn(q.idle, nd), 0);
-            const double v1 = __shfl_sync(kFull, __ddiv_rn(q.sumw, nd), 0);
-            const double v2 = __shfl_sync(kFull, __ddiv_rn(q.sums, nd), 0);
+            const double acc = mm1_warp_rep<INV>(st, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu, m.logtab,
+                                                 m.skip, *m.W, lane);
+            const double avg = __ddiv_rn(acc, static_cast<double>(a.n));  // lanes 0/1/2: wait/sys/idle
+            const double v0 = __shfl_sync(kFull, avg, 2);
+            const double v1 = __shfl_sync(kFull, avg, 0);
+            const double v2 = __shfl_sync(kFull, avg, 1);
             if (lane == static_cast<int>(r - base)) {
                 k0 = v0;
                 k1 = v1;
@@ -564,7 +644,7 @@ __global__ void __launch_bounds__(kMm1Block) k_wlp_mm1(RepArgs a, const uint32_t
             a.out2[base + lane] = k2;
         }
         if (COUNT) {
-            hw.ld += 3 * static_cast<unsigned>(end - base);
+            hw.ld += (3 + 24) * static_cast<unsigned>(end - base);  // seed words, lane-jump table reads
             hw.st += 3;
         }
         base = grab_take(ticket);
@@ -796,16 +876,14 @@ __global__ void __launch_bounds__(kMm1Block) k_plan_mm1(PlanArgs a, const uint32
     for (int64_t r = next_rep(a, lane); r < a.count; r = next_rep(a, lane)) {
         const SetParam S = a.sets[find_set(a.sets, a.n_sets, r)];
         const Taus st = lane_jump(m.tab, lane, plan_seed(a, r));
-        const Queue q = (S.inv_lambda != 0.0 && S.inv_mu != 0.0)
-                            ? mm1_warp_rep<true>(st, S.n, S.lambda, S.mu, S.inv_lambda, S.inv_mu, m.logtab, m.skip,
-                                                 *m.W, lane)
-                            : mm1_warp_rep<false>(st, S.n, S.lambda, S.mu, S.inv_lambda, S.inv_mu, m.logtab, m.skip,
-                                                  *m.W, lane);
-        if (lane == 0) {
-            const double nd = static_cast<double>(S.n);
-            a.out0[r] = __ddiv_rn(q.idle, nd);
-            a.out1[r] = __ddiv_rn(q.sumw, nd);
-            a.out2[r] = __ddiv_rn(q.sums, nd);
+        const double acc = (S.inv_lambda != 0.0 && S.inv_mu != 0.0)
+                               ? mm1_warp_rep<true>(st, S.n, S.lambda, S.mu, S.inv_lambda, S.inv_mu, m.logtab,
+                                                    m.skip, *m.W, lane)
+                               : mm1_warp_rep<false>(st, S.n, S.lambda, S.mu, S.inv_lambda, S.inv_mu, m.logtab,
+                                                     m.skip, *m.W, lane);
+        if (lane < 3) {  // lanes 0/1/2 hold sumw/sums/idle
+            double* out = lane == 0 ? a.out1 : (lane == 1 ? a.out2 : a.out0);
+            out[r] = __ddiv_rn(acc, static_cast<double>(S.n));
         }
     }
 }

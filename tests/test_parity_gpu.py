@@ -108,6 +108,19 @@ def test_medium_runs_vs_port(gpu, port, model):
             assert np.array_equal(run.outputs[name], want[name]), (mode, name)
 
 
+@pytest.mark.parametrize("lam,mu", [(0.5, 1.0), (0.95, 1.0), (0.999, 1.0), (2.0, 1.0), (0.05, 1.0), (0.3, 0.7)])
+@pytest.mark.parametrize("clients", [1, 7, 255, 256, 257, 511, 1234])
+def test_mm1_wlp_segment_chaining_all_loads(gpu, port, lam, mu, clients):
+    # WLP mm1 chains the Lindley recursion across 32 lane segments of a 256-client panel by
+    # fixed-point rounds: light load (regenerates within a segment), heavy and overloaded
+    # queues (the waiting time never returns to 0: up to 32 rounds), ragged last panels
+    p = gpu.ModelParams(replications=97, clients=clients, lambda_=lam, mu=mu)
+    want = port.run_model(1, oracle.params_from(p), 31337)
+    run = gpu.run_model(gpu.ModelKind.Mm1, p, gpu.ExecutionMode.Wlp, master_seed=31337)
+    for name in oracle.OUTPUTS[1]:
+        assert np.array_equal(run.outputs[name], want[name]), name
+
+
 def test_run_streams_pi_mm1_walk_replication(gpu, port):
     keys = port.random_spacing(3, 50)
     st = gpu.RngState(*[int(x) for x in keys[:, 7]])
