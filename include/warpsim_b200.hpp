@@ -16,7 +16,8 @@
 //   * run_model lifts plan_launch's 65535-block grid cap to the hardware's 2^31-1
 //     (BASELINE configs need 10^6-10^7 WLP replications); plan_launch itself keeps the
 //     reference default.
-// The IR / simulator / kernel-text layers of the reference are not part of this path.
+// The kernel IR and its text form run on the GPU through include/warpsim_ir_b200.hpp
+// (an IR interpreter on the B200 in place of the reference's host simulator).
 #pragma once
 
 #include <cstdint>
@@ -93,10 +94,17 @@ struct DeviceProfile {
 };
 struct SimOptions {
     std::optional<std::uint64_t> smPermutationSeed;  // accepted, ignored (real hardware)
-    int maskStackDepth = 32;                         // accepted, ignored
+    int maskStackDepth = 32;  // IR interpreter: mask-stack bound, as in the reference
     // B200 extension: fill SimReport::divergenceEvents / memReads / memWrites from
     // instrumented kernels (wlp_set_hw_counters). Off by default: costs some speed.
     bool hardwareCounters = false;
+    // B200 extension: run Tlp / Wlp through the reference's IR kernels on the GPU IR
+    // interpreter (warpsim_ir_b200.hpp) instead of the hand-written kernels: same
+    // outputs, and the reference simulator's exact issue / divergence / memory counters.
+    bool irInterpreter = false;
+    // IR interpreter: statements one IR warp may issue before FaultError (guards
+    // against kernels that never terminate).
+    std::int64_t maxIssuesPerWarp = std::int64_t{1} << 50;
 };
 struct SimReport {
     std::int64_t totalCycles = 0;

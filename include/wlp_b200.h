@@ -36,6 +36,7 @@ extern "C" {
 #define WLP_EFAULT 3    /* FaultError: a device lane fault                                 */
 #define WLP_ESPACING 4  /* Error: random_spacing found no distinct seed (rng.cpp:81-82)    */
 #define WLP_ECUDA 5     /* Error: CUDA runtime failure / no device                         */
+#define WLP_EPARSE 6    /* ParseError: kernel text (kernel_text.hpp; libwarpsim_b200.so)    */
 #define WLP_EINTERNAL 7 /* Error: anything else                                            */
 
 /* ModelKind (models.hpp:18) and ExecutionMode (wlp.hpp:16). */
@@ -234,6 +235,101 @@ int wlp_confidence_interval(const double* samples, int64_t n, double level, wlp_
 
 /* Test hook: -log(1 - k[i]*2^-32) through the device glibc-log port (host arrays). */
 int wlp_debug_neg_log1m(const uint32_t* k, int64_t n, double* out);
+
+/* ---- kernel IR on the GPU ------------------------------------
+ *
+ * The reference's kernel IR (kernel_ir.hpp:67-141; text form kernel_text.hpp) executed
+ * by a SIMT interpreter ON the B200 instead of the reference's host simulator
+ * (simulate, device.cpp:140-226; WarpState::step, warp_exec.cpp:178-298). Each IR warp
+ * runs on one hardware warp, IR lane l on lane l; the warp walks the statement tree
+ * with the reference's mask-stack semantics (then before else, loop re-tests, permanent
+ * halts, reconvergence, stores resolved in ascending lane order), so per-lane values,
+ * memory contents and the issue / divergence / memory counters are the reference
+ * simulator's exactly. IR warps of one launch run concurrently: kernels whose warps
+ * communicate through global memory are outside that guarantee (the reference runs
+ * them one after another); the bundled models never do.
+ *
+ * The host C++ layer (include/warpsim_ir_b200.hpp) builds / parses programs and
+ * flattens them into this form: statements laid out so every statement list is a
+ * contiguous index range, expressions as typed stack bytecode (opcodes WLP_IR_OP_*;
+ * every expression ends with WLP_IR_OP_END). */
+
+/* Statement kinds (StmtKind order, kernel_ir.hpp:101). */
+#define WLP_IR_ASSIGN 0
+#define WLP_IR_LOAD 1
+#define WLP_IR_STORE 2
+#define WLP_IR_IF 3
+#define WLP_IR_WHILE 4
+#define WLP_IR_HALT 5
+
+/* Statement flags: faults the type rules decide statically, raised when executed. */
+#define WLP_IR_F_REAL_INTO_INT 1 /* assign of a real value into an int local      */
+#define WLP_IR_F_INT_TO_REAL 2   /* assign of an int value into a real local      */
+#define WLP_IR_F_REAL_INDEX 4    /* load / store index is a real                   */
+
+typedef struct wlp_ir_stmt {
+    int32_t kind;
+    int32_t slot;    /* assign / load: local slot; store: array param slot */
+    int32_t arr;     /* load: array param slot */
+    int32_t code_a;  /* expression offset: assign value, load / store index, if / while condition */
+    int32_t code_b;  /* store value */
+    int32_t b1_begin, b1_end; /* then / loop body */
+    int32_t b2_begin, b2_end; /* else body */
+    int32_t flags;
+} wlp_ir_stmt;
+
+/* Expression bytecode: per IR lane a stack of 64-bit slots whose types are static. */
+enum {
+    WLP_IR_OP_END = 0,
+    WLP_IR_OP_CONST,    /* + 2 words (lo, hi of the 64-bit pattern) */
+    WLP_IR_OP_LOCAL,    /* + slot */
+    WLP_IR_OP_PARAM,    /* + slot */
+    WLP_IR_OP_SREG,     /* + Sreg (kernel_ir.hpp:73-79 order) */
+    WLP_IR_OP_DRAW,     /* uniform01 of the lane's taus88 stream */
+    WLP_IR_OP_I2R_0,    /* int -> real, top of stack */
+    WLP_IR_OP_I2R_1,    /* int -> real, second from the top */
+    WLP_IR_OP_TRUTH_0,  /* real -> int truth (r != 0), top */
+    WLP_IR_OP_TRUTH_1,  /* real -> int truth, second from the top */
+    WLP_IR_OP_ADD_I, WLP_IR_OP_SUB_I, WLP_IR_OP_MUL_I, WLP_IR_OP_DIV_I, WLP_IR_OP_MOD_I,
+    WLP_IR_OP_ADD_R, WLP_IR_OP_SUB_R, WLP_IR_OP_MUL_R, WLP_IR_OP_DIV_R, WLP_IR_OP_MOD_R,
+    WLP_IR_OP_LT_I, WLP_IR_OP_LE_I, WLP_IR_OP_GT_I, WLP_IR_OP_GE_I, WLP_IR_OP_EQ_I, WLP_IR_OP_NE_I,
+    WLP_IR_OP_LT_R, WLP_IR_OP_LE_R, WLP_IR_OP_GT_R, WLP_IR_OP_GE_R, WLP_IR_OP_EQ_R, WLP_IR_OP_NE_R,
+    WLP_IR_OP_AND, WLP_IR_OP_OR, /* on int truths */
+    WLP_IR_OP_NEG_I, WLP_IR_OP_NEG_R, WLP_IR_OP_LOG, WLP_IR_OP_FLOOR,
+    WLP_IR_OP_COUNT
+};
+
+/* Interpreter limits (the host layer rejects larger programs with WLP_EDOMAIN). */
+#define WLP_IR_MAX_LOCALS 64
+#define WLP_IR_MAX_STACK 32
+
+typedef struct wlp_ir_program {
+    const wlp_ir_stmt* stmts;
+    int32_t n_stmts;
+    int32_t top_begin, top_end; /* the kernel body */
+    const int32_t* code;
+    int32_t n_code;
+    int32_t n_locals;
+    const int64_t* local_init; /* per local: initial bits (0 / +0.0 or an initial value) */
+    int32_t n_params;
+    const int64_t* param_bits; /* scalar params: value bits (reals already promoted) */
+    const int32_t* param_is_array;
+} wlp_ir_program;
+
+/* simulate (device.cpp:140-226) on the GPU: runs every IR warp of `cfg` (warp_size in
+ * [1, 32]; threads per block <= max_threads_per_block) over the arrays (indexed by
+ * param slot; NULL for scalar params; host or device memory, sizes in array_len) with
+ * lane streams streams[3*n_streams] (SoA; thread t draws from stream t, the default
+ * state when t >= n_streams). mask_depth bounds the mask stack (SimOptions, 1..64);
+ * max_issues (> 0) bounds the statements one IR warp may issue (a guard against
+ * kernels that never terminate; WLP_EFAULT when hit). Fills the report's issue /
+ * alu / memory / divergence counters exactly as the reference simulator counts them,
+ * plus measured time. Lane faults (division by zero, log of a non-positive value, ...)
+ * return WLP_EFAULT with the reference's message. Synchronous. */
+int wlp_ir_simulate(const wlp_ir_program* prog, const wlp_launch_cfg* cfg, int64_t max_threads_per_block,
+                    double* const* arrays, const int64_t* array_len, int arrays_on_device,
+                    const uint32_t* streams, int64_t n_streams, int streams_on_device, int mask_depth,
+                    int64_t max_issues, void* stream, wlp_report* report);
 
 /* Release all device scratch of the current device. */
 int wlp_shutdown(void);

@@ -182,6 +182,53 @@ class Oracle:
                 "divergenceEvents")
         return dict(zip(keys, list(out)))
 
+    # kernel IR (reference-only): the checker of the GPU IR interpreter
+    def _ir_text(self, fn, *args) -> str:
+        need = C.c_int(0)
+        self._check(fn(*args, None, 0, C.byref(need)))
+        buf = C.create_string_buffer(need.value)
+        self._check(fn(*args, buf, need.value, None))
+        return buf.value.decode()
+
+    def ir_model_text(self, model: int, mode: int = 0) -> str:
+        """dump_kernel of build_model_body(model), wrap_tlp (mode 1) / wrap_wlp (mode 2)."""
+        f = self.lib.ref_ir_model_text
+        f.argtypes = [C.c_int, C.c_int, C.c_char_p, C.c_int, C.POINTER(C.c_int)]
+        return self._ir_text(f, model, mode)
+
+    def ir_canonical(self, text: str) -> str:
+        f = self.lib.ref_ir_canonical
+        f.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.POINTER(C.c_int)]
+        return self._ir_text(f, text.encode())
+
+    def ir_simulate(self, text: str, cfg: tuple, scalars: dict, arrays: dict, streams: Optional[np.ndarray] = None,
+                    mask_depth: int = 32, max_threads_per_block: int = 1024) -> dict:
+        """The reference simulator (simulate, device.cpp:140-226) on a kernel text.
+        cfg = (bx, by, bz, gx, gy, warpSize); arrays (float64) are updated in place;
+        streams (3, n) uint32. Returns the SimReport fields."""
+        names = list(scalars)
+        n = max(len(names), 1)
+        is_int = (C.c_int * n)(*[isinstance(scalars[k], (int, np.integer)) for k in names])
+        ivals = (C.c_int64 * n)(*[int(scalars[k]) if is_int[i] else 0 for i, k in enumerate(names)])
+        rvals = (C.c_double * n)(*[0.0 if is_int[i] else float(scalars[k]) for i, k in enumerate(names)])
+        cn = (C.c_char_p * n)(*[k.encode() for k in names])
+        an = list(arrays)
+        m = max(len(an), 1)
+        can = (C.c_char_p * m)(*[k.encode() for k in an])
+        ap = (C.c_void_p * m)(*[arrays[k].ctypes.data for k in an])
+        al = (C.c_int64 * m)(*[arrays[k].size for k in an])
+        st = np.zeros((3, 0), dtype=np.uint32) if streams is None else np.ascontiguousarray(streams, dtype=np.uint32)
+        c6 = (C.c_int64 * 6)(*cfg)
+        out = (C.c_int64 * 8)()
+        f = self.lib.ref_ir_simulate_text
+        f.argtypes = [C.c_char_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                      C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_void_p]
+        self._check(f(text.encode(), c6, max_threads_per_block, len(names), cn, is_int, ivals, rvals, len(an), can, ap,
+                      al, st.ctypes.data if st.size else None, st.shape[1], mask_depth, out))
+        keys = ("totalCycles", "wavesExecuted", "peakResidentWarps", "issues", "aluIssues", "memReads", "memWrites",
+                "divergenceEvents")
+        return dict(zip(keys, list(out)))
+
     def plan_launch(self, R: int, mode: int, tlp_block: int = 256):
         dims = (C.c_int64 * 3)()
         warn = C.create_string_buffer(512)

@@ -10,14 +10,18 @@
 // exception taxonomy (proj/include/warpsim/error.hpp:8-36) onto the status codes the
 // product C-ABI uses (include/wlp_b200.h), so parity tests can compare errors too.
 
+#include <algorithm>
 #include <cstdint>
+#include <map>
 #include <cstring>
 #include <exception>
 #include <string>
 #include <thread>
 #include <vector>
 
+#include "warpsim/device.hpp"
 #include "warpsim/error.hpp"
+#include "warpsim/kernel_text.hpp"
 #include "warpsim/models.hpp"
 #include "warpsim/rng.hpp"
 #include "warpsim/sweep.hpp"
@@ -297,6 +301,71 @@ int ref_sweep_csv(int model, int modes_mask, std::int64_t r_min, std::int64_t r_
         std::string s = warpsim::csv_string(warpsim::run_sweep(spec, prof));
         if (static_cast<std::int64_t>(s.size()) + 1 > cap) throw warpsim::Error("csv buffer too small");
         std::memcpy(buf, s.c_str(), s.size() + 1);
+    });
+}
+
+
+// ---- kernel IR (the checker of the GPU IR interpreter) -----------------------------------
+
+namespace {
+int put_text(const std::string& s, char* out, int cap, int* need) {
+    if (need) *need = static_cast<int>(s.size()) + 1;
+    if (out && cap > 0) {
+        const std::size_t n = std::min<std::size_t>(s.size(), static_cast<std::size_t>(cap - 1));
+        std::memcpy(out, s.data(), n);
+        out[n] = 0;
+    }
+    return 0;
+}
+}  // namespace
+
+// dump_kernel (kernel_text.cpp:344-366) of build_model_body (mode 0) or its wrap_tlp (1) /
+// wrap_wlp (2) form (wlp.cpp:107-138).
+int ref_ir_model_text(int model, int mode, char* out, int cap, int* need) {
+    return guarded([&] {
+        warpsim::KernelProgram body = warpsim::build_model_body(to_model(model));
+        warpsim::KernelProgram prog = mode == 0 ? body : mode == 1 ? warpsim::wrap_tlp(body) : warpsim::wrap_wlp(body);
+        put_text(warpsim::dump_kernel(prog), out, cap, need);
+    });
+}
+
+// dump_kernel(parse_kernel(text)).
+int ref_ir_canonical(const char* text, char* out, int cap, int* need) {
+    return guarded([&] { put_text(warpsim::dump_kernel(warpsim::parse_kernel(text)), out, cap, need); });
+}
+
+// simulate (device.cpp:140-226) of a kernel text: scalars by name, arrays by name (updated
+// in place), lane streams SoA[3*n_streams]; report8 as ref_run_model_report.
+int ref_ir_simulate_text(const char* text, const std::int64_t* cfg6, int max_threads_per_block, int n_scalars,
+                         const char* const* names, const int* is_int, const std::int64_t* ivals,
+                         const double* rvals, int n_arrays, const char* const* anames, double* const* arrays,
+                         const std::int64_t* alen, const std::uint32_t* streams, std::int64_t n_streams,
+                         int mask_depth, std::int64_t* report8) {
+    return guarded([&] {
+        warpsim::KernelProgram prog = warpsim::parse_kernel(text);
+        warpsim::LaunchConfig cfg;
+        cfg.blockDim = {cfg6[0], cfg6[1], cfg6[2]};
+        cfg.gridDim = {cfg6[3], cfg6[4]};
+        cfg.warpSize = static_cast<int>(cfg6[5]);
+        std::map<std::string, warpsim::Value> scalars;
+        for (int k = 0; k < n_scalars; ++k)
+            scalars[names[k]] = is_int[k] ? warpsim::Value::integer(ivals[k]) : warpsim::Value::real(rvals[k]);
+        warpsim::GlobalMemory mem;
+        for (int k = 0; k < n_arrays; ++k) mem.arrays[anames[k]].assign(arrays[k], arrays[k] + alen[k]);
+        std::vector<warpsim::RngState> st(static_cast<std::size_t>(n_streams));
+        for (std::int64_t t = 0; t < n_streams; ++t)
+            st[t] = warpsim::RngState{streams[t], streams[n_streams + t], streams[2 * n_streams + t]};
+        warpsim::DeviceProfile prof;
+        prof.maxThreadsPerBlock = max_threads_per_block;
+        warpsim::SimOptions opts;
+        opts.maskStackDepth = mask_depth;
+        const warpsim::SimReport r = warpsim::simulate(prog, cfg, prof, mem, scalars, st, opts);
+        for (int k = 0; k < n_arrays; ++k) std::copy(mem.arrays[anames[k]].begin(), mem.arrays[anames[k]].end(), arrays[k]);
+        const std::int64_t v[8] = {r.totalCycles, r.wavesExecuted, r.peakResidentWarps,
+                                   static_cast<std::int64_t>(r.issues), static_cast<std::int64_t>(r.aluIssues),
+                                   static_cast<std::int64_t>(r.memReads), static_cast<std::int64_t>(r.memWrites),
+                                   static_cast<std::int64_t>(r.divergenceEvents)};
+        std::memcpy(report8, v, sizeof v);
     });
 }
 

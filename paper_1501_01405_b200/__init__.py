@@ -54,9 +54,9 @@ class AnalysisError(Error):
     """warpsim::AnalysisError"""
 
 
-OK, EDOMAIN, EPLAN, EFAULT, ESPACING, ECUDA, EINTERNAL = 0, 1, 2, 3, 4, 5, 7
+OK, EDOMAIN, EPLAN, EFAULT, ESPACING, ECUDA, EPARSE, EINTERNAL = 0, 1, 2, 3, 4, 5, 6, 7
 _EXC = {EDOMAIN: DomainError, EPLAN: PlanError, EFAULT: FaultError, ESPACING: Error, ECUDA: Error,
-        EINTERNAL: Error}
+        EPARSE: ParseError, EINTERNAL: Error}
 
 # ---- enums and records --------------------------------------------------------------------
 
@@ -135,9 +135,13 @@ class DeviceProfile:  # device.hpp:19-28 — accepted for signature compatibilit
 
 
 @dataclass
-class SimOptions:  # device.hpp:53-60 — accepted, ignored
-    smPermutationSeed: Optional[int] = None
-    maskStackDepth: int = 32
+class SimOptions:  # device.hpp:53-60
+    smPermutationSeed: Optional[int] = None  # accepted, ignored (real hardware)
+    maskStackDepth: int = 32  # IR interpreter mask-stack bound
+    # B200 extensions: run Tlp / Wlp through the reference's IR kernels on the GPU IR
+    # interpreter (paper_1501_01405_b200.ir), and its per-IR-warp issue guard
+    irInterpreter: bool = False
+    maxIssuesPerWarp: int = 1 << 50
 
 
 @dataclass
@@ -260,6 +264,8 @@ _SIGS = {
     "wlp_stats_device": (C.c_int, [_P, _I64, C.c_int, C.POINTER(Stats), _P]),
     "wlp_confidence_interval": (C.c_int, [_P, _I64, C.c_double, C.POINTER(_CI)]),
     "wlp_debug_neg_log1m": (C.c_int, [_P, _I64, _P]),
+    "wlp_ir_simulate": (C.c_int, [_P, C.POINTER(_Cfg), _I64, _P, _P, C.c_int, _P, _I64, C.c_int, C.c_int, _I64, _P,
+                                  C.POINTER(_Report)]),
     "wlp_shutdown": (C.c_int, []),
 }
 EXPORTS = tuple(_SIGS)
@@ -509,6 +515,10 @@ def run_model(model: ModelKind, p: ModelParams, mode: ExecutionMode, prof: Optio
     its `cfg` is the reference's single-thread geometry.
     """
     model, mode = ModelKind(model), ExecutionMode(mode)
+    if opts is not None and opts.irInterpreter and mode != ExecutionMode.Sequential:
+        from . import ir  # the reference's IR kernels on the GPU interpreter
+
+        return ir.run_model(model, p, mode, master_seed, tlp_block_size)
     plan = plan_launch(p.replications, mode, prof, tlp_block_size, grid_limit=0x7FFFFFFF)
     R = int(p.replications)
     names = OUTPUT_NAMES[model]

@@ -45,7 +45,7 @@ def _stale(out: Path, deps: list[Path]) -> bool:
 
 
 def build_cuda(force: bool = False) -> Path:
-    srcs = [CSRC / "kernels.cu", CSRC / "runtime.cu"]
+    srcs = [CSRC / "kernels.cu", CSRC / "ir_interp.cu", CSRC / "runtime.cu"]
     deps = srcs + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.hpp")) + sorted(CSRC.glob("*.h")) + [
         ROOT / "include" / "wlp_b200.h"]
     if force or _stale(LIB, deps):
@@ -54,8 +54,9 @@ def build_cuda(force: bool = False) -> Path:
 
 
 def build_cxx(force: bool = False) -> Path:
-    srcs = [HOST / "warpsim_api.cpp"]
-    deps = srcs + [ROOT / "include" / "warpsim_b200.hpp", ROOT / "include" / "wlp_b200.h", LIB]
+    srcs = [HOST / "warpsim_api.cpp", HOST / "ir.cpp"]
+    deps = srcs + [ROOT / "include" / "warpsim_b200.hpp", ROOT / "include" / "warpsim_ir_b200.hpp",
+                   ROOT / "include" / "wlp_b200.h", LIB]
     if force or _stale(CXXLIB, deps):
         _run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-fPIC", "-shared", f"-I{ROOT / 'include'}",
               *map(str, srcs), "-o", str(CXXLIB), f"-L{PKG}", "-lwlp_b200", "-Wl,-rpath,$ORIGIN"])

@@ -18,6 +18,7 @@
 
 #include "../../include/wlp_b200.h"
 #include "jump.hpp"
+#include "ir_interp.cuh"
 #include "kernels.cuh"
 
 static_assert(sizeof(wlp_special) == sizeof(wlp::SpecialRec), "wlp_special layout");
@@ -1027,6 +1028,271 @@ int wlp_confidence_interval(const double* samples, int64_t n, double level, wlp_
     WLP_CUDA(c->stats_in.ensure(n));
     WLP_CUDA(cudaMemcpy(c->stats_in.p, samples, n * 8, cudaMemcpyHostToDevice));
     return ci_device(*c, c->stats_in.p, n, level, ci, nullptr);
+}
+
+// ---- kernel IR interpreter ---------------------------------------------------------
+
+}  // extern "C"
+
+namespace wlp {
+namespace {
+
+// Structural check of a flattened program, so that nothing malformed reaches the device:
+// every index in range, every expression well formed, stack within WLP_IR_MAX_STACK.
+int ir_check(const wlp_ir_program& p) {
+    auto bad = [](const std::string& m) { return fail(WLP_EDOMAIN, "ir program: " + m); };
+    if (p.n_stmts < 0 || p.n_code < 1 || !p.code || (p.n_stmts > 0 && !p.stmts)) return bad("empty tables");
+    if (p.n_locals < 0 || p.n_locals > WLP_IR_MAX_LOCALS)
+        return bad("more than " + std::to_string(WLP_IR_MAX_LOCALS) + " locals");
+    if (p.n_params < 0 || (p.n_params > 0 && (!p.param_bits || !p.param_is_array))) return bad("params");
+    if (p.n_locals > 0 && !p.local_init) return bad("local_init");
+    // expressions: walk the code, each expression ends with END at stack depth 1
+    std::vector<char> starts(p.n_code, 0);
+    for (int pc = 0; pc < p.n_code;) {
+        starts[pc] = 1;
+        int depth = 0;
+        for (;;) {
+            if (pc >= p.n_code) return bad("unterminated expression");
+            const int op = p.code[pc++];
+            int need = 0, push = 0, args = 0;
+            switch (op) {
+                case WLP_IR_OP_END: need = 1; break;
+                case WLP_IR_OP_CONST: push = 1; args = 2; break;
+                case WLP_IR_OP_LOCAL: case WLP_IR_OP_PARAM: case WLP_IR_OP_SREG: push = 1; args = 1; break;
+                case WLP_IR_OP_DRAW: push = 1; break;
+                case WLP_IR_OP_I2R_0: case WLP_IR_OP_TRUTH_0: case WLP_IR_OP_NEG_I: case WLP_IR_OP_NEG_R:
+                case WLP_IR_OP_LOG: case WLP_IR_OP_FLOOR: need = 1; break;
+                case WLP_IR_OP_I2R_1: case WLP_IR_OP_TRUTH_1: need = 2; break;
+                default:
+                    if (op < WLP_IR_OP_ADD_I || op >= WLP_IR_OP_COUNT) return bad("unknown opcode " + std::to_string(op));
+                    need = 2;
+                    push = -1;
+                    break;
+            }
+            if (pc + args > p.n_code) return bad("truncated operand");
+            if (op == WLP_IR_OP_LOCAL && (p.code[pc] < 0 || p.code[pc] >= p.n_locals)) return bad("local slot");
+            if (op == WLP_IR_OP_PARAM &&
+                (p.code[pc] < 0 || p.code[pc] >= p.n_params || p.param_is_array[p.code[pc]]))
+                return bad("param slot");
+            if (op == WLP_IR_OP_SREG && (p.code[pc] < 0 || p.code[pc] > 10)) return bad("special register");
+            pc += args;
+            if (depth < need) return bad("stack underflow");
+            if (op == WLP_IR_OP_END) {
+                if (depth != 1) return bad("expression leaves " + std::to_string(depth) + " values");
+                break;
+            }
+            depth += push;
+            if (depth > WLP_IR_MAX_STACK)
+                return bad("expression deeper than " + std::to_string(WLP_IR_MAX_STACK) + " values");
+        }
+    }
+    auto expr_ok = [&](int off) { return off >= 0 && off < p.n_code && starts[off]; };
+    auto range_ok = [&](int b, int e) { return 0 <= b && b <= e && e <= p.n_stmts; };
+    if (!range_ok(p.top_begin, p.top_end)) return bad("body range");
+    for (int i = 0; i < p.n_stmts; ++i) {
+        const wlp_ir_stmt& st = p.stmts[i];
+        const bool arr_slot = st.slot >= 0 && st.slot < p.n_params && p.param_is_array[st.slot];
+        switch (st.kind) {
+            case WLP_IR_ASSIGN:
+                if (st.slot < 0 || st.slot >= p.n_locals || !expr_ok(st.code_a)) return bad("assign");
+                break;
+            case WLP_IR_LOAD:
+                if (st.slot < 0 || st.slot >= p.n_locals || st.arr < 0 || st.arr >= p.n_params ||
+                    !p.param_is_array[st.arr] || !expr_ok(st.code_a))
+                    return bad("load");
+                break;
+            case WLP_IR_STORE:
+                if (!arr_slot || !expr_ok(st.code_a) || !expr_ok(st.code_b)) return bad("store");
+                break;
+            case WLP_IR_IF:
+                if (!expr_ok(st.code_a) || !range_ok(st.b1_begin, st.b1_end) || !range_ok(st.b2_begin, st.b2_end))
+                    return bad("if");
+                break;
+            case WLP_IR_WHILE:
+                if (!expr_ok(st.code_a) || !range_ok(st.b1_begin, st.b1_end)) return bad("while");
+                break;
+            case WLP_IR_HALT: break;
+            default: return bad("statement kind");
+        }
+    }
+    return WLP_OK;
+}
+
+std::string ir_fault_message(const IrFault& f, int mask_depth) {
+    const std::string a = std::to_string(f.a), b = std::to_string(f.b);
+    switch (f.code) {  // the reference's messages (kernel_ir.cpp:46-107, warp_exec.cpp)
+        case 1: return "kernel: integer division by zero";
+        case 2: return "kernel: division by zero";
+        case 3: return "kernel: integer modulo by zero";
+        case 4: return "kernel: modulo by zero";
+        case 5: return "kernel: log of a non-positive value";
+        case 6: return "kernel: floor result outside the integer range";
+        case 7: return "load: non-integer index";
+        case 8: return "load: index " + a + " out of bounds for array of " + b;
+        case 9: return "store: non-integer index";
+        case 10: return "store: index " + a + " out of bounds for array of " + b;
+        case 11: return "assign: real value into int local #" + a;
+        case 12: return "mask stack overflow: nesting deeper than " + std::to_string(mask_depth) + " levels";
+        case 13: return "issue budget exhausted: an IR warp issued " + a + " statements";
+    }
+    return "kernel: fault " + std::to_string(f.code);
+}
+
+template <class T>
+struct Scratch {  // per-call device allocation
+    T* p = nullptr;
+    ~Scratch() {
+        if (p) cudaFree(p);
+    }
+    cudaError_t alloc(int64_t n) { return cudaMalloc(&p, static_cast<size_t>(std::max<int64_t>(n, 1)) * sizeof(T)); }
+};
+
+}  // namespace
+}  // namespace wlp
+
+extern "C" {
+
+int wlp_ir_simulate(const wlp_ir_program* prog, const wlp_launch_cfg* cfg, int64_t max_threads_per_block,
+                    double* const* arrays, const int64_t* array_len, int arrays_on_device,
+                    const uint32_t* streams, int64_t n_streams, int streams_on_device, int mask_depth,
+                    int64_t max_issues, void* stream, wlp_report* report) {
+    using namespace wlp;
+    if (!prog || !cfg) return fail(WLP_EDOMAIN, "ir_simulate: null program or launch");
+    if (cfg->block_x < 1 || cfg->block_y < 1 || cfg->block_z < 1)
+        return fail(WLP_EDOMAIN, "launch: blockDim components must be >= 1");
+    if (cfg->grid_x < 1 || cfg->grid_y < 1) return fail(WLP_EDOMAIN, "launch: gridDim components must be >= 1");
+    if (cfg->warp_size < 1 || cfg->warp_size > 64) return fail(WLP_EDOMAIN, "launch: warpSize must be in [1,64]");
+    if (cfg->warp_size > 32)
+        return fail(WLP_EDOMAIN, "launch: the B200 interpreter maps an IR warp onto one hardware warp; warpSize "
+                                 "must be <= 32");
+    if (mask_depth < 1 || mask_depth > 64) return fail(WLP_EDOMAIN, "mask stack depth must be in [1, 64]");
+    if (max_issues < 1) return fail(WLP_EDOMAIN, "ir_simulate: max_issues must be >= 1");
+    const int64_t tpb = cfg->block_x * cfg->block_y * cfg->block_z;
+    if (tpb > max_threads_per_block)
+        return fail(WLP_EPLAN, "block of " + std::to_string(tpb) + " threads exceeds maxThreadsPerBlock " +
+                                   std::to_string(max_threads_per_block));
+    if (n_streams < 0 || (n_streams > 0 && !streams)) return fail(WLP_EDOMAIN, "ir_simulate: streams");
+    WLP_TRY(ir_check(*prog));
+    for (int i = 0; i < prog->n_params; ++i)
+        if (prog->param_is_array[i] && (!array_len || array_len[i] < 0 || (array_len[i] > 0 && !arrays[i])))
+            return fail(WLP_EDOMAIN, "ir_simulate: array argument #" + std::to_string(i));
+    const int64_t ws = cfg->warp_size;
+    const int64_t wpb = (tpb + ws - 1) / ws;
+    const int64_t total_warps = wpb * cfg->grid_x * cfg->grid_y;
+
+    DevCtx* c;
+    std::unique_lock<std::mutex> lk;
+    WLP_TRY(acquire(c, lk));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamOrder so(*c, st);
+
+    const int np = std::max(prog->n_params, 1);
+    Scratch<wlp_ir_stmt> d_stmts;
+    Scratch<int32_t> d_code;
+    Scratch<int64_t> d_init, d_params, d_alen;
+    Scratch<double*> d_arrs;
+    Scratch<uint32_t> d_streams;
+    Scratch<unsigned long long> d_cnt;
+    Scratch<IrFault> d_fault;
+    std::vector<Scratch<double>> host_arrays(np);
+    WLP_CUDA(d_stmts.alloc(prog->n_stmts));
+    WLP_CUDA(d_code.alloc(prog->n_code));
+    WLP_CUDA(d_init.alloc(prog->n_locals));
+    WLP_CUDA(d_params.alloc(np));
+    WLP_CUDA(d_alen.alloc(np));
+    WLP_CUDA(d_arrs.alloc(np));
+    WLP_CUDA(d_cnt.alloc(5));
+    WLP_CUDA(d_fault.alloc(1));
+    if (prog->n_stmts)
+        WLP_CUDA(cudaMemcpyAsync(d_stmts.p, prog->stmts, prog->n_stmts * sizeof(wlp_ir_stmt), cudaMemcpyHostToDevice, st));
+    WLP_CUDA(cudaMemcpyAsync(d_code.p, prog->code, prog->n_code * 4, cudaMemcpyHostToDevice, st));
+    if (prog->n_locals)
+        WLP_CUDA(cudaMemcpyAsync(d_init.p, prog->local_init, prog->n_locals * 8, cudaMemcpyHostToDevice, st));
+    std::vector<int64_t> pbits(np, 0), alen(np, 0);
+    std::vector<double*> aptr(np, nullptr);
+    for (int i = 0; i < prog->n_params; ++i) {
+        if (!prog->param_is_array[i]) {
+            pbits[i] = prog->param_bits[i];
+            continue;
+        }
+        alen[i] = array_len[i];
+        if (arrays_on_device) {
+            aptr[i] = arrays[i];
+        } else if (alen[i] > 0) {
+            WLP_CUDA(host_arrays[i].alloc(alen[i]));
+            WLP_CUDA(cudaMemcpyAsync(host_arrays[i].p, arrays[i], alen[i] * 8, cudaMemcpyHostToDevice, st));
+            aptr[i] = host_arrays[i].p;
+        }
+    }
+    WLP_CUDA(cudaMemcpyAsync(d_params.p, pbits.data(), np * 8, cudaMemcpyHostToDevice, st));
+    WLP_CUDA(cudaMemcpyAsync(d_alen.p, alen.data(), np * 8, cudaMemcpyHostToDevice, st));
+    WLP_CUDA(cudaMemcpyAsync(d_arrs.p, aptr.data(), np * sizeof(double*), cudaMemcpyHostToDevice, st));
+    const uint32_t* ds = streams;
+    if (n_streams > 0 && !streams_on_device) {
+        WLP_CUDA(d_streams.alloc(3 * n_streams));
+        WLP_CUDA(cudaMemcpyAsync(d_streams.p, streams, 3 * n_streams * 4, cudaMemcpyHostToDevice, st));
+        ds = d_streams.p;
+    }
+    WLP_CUDA(cudaMemsetAsync(d_cnt.p, 0, 5 * sizeof(unsigned long long), st));
+    WLP_CUDA(cudaMemsetAsync(d_fault.p, 0, sizeof(IrFault), st));
+
+    IrArgs a{};
+    a.stmts = d_stmts.p;
+    a.code = d_code.p;
+    a.top_begin = prog->top_begin;
+    a.top_end = prog->top_end;
+    a.n_locals = prog->n_locals;
+    a.local_init = d_init.p;
+    a.params = d_params.p;
+    a.arrays = d_arrs.p;
+    a.alen = d_alen.p;
+    a.streams = ds;
+    a.n_streams = n_streams;
+    a.bx = cfg->block_x;
+    a.by = cfg->block_y;
+    a.bz = cfg->block_z;
+    a.gx = cfg->grid_x;
+    a.gy = cfg->grid_y;
+    a.ws = ws;
+    a.tpb = tpb;
+    a.wpb = wpb;
+    a.total_warps = total_warps;
+    a.mask_depth = mask_depth;
+    a.max_issues = max_issues;
+    a.counters = d_cnt.p;
+    a.fault = d_fault.p;
+    const int64_t resident_blocks = static_cast<int64_t>(ir_blocks_per_sm()) * c->sms;
+    const int64_t need_blocks = (total_warps * 32 + kIrBlock - 1) / kIrBlock;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min(resident_blocks, need_blocks)));
+    WLP_CUDA(cudaEventRecord(c->ev0, st));
+    WLP_CUDA(launch_ir(a, grid, st));
+    WLP_CUDA(cudaEventRecord(c->ev1, st));
+    if (!arrays_on_device)
+        for (int i = 0; i < prog->n_params; ++i)
+            if (prog->param_is_array[i] && alen[i] > 0)
+                WLP_CUDA(cudaMemcpyAsync(arrays[i], aptr[i], alen[i] * 8, cudaMemcpyDeviceToHost, st));
+    unsigned long long cnt[5];
+    IrFault fault{};
+    WLP_CUDA(cudaMemcpyAsync(cnt, d_cnt.p, sizeof cnt, cudaMemcpyDeviceToHost, st));
+    WLP_CUDA(cudaMemcpyAsync(&fault, d_fault.p, sizeof fault, cudaMemcpyDeviceToHost, st));
+    WLP_CUDA(cudaStreamSynchronize(st));
+    if (fault.code != 0) return fail(WLP_EFAULT, ir_fault_message(fault, mask_depth));
+    if (report) {
+        float ms = 0.f;
+        WLP_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+        std::memset(report, 0, sizeof *report);
+        report->kernel_ms = ms;
+        report->total_cycles = static_cast<int64_t>(std::llround(static_cast<double>(ms) * c->clock_khz));
+        const int64_t resident_warps = resident_blocks * (kIrBlock / 32);
+        report->waves_executed = (total_warps + resident_warps - 1) / resident_warps;
+        report->peak_resident_warps = std::min(total_warps, resident_warps);
+        report->issues = cnt[0];
+        report->alu_issues = cnt[1];
+        report->mem_reads = cnt[2];
+        report->mem_writes = cnt[3];
+        report->divergence_events = cnt[4];
+    }
+    return WLP_OK;
 }
 
 int wlp_shutdown(void) {

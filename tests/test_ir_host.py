@@ -1,0 +1,64 @@
+"""Kernel IR front end without a GPU: the model kernels' text, the
+s-expression parser / printer and its errors, against the reference (kernel_text.cpp,
+models.cpp:124-268, wlp.cpp:107-138) and its committed dumps (tests/golden/ir)."""
+import pytest
+
+import paper_1501_01405_b200 as w
+from conftest import GOLD
+from ir_corpus import CASES, FAULTS
+from paper_1501_01405_b200 import ir
+
+NAMES = {0: "pi", 1: "mm1", 2: "walk"}
+
+
+@pytest.mark.parametrize("model", [0, 1, 2])
+@pytest.mark.parametrize("mode,tag", [(None, "body"), (w.ExecutionMode.Tlp, "tlp"), (w.ExecutionMode.Wlp, "wlp")])
+def test_model_kernels_print_as_the_reference(model, mode, tag):
+    want = (GOLD / "ir" / f"{NAMES[model]}_{tag}.sexp").read_text()  # dump_kernel of the reference's programs
+    assert ir.model_text(w.ModelKind(model), mode) == want
+
+
+@pytest.mark.parametrize("name", sorted(CASES) + sorted(FAULTS))
+def test_canonical_text_is_a_fixpoint_and_matches_reference(ref, name):
+    text = CASES[name]["text"] if name in CASES else FAULTS[name][0]
+    once = ir.canonical(text)
+    assert ir.canonical(once) == once
+    assert once == ref.ir_canonical(text)
+
+
+def test_literals_comments_and_registers():
+    t = ir.canonical("""; header comment
+    (kernel (param o array) (local a real) (local k int)
+      (body
+        (assign a 1e5)   ; real: exponent
+        (assign a -0.0)
+        (assign a 3.)
+        (assign k -7)
+        (store o 0 (add warpsize (mul bdim.z gdim.y)))))""")
+    assert "(assign a 1e+05)" in t and "(assign a -0.0)" in t and "(assign a 3.0)" in t
+    assert "(assign k -7)" in t and "(add warpsize (mul bdim.z gdim.y))" in t
+
+
+BAD = [
+    "", "(kernel", "(kernel))", "(kernel (body (assign x 1)))", "(kernel (param x int) (param x real) (body))",
+    "(kernel (local tid.x int) (body))", "(kernel (param a array) (body (assign a 1)))",
+    "(kernel (param a array) (local x real) (body (assign x a)))", "(kernel (local x int) (body (assign x (pow 2 3))))",
+    "(kernel (local x int) (body (assign x (add 1))))", "(kernel (local x int) (body (frob x)))",
+    "(kernel (local x int) (body (if x (else (halt)))))", "(kernel (local x int) (body (halt 1)))",
+    "(kernel (local x int) (param p array) (body (load x p 0)))", "(kernel (local x int) (body) (body))",
+    "(kernel (local x float) (body))", "(kernel (param x vector) (body))", "(foo)", "(kernel) (kernel)",
+    "(kernel (local x int) (body (assign x (draw 1))))",
+]
+
+
+@pytest.mark.parametrize("text", BAD)
+def test_malformed_text_is_a_parse_error_in_both(ref, text):
+    with pytest.raises(w.ParseError):
+        ir.canonical(text)
+    with pytest.raises(Exception):
+        ref.ir_canonical(text)
+
+
+def test_parse_error_carries_a_line_reference():
+    with pytest.raises(w.ParseError, match=r"line 3"):
+        ir.canonical("(kernel (local x int)\n (body\n  (assign y 1)))")
