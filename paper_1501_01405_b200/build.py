@@ -65,7 +65,8 @@ def build_cxx(force: bool = False) -> Path:
 
 def build_cli(force: bool = False) -> Path:
     src = HOST / "cli.cpp"
-    if force or _stale(CLI, [src, ROOT / "include" / "warpsim_b200.hpp", CXXLIB]):
+    if force or _stale(CLI, [src, ROOT / "include" / "warpsim_b200.hpp", ROOT / "include" / "warpsim_ir_b200.hpp",
+                             CXXLIB]):
         _run(["g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", str(src), "-o", str(CLI), f"-L{PKG}",
               "-lwarpsim_b200", "-lwlp_b200", "-Wl,-rpath,$ORIGIN"])
     return CLI

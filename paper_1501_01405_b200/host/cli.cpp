@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "warpsim_b200.hpp"
+#include "warpsim_ir_b200.hpp"
 
 using namespace warpsim;
 
@@ -55,7 +56,7 @@ const char* kUsage =
     "usage: warpsim <sweep|steps|ci> [options]\n"
     "  common:  --model pi|mm1|walk --seed N --tlp-block-size N --profile FILE (ignored)\n"
     "           --draws N --clients N --lambda X --mu X --steps N --chunks N\n"
-    "  sweep:   --modes sequential,tlp,wlp --r-min N --r-max N --r-step N [--out FILE] [--wallclock]\n"
+    "  sweep:   --modes sequential,tlp,wlp --r-min N --r-max N --r-step N [--out FILE] [--wallclock] [--dump-kernel]\n"
     "  steps:   CSV_FILE\n"
     "  ci:      --mode wlp --replications N --level 0.95\n";
 
@@ -71,7 +72,7 @@ Args parse(int argc, char** argv) {
             if (eq != std::string::npos) {
                 val = key.substr(eq + 1);
                 key = key.substr(0, eq);
-            } else if (key == "wallclock" || key == "help") {
+            } else if (key == "wallclock" || key == "help" || key == "dump-kernel") {
                 val = "1";
             } else {
                 if (i + 1 >= argc) throw Usage("--" + key + " needs a value");
@@ -111,7 +112,6 @@ std::vector<ExecutionMode> parse_modes(const std::string& csv) {
 }
 
 int cmd_sweep(const Args& a) {
-    if (a.has("dump-kernel")) throw Usage("--dump-kernel: this engine runs hand-written kernels, there is no IR to dump");
     SweepSpec spec;
     spec.model = model_from_name(a.str("model", "pi"));
     spec.modes = parse_modes(a.str("modes", "sequential,tlp,wlp"));
@@ -121,6 +121,16 @@ int cmd_sweep(const Args& a) {
     spec.params = model_params(a);
     spec.masterSeed = a.uinteger("seed", 1);
     spec.tlpBlockSize = static_cast<int>(a.integer("tlp-block-size", 256));
+    if (a.has("dump-kernel")) {  // the IR kernel each mode would run (warpsim_main.cpp:101-110)
+        ModelParams p = spec.params;
+        p.replications = spec.rMax;
+        for (ExecutionMode mode : spec.modes) {
+            const KernelBundle b = build_kernel(spec.model, p, mode, DeviceProfile{}, spec.tlpBlockSize);
+            std::printf("; %s, %s, R=%lld\n%s\n", model_name(spec.model), mode_name(mode),
+                        static_cast<long long>(spec.rMax), dump_kernel(b.program).c_str());
+        }
+        return 0;
+    }
     const auto t0 = std::chrono::steady_clock::now();
     const std::vector<SweepRow> rows = run_sweep(spec, DeviceProfile{});
     const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

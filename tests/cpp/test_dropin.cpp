@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "warpsim_b200.hpp"
+#include "warpsim_ir_b200.hpp"
 
 extern "C" {  // oracle/oracle.c (test infrastructure)
 typedef struct {
@@ -311,11 +312,110 @@ static void gpu_tests() {
     });
 }
 
+static void ir_host_tests() {
+    test_case("IR values: promotion, truncation, comparisons, faults (kernel_ir.cpp:46-107)", [&] {
+        CHECK(apply_bin(BinOp::Div, Value::integer(-7), Value::integer(2), "t").bit_equal(Value::integer(-3)));
+        CHECK(apply_bin(BinOp::Mod, Value::integer(-7), Value::integer(2), "t").bit_equal(Value::integer(-1)));
+        CHECK(apply_bin(BinOp::Add, Value::integer(1), Value::real(0.5), "t").bit_equal(Value::real(1.5)));
+        const Value nan = Value::real(std::nan(""));
+        CHECK(apply_bin(BinOp::Le, nan, Value::real(1.0), "t").bit_equal(Value::integer(1)));
+        CHECK(apply_bin(BinOp::Lt, nan, Value::real(1.0), "t").bit_equal(Value::integer(0)));
+        CHECK(apply_un(UnOp::Floor, Value::real(-2.5), "t").bit_equal(Value::integer(-3)));
+        CHECK(!Value::real(0.0).bit_equal(Value::real(-0.0)) && nan.bit_equal(nan));
+        CHECK_THROWS_AS(apply_bin(BinOp::Div, Value::integer(1), Value::integer(0), "t"), FaultError);
+        CHECK_THROWS_AS(apply_un(UnOp::Log, Value::real(0.0), "t"), FaultError);
+    });
+    test_case("IR builder validation and kernel text round trip (kernel_text.hpp)", [&] {
+        KernelProgram p;
+        p.add_param("n", ParamKind::Int);
+        p.add_param("out", ParamKind::Array);
+        p.add_local("x", ValueType::Int);
+        CHECK_THROWS_AS(p.add_local("n", ValueType::Real), DomainError);
+        CHECK_THROWS_AS(p.param("out"), DomainError);
+        CHECK_THROWS_AS(p.load("x", "out", p.ci(0)), DomainError);  // load target must be real
+        p.body.push_back(p.assign("x", p.sreg(Sreg::TidX)));
+        p.body.push_back(KernelProgram::if_(p.bin(BinOp::Lt, p.local("x"), p.param("n")),
+                                            {p.store("out", p.local("x"), p.bin(BinOp::Mul, p.local("x"), p.cr(0.5)))}));
+        p.finalize();
+        const std::string text = dump_kernel(p);
+        CHECK(dump_kernel(parse_kernel(text)) == text);
+        CHECK_THROWS_AS(parse_kernel("(kernel (body (frob)))"), ParseError);
+        for (auto m : {ModelKind::Pi, ModelKind::Mm1, ModelKind::Walk}) {
+            const KernelProgram body = build_model_body(m);
+            CHECK(dump_kernel(parse_kernel(dump_kernel(wrap_wlp(body)))) == dump_kernel(wrap_wlp(body)));
+            CHECK_THROWS_AS(wrap_tlp(wrap_tlp(body)), DomainError);  // double wrap
+        }
+        const std::string names[] = {"pi", "mm1", "walk"};
+        for (int m = 0; m < 3; ++m)  // the reference's own dumps (tests/golden/ir)
+            CHECK(dump_kernel(wrap_tlp(build_model_body(static_cast<ModelKind>(m)))) ==
+                  slurp(root + "/tests/golden/ir/" + names[m] + "_tlp.sexp"));
+    });
+}
+
+static void ir_gpu_tests() {
+    DeviceProfile prof;
+    test_case("IR on the GPU: divergent branch, then before else, halts (test_kernel_ir.cpp:225-278)", [&] {
+        KernelProgram p;
+        p.add_param("out", ParamKind::Array);
+        p.add_local("x", ValueType::Int);
+        p.body.push_back(p.assign("x", p.sreg(Sreg::TidX)));
+        std::vector<Statement> inner{p.assign("x", p.bin(BinOp::Mul, p.local("x"), p.ci(2)))};
+        std::vector<Statement> then_body{p.assign("x", p.bin(BinOp::Add, p.local("x"), p.ci(10))),
+                                         KernelProgram::if_(p.bin(BinOp::Lt, p.local("x"), p.ci(12)), inner),
+                                         p.assign("x", p.bin(BinOp::Add, p.local("x"), p.ci(1)))};
+        p.body.push_back(KernelProgram::if_(p.bin(BinOp::Lt, p.local("x"), p.ci(4)), then_body, {KernelProgram::halt()}));
+        p.body.push_back(p.assign("x", p.bin(BinOp::Add, p.local("x"), p.ci(100))));
+        p.body.push_back(p.store("out", p.sreg(Sreg::TidX), p.local("x")));
+        p.finalize();
+        LaunchConfig cfg;
+        cfg.blockDim = {8, 1, 1};
+        cfg.warpSize = 8;
+        GlobalMemory mem;
+        mem.arrays["out"] = std::vector<double>(8, -1.0);
+        const SimReport rep = simulate(p, cfg, prof, mem, {}, {});
+        const double want[8] = {121, 123, 113, 114, -1, -1, -1, -1};
+        for (int l = 0; l < 8; ++l) CHECK(mem.arrays["out"][l] == want[l]);
+        CHECK(rep.issues == 9 && rep.divergenceEvents == 1 && rep.memWrites == 1 && rep.aluIssues == 8);
+    });
+    test_case("IR on the GPU: run_model via SimOptions::irInterpreter equals the engine", [&] {
+        ModelParams p;
+        p.replications = 40;
+        p.clients = 50;
+        p.steps = 50;
+        p.draws = 50;
+        SimOptions opts;
+        opts.irInterpreter = true;
+        for (auto m : {ModelKind::Pi, ModelKind::Mm1, ModelKind::Walk})
+            for (auto mode : {ExecutionMode::Tlp, ExecutionMode::Wlp}) {
+                const ModelRun a = run_model(m, p, mode, prof, 7, 256, opts);
+                const ModelRun b = run_model(m, p, ExecutionMode::Sequential, prof, 7);
+                CHECK(a.outputs == b.outputs);
+                CHECK(a.report.issues > 0 && a.report.memWrites > 0);
+            }
+        CHECK_THROWS_AS(run_model_ir(ModelKind::Pi, p, ExecutionMode::Sequential, prof, 7), DomainError);
+    });
+    test_case("IR on the GPU: faults are FaultError", [&] {
+        GlobalMemory mem;
+        mem.arrays["o"] = std::vector<double>(4, 0.0);
+        LaunchConfig cfg;
+        cfg.blockDim = {32, 1, 1};
+        CHECK_THROWS_AS(simulate(parse_kernel("(kernel (param o array) (body (store o tid.x 1.0)))"), cfg, prof, mem, {}, {}),
+                        FaultError);
+        CHECK_THROWS_AS(simulate(parse_kernel("(kernel (local a int) (body (assign a (div 1 (sub tid.x 5)))))"), cfg, prof,
+                                 mem, {}, {}),
+                        FaultError);
+    });
+}
+
 int main(int argc, char** argv) {
     root = argc > 2 ? argv[2] : ".";
     const bool cpu_only = argc > 1 && std::strcmp(argv[1], "--cpu") == 0;
     host_tests();
-    if (!cpu_only) gpu_tests();
+    ir_host_tests();
+    if (!cpu_only) {
+        gpu_tests();
+        ir_gpu_tests();
+    }
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail ? 1 : 0;
 }

@@ -69,3 +69,13 @@ def test_cli_sweep_steps_ci(tmp_path):
     assert r.returncode == 0 and "wait" in r.stdout and "n=30" in r.stdout
     r = _run([str(cli), "ci", "--model", "pi", "--draws", "0"])
     assert r.returncode == 2  # DomainError
+
+
+def test_cli_dump_kernel_prints_the_reference_ir():
+    # warpsim_main.cpp:101-110: `sweep --dump-kernel` prints each mode's kernel text
+    out = _run([str(PKG / "warpsim"), "sweep", "--model", "mm1", "--modes", "tlp,wlp", "--r-max", "9",
+                "--dump-kernel"])
+    assert out.returncode == 0
+    want = "".join(f"; mm1, {m}, R=9\n" + (ROOT / "tests" / "golden" / "ir" / f"mm1_{m}.sexp").read_text() + "\n"
+                   for m in ("tlp", "wlp"))
+    assert out.stdout == want
