@@ -417,6 +417,29 @@ def main():
             pms = device_timed(pstep, 5, 3, 1)
             extras["cfg5_plan_mm1_64x30x1e4"][w.mode_name(md)] = {
                 "reps_per_s": 1920 / (pms * 1e-3), "ms_per_run": pms, "kernel_ms": sum(kms[3:]) / len(kms[3:])}
+        # the reference's own IR kernel (TLP walk) on the GPU IR interpreter:
+        # statements issued per second, counters exact; the reference's host simulator on
+        # a 10x smaller sample beside it when the CPU legs run
+        from paper_1501_01405_b200 import ir
+
+        pir = w.ModelParams(replications=20_000, steps=1000, chunks=30)
+        runs = [ir.run_model(w.ModelKind.Walk, pir, w.ExecutionMode.Tlp, SEED) for _ in range(3)]
+        kms = min(r.report.kernel_ms for r in runs)
+        extras["ir_walk_tlp_2e4x1e3"] = {"kernel_ms": kms, "issues": runs[-1].report.issues,
+                                         "divergence_events": runs[-1].report.divergenceEvents,
+                                         "issues_per_s": runs[-1].report.issues / (kms * 1e-3)}
+        if not args.no_cpu:
+            try:
+                import oracle
+
+                t0 = time.perf_counter()
+                rr = oracle.Oracle("reference").run_model_report(2, oracle.params(replications=2000, steps=1000,
+                                                                                  chunks=30), SEED, 1)
+                dt = time.perf_counter() - t0
+                extras["ir_walk_tlp_2e4x1e3"]["reference_simulator"] = {
+                    "sample": "R=2000 (1 host thread)", "seconds": dt, "issues_per_s": rr["issues"] / dt}
+            except Exception as e:  # pragma: no cover - oracle/_ref absent
+                extras["ir_walk_tlp_2e4x1e3"]["reference_simulator"] = {"unavailable": str(e)}
         line["extras"] = extras
     if world == 1 and rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = {k: v for k, v in cpu_baseline(0, p).items() if k != "step_s"}

@@ -22,9 +22,18 @@ ap.add_argument("R", type=int)
 ap.add_argument("N", type=int)
 ap.add_argument("--repeat", type=int, default=2)
 ap.add_argument("--counters", action="store_true", help="instrumented kernels; print the SimReport tallies")
+ap.add_argument("--ir", action="store_true", help="run the reference's IR kernel on the GPU IR interpreter")
+ap.add_argument("--lambda", dest="lam", type=float, default=0.5)
 a = ap.parse_args()
 m = w.model_from_name(a.model)
-p = w.ModelParams(replications=a.R, draws=a.N, clients=a.N, steps=a.N)
+p = w.ModelParams(replications=a.R, draws=a.N, clients=a.N, steps=a.N, lambda_=a.lam)
+if a.ir:
+    from paper_1501_01405_b200 import ir
+
+    for _ in range(a.repeat):
+        run = ir.run_model(m, p, w.mode_from_name(a.mode), 42)
+    print(a.model, a.mode, a.R, a.N, "IR", "mean", float(run.primary.mean()), "report", run.report)
+    sys.exit(0)
 outs = [torch.empty(a.R, dtype=torch.float64, device="cuda") for _ in w.OUTPUT_NAMES[m]]
 rep = w.SimReport()
 ctx = w.hw_counters() if a.counters else None
