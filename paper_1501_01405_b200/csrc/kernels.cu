@@ -463,14 +463,16 @@ constexpr size_t kMm1Smem = kUniTabWords * 4 + 256 * 8 + (kMm1Block / 32) * size
 // One client of the Lindley recursion, models.hpp:67-78 in the reference's rounding:
 // t = (w + s_prev) - a with u = fl(w + s_prev) carried from the previous client (it is
 // the previous client's sums term, the same fl(w + s)); w = t < 0 ? 0 : t; u = fl(w + s).
-// * w = fmax(t, +0) is the branch: t is never -0 or NaN here (u >= +0, a finite), so
-//   both give +0 for t < 0 and t otherwise.
+// * The branch is w = t < 0 ? +0 : t. t is never -0 or NaN here (u >= +0, a finite), so
+//   clearing both words when the sign bit is set is the same; it is two integer ops
+//   (DMNMX / DSETP would put 8-25 cycles of FP64 latency on the recursion's chain).
 // * d is the idle increment, d = fl(w - t): -t when dry, +0 otherwise, exactly. idle - t
 //   == idle + (-t), and idle + (+0) == idle (idle >= +0), so the reference's conditional
 //   `idle = idle - t` becomes a plain ordered sum of d like the other two.
 __device__ __forceinline__ void lindley(double& w, double& u, double a, double s, double& d) {
     const double t = __dsub_rn(u, a);
-    w = fmax(t, 0.0);
+    const int hi = __double2hiint(t), keep = ~(hi >> 31);
+    w = __hiloint2double(hi & keep, __double2loint(t) & keep);
     d = __dsub_rn(w, t);
     u = __dadd_rn(w, s);
 }
@@ -553,7 +555,7 @@ __device__ __forceinline__ double mm1_warp_rep(Taus st, int64_t n, double lambda
                     term[c] = w;
                     term[kMm1Arr + c] = u;
                     term[2 * kMm1Arr + c] = d;
-                    run = w != 0.0;  // met the previous trajectory: the rest is unchanged
+                    run = (__double2hiint(w) | __double2loint(w)) != 0;  // w == +0: met the old trajectory
                     if (c == T - 1 && run) end = w;
                 }
             }
