@@ -247,6 +247,23 @@ def cpu_baseline(model: int, p, budget_s: float = 15.0, steps: int = 1):
             "step_s": tsp + trep}
 
 
+def ir_simulator_baseline() -> dict:
+    """The reference's own simulator (simulate, device.cpp:140-226 via run_model Tlp) on the
+    IR walk that extras.ir_walk_tlp_2e4x1e3 runs on the GPU interpreter, on a 10x smaller
+    sample (R = 2000, 1 host thread: the simulator is single-threaded)."""
+    try:
+        import oracle
+
+        t0 = time.perf_counter()
+        rr = oracle.Oracle("reference").run_model_report(2, oracle.params(replications=2000, steps=1000, chunks=30),
+                                                         SEED, 1)
+        dt = time.perf_counter() - t0
+        return {"sample": "walk TLP R=2000 x 1000 steps, 1 host thread", "seconds": dt, "issues": rr["issues"],
+                "issues_per_s": rr["issues"] / dt, "cores": 1, "kind": "reference"}
+    except Exception as e:  # pragma: no cover - oracle/_ref absent
+        return {"unavailable": str(e)}
+
+
 def run_reference_arm(args):
     """--impl reference: the reference CPU path on this box's host cores."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -428,21 +445,11 @@ def main():
         extras["ir_walk_tlp_2e4x1e3"] = {"kernel_ms": kms, "issues": runs[-1].report.issues,
                                          "divergence_events": runs[-1].report.divergenceEvents,
                                          "issues_per_s": runs[-1].report.issues / (kms * 1e-3)}
-        if not args.no_cpu:
-            try:
-                import oracle
-
-                t0 = time.perf_counter()
-                rr = oracle.Oracle("reference").run_model_report(2, oracle.params(replications=2000, steps=1000,
-                                                                                  chunks=30), SEED, 1)
-                dt = time.perf_counter() - t0
-                extras["ir_walk_tlp_2e4x1e3"]["reference_simulator"] = {
-                    "sample": "R=2000 (1 host thread)", "seconds": dt, "issues_per_s": rr["issues"] / dt}
-            except Exception as e:  # pragma: no cover - oracle/_ref absent
-                extras["ir_walk_tlp_2e4x1e3"]["reference_simulator"] = {"unavailable": str(e)}
         line["extras"] = extras
     if world == 1 and rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = {k: v for k, v in cpu_baseline(0, p).items() if k != "step_s"}
+        if "extras" in line:  # the reference's host simulator beside the GPU IR interpreter
+            line["cpu_baseline"]["ir_reference_simulator"] = ir_simulator_baseline()
     if rank == 0:
         print(json.dumps(line), flush=True)
     import torch.distributed as dist
