@@ -239,6 +239,7 @@ _SIGS = {
     "wlp_last_error": (C.c_char_p, []),
     "wlp_version": (C.c_int, []),
     "wlp_set_hw_counters": (C.c_int, [C.c_int]),
+    "wlp_set_wlp_variant": (C.c_int, [C.c_int]),
     "wlp_validate_params": (C.c_int, [C.c_int, C.POINTER(_Params), C.c_char_p, C.c_int]),
     "wlp_plan_launch": (C.c_int, [_I64, C.c_int, C.c_int, _I64, C.POINTER(_Cfg), C.c_char_p, C.c_int]),
     "wlp_master_from_seed": (C.c_int, [C.c_uint64, _P]),
@@ -487,6 +488,21 @@ def walk_replication(steps: int, chunks: int, stream: RngState) -> float:
     """walk_replication (models.cpp:56-59)."""
     s = np.array([[stream.s1], [stream.s2], [stream.s3]], dtype=np.uint32)
     return float(run_streams(ModelKind.Walk, ModelParams(steps=steps, chunks=chunks), ExecutionMode.Wlp, s)["out"][0])
+
+
+class wlp_variant:
+    """Context manager selecting the WLP pi/walk kernel for calls on this thread:
+    0 automatic, 1 lane jumps, 2 warp pipeline (outputs identical; wlp_set_wlp_variant)."""
+
+    def __init__(self, variant: int):
+        self.variant = int(variant)
+
+    def __enter__(self):
+        _check(_lib.wlp_set_wlp_variant(self.variant))
+        return self
+
+    def __exit__(self, *exc):
+        _check(_lib.wlp_set_wlp_variant(0))
 
 
 class hw_counters:

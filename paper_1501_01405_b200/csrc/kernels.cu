@@ -445,6 +445,78 @@ __global__ void __launch_bounds__(kWlpBlock, 3) k_wlp_lanes(RepArgs a, const uin
     if (COUNT) flush_tally(hw, a.hw);
 }
 
+// WLP as a systolic warp pipeline (pi / walk, many short replications per warp). Lane l
+// still owns units [l*K, (l+1)*K) of every replication, but instead of each lane jumping
+// its stream ahead (lane_jump: ~24 table reads per lane per replication), replication r
+// enters at lane 0 and moves one lane per step: at step t lane l runs its chunk of the
+// replication that entered at step t - l, starting from the stream state lane l-1 ended
+// with (its chunk ends exactly where chunk l begins), and passes (state, partial sum,
+// index) up with __shfl_up_sync. Lane 31 completes a replication every step; finished
+// sums collect in shared memory and 32 of them are finalised and stored by the 32 lanes
+// at once. No jump tables at all; the cost is the 31-step drain per warp, so the launcher
+// picks this kernel when replications per warp are many and units per replication few
+// (config 4: 1400 replications of 32 units per lane).
+template <int MODEL>
+__global__ void __launch_bounds__(kWlpBlock, 3) k_wlp_pipe(RepArgs a, int64_t K) {
+    __shared__ long long emit_rep[kWlpBlock / 32][32];
+    __shared__ long long emit_sum[kWlpBlock / 32][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int64_t mine = a.n - static_cast<int64_t>(lane) * K;
+    mine = mine < 0 ? 0 : (mine > K ? K : mine);
+    const uint32_t units = static_cast<uint32_t>(mine);
+    Taus st{kMin1, kMin2, kMin3};
+    long long sum = 0, rep = -1;
+    int64_t cur = 0, cend = 0;  // lane 0's current group of replications (warp-uniform)
+    bool more = true;
+    int nemit = 0;
+    auto flush = [&](int cnt) {
+        __syncwarp();
+        if (lane < cnt) {
+            const long long r = emit_rep[wid][lane], c = emit_sum[wid][lane];
+            a.out0[r] = MODEL == 0 ? __ddiv_rn(__dmul_rn(4.0, static_cast<double>(c)), static_cast<double>(a.n))
+                                   : walk_fold(c, a.chunks);
+        }
+        __syncwarp();
+    };
+    for (;;) {
+        if (more && cur >= cend) {  // next group from the global counter
+            const int64_t base = grab_take(grab_issue(a, lane));
+            if (base >= a.count) {
+                more = false;
+            } else {
+                cur = base;
+                cend = base + a.grab < a.count ? base + a.grab : a.count;
+            }
+        }
+        if (lane == 0) {  // feed
+            rep = more ? cur : -1;
+            if (more) {
+                st = load_seed(a, cur);
+                sum = 0;
+            }
+        }
+        if (more) ++cur;
+        if (!__any_sync(kFull, rep >= 0)) break;
+        if (rep >= 0) sum += MODEL == 0 ? static_cast<long long>(pi_hits(st, units)) : walk_dx(st, units);
+        if (__shfl_sync(kFull, rep, 31) >= 0) {  // lane 31 finished a replication
+            if (lane == 31) {
+                emit_rep[wid][nemit] = rep;
+                emit_sum[wid][nemit] = sum;
+            }
+            if (++nemit == 32) {
+                flush(32);
+                nemit = 0;
+            }
+        }
+        st.s1 = __shfl_up_sync(kFull, st.s1, 1);
+        st.s2 = __shfl_up_sync(kFull, st.s2, 1);
+        st.s3 = __shfl_up_sync(kFull, st.s3, 1);
+        sum = __shfl_up_sync(kFull, sum, 1);
+        rep = __shfl_up_sync(kFull, rep, 1);
+    }
+    flush(nemit);
+}
+
 // mm1 WLP shared memory: lane-start tables, panel-skip table, log table, then per warp
 // the panel's per-client terms of the three ordered sums and the near-one compaction list.
 constexpr int kMm1P = 32 * kMm1PanelT;
@@ -1084,6 +1156,21 @@ cudaError_t launch_wlp(int model, const RepArgs& a, const uint32_t* lane_tab, co
             count ? go(k_wlp_lanes<2, true>) : go(k_wlp_lanes<2, false>);
     }
     return cudaGetLastError();
+}
+
+cudaError_t launch_wlp_pipe(int model, const RepArgs& a, int64_t lane_units, int grid, cudaStream_t st) {
+    if (a.count <= 0) return cudaSuccess;
+    if (model == 0)
+        k_wlp_pipe<0><<<grid, kWlpBlock, 0, st>>>(a, lane_units);
+    else
+        k_wlp_pipe<2><<<grid, kWlpBlock, 0, st>>>(a, lane_units);
+    return cudaGetLastError();
+}
+
+int wlp_pipe_blocks_per_sm() {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_pipe<0>, kWlpBlock, 0);
+    return nb < 1 ? 1 : nb;
 }
 
 cudaError_t launch_tlp(int model, const RepArgs& a, int tlp_block, cudaStream_t st) {

@@ -28,6 +28,7 @@ namespace {
 
 thread_local std::string g_err;
 thread_local bool g_hw_counters = false;  // wlp_set_hw_counters
+thread_local int g_wlp_variant = 0;       // wlp_set_wlp_variant: 0 auto, 1 lane jumps, 2 pipeline
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
@@ -77,6 +78,7 @@ struct DevCtx {
     int sms = 0;
     int clock_khz = 0;
     int wlp_bps[3] = {1, 1, 1};
+    int pipe_bps = 1;
     std::mutex mu;
     bool ready = false;
     DevBuf<uint32_t> powers;
@@ -117,6 +119,7 @@ int ctx_init(DevCtx& c) {
     WLP_TRY(upload_u32(c.mm1_skip, uniform_table(2ull * 31 * kMm1PanelT)));
     WLP_TRY(upload_u32(c.plan_lane, lane_tables(2ull * kPlanT)));
     WLP_TRY(upload_u32(c.plan_skip, uniform_table(2ull * 31 * kPlanT)));
+    c.pipe_bps = wlp_pipe_blocks_per_sm();
     for (int m = 0; m < 3; ++m) {
         c.wlp_bps[m] = wlp_blocks_per_sm(m);
         c.plan_bps[m] = plan_blocks_per_sm(m);
@@ -428,9 +431,21 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
         WLP_CUDA(launch_wlp(model, a, c.mm1_lane.p, c.mm1_skip.p, 0, grid_out, st));
     } else {
         const int64_t K = (a.n + 31) / 32;
-        const uint32_t* tab = nullptr;
-        WLP_TRY(lane_table(c, 2ull * static_cast<uint64_t>(K), tab));
-        WLP_CUDA(launch_wlp(model, a, tab, nullptr, K, grid_out, st));
+        // Lane jumps cost ~80 instructions per lane per replication against K units of
+        // ~35-39; the pipeline costs a 31-step drain per warp against its replications.
+        const double per_warp = static_cast<double>(count) / static_cast<double>(warps);
+        const bool pipe = !g_hw_counters &&
+                          (g_wlp_variant == 2 ||
+                           (g_wlp_variant == 0 && 31.0 / (per_warp + 31.0) < 80.0 / (35.0 * K + 80.0)));
+        if (pipe) {
+            const int64_t cap = static_cast<int64_t>(c.sms) * c.pipe_bps;
+            grid_out = static_cast<int>(std::min<int64_t>(grid_out, cap));
+            WLP_CUDA(launch_wlp_pipe(model, a, K, grid_out, st));
+        } else {
+            const uint32_t* tab = nullptr;
+            WLP_TRY(lane_table(c, 2ull * static_cast<uint64_t>(K), tab));
+            WLP_CUDA(launch_wlp(model, a, tab, nullptr, K, grid_out, st));
+        }
     }
     return WLP_OK;
 }
@@ -535,6 +550,12 @@ extern "C" {
 
 const char* wlp_last_error(void) { return g_err.c_str(); }
 int wlp_version(void) { return 1; }
+
+int wlp_set_wlp_variant(int variant) {
+    if (variant < 0 || variant > 2) return fail(WLP_EDOMAIN, "wlp variant must be 0 (auto), 1 or 2");
+    g_wlp_variant = variant;
+    return WLP_OK;
+}
 
 int wlp_set_hw_counters(int enable) {
     g_hw_counters = enable != 0;

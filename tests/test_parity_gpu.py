@@ -276,3 +276,29 @@ def test_full_size_wlp_equals_tlp_and_sampled_oracle(gpu, ref, model, kw):
         assert abs(wlp[0].mean() - np.pi) < 1e-3
     if model == 2:
         assert wlp[0].min() >= 0 and wlp[0].max() < kw["chunks"] and np.all(wlp[0] == np.floor(wlp[0]))
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("model,kw", [(0, dict(replications=5000, draws=1000)), (0, dict(replications=777, draws=31)),
+                                      (0, dict(replications=3, draws=5000)), (0, dict(replications=2000, draws=1)),
+                                      (2, dict(replications=4099, steps=1000, chunks=30)),
+                                      (2, dict(replications=100, steps=33, chunks=7)),
+                                      (2, dict(replications=1, steps=70, chunks=4))])
+def test_wlp_lane_jump_and_pipeline_kernels_agree_with_oracle(gpu, port, variant, model, kw):
+    # the two WLP kernels for pi / walk (lane jumps, warp pipeline) give the reference's bits
+    p = gpu.ModelParams(**kw)
+    want = port.run_model(model, oracle.params_from(p), 777)
+    with gpu.wlp_variant(variant):
+        run = gpu.run_model(gpu.ModelKind(model), p, gpu.ExecutionMode.Wlp, master_seed=777)
+    assert np.array_equal(run.primary, want["out"])
+
+
+@pytest.mark.parametrize("model,kw", [(0, dict(replications=10_000_000, draws=1000)),
+                                      (2, dict(replications=10_000_000, steps=1000, chunks=30))])
+def test_pipeline_full_size_equals_lane_jumps(gpu, model, kw):
+    p = gpu.ModelParams(**kw)
+    outs = {}
+    for v in (1, 2):
+        with gpu.wlp_variant(v):
+            outs[v] = _device_run(gpu, model, p, gpu.ExecutionMode.Wlp, 42)[0]
+    assert np.array_equal(outs[1], outs[2])
