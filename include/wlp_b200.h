@@ -120,10 +120,12 @@ int wlp_version(void);              /* ABI version (1)                          
  * Costs some speed; off by default. */
 int wlp_set_hw_counters(int enable);
 
-/* Tuning / test hook for later calls on this thread: which WLP kernel runs pi and walk.
- * 0 = automatic (default), 1 = lane jumps (each lane jumps its stream to its chunk), 2 =
- * warp pipeline (replications move lane to lane; no jumps, a 31-step drain per warp).
- * Outputs are identical; only speed differs. */
+/* Tuning / test hook for later calls on this thread: which WLP kernel runs a model.
+ * 0 = automatic (default); 1 = lane jumps (pi / walk: each lane jumps its stream to its
+ * chunk; mm1: segment chaining by fixed-point rounds); 2 = warp pipeline (replications
+ * move lane to lane, each lane runs its segment in order from the state its neighbour
+ * hands over; a 31-step drain per warp). Outputs are identical; only speed differs
+ * (DESIGN.md §4). */
 int wlp_set_wlp_variant(int variant);
 
 /* validate_params (models.cpp:26-44): WLP_EDOMAIN on invalid values; a non-empty

@@ -845,6 +845,113 @@ __device__ __forceinline__ Queue mm1_thread_rep(Taus st, int64_t n, int64_t n_wa
     return q;
 }
 
+// mm1 WLP as a warp pipeline (many replications per warp). Replication r enters at lane
+// 0 and moves one lane per step; lane l runs clients [l*K, (l+1)*K) of it strictly in
+// order (the reference's recursion and ordered sums, models.hpp:65-79) from the queue
+// and stream state lane l-1 hands over, so every operation happens in the reference's
+// order on one lane and no chaining rounds or separate sum phase are needed. All 32 lanes
+// work every step (each on a different replication's segment); the exponentials go
+// through the warp-cooperative log batches as in TLP. Draws of a segment's last, partial
+// batch are predicated so each lane hands over the state exactly at its segment's end.
+template <bool INV>
+__device__ __forceinline__ void mm1_segment(Taus& st, Queue& q, uint32_t units, uint32_t units_max, double lambda,
+                                            double mu, double inv_l, double inv_m, const double* logtab,
+                                            TlpMm1Warp& W, int lane) {
+    for (uint32_t done = 0; done < units_max; done += kExpoB / 2) {
+        const int cnt = units <= done ? 0 : (units - done < kExpoB / 2 ? static_cast<int>(units - done) : kExpoB / 2);
+        uint32_t d[kExpoB];
+        double e[kExpoB];
+#pragma unroll
+        for (int j = 0; j < kExpoB; ++j) d[j] = j < 2 * cnt ? taus_next(st) : 0u;
+        neg_log1m_batch<kExpoB, true>(d, e, logtab, W.nl, W.res, kFull, lane);
+#pragma unroll
+        for (int c = 0; c < kExpoB / 2; ++c)
+            if (c < cnt) q.client(scale<INV>(e[2 * c], lambda, inv_l), scale<INV>(e[2 * c + 1], mu, inv_m));
+    }
+}
+
+struct Mm1PipeWarp {
+    TlpMm1Warp tw;
+    long long rep[32];
+    double sums[32][3];  // idle, sumw, sums
+};
+
+template <bool INV>
+__global__ void __launch_bounds__(kMm1Block, 3) k_wlp_mm1_pipe(RepArgs a, int64_t K) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double* logtab = reinterpret_cast<double*>(smraw);
+    Mm1PipeWarp& P = reinterpret_cast<Mm1PipeWarp*>(logtab + 256)[threadIdx.x >> 5];
+    stage_log_table(logtab);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    int64_t mine = a.n - static_cast<int64_t>(lane) * K;
+    mine = mine < 0 ? 0 : (mine > K ? K : mine);
+    const uint32_t seg = static_cast<uint32_t>(mine), seg_max = static_cast<uint32_t>(K);
+    const double nd = static_cast<double>(a.n);
+    Taus st{kMin1, kMin2, kMin3};
+    Queue q;
+    long long rep = -1;
+    int64_t cur = 0, cend = 0;
+    bool more = true;
+    int nemit = 0;
+    auto flush = [&](int cnt) {
+        __syncwarp();
+        if (lane < cnt) {
+            const long long r = P.rep[lane];
+            a.out0[r] = __ddiv_rn(P.sums[lane][0], nd);
+            a.out1[r] = __ddiv_rn(P.sums[lane][1], nd);
+            a.out2[r] = __ddiv_rn(P.sums[lane][2], nd);
+        }
+        __syncwarp();
+    };
+    for (;;) {
+        if (more && cur >= cend) {
+            const int64_t base = grab_take(grab_issue(a, lane));
+            if (base >= a.count) {
+                more = false;
+            } else {
+                cur = base;
+                cend = base + a.grab < a.count ? base + a.grab : a.count;
+            }
+        }
+        if (lane == 0) {  // feed: a fresh queue on the next replication's stream
+            rep = more ? cur : -1;
+            if (more) {
+                st = load_seed(a, cur);
+                q = Queue();
+            }
+        }
+        if (more) ++cur;
+        if (!__any_sync(kFull, rep >= 0)) break;
+        mm1_segment<INV>(st, q, rep >= 0 ? seg : 0u, seg_max, a.lambda, a.mu, a.inv_lambda, a.inv_mu, logtab, P.tw,
+                         lane);
+        if (__shfl_sync(kFull, rep, 31) >= 0) {  // lane 31 finished a replication
+            if (lane == 31) {
+                P.rep[nemit] = rep;
+                P.sums[nemit][0] = q.idle;
+                P.sums[nemit][1] = q.sumw;
+                P.sums[nemit][2] = q.sums;
+            }
+            if (++nemit == 32) {
+                flush(32);
+                nemit = 0;
+            }
+        }
+        st.s1 = __shfl_up_sync(kFull, st.s1, 1);
+        st.s2 = __shfl_up_sync(kFull, st.s2, 1);
+        st.s3 = __shfl_up_sync(kFull, st.s3, 1);
+        q.w = __shfl_up_sync(kFull, q.w, 1);
+        q.s = __shfl_up_sync(kFull, q.s, 1);
+        q.idle = __shfl_up_sync(kFull, q.idle, 1);
+        q.sumw = __shfl_up_sync(kFull, q.sumw, 1);
+        q.sums = __shfl_up_sync(kFull, q.sums, 1);
+        rep = __shfl_up_sync(kFull, rep, 1);
+    }
+    flush(nemit);
+}
+
+constexpr size_t kMm1PipeSmem = 256 * 8 + (kMm1Block / 32) * sizeof(Mm1PipeWarp);
+
 __device__ __forceinline__ unsigned block_lane_mask() {  // partial last warp of odd-sized blocks
     const int in_warp = static_cast<int>(blockDim.x) - (static_cast<int>(threadIdx.x) & ~31);
     return in_warp >= 32 ? kFull : ((1u << in_warp) - 1u);
@@ -1165,6 +1272,23 @@ cudaError_t launch_wlp_pipe(int model, const RepArgs& a, int64_t lane_units, int
     else
         k_wlp_pipe<2><<<grid, kWlpBlock, 0, st>>>(a, lane_units);
     return cudaGetLastError();
+}
+
+cudaError_t launch_wlp_mm1_pipe(const RepArgs& a, int64_t lane_units, int grid, cudaStream_t st) {
+    if (a.count <= 0) return cudaSuccess;
+    if (a.inv_lambda != 0.0 && a.inv_mu != 0.0)
+        k_wlp_mm1_pipe<true><<<grid, kMm1Block, kMm1PipeSmem, st>>>(a, lane_units);
+    else
+        k_wlp_mm1_pipe<false><<<grid, kMm1Block, kMm1PipeSmem, st>>>(a, lane_units);
+    return cudaGetLastError();
+}
+
+int wlp_mm1_pipe_blocks_per_sm() {
+    int nb = 0;
+    allow_smem(k_wlp_mm1_pipe<true>, kMm1PipeSmem);
+    allow_smem(k_wlp_mm1_pipe<false>, kMm1PipeSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_mm1_pipe<false>, kMm1Block, kMm1PipeSmem);
+    return nb < 1 ? 1 : nb;
 }
 
 int wlp_pipe_blocks_per_sm() {

@@ -107,6 +107,9 @@ cudaError_t launch_wlp(int model, const RepArgs& a, const uint32_t* lane_tab,
 // WLP as a warp pipeline (pi / walk): no lane jumps; lane_units = ceil(n / 32).
 cudaError_t launch_wlp_pipe(int model, const RepArgs& a, int64_t lane_units, int grid, cudaStream_t st);
 int wlp_pipe_blocks_per_sm();
+// mm1 WLP as a warp pipeline: lane_units = ceil(clients / 32).
+cudaError_t launch_wlp_mm1_pipe(const RepArgs& a, int64_t lane_units, int grid, cudaStream_t st);
+int wlp_mm1_pipe_blocks_per_sm();
 // TLP: thread per replication, block = tlp_block, grid = ceil(count / tlp_block).
 cudaError_t launch_tlp(int model, const RepArgs& a, int tlp_block, cudaStream_t st);
 // Plan: batched seeding (specials carry the job index in `pad`), then one model launch.

@@ -78,7 +78,7 @@ struct DevCtx {
     int sms = 0;
     int clock_khz = 0;
     int wlp_bps[3] = {1, 1, 1};
-    int pipe_bps = 1;
+    int pipe_bps = 1, mm1_pipe_bps = 1;
     std::mutex mu;
     bool ready = false;
     DevBuf<uint32_t> powers;
@@ -120,6 +120,7 @@ int ctx_init(DevCtx& c) {
     WLP_TRY(upload_u32(c.plan_lane, lane_tables(2ull * kPlanT)));
     WLP_TRY(upload_u32(c.plan_skip, uniform_table(2ull * 31 * kPlanT)));
     c.pipe_bps = wlp_pipe_blocks_per_sm();
+    c.mm1_pipe_bps = wlp_mm1_pipe_blocks_per_sm();
     for (int m = 0; m < 3; ++m) {
         c.wlp_bps[m] = wlp_blocks_per_sm(m);
         c.plan_bps[m] = plan_blocks_per_sm(m);
@@ -428,7 +429,18 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
     a.next = c.work.p;
     WLP_CUDA(cudaMemsetAsync(c.work.p, 0, sizeof(unsigned long long), st));
     if (model == WLP_MODEL_MM1) {
-        WLP_CUDA(launch_wlp(model, a, c.mm1_lane.p, c.mm1_skip.p, 0, grid_out, st));
+        // The pipeline runs each segment's recursion and sums in order on one lane (TLP's
+        // per-client cost) but drains 31 steps per warp; segment chaining pays ~1.8x per
+        // client but has no drain. Pipeline when the drain is the smaller loss.
+        const double per_warp = static_cast<double>(count) / static_cast<double>(warps);
+        const bool pipe = !g_hw_counters && (g_wlp_variant == 2 || (g_wlp_variant == 0 && per_warp > 64.0));
+        if (pipe) {
+            const int64_t cap = static_cast<int64_t>(c.sms) * c.mm1_pipe_bps;
+            grid_out = static_cast<int>(std::min<int64_t>(grid_out, cap));
+            WLP_CUDA(launch_wlp_mm1_pipe(a, (a.n + 31) / 32, grid_out, st));
+        } else {
+            WLP_CUDA(launch_wlp(model, a, c.mm1_lane.p, c.mm1_skip.p, 0, grid_out, st));
+        }
     } else {
         const int64_t K = (a.n + 31) / 32;
         // Lane jumps cost ~80 instructions per lane per replication against K units of

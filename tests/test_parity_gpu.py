@@ -283,22 +283,30 @@ def test_full_size_wlp_equals_tlp_and_sampled_oracle(gpu, ref, model, kw):
                                       (0, dict(replications=3, draws=5000)), (0, dict(replications=2000, draws=1)),
                                       (2, dict(replications=4099, steps=1000, chunks=30)),
                                       (2, dict(replications=100, steps=33, chunks=7)),
-                                      (2, dict(replications=1, steps=70, chunks=4))])
+                                      (2, dict(replications=1, steps=70, chunks=4)),
+                                      (1, dict(replications=3000, clients=1000)),
+                                      (1, dict(replications=500, clients=37, lambda_=0.9, mu=1.0)),
+                                      (1, dict(replications=64, clients=5, lambda_=2.0, mu=1.0)),
+                                      (1, dict(replications=2, clients=3000, lambda_=0.7, mu=0.75))])
 def test_wlp_lane_jump_and_pipeline_kernels_agree_with_oracle(gpu, port, variant, model, kw):
-    # the two WLP kernels for pi / walk (lane jumps, warp pipeline) give the reference's bits
+    # the two WLP kernels of each model (pi / walk: lane jumps or warp pipeline; mm1:
+    # segment chaining or warp pipeline) give the reference's bits
     p = gpu.ModelParams(**kw)
     want = port.run_model(model, oracle.params_from(p), 777)
     with gpu.wlp_variant(variant):
         run = gpu.run_model(gpu.ModelKind(model), p, gpu.ExecutionMode.Wlp, master_seed=777)
-    assert np.array_equal(run.primary, want["out"])
+    for name in oracle.OUTPUTS[model]:
+        assert np.array_equal(run.outputs[name], want[name]), name
 
 
 @pytest.mark.parametrize("model,kw", [(0, dict(replications=10_000_000, draws=1000)),
-                                      (2, dict(replications=10_000_000, steps=1000, chunks=30))])
+                                      (2, dict(replications=10_000_000, steps=1000, chunks=30)),
+                                      (1, dict(replications=2_000_000, clients=1000))])
 def test_pipeline_full_size_equals_lane_jumps(gpu, model, kw):
     p = gpu.ModelParams(**kw)
     outs = {}
     for v in (1, 2):
         with gpu.wlp_variant(v):
-            outs[v] = _device_run(gpu, model, p, gpu.ExecutionMode.Wlp, 42)[0]
-    assert np.array_equal(outs[1], outs[2])
+            outs[v] = _device_run(gpu, model, p, gpu.ExecutionMode.Wlp, 42)
+    for a, b in zip(outs[1], outs[2]):
+        assert np.array_equal(a, b)
