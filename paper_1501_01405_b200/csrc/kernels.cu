@@ -830,7 +830,7 @@ __device__ __forceinline__ Queue mm1_thread_rep(Taus st, int64_t n, int64_t n_wa
         uint32_t d[kExpoB];
         double e[kExpoB];
 #pragma unroll
-        for (int j = 0; j < kExpoB; ++j) d[j] = taus_next(st);
+        for (int j = 0; j < kExpoB; j += 2) taus_next2(st, d[j], d[j + 1]);
         neg_log1m_batch<kExpoB, FULL>(d, e, logtab, W.nl, W.res, mask, lane);
         const int64_t left = n - done;
         const int cnt = left <= 0 ? 0 : (left < kExpoB / 2 ? static_cast<int>(left) : kExpoB / 2);
@@ -853,7 +853,10 @@ __device__ __forceinline__ Queue mm1_thread_rep(Taus st, int64_t n, int64_t n_wa
 // work every step (each on a different replication's segment); the exponentials go
 // through the warp-cooperative log batches as in TLP. Draws of a segment's last, partial
 // batch are predicated so each lane hands over the state exactly at its segment's end.
-template <bool INV>
+// EXACT = false: every lane whose hand-over state matters (lanes 0-30) has whole batches
+// (31*K <= n and K % 4 == 0), so draws need no predication (lane 31, and lanes between
+// replications, may overdraw: their stream state is never handed over).
+template <bool INV, bool EXACT>
 __device__ __forceinline__ void mm1_segment(Taus& st, Queue& q, uint32_t units, uint32_t units_max, double lambda,
                                             double mu, double inv_l, double inv_m, const double* logtab,
                                             TlpMm1Warp& W, int lane) {
@@ -861,8 +864,13 @@ __device__ __forceinline__ void mm1_segment(Taus& st, Queue& q, uint32_t units, 
         const int cnt = units <= done ? 0 : (units - done < kExpoB / 2 ? static_cast<int>(units - done) : kExpoB / 2);
         uint32_t d[kExpoB];
         double e[kExpoB];
+        if (EXACT) {
 #pragma unroll
-        for (int j = 0; j < kExpoB; ++j) d[j] = j < 2 * cnt ? taus_next(st) : 0u;
+            for (int j = 0; j < kExpoB; ++j) d[j] = j < 2 * cnt ? taus_next(st) : 0u;
+        } else {
+#pragma unroll
+            for (int j = 0; j < kExpoB; j += 2) taus_next2(st, d[j], d[j + 1]);
+        }
         neg_log1m_batch<kExpoB, true>(d, e, logtab, W.nl, W.res, kFull, lane);
 #pragma unroll
         for (int c = 0; c < kExpoB / 2; ++c)
@@ -876,7 +884,7 @@ struct Mm1PipeWarp {
     double sums[32][3];  // idle, sumw, sums
 };
 
-template <bool INV>
+template <bool INV, bool EXACT>
 __global__ void __launch_bounds__(kMm1Block, 3) k_wlp_mm1_pipe(RepArgs a, int64_t K) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double* logtab = reinterpret_cast<double*>(smraw);
@@ -923,8 +931,8 @@ __global__ void __launch_bounds__(kMm1Block, 3) k_wlp_mm1_pipe(RepArgs a, int64_
         }
         if (more) ++cur;
         if (!__any_sync(kFull, rep >= 0)) break;
-        mm1_segment<INV>(st, q, rep >= 0 ? seg : 0u, seg_max, a.lambda, a.mu, a.inv_lambda, a.inv_mu, logtab, P.tw,
-                         lane);
+        mm1_segment<INV, EXACT>(st, q, rep >= 0 ? seg : 0u, seg_max, a.lambda, a.mu, a.inv_lambda, a.inv_mu, logtab,
+                                P.tw, lane);
         if (__shfl_sync(kFull, rep, 31) >= 0) {  // lane 31 finished a replication
             if (lane == 31) {
                 P.rep[nemit] = rep;
@@ -1276,18 +1284,22 @@ cudaError_t launch_wlp_pipe(int model, const RepArgs& a, int64_t lane_units, int
 
 cudaError_t launch_wlp_mm1_pipe(const RepArgs& a, int64_t lane_units, int grid, cudaStream_t st) {
     if (a.count <= 0) return cudaSuccess;
+    const bool exact = 31 * lane_units > a.n || lane_units % (kExpoB / 2) != 0;
+    auto go = [&](auto kernel) { kernel<<<grid, kMm1Block, kMm1PipeSmem, st>>>(a, lane_units); };
     if (a.inv_lambda != 0.0 && a.inv_mu != 0.0)
-        k_wlp_mm1_pipe<true><<<grid, kMm1Block, kMm1PipeSmem, st>>>(a, lane_units);
+        exact ? go(k_wlp_mm1_pipe<true, true>) : go(k_wlp_mm1_pipe<true, false>);
     else
-        k_wlp_mm1_pipe<false><<<grid, kMm1Block, kMm1PipeSmem, st>>>(a, lane_units);
+        exact ? go(k_wlp_mm1_pipe<false, true>) : go(k_wlp_mm1_pipe<false, false>);
     return cudaGetLastError();
 }
 
 int wlp_mm1_pipe_blocks_per_sm() {
     int nb = 0;
-    allow_smem(k_wlp_mm1_pipe<true>, kMm1PipeSmem);
-    allow_smem(k_wlp_mm1_pipe<false>, kMm1PipeSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_mm1_pipe<false>, kMm1Block, kMm1PipeSmem);
+    allow_smem(k_wlp_mm1_pipe<true, true>, kMm1PipeSmem);
+    allow_smem(k_wlp_mm1_pipe<false, true>, kMm1PipeSmem);
+    allow_smem(k_wlp_mm1_pipe<true, false>, kMm1PipeSmem);
+    allow_smem(k_wlp_mm1_pipe<false, false>, kMm1PipeSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_mm1_pipe<false, true>, kMm1Block, kMm1PipeSmem);
     return nb < 1 ? 1 : nb;
 }
 
