@@ -157,6 +157,11 @@ __device__ __forceinline__ double one_minus_u32_dev(uint32_t n) {
     return __dsub_rn(__hiloint2double(hi, static_cast<int>(0u - n)), 0x1p20);
 }
 
+// The same for n != 0 without the n == 0 bump (callers route n == 0 to the near path).
+__device__ __forceinline__ double one_minus_u32_nz(uint32_t n) {
+    return __dsub_rn(__hiloint2double(0x41300000, static_cast<int>(0u - n)), 0x1p20);
+}
+
 // The near-one window and OFF have zero low words, so the tests and the table-path
 // decomposition only touch the high word of x.
 __device__ __forceinline__ bool near_one_dev(double x) {

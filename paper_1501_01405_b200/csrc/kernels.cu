@@ -212,9 +212,11 @@ __device__ __forceinline__ void neg_log1m_batch(const uint32_t (&n)[B], double (
     const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
     for (int j = 0; j < B; ++j) {
-        const double x = one_minus_u32_dev(n[j]);
-        const bool near = near_one_dev(x);
-        e[j] = -log_table_dev(x, tab);
+        // 1 - u >= 1 - 2^-4 (glibc's near-one window) exactly when n <= 2^28; n = 0 (1 - u
+        // = 1) is near too, so the table path may see the wrapped x = 0 there: its value is
+        // replaced below
+        const bool near = n[j] <= 0x10000000u;
+        e[j] = -log_table_dev(one_minus_u32_nz(n[j]), tab);
         const unsigned b = __ballot_sync(mask, near);
         pos[j] = near ? total + __popc(b & lt) : -1;
         if (near) nl.n[pos[j]] = n[j];
@@ -239,24 +241,27 @@ __device__ __forceinline__ double scale(double e, double rate, double inv) {
     return INV ? __dmul_rn(e, inv) : __ddiv_rn(e, rate);
 }
 
-// One step of the Lindley recursion with the reference's operation order
-// (models.hpp:67-77): t = (w + s) - a; idle/w update; s = next service; sums.
+// One client of the Lindley recursion (models.hpp:67-78) in the reference's rounding:
+//   t = (w + s) - a;  if (t < 0) { idle -= t; w = 0 } else w = t;  s = s';
+//   sumw += w;  sums += (w + s)
+// * u = fl(w + s) is carried: the next client's (w + s) has the same operands as this
+//   client's sums term.
+// * The branch clears t's two words when its sign bit is set. t is never -0 or NaN here
+//   (u >= +0, a finite), so this is w = t < 0 ? +0 : t.
+// * idle - t == idle + fl(w - t) exactly: -t when dry, and idle + (+0) == idle otherwise
+//   (idle >= +0).
 struct Queue {
-    double w = 0.0, s = 0.0, idle = 0.0, sumw = 0.0, sums = 0.0;
+    double u = 0.0, idle = 0.0, sumw = 0.0, sums = 0.0;
     // returns whether the `t < 0` branch (server idle) was taken
     __device__ __forceinline__ bool client(double a, double s_next) {
-        const double t = __dsub_rn(__dadd_rn(w, s), a);
-        const bool dry = t < 0.0;
-        if (dry) {  // the server ran dry before this arrival
-            idle = __dsub_rn(idle, t);
-            w = 0.0;
-        } else {
-            w = t;
-        }
-        s = s_next;
+        const double t = __dsub_rn(u, a);
+        const int hi = __double2hiint(t), keep = ~(hi >> 31);
+        const double w = __hiloint2double(hi & keep, __double2loint(t) & keep);
+        idle = __dadd_rn(idle, __dsub_rn(w, t));
+        u = __dadd_rn(w, s_next);
         sumw = __dadd_rn(sumw, w);
-        sums = __dadd_rn(sums, __dadd_rn(w, s));
-        return dry;
+        sums = __dadd_rn(sums, u);
+        return hi < 0;
     }
 };
 
@@ -948,8 +953,7 @@ __global__ void __launch_bounds__(kMm1Block, 3) k_wlp_mm1_pipe(RepArgs a, int64_
         st.s1 = __shfl_up_sync(kFull, st.s1, 1);
         st.s2 = __shfl_up_sync(kFull, st.s2, 1);
         st.s3 = __shfl_up_sync(kFull, st.s3, 1);
-        q.w = __shfl_up_sync(kFull, q.w, 1);
-        q.s = __shfl_up_sync(kFull, q.s, 1);
+        q.u = __shfl_up_sync(kFull, q.u, 1);
         q.idle = __shfl_up_sync(kFull, q.idle, 1);
         q.sumw = __shfl_up_sync(kFull, q.sumw, 1);
         q.sums = __shfl_up_sync(kFull, q.sums, 1);
