@@ -22,6 +22,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "glibc_log.cuh"
 #include "jump.hpp"
 #include "kernels.cuh"
@@ -461,25 +463,27 @@ __global__ void __launch_bounds__(kWlpBlock, 3) k_wlp_lanes(RepArgs a, const uin
 // at once. No jump tables at all; the cost is the 31-step drain per warp, so the launcher
 // picks this kernel when replications per warp are many and units per replication few
 // (config 4: 1400 replications of 32 units per lane).
-template <int MODEL>
+// WIDE: 64-bit sums and indices (n or count >= 2^31); else 32-bit, fewer shuffles.
+template <int MODEL, bool WIDE>
 __global__ void __launch_bounds__(kWlpBlock, 3) k_wlp_pipe(RepArgs a, int64_t K) {
-    __shared__ long long emit_rep[kWlpBlock / 32][32];
-    __shared__ long long emit_sum[kWlpBlock / 32][32];
+    using I = typename std::conditional<WIDE, long long, int>::type;
+    __shared__ I emit_rep[kWlpBlock / 32][32];
+    __shared__ I emit_sum[kWlpBlock / 32][32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int64_t mine = a.n - static_cast<int64_t>(lane) * K;
     mine = mine < 0 ? 0 : (mine > K ? K : mine);
     const uint32_t units = static_cast<uint32_t>(mine);
     Taus st{kMin1, kMin2, kMin3};
-    long long sum = 0, rep = -1;
+    I sum = 0, rep = -1;
     int64_t cur = 0, cend = 0;  // lane 0's current group of replications (warp-uniform)
     bool more = true;
     int nemit = 0;
     auto flush = [&](int cnt) {
         __syncwarp();
         if (lane < cnt) {
-            const long long r = emit_rep[wid][lane], c = emit_sum[wid][lane];
+            const I r = emit_rep[wid][lane], c = emit_sum[wid][lane];
             a.out0[r] = MODEL == 0 ? __ddiv_rn(__dmul_rn(4.0, static_cast<double>(c)), static_cast<double>(a.n))
-                                   : walk_fold(c, a.chunks);
+                                   : walk_fold(static_cast<int64_t>(c), a.chunks);
         }
         __syncwarp();
     };
@@ -494,7 +498,7 @@ __global__ void __launch_bounds__(kWlpBlock, 3) k_wlp_pipe(RepArgs a, int64_t K)
             }
         }
         if (lane == 0) {  // feed
-            rep = more ? cur : -1;
+            rep = more ? static_cast<I>(cur) : I(-1);
             if (more) {
                 st = load_seed(a, cur);
                 sum = 0;
@@ -502,7 +506,7 @@ __global__ void __launch_bounds__(kWlpBlock, 3) k_wlp_pipe(RepArgs a, int64_t K)
         }
         if (more) ++cur;
         if (!__any_sync(kFull, rep >= 0)) break;
-        if (rep >= 0) sum += MODEL == 0 ? static_cast<long long>(pi_hits(st, units)) : walk_dx(st, units);
+        if (rep >= 0) sum += MODEL == 0 ? static_cast<I>(pi_hits(st, units)) : static_cast<I>(walk_dx(st, units));
         if (__shfl_sync(kFull, rep, 31) >= 0) {  // lane 31 finished a replication
             if (lane == 31) {
                 emit_rep[wid][nemit] = rep;
@@ -1279,10 +1283,13 @@ cudaError_t launch_wlp(int model, const RepArgs& a, const uint32_t* lane_tab, co
 
 cudaError_t launch_wlp_pipe(int model, const RepArgs& a, int64_t lane_units, int grid, cudaStream_t st) {
     if (a.count <= 0) return cudaSuccess;
+    const bool wide = a.n >= (int64_t(1) << 31) || a.count >= (int64_t(1) << 31);
     if (model == 0)
-        k_wlp_pipe<0><<<grid, kWlpBlock, 0, st>>>(a, lane_units);
+        wide ? k_wlp_pipe<0, true><<<grid, kWlpBlock, 0, st>>>(a, lane_units)
+             : k_wlp_pipe<0, false><<<grid, kWlpBlock, 0, st>>>(a, lane_units);
     else
-        k_wlp_pipe<2><<<grid, kWlpBlock, 0, st>>>(a, lane_units);
+        wide ? k_wlp_pipe<2, true><<<grid, kWlpBlock, 0, st>>>(a, lane_units)
+             : k_wlp_pipe<2, false><<<grid, kWlpBlock, 0, st>>>(a, lane_units);
     return cudaGetLastError();
 }
 
@@ -1309,7 +1316,7 @@ int wlp_mm1_pipe_blocks_per_sm() {
 
 int wlp_pipe_blocks_per_sm() {
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_pipe<0>, kWlpBlock, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_pipe<0, true>, kWlpBlock, 0);
     return nb < 1 ? 1 : nb;
 }
 
