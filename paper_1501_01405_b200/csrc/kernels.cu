@@ -674,6 +674,64 @@ __device__ __forceinline__ double mm1_warp_rep(Taus st, int64_t n, double lambda
     return acc;
 }
 
+// Heavy traffic: the segment chain barely regenerates, ripple rounds go one lane at a
+// time, and the separate sum phase adds its own chain. Then lane 0 runs the recursion and
+// the three sums of the panel in one ordered loop (the four chains overlap), reading the
+// client-ordered (a, s) pairs the lanes staged in shared memory. Same result bits;
+// returns the same per-lane layout as mm1_warp_rep (lanes 0/1/2: sumw/sums/idle).
+template <bool INV>
+__device__ __forceinline__ double mm1_warp_rep_serial(Taus st, int64_t n, double lambda, double mu, double inv_l,
+                                                      double inv_m, const double* logtab, const uint32_t* skip,
+                                                      Mm1Warp& W, int lane) {
+    constexpr int T = kMm1PanelT;
+    constexpr int P = kMm1P;
+    static_assert(sizeof(double2) * 32 * (T + 1) <= sizeof(W.term), "pair panel fits the term arrays");
+    double2* const pair = reinterpret_cast<double2*>(W.term);
+    Queue q;
+    for (int64_t base = 0; base < n; base += P) {
+        double ea[T], es[T];
+#pragma unroll
+        for (int h = 0; h < 2 * T; h += kExpoB) {
+            uint32_t d[kExpoB];
+            double e[kExpoB];
+#pragma unroll
+            for (int j = 0; j < kExpoB; j += 2) taus_next2(st, d[j], d[j + 1]);
+            neg_log1m_batch<kExpoB, true>(d, e, logtab, W.nl, W.term, kFull, lane);
+#pragma unroll
+            for (int j = 0; j < kExpoB; j += 2) {
+                ea[(h + j) / 2] = scale<INV>(e[j], lambda, inv_l);
+                es[(h + j) / 2] = scale<INV>(e[j + 1], mu, inv_m);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < T; ++c) pair[lane * (T + 1) + c] = make_double2(ea[c], es[c]);
+        __syncwarp();
+        if (lane == 0) {
+            const int64_t left = n - base;
+            if (left >= P) {
+                const double2* p = pair;
+                for (int seg = 0; seg < 32; ++seg, p += T + 1) {
+                    double2 v[T];
+#pragma unroll
+                    for (int j = 0; j < T; ++j) v[j] = p[j];
+#pragma unroll
+                    for (int j = 0; j < T; ++j) q.client(v[j].x, v[j].y);
+                }
+            } else {
+                for (int c = 0; c < static_cast<int>(left); ++c) {
+                    const double2 v = pair[(c / T) * (T + 1) + c % T];
+                    q.client(v.x, v.y);
+                }
+            }
+        }
+        __syncwarp();
+        st = uni_jump(skip, st);
+    }
+    const double sumw = __shfl_sync(kFull, q.sumw, 0), sums = __shfl_sync(kFull, q.sums, 0),
+                 idle = __shfl_sync(kFull, q.idle, 0);
+    return lane == 0 ? sumw : (lane == 1 ? sums : idle);
+}
+
 // The lane-start tables stay in global memory (L1/L2 resident): one 24-load jump per
 // replication of ~10^3 clients is noise, and the 48 KB are better spent on term arrays.
 struct Mm1Smem {
@@ -709,8 +767,11 @@ __global__ void __launch_bounds__(kMm1Block, 3) k_wlp_mm1(RepArgs a, const uint3
         double k0 = 0.0, k1 = 0.0, k2 = 0.0;
         for (int64_t r = base; r < end; ++r) {
             const Taus st = lane_jump(m.tab, lane, load_seed(a, r));
-            const double acc = mm1_warp_rep<INV>(st, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu, m.logtab,
-                                                 m.skip, *m.W, lane);
+            const double acc =
+                a.lambda >= a.serial_rho * a.mu
+                    ? mm1_warp_rep_serial<INV>(st, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu, m.logtab, m.skip,
+                                               *m.W, lane)
+                    : mm1_warp_rep<INV>(st, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu, m.logtab, m.skip, *m.W, lane);
             const double avg = __ddiv_rn(acc, static_cast<double>(a.n));  // lanes 0/1/2: wait/sys/idle
             const double v0 = __shfl_sync(kFull, avg, 2);
             const double v1 = __shfl_sync(kFull, avg, 0);
@@ -1073,11 +1134,18 @@ __global__ void __launch_bounds__(kMm1Block) k_plan_mm1(PlanArgs a, const uint32
     for (int64_t r = next_rep(a, lane); r < a.count; r = next_rep(a, lane)) {
         const SetParam S = a.sets[find_set(a.sets, a.n_sets, r)];
         const Taus st = lane_jump(m.tab, lane, plan_seed(a, r));
-        const double acc = (S.inv_lambda != 0.0 && S.inv_mu != 0.0)
-                               ? mm1_warp_rep<true>(st, S.n, S.lambda, S.mu, S.inv_lambda, S.inv_mu, m.logtab,
-                                                    m.skip, *m.W, lane)
-                               : mm1_warp_rep<false>(st, S.n, S.lambda, S.mu, S.inv_lambda, S.inv_mu, m.logtab,
-                                                     m.skip, *m.W, lane);
+        const bool inv = S.inv_lambda != 0.0 && S.inv_mu != 0.0;
+        double acc;
+        if (S.lambda >= a.serial_rho * S.mu)  // heavy traffic: ordered loop on lane 0
+            acc = inv ? mm1_warp_rep_serial<true>(st, S.n, S.lambda, S.mu, S.inv_lambda, S.inv_mu, m.logtab, m.skip,
+                                                  *m.W, lane)
+                      : mm1_warp_rep_serial<false>(st, S.n, S.lambda, S.mu, S.inv_lambda, S.inv_mu, m.logtab,
+                                                   m.skip, *m.W, lane);
+        else
+            acc = inv ? mm1_warp_rep<true>(st, S.n, S.lambda, S.mu, S.inv_lambda, S.inv_mu, m.logtab, m.skip, *m.W,
+                                           lane)
+                      : mm1_warp_rep<false>(st, S.n, S.lambda, S.mu, S.inv_lambda, S.inv_mu, m.logtab, m.skip,
+                                            *m.W, lane);
         if (lane < 3) {  // lanes 0/1/2 hold sumw/sums/idle
             double* out = lane == 0 ? a.out1 : (lane == 1 ? a.out2 : a.out0);
             out[r] = __ddiv_rn(acc, static_cast<double>(S.n));

@@ -28,6 +28,9 @@ struct RepArgs {
     // model's data-dependent `if`s (the reference's event definition,
     // warp_exec.cpp:272-284), [1] global load and [2] global store warp-instructions.
     unsigned long long* hw = nullptr;
+    // mm1 WLP with segment chaining: replications with lambda >= serial_rho * mu run the
+    // heavy-traffic ordered loop on lane 0 instead (0.75 by default, runtime.cu)
+    double serial_rho = 2.0;
 };
 
 // Per-warp instrumentation tally (identical in every lane; the leader flushes it).
@@ -67,6 +70,7 @@ struct PlanArgs {
     double* out1;
     double* out2;
     unsigned long long* next;  // dynamic work counter (zeroed before launch)
+    double serial_rho = 2.0;   // as RepArgs::serial_rho, per set
 };
 
 // Batched seeding of many independent random_spacing runs (one per set).

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -29,6 +30,16 @@ namespace {
 thread_local std::string g_err;
 thread_local bool g_hw_counters = false;  // wlp_set_hw_counters
 thread_local int g_wlp_variant = 0;       // wlp_set_wlp_variant: 0 auto, 1 lane jumps, 2 pipeline
+
+// mm1 WLP segment chaining hands replications with lambda >= rho * mu to the serial
+// heavy-traffic loop; WLP_MM1_SERIAL_RHO overrides the measured default.
+double mm1_serial_rho() {
+    static const double rho = [] {
+        const char* e = std::getenv("WLP_MM1_SERIAL_RHO");
+        return e ? std::atof(e) : 0.75;
+    }();
+    return rho;
+}
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
@@ -411,6 +422,7 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
     a.out0 = o0;
     a.out1 = o1;
     a.out2 = o2;
+    a.serial_rho = mm1_serial_rho();
     if (g_hw_counters) {
         WLP_CUDA(cudaMemsetAsync(c.hw.p, 0, 3 * sizeof(unsigned long long), st));
         a.hw = c.hw.p;
@@ -433,7 +445,7 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
         // per-client cost) but drains 31 steps per warp; segment chaining pays ~1.8x per
         // client but has no drain. Pipeline when the drain is the smaller loss.
         const double per_warp = static_cast<double>(count) / static_cast<double>(warps);
-        const bool pipe = !g_hw_counters && (g_wlp_variant == 2 || (g_wlp_variant == 0 && per_warp > 64.0));
+        const bool pipe = !g_hw_counters && (g_wlp_variant == 2 || (g_wlp_variant == 0 && per_warp > 40.0));
         if (pipe) {
             const int64_t cap = static_cast<int64_t>(c.sms) * c.mm1_pipe_bps;
             grid_out = static_cast<int>(std::min<int64_t>(grid_out, cap));
@@ -1006,6 +1018,7 @@ int wlp_run_plan(int model, const wlp_params* sets, const uint64_t* master_seeds
         }
     }
     PlanArgs pa;
+    pa.serial_rho = mm1_serial_rho();
     pa.seeds = c->seeds.p;
     pa.count = R;
     pa.sets = c->setp.p;
