@@ -162,12 +162,9 @@ __device__ __forceinline__ double one_minus_u32_nz(uint32_t n) {
     return __dsub_rn(__hiloint2double(0x41300000, static_cast<int>(0u - n)), 0x1p20);
 }
 
-// The near-one window and OFF have zero low words, so the tests and the table-path
-// decomposition only touch the high word of x.
-__device__ __forceinline__ bool near_one_dev(double x) {
-    return static_cast<uint32_t>(__double2hiint(x)) - 0x3FEE0000u < 0x00030900u;
-}
-
+// For x = 1 - n*2^-32 the near-one window (x >= 1 - 2^-4) is exactly n <= 2^28, so callers
+// test the draw itself. OFF has a zero low word, so the table-path decomposition only
+// touches the high word of x.
 __device__ __forceinline__ double log_table_dev(double x, const double* tab) {
     const uint32_t hx = static_cast<uint32_t>(__double2hiint(x));
     const uint32_t thi = hx - 0x3fe60000u;  // high word of ix - OFF
