@@ -445,6 +445,11 @@ def main():
         extras["ir_walk_tlp_2e4x1e3"] = {"kernel_ms": kms, "issues": runs[-1].report.issues,
                                          "divergence_events": runs[-1].report.divergenceEvents,
                                          "issues_per_s": runs[-1].report.issues / (kms * 1e-3)}
+        # the same IR kernel compiled (IR -> CUDA C++ -> NVRTC), first call compiles
+        jruns = [ir.run_model(w.ModelKind.Walk, pir, w.ExecutionMode.Tlp, SEED, jit=True) for _ in range(4)]
+        jms = min(r.report.kernel_ms for r in jruns[1:])
+        assert all((r.primary == runs[-1].primary).all() for r in jruns)
+        extras["ir_walk_tlp_2e4x1e3"]["jit"] = {"kernel_ms": jms, "speedup_vs_interpreter": kms / jms}
         line["extras"] = extras
     if world == 1 and rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = {k: v for k, v in cpu_baseline(0, p).items() if k != "step_s"}

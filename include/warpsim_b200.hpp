@@ -103,8 +103,11 @@ struct SimOptions {
     // outputs, and the reference simulator's exact issue / divergence / memory counters.
     bool irInterpreter = false;
     // IR interpreter: statements one IR warp may issue before FaultError (guards
-    // against kernels that never terminate).
+    // against kernels that never terminate); under irJit, loop iterations per IR thread.
     std::int64_t maxIssuesPerWarp = std::int64_t{1} << 50;
+    // B200 extension: simulate() compiles the IR kernel (CUDA C++ via NVRTC) instead of
+    // interpreting it. Same memory results; the report has measured time only.
+    bool irJit = false;
 };
 struct SimReport {
     std::int64_t totalCycles = 0;

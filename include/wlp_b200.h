@@ -339,6 +339,21 @@ int wlp_ir_simulate(const wlp_ir_program* prog, const wlp_launch_cfg* cfg, int64
                     const uint32_t* streams, int64_t n_streams, int streams_on_device, int mask_depth,
                     int64_t max_issues, void* stream, wlp_report* report);
 
+/* The same program compiled instead of interpreted: translated to CUDA C++, compiled for
+ * sm_100a by NVRTC (loaded on first use; cached by source) and launched with the same
+ * IR-warp mapping. Memory results equal the interpreter's for kernels without cross-lane
+ * memory traffic between the two sides of a divergent branch; the report carries the
+ * measured time only (the issue / divergence counters need the interpreter's lockstep
+ * accounting). max_iterations (> 0) bounds the loop iterations of one IR thread
+ * (WLP_EFAULT when hit). WLP_ECUDA when NVRTC is unavailable. */
+int wlp_ir_jit_simulate(const wlp_ir_program* prog, const wlp_launch_cfg* cfg, int64_t max_threads_per_block,
+                        double* const* arrays, const int64_t* array_len, int arrays_on_device,
+                        const uint32_t* streams, int64_t n_streams, int streams_on_device, int64_t max_iterations,
+                        void* stream, wlp_report* report);
+
+/* The CUDA C++ source the JIT generates for a program (for inspection). */
+int wlp_ir_jit_source(const wlp_ir_program* prog, char* out, int cap, int* need);
+
 /* Release all device scratch of the current device. */
 int wlp_shutdown(void);
 

@@ -142,6 +142,7 @@ class SimOptions:  # device.hpp:53-60
     # interpreter (paper_1501_01405_b200.ir), and its per-IR-warp issue guard
     irInterpreter: bool = False
     maxIssuesPerWarp: int = 1 << 50
+    irJit: bool = False  # with irInterpreter: compile the IR kernel (NVRTC) instead
 
 
 @dataclass
@@ -267,6 +268,9 @@ _SIGS = {
     "wlp_debug_neg_log1m": (C.c_int, [_P, _I64, _P]),
     "wlp_ir_simulate": (C.c_int, [_P, C.POINTER(_Cfg), _I64, _P, _P, C.c_int, _P, _I64, C.c_int, C.c_int, _I64, _P,
                                   C.POINTER(_Report)]),
+    "wlp_ir_jit_simulate": (C.c_int, [_P, C.POINTER(_Cfg), _I64, _P, _P, C.c_int, _P, _I64, C.c_int, _I64, _P,
+                                      C.POINTER(_Report)]),
+    "wlp_ir_jit_source": (C.c_int, [_P, C.c_char_p, C.c_int, C.POINTER(C.c_int)]),
     "wlp_shutdown": (C.c_int, []),
 }
 EXPORTS = tuple(_SIGS)
@@ -532,9 +536,9 @@ def run_model(model: ModelKind, p: ModelParams, mode: ExecutionMode, prof: Optio
     """
     model, mode = ModelKind(model), ExecutionMode(mode)
     if opts is not None and opts.irInterpreter and mode != ExecutionMode.Sequential:
-        from . import ir  # the reference's IR kernels on the GPU interpreter
+        from . import ir  # the reference's IR kernels on the GPU interpreter (or compiled)
 
-        return ir.run_model(model, p, mode, master_seed, tlp_block_size)
+        return ir.run_model(model, p, mode, master_seed, tlp_block_size, jit=opts.irJit)
     plan = plan_launch(p.replications, mode, prof, tlp_block_size, grid_limit=0x7FFFFFFF)
     R = int(p.replications)
     names = OUTPUT_NAMES[model]

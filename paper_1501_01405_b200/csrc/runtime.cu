@@ -1196,13 +1196,15 @@ struct Scratch {  // per-call device allocation
 }  // namespace
 }  // namespace wlp
 
-extern "C" {
+namespace wlp {
+std::string ir_jit_source(const wlp_ir_program& p);
+int ir_jit_kernel(const wlp_ir_program& p, int device, void** kernel, std::string& err);
+namespace {
 
-int wlp_ir_simulate(const wlp_ir_program* prog, const wlp_launch_cfg* cfg, int64_t max_threads_per_block,
-                    double* const* arrays, const int64_t* array_len, int arrays_on_device,
-                    const uint32_t* streams, int64_t n_streams, int streams_on_device, int mask_depth,
-                    int64_t max_issues, void* stream, wlp_report* report) {
-    using namespace wlp;
+int ir_run(const wlp_ir_program* prog, const wlp_launch_cfg* cfg, int64_t max_threads_per_block,
+           double* const* arrays, const int64_t* array_len, int arrays_on_device, const uint32_t* streams,
+           int64_t n_streams, int streams_on_device, int mask_depth, int64_t max_issues, void* stream,
+           wlp_report* report, bool jit) {
     if (!prog || !cfg) return fail(WLP_EDOMAIN, "ir_simulate: null program or launch");
     if (cfg->block_x < 1 || cfg->block_y < 1 || cfg->block_z < 1)
         return fail(WLP_EDOMAIN, "launch: blockDim components must be >= 1");
@@ -1307,11 +1309,33 @@ int wlp_ir_simulate(const wlp_ir_program* prog, const wlp_launch_cfg* cfg, int64
     a.max_issues = max_issues;
     a.counters = d_cnt.p;
     a.fault = d_fault.p;
-    const int64_t resident_blocks = static_cast<int64_t>(ir_blocks_per_sm()) * c->sms;
+    int64_t resident_blocks = static_cast<int64_t>(ir_blocks_per_sm()) * c->sms;
+    void* jk = nullptr;
+    if (jit) {
+        std::string err;
+        const int rc = ir_jit_kernel(*prog, c->dev, &jk, err);
+        if (rc != WLP_OK) return fail(rc, err);
+        int nb = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, jk, kIrBlock, 0) != cudaSuccess || nb < 1) nb = 4;
+        resident_blocks = static_cast<int64_t>(nb) * c->sms;
+    }
     const int64_t need_blocks = (total_warps * 32 + kIrBlock - 1) / kIrBlock;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min(resident_blocks, need_blocks)));
     WLP_CUDA(cudaEventRecord(c->ev0, st));
-    WLP_CUDA(launch_ir(a, grid, st));
+    if (jit) {
+        // wlp_ir_jit(P, A, AL, S, nS, bx, by, bz, gx, gy, ws, tpb, wpb, total_warps, max_iters, fault)
+        const int64_t* P_ = d_params.p;
+        double* const* A_ = d_arrs.p;
+        const int64_t* AL_ = d_alen.p;
+        const uint32_t* S_ = ds;
+        long long nS = n_streams, bx = a.bx, by = a.by, bz = a.bz, gx = a.gx, gy = a.gy, wsz = ws, tp = tpb,
+                  wp = wpb, tw = total_warps, mi = max_issues;
+        IrFault* F_ = d_fault.p;
+        void* args[] = {&P_, &A_, &AL_, &S_, &nS, &bx, &by, &bz, &gx, &gy, &wsz, &tp, &wp, &tw, &mi, &F_};
+        WLP_CUDA(cudaLaunchKernel(jk, dim3(grid), dim3(kIrBlock), args, 0, st));
+    } else {
+        WLP_CUDA(launch_ir(a, grid, st));
+    }
     WLP_CUDA(cudaEventRecord(c->ev1, st));
     if (!arrays_on_device)
         for (int i = 0; i < prog->n_params; ++i)
@@ -1332,11 +1356,47 @@ int wlp_ir_simulate(const wlp_ir_program* prog, const wlp_launch_cfg* cfg, int64
         const int64_t resident_warps = resident_blocks * (kIrBlock / 32);
         report->waves_executed = (total_warps + resident_warps - 1) / resident_warps;
         report->peak_resident_warps = std::min(total_warps, resident_warps);
-        report->issues = cnt[0];
-        report->alu_issues = cnt[1];
-        report->mem_reads = cnt[2];
-        report->mem_writes = cnt[3];
-        report->divergence_events = cnt[4];
+        if (!jit) {  // the JIT has no lockstep accounting
+            report->issues = cnt[0];
+            report->alu_issues = cnt[1];
+            report->mem_reads = cnt[2];
+            report->mem_writes = cnt[3];
+            report->divergence_events = cnt[4];
+        }
+    }
+    return WLP_OK;
+}
+
+}  // namespace
+}  // namespace wlp
+
+extern "C" {
+
+int wlp_ir_simulate(const wlp_ir_program* prog, const wlp_launch_cfg* cfg, int64_t max_threads_per_block,
+                    double* const* arrays, const int64_t* array_len, int arrays_on_device,
+                    const uint32_t* streams, int64_t n_streams, int streams_on_device, int mask_depth,
+                    int64_t max_issues, void* stream, wlp_report* report) {
+    return wlp::ir_run(prog, cfg, max_threads_per_block, arrays, array_len, arrays_on_device, streams, n_streams,
+                       streams_on_device, mask_depth, max_issues, stream, report, false);
+}
+
+int wlp_ir_jit_simulate(const wlp_ir_program* prog, const wlp_launch_cfg* cfg, int64_t max_threads_per_block,
+                        double* const* arrays, const int64_t* array_len, int arrays_on_device,
+                        const uint32_t* streams, int64_t n_streams, int streams_on_device, int64_t max_iterations,
+                        void* stream, wlp_report* report) {
+    return wlp::ir_run(prog, cfg, max_threads_per_block, arrays, array_len, arrays_on_device, streams, n_streams,
+                       streams_on_device, 32, max_iterations, stream, report, true);
+}
+
+int wlp_ir_jit_source(const wlp_ir_program* prog, char* out, int cap, int* need) {
+    if (!prog) return fail(WLP_EDOMAIN, "ir_jit_source: null program");
+    WLP_TRY(wlp::ir_check(*prog));
+    const std::string src = wlp::ir_jit_source(*prog);
+    if (need) *need = static_cast<int>(src.size()) + 1;
+    if (out && cap > 0) {
+        const size_t k = std::min<size_t>(src.size(), static_cast<size_t>(cap - 1));
+        std::memcpy(out, src.data(), k);
+        out[k] = 0;
     }
     return WLP_OK;
 }

@@ -881,8 +881,6 @@ KernelBundle build_kernel(ModelKind model, const ModelParams& p, ExecutionMode m
 
 // ---- flattening to the device form (include/wlp_b200.h) ----------------------------------
 
-namespace {
-
 struct Flat {
     std::vector<wlp_ir_stmt> stmts;
     std::vector<std::int32_t> code;
@@ -1056,6 +1054,8 @@ wlp_ir_program view(const Flat& f) {
     return v;
 }
 
+namespace {
+
 SimReport report_of(const wlp_report& r) {
     SimReport s;
     s.totalCycles = r.total_cycles;
@@ -1101,8 +1101,11 @@ SimReport simulate(const KernelProgram& prog, const LaunchConfig& cfg, const Dev
     }
     const wlp_launch_cfg c{cfg.blockDim.x, cfg.blockDim.y, cfg.blockDim.z, cfg.gridDim.x, cfg.gridDim.y, cfg.warpSize};
     wlp_report rep{};
-    const int st = wlp_ir_simulate(&v, &c, prof.maxThreadsPerBlock, arrays.data(), lens.data(), 0, soa.data(), n, 0,
-                                   opts.maskStackDepth, opts.maxIssuesPerWarp, nullptr, &rep);
+    const int st = opts.irJit ? wlp_ir_jit_simulate(&v, &c, prof.maxThreadsPerBlock, arrays.data(), lens.data(), 0,
+                                                    soa.data(), n, 0, opts.maxIssuesPerWarp, nullptr, &rep)
+                              : wlp_ir_simulate(&v, &c, prof.maxThreadsPerBlock, arrays.data(), lens.data(), 0,
+                                                soa.data(), n, 0, opts.maskStackDepth, opts.maxIssuesPerWarp, nullptr,
+                                                &rep);
     if (st == WLP_EFAULT) {  // name the local of a typed-assign fault, as warp_exec.cpp does
         std::string msg = wlp_last_error();
         const std::string tag = "assign: real value into int local #";
@@ -1202,6 +1205,27 @@ int warpsim_ir_canonical(const char* text, char* out, int cap, int* need) {
     }
 }
 
+// The CUDA C++ the JIT generates for a kernel text (parse, flatten, translate).
+int warpsim_ir_jit_source_text(const char* text, char* out, int cap, int* need) {
+    try {
+        const warpsim::KernelProgram prog = warpsim::parse_kernel(text);
+        const warpsim::Flat f = warpsim::flatten(prog, nullptr);
+        const wlp_ir_program v = warpsim::view(f);
+        int n = 0;
+        int st = wlp_ir_jit_source(&v, nullptr, 0, &n);
+        if (st != WLP_OK) {
+            g_ir_err = wlp_last_error();
+            return st;
+        }
+        std::string src(static_cast<std::size_t>(n), '\0');
+        st = wlp_ir_jit_source(&v, src.data(), n, nullptr);
+        src.resize(std::strlen(src.c_str()));
+        return copy_text(src, out, cap, need);
+    } catch (...) {
+        return map_exception();
+    }
+}
+
 // dump_kernel of a model body (mode 0) or its Tlp (1) / Wlp (2) wrapping.
 int warpsim_ir_model_text(int model, int mode, char* out, int cap, int* need) {
     try {
@@ -1220,7 +1244,7 @@ int warpsim_ir_simulate_text(const char* text, const wlp_launch_cfg* cfg, int ma
                              const char* const* names, const int* is_int, const int64_t* ivals, const double* rvals,
                              int n_arrays, const char* const* anames, double* const* arrays, const int64_t* alen,
                              const uint32_t* streams, int64_t n_streams, int mask_depth, int64_t max_issues,
-                             wlp_report* report) {
+                             int jit, wlp_report* report) {
     try {
         const warpsim::KernelProgram prog = warpsim::parse_kernel(text);
         warpsim::LaunchConfig lc;
@@ -1239,6 +1263,7 @@ int warpsim_ir_simulate_text(const char* text, const wlp_launch_cfg* cfg, int ma
         warpsim::SimOptions opts;
         opts.maskStackDepth = mask_depth;
         opts.maxIssuesPerWarp = max_issues;
+        opts.irJit = jit != 0;
         const warpsim::SimReport rep = warpsim::simulate(prog, lc, prof, mem, scalars, st, opts);
         for (int k = 0; k < n_arrays; ++k) std::copy(mem.arrays[anames[k]].begin(), mem.arrays[anames[k]].end(), arrays[k]);
         to_report(rep, report);
@@ -1250,7 +1275,7 @@ int warpsim_ir_simulate_text(const char* text, const wlp_launch_cfg* cfg, int ma
 
 // run_model through the IR path on the GPU interpreter (mode Tlp / Wlp).
 int warpsim_ir_run_model(int model, const wlp_params* p, int mode, uint64_t seed, int tlp_block, double* out0,
-                         double* out1, double* out2, wlp_report* report, char* warn, int warn_cap) {
+                         double* out1, double* out2, wlp_report* report, char* warn, int warn_cap, int jit) {
     try {
         if (model < 0 || model > 2 || mode < 0 || mode > 2) throw warpsim::DomainError("model / mode id");
         warpsim::ModelParams mp;
@@ -1261,9 +1286,11 @@ int warpsim_ir_run_model(int model, const wlp_params* p, int mode, uint64_t seed
         mp.mu = p->mu;
         mp.steps = p->steps;
         mp.chunks = p->chunks;
+        warpsim::SimOptions opts;
+        opts.irJit = jit != 0;
         const warpsim::ModelRun run =
             warpsim::run_model_ir(static_cast<warpsim::ModelKind>(model), mp, static_cast<warpsim::ExecutionMode>(mode),
-                                  warpsim::DeviceProfile{}, seed, tlp_block);
+                                  warpsim::DeviceProfile{}, seed, tlp_block, opts);
         const bool mm1 = model == 1;
         const auto put = [&](const char* name, double* dst) {
             if (dst) std::copy(run.outputs.at(name).begin(), run.outputs.at(name).end(), dst);

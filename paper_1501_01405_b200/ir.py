@@ -32,9 +32,10 @@ _SIGS = {
     "warpsim_ir_canonical": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int, C.POINTER(C.c_int)]),
     "warpsim_ir_model_text": (C.c_int, [C.c_int, C.c_int, C.c_char_p, C.c_int, C.POINTER(C.c_int)]),
     "warpsim_ir_simulate_text": (C.c_int, [C.c_char_p, C.POINTER(_Cfg), C.c_int, C.c_int, _P, _P, _P, _P, C.c_int, _P,
-                                           _P, _P, _P, C.c_int64, C.c_int, C.c_int64, C.POINTER(_Report)]),
+                                           _P, _P, _P, C.c_int64, C.c_int, C.c_int64, C.c_int, C.POINTER(_Report)]),
     "warpsim_ir_run_model": (C.c_int, [C.c_int, C.POINTER(_Params), C.c_int, C.c_uint64, C.c_int, _P, _P, _P,
-                                       C.POINTER(_Report), C.c_char_p, C.c_int]),
+                                       C.POINTER(_Report), C.c_char_p, C.c_int, C.c_int]),
+    "warpsim_ir_jit_source_text": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int, C.POINTER(C.c_int)]),
 }
 _lib: Optional[C.CDLL] = None
 
@@ -91,9 +92,16 @@ def _streams_soa(streams) -> np.ndarray:
                                           [s.s3 for s in streams]], dtype=np.uint32).reshape(3, -1))
 
 
+def jit_source(text: str) -> str:
+    """The CUDA C++ the IR JIT generates for a kernel text (compiled by NVRTC on use)."""
+    return _text(_cxx().warpsim_ir_jit_source_text, text.encode())
+
+
 def simulate(text: str, cfg: LaunchConfig, scalars: Mapping[str, object], arrays: Mapping[str, np.ndarray],
-             streams=None, opts: Optional[SimOptions] = None, max_threads_per_block: int = 1024) -> SimReport:
-    """simulate (device.cpp:140-226) of a kernel given as text, on the GPU interpreter.
+             streams=None, opts: Optional[SimOptions] = None, max_threads_per_block: int = 1024,
+             jit: bool = False) -> SimReport:
+    """simulate (device.cpp:140-226) of a kernel given as text, on the GPU interpreter
+    (jit=True: compiled to sm_100a through NVRTC instead; same memory results, time only).
     `scalars`: name -> int (Int params) or float; `arrays`: name -> float64 numpy array,
     updated in place; `streams`: lane streams by global thread id ((3, n) uint32 or a
     sequence of RngState)."""
@@ -119,14 +127,16 @@ def simulate(text: str, cfg: LaunchConfig, scalars: Mapping[str, object], arrays
     _check(_cxx().warpsim_ir_simulate_text(text.encode(), C.byref(c), int(max_threads_per_block), len(names), cnames,
                                            is_int, ivals, rvals, len(anames), canames, aptrs, alen,
                                            st.ctypes.data if st.size else None, st.shape[1],
-                                           int(opts.maskStackDepth), int(opts.maxIssuesPerWarp), C.byref(rep)))
+                                           int(opts.maskStackDepth), int(opts.maxIssuesPerWarp), int(bool(jit)),
+                                           C.byref(rep)))
     return _report(rep)
 
 
 def run_model(model: ModelKind, p: ModelParams, mode: ExecutionMode, master_seed: int = 1,
-              tlp_block_size: int = 256) -> ModelRun:
+              tlp_block_size: int = 256, jit: bool = False) -> ModelRun:
     """run_model (models.cpp:329-397) through the reference's IR path, on the GPU
-    interpreter: build_kernel -> random_spacing -> assign_lane_streams -> simulate."""
+    interpreter (or compiled, jit=True): build_kernel -> random_spacing ->
+    assign_lane_streams -> simulate."""
     model, mode = ModelKind(model), ExecutionMode(mode)
     names = OUTPUT_NAMES[model]
     R = int(p.replications)
@@ -135,7 +145,8 @@ def run_model(model: ModelKind, p: ModelParams, mode: ExecutionMode, master_seed
     rep = _Report()
     warn = C.create_string_buffer(512)
     _check(_cxx().warpsim_ir_run_model(int(model), C.byref(_params(p)), int(mode), master_seed & (2**64 - 1),
-                                       int(tlp_block_size), o[0], o[1], o[2], C.byref(rep), warn, 512))
+                                       int(tlp_block_size), o[0], o[1], o[2], C.byref(rep), warn, 512,
+                                       int(bool(jit))))
     outputs = dict(zip(names, outs))
     plan = plan_launch(R, mode, None, tlp_block_size)
     return ModelRun(outputs, outputs[PRIMARY[model]], _report(rep), plan.cfg, mode, warn.value.decode() or None)

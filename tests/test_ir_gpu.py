@@ -107,3 +107,43 @@ def test_user_defined_kernel_runs_a_model_without_recompiling(gpu, port):
     ir.simulate(c["text"], cfg_of(c["cfg"]), {"replications": 150, "draws": 200}, {"out": out}, keys)
     want = port.replications(0, oracle.params(draws=200), keys)["out"]
     assert np.array_equal(out, want)
+
+
+# ---- the same kernels compiled (IR -> CUDA C++ -> NVRTC -> sm_100a) ---------------------------
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_jit_corpus_memory_matches_reference_simulator(gpu, name):
+    c = CASES[name]
+    arrays = fresh_arrays(c)
+    rep = ir.simulate(c["text"], cfg_of(c["cfg"]), c["scalars"], arrays, streams_for(c), jit=True)
+    want = CORPUS["cases"][name]
+    for k, v in arrays.items():
+        assert [float(x).hex() for x in v] == want["arrays"][k], k
+    assert rep.kernel_ms > 0 and rep.issues == 0  # no lockstep accounting when compiled
+
+
+@pytest.mark.parametrize("name", sorted(set(FAULTS) - {"mask_stack"}))  # no mask stack when compiled
+def test_jit_faults_raise_fault_error(gpu, name):
+    text, _ = FAULTS[name]
+    with pytest.raises(w.FaultError) as e:
+        ir.simulate(text, w.LaunchConfig((32, 1, 1), (1, 1), 32), {}, {"o": np.zeros(4)}, None, jit=True)
+    want = CORPUS["faults"][name]["message"]
+    assert str(e.value).split(":")[0] == want.split(":")[0]
+
+
+def test_jit_loop_guard_stops_a_kernel_that_never_ends(gpu):
+    text = "(kernel (local x int) (body (while (ge x 0) (assign x (add x 1)))))"
+    with pytest.raises(w.FaultError, match="issue budget"):
+        ir.simulate(text, w.LaunchConfig((64, 1, 1), (4, 1), 32), {}, {}, None, w.SimOptions(maxIssuesPerWarp=5000),
+                    jit=True)
+
+
+@pytest.mark.parametrize("model", [0, 1, 2])
+@pytest.mark.parametrize("mode", [w.ExecutionMode.Tlp, w.ExecutionMode.Wlp])
+def test_jit_run_model_equals_engine(gpu, port, model, mode):
+    p = w.ModelParams(replications=300, draws=200, clients=150, steps=170, chunks=9, lambda_=0.8, mu=1.1)
+    run = w.run_model(w.ModelKind(model), p, mode, master_seed=5, opts=w.SimOptions(irInterpreter=True, irJit=True))
+    want = port.run_model(model, oracle.params_from(p), 5)
+    for name in oracle.OUTPUTS[model]:
+        assert np.array_equal(run.outputs[name], want[name]), name

@@ -62,3 +62,40 @@ def test_malformed_text_is_a_parse_error_in_both(ref, text):
 def test_parse_error_carries_a_line_reference():
     with pytest.raises(w.ParseError, match=r"line 3"):
         ir.canonical("(kernel (local x int)\n (body\n  (assign y 1)))")
+
+
+def _nvrtc_compile(src: str) -> str:
+    """Compile a JIT source for sm_100a with NVRTC (no GPU needed); returns '' or the log."""
+    import ctypes as C
+
+    from conftest import ROOT
+
+    lib = C.CDLL("libnvrtc.so.12")
+    csrc = ROOT / "paper_1501_01405_b200" / "csrc"
+    names = ["taus88.cuh", "glibc_log.cuh", "glibc_log_data.h", "stdint.h"]
+    texts = [(csrc / n).read_text() for n in names[:3]] + [
+        "#pragma once\ntypedef unsigned int uint32_t; typedef int int32_t; typedef unsigned long long uint64_t;\n"
+        "typedef long long int64_t;\n"]
+    prog = C.c_void_p()
+    arr = C.c_char_p * 4
+    assert lib.nvrtcCreateProgram(C.byref(prog), src.encode(), b"k.cu", 4, arr(*[t.encode() for t in texts]),
+                                  arr(*[n.encode() for n in names])) == 0
+    opts = (C.c_char_p * 4)(b"--gpu-architecture=sm_100a", b"--fmad=false", b"--std=c++17", b"-default-device")
+    rc = lib.nvrtcCompileProgram(prog, 4, opts)
+    size = C.c_size_t()
+    lib.nvrtcGetProgramLogSize(prog, C.byref(size))
+    log = C.create_string_buffer(size.value)
+    lib.nvrtcGetProgramLog(prog, log)
+    lib.nvrtcDestroyProgram(C.byref(prog))
+    return "" if rc == 0 else log.value.decode()
+
+
+@pytest.mark.parametrize("which", ["models"] + sorted(CASES))
+def test_jit_sources_compile_for_sm100a(which):
+    # the IR JIT's generated CUDA C++ compiles with NVRTC (the compiler the library dlopens)
+    texts = ([ir.model_text(w.ModelKind(m), w.ExecutionMode(md)) for m in range(3) for md in (1, 2)]
+             if which == "models" else [CASES[which]["text"]])
+    for t in texts:
+        src = ir.jit_source(t)
+        assert "extern \"C\" __global__" in src
+        assert _nvrtc_compile(src) == ""
