@@ -14,8 +14,8 @@
 // User-defined models therefore run on the B200 without recompiling: write the kernel
 // in the text form, parse_kernel, simulate.
 //
-// Not provided: the host simulator itself (WarpState / run_warp / run_single_thread,
-// warp_exec.hpp) and the Fermi dispatch model (plan_dispatch, load_profile,
+// Not provided: the host simulator itself (WarpState / run_warp, warp_exec.hpp;
+// simulate_single_thread stands in for run_single_thread) and the Fermi dispatch model (plan_dispatch, load_profile,
 // report_mem_ratio) — the hardware replaces them. warpSize must be <= 32 (one hardware
 // warp per IR warp); the reference accepts up to 64.
 #pragma once
@@ -183,10 +183,18 @@ SimReport simulate(const KernelProgram& prog, const LaunchConfig& cfg, const Dev
                    GlobalMemory& memory, const std::map<std::string, Value>& scalars,
                    const std::vector<RngState>& streams, const SimOptions& opts = {});
 
+// run_single_thread (warp_exec.hpp:95-98) on the GPU interpreter: one thread, warpSize 1,
+// the given stream and initial locals; the report holds that run's counters.
+SimReport simulate_single_thread(const KernelProgram& prog, GlobalMemory& memory,
+                                 const std::map<std::string, Value>& scalars, RngState stream,
+                                 const std::map<std::string, Value>& initial_locals = {},
+                                 const SimOptions& opts = {});
+
 // run_model through the IR path of the reference (build_kernel -> random_spacing ->
-// assign_lane_streams -> simulate), on the GPU interpreter, for mode Tlp or Wlp. Same
-// outputs as run_model (bit-identical to Sequential) and the reference simulator's
-// counters. run_model itself does this when SimOptions::irInterpreter is set.
+// assign_lane_streams -> simulate), on the GPU interpreter. Same outputs as run_model
+// (bit-identical to Sequential) and the reference simulator's counters; for Sequential,
+// the reference's unit-cost report (one body execution times R, models.cpp:377-389).
+// run_model itself does this when SimOptions::irInterpreter is set.
 ModelRun run_model_ir(ModelKind model, const ModelParams& p, ExecutionMode mode, const DeviceProfile& prof,
                       std::uint64_t master_seed, int tlp_block_size = 256, const SimOptions& opts = {});
 

@@ -535,7 +535,7 @@ def run_model(model: ModelKind, p: ModelParams, mode: ExecutionMode, prof: Optio
     its `cfg` is the reference's single-thread geometry.
     """
     model, mode = ModelKind(model), ExecutionMode(mode)
-    if opts is not None and opts.irInterpreter and mode != ExecutionMode.Sequential:
+    if opts is not None and opts.irInterpreter:
         from . import ir  # the reference's IR kernels on the GPU interpreter (or compiled)
 
         return ir.run_model(model, p, mode, master_seed, tlp_block_size, jit=opts.irJit)

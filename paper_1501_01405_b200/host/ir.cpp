@@ -1072,16 +1072,29 @@ SimReport report_of(const wlp_report& r) {
 
 }  // namespace
 
-SimReport simulate(const KernelProgram& prog, const LaunchConfig& cfg, const DeviceProfile& prof, GlobalMemory& memory,
-                   const std::map<std::string, Value>& scalars, const std::vector<RngState>& streams,
-                   const SimOptions& opts) {
+namespace {
+
+SimReport simulate_impl(const KernelProgram& prog, const LaunchConfig& cfg, const DeviceProfile& prof,
+                        GlobalMemory& memory, const std::map<std::string, Value>& scalars,
+                        const std::vector<RngState>& streams, const SimOptions& opts,
+                        const std::map<std::string, Value>& initial_locals) {
     validate_launch(cfg);
     prog.finalize();
     if (cfg.threads_per_block() > prof.maxThreadsPerBlock)
         throw PlanError("block of " + std::to_string(cfg.threads_per_block()) + " threads exceeds maxThreadsPerBlock " +
                         std::to_string(prof.maxThreadsPerBlock));
     ParamEnv env = bind_params(prog, scalars, memory);
-    const Flat f = flatten(prog, &env);
+    Flat f = flatten(prog, &env);
+    for (const auto& [name, v] : initial_locals) {  // WarpState's initial_locals (warp_exec.cpp:79-86)
+        const int slot = prog.local_slot(name);
+        if (slot < 0) throw DomainError("initial value for undeclared local '" + name + "'");
+        if (prog.locals[slot].type == ValueType::Int) {
+            if (!v.is_int()) throw FaultError("assign: real value into int local '" + name + "'");
+            f.local_init[slot] = v.i;
+        } else {
+            f.local_init[slot] = static_cast<std::int64_t>(bits_of(v.as_real()));
+        }
+    }
     const wlp_ir_program v = view(f);
     std::vector<double*> arrays(prog.params.size(), nullptr);
     std::vector<std::int64_t> lens(prog.params.size(), 0);
@@ -1119,13 +1132,50 @@ SimReport simulate(const KernelProgram& prog, const LaunchConfig& cfg, const Dev
     return report_of(rep);
 }
 
+}  // namespace
+
+SimReport simulate(const KernelProgram& prog, const LaunchConfig& cfg, const DeviceProfile& prof, GlobalMemory& memory,
+                   const std::map<std::string, Value>& scalars, const std::vector<RngState>& streams,
+                   const SimOptions& opts) {
+    return simulate_impl(prog, cfg, prof, memory, scalars, streams, opts, {});
+}
+
+SimReport simulate_single_thread(const KernelProgram& prog, GlobalMemory& memory,
+                                 const std::map<std::string, Value>& scalars, RngState stream,
+                                 const std::map<std::string, Value>& initial_locals, const SimOptions& opts) {
+    LaunchConfig cfg;  // run_single_thread (warp_exec.cpp:308-316): one thread, warpSize 1
+    cfg.blockDim = {1, 1, 1};
+    cfg.gridDim = {1, 1};
+    cfg.warpSize = 1;
+    return simulate_impl(prog, cfg, DeviceProfile{}, memory, scalars, {stream}, opts, initial_locals);
+}
+
 ModelRun run_model_ir(ModelKind model, const ModelParams& p, ExecutionMode mode, const DeviceProfile& prof,
                       std::uint64_t master_seed, int tlp_block_size, const SimOptions& opts) {
-    if (mode == ExecutionMode::Sequential)
-        throw DomainError("run_model_ir: the IR path runs the Tlp or Wlp kernel (Sequential is the host loop)");
     KernelBundle b = build_kernel(model, p, mode, prof, tlp_block_size);
     RngState master = rng_state_from_seed(master_seed);
     const std::vector<RngState> streams = random_spacing(master, static_cast<std::size_t>(p.replications));
+    if (mode == ExecutionMode::Sequential) {
+        // models.cpp:345-389: the outputs of the host loop (here the engine, bit-identical)
+        // and the unit-cost report of ONE body execution (rid = 0, stream 0) times R
+        ModelRun run = run_model(model, p, mode, prof, master_seed, tlp_block_size);
+        GlobalMemory mem;
+        for (const auto& [name, size] : b.arrays) mem.arrays[name].assign(static_cast<std::size_t>(size), 0.0);
+        SimOptions one = opts;
+        one.irJit = false;  // the accounting needs the interpreter
+        const SimReport st = simulate_single_thread(b.program, mem, b.scalars, streams[0], {{"rid", Value::integer(0)}},
+                                                    one);
+        const auto R = static_cast<std::uint64_t>(p.replications);
+        run.report = SimReport{};
+        run.report.totalCycles = static_cast<std::int64_t>(st.issues * R);
+        run.report.peakResidentWarps = 1;
+        run.report.issues = st.issues * R;
+        run.report.aluIssues = st.aluIssues * R;
+        run.report.memReads = st.memReads * R;
+        run.report.memWrites = st.memWrites * R;
+        run.report.kernelMs = st.kernelMs;
+        return run;
+    }
     ModelRun run;
     run.cfg = b.cfg;
     run.mode = mode;

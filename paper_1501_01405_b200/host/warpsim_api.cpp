@@ -224,7 +224,7 @@ ModelRun run_model(ModelKind model, const ModelParams& p, ExecutionMode mode, co
             if (on) wlp_set_hw_counters(0);
         }
     } counters(opts.hardwareCounters);
-    if (opts.irInterpreter && mode != ExecutionMode::Sequential)  // the reference's IR kernels, on the GPU
+    if (opts.irInterpreter)  // the reference's IR kernels (and its Sequential accounting), on the GPU
         return run_model_ir(model, p, mode, prof, master_seed, tlp_block_size, opts);
     const LaunchPlan plan = plan_launch(p.replications, mode, prof, tlp_block_size, 0x7FFFFFFF);
     const wlp_params c = to_c(p);

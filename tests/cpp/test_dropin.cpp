@@ -392,7 +392,9 @@ static void ir_gpu_tests() {
                 CHECK(a.outputs == b.outputs);
                 CHECK(a.report.issues > 0 && a.report.memWrites > 0);
             }
-        CHECK_THROWS_AS(run_model_ir(ModelKind::Pi, p, ExecutionMode::Sequential, prof, 7), DomainError);
+        const ModelRun seq = run_model_ir(ModelKind::Pi, p, ExecutionMode::Sequential, prof, 7);
+        CHECK(seq.outputs == run_model(ModelKind::Pi, p, ExecutionMode::Sequential, prof, 7).outputs);
+        CHECK(seq.report.issues > 0 && seq.report.totalCycles == static_cast<std::int64_t>(seq.report.issues));
     });
     test_case("IR on the GPU: faults are FaultError", [&] {
         GlobalMemory mem;

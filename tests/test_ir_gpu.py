@@ -147,3 +147,19 @@ def test_jit_run_model_equals_engine(gpu, port, model, mode):
     want = port.run_model(model, oracle.params_from(p), 5)
     for name in oracle.OUTPUTS[model]:
         assert np.array_equal(run.outputs[name], want[name]), name
+
+
+@pytest.mark.parametrize("model", [0, 1, 2])
+def test_sequential_report_is_the_reference_unit_cost_accounting(gpu, ref, model):
+    # models.cpp:377-389: Sequential charges R x the issues of ONE body execution (rid 0,
+    # stream 0, one thread of warpSize 1); the IR path reproduces those numbers exactly
+    kw = dict(replications=23, draws=70, clients=60, steps=50, chunks=7)
+    p = w.ModelParams(**kw)
+    run = w.run_model(w.ModelKind(model), p, w.ExecutionMode.Sequential, master_seed=11,
+                      opts=w.SimOptions(irInterpreter=True))
+    want = ref.run_model_report(model, oracle.params(**kw), 11, 0)
+    for k in ("totalCycles", "issues", "aluIssues", "memReads", "memWrites", "divergenceEvents", "peakResidentWarps"):
+        assert getattr(run.report, k) == want[k], k
+    plain = w.run_model(w.ModelKind(model), p, w.ExecutionMode.Sequential, master_seed=11)
+    for name in oracle.OUTPUTS[model]:
+        assert np.array_equal(run.outputs[name], plain.outputs[name])
