@@ -99,3 +99,55 @@ def test_jit_sources_compile_for_sm100a(which):
         src = ir.jit_source(t)
         assert "extern \"C\" __global__" in src
         assert _nvrtc_compile(src) == ""
+
+
+def test_c_abi_rejects_malformed_flattened_programs():
+    # wlp_ir_simulate / wlp_ir_jit_source check every index and every expression of a
+    # flattened program on the host before anything reaches a device (include/wlp_b200.h)
+    import ctypes as C
+
+    lib = w.native_library()
+
+    class Stmt(C.Structure):
+        _fields_ = [(n, C.c_int32) for n in ("kind", "slot", "arr", "code_a", "code_b", "b1_begin", "b1_end",
+                                              "b2_begin", "b2_end", "flags")]
+
+    class Prog(C.Structure):
+        _fields_ = [("stmts", C.POINTER(Stmt)), ("n_stmts", C.c_int32), ("top_begin", C.c_int32),
+                    ("top_end", C.c_int32), ("code", C.POINTER(C.c_int32)), ("n_code", C.c_int32),
+                    ("n_locals", C.c_int32), ("local_init", C.POINTER(C.c_int64)), ("n_params", C.c_int32),
+                    ("param_bits", C.POINTER(C.c_int64)), ("param_is_array", C.POINTER(C.c_int32))]
+
+    def prog(stmts, code, n_locals=1, top=None):
+        S = (Stmt * max(len(stmts), 1))(*[Stmt(*s) for s in stmts])
+        K = (C.c_int32 * len(code))(*code)
+        L = (C.c_int64 * max(n_locals, 1))()
+        P = (C.c_int64 * 1)()
+        A = (C.c_int32 * 1)(0)
+        t = top or (0, len(stmts))
+        return Prog(S, len(stmts), t[0], t[1], K, len(code), n_locals, L, 1, P, A), (S, K, L, P, A)
+
+    OP_CONST, OP_LOCAL, OP_END, OP_ADD_I = 1, 2, 0, 10
+    good = ([(0, 0, -1, 0, -1, 0, 0, 0, 0, 0)], [OP_CONST, 5, 0, OP_END])
+    bad = [
+        ([(0, 3, -1, 0, -1, 0, 0, 0, 0, 0)], [OP_CONST, 5, 0, OP_END]),          # local slot out of range
+        ([(0, 0, -1, 9, -1, 0, 0, 0, 0, 0)], [OP_CONST, 5, 0, OP_END]),          # code offset out of range
+        ([(0, 0, -1, 1, -1, 0, 0, 0, 0, 0)], [OP_CONST, 5, 0, OP_END]),          # offset inside an expression
+        ([(0, 0, -1, 0, -1, 0, 0, 0, 0, 0)], [OP_ADD_I, OP_END]),                 # stack underflow
+        ([(0, 0, -1, 0, -1, 0, 0, 0, 0, 0)], [OP_CONST, 5, 0, OP_CONST, 1, 0, OP_END]),  # two values left
+        ([(0, 0, -1, 0, -1, 0, 0, 0, 0, 0)], [OP_LOCAL, 7, OP_END]),              # bad local in code
+        ([(0, 0, -1, 0, -1, 0, 0, 0, 0, 0)], [99, OP_END]),                       # unknown opcode
+        ([(0, 0, -1, 0, -1, 0, 0, 0, 0, 0)], [OP_CONST, 5]),                      # unterminated
+        ([(3, -1, -1, 0, -1, 0, 5, 0, 0, 0)], [OP_CONST, 1, 0, OP_END]),          # body range past the end
+        ([(2, 0, -1, 0, 0, 0, 0, 0, 0, 0)], [OP_CONST, 1, 0, OP_END]),            # store to a scalar param
+        ([(7, 0, -1, 0, -1, 0, 0, 0, 0, 0)], [OP_CONST, 1, 0, OP_END]),           # unknown statement kind
+    ]
+    need = C.c_int(0)
+    p, keep = prog(*good)
+    assert lib.wlp_ir_jit_source(C.byref(p), None, 0, C.byref(need)) == 0 and need.value > 100
+    for stmts, code in bad:
+        p, keep = prog(stmts, code)
+        assert lib.wlp_ir_jit_source(C.byref(p), None, 0, C.byref(need)) == w.EDOMAIN, (stmts, code)
+        cfg = w._Cfg(32, 1, 1, 1, 1, 32)
+        rc = lib.wlp_ir_simulate(C.byref(p), C.byref(cfg), 1024, None, None, 0, None, 0, 0, 32, 1000, None, None)
+        assert rc == w.EDOMAIN, (stmts, code)
