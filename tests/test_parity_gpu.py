@@ -310,3 +310,26 @@ def test_pipeline_full_size_equals_lane_jumps(gpu, model, kw):
             outs[v] = _device_run(gpu, model, p, gpu.ExecutionMode.Wlp, 42)
     for a, b in zip(outs[1], outs[2]):
         assert np.array_equal(a, b)
+
+
+def test_randomized_configurations_all_kernels_vs_oracle(gpu, port):
+    # 150 random small configurations: every model, mode and WLP kernel variant, ragged
+    # unit counts, rates that are / are not powers of two, light to overloaded queues
+    rng = np.random.default_rng(20261017)
+    for it in range(150):
+        model = int(rng.integers(0, 3))
+        R = int(rng.choice([1, 2, 31, 32, 33, 64, 65, 100, 257, 1000, 3000]))
+        N = int(rng.choice([1, 2, 3, 7, 31, 32, 33, 63, 64, 65, 127, 128, 129, 255, 256, 257, 500, 1000, 2049]))
+        lam = float(rng.choice([0.125, 0.25, 0.5, 0.3, 0.7, 0.9, 1.0, 1.7]))
+        mu = float(rng.choice([0.5, 1.0, 2.0, 0.8, 1.3]))
+        p = gpu.ModelParams(replications=R, draws=N, clients=N, steps=N, chunks=int(rng.integers(2, 40)),
+                            lambda_=lam, mu=mu)
+        seed = int(rng.integers(0, 2**63))
+        want = port.run_model(model, oracle.params_from(p), seed)
+        mode = gpu.ExecutionMode(int(rng.integers(0, 3)))
+        variant = int(rng.integers(0, 3))
+        with gpu.wlp_variant(variant):
+            run = gpu.run_model(gpu.ModelKind(model), p, mode, master_seed=seed,
+                                tlp_block_size=int(rng.choice([32, 50, 128, 256])))
+        for name in oracle.OUTPUTS[model]:
+            assert np.array_equal(run.outputs[name], want[name]), (it, model, R, N, lam, mu, mode, variant, name)
