@@ -21,9 +21,11 @@ across ranks (all_gather of sufficient statistics), -> mean / 95% CI.
          CI; at N>1 the sharded step plus the D2H of the shard's outputs. Wall clock
          (perf_counter with synchronize), max over ranks.
 
-Extras (N=1): WLP and TLP rates for every model/config of BASELINE (2, 3, 4), the
-ALU-issue roofline of the dominant kernel, and the CPU baseline (the reference's own
-replication functions, oracle/_ref, on all host cores, bounded sample).
+Extras (N=1): WLP and TLP rates for every model/config of BASELINE (2, 3, 4, 5), the
+ALU-issue roofline of the dominant kernel, the IR path (interpreter and JIT), and the CPU
+baseline (the reference's own replication functions, oracle/_ref, on all host cores,
+bounded sample). Under torchrun (every N): "cfg4_sharded_1e7" — BASELINE config 4 as
+stated, all three models with 10^7 replications in total sharded over the N GPUs.
 """
 from __future__ import annotations
 
@@ -139,7 +141,19 @@ def dist_setup():
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL's "NCCL version ..." banner goes to stdout at communicator creation; keep
+        # stdout for the one JSON line by pointing fd 1 at stderr while the comm comes up
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.barrier()
+            torch.cuda.synchronize()
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
     else:
         torch.cuda.set_device(0)
     return world, rank, local
@@ -389,6 +403,22 @@ def main():
             "gpu_launches": launches, "clocks": clk, "roofline": roofline,
             "result": {"mean": ci.mean, "half_width": ci.halfWidth, "n": ci.n}}
 
+    if (world > 1 or "LOCAL_RANK" in os.environ) and not args.no_extras:
+        # BASELINE config 4 as stated (every torchrun launch, N >= 1): all models, 10^7
+        # replications in total sharded over the N GPUs (strong scaling), WLP, the two
+        # statistics exchanges included; time is the max over ranks of the device time
+        sharded = {}
+        for name, m, kw in [("pi", w.ModelKind.Pi, dict(draws=1000)), ("mm1", w.ModelKind.Mm1, dict(clients=1000)),
+                            ("walk", w.ModelKind.Walk, dict(steps=1000, chunks=30))]:
+            p4 = w.ModelParams(replications=10_000_000, **kw)
+            run4 = D.gpu_runner(m, p4, w.ExecutionMode.Wlp, SEED, stream=stream)
+
+            def step4():
+                D.run_sharded(m, p4.replications, run4, stats, comm=comm)
+
+            ms4 = device_timed(step4, 3, 3, world)
+            sharded[name] = {"reps_per_s": p4.replications / (ms4 * 1e-3), "ms_per_run": ms4}
+        line["cfg4_sharded_1e7"] = sharded
     if world == 1 and not args.no_extras:
         extras = {}
         cfgs = [("cfg2_pi_1e6x1e4", w.ModelKind.Pi, dict(replications=1_000_000, draws=10_000)),
