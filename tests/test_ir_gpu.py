@@ -163,3 +163,18 @@ def test_sequential_report_is_the_reference_unit_cost_accounting(gpu, ref, model
     plain = w.run_model(w.ModelKind(model), p, w.ExecutionMode.Sequential, master_seed=11)
     for name in oracle.OUTPUTS[model]:
         assert np.array_equal(run.outputs[name], plain.outputs[name])
+
+
+@pytest.mark.parametrize("jit", [False, True])
+def test_readme_user_model_example(gpu, port, jit):
+    text = """(kernel (param n int) (param draws int) (param out array)
+  (local r int) (local i int) (local x real) (local c real)
+  (body (assign r (add tid.x (mul bdim.x bid.x)))
+        (if (lt r n) (then
+          (while (lt i draws) (assign x (draw)) (assign c (add c (lt x 0.25))) (assign i (add i 1)))
+          (store out r (div c draws))))))"""
+    out = np.zeros(1000)
+    keys = w.random_spacing_seed(7, 1000)
+    ir.simulate(text, w.LaunchConfig((256, 1, 1), (4, 1), 32), {"n": 1000, "draws": 500}, {"out": out}, keys, jit=jit)
+    want = [np.count_nonzero(port.taus_stream(*map(int, keys[:, r]), 500) < 2**30) / 500 for r in range(1000)]
+    assert np.array_equal(out, np.array(want))
