@@ -202,39 +202,49 @@ struct NearList {  // per-warp compaction scratch
     uint32_t n[32 * kExpoB];
 };
 
-// -log(1 - n*2^-32) for every lane's B inputs. The near-one inputs are listed in nl, each
-// evaluated by one lane into res[pos], and picked up by their owner. FULL: all 32 lanes
-// take part (no divergence checks); else `mask_` names the lanes of a partial warp.
+// -log(1 - n*2^-32) for every lane's B inputs. Each lane flags its near-one inputs in a
+// B-bit mask; an exclusive prefix sum of the flag counts over the lanes (five shuffles per
+// batch, instead of a ballot and popcounts per input) places them in nl, each is
+// evaluated by one lane into res[pos], and picked up by its owner. FULL: all 32 lanes take
+// part; else `mask_` names the (contiguous, low) lanes of a partial warp.
 template <int B, bool FULL>
 __device__ __forceinline__ void neg_log1m_batch(const uint32_t (&n)[B], double (&e)[B], const double* tab,
                                                 NearList& nl, double* res, unsigned mask_, int lane) {
+    static_assert(B <= 32, "near flags fit one word");
     const unsigned mask = FULL ? kFull : mask_;
-    int pos[B];
-    int total = 0;
-    const unsigned lt = (1u << lane) - 1u;
+    unsigned near = 0;
 #pragma unroll
     for (int j = 0; j < B; ++j) {
         // 1 - u >= 1 - 2^-4 (glibc's near-one window) exactly when n <= 2^28; n = 0 (1 - u
         // = 1) is near too, so the table path may see the wrapped x = 0 there: its value is
         // replaced below
-        const bool near = n[j] <= 0x10000000u;
         e[j] = -log_table_dev(one_minus_u32_nz(n[j]), tab);
-        const unsigned b = __ballot_sync(mask, near);
-        pos[j] = near ? total + __popc(b & lt) : -1;
-        if (near) nl.n[pos[j]] = n[j];
-        total += __popc(b);
+        if (n[j] <= 0x10000000u) near |= 1u << j;
     }
-    if (total == 0) return;  // warp-uniform
-    __syncwarp(mask);
+    const int c = __popc(near);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(mask, incl, o);
+        if (lane >= o) incl += v;
+    }
     const int width = FULL ? 32 : __popc(mask);
+    const int total = __shfl_sync(mask, incl, width - 1);
+    if (total == 0) return;  // warp-uniform
+    int pos = incl - c;
+#pragma unroll
+    for (int j = 0; j < B; ++j)
+        if (near >> j & 1u) nl.n[pos++] = n[j];
+    __syncwarp(mask);
     for (int p = lane; p < total; p += width) {
         const uint32_t v = nl.n[p];
         res[p] = v == 0u ? -0.0 : -log_near_one(one_minus_u32_dev(v));
     }
     __syncwarp(mask);
+    pos = incl - c;
 #pragma unroll
     for (int j = 0; j < B; ++j)
-        if (pos[j] >= 0) e[j] = res[pos[j]];
+        if (near >> j & 1u) e[j] = res[pos++];
     __syncwarp(mask);
 }
 
