@@ -145,6 +145,24 @@ __device__ __forceinline__ uint32_t pi_hits(Taus& st, uint32_t units) {
 // step we add the cubic q(d) = -4d^3 + 21d^2 - 29d (= 6*([d==0]-[d==1]) - 6 on {0..3}) by
 // Horner in three IMADs (FMA pipe) instead of compares and selects (ALU pipe); then
 // dx = (sum q + 6*units) / 6 exactly. |sum| <= 12*units < 2^31 for units < 2^27.
+// The raw sum of q over `units` steps (units < 2^27); dx = (sum + 6*units) / 6.
+__device__ __forceinline__ int walk_q(Taus& st, uint32_t units) {
+    int acc = 0;
+    uint32_t u = 0;
+    for (; u + 8 <= units; u += 8) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int d = static_cast<int>(taus_next_skip1(st) >> 30);
+            acc += (((21 - 4 * d) * d) - 29) * d;
+        }
+    }
+    for (; u < units; ++u) {
+        const int d = static_cast<int>(taus_next_skip1(st) >> 30);
+        acc += (((21 - 4 * d) * d) - 29) * d;
+    }
+    return acc;
+}
+
 __device__ __forceinline__ int walk_dx_block(Taus& st, uint32_t units) {
     int acc = 0;
     uint32_t u = 0;
@@ -473,7 +491,7 @@ __global__ void __launch_bounds__(kWlpBlock, 3) k_wlp_lanes(RepArgs a, const uin
 // at once. No jump tables at all; the cost is the 31-step drain per warp, so the launcher
 // picks this kernel when replications per warp are many and units per replication few
 // (config 4: 1400 replications of 32 units per lane).
-// WIDE: 64-bit sums and indices (n or count >= 2^31); else 32-bit, fewer shuffles.
+// WIDE: 64-bit sums and indices (n >= 2^27 or count >= 2^31); else 32-bit, fewer shuffles.
 template <int MODEL, bool WIDE>
 __global__ void __launch_bounds__(kWlpBlock, 3) k_wlp_pipe(RepArgs a, int64_t K) {
     using I = typename std::conditional<WIDE, long long, int>::type;
@@ -490,10 +508,10 @@ __global__ void __launch_bounds__(kWlpBlock, 3) k_wlp_pipe(RepArgs a, int64_t K)
     int nemit = 0;
     auto flush = [&](int cnt) {
         __syncwarp();
-        if (lane < cnt) {
+        if (lane < cnt) {  // pi: hits; walk: the raw q sum, dx = (sum + 6n) / 6
             const I r = emit_rep[wid][lane], c = emit_sum[wid][lane];
             a.out0[r] = MODEL == 0 ? __ddiv_rn(__dmul_rn(4.0, static_cast<double>(c)), static_cast<double>(a.n))
-                                   : walk_fold(static_cast<int64_t>(c), a.chunks);
+                                   : walk_fold((static_cast<int64_t>(c) + 6 * a.n) / 6, a.chunks);
         }
         __syncwarp();
     };
@@ -516,7 +534,7 @@ __global__ void __launch_bounds__(kWlpBlock, 3) k_wlp_pipe(RepArgs a, int64_t K)
         }
         if (more) ++cur;
         if (!__any_sync(kFull, rep >= 0)) break;
-        if (rep >= 0) sum += MODEL == 0 ? static_cast<I>(pi_hits(st, units)) : static_cast<I>(walk_dx(st, units));
+        if (rep >= 0) sum += MODEL == 0 ? static_cast<I>(pi_hits(st, units)) : static_cast<I>(walk_q(st, units));
         if (__shfl_sync(kFull, rep, 31) >= 0) {  // lane 31 finished a replication
             if (lane == 31) {
                 emit_rep[wid][nemit] = rep;
@@ -1361,7 +1379,8 @@ cudaError_t launch_wlp(int model, const RepArgs& a, const uint32_t* lane_tab, co
 
 cudaError_t launch_wlp_pipe(int model, const RepArgs& a, int64_t lane_units, int grid, cudaStream_t st) {
     if (a.count <= 0) return cudaSuccess;
-    const bool wide = a.n >= (int64_t(1) << 31) || a.count >= (int64_t(1) << 31);
+    // 32-bit sums hold pi's hits (< n) and the walk's raw q sum (|sum| <= 12 n)
+    const bool wide = a.n >= (int64_t(1) << 27) || a.count >= (int64_t(1) << 31);
     if (model == 0)
         wide ? k_wlp_pipe<0, true><<<grid, kWlpBlock, 0, st>>>(a, lane_units)
              : k_wlp_pipe<0, false><<<grid, kWlpBlock, 0, st>>>(a, lane_units);
