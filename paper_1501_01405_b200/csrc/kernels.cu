@@ -438,7 +438,7 @@ __device__ __forceinline__ int64_t grab_take(unsigned long long ticket) {
 }
 
 template <int MODEL, bool COUNT>
-__global__ void __launch_bounds__(kWlpBlock, 3) k_wlp_lanes(RepArgs a, const uint32_t* __restrict__ gtab,
+__global__ void __launch_bounds__(kWlpBlock, 4) k_wlp_lanes(RepArgs a, const uint32_t* __restrict__ gtab,
                                                              int64_t K) {
     extern __shared__ uint32_t tab[];  // kLaneTabWords
     stage_u32<kLaneTabWords>(tab, gtab);
