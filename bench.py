@@ -287,9 +287,11 @@ def run_reference_arm(args):
     import paper_1501_01405_b200 as w
 
     p = w.ModelParams(replications=R_PER_GPU * world, draws=DRAWS)
-    # one calibration/warm-up step sizes each step at ~6 s of CPU work, then exactly K steps
-    cal = cpu_baseline(0, p, budget_s=6.0)
-    rates = [cpu_baseline(0, p, budget_s=6.0)["value"] for _ in range(args.steps)]
+    # one calibration/warm-up step, then exactly K steps, each a bounded sample: ~6 s of CPU
+    # work, less when K is large, so the whole arm stays within ~2.5 minutes
+    budget = max(1.0, min(6.0, 150.0 / (args.steps + 1)))
+    cal = cpu_baseline(0, p, budget_s=budget)
+    rates = [cpu_baseline(0, p, budget_s=budget)["value"] for _ in range(args.steps)]
     v = statistics.mean(rates)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * p.replications / v,
