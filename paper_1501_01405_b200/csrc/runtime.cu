@@ -445,7 +445,7 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
         // per-client cost) but drains 31 steps per warp; segment chaining pays ~1.8x per
         // client but has no drain. Pipeline when the drain is the smaller loss.
         const double per_warp = static_cast<double>(count) / static_cast<double>(warps);
-        const bool pipe = !g_hw_counters && (g_wlp_variant == 2 || (g_wlp_variant == 0 && per_warp > 40.0));
+        const bool pipe = !g_hw_counters && (g_wlp_variant == 2 || (g_wlp_variant == 0 && per_warp > 30.0));
         if (pipe) {
             const int64_t cap = static_cast<int64_t>(c.sms) * c.mm1_pipe_bps;
             grid_out = static_cast<int>(std::min<int64_t>(grid_out, cap));
