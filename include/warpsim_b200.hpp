@@ -196,6 +196,11 @@ struct SweepSpec {
     ModelParams params;
     std::uint64_t masterSeed = 1;
     int tlpBlockSize = 256;
+    // B200 extension: run every point through the reference's IR kernels on the GPU
+    // interpreter (SimOptions::irInterpreter), so the mem_reads / mem_writes /
+    // divergence_events columns are the reference simulator's and the sequential rows are
+    // its unit-cost accounting; total_cycles of the tlp / wlp rows stay measured.
+    bool irCounters = false;
 };
 struct SweepRow {
     std::int64_t replications = 0;

@@ -57,6 +57,7 @@ const char* kUsage =
     "  common:  --model pi|mm1|walk --seed N --tlp-block-size N --profile FILE (ignored)\n"
     "           --draws N --clients N --lambda X --mu X --steps N --chunks N\n"
     "  sweep:   --modes sequential,tlp,wlp --r-min N --r-max N --r-step N [--out FILE] [--wallclock] [--dump-kernel]\n"
+    "           [--ir-counters]  (the reference's IR kernels on the GPU interpreter: its counters)\n"
     "  steps:   CSV_FILE\n"
     "  ci:      --mode wlp --replications N --level 0.95\n";
 
@@ -72,7 +73,7 @@ Args parse(int argc, char** argv) {
             if (eq != std::string::npos) {
                 val = key.substr(eq + 1);
                 key = key.substr(0, eq);
-            } else if (key == "wallclock" || key == "help" || key == "dump-kernel") {
+            } else if (key == "wallclock" || key == "help" || key == "dump-kernel" || key == "ir-counters") {
                 val = "1";
             } else {
                 if (i + 1 >= argc) throw Usage("--" + key + " needs a value");
@@ -121,6 +122,7 @@ int cmd_sweep(const Args& a) {
     spec.params = model_params(a);
     spec.masterSeed = a.uinteger("seed", 1);
     spec.tlpBlockSize = static_cast<int>(a.integer("tlp-block-size", 256));
+    spec.irCounters = a.has("ir-counters");
     if (a.has("dump-kernel")) {  // the IR kernel each mode would run (warpsim_main.cpp:101-110)
         ModelParams p = spec.params;
         p.replications = spec.rMax;

@@ -267,7 +267,9 @@ std::vector<SweepRow> run_sweep(const SweepSpec& spec, const DeviceProfile& prof
         for (std::int64_t R = spec.rMin; R <= spec.rMax; R += spec.rStep) {
             ModelParams params = spec.params;
             params.replications = R;
-            const ModelRun run = run_model(spec.model, params, mode, prof, spec.masterSeed, spec.tlpBlockSize);
+            SimOptions opts;
+            opts.irInterpreter = spec.irCounters;
+            const ModelRun run = run_model(spec.model, params, mode, prof, spec.masterSeed, spec.tlpBlockSize, opts);
             SweepRow row;
             row.replications = R;
             row.mode = mode;

@@ -79,3 +79,21 @@ def test_cli_dump_kernel_prints_the_reference_ir():
     want = "".join(f"; mm1, {m}, R=9\n" + (ROOT / "tests" / "golden" / "ir" / f"mm1_{m}.sexp").read_text() + "\n"
                    for m in ("tlp", "wlp"))
     assert out.stdout == want
+
+
+@pytest.mark.gpu
+def test_cli_sweep_with_ir_counters_matches_reference_golden_csv():
+    # proj/tests/golden/sweep_pi.golden through `warpsim sweep --ir-counters`: every column
+    # of the sequential rows (the unit-cost accounting) and every column but the
+    # Fermi-modelled total_cycles of the tlp / wlp rows equal the reference's CSV
+    out = _run([str(PKG / "warpsim"), "sweep", "--model", "pi", "--modes", "sequential,tlp,wlp", "--r-min", "1",
+                "--r-max", "2", "--draws", "100", "--seed", "42", "--ir-counters"])
+    assert out.returncode == 0
+    got = [r.split(",") for r in out.stdout.strip().splitlines()]
+    want = [r.split(",") for r in (ROOT / "tests" / "golden" / "sweep_pi.csv").read_text().strip().splitlines()]
+    assert got[0] == want[0] and len(got) == len(want)
+    for g, r in zip(got[1:], want[1:]):
+        if g[1] == "sequential":
+            assert g == r
+        else:
+            assert g[:3] + g[4:] == r[:3] + r[4:] and int(g[3]) > 0
