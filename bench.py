@@ -466,6 +466,22 @@ def main():
             pms = device_timed(pstep, 5, 3, 1)
             extras["cfg5_plan_mm1_64x30x1e4"][w.mode_name(md)] = {
                 "reps_per_s": 1920 / (pms * 1e-3), "ms_per_run": pms, "kernel_ms": sum(kms[3:]) / len(kms[3:])}
+        # config 5's trip-count-heterogeneous variant: walk sets with
+        # steps_k = 100 + 30k, so a TLP warp spanning two sets idles lanes; one launch each
+        hsets = [w.ModelParams(replications=30, steps=100 + 30 * k, chunks=30) for k in range(64)]
+        extras["cfg5_plan_walk_hetero_64x30"] = {}
+        for md in (w.ExecutionMode.Wlp, w.ExecutionMode.Tlp):
+            hout = [torch.empty(64 * 30, dtype=torch.float64, device="cuda")]
+            hk = []
+
+            def hstep():
+                rep = w.SimReport()
+                w.run_plan(w.ModelKind.Walk, hsets, seeds, md, hout, on_device=True, report=rep)
+                hk.append(rep.kernel_ms)
+
+            hms = device_timed(hstep, 5, 3, 1)
+            extras["cfg5_plan_walk_hetero_64x30"][w.mode_name(md)] = {
+                "reps_per_s": 1920 / (hms * 1e-3), "ms_per_run": hms, "kernel_ms": sum(hk[3:]) / len(hk[3:])}
         # the reference's own IR kernel (TLP walk) on the GPU IR interpreter:
         # statements issued per second, counters exact; the reference's host simulator on
         # a 10x smaller sample beside it when the CPU legs run
