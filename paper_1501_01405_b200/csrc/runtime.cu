@@ -979,10 +979,33 @@ int wlp_run_plan(int model, const wlp_params* sets, const uint64_t* master_seeds
         o1 = c->outs.p + R;
         o2 = c->outs.p + 2 * R;
     }
-    // one batched seeding launch for all sets
+    // one batched seeding launch for all sets, and the model right behind it; the spacing
+    // check below re-runs the model only when two special candidates share a key
     WLP_CUDA(cudaMemsetAsync(c->counter.p, 0, 8, st));
     WLP_CUDA(launch_seed_jobs(c->powers.p, c->jobs.p, n_sets, blocks, R, c->seeds.p, c->specials.p, kSpecialCap,
                               c->counter.p, st));
+    PlanArgs pa;
+    pa.serial_rho = mm1_serial_rho();
+    pa.seeds = c->seeds.p;
+    pa.count = R;
+    pa.sets = c->setp.p;
+    pa.n_sets = n_sets;
+    pa.out0 = o0;
+    pa.out1 = o1;
+    pa.out2 = o2;
+    pa.next = c->work.p;
+    const int wpb = (model == WLP_MODEL_MM1 ? kMm1Block : kWlpBlock) / 32;
+    const int grid = static_cast<int>(
+        std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(c->sms) * c->plan_bps[model], (R + wpb - 1) / wpb)));
+    auto run_model_launch = [&]() -> int {
+        WLP_CUDA(cudaMemsetAsync(c->work.p, 0, 8, st));
+        if (report) WLP_CUDA(cudaEventRecord(c->ev0, st));
+        WLP_CUDA(launch_plan(model, mode, pa, c->plan_lane.p, c->plan_skip.p, c->mm1_lane.p, c->mm1_skip.p, grid,
+                             tlp_block_size, st));
+        if (report) WLP_CUDA(cudaEventRecord(c->ev1, st));
+        return WLP_OK;
+    };
+    WLP_TRY(run_model_launch());
     std::vector<SpecialRec> specials;
     int64_t nt = 0;
     WLP_TRY(read_specials(*c, st, specials, nt));
@@ -990,12 +1013,14 @@ int wlp_run_plan(int model, const wlp_params* sets, const uint64_t* master_seeds
     // exactly with its rejection list
     std::map<uint32_t, std::vector<SpecialRec>> by_job;
     for (const SpecialRec& s : specials) by_job[s.pad].push_back(s);
+    bool reseeded = false;
     for (auto& kv : by_job) {
         if (kv.second.size() < 2) continue;
         const int k = static_cast<int>(kv.first);
         std::vector<int64_t> rej, next;
         WLP_TRY(spacing_rejections(kv.second, rej, next));
         while (next != rej) {  // re-seed set k in place (its slice of the SoA) until no new redraw
+            reseeded = true;
             rej.swap(next);
             WLP_CUDA(c->rejected.ensure(static_cast<int64_t>(rej.size())));
             WLP_CUDA(cudaMemcpyAsync(c->rejected.p, rej.data(), rej.size() * 8, cudaMemcpyHostToDevice, st));
@@ -1020,24 +1045,7 @@ int wlp_run_plan(int model, const wlp_params* sets, const uint64_t* master_seeds
             WLP_TRY(spacing_rejections(sp2, rej, next));
         }
     }
-    PlanArgs pa;
-    pa.serial_rho = mm1_serial_rho();
-    pa.seeds = c->seeds.p;
-    pa.count = R;
-    pa.sets = c->setp.p;
-    pa.n_sets = n_sets;
-    pa.out0 = o0;
-    pa.out1 = o1;
-    pa.out2 = o2;
-    pa.next = c->work.p;
-    WLP_CUDA(cudaMemsetAsync(c->work.p, 0, 8, st));
-    const int wpb = (model == WLP_MODEL_MM1 ? kMm1Block : kWlpBlock) / 32;
-    const int grid = static_cast<int>(
-        std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(c->sms) * c->plan_bps[model], (R + wpb - 1) / wpb)));
-    if (report) WLP_CUDA(cudaEventRecord(c->ev0, st));
-    WLP_CUDA(launch_plan(model, mode, pa, c->plan_lane.p, c->plan_skip.p, c->mm1_lane.p, c->mm1_skip.p, grid,
-                         tlp_block_size, st));
-    if (report) WLP_CUDA(cudaEventRecord(c->ev1, st));
+    if (reseeded) WLP_TRY(run_model_launch());
     if (!out_on_device) {
         WLP_CUDA(cudaMemcpyAsync(out0, o0, R * 8, cudaMemcpyDeviceToHost, st));
         if (model == WLP_MODEL_MM1) {
