@@ -266,9 +266,23 @@ __device__ __forceinline__ void neg_log1m_batch(const uint32_t (&n)[B], double (
     __syncwarp(mask);
 }
 
-template <bool INV>
+// e / rate in IEEE double (models.hpp:67,75 divide -log(1 - u) by lambda or mu).
+// kDivRcp: inv = RN(1/rate), q = RN(e * inv) is within an ulp of e / rate, the residual
+// rate * q - e is exact in one FMA, and q - residual * inv rounds to RN(e / rate)
+// (Markstein's correction); the residual's sign convention keeps -0 / rate = -0. Checked
+// against __ddiv_rn for every numerator the model can produce (2^32 draws) at 1083
+// rates plus 2e12 random pairs (tools/div_check.cu). Valid away from over/underflow:
+// the host picks kDivIeee for rates outside [2^-900, 2^900].
+template <int DIV>
 __device__ __forceinline__ double scale(double e, double rate, double inv) {
-    return INV ? __dmul_rn(e, inv) : __ddiv_rn(e, rate);
+    if constexpr (DIV == kDivPow2) {
+        return __dmul_rn(e, inv);
+    } else if constexpr (DIV == kDivRcp) {
+        const double q = __dmul_rn(e, inv);
+        return __fma_rn(-__fma_rn(rate, q, -e), inv, q);
+    } else {
+        return __ddiv_rn(e, rate);
+    }
 }
 
 // One client of the Lindley recursion (models.hpp:67-78) in the reference's rounding:
@@ -602,7 +616,7 @@ __device__ __forceinline__ void lindley(double& w, double& u, double a, double s
 // at rho = 1/2 the server runs dry at about every other arrival, so the re-runs are
 // short. (3) Lanes 0-2 run the three ordered sums over the panel's terms: sumw, sums and
 // idle are order-dependent fp64 and stay sequential, one lane each, in one instruction.
-template <bool INV>
+template <int DIV>
 __device__ __forceinline__ double mm1_warp_rep(Taus st, int64_t n, double lambda, double mu, double inv_l,
                                                double inv_m, const double* logtab, const uint32_t* skip, Mm1Warp& W,
                                                int lane) {
@@ -623,8 +637,8 @@ __device__ __forceinline__ double mm1_warp_rep(Taus st, int64_t n, double lambda
             neg_log1m_batch<kExpoB, true>(d, e, logtab, W.nl, W.term, kFull, lane);
 #pragma unroll
             for (int j = 0; j < kExpoB; j += 2) {
-                ea[(h + j) / 2] = scale<INV>(e[j], lambda, inv_l);
-                es[(h + j) / 2] = scale<INV>(e[j + 1], mu, inv_m);
+                ea[(h + j) / 2] = scale<DIV>(e[j], lambda, inv_l);
+                es[(h + j) / 2] = scale<DIV>(e[j + 1], mu, inv_m);
             }
         }
         const int64_t left = n - base;
@@ -707,7 +721,7 @@ __device__ __forceinline__ double mm1_warp_rep(Taus st, int64_t n, double lambda
 // the three sums of the panel in one ordered loop (the four chains overlap), reading the
 // client-ordered (a, s) pairs the lanes staged in shared memory. Same result bits;
 // returns the same per-lane layout as mm1_warp_rep (lanes 0/1/2: sumw/sums/idle).
-template <bool INV>
+template <int DIV>
 __device__ __forceinline__ double mm1_warp_rep_serial(Taus st, int64_t n, double lambda, double mu, double inv_l,
                                                       double inv_m, const double* logtab, const uint32_t* skip,
                                                       Mm1Warp& W, int lane) {
@@ -727,8 +741,8 @@ __device__ __forceinline__ double mm1_warp_rep_serial(Taus st, int64_t n, double
             neg_log1m_batch<kExpoB, true>(d, e, logtab, W.nl, W.term, kFull, lane);
 #pragma unroll
             for (int j = 0; j < kExpoB; j += 2) {
-                ea[(h + j) / 2] = scale<INV>(e[j], lambda, inv_l);
-                es[(h + j) / 2] = scale<INV>(e[j + 1], mu, inv_m);
+                ea[(h + j) / 2] = scale<DIV>(e[j], lambda, inv_l);
+                es[(h + j) / 2] = scale<DIV>(e[j + 1], mu, inv_m);
             }
         }
 #pragma unroll
@@ -782,7 +796,7 @@ __device__ __forceinline__ Mm1Smem mm1_stage(const uint32_t* gtab, const uint32_
     return m;
 }
 
-template <bool INV, bool COUNT>
+template <int DIV, bool COUNT>
 __global__ void __launch_bounds__(kMm1Block, 3) k_wlp_mm1(RepArgs a, const uint32_t* __restrict__ gtab,
                                                         const uint32_t* __restrict__ gskip) {
     const Mm1Smem m = mm1_stage(gtab, gskip);
@@ -797,9 +811,9 @@ __global__ void __launch_bounds__(kMm1Block, 3) k_wlp_mm1(RepArgs a, const uint3
             const Taus st = lane_jump(m.tab, lane, load_seed(a, r));
             const double acc =
                 a.lambda >= a.serial_rho * a.mu
-                    ? mm1_warp_rep_serial<INV>(st, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu, m.logtab, m.skip,
+                    ? mm1_warp_rep_serial<DIV>(st, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu, m.logtab, m.skip,
                                                *m.W, lane)
-                    : mm1_warp_rep<INV>(st, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu, m.logtab, m.skip, *m.W, lane);
+                    : mm1_warp_rep<DIV>(st, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu, m.logtab, m.skip, *m.W, lane);
             const double avg = __ddiv_rn(acc, static_cast<double>(a.n));  // lanes 0/1/2: wait/sys/idle
             const double v0 = __shfl_sync(kFull, avg, 2);
             const double v1 = __shfl_sync(kFull, avg, 0);
@@ -917,7 +931,7 @@ struct TlpMm1Warp {
     double res[32 * kExpoB];
 };
 
-template <bool INV, bool FULL, bool COUNT = false>
+template <int DIV, bool FULL, bool COUNT = false>
 __device__ __forceinline__ Queue mm1_thread_rep(Taus st, int64_t n, int64_t n_warp, double lambda, double mu,
                                                 double inv_l, double inv_m, const double* logtab, TlpMm1Warp& W,
                                                 unsigned mask, int lane, bool live = true,
@@ -936,7 +950,7 @@ __device__ __forceinline__ Queue mm1_thread_rep(Taus st, int64_t n, int64_t n_wa
         for (int c = 0; c < kExpoB / 2; ++c)
             if (c < cnt) {
                 const bool dry =
-                    q.client(scale<INV>(e[2 * c], lambda, inv_l), scale<INV>(e[2 * c + 1], mu, inv_m));
+                    q.client(scale<DIV>(e[2 * c], lambda, inv_l), scale<DIV>(e[2 * c + 1], mu, inv_m));
                 if (COUNT && act) split_if(act, dry, *events, mask);  // models.cpp:199-201's if
             }
     }
@@ -954,7 +968,7 @@ __device__ __forceinline__ Queue mm1_thread_rep(Taus st, int64_t n, int64_t n_wa
 // EXACT = false: every lane whose hand-over state matters (lanes 0-30) has whole batches
 // (31*K <= n and K % 4 == 0), so draws need no predication (lane 31, and lanes between
 // replications, may overdraw: their stream state is never handed over).
-template <bool INV, bool EXACT>
+template <int DIV, bool EXACT>
 __device__ __forceinline__ void mm1_segment(Taus& st, Queue& q, uint32_t units, uint32_t units_max, double lambda,
                                             double mu, double inv_l, double inv_m, const double* logtab,
                                             TlpMm1Warp& W, int lane) {
@@ -972,7 +986,7 @@ __device__ __forceinline__ void mm1_segment(Taus& st, Queue& q, uint32_t units, 
         neg_log1m_batch<kExpoB, true>(d, e, logtab, W.nl, W.res, kFull, lane);
 #pragma unroll
         for (int c = 0; c < kExpoB / 2; ++c)
-            if (c < cnt) q.client(scale<INV>(e[2 * c], lambda, inv_l), scale<INV>(e[2 * c + 1], mu, inv_m));
+            if (c < cnt) q.client(scale<DIV>(e[2 * c], lambda, inv_l), scale<DIV>(e[2 * c + 1], mu, inv_m));
     }
 }
 
@@ -982,7 +996,7 @@ struct Mm1PipeWarp {
     double sums[32][3];  // idle, sumw, sums
 };
 
-template <bool INV, bool EXACT>
+template <int DIV, bool EXACT>
 __global__ void __launch_bounds__(kMm1Block, 3) k_wlp_mm1_pipe(RepArgs a, int64_t K) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double* logtab = reinterpret_cast<double*>(smraw);
@@ -1029,7 +1043,7 @@ __global__ void __launch_bounds__(kMm1Block, 3) k_wlp_mm1_pipe(RepArgs a, int64_
         }
         if (more) ++cur;
         if (!__any_sync(kFull, rep >= 0)) break;
-        mm1_segment<INV, EXACT>(st, q, rep >= 0 ? seg : 0u, seg_max, a.lambda, a.mu, a.inv_lambda, a.inv_mu, logtab,
+        mm1_segment<DIV, EXACT>(st, q, rep >= 0 ? seg : 0u, seg_max, a.lambda, a.mu, a.inv_lambda, a.inv_mu, logtab,
                                 P.tw, lane);
         if (__shfl_sync(kFull, rep, 31) >= 0) {  // lane 31 finished a replication
             if (lane == 31) {
@@ -1062,7 +1076,7 @@ __device__ __forceinline__ unsigned block_lane_mask() {  // partial last warp of
     return in_warp >= 32 ? kFull : ((1u << in_warp) - 1u);
 }
 
-template <bool INV, bool COUNT>
+template <int DIV, bool COUNT>
 __global__ void k_tlp_mm1(RepArgs a) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double* logtab = reinterpret_cast<double*>(smraw);
@@ -1076,9 +1090,9 @@ __global__ void k_tlp_mm1(RepArgs a) {
     const unsigned mask = block_lane_mask();
     unsigned events = 0;
     const Queue q = mask == kFull
-                        ? mm1_thread_rep<INV, true, COUNT>(st, a.n, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu,
+                        ? mm1_thread_rep<DIV, true, COUNT>(st, a.n, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu,
                                                            logtab, W, mask, lane, live, &events)
-                        : mm1_thread_rep<INV, false, COUNT>(st, a.n, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu,
+                        : mm1_thread_rep<DIV, false, COUNT>(st, a.n, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu,
                                                             logtab, W, mask, lane, live, &events);
     if (COUNT) {
         HwTally hw;
@@ -1162,18 +1176,17 @@ __global__ void __launch_bounds__(kMm1Block) k_plan_mm1(PlanArgs a, const uint32
     for (int64_t r = next_rep(a, lane); r < a.count; r = next_rep(a, lane)) {
         const SetParam S = a.sets[find_set(a.sets, a.n_sets, r)];
         const Taus st = lane_jump(m.tab, lane, plan_seed(a, r));
-        const bool inv = S.inv_lambda != 0.0 && S.inv_mu != 0.0;
-        double acc;
-        if (S.lambda >= a.serial_rho * S.mu)  // heavy traffic: ordered loop on lane 0
-            acc = inv ? mm1_warp_rep_serial<true>(st, S.n, S.lambda, S.mu, S.inv_lambda, S.inv_mu, m.logtab, m.skip,
-                                                  *m.W, lane)
-                      : mm1_warp_rep_serial<false>(st, S.n, S.lambda, S.mu, S.inv_lambda, S.inv_mu, m.logtab,
-                                                   m.skip, *m.W, lane);
-        else
-            acc = inv ? mm1_warp_rep<true>(st, S.n, S.lambda, S.mu, S.inv_lambda, S.inv_mu, m.logtab, m.skip, *m.W,
-                                           lane)
-                      : mm1_warp_rep<false>(st, S.n, S.lambda, S.mu, S.inv_lambda, S.inv_mu, m.logtab, m.skip,
-                                            *m.W, lane);
+        auto rep = [&](auto div) {
+            constexpr int D = decltype(div)::value;
+            return S.lambda >= a.serial_rho * S.mu  // heavy traffic: ordered loop on lane 0
+                       ? mm1_warp_rep_serial<D>(st, S.n, S.lambda, S.mu, S.inv_lambda, S.inv_mu, m.logtab, m.skip,
+                                                *m.W, lane)
+                       : mm1_warp_rep<D>(st, S.n, S.lambda, S.mu, S.inv_lambda, S.inv_mu, m.logtab, m.skip, *m.W,
+                                         lane);
+        };
+        const double acc = S.div == kDivPow2  ? rep(std::integral_constant<int, kDivPow2>{})
+                           : S.div == kDivRcp ? rep(std::integral_constant<int, kDivRcp>{})
+                                              : rep(std::integral_constant<int, kDivIeee>{});
         if (lane < 3) {  // lanes 0/1/2 hold sumw/sums/idle
             double* out = lane == 0 ? a.out1 : (lane == 1 ? a.out2 : a.out0);
             out[r] = __ddiv_rn(acc, static_cast<double>(S.n));
@@ -1204,10 +1217,17 @@ __global__ void k_plan_tlp_mm1(PlanArgs a) {
     const int64_t n = live ? S.n : 0;
     const int64_t n_warp = static_cast<int64_t>(__reduce_max_sync(mask, static_cast<unsigned>(n)));
     const Taus st = live ? plan_seed(a, r) : Taus{2u, 8u, 16u};
-    // per-lane rates differ across sets: always divide unless the lane's rates are 2^k
-    const Queue q = mask == kFull
-                        ? mm1_thread_rep<false, true>(st, n, n_warp, S.lambda, S.mu, 0.0, 0.0, logtab, W, mask, lane)
-                        : mm1_thread_rep<false, false>(st, n, n_warp, S.lambda, S.mu, 0.0, 0.0, logtab, W, mask, lane);
+    // lanes of one warp may belong to different sets: the reciprocal form takes per-lane
+    // rates (an exact 2^-k reciprocal included); IEEE division when any set needs it
+    auto rep = [&](auto div) {
+        constexpr int D = decltype(div)::value;
+        return mask == kFull ? mm1_thread_rep<D, true>(st, n, n_warp, S.lambda, S.mu, S.inv_lambda, S.inv_mu, logtab,
+                                                       W, mask, lane)
+                             : mm1_thread_rep<D, false>(st, n, n_warp, S.lambda, S.mu, S.inv_lambda, S.inv_mu, logtab,
+                                                        W, mask, lane);
+    };
+    const Queue q = a.tlp_div == kDivRcp ? rep(std::integral_constant<int, kDivRcp>{})
+                                         : rep(std::integral_constant<int, kDivIeee>{});
     if (!live) return;
     const double nd = static_cast<double>(S.n);
     a.out0[r] = __ddiv_rn(q.idle, nd);
@@ -1294,11 +1314,13 @@ void allow_smem(K kernel, size_t bytes) {
 int wlp_blocks_per_sm(int model) {
     int nb = 0;
     if (model == 1) {
-        allow_smem(k_wlp_mm1<false, false>, kMm1Smem);
-        allow_smem(k_wlp_mm1<true, false>, kMm1Smem);
-        allow_smem(k_wlp_mm1<false, true>, kMm1Smem);
-        allow_smem(k_wlp_mm1<true, true>, kMm1Smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_mm1<false, false>, kMm1Block, kMm1Smem);
+        allow_smem(k_wlp_mm1<kDivIeee, false>, kMm1Smem);
+        allow_smem(k_wlp_mm1<kDivIeee, true>, kMm1Smem);
+        allow_smem(k_wlp_mm1<kDivPow2, false>, kMm1Smem);
+        allow_smem(k_wlp_mm1<kDivPow2, true>, kMm1Smem);
+        allow_smem(k_wlp_mm1<kDivRcp, false>, kMm1Smem);
+        allow_smem(k_wlp_mm1<kDivRcp, true>, kMm1Smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_mm1<kDivIeee, false>, kMm1Block, kMm1Smem);
     } else {
         const size_t smem = kLaneTabWords * 4;
         allow_smem(k_wlp_lanes<0, false>, smem);
@@ -1319,8 +1341,8 @@ int tlp_blocks_per_sm(int model, int block) {
         case 0: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tlp<0, false>, block, 0); break;
         case 1: {
             const size_t smem = tlp_mm1_smem(block);
-            allow_smem(k_tlp_mm1<false, false>, smem);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tlp_mm1<false, false>, block, smem);
+            allow_smem(k_tlp_mm1<kDivIeee, false>, smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tlp_mm1<kDivIeee, false>, block, smem);
             break;
         }
         default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tlp<2, false>, block, 0); break;
@@ -1357,16 +1379,27 @@ cudaError_t launch_taus_stream(const uint32_t* powers, Taus seed, int64_t n, uin
     return cudaGetLastError();
 }
 
+// Calls f(std::integral_constant<int, div>) for a RepArgs::div value.
+template <class F>
+void by_div(int div, F&& f) {
+    if (div == kDivPow2)
+        f(std::integral_constant<int, kDivPow2>{});
+    else if (div == kDivRcp)
+        f(std::integral_constant<int, kDivRcp>{});
+    else
+        f(std::integral_constant<int, kDivIeee>{});
+}
+
 cudaError_t launch_wlp(int model, const RepArgs& a, const uint32_t* lane_tab, const uint32_t* uni_tab,
                        int64_t lane_units, int grid, cudaStream_t st) {
     if (a.count <= 0) return cudaSuccess;
     const bool count = a.hw != nullptr;
     if (model == 1) {
         auto go = [&](auto kernel) { kernel<<<grid, kMm1Block, kMm1Smem, st>>>(a, lane_tab, uni_tab); };
-        if (a.inv_lambda != 0.0 && a.inv_mu != 0.0)
-            count ? go(k_wlp_mm1<true, true>) : go(k_wlp_mm1<true, false>);
-        else
-            count ? go(k_wlp_mm1<false, true>) : go(k_wlp_mm1<false, false>);
+        by_div(a.div, [&](auto d) {
+            constexpr int D = decltype(d)::value;
+            count ? go(k_wlp_mm1<D, true>) : go(k_wlp_mm1<D, false>);
+        });
     } else {
         auto go = [&](auto kernel) { kernel<<<grid, kWlpBlock, kLaneTabWords * 4, st>>>(a, lane_tab, lane_units); };
         if (model == 0)
@@ -1394,20 +1427,22 @@ cudaError_t launch_wlp_mm1_pipe(const RepArgs& a, int64_t lane_units, int grid, 
     if (a.count <= 0) return cudaSuccess;
     const bool exact = 31 * lane_units > a.n || lane_units % (kExpoB / 2) != 0;
     auto go = [&](auto kernel) { kernel<<<grid, kMm1Block, kMm1PipeSmem, st>>>(a, lane_units); };
-    if (a.inv_lambda != 0.0 && a.inv_mu != 0.0)
-        exact ? go(k_wlp_mm1_pipe<true, true>) : go(k_wlp_mm1_pipe<true, false>);
-    else
-        exact ? go(k_wlp_mm1_pipe<false, true>) : go(k_wlp_mm1_pipe<false, false>);
+    by_div(a.div, [&](auto d) {
+        constexpr int D = decltype(d)::value;
+        exact ? go(k_wlp_mm1_pipe<D, true>) : go(k_wlp_mm1_pipe<D, false>);
+    });
     return cudaGetLastError();
 }
 
 int wlp_mm1_pipe_blocks_per_sm() {
     int nb = 0;
-    allow_smem(k_wlp_mm1_pipe<true, true>, kMm1PipeSmem);
-    allow_smem(k_wlp_mm1_pipe<false, true>, kMm1PipeSmem);
-    allow_smem(k_wlp_mm1_pipe<true, false>, kMm1PipeSmem);
-    allow_smem(k_wlp_mm1_pipe<false, false>, kMm1PipeSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_mm1_pipe<false, true>, kMm1Block, kMm1PipeSmem);
+    allow_smem(k_wlp_mm1_pipe<kDivIeee, true>, kMm1PipeSmem);
+    allow_smem(k_wlp_mm1_pipe<kDivIeee, false>, kMm1PipeSmem);
+    allow_smem(k_wlp_mm1_pipe<kDivPow2, true>, kMm1PipeSmem);
+    allow_smem(k_wlp_mm1_pipe<kDivPow2, false>, kMm1PipeSmem);
+    allow_smem(k_wlp_mm1_pipe<kDivRcp, true>, kMm1PipeSmem);
+    allow_smem(k_wlp_mm1_pipe<kDivRcp, false>, kMm1PipeSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_mm1_pipe<kDivIeee, true>, kMm1Block, kMm1PipeSmem);
     return nb < 1 ? 1 : nb;
 }
 
@@ -1421,7 +1456,6 @@ cudaError_t launch_tlp(int model, const RepArgs& a, int tlp_block, cudaStream_t 
     if (a.count <= 0) return cudaSuccess;
     const int64_t block = a.count < tlp_block ? a.count : tlp_block;
     const int64_t grid = (a.count + block - 1) / block;
-    const bool inv = a.inv_lambda != 0.0 && a.inv_mu != 0.0;
     const dim3 g(static_cast<unsigned>(grid)), b(static_cast<unsigned>(block));
     const bool count = a.hw != nullptr;
     switch (model) {
@@ -1437,10 +1471,10 @@ cudaError_t launch_tlp(int model, const RepArgs& a, int tlp_block, cudaStream_t 
                 allow_smem(kernel, smem);
                 kernel<<<g, b, smem, st>>>(a);
             };
-            if (inv)
-                count ? go(k_tlp_mm1<true, true>) : go(k_tlp_mm1<true, false>);
-            else
-                count ? go(k_tlp_mm1<false, true>) : go(k_tlp_mm1<false, false>);
+            by_div(a.div, [&](auto d) {
+                constexpr int D = decltype(d)::value;
+                count ? go(k_tlp_mm1<D, true>) : go(k_tlp_mm1<D, false>);
+            });
             break;
         }
         default:

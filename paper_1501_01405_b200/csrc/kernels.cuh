@@ -8,6 +8,11 @@
 
 namespace wlp {
 
+// How the mm1 kernels divide a log by a rate (models.hpp:67,75); all three give IEEE
+// e / rate bit for bit (kernels.cu scale()). kDivPow2: rate = 2^k, inv = 1/rate exactly;
+// kDivRcp: inv = RN(1/rate), rate in [2^-900, 2^900]; kDivIeee: anything else.
+enum : int { kDivIeee = 0, kDivPow2 = 1, kDivRcp = 2 };
+
 // Replication-kernel arguments shared by every model/mapping.
 struct RepArgs {
     const uint32_t* seeds;  // SoA: s1[count], s2[count], s3[count]
@@ -15,7 +20,8 @@ struct RepArgs {
     int64_t n;              // units per replication (draws / clients / steps)
     int64_t chunks;         // walk
     double lambda, mu;      // mm1 rates
-    double inv_lambda, inv_mu;  // exact reciprocals when the rate is a power of two, else 0
+    double inv_lambda, inv_mu;  // reciprocals for `div` (0 under kDivIeee)
+    int div = kDivIeee;
     double* out0;
     double* out1;
     double* out2;
@@ -59,6 +65,7 @@ struct SetParam {
     int64_t n;       // units per replication
     int64_t chunks;  // walk
     double lambda, mu, inv_lambda, inv_mu;
+    int div;
 };
 
 struct PlanArgs {
@@ -71,6 +78,7 @@ struct PlanArgs {
     double* out2;
     unsigned long long* next;  // dynamic work counter (zeroed before launch)
     double serial_rho = 2.0;   // as RepArgs::serial_rho, per set
+    int tlp_div = kDivIeee;    // TLP plan: kDivRcp when every set allows it
 };
 
 // Batched seeding of many independent random_spacing runs (one per set).

@@ -201,6 +201,20 @@ double exact_reciprocal(double rate) {
     return std::ldexp(1.0, 1 - e);
 }
 
+// The mm1 division mode for a pair of rates (kernels.cuh kDiv*) and the reciprocals it
+// uses: exact ones for powers of two, RN(1/rate) inside [2^-900, 2^900].
+struct DivMode {
+    int div;
+    double inv_lambda, inv_mu;
+};
+DivMode div_mode(double lambda, double mu) {
+    const double el = exact_reciprocal(lambda), em = exact_reciprocal(mu);
+    if (el != 0.0 && em != 0.0) return {kDivPow2, el, em};
+    auto ok = [](double r) { return r >= 0x1p-900 && r <= 0x1p900; };
+    if (ok(lambda) && ok(mu)) return {kDivRcp, 1.0 / lambda, 1.0 / mu};
+    return {kDivIeee, 0.0, 0.0};
+}
+
 int lane_table(DevCtx& c, uint64_t stride, const uint32_t*& out) {
     auto it = c.lane_tabs.find(stride);
     if (it == c.lane_tabs.end()) {
@@ -417,8 +431,14 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
     a.chunks = p.chunks;
     a.lambda = p.lambda;
     a.mu = p.mu;
-    a.inv_lambda = model == WLP_MODEL_MM1 ? exact_reciprocal(p.lambda) : 0.0;
-    a.inv_mu = model == WLP_MODEL_MM1 ? exact_reciprocal(p.mu) : 0.0;
+    if (model == WLP_MODEL_MM1) {
+        const DivMode d = div_mode(p.lambda, p.mu);
+        a.div = d.div;
+        a.inv_lambda = d.inv_lambda;
+        a.inv_mu = d.inv_mu;
+    } else {
+        a.inv_lambda = a.inv_mu = 0.0;
+    }
     a.out0 = o0;
     a.out1 = o1;
     a.out2 = o2;
@@ -949,14 +969,15 @@ int wlp_run_plan(int model, const wlp_params* sets, const uint64_t* master_seeds
     std::vector<SetParam> sp(n_sets);
     std::vector<SeedJob> jobs(n_sets);
     int64_t R = 0, blocks = 0;
+    bool all_rcp = true;
     const int64_t per_block = static_cast<int64_t>(kSeedBlock) * kSeedPerThread;
     for (int k = 0; k < n_sets; ++k) {
         WLP_TRY(validate(model, &sets[k], nullptr));
         const int64_t n = units_of(model, sets[k]);
         if (n > 0xFFFFFFFFll) return fail(WLP_EPLAN, "plan: units per replication must be < 2^32");
-        sp[k] = SetParam{R, n, sets[k].chunks, sets[k].lambda, sets[k].mu,
-                         model == WLP_MODEL_MM1 ? exact_reciprocal(sets[k].lambda) : 0.0,
-                         model == WLP_MODEL_MM1 ? exact_reciprocal(sets[k].mu) : 0.0};
+        const DivMode d = model == WLP_MODEL_MM1 ? div_mode(sets[k].lambda, sets[k].mu) : DivMode{kDivIeee, 0.0, 0.0};
+        sp[k] = SetParam{R, n, sets[k].chunks, sets[k].lambda, sets[k].mu, d.inv_lambda, d.inv_mu, d.div};
+        all_rcp = all_rcp && d.div != kDivIeee;
         jobs[k] = SeedJob{master_from_seed(master_seeds[k]), 0u, sets[k].replications, R, blocks};
         R += sets[k].replications;
         blocks += (sets[k].replications + per_block - 1) / per_block;
@@ -986,6 +1007,7 @@ int wlp_run_plan(int model, const wlp_params* sets, const uint64_t* master_seeds
                               c->counter.p, st));
     PlanArgs pa;
     pa.serial_rho = mm1_serial_rho();
+    pa.tlp_div = all_rcp ? kDivRcp : kDivIeee;
     pa.seeds = c->seeds.p;
     pa.count = R;
     pa.sets = c->setp.p;

@@ -121,6 +121,22 @@ def test_mm1_wlp_segment_chaining_all_loads(gpu, port, lam, mu, clients):
         assert np.array_equal(run.outputs[name], want[name]), name
 
 
+@pytest.mark.parametrize("lam,mu", [(float.fromhex("0x1.fffffffffffffp-1"), float.fromhex("0x1.0000000000001p0")),
+                                    (0.1, 1e-3), (1.3e-290, 1.7e-290), (0.3, 1e300), (2.0**-950, 2.0**-949),
+                                    (3.0, 7.0)])
+def test_mm1_rate_division_modes_all_mappings(gpu, port, lam, mu):
+    # -log(1-u)/rate is a multiply for 2^k rates, a reciprocal + Markstein correction inside
+    # [2^-900, 2^900] (tools/div_check.cu) and IEEE division outside: same bits either way
+    p = gpu.ModelParams(replications=70, clients=300, lambda_=lam, mu=mu)
+    want = port.run_model(1, oracle.params_from(p), 99)
+    for mode in (gpu.ExecutionMode.Tlp, gpu.ExecutionMode.Wlp):
+        for variant in (0, 1, 2):
+            with gpu.wlp_variant(variant):
+                run = gpu.run_model(gpu.ModelKind.Mm1, p, mode, master_seed=99)
+            for name in oracle.OUTPUTS[1]:
+                assert np.array_equal(run.outputs[name], want[name]), (mode, variant, name)
+
+
 def test_run_streams_pi_mm1_walk_replication(gpu, port):
     keys = port.random_spacing(3, 50)
     st = gpu.RngState(*[int(x) for x in keys[:, 7]])

@@ -34,6 +34,16 @@ def test_plan_heterogeneous_trip_counts(gpu, port):
     _check_plan(gpu, port, gpu.ModelKind.Mm1, mm1_sets, [99 + k for k in range(12)])
 
 
+def test_plan_mm1_mixed_division_modes(gpu, port):
+    # sets whose rates take the 2^k multiply, the reciprocal form and IEEE division in one
+    # launch (the TLP plan falls back to division for every lane when any set needs it)
+    rates = [(0.5, 1.0), (0.3, 0.9), (0.25, 2.0), (1.3e-290, 1.7e-290), (0.7, 0.75), (4.0, 3.0)]
+    for pick in (rates, [r for r in rates if r[0] > 1e-100]):
+        sets = [gpu.ModelParams(replications=7 + k, clients=200 + 31 * k, lambda_=lam, mu=mu)
+                for k, (lam, mu) in enumerate(pick)]
+        _check_plan(gpu, port, gpu.ModelKind.Mm1, sets, [5 + k for k in range(len(pick))])
+
+
 def test_plan_errors(gpu):
     with pytest.raises(gpu.DomainError):
         gpu.run_plan(gpu.ModelKind.Pi, [gpu.ModelParams(draws=0)], [1], gpu.ExecutionMode.Wlp)
