@@ -381,8 +381,10 @@ def main():
     units = R_PER_GPU * DRAWS
     achieved = units * INSTR_PER_UNIT[0] / 32 / (kernel_avg * 1e-3) / 1e9  # G warp-instr/s
     peak = 4 * sms * fmax * 1e6 / 1e9
-    nc_all = ncu_traffic().get("k_wlp_lanes<0>", {})
-    nc = nc_all[sorted(nc_all)[-1]] if nc_all else {}  # latest committed capture
+    # latest committed capture of this kernel at this workload (the capture names end in R)
+    caps = {k: v for name in ("k_wlp_lanes<0>", "k_wlp_lanes<0, 0>")
+            for k, v in ncu_traffic().get(name, {}).items() if k.endswith(f"_{R_PER_GPU}")}
+    nc = caps[sorted(caps)[-1]] if caps else {}
     roofline = {"bound": "issue", "kernel": "k_wlp_lanes<0> (pi WLP)", "achieved": achieved, "peak": peak,
                 "unit": "Gwarp-inst/s", "frac": achieved / peak, "traffic": nc.get("dram_bytes_per_launch"),
                 "algorithmic": f"{INSTR_PER_UNIT[0]} lane-instr/point x {units:.0e} points per launch / 32",
