@@ -231,13 +231,15 @@ __device__ __forceinline__ void neg_log1m_batch(const uint32_t (&n)[B], double (
     static_assert(B <= 32, "near flags fit one word");
     const unsigned mask = FULL ? kFull : mask_;
     unsigned near = 0;
+    bool nr[B];
 #pragma unroll
     for (int j = 0; j < B; ++j) {
         // 1 - u >= 1 - 2^-4 (glibc's near-one window) exactly when n <= 2^28; n = 0 (1 - u
         // = 1) is near too, so the table path may see the wrapped x = 0 there: its value is
         // replaced below
         e[j] = -log_table_dev(one_minus_u32_nz(n[j]), tab);
-        if (n[j] <= 0x10000000u) near |= 1u << j;
+        nr[j] = n[j] <= 0x10000000u;
+        if (nr[j]) near |= 1u << j;
     }
     const int c = __popc(near);
     int incl = c;
@@ -249,20 +251,30 @@ __device__ __forceinline__ void neg_log1m_batch(const uint32_t (&n)[B], double (
     const int width = FULL ? 32 : __popc(mask);
     const int total = __shfl_sync(mask, incl, width - 1);
     if (total == 0) return;  // warp-uniform
-    int pos = incl - c;
+    // predicated store then pointer bump, in this order (as C++ the compiler bumps into a
+    // temporary first and copies it back: one instruction more per input)
+    uint32_t sp = static_cast<uint32_t>(__cvta_generic_to_shared(nl.n + (incl - c)));
 #pragma unroll
     for (int j = 0; j < B; ++j)
-        if (near >> j & 1u) nl.n[pos++] = n[j];
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.shared.u32 [%0], %1;\n\t"
+                     "@p add.u32 %0, %0, 4;\n\t}"
+                     : "+r"(sp)
+                     : "r"(n[j]), "r"(static_cast<uint32_t>(nr[j]))
+                     : "memory");
     __syncwarp(mask);
     for (int p = lane; p < total; p += width) {
         const uint32_t v = nl.n[p];
         res[p] = v == 0u ? -0.0 : -log_near_one(one_minus_u32_dev(v));
     }
     __syncwarp(mask);
-    pos = incl - c;
+    uint32_t rp = static_cast<uint32_t>(__cvta_generic_to_shared(res + (incl - c)));
 #pragma unroll
     for (int j = 0; j < B; ++j)
-        if (near >> j & 1u) e[j] = res[pos++];
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.shared.f64 %1, [%0];\n\t"
+                     "@p add.u32 %0, %0, 8;\n\t}"
+                     : "+r"(rp), "+d"(e[j])
+                     : "r"(static_cast<uint32_t>(nr[j]))
+                     : "memory");
     __syncwarp(mask);
 }
 
