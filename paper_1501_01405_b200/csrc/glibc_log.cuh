@@ -183,6 +183,35 @@ __device__ __forceinline__ double log_table_dev(double x, const double* tab) {
     const double y = __fma_rn(__dmul_rn(r, r2), q, __fma_rn(r2, A[0], lo));
     return __dadd_rn(y, hi);
 }
+
+// -log(1 - n*2^-32) on the table path (n > 2^28; for n = 0 the value is garbage and the
+// caller replaces it), the form the mm1 kernels use. Same arithmetic as
+// -log_table_dev(one_minus_u32_nz(n)) with two instructions fewer:
+// * x = m*2^-32 for m = 2^32 - n, and m converts to double exactly (I2F, off the FP64
+//   pipe), so hi(x) = hi(m) - (32 << 20): thi is the same value against a shifted OFF, and
+//   z's high word takes the shift in the same integer subtraction;
+// * the result is negated in the final add (-(y + hi) == (-y) + (-hi) in round-to-nearest;
+//   y + hi is never an exact zero here since x != 1).
+// tools/log_check.cu compares it with the two-step form for every n.
+__device__ __forceinline__ double neg_log1m_table_dev(uint32_t n, const double* tab) {
+    const double dm = __uint2double_rn(0u - n);
+    const uint32_t hm = static_cast<uint32_t>(__double2hiint(dm));
+    const uint32_t thi = hm - (0x3fe60000u + (32u << 20));  // == hi(x) - hi(OFF)
+    const int i = static_cast<int>((thi >> 13) & 127u);
+    const int k = static_cast<int>(thi) >> 20;
+    const double z = __hiloint2double(static_cast<int>(hm - (thi & 0xfff00000u) - (32u << 20)), __double2loint(dm));
+    const double2 c = reinterpret_cast<const double2*>(tab)[i];  // {invc, logc}
+    const double kd = static_cast<double>(k);
+    constexpr double A[5] = WLP_LOG_POLY_INIT;
+    const double r = __fma_rn(z, c.x, -1.0);
+    const double w = __fma_rn(kd, WLP_LOG_LN2HI, c.y);
+    const double hi = __dadd_rn(r, w);
+    const double lo = __fma_rn(kd, WLP_LOG_LN2LO, __dadd_rn(__dsub_rn(w, hi), r));
+    const double r2 = __dmul_rn(r, r);
+    const double q = __fma_rn(__fma_rn(r, A[4], A[3]), r2, __fma_rn(r, A[2], A[1]));
+    const double y = __fma_rn(__dmul_rn(r, r2), q, __fma_rn(r2, A[0], lo));
+    return __dadd_rn(-y, -hi);
+}
 #endif
 
 // -log(1 - n*2^-32) for a taus88 output n: the exponential numerator of mm1

@@ -237,7 +237,7 @@ __device__ __forceinline__ void neg_log1m_batch(const uint32_t (&n)[B], double (
         // 1 - u >= 1 - 2^-4 (glibc's near-one window) exactly when n <= 2^28; n = 0 (1 - u
         // = 1) is near too, so the table path may see the wrapped x = 0 there: its value is
         // replaced below
-        e[j] = -log_table_dev(one_minus_u32_nz(n[j]), tab);
+        e[j] = neg_log1m_table_dev(n[j], tab);
         nr[j] = n[j] <= 0x10000000u;
         if (nr[j]) near |= 1u << j;
     }
