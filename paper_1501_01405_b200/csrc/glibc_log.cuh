@@ -91,6 +91,32 @@ WLP_HD double log_near_one(double x) {
     return WLP_ADD(hi, WLP_FMA(p, r3, lo));
 }
 
+#if defined(__CUDACC__)
+__constant__ double kLogPoly1Dev[11] = WLP_LOG_POLY1_INIT;
+
+// log_near_one on the device with the coefficients as constant-bank operands of the
+// DFMAs: from a constexpr array they are rebuilt in uniform registers on every call inside
+// the mm1 batch loop (26 moves per batch). Same operations in the same order.
+__device__ __forceinline__ double log_near_one_dev(double x) {
+    const double* B = kLogPoly1Dev;
+    const double r = __dsub_rn(x, 1.0);
+    const double r2 = __dmul_rn(r, r);
+    const double r3 = __dmul_rn(r, r2);
+    const double ta = __fma_rn(r2, B[3], __fma_rn(r, B[2], B[1]));
+    const double tb = __fma_rn(r2, B[6], __fma_rn(r, B[5], B[4]));
+    const double tc = __fma_rn(r3, B[10], __fma_rn(r2, B[9], __fma_rn(r, B[8], B[7])));
+    const double p = __fma_rn(__fma_rn(tc, r3, tb), r3, ta);
+    const double rw = __fma_rn(r, 0x1p27, r);
+    const double rhi = __fma_rn(-0x1p27, r, rw);
+    const double rhi2 = __dmul_rn(rhi, rhi);
+    const double rlo = __dsub_rn(r, rhi);
+    const double hi = __fma_rn(rhi2, B[0], r);
+    double lo = __fma_rn(rhi2, B[0], __dsub_rn(r, hi));
+    lo = __fma_rn(__dmul_rn(B[0], rlo), __dadd_rn(r, rhi), lo);
+    return __dadd_rn(hi, __fma_rn(p, r3, lo));
+}
+#endif
+
 // log(x) for positive normal x outside the near-one window: x = 2^k * z, z in
 // [OFF, 2*OFF); log x = k*ln2 + log(c) + log1p(z/c - 1), c from the 128-entry table
 // `tab` = {invc, logc} pairs.

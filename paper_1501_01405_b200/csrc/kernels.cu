@@ -264,7 +264,7 @@ __device__ __forceinline__ void neg_log1m_batch(const uint32_t (&n)[B], double (
     __syncwarp(mask);
     for (int p = lane; p < total; p += width) {
         const uint32_t v = nl.n[p];
-        res[p] = v == 0u ? -0.0 : -log_near_one(one_minus_u32_dev(v));
+        res[p] = v == 0u ? -0.0 : -log_near_one_dev(one_minus_u32_dev(v));
     }
     __syncwarp(mask);
     uint32_t rp = static_cast<uint32_t>(__cvta_generic_to_shared(res + (incl - c)));
