@@ -115,27 +115,32 @@ __device__ __forceinline__ void flush_tally(const HwTally& h, unsigned long long
 // evaluated on the unscaled draws: with x = a*2^-32 every product and sum is the
 // reference's value times 2^64 exactly (power-of-two scaling commutes with rounding
 // in the normal range), so the test is fl(fl(a*a) + fl(b*b)) <= 2^64.
-__device__ __forceinline__ bool pi_inside(uint32_t a, uint32_t b) {
+// hits += inside as one compare and one predicated add (from C++ the compiler adds
+// unconditionally and then undoes the add under the opposite predicate).
+__device__ __forceinline__ void pi_count(uint32_t& hits, uint32_t a, uint32_t b) {
     const double x = __uint2double_rn(a), y = __uint2double_rn(b);
-    return __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)) <= 0x1p64;
+    const double s = __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y));
+    asm("{\n\t.reg .pred p;\n\tsetp.le.f64 p, %1, 0d43F0000000000000;\n\t@p add.u32 %0, %0, 1;\n\t}"
+        : "+r"(hits)
+        : "d"(s));
 }
 
 
-// Hits among `units` consecutive points of a stream (main loop unrolled by 4).
+// Hits among `units` consecutive points of a stream (main loop unrolled by 8).
 __device__ __forceinline__ uint32_t pi_hits(Taus& st, uint32_t units) {
     uint32_t hits = 0, u = 0;
-    for (; u + 4 <= units; u += 4) {
+    for (; u + 8 <= units; u += 8) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < 8; ++k) {
             uint32_t x, y;
             taus_next2(st, x, y);
-            if (pi_inside(x, y)) ++hits;
+            pi_count(hits, x, y);
         }
     }
     for (; u < units; ++u) {
         uint32_t x, y;
         taus_next2(st, x, y);
-        if (pi_inside(x, y)) ++hits;
+        pi_count(hits, x, y);
     }
     return hits;
 }
