@@ -128,6 +128,12 @@ int wlp_set_hw_counters(int enable);
  * (DESIGN.md §4). */
 int wlp_set_wlp_variant(int variant);
 
+/* The same for the TLP (thread-level) mapping: 0 = automatic (default: one thread per
+ * replication, the paper's comparison mapping); 1 = one thread per replication; 2 = walk
+ * bitsliced, one thread per 32 replications, each state bit of the 32 streams in one
+ * word (pi / mm1 keep the per-replication kernel). Outputs are identical. */
+int wlp_set_tlp_variant(int variant);
+
 /* validate_params (models.cpp:26-44): WLP_EDOMAIN on invalid values; a non-empty
  * warning (lambda >= mu) is copied into warn[cap]. */
 int wlp_validate_params(int model, const wlp_params* p, char* warn, int warn_cap);

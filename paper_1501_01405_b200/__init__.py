@@ -241,6 +241,7 @@ _SIGS = {
     "wlp_version": (C.c_int, []),
     "wlp_set_hw_counters": (C.c_int, [C.c_int]),
     "wlp_set_wlp_variant": (C.c_int, [C.c_int]),
+    "wlp_set_tlp_variant": (C.c_int, [C.c_int]),
     "wlp_validate_params": (C.c_int, [C.c_int, C.POINTER(_Params), C.c_char_p, C.c_int]),
     "wlp_plan_launch": (C.c_int, [_I64, C.c_int, C.c_int, _I64, C.POINTER(_Cfg), C.c_char_p, C.c_int]),
     "wlp_master_from_seed": (C.c_int, [C.c_uint64, _P]),
@@ -507,6 +508,22 @@ class wlp_variant:
 
     def __exit__(self, *exc):
         _check(_lib.wlp_set_wlp_variant(0))
+
+
+class tlp_variant:
+    """Context manager selecting the TLP kernel for calls on this thread: 0 automatic,
+    1 thread per replication, 2 bitsliced walk (thread per 32 replications; outputs
+    identical; wlp_set_tlp_variant)."""
+
+    def __init__(self, variant: int):
+        self.variant = int(variant)
+
+    def __enter__(self):
+        _check(_lib.wlp_set_tlp_variant(self.variant))
+        return self
+
+    def __exit__(self, *exc):
+        _check(_lib.wlp_set_tlp_variant(0))
 
 
 class hw_counters:

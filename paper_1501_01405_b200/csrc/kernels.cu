@@ -24,6 +24,7 @@
 
 #include <type_traits>
 
+#include "bitslice.cuh"
 #include "glibc_log.cuh"
 #include "jump.hpp"
 #include "kernels.cuh"
@@ -940,6 +941,110 @@ __global__ void k_tlp(RepArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------------
+// Walk, bitsliced thread per 32 replications (TLP variant; bitslice.cuh). Thread t owns
+// replications 32t .. 32t+31: their seeds are transposed into bit planes, every step
+// costs ~33 XORs per draw for all 32, and the +x / -x step masks are counted per stream
+// by a Harley-Seal carry-save tree (16 steps per tree, weight-16 carries rippled into
+// the higher digits). Counts stay exact below 2^16; longer walks flush every 65520 steps
+// into per-stream int32 sums in shared memory. Same draws, same d, same dx as
+// walk_replication: the outputs are the reference's bit for bit.
+// ---------------------------------------------------------------------------------
+constexpr int kBsBlock = 128;
+constexpr int64_t kBsFlushBlocks = 4095;  // 4095 * 16 steps keep every count below 2^16
+
+__device__ __forceinline__ void bs_pair(BsTaus& t, BsCount& P, BsCount& Q, uint32_t& p2, uint32_t& q2) {
+    uint32_t pa, ma, pb, mb;
+    bs_walk_step(t, pa, ma);
+    bs_walk_step(t, pb, mb);
+    bs_csa(p2, P.c[0], P.c[0], pa, pb);
+    bs_csa(q2, Q.c[0], Q.c[0], ma, mb);
+}
+
+__device__ __forceinline__ void bs_quad(BsTaus& t, BsCount& P, BsCount& Q, uint32_t& p4, uint32_t& q4) {
+    uint32_t pa, qa, pb, qb;
+    bs_pair(t, P, Q, pa, qa);
+    bs_pair(t, P, Q, pb, qb);
+    bs_csa(p4, P.c[1], P.c[1], pa, pb);
+    bs_csa(q4, Q.c[1], Q.c[1], qa, qb);
+}
+
+__device__ __forceinline__ void bs_oct(BsTaus& t, BsCount& P, BsCount& Q, uint32_t& p8, uint32_t& q8) {
+    uint32_t pa, qa, pb, qb;
+    bs_quad(t, P, Q, pa, qa);
+    bs_quad(t, P, Q, pb, qb);
+    bs_csa(p8, P.c[2], P.c[2], pa, pb);
+    bs_csa(q8, Q.c[2], Q.c[2], qa, qb);
+}
+
+__device__ __forceinline__ void bs_ripple16(BsCount& k, uint32_t m) {  // add m at weight 16
+#pragma unroll
+    for (int w = 4; w < 16; ++w) {
+        const uint32_t carry = k.c[w] & m;
+        k.c[w] ^= m;
+        m = carry;
+    }
+}
+
+__global__ void __launch_bounds__(kBsBlock) k_tlp_walk_bs(RepArgs a) {
+    extern __shared__ int32_t bs_acc[];  // [kBsBlock][33] when n > 65520 steps
+    const int64_t r0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 32;
+    if (r0 >= a.count) return;
+    BsTaus t;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const Taus st = r0 + j < a.count ? load_seed(a, r0 + j) : Taus{kMin1, kMin2, kMin3};
+        t.b1[j] = st.s1;
+        t.b2[j] = st.s2;
+        t.b3[j] = st.s3;
+    }
+    transpose32(t.b1);
+    transpose32(t.b2);
+    transpose32(t.b3);
+    BsCount P, Q;
+    bs_count_init(P);
+    bs_count_init(Q);
+    const bool flushing = a.n > kBsFlushBlocks * 16;
+    int32_t* acc = bs_acc + threadIdx.x * 33;
+    if (flushing)
+        for (int j = 0; j < 32; ++j) acc[j] = 0;
+    auto flush = [&]() {
+        uint32_t pv[32], qv[32];
+        bs_count_values(P, pv);
+        bs_count_values(Q, qv);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] += static_cast<int32_t>(pv[j]) - static_cast<int32_t>(qv[j]);
+        bs_count_init(P);
+        bs_count_init(Q);
+    };
+    const int64_t blocks = a.n / 16;
+    for (int64_t b = 0; b < blocks; ++b) {
+        uint32_t pa, qa, pb, qb, p16, q16;
+        bs_oct(t, P, Q, pa, qa);
+        bs_oct(t, P, Q, pb, qb);
+        bs_csa(p16, P.c[3], P.c[3], pa, pb);
+        bs_csa(q16, Q.c[3], Q.c[3], qa, qb);
+        bs_ripple16(P, p16);
+        bs_ripple16(Q, q16);
+        if (flushing && (b + 1) % kBsFlushBlocks == 0) flush();
+    }
+    for (int64_t s = blocks * 16; s < a.n; ++s) {
+        uint32_t pl, mi;
+        bs_walk_step(t, pl, mi);
+        bs_count_add1(P, pl);
+        bs_count_add1(Q, mi);
+    }
+    uint32_t pv[32], qv[32];
+    bs_count_values(P, pv);
+    bs_count_values(Q, qv);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        if (r0 + j >= a.count) break;
+        const int64_t dx = static_cast<int64_t>(pv[j]) - static_cast<int64_t>(qv[j]) + (flushing ? acc[j] : 0);
+        a.out0[r0 + j] = walk_fold(dx, a.chunks);
+    }
+}
+
 // mm1 thread per replication: each lane runs its own queue; the exponentials of 4
 // clients (8 draws) per lane go through the warp-cooperative batch log. Every thread of
 // a warp takes part in each batch up to the warp's longest replication (`n_warp`).
@@ -1501,6 +1606,15 @@ cudaError_t launch_tlp(int model, const RepArgs& a, int tlp_block, cudaStream_t 
                 k_tlp<2, false><<<g, b, 0, st>>>(a);
             break;
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tlp_walk_bs(const RepArgs& a, cudaStream_t st) {
+    if (a.count <= 0) return cudaSuccess;
+    const int64_t threads = (a.count + 31) / 32;
+    const int64_t grid = (threads + kBsBlock - 1) / kBsBlock;
+    const size_t smem = a.n > kBsFlushBlocks * 16 ? kBsBlock * 33 * sizeof(int32_t) : 0;
+    k_tlp_walk_bs<<<static_cast<unsigned>(grid), kBsBlock, smem, st>>>(a);
     return cudaGetLastError();
 }
 

@@ -124,6 +124,8 @@ cudaError_t launch_wlp_mm1_pipe(const RepArgs& a, int64_t lane_units, int grid, 
 int wlp_mm1_pipe_blocks_per_sm();
 // TLP: thread per replication, block = tlp_block, grid = ceil(count / tlp_block).
 cudaError_t launch_tlp(int model, const RepArgs& a, int tlp_block, cudaStream_t st);
+// Walk, bitsliced thread per 32 replications (needs n < 2^31).
+cudaError_t launch_tlp_walk_bs(const RepArgs& a, cudaStream_t st);
 // Plan: batched seeding (specials carry the job index in `pad`), then one model launch.
 cudaError_t launch_seed_jobs(const uint32_t* powers, const SeedJob* d_jobs, int n_jobs, int64_t total_blocks,
                              int64_t total_slots, uint32_t* out, void* specials, int64_t special_cap,

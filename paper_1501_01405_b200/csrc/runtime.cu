@@ -30,6 +30,7 @@ namespace {
 thread_local std::string g_err;
 thread_local bool g_hw_counters = false;  // wlp_set_hw_counters
 thread_local int g_wlp_variant = 0;       // wlp_set_wlp_variant: 0 auto, 1 lane jumps, 2 pipeline
+thread_local int g_tlp_variant = 0;       // wlp_set_tlp_variant: 0 auto, 1 per replication, 2 bitsliced walk
 
 // mm1 WLP segment chaining hands replications with lambda >= rho * mu to the serial
 // heavy-traffic loop; WLP_MM1_SERIAL_RHO overrides the measured default.
@@ -448,6 +449,11 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
         a.hw = c.hw.p;
     }
     if (mode == WLP_MODE_TLP) {
+        if (model == WLP_MODEL_WALK && g_tlp_variant == 2 && !g_hw_counters && a.n < (int64_t(1) << 31)) {
+            grid_out = static_cast<int>((count + 32 * 128 - 1) / (32 * 128));
+            WLP_CUDA(launch_tlp_walk_bs(a, st));
+            return WLP_OK;
+        }
         const int64_t block = std::min<int64_t>(count, tlp_block);
         grid_out = static_cast<int>((count + block - 1) / block);
         WLP_CUDA(launch_tlp(model, a, tlp_block, st));
@@ -601,6 +607,12 @@ int wlp_version(void) { return 1; }
 int wlp_set_wlp_variant(int variant) {
     if (variant < 0 || variant > 2) return fail(WLP_EDOMAIN, "wlp variant must be 0 (auto), 1 or 2");
     g_wlp_variant = variant;
+    return WLP_OK;
+}
+
+int wlp_set_tlp_variant(int variant) {
+    if (variant < 0 || variant > 2) return fail(WLP_EDOMAIN, "tlp variant must be 0 (auto), 1 or 2");
+    g_tlp_variant = variant;
     return WLP_OK;
 }
 

@@ -137,6 +137,18 @@ def test_mm1_rate_division_modes_all_mappings(gpu, port, lam, mu):
                 assert np.array_equal(run.outputs[name], want[name]), (mode, variant, name)
 
 
+@pytest.mark.parametrize("R,steps", [(1, 1), (31, 15), (32, 16), (33, 17), (100, 1000), (4097, 333), (45, 70_000)])
+def test_walk_bitsliced_tlp_matches_oracle(gpu, port, R, steps):
+    # thread per 32 replications, state bits of 32 streams per word (bitslice.cuh): ragged
+    # last group, step counts around the 16-step carry-save blocks, and a walk past 65520
+    # steps (the int32 shared-memory flush)
+    p = gpu.ModelParams(replications=R, steps=steps, chunks=7 + R % 23)
+    want = port.run_model(2, oracle.params_from(p), 1234 + R)
+    with gpu.tlp_variant(2):
+        run = gpu.run_model(gpu.ModelKind.Walk, p, gpu.ExecutionMode.Tlp, master_seed=1234 + R)
+    assert np.array_equal(run.outputs["out"], want["out"])
+
+
 def test_run_streams_pi_mm1_walk_replication(gpu, port):
     keys = port.random_spacing(3, 50)
     st = gpu.RngState(*[int(x) for x in keys[:, 7]])
@@ -344,7 +356,7 @@ def test_randomized_configurations_all_kernels_vs_oracle(gpu, port):
         want = port.run_model(model, oracle.params_from(p), seed)
         mode = gpu.ExecutionMode(int(rng.integers(0, 3)))
         variant = int(rng.integers(0, 3))
-        with gpu.wlp_variant(variant):
+        with gpu.wlp_variant(variant), gpu.tlp_variant(variant):
             run = gpu.run_model(gpu.ModelKind(model), p, mode, master_seed=seed,
                                 tlp_block_size=int(rng.choice([32, 50, 128, 256])))
         for name in oracle.OUTPUTS[model]:
