@@ -124,8 +124,9 @@ int wlp_set_hw_counters(int enable);
  * 0 = automatic (default); 1 = lane jumps (pi / walk: each lane jumps its stream to its
  * chunk; mm1: segment chaining by fixed-point rounds); 2 = warp pipeline (replications
  * move lane to lane, each lane runs its segment in order from the state its neighbour
- * hands over; a 31-step drain per warp). Outputs are identical; only speed differs
- * (DESIGN.md §4). */
+ * hands over; a 31-step drain per warp); 3 = walk: bitsliced warp pipeline (each pipeline
+ * slot carries 32 replications as bit planes; chosen automatically for large R; other
+ * models treat 3 as 0). Outputs are identical; only speed differs. */
 int wlp_set_wlp_variant(int variant);
 
 /* The same for the TLP (thread-level) mapping: 0 = automatic (default: one thread per

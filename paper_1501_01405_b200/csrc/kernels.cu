@@ -953,26 +953,44 @@ __global__ void k_tlp(RepArgs a) {
 constexpr int kBsBlock = 128;
 constexpr int64_t kBsFlushBlocks = 4095;  // 4095 * 16 steps keep every count below 2^16
 
-__device__ __forceinline__ void bs_pair(BsTaus& t, BsCount& P, BsCount& Q, uint32_t& p2, uint32_t& q2) {
+// Steps k of a 16-step block count only while k < valid (MASK; the masks fold into the
+// LOP3s that form them). Without MASK every step counts.
+template <bool MASK>
+__device__ __forceinline__ void bs_step_m(BsTaus& t, uint32_t& pl, uint32_t& mi, int k, int valid) {
+    bs_walk_step(t, pl, mi);
+    if (MASK) {
+        const uint32_t keep = k < valid ? ~0u : 0u;
+        pl &= keep;
+        mi &= keep;
+    }
+}
+
+template <bool MASK>
+__device__ __forceinline__ void bs_pair(BsTaus& t, BsCount& P, BsCount& Q, uint32_t& p2, uint32_t& q2, int k,
+                                        int valid) {
     uint32_t pa, ma, pb, mb;
-    bs_walk_step(t, pa, ma);
-    bs_walk_step(t, pb, mb);
+    bs_step_m<MASK>(t, pa, ma, k, valid);
+    bs_step_m<MASK>(t, pb, mb, k + 1, valid);
     bs_csa(p2, P.c[0], P.c[0], pa, pb);
     bs_csa(q2, Q.c[0], Q.c[0], ma, mb);
 }
 
-__device__ __forceinline__ void bs_quad(BsTaus& t, BsCount& P, BsCount& Q, uint32_t& p4, uint32_t& q4) {
+template <bool MASK>
+__device__ __forceinline__ void bs_quad(BsTaus& t, BsCount& P, BsCount& Q, uint32_t& p4, uint32_t& q4, int k,
+                                        int valid) {
     uint32_t pa, qa, pb, qb;
-    bs_pair(t, P, Q, pa, qa);
-    bs_pair(t, P, Q, pb, qb);
+    bs_pair<MASK>(t, P, Q, pa, qa, k, valid);
+    bs_pair<MASK>(t, P, Q, pb, qb, k + 2, valid);
     bs_csa(p4, P.c[1], P.c[1], pa, pb);
     bs_csa(q4, Q.c[1], Q.c[1], qa, qb);
 }
 
-__device__ __forceinline__ void bs_oct(BsTaus& t, BsCount& P, BsCount& Q, uint32_t& p8, uint32_t& q8) {
+template <bool MASK>
+__device__ __forceinline__ void bs_oct(BsTaus& t, BsCount& P, BsCount& Q, uint32_t& p8, uint32_t& q8, int k,
+                                       int valid) {
     uint32_t pa, qa, pb, qb;
-    bs_quad(t, P, Q, pa, qa);
-    bs_quad(t, P, Q, pb, qb);
+    bs_quad<MASK>(t, P, Q, pa, qa, k, valid);
+    bs_quad<MASK>(t, P, Q, pb, qb, k + 4, valid);
     bs_csa(p8, P.c[2], P.c[2], pa, pb);
     bs_csa(q8, Q.c[2], Q.c[2], qa, qb);
 }
@@ -1020,8 +1038,8 @@ __global__ void __launch_bounds__(kBsBlock) k_tlp_walk_bs(RepArgs a) {
     const int64_t blocks = a.n / 16;
     for (int64_t b = 0; b < blocks; ++b) {
         uint32_t pa, qa, pb, qb, p16, q16;
-        bs_oct(t, P, Q, pa, qa);
-        bs_oct(t, P, Q, pb, qb);
+        bs_oct<false>(t, P, Q, pa, qa, 0, 16);
+        bs_oct<false>(t, P, Q, pb, qb, 8, 16);
         bs_csa(p16, P.c[3], P.c[3], pa, pb);
         bs_csa(q16, Q.c[3], Q.c[3], qa, qb);
         bs_ripple16(P, p16);
@@ -1043,6 +1061,174 @@ __global__ void __launch_bounds__(kBsBlock) k_tlp_walk_bs(RepArgs a) {
         const int64_t dx = static_cast<int64_t>(pv[j]) - static_cast<int64_t>(qv[j]) + (flushing ? acc[j] : 0);
         a.out0[r0 + j] = walk_fold(dx, a.chunks);
     }
+}
+
+// ---------------------------------------------------------------------------------
+// Walk WLP, bitsliced warp pipeline. The warp pipeline of k_wlp_pipe (a replication
+// enters at lane 0, lane l runs steps [l*K, (l+1)*K) of it from the state lane l-1 hands
+// over, lane 31 completes one every pipeline step) with 32 replications per slot held as
+// bit planes (bitslice.cuh): each lane advances a group of 32 replications, so a warp
+// still owns every replication it runs and its lanes split each one's steps. Per step a
+// lane hands over 88 live state words and the 32 counter digits. Group seeds are
+// transposed once by k_bs_seeds; lane 31's finished counters collect in shared memory and
+// 32 groups are finalised at once (one per lane). Counts must stay below 2^16 (n < 65536).
+// ---------------------------------------------------------------------------------
+constexpr int kBsLive = 88;  // b1[1..31], b2[3..31], b3[4..31]
+
+__global__ void __launch_bounds__(kBsBlock) k_bs_seeds(RepArgs a, int64_t groups, uint32_t* __restrict__ out) {
+    const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (g >= groups) return;
+    BsTaus t;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const int64_t r = g * 32 + j;
+        const Taus st = r < a.count ? load_seed(a, r) : Taus{kMin1, kMin2, kMin3};
+        t.b1[j] = st.s1;
+        t.b2[j] = st.s2;
+        t.b3[j] = st.s3;
+    }
+    transpose32(t.b1);
+    transpose32(t.b2);
+    transpose32(t.b3);
+    uint32_t w[kBsLive];
+#pragma unroll
+    for (int i = 1; i < 32; ++i) w[i - 1] = t.b1[i];
+#pragma unroll
+    for (int i = 3; i < 32; ++i) w[31 + i - 3] = t.b2[i];
+#pragma unroll
+    for (int i = 4; i < 32; ++i) w[60 + i - 4] = t.b3[i];
+    uint4* o = reinterpret_cast<uint4*>(out + g * kBsLive);
+#pragma unroll
+    for (int k = 0; k < kBsLive / 4; ++k) o[k] = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+}
+
+// A lane's chunk of its group: `blocks` 16-step carry-save blocks for every lane of the
+// warp alike (no lane runs a tail the others wait for); steps past the lane's `units`
+// do not count. Only a group's last chunk is partial (the lane chunk is a multiple of
+// 16), and the state it ends with is never used.
+__device__ __forceinline__ void bs_walk_units(BsTaus& t, BsCount& P, BsCount& Q, uint32_t units, uint32_t blocks) {
+    for (uint32_t b = 0; b < blocks; ++b) {
+        const int valid = static_cast<int>(units > 16 * b ? (units - 16 * b < 16 ? units - 16 * b : 16) : 0);
+        uint32_t pa, qa, pb, qb, p16, q16;
+        bs_oct<true>(t, P, Q, pa, qa, 0, valid);
+        bs_oct<true>(t, P, Q, pb, qb, 8, valid);
+        bs_csa(p16, P.c[3], P.c[3], pa, pb);
+        bs_csa(q16, Q.c[3], Q.c[3], qa, qb);
+        bs_ripple16(P, p16);
+        bs_ripple16(Q, q16);
+    }
+}
+
+struct BsPipeWarp {
+    uint32_t cnt[32][33];  // finished groups: P digits 0..15, Q digits 16..31 (+1 pad)
+    long long grp[32];
+};
+
+__global__ void __launch_bounds__(kBsPipeBlock) k_wlp_walk_bs_pipe(RepArgs a, const uint32_t* __restrict__ bseeds,
+                                                                    int64_t groups, int64_t K) {
+    __shared__ BsPipeWarp sh[kBsPipeBlock / 32];
+    BsPipeWarp& E = sh[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    int64_t mine = a.n - static_cast<int64_t>(lane) * K;
+    mine = mine < 0 ? 0 : (mine > K ? K : mine);
+    const uint32_t units = static_cast<uint32_t>(mine);
+    RepArgs ga = a;  // the grab scheduler hands out groups
+    ga.count = groups;
+    BsTaus t;
+    BsCount P, Q;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) t.b1[i] = t.b2[i] = t.b3[i] = 0u;
+    bs_count_init(P);
+    bs_count_init(Q);
+    long long grp = -1;
+    int64_t cur = 0, cend = 0;
+    bool more = true;
+    int nemit = 0;
+    auto flush = [&](int cnt) {
+        __syncwarp();
+        if (lane < cnt) {
+            const long long g = E.grp[lane];
+            uint32_t pv[32], qv[32];
+#pragma unroll
+            for (int w = 0; w < 32; ++w) {
+                pv[w] = w < 16 ? E.cnt[lane][w] : 0u;
+                qv[w] = w < 16 ? E.cnt[lane][16 + w] : 0u;
+            }
+            transpose32(pv);
+            transpose32(qv);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const int64_t r = g * 32 + j;
+                if (r < a.count)
+                    a.out0[r] = walk_fold(static_cast<int64_t>(pv[j]) - static_cast<int64_t>(qv[j]), a.chunks);
+            }
+        }
+        __syncwarp();
+    };
+    for (;;) {
+        if (more && cur >= cend) {
+            const int64_t base = grab_take(grab_issue(ga, lane));
+            if (base >= groups) {
+                more = false;
+            } else {
+                cur = base;
+                cend = base + a.grab < groups ? base + a.grab : groups;
+            }
+        }
+        if (lane == 0) {  // feed the next group's bit planes
+            grp = more ? cur : -1;
+            if (more) {
+                const uint4* src = reinterpret_cast<const uint4*>(bseeds + cur * kBsLive);
+                uint32_t w[kBsLive];
+#pragma unroll
+                for (int k = 0; k < kBsLive / 4; ++k) {
+                    const uint4 v = __ldg(src + k);
+                    w[4 * k] = v.x;
+                    w[4 * k + 1] = v.y;
+                    w[4 * k + 2] = v.z;
+                    w[4 * k + 3] = v.w;
+                }
+#pragma unroll
+                for (int i = 1; i < 32; ++i) t.b1[i] = w[i - 1];
+#pragma unroll
+                for (int i = 3; i < 32; ++i) t.b2[i] = w[31 + i - 3];
+#pragma unroll
+                for (int i = 4; i < 32; ++i) t.b3[i] = w[60 + i - 4];
+                bs_count_init(P);
+                bs_count_init(Q);
+            }
+        }
+        if (more) ++cur;
+        if (!__any_sync(kFull, grp >= 0)) break;
+        if (grp >= 0) bs_walk_units(t, P, Q, units, static_cast<uint32_t>(K / 16));
+        if (__shfl_sync(kFull, grp, 31) >= 0) {  // lane 31 finished a group
+            if (lane == 31) {
+#pragma unroll
+                for (int w = 0; w < 16; ++w) {
+                    E.cnt[nemit][w] = P.c[w];
+                    E.cnt[nemit][16 + w] = Q.c[w];
+                }
+                E.grp[nemit] = grp;
+            }
+            if (++nemit == 32) {
+                flush(32);
+                nemit = 0;
+            }
+        }
+#pragma unroll
+        for (int i = 1; i < 32; ++i) t.b1[i] = __shfl_up_sync(kFull, t.b1[i], 1);
+#pragma unroll
+        for (int i = 3; i < 32; ++i) t.b2[i] = __shfl_up_sync(kFull, t.b2[i], 1);
+#pragma unroll
+        for (int i = 4; i < 32; ++i) t.b3[i] = __shfl_up_sync(kFull, t.b3[i], 1);
+#pragma unroll
+        for (int w = 0; w < 16; ++w) {
+            P.c[w] = __shfl_up_sync(kFull, P.c[w], 1);
+            Q.c[w] = __shfl_up_sync(kFull, Q.c[w], 1);
+        }
+        grp = __shfl_up_sync(kFull, grp, 1);
+    }
+    flush(nemit);
 }
 
 // mm1 thread per replication: each lane runs its own queue; the exponentials of 4
@@ -1616,6 +1802,20 @@ cudaError_t launch_tlp_walk_bs(const RepArgs& a, cudaStream_t st) {
     const size_t smem = a.n > kBsFlushBlocks * 16 ? kBsBlock * 33 * sizeof(int32_t) : 0;
     k_tlp_walk_bs<<<static_cast<unsigned>(grid), kBsBlock, smem, st>>>(a);
     return cudaGetLastError();
+}
+
+cudaError_t launch_wlp_walk_bs_pipe(const RepArgs& a, uint32_t* bseeds, int64_t K, int grid, cudaStream_t st) {
+    if (a.count <= 0) return cudaSuccess;
+    const int64_t groups = (a.count + 31) / 32;
+    k_bs_seeds<<<static_cast<unsigned>((groups + kBsBlock - 1) / kBsBlock), kBsBlock, 0, st>>>(a, groups, bseeds);
+    k_wlp_walk_bs_pipe<<<grid, kBsPipeBlock, 0, st>>>(a, bseeds, groups, K);
+    return cudaGetLastError();
+}
+
+int wlp_walk_bs_pipe_blocks_per_sm() {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_walk_bs_pipe, kBsPipeBlock, 0);
+    return nb < 1 ? 1 : nb;
 }
 
 int plan_blocks_per_sm(int model) {

@@ -126,6 +126,11 @@ int wlp_mm1_pipe_blocks_per_sm();
 cudaError_t launch_tlp(int model, const RepArgs& a, int tlp_block, cudaStream_t st);
 // Walk, bitsliced thread per 32 replications (needs n < 2^31).
 cudaError_t launch_tlp_walk_bs(const RepArgs& a, cudaStream_t st);
+// Walk WLP, bitsliced warp pipeline (groups of 32 replications; n < 65536). bseeds:
+// scratch of 88 words per group; a.next zeroed, a.grab groups per grab.
+cudaError_t launch_wlp_walk_bs_pipe(const RepArgs& a, uint32_t* bseeds, int64_t K, int grid, cudaStream_t st);
+int wlp_walk_bs_pipe_blocks_per_sm();
+constexpr int kBsPipeBlock = 64;  // threads per block of the bitsliced walk pipeline
 // Plan: batched seeding (specials carry the job index in `pad`), then one model launch.
 cudaError_t launch_seed_jobs(const uint32_t* powers, const SeedJob* d_jobs, int n_jobs, int64_t total_blocks,
                              int64_t total_slots, uint32_t* out, void* specials, int64_t special_cap,

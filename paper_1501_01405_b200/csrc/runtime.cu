@@ -90,13 +90,14 @@ struct DevCtx {
     int sms = 0;
     int clock_khz = 0;
     int wlp_bps[3] = {1, 1, 1};
-    int pipe_bps = 1, mm1_pipe_bps = 1;
+    int pipe_bps = 1, mm1_pipe_bps = 1, bs_pipe_bps = 1;
     std::mutex mu;
     bool ready = false;
     DevBuf<uint32_t> powers;
     std::map<uint64_t, DevBuf<uint32_t>> lane_tabs;  // by lane jump stride (draws)
     DevBuf<uint32_t> mm1_lane, mm1_skip;
     DevBuf<uint32_t> seeds, in_seeds;
+    DevBuf<uint32_t> bseeds;  // walk bitsliced pipeline: group seed bit planes
     DevBuf<double> outs, partials, stats_in;
     DevBuf<SpecialRec> specials;
     DevBuf<unsigned long long> counter;
@@ -133,6 +134,7 @@ int ctx_init(DevCtx& c) {
     WLP_TRY(upload_u32(c.plan_skip, uniform_table(2ull * 31 * kPlanT)));
     c.pipe_bps = wlp_pipe_blocks_per_sm();
     c.mm1_pipe_bps = wlp_mm1_pipe_blocks_per_sm();
+    c.bs_pipe_bps = wlp_walk_bs_pipe_blocks_per_sm();
     for (int m = 0; m < 3; ++m) {
         c.wlp_bps[m] = wlp_blocks_per_sm(m);
         c.plan_bps[m] = plan_blocks_per_sm(m);
@@ -479,6 +481,23 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
         } else {
             WLP_CUDA(launch_wlp(model, a, c.mm1_lane.p, c.mm1_skip.p, 0, grid_out, st));
         }
+    } else if (model == WLP_MODEL_WALK && !g_hw_counters && a.n < 65536 &&
+               (g_wlp_variant == 3 ||
+                (g_wlp_variant == 0 &&
+                 (count + 31) / 32 >= 8 * static_cast<int64_t>(c.sms) * c.bs_pipe_bps * (kBsPipeBlock / 32)))) {
+        // bitsliced pipeline: groups of 32 replications; at least ~64 groups per warp so
+        // the 31-step drain stays small. Automatic once every resident warp gets 8 or more
+        // groups (R >= ~3.8e5 on 148 SMs); below that the per-replication kernels win
+        // (config 3, R = 1e5: 0.143 vs 0.293 ms).
+        const int64_t groups = (count + 31) / 32;
+        const int64_t warps_want = std::max<int64_t>(1, groups / 64);
+        const int64_t cap = static_cast<int64_t>(c.sms) * c.bs_pipe_bps;
+        grid_out = static_cast<int>(std::clamp<int64_t>((warps_want + 1) / 2, 1, cap));
+        a.grab = static_cast<int>(std::clamp<int64_t>(groups / (2 * grid_out * 32), 1, 32));
+        WLP_CUDA(c.bseeds.ensure(groups * 88));
+        // lane chunk: a multiple of 16 steps, so only a group's last chunk is partial
+        const int64_t K = ((a.n + 31) / 32 + 15) / 16 * 16;
+        WLP_CUDA(launch_wlp_walk_bs_pipe(a, c.bseeds.p, K, grid_out, st));
     } else {
         const int64_t K = (a.n + 31) / 32;
         // Lane jumps cost ~80 instructions per lane per replication against K units of
@@ -605,7 +624,7 @@ const char* wlp_last_error(void) { return g_err.c_str(); }
 int wlp_version(void) { return 1; }
 
 int wlp_set_wlp_variant(int variant) {
-    if (variant < 0 || variant > 2) return fail(WLP_EDOMAIN, "wlp variant must be 0 (auto), 1 or 2");
+    if (variant < 0 || variant > 3) return fail(WLP_EDOMAIN, "wlp variant must be 0 (auto), 1, 2 or 3");
     g_wlp_variant = variant;
     return WLP_OK;
 }

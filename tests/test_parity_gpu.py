@@ -149,6 +149,26 @@ def test_walk_bitsliced_tlp_matches_oracle(gpu, port, R, steps):
     assert np.array_equal(run.outputs["out"], want["out"])
 
 
+@pytest.mark.parametrize("R,steps", [(1, 1), (33, 17), (64, 16), (100, 1000), (5000, 333), (70, 40_000),
+                                     (40, 65_535), (3000, 511)])
+def test_walk_bitsliced_wlp_pipeline_matches_oracle(gpu, port, R, steps):
+    # groups of 32 replications move lane to lane as bit planes; lane chunks are whole
+    # 16-step blocks with the steps past a group's end masked out of the counts
+    p = gpu.ModelParams(replications=R, steps=steps, chunks=3 + R % 29)
+    want = port.run_model(2, oracle.params_from(p), 4321 + R)
+    with gpu.wlp_variant(3):
+        run = gpu.run_model(gpu.ModelKind.Walk, p, gpu.ExecutionMode.Wlp, master_seed=4321 + R)
+    assert np.array_equal(run.outputs["out"], want["out"])
+
+
+def test_walk_wlp_auto_picks_the_bitsliced_pipeline_at_large_R(gpu, port):
+    # R = 6e5: above the automatic threshold; the result is still the reference's
+    p = gpu.ModelParams(replications=600_000, steps=100, chunks=30)
+    want = port.run_model(2, oracle.params_from(p), 42)
+    run = gpu.run_model(gpu.ModelKind.Walk, p, gpu.ExecutionMode.Wlp, master_seed=42)
+    assert np.array_equal(run.outputs["out"], want["out"])
+
+
 def test_run_streams_pi_mm1_walk_replication(gpu, port):
     keys = port.random_spacing(3, 50)
     st = gpu.RngState(*[int(x) for x in keys[:, 7]])
@@ -355,8 +375,8 @@ def test_randomized_configurations_all_kernels_vs_oracle(gpu, port):
         seed = int(rng.integers(0, 2**63))
         want = port.run_model(model, oracle.params_from(p), seed)
         mode = gpu.ExecutionMode(int(rng.integers(0, 3)))
-        variant = int(rng.integers(0, 3))
-        with gpu.wlp_variant(variant), gpu.tlp_variant(variant):
+        variant = int(rng.integers(0, 4))
+        with gpu.wlp_variant(variant), gpu.tlp_variant(min(variant, 2)):
             run = gpu.run_model(gpu.ModelKind(model), p, mode, master_seed=seed,
                                 tlp_block_size=int(rng.choice([32, 50, 128, 256])))
         for name in oracle.OUTPUTS[model]:
