@@ -1122,7 +1122,18 @@ __device__ __forceinline__ void bs_walk_units(BsTaus& t, BsCount& P, BsCount& Q,
 struct BsPipeWarp {
     uint32_t cnt[32][33];  // finished groups: P digits 0..15, Q digits 16..31 (+1 pad)
     long long grp[32];
+    __align__(16) uint32_t seed[2][kBsLive];  // next groups' bit planes, fetched a step ahead
 };
+
+// Lanes 0..21 copy one 16-byte piece each of a group's 352-byte bit planes into shared
+// memory, asynchronously (cp.async), so lane 0's feed never waits on global memory.
+__device__ __forceinline__ void bs_prefetch(uint32_t* dst, const uint32_t* src, int lane) {
+    if (lane < kBsLive / 4) {
+        const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst + 4 * lane));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + 4 * lane) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
 
 __global__ void __launch_bounds__(kBsPipeBlock) k_wlp_walk_bs_pipe(RepArgs a, const uint32_t* __restrict__ bseeds,
                                                                     int64_t groups, int64_t K) {
@@ -1156,16 +1167,17 @@ __global__ void __launch_bounds__(kBsPipeBlock) k_wlp_walk_bs_pipe(RepArgs a, co
             }
             transpose32(pv);
             transpose32(qv);
+            int32_t* dx = reinterpret_cast<int32_t*>(E.cnt[lane]);  // the slot's own row
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
+            for (int j = 0; j < 32; ++j) dx[j] = static_cast<int32_t>(pv[j]) - static_cast<int32_t>(qv[j]);
+            for (int j = 0; j < 32; ++j) {  // not unrolled: one copy of fmod's code
                 const int64_t r = g * 32 + j;
-                if (r < a.count)
-                    a.out0[r] = walk_fold(static_cast<int64_t>(pv[j]) - static_cast<int64_t>(qv[j]), a.chunks);
+                if (r < a.count) a.out0[r] = walk_fold(dx[j], a.chunks);
             }
         }
         __syncwarp();
     };
-    for (;;) {
+    auto next_group = [&]() -> long long {  // warp-uniform
         if (more && cur >= cend) {
             const int64_t base = grab_take(grab_issue(ga, lane));
             if (base >= groups) {
@@ -1175,14 +1187,22 @@ __global__ void __launch_bounds__(kBsPipeBlock) k_wlp_walk_bs_pipe(RepArgs a, co
                 cend = base + a.grab < groups ? base + a.grab : groups;
             }
         }
-        if (lane == 0) {  // feed the next group's bit planes
-            grp = more ? cur : -1;
-            if (more) {
-                const uint4* src = reinterpret_cast<const uint4*>(bseeds + cur * kBsLive);
+        return more ? cur++ : -1;
+    };
+    long long feed = next_group();
+    int buf = 0;
+    if (feed >= 0) bs_prefetch(E.seed[buf], bseeds + feed * kBsLive, lane);
+    for (;;) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {  // feed the group fetched last step
+            grp = feed;
+            if (feed >= 0) {
+                const uint4* src = reinterpret_cast<const uint4*>(E.seed[buf]);
                 uint32_t w[kBsLive];
 #pragma unroll
                 for (int k = 0; k < kBsLive / 4; ++k) {
-                    const uint4 v = __ldg(src + k);
+                    const uint4 v = src[k];
                     w[4 * k] = v.x;
                     w[4 * k + 1] = v.y;
                     w[4 * k + 2] = v.z;
@@ -1198,7 +1218,10 @@ __global__ void __launch_bounds__(kBsPipeBlock) k_wlp_walk_bs_pipe(RepArgs a, co
                 bs_count_init(Q);
             }
         }
-        if (more) ++cur;
+        __syncwarp();
+        feed = next_group();
+        buf ^= 1;
+        if (feed >= 0) bs_prefetch(E.seed[buf], bseeds + feed * kBsLive, lane);
         if (!__any_sync(kFull, grp >= 0)) break;
         if (grp >= 0) bs_walk_units(t, P, Q, units, static_cast<uint32_t>(K / 16));
         if (__shfl_sync(kFull, grp, 31) >= 0) {  // lane 31 finished a group

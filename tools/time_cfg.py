@@ -1,7 +1,8 @@
 #!/usr/bin/env python3
 """Time replication kernels on the GPU box (device-resident outputs, SimReport kernel_ms).
 
-    python tools/time_cfg.py mm1:wlp:10000000:1000 mm1:tlp:10000000:1000 ...
+    python tools/time_cfg.py mm1:wlp:10000000:1000 mm1:tlp:10000000:1000 walk:wlp:1000000:1000:wv=3 ...
+(extra key=value fields: ModelParams fields, wv= / tv= the WLP / TLP kernel variant)
 """
 import sys
 from pathlib import Path
@@ -18,15 +19,17 @@ for spec in sys.argv[1:]:
     m = w.model_from_name(model)
     R, N = int(R), int(N)
     kw = dict(replications=R, draws=N, clients=N, steps=N)
+    wv, tv = int(extra.pop("wv", 0)), int(extra.pop("tv", 0))  # WLP / TLP kernel variants
     for k, v in extra.items():
         kw[k] = float(v) if "." in v else int(v)
     p = w.ModelParams(**kw)
     outs = [torch.empty(R, dtype=torch.float64, device="cuda") for _ in w.OUTPUT_NAMES[m]]
     ms = []
-    for i in range(4):
-        rep = w.SimReport()
-        w.run_shard(m, p, w.mode_from_name(mode), 42, 0, R, outs, on_device=True, report=rep)
-        torch.cuda.synchronize()
-        if i:
-            ms.append(rep.kernel_ms)
+    with w.wlp_variant(wv), w.tlp_variant(tv):
+        for i in range(4):
+            rep = w.SimReport()
+            w.run_shard(m, p, w.mode_from_name(mode), 42, 0, R, outs, on_device=True, report=rep)
+            torch.cuda.synchronize()
+            if i:
+                ms.append(rep.kernel_ms)
     print(f"{spec:40s} kernel_ms min {min(ms):9.3f} med {sorted(ms)[len(ms) // 2]:9.3f}", flush=True)
