@@ -56,6 +56,9 @@ SEED = 42
 # 2 exact u32->f64 + 2 DMUL + DADD + DSETP + count = 39; walk step = 2 draws + shift +
 # 2 compare/add = 35.
 INSTR_PER_UNIT = {0: 39, 2: 35}
+# Bitsliced walk (csrc/bitslice.cuh): LOP3 per walk step for 32 replications at once, as
+# compiled (726 per 16-step carry-save block of k_tlp_walk_bs).
+BS_LOP3_PER_STEP = 45.4
 # mm1 is FP64-pipe work: per client two exponentials, each 1-u (1) + glibc log (15 fp ops
 # on the table path as compiled in __log_fma, 26 on the near-one path taken 1 time in 16:
 # 15.7 average) + negate/scale (1), plus the Lindley step (6 DADD + 1 compare) = 42.
@@ -323,7 +326,8 @@ def model_rate(w, model, p, mode, steps=5, warmup=3):
 
     ms = device_timed(step, steps, warmup, 1)
     k = kms[warmup:]
-    return {"reps_per_s": p.replications / (ms * 1e-3), "ms_per_run": ms, "kernel_ms": sum(k) / len(k)}
+    return {"reps_per_s": p.replications / (ms * 1e-3), "ms_per_run": ms, "kernel_ms": sum(k) / len(k),
+            "kernel": w.last_kernel()}
 
 
 def main():
@@ -436,11 +440,28 @@ def main():
             for md in (w.ExecutionMode.Wlp, w.ExecutionMode.Tlp):
                 r = model_rate(w, m, pp, md)
                 units_ = pp.replications * pp.units(m)
-                if m in INSTR_PER_UNIT:
+                if "walk_bs" in r["kernel"]:  # bitsliced: ALU pipe against its own LOP3 count
+                    r["alu_frac"] = units_ * BS_LOP3_PER_STEP / 32 / 32 / (r["kernel_ms"] * 1e-3) / (2 * sms * fmax * 1e6)
+                elif m in INSTR_PER_UNIT:
                     r["issue_frac"] = units_ * INSTR_PER_UNIT[int(m)] / 32 / (r["kernel_ms"] * 1e-3) / (peak * 1e9)
                 else:  # FP64 pipe: 64 lanes/clk/SM (measured, profiles/round1_microbench.txt)
                     r["fp64_frac"] = units_ * FP64_PER_CLIENT / (r["kernel_ms"] * 1e-3) / (64 * sms * fmax * 1e6)
                 extras[name][w.mode_name(md)] = r
+            if m == w.ModelKind.Walk:
+                # the walk's other kernels (DESIGN.md §4 bitsliced walk): per-replication
+                # WLP pipeline / lane jumps, and the bitsliced TLP (thread per 32 replications).
+                # Bitsliced work is ~45 LOP3 per step per 32 replications, ALU pipe 2/clk/SM.
+                units_ = pp.replications * pp.steps
+                for label, wv, tv, md in (("wlp_per_replication", 2 if pp.replications >= 1_000_000 else 1, 0,
+                                           w.ExecutionMode.Wlp),
+                                          ("tlp_bitsliced", 0, 2, w.ExecutionMode.Tlp)):
+                    with w.wlp_variant(wv), w.tlp_variant(tv):
+                        r = model_rate(w, m, pp, md)
+                    if "walk_bs" in r["kernel"]:
+                        r["alu_frac"] = units_ * BS_LOP3_PER_STEP / 32 / 32 / (r["kernel_ms"] * 1e-3) / (2 * sms * fmax * 1e6)
+                    else:
+                        r["issue_frac"] = units_ * INSTR_PER_UNIT[2] / 32 / (r["kernel_ms"] * 1e-3) / (peak * 1e9)
+                    extras[name][label] = r
         # config 3's warp-execution evidence (paper Table 1 / Fig. 7 analogue): divergence
         # events with the reference's definition and global memory warp-instructions, from
         # the instrumented kernels (outputs identical; counters cost a little speed)

@@ -135,6 +135,10 @@ int wlp_set_wlp_variant(int variant);
  * word (pi / mm1 keep the per-replication kernel). Outputs are identical. */
 int wlp_set_tlp_variant(int variant);
 
+/* Name of the model kernel the last run on this thread launched (e.g. "k_wlp_pipe<pi>",
+ * "k_wlp_walk_bs_pipe", "k_tlp_mm1"); "" before any run. Static storage. */
+const char* wlp_last_kernel(void);
+
 /* validate_params (models.cpp:26-44): WLP_EDOMAIN on invalid values; a non-empty
  * warning (lambda >= mu) is copied into warn[cap]. */
 int wlp_validate_params(int model, const wlp_params* p, char* warn, int warn_cap);

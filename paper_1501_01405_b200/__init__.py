@@ -242,6 +242,7 @@ _SIGS = {
     "wlp_set_hw_counters": (C.c_int, [C.c_int]),
     "wlp_set_wlp_variant": (C.c_int, [C.c_int]),
     "wlp_set_tlp_variant": (C.c_int, [C.c_int]),
+    "wlp_last_kernel": (C.c_char_p, []),
     "wlp_validate_params": (C.c_int, [C.c_int, C.POINTER(_Params), C.c_char_p, C.c_int]),
     "wlp_plan_launch": (C.c_int, [_I64, C.c_int, C.c_int, _I64, C.POINTER(_Cfg), C.c_char_p, C.c_int]),
     "wlp_master_from_seed": (C.c_int, [C.c_uint64, _P]),
@@ -509,6 +510,11 @@ class wlp_variant:
 
     def __exit__(self, *exc):
         _check(_lib.wlp_set_wlp_variant(0))
+
+
+def last_kernel() -> str:
+    """Name of the model kernel the last run on this thread launched (wlp_last_kernel)."""
+    return _lib.wlp_last_kernel().decode()
 
 
 class tlp_variant:

@@ -30,6 +30,7 @@ namespace {
 thread_local std::string g_err;
 thread_local bool g_hw_counters = false;  // wlp_set_hw_counters
 thread_local int g_wlp_variant = 0;       // wlp_set_wlp_variant: 0 auto, 1 lane jumps, 2 pipeline
+thread_local const char* g_last_kernel = "";  // wlp_last_kernel
 thread_local int g_tlp_variant = 0;       // wlp_set_tlp_variant: 0 auto, 1 per replication, 2 bitsliced walk
 
 // mm1 WLP segment chaining hands replications with lambda >= rho * mu to the serial
@@ -453,11 +454,13 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
     if (mode == WLP_MODE_TLP) {
         if (model == WLP_MODEL_WALK && g_tlp_variant == 2 && !g_hw_counters && a.n < (int64_t(1) << 31)) {
             grid_out = static_cast<int>((count + 32 * 128 - 1) / (32 * 128));
+            g_last_kernel = "k_tlp_walk_bs";
             WLP_CUDA(launch_tlp_walk_bs(a, st));
             return WLP_OK;
         }
         const int64_t block = std::min<int64_t>(count, tlp_block);
         grid_out = static_cast<int>((count + block - 1) / block);
+        g_last_kernel = model == WLP_MODEL_PI ? "k_tlp<pi>" : (model == WLP_MODEL_MM1 ? "k_tlp_mm1" : "k_tlp<walk>");
         WLP_CUDA(launch_tlp(model, a, tlp_block, st));
         return WLP_OK;
     }
@@ -477,8 +480,10 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
         if (pipe) {
             const int64_t cap = static_cast<int64_t>(c.sms) * c.mm1_pipe_bps;
             grid_out = static_cast<int>(std::min<int64_t>(grid_out, cap));
+            g_last_kernel = "k_wlp_mm1_pipe";
             WLP_CUDA(launch_wlp_mm1_pipe(a, (a.n + 31) / 32, grid_out, st));
         } else {
+            g_last_kernel = "k_wlp_mm1";
             WLP_CUDA(launch_wlp(model, a, c.mm1_lane.p, c.mm1_skip.p, 0, grid_out, st));
         }
     } else if (model == WLP_MODEL_WALK && !g_hw_counters && a.n < 65536 &&
@@ -497,6 +502,7 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
         WLP_CUDA(c.bseeds.ensure(groups * 88));
         // lane chunk: a multiple of 16 steps, so only a group's last chunk is partial
         const int64_t K = ((a.n + 31) / 32 + 15) / 16 * 16;
+        g_last_kernel = "k_wlp_walk_bs_pipe";
         WLP_CUDA(launch_wlp_walk_bs_pipe(a, c.bseeds.p, K, grid_out, st));
     } else {
         const int64_t K = (a.n + 31) / 32;
@@ -509,6 +515,7 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
         if (pipe) {
             const int64_t cap = static_cast<int64_t>(c.sms) * c.pipe_bps;
             grid_out = static_cast<int>(std::min<int64_t>(grid_out, cap));
+            g_last_kernel = model == WLP_MODEL_PI ? "k_wlp_pipe<pi>" : "k_wlp_pipe<walk>";
             WLP_CUDA(launch_wlp_pipe(model, a, K, grid_out, st));
         } else {
             // With few replications per warp the last groups leave a tail: 3 of the 4
@@ -516,6 +523,7 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
             if (per_warp < 32.0) grid_out = std::min(grid_out, 3 * c.sms);
             const uint32_t* tab = nullptr;
             WLP_TRY(lane_table(c, 2ull * static_cast<uint64_t>(K), tab));
+            g_last_kernel = model == WLP_MODEL_PI ? "k_wlp_lanes<pi>" : "k_wlp_lanes<walk>";
             WLP_CUDA(launch_wlp(model, a, tab, nullptr, K, grid_out, st));
         }
     }
@@ -628,6 +636,8 @@ int wlp_set_wlp_variant(int variant) {
     g_wlp_variant = variant;
     return WLP_OK;
 }
+
+const char* wlp_last_kernel(void) { return g_last_kernel; }
 
 int wlp_set_tlp_variant(int variant) {
     if (variant < 0 || variant > 2) return fail(WLP_EDOMAIN, "tlp variant must be 0 (auto), 1 or 2");

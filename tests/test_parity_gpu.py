@@ -166,7 +166,13 @@ def test_walk_wlp_auto_picks_the_bitsliced_pipeline_at_large_R(gpu, port):
     p = gpu.ModelParams(replications=600_000, steps=100, chunks=30)
     want = port.run_model(2, oracle.params_from(p), 42)
     run = gpu.run_model(gpu.ModelKind.Walk, p, gpu.ExecutionMode.Wlp, master_seed=42)
+    assert gpu.last_kernel() == "k_wlp_walk_bs_pipe"
     assert np.array_equal(run.outputs["out"], want["out"])
+    small = gpu.ModelParams(replications=1000, steps=100, chunks=30)
+    gpu.run_model(gpu.ModelKind.Walk, small, gpu.ExecutionMode.Wlp, master_seed=42)
+    assert gpu.last_kernel() in ("k_wlp_lanes<walk>", "k_wlp_pipe<walk>")
+    gpu.run_model(gpu.ModelKind.Walk, small, gpu.ExecutionMode.Tlp, master_seed=42)
+    assert gpu.last_kernel() == "k_tlp<walk>"
 
 
 def test_run_streams_pi_mm1_walk_replication(gpu, port):
