@@ -1135,7 +1135,9 @@ __device__ __forceinline__ void bs_prefetch(uint32_t* dst, const uint32_t* src, 
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-__global__ void __launch_bounds__(kBsPipeBlock) k_wlp_walk_bs_pipe(RepArgs a, const uint32_t* __restrict__ bseeds,
+// 6 blocks (12 warps) per SM: more warps hide the XOR chains' latency better than the
+// longer drain costs (4 blocks: 1.374 ms, 6: 1.348 ms at config 4; a few spilled bytes)
+__global__ void __launch_bounds__(kBsPipeBlock, 6) k_wlp_walk_bs_pipe(RepArgs a, const uint32_t* __restrict__ bseeds,
                                                                     int64_t groups, int64_t K) {
     __shared__ BsPipeWarp sh[kBsPipeBlock / 32];
     BsPipeWarp& E = sh[threadIdx.x >> 5];
