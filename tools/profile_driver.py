@@ -24,6 +24,8 @@ ap.add_argument("--repeat", type=int, default=2)
 ap.add_argument("--counters", action="store_true", help="instrumented kernels; print the SimReport tallies")
 ap.add_argument("--ir", action="store_true", help="run the reference's IR kernel on the GPU IR interpreter")
 ap.add_argument("--lambda", dest="lam", type=float, default=0.5)
+ap.add_argument("--wlp-variant", type=int, default=0)
+ap.add_argument("--tlp-variant", type=int, default=0)
 a = ap.parse_args()
 m = w.model_from_name(a.model)
 p = w.ModelParams(replications=a.R, draws=a.N, clients=a.N, steps=a.N, lambda_=a.lam)
@@ -39,9 +41,10 @@ rep = w.SimReport()
 ctx = w.hw_counters() if a.counters else None
 if ctx:
     ctx.__enter__()
-for _ in range(a.repeat):
-    w.run_shard(m, p, w.mode_from_name(a.mode), 42, 0, a.R, outs, on_device=True, report=rep)
+with w.wlp_variant(a.wlp_variant), w.tlp_variant(a.tlp_variant):
+    for _ in range(a.repeat):
+        w.run_shard(m, p, w.mode_from_name(a.mode), 42, 0, a.R, outs, on_device=True, report=rep)
 if ctx:
     ctx.__exit__(None, None, None)
 torch.cuda.synchronize()
-print(a.model, a.mode, a.R, a.N, "mean", float(outs[0].mean()), "report", rep)
+print(a.model, a.mode, a.R, a.N, "mean", float(outs[0].mean()), "kernel", w.last_kernel(), "report", rep)
