@@ -205,6 +205,14 @@ __device__ __forceinline__ int64_t warp_sum_i64(int64_t v) {
 // c = (double)chunks (rounded above 2^53, as there), fmod(fmod(px, c) + c, c). fmod is
 // exact in IEEE arithmetic on both sides; px is an exact integer (|px| <= steps).
 __device__ __forceinline__ double walk_fold(int64_t px, int64_t chunks) {
+    // For integers below 2^31 both fmods are exact integer remainders (fmod is exact, the
+    // operands are exact doubles, r + c is exact), and the result is never -0 (r + c > 0),
+    // so 32-bit remainders give the same value at a fraction of fmod's cost.
+    if (chunks > 0 && chunks <= 0x7FFFFFFF && px >= -0x7FFFFFFF && px <= 0x7FFFFFFF) {
+        const int32_t c = static_cast<int32_t>(chunks);
+        const int32_t r = static_cast<int32_t>(px) % c;  // sign of px, as fmod; |r| < c
+        return static_cast<double>(r < 0 ? r + c : r);    // (r + c) mod c
+    }
     const double c = static_cast<double>(chunks);
     return fmod(__dadd_rn(fmod(static_cast<double>(px), c), c), c);
 }
