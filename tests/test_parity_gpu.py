@@ -366,6 +366,19 @@ def test_pipeline_full_size_equals_lane_jumps(gpu, model, kw):
         assert np.array_equal(a, b)
 
 
+def test_walk_full_size_all_four_kernels_agree(gpu):
+    # config 4 walk through the per-replication WLP pipeline, the bitsliced WLP pipeline,
+    # the per-replication TLP and the bitsliced TLP: one array, bit for bit
+    p = gpu.ModelParams(replications=10_000_000, steps=1000, chunks=30)
+    runs = []
+    for wv, tv, mode in ((2, 0, gpu.ExecutionMode.Wlp), (3, 0, gpu.ExecutionMode.Wlp), (0, 1, gpu.ExecutionMode.Tlp),
+                         (0, 2, gpu.ExecutionMode.Tlp)):
+        with gpu.wlp_variant(wv), gpu.tlp_variant(tv):
+            runs.append(_device_run(gpu, 2, p, mode, 42)[0])
+    for r in runs[1:]:
+        assert np.array_equal(r, runs[0])
+
+
 def test_randomized_configurations_all_kernels_vs_oracle(gpu, port):
     # 150 random small configurations: every model, mode and WLP kernel variant, ragged
     # unit counts, rates that are / are not powers of two, light to overloaded queues
