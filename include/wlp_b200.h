@@ -125,8 +125,10 @@ int wlp_set_hw_counters(int enable);
  * chunk; mm1: segment chaining by fixed-point rounds); 2 = warp pipeline (replications
  * move lane to lane, each lane runs its segment in order from the state its neighbour
  * hands over; a 31-step drain per warp); 3 = walk: bitsliced warp pipeline (each pipeline
- * slot carries 32 replications as bit planes; chosen automatically for large R; other
- * models treat 3 as 0). Outputs are identical; only speed differs. */
+ * slot carries 32 replications as bit planes); 4 = walk: bitsliced lane chunks (a warp per
+ * group of 32 replications, each lane jumps all 32 to its chunk). The walk picks 3 / 4 /
+ * per-replication automatically by R; pi and mm1 treat 3 and 4 as 0. Outputs are
+ * identical; only speed differs. */
 int wlp_set_wlp_variant(int variant);
 
 /* The same for the TLP (thread-level) mapping: 0 = automatic (default: one thread per

@@ -498,8 +498,8 @@ def walk_replication(steps: int, chunks: int, stream: RngState) -> float:
 
 class wlp_variant:
     """Context manager selecting the WLP kernel for calls on this thread: 0 automatic,
-    1 lane jumps, 2 warp pipeline, 3 walk bitsliced warp pipeline (outputs identical;
-    wlp_set_wlp_variant)."""
+    1 lane jumps, 2 warp pipeline, 3 walk bitsliced warp pipeline, 4 walk bitsliced lane
+    chunks (outputs identical; wlp_set_wlp_variant)."""
 
     def __init__(self, variant: int):
         self.variant = int(variant)

@@ -1264,6 +1264,77 @@ __global__ void __launch_bounds__(kBsPipeBlock, 6) k_wlp_walk_bs_pipe(RepArgs a,
     flush(nemit);
 }
 
+// ---------------------------------------------------------------------------------
+// Walk WLP, bitsliced lane chunks: one warp per group of 32 replications, lane l runs
+// steps [l*K, (l+1)*K) of all 32 (as k_wlp_lanes does for one replication). Each lane
+// jumps the 32 seeds to its chunk (lane_jump, nibble tables in shared memory), transposes
+// them into bit planes, walks its chunk with the carry-save counters (all lanes run the
+// same ceil(K/16) blocks; steps past a lane's chunk are masked out of the counts and its
+// end state is never used), turns the counts into per-stream dx and the warp sums them
+// over lanes with a 31-shuffle transpose-reduce that leaves stream j's total in lane j,
+// which folds and stores it (coalesced). No drain: a warp per group from the first step,
+// so it suits R too small for the pipeline (config 3). Chunk counts < 2^16: K < 65536.
+// ---------------------------------------------------------------------------------
+constexpr int kBsLanesBlock = 128;  // 2 blocks (8 warps) per SM at ~250 registers
+
+__global__ void __launch_bounds__(kBsLanesBlock, 2) k_wlp_walk_bs_lanes(RepArgs a, const uint32_t* __restrict__ gtab,
+                                                                    int64_t K) {
+    extern __shared__ uint32_t tab[];  // kLaneTabWords
+    stage_u32<kLaneTabWords>(tab, gtab);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    int64_t mine = a.n - static_cast<int64_t>(lane) * K;
+    mine = mine < 0 ? 0 : (mine > K ? K : mine);
+    const uint32_t units = static_cast<uint32_t>(mine);
+    const uint32_t blocks = static_cast<uint32_t>((K + 15) / 16);
+    const int64_t groups = (a.count + 31) / 32;
+    RepArgs ga = a;
+    ga.count = groups;
+    for (int64_t g = grab_take(grab_issue(ga, lane)); g < groups;) {
+        const unsigned long long ticket = grab_issue(ga, lane);
+        const int64_t gend = g + a.grab < groups ? g + a.grab : groups;
+        for (; g < gend; ++g) {
+            BsTaus t;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {  // every lane reads the same 32 seeds (broadcast)
+                const int64_t r = g * 32 + j;
+                const Taus st = lane_jump(tab, lane, r < a.count ? load_seed(a, r) : Taus{kMin1, kMin2, kMin3});
+                t.b1[j] = st.s1;
+                t.b2[j] = st.s2;
+                t.b3[j] = st.s3;
+            }
+            transpose32(t.b1);
+            transpose32(t.b2);
+            transpose32(t.b3);
+            BsCount P, Q;
+            bs_count_init(P);
+            bs_count_init(Q);
+            bs_walk_units(t, P, Q, units, blocks);
+            uint32_t pv[32], qv[32];
+            bs_count_values(P, pv);
+            bs_count_values(Q, qv);
+            int32_t v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = static_cast<int32_t>(pv[j]) - static_cast<int32_t>(qv[j]);
+            // transpose-reduce: after the round with offset s, slot k of lane l stands for
+            // stream k + (the lane bits above s already folded in); lane j ends with stream j
+#pragma unroll
+            for (int s = 16; s >= 1; s >>= 1) {
+                const bool up = (lane & s) != 0;
+#pragma unroll
+                for (int k = 0; k < s; ++k) {
+                    const int32_t send = up ? v[k] : v[k + s];
+                    const int32_t keep = up ? v[k + s] : v[k];
+                    v[k] = keep + __shfl_xor_sync(kFull, send, s);
+                }
+            }
+            const int64_t r = g * 32 + lane;
+            if (r < a.count) a.out0[r] = walk_fold(v[0], a.chunks);
+        }
+        g = grab_take(ticket);
+    }
+}
+
 // mm1 thread per replication: each lane runs its own queue; the exponentials of 4
 // clients (8 draws) per lane go through the warp-cooperative batch log. Every thread of
 // a warp takes part in each batch up to the warp's longest replication (`n_warp`).
@@ -1842,6 +1913,14 @@ cudaError_t launch_wlp_walk_bs_pipe(const RepArgs& a, uint32_t* bseeds, int64_t 
     const int64_t groups = (a.count + 31) / 32;
     k_bs_seeds<<<static_cast<unsigned>((groups + kBsBlock - 1) / kBsBlock), kBsBlock, 0, st>>>(a, groups, bseeds);
     k_wlp_walk_bs_pipe<<<grid, kBsPipeBlock, 0, st>>>(a, bseeds, groups, K);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_wlp_walk_bs_lanes(const RepArgs& a, const uint32_t* lane_tab, int64_t K, int grid,
+                                     cudaStream_t st) {
+    if (a.count <= 0) return cudaSuccess;
+    allow_smem(k_wlp_walk_bs_lanes, kLaneTabWords * 4);
+    k_wlp_walk_bs_lanes<<<grid, kBsLanesBlock, kLaneTabWords * 4, st>>>(a, lane_tab, K);
     return cudaGetLastError();
 }
 

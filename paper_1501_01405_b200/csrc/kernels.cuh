@@ -130,6 +130,9 @@ cudaError_t launch_tlp_walk_bs(const RepArgs& a, cudaStream_t st);
 // scratch of 88 words per group; a.next zeroed, a.grab groups per grab.
 cudaError_t launch_wlp_walk_bs_pipe(const RepArgs& a, uint32_t* bseeds, int64_t K, int grid, cudaStream_t st);
 int wlp_walk_bs_pipe_blocks_per_sm();
+// Walk WLP, bitsliced lane chunks: a warp per group of 32 replications (K < 65536; lane
+// jump table of stride 2K draws; a.next zeroed, a.grab groups per grab).
+cudaError_t launch_wlp_walk_bs_lanes(const RepArgs& a, const uint32_t* lane_tab, int64_t K, int grid, cudaStream_t st);
 constexpr int kBsPipeBlock = 64;  // threads per block of the bitsliced walk pipeline
 // Plan: batched seeding (specials carry the job index in `pad`), then one model launch.
 cudaError_t launch_seed_jobs(const uint32_t* powers, const SeedJob* d_jobs, int n_jobs, int64_t total_blocks,

@@ -425,6 +425,23 @@ int wlp_grid(DevCtx& c, int model, int64_t count) {
     return static_cast<int>(std::max<int64_t>(1, std::min(cap, need)));
 }
 
+// Which WLP walk kernel (wlp_set_wlp_variant numbering): 3 bitsliced pipeline, 4 bitsliced
+// lane chunks, 0 the per-replication kernels. Automatic: the pipeline once every resident
+// warp gets 8 or more groups of 32 replications (its 31-step drain is then small; R >=
+// ~3.8e5 on 148 SMs), lane chunks from one group per SM up to there (config 3, R = 1e5:
+// 0.053 ms against 0.143 per replication), per replication below that or when the
+// counts could pass 2^16 per chunk.
+int walk_bs_choice(const DevCtx& c, int64_t count, int64_t n) {
+    const bool pipe_ok = n < 65536, lanes_ok = (n + 31) / 32 < 65536;
+    if (g_wlp_variant == 3) return pipe_ok ? 3 : 0;
+    if (g_wlp_variant == 4) return lanes_ok ? 4 : 0;
+    if (g_wlp_variant != 0) return 0;
+    const int64_t groups = (count + 31) / 32;
+    if (pipe_ok && groups >= 8 * static_cast<int64_t>(c.sms) * c.bs_pipe_bps * (kBsPipeBlock / 32)) return 3;
+    if (lanes_ok && groups >= c.sms) return 4;
+    return 0;
+}
+
 // Launch the model over d_seeds (count replications). Async.
 int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_block, const uint32_t* d_seeds,
                 int64_t count, double* o0, double* o1, double* o2, cudaStream_t st, int& grid_out) {
@@ -486,14 +503,20 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
             g_last_kernel = "k_wlp_mm1";
             WLP_CUDA(launch_wlp(model, a, c.mm1_lane.p, c.mm1_skip.p, 0, grid_out, st));
         }
-    } else if (model == WLP_MODEL_WALK && !g_hw_counters && a.n < 65536 &&
-               (g_wlp_variant == 3 ||
-                (g_wlp_variant == 0 &&
-                 (count + 31) / 32 >= 8 * static_cast<int64_t>(c.sms) * c.bs_pipe_bps * (kBsPipeBlock / 32)))) {
+    } else if (model == WLP_MODEL_WALK && !g_hw_counters && walk_bs_choice(c, count, a.n) == 4) {
+        // bitsliced lane chunks: a warp per group of 32 replications
+        const int64_t groups = (count + 31) / 32;
+        const int64_t K = (a.n + 31) / 32;
+        const int64_t cap = static_cast<int64_t>(c.sms) * 2;  // 2 blocks of 4 warps per SM
+        grid_out = static_cast<int>(std::clamp<int64_t>((groups + 3) / 4, 1, cap));
+        a.grab = static_cast<int>(std::clamp<int64_t>(groups / (4 * grid_out * 8), 1, 32));
+        const uint32_t* tab = nullptr;
+        WLP_TRY(lane_table(c, 2ull * static_cast<uint64_t>(K), tab));
+        g_last_kernel = "k_wlp_walk_bs_lanes";
+        WLP_CUDA(launch_wlp_walk_bs_lanes(a, tab, K, grid_out, st));
+    } else if (model == WLP_MODEL_WALK && !g_hw_counters && walk_bs_choice(c, count, a.n) == 3) {
         // bitsliced pipeline: groups of 32 replications; at least ~64 groups per warp so
-        // the 31-step drain stays small. Automatic once every resident warp gets 8 or more
-        // groups (R >= ~3.8e5 on 148 SMs); below that the per-replication kernels win
-        // (config 3, R = 1e5: 0.143 vs 0.293 ms).
+        // the 31-step drain stays small (walk_bs_choice)
         const int64_t groups = (count + 31) / 32;
         const int64_t warps_want = std::max<int64_t>(1, groups / 64);
         const int64_t cap = static_cast<int64_t>(c.sms) * c.bs_pipe_bps;
@@ -632,7 +655,7 @@ const char* wlp_last_error(void) { return g_err.c_str(); }
 int wlp_version(void) { return 1; }
 
 int wlp_set_wlp_variant(int variant) {
-    if (variant < 0 || variant > 3) return fail(WLP_EDOMAIN, "wlp variant must be 0 (auto), 1, 2 or 3");
+    if (variant < 0 || variant > 4) return fail(WLP_EDOMAIN, "wlp variant must be 0 (auto), 1, 2, 3 or 4");
     g_wlp_variant = variant;
     return WLP_OK;
 }

@@ -149,14 +149,17 @@ def test_walk_bitsliced_tlp_matches_oracle(gpu, port, R, steps):
     assert np.array_equal(run.outputs["out"], want["out"])
 
 
+@pytest.mark.parametrize("variant", [3, 4], ids=["pipeline", "lane-chunks"])
 @pytest.mark.parametrize("R,steps", [(1, 1), (33, 17), (64, 16), (100, 1000), (5000, 333), (70, 40_000),
-                                     (40, 65_535), (3000, 511)])
-def test_walk_bitsliced_wlp_pipeline_matches_oracle(gpu, port, R, steps):
-    # groups of 32 replications move lane to lane as bit planes; lane chunks are whole
-    # 16-step blocks with the steps past a group's end masked out of the counts
+                                     (40, 65_535), (3000, 511), (50, 100_000)])
+def test_walk_bitsliced_wlp_matches_oracle(gpu, port, R, steps, variant):
+    # 3: groups of 32 replications move lane to lane as bit planes, lane chunks of whole
+    # 16-step blocks with the steps past a group's end masked out of the counts;
+    # 4: a warp per group, every lane jumps the 32 streams to its chunk and the counts are
+    # summed over lanes by a transpose-reduce (n = 100000: the pipeline's fallback)
     p = gpu.ModelParams(replications=R, steps=steps, chunks=3 + R % 29)
     want = port.run_model(2, oracle.params_from(p), 4321 + R)
-    with gpu.wlp_variant(3):
+    with gpu.wlp_variant(variant):
         run = gpu.run_model(gpu.ModelKind.Walk, p, gpu.ExecutionMode.Wlp, master_seed=4321 + R)
     assert np.array_equal(run.outputs["out"], want["out"])
 
@@ -171,6 +174,9 @@ def test_walk_wlp_auto_picks_the_bitsliced_pipeline_at_large_R(gpu, port):
     small = gpu.ModelParams(replications=1000, steps=100, chunks=30)
     gpu.run_model(gpu.ModelKind.Walk, small, gpu.ExecutionMode.Wlp, master_seed=42)
     assert gpu.last_kernel() in ("k_wlp_lanes<walk>", "k_wlp_pipe<walk>")
+    mid = gpu.ModelParams(replications=100_000, steps=1000, chunks=30)
+    gpu.run_model(gpu.ModelKind.Walk, mid, gpu.ExecutionMode.Wlp, master_seed=42)
+    assert gpu.last_kernel() == "k_wlp_walk_bs_lanes"
     gpu.run_model(gpu.ModelKind.Walk, small, gpu.ExecutionMode.Tlp, master_seed=42)
     assert gpu.last_kernel() == "k_tlp<walk>"
 
@@ -366,13 +372,13 @@ def test_pipeline_full_size_equals_lane_jumps(gpu, model, kw):
         assert np.array_equal(a, b)
 
 
-def test_walk_full_size_all_four_kernels_agree(gpu):
-    # config 4 walk through the per-replication WLP pipeline, the bitsliced WLP pipeline,
-    # the per-replication TLP and the bitsliced TLP: one array, bit for bit
+def test_walk_full_size_all_five_kernels_agree(gpu):
+    # config 4 walk through the per-replication WLP pipeline, the bitsliced WLP pipeline and
+    # lane chunks, the per-replication TLP and the bitsliced TLP: one array, bit for bit
     p = gpu.ModelParams(replications=10_000_000, steps=1000, chunks=30)
     runs = []
-    for wv, tv, mode in ((2, 0, gpu.ExecutionMode.Wlp), (3, 0, gpu.ExecutionMode.Wlp), (0, 1, gpu.ExecutionMode.Tlp),
-                         (0, 2, gpu.ExecutionMode.Tlp)):
+    for wv, tv, mode in ((2, 0, gpu.ExecutionMode.Wlp), (3, 0, gpu.ExecutionMode.Wlp), (4, 0, gpu.ExecutionMode.Wlp),
+                         (0, 1, gpu.ExecutionMode.Tlp), (0, 2, gpu.ExecutionMode.Tlp)):
         with gpu.wlp_variant(wv), gpu.tlp_variant(tv):
             runs.append(_device_run(gpu, 2, p, mode, 42)[0])
     for r in runs[1:]:
@@ -394,7 +400,7 @@ def test_randomized_configurations_all_kernels_vs_oracle(gpu, port):
         seed = int(rng.integers(0, 2**63))
         want = port.run_model(model, oracle.params_from(p), seed)
         mode = gpu.ExecutionMode(int(rng.integers(0, 3)))
-        variant = int(rng.integers(0, 4))
+        variant = int(rng.integers(0, 5))
         with gpu.wlp_variant(variant), gpu.tlp_variant(min(variant, 2)):
             run = gpu.run_model(gpu.ModelKind(model), p, mode, master_seed=seed,
                                 tlp_block_size=int(rng.choice([32, 50, 128, 256])))
