@@ -43,6 +43,22 @@ def test_compute_without_gpu_fails_loudly():
         w.run_model(w.ModelKind.Pi, w.ModelParams(replications=2, draws=10), w.ExecutionMode.Wlp, master_seed=1)
 
 
+def test_kernel_variant_knobs_and_last_kernel():
+    # host-side setters: ranges checked, reset by the context managers; no run yet on this
+    # thread, so no kernel name
+    for bad in (-1, 5):
+        with pytest.raises(w.DomainError):
+            with w.wlp_variant(bad):
+                pass
+    for bad in (-1, 3):
+        with pytest.raises(w.DomainError):
+            with w.tlp_variant(bad):
+                pass
+    with w.wlp_variant(4), w.tlp_variant(2):
+        pass
+    assert isinstance(w.last_kernel(), str)
+
+
 def test_validate_params_matches_reference_semantics():
     P = w.ModelParams
     assert w.validate_params(w.ModelKind.Pi, P()) is None
