@@ -340,21 +340,22 @@ struct Queue {
 // ---------------------------------------------------------------------------------
 
 // One block of stream slots of one random_spacing run: slots [blk*B, (blk+1)*B) of
-// `count` (B = kSeedBlock * kSeedPerThread), slot i = candidate c(slot_begin + i) after
+// `count` (B = kSeedBlock * PER), slot i = candidate c(slot_begin + i) after
 // the sorted rejection list; keys land SoA at out[plane*stride + out_off + i].
+template <int PER>
 __device__ __forceinline__ void seed_block(const uint32_t* __restrict__ pw, Taus master, int64_t slot_begin,
                                            int64_t count, int64_t blk, const int64_t* __restrict__ rejected,
                                            int64_t n_rejected, uint32_t* __restrict__ out, int64_t out_off,
                                            int64_t stride, SpecialRec* specials, int64_t special_cap,
                                            unsigned long long* n_special, uint32_t job) {
-    extern __shared__ uint32_t sh[];  // 3 x [kSeedBlock][33] (padded: conflict-free)
-    constexpr int kRow = kSeedPerThread + 1;
+    extern __shared__ uint32_t sh[];  // 3 x [kSeedBlock][PER + 1] (padded: conflict-free)
+    constexpr int kRow = PER + 1;
     constexpr int kPlane = kSeedBlock * kRow;
     const int tid = threadIdx.x;
-    const int64_t blk0 = blk * kSeedBlock * kSeedPerThread;
-    const int64_t my0 = blk0 + static_cast<int64_t>(tid) * kSeedPerThread;
+    const int64_t blk0 = blk * kSeedBlock * PER;
+    const int64_t my0 = blk0 + static_cast<int64_t>(tid) * PER;
     const int64_t left = count - my0;
-    const int nmine = left <= 0 ? 0 : (left < kSeedPerThread ? static_cast<int>(left) : kSeedPerThread);
+    const int nmine = left <= 0 ? 0 : (left < PER ? static_cast<int>(left) : PER);
     if (nmine > 0) {
         int64_t c = slot_begin + my0;  // candidate index of my first slot
         int64_t ri = 0;
@@ -394,17 +395,18 @@ __device__ __forceinline__ void seed_block(const uint32_t* __restrict__ pw, Taus
     }
     __syncthreads();
     int64_t nblk = count - blk0;
-    if (nblk > kSeedBlock * kSeedPerThread) nblk = kSeedBlock * kSeedPerThread;
+    if (nblk > kSeedBlock * PER) nblk = kSeedBlock * PER;
     for (int i = tid; i < nblk; i += kSeedBlock) {
-        const int si = (i / kSeedPerThread) * kRow + (i % kSeedPerThread);
+        const int si = (i / PER) * kRow + (i % PER);
         out[out_off + blk0 + i] = sh[si];
         out[stride + out_off + blk0 + i] = sh[kPlane + si];
         out[2 * stride + out_off + blk0 + i] = sh[2 * kPlane + si];
     }
 }
 
+template <int PER>
 __global__ void __launch_bounds__(kSeedBlock) k_seed(SeedArgs a) {
-    seed_block(a.powers, a.master, a.slot_begin, a.count, blockIdx.x, a.rejected, a.n_rejected, a.out, a.out_off,
+    seed_block<PER>(a.powers, a.master, a.slot_begin, a.count, blockIdx.x, a.rejected, a.n_rejected, a.out, a.out_off,
                a.stride ? a.stride : a.count,
                static_cast<SpecialRec*>(a.specials), a.special_cap, a.n_special, 0u);
 }
@@ -424,7 +426,7 @@ __global__ void __launch_bounds__(kSeedBlock) k_seed_jobs(const uint32_t* __rest
             hi = mid - 1;
     }
     const SeedJob& J = jobs[lo];
-    seed_block(pw, J.master, 0, J.count, blockIdx.x - J.block0, nullptr, 0, out, J.out_off, total, specials,
+    seed_block<kSeedJobPer>(pw, J.master, 0, J.count, blockIdx.x - J.block0, nullptr, 0, out, J.out_off, total, specials,
                special_cap, n_special, static_cast<uint32_t>(lo));
 }
 
@@ -1762,18 +1764,25 @@ int tlp_blocks_per_sm(int model, int block) {
     return nb < 1 ? 1 : nb;
 }
 
+// Slots per thread by run size: a thread's cost is one jump-ahead (a chain of dependent
+// table lookups) plus its slots, so large runs amortise the jump over 128 slots
+// (R = 1e7: 0.155 ms against 0.245 ms at 32) while small runs want threads (R = 1e5: 25
+// blocks at 128).
+template <int PER>
+cudaError_t launch_seed_per(const SeedArgs& a, cudaStream_t st) {
+    const int64_t per_block = static_cast<int64_t>(kSeedBlock) * PER;
+    const int64_t grid = (a.count + per_block - 1) / per_block;
+    const size_t smem = 3 * kSeedBlock * (PER + 1) * 4;
+    allow_smem(k_seed<PER>, smem);
+    k_seed<PER><<<static_cast<unsigned>(grid), kSeedBlock, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_seed(const SeedArgs& a, cudaStream_t st) {
     if (a.count <= 0) return cudaSuccess;
-    const int64_t per_block = static_cast<int64_t>(kSeedBlock) * kSeedPerThread;
-    const int64_t grid = (a.count + per_block - 1) / per_block;
-    const size_t smem = 3 * kSeedBlock * (kSeedPerThread + 1) * 4;
-    static bool attr = false;
-    if (!attr) {
-        allow_smem(k_seed, smem);
-        attr = true;
-    }
-    k_seed<<<static_cast<unsigned>(grid), kSeedBlock, smem, st>>>(a);
-    return cudaGetLastError();
+    if (a.count >= (int64_t(1) << 22)) return launch_seed_per<128>(a, st);
+    if (a.count >= (int64_t(1) << 18)) return launch_seed_per<32>(a, st);
+    return launch_seed_per<8>(a, st);
 }
 
 cudaError_t launch_neg_log1m(const uint32_t* k, int64_t n, double* out, cudaStream_t st) {
@@ -1948,7 +1957,7 @@ cudaError_t launch_seed_jobs(const uint32_t* powers, const SeedJob* d_jobs, int 
                              int64_t total_slots, uint32_t* out, void* specials, int64_t special_cap,
                              unsigned long long* n_special, cudaStream_t st) {
     if (total_blocks <= 0) return cudaSuccess;
-    const size_t smem = 3 * kSeedBlock * (kSeedPerThread + 1) * 4;
+    const size_t smem = 3 * kSeedBlock * (kSeedJobPer + 1) * 4;
     allow_smem(k_seed_jobs, smem);
     k_seed_jobs<<<static_cast<unsigned>(total_blocks), kSeedBlock, smem, st>>>(
         powers, d_jobs, n_jobs, out, total_slots, static_cast<SpecialRec*>(specials), special_cap, n_special);

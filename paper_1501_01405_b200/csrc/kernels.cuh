@@ -94,9 +94,8 @@ constexpr int kPlanT = 32;          // pi/walk plan kernels: units per lane per 
 constexpr int kWlpBlock = 512;     // pi / walk WLP block (16 warps; 3 blocks = 48 warps per SM)
 constexpr int kMm1Block = 256;     // mm1 WLP block (8 warps)
 constexpr int kMm1PanelT = 8;      // mm1: clients per lane per panel
-constexpr int kSeedBlock = 32;       // seeding: 32 threads x 128 slots per block; fewer, longer
-                                   // threads amortise the jump-ahead (1e7: 0.245 -> 0.155 ms)
-constexpr int kSeedPerThread = 128;
+constexpr int kSeedBlock = 32;     // seeding threads per block (slots per thread by run size)
+constexpr int kSeedJobPer = 8;     // slots per thread of the plan seeding (small runs)
 
 // Layout of wlp_special (include/wlp_b200.h).
 struct SpecialRec {

@@ -1034,7 +1034,7 @@ int wlp_run_plan(int model, const wlp_params* sets, const uint64_t* master_seeds
     std::vector<SeedJob> jobs(n_sets);
     int64_t R = 0, blocks = 0;
     bool all_rcp = true;
-    const int64_t per_block = static_cast<int64_t>(kSeedBlock) * kSeedPerThread;
+    const int64_t per_block = static_cast<int64_t>(kSeedBlock) * kSeedJobPer;
     for (int k = 0; k < n_sets; ++k) {
         WLP_TRY(validate(model, &sets[k], nullptr));
         const int64_t n = units_of(model, sets[k]);
