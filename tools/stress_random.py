@@ -2,7 +2,7 @@
 """Randomised stress of every model x mode x kernel variant against the oracle port
 (one-off, longer than the pytest suite's 150 configurations):
 
-    python tools/stress_random.py [seconds] [seed]
+    python tools/stress_random.py [seconds] [seed] [large_share]
 """
 import sys
 import time
@@ -16,13 +16,18 @@ import oracle  # noqa: E402
 import paper_1501_01405_b200 as w  # noqa: E402
 
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
+LARGE = float(sys.argv[3]) if len(sys.argv) > 3 else 0.0  # share of large-R configurations
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
 port = oracle.Oracle("port")
 t0, n, bad = time.time(), 0, 0
 while time.time() - t0 < budget:
     model = int(rng.integers(0, 3))
-    R = int(rng.choice([1, 7, 31, 32, 33, 63, 64, 65, 97, 128, 500, 1000, 4097, 6000]))
-    N = int(rng.choice([1, 2, 15, 16, 17, 31, 32, 33, 100, 255, 256, 257, 999, 1000, 2049, 4096, 5000]))
+    if rng.random() < LARGE:  # large R with few units: the walk's pipeline / lane-chunk switch
+        R = int(rng.choice([100_000, 150_001, 400_000, 700_003, 1_000_000]))
+        N = int(rng.choice([1, 16, 17, 33, 64, 100]))
+    else:
+        R = int(rng.choice([1, 7, 31, 32, 33, 63, 64, 65, 97, 128, 500, 1000, 4097, 6000]))
+        N = int(rng.choice([1, 2, 15, 16, 17, 31, 32, 33, 100, 255, 256, 257, 999, 1000, 2049, 4096, 5000]))
     chunks = int(rng.choice([1, 2, 3, 30, 97, 1 << 20, (1 << 31) + 5, (1 << 53) + 3]))
     lam = float(rng.choice([0.125, 0.3, 0.5, 0.7, 0.9, 0.99, 1.5, 2.0]))
     mu = float(rng.choice([0.5, 1.0, 1.3, 0.9]))
