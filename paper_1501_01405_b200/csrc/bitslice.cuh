@@ -79,6 +79,32 @@ TAUS_HD void bs_walk_step(BsTaus& t, uint32_t& plus, uint32_t& minus) {
     bs_step(t);
 }
 
+// The live bit planes of a group (b1[1..31], b2[3..31], b3[4..31]): the layout the
+// bitsliced walk pipeline feeds from.
+constexpr int kBsLive = 88;
+
+// Transposes 32 streams' words (t.bc[j] = component c of stream j) into bit planes and
+// stores the 88 live planes at out (16-byte aligned on the device).
+TAUS_HD void bs_store_planes(BsTaus& t, uint32_t* out) {
+    transpose32(t.b1);
+    transpose32(t.b2);
+    transpose32(t.b3);
+    uint32_t w[kBsLive];
+#pragma unroll
+    for (int i = 1; i < 32; ++i) w[i - 1] = t.b1[i];
+#pragma unroll
+    for (int i = 3; i < 32; ++i) w[31 + i - 3] = t.b2[i];
+#pragma unroll
+    for (int i = 4; i < 32; ++i) w[60 + i - 4] = t.b3[i];
+#if defined(__CUDA_ARCH__)
+    uint4* o = reinterpret_cast<uint4*>(out);
+#pragma unroll
+    for (int k = 0; k < kBsLive / 4; ++k) o[k] = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+#else
+    for (int k = 0; k < kBsLive; ++k) out[k] = w[k];
+#endif
+}
+
 // Carry-save adder over bitsliced words: (hi, lo) = a + b + c, per bit position.
 TAUS_HD void bs_csa(uint32_t& hi, uint32_t& lo, uint32_t a, uint32_t b, uint32_t c) {
     const uint32_t u = a ^ b;

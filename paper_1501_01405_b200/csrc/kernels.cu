@@ -347,7 +347,8 @@ __device__ __forceinline__ void seed_block(const uint32_t* __restrict__ pw, Taus
                                            int64_t count, int64_t blk, const int64_t* __restrict__ rejected,
                                            int64_t n_rejected, uint32_t* __restrict__ out, int64_t out_off,
                                            int64_t stride, SpecialRec* specials, int64_t special_cap,
-                                           unsigned long long* n_special, uint32_t job) {
+                                           unsigned long long* n_special, uint32_t job,
+                                           uint32_t* __restrict__ planes = nullptr) {
     extern __shared__ uint32_t sh[];  // 3 x [kSeedBlock][PER + 1] (padded: conflict-free)
     constexpr int kRow = PER + 1;
     constexpr int kPlane = kSeedBlock * kRow;
@@ -394,6 +395,22 @@ __device__ __forceinline__ void seed_block(const uint32_t* __restrict__ pw, Taus
         }
     }
     __syncthreads();
+    if (PER >= 32 && planes != nullptr) {  // the walk's bit planes, group by group (PER % 32 == 0)
+        for (int q = 0; q < PER / 32; ++q) {
+            const int64_t s0 = my0 + 32 * q;
+            if (s0 >= count) break;
+            BsTaus t;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const bool in = s0 + j < count;
+                const int si = tid * kRow + 32 * q + j;
+                t.b1[j] = in ? sh[si] : kMin1;
+                t.b2[j] = in ? sh[kPlane + si] : kMin2;
+                t.b3[j] = in ? sh[2 * kPlane + si] : kMin3;
+            }
+            bs_store_planes(t, planes + (s0 / 32) * kBsLive);
+        }
+    }
     int64_t nblk = count - blk0;
     if (nblk > kSeedBlock * PER) nblk = kSeedBlock * PER;
     for (int i = tid; i < nblk; i += kSeedBlock) {
@@ -408,7 +425,7 @@ template <int PER>
 __global__ void __launch_bounds__(kSeedBlock) k_seed(SeedArgs a) {
     seed_block<PER>(a.powers, a.master, a.slot_begin, a.count, blockIdx.x, a.rejected, a.n_rejected, a.out, a.out_off,
                a.stride ? a.stride : a.count,
-               static_cast<SpecialRec*>(a.specials), a.special_cap, a.n_special, 0u);
+               static_cast<SpecialRec*>(a.specials), a.special_cap, a.n_special, 0u, a.planes);
 }
 
 // Many independent runs (one per plan set) in one launch; block -> job by binary search.
@@ -983,14 +1000,6 @@ __device__ __forceinline__ void bs_load_component(const RepArgs& a, int comp, in
     __syncthreads();
 }
 
-__device__ __forceinline__ void bs_load_group(const RepArgs& a, int64_t g0, uint32_t* sm, BsTaus& t) {
-    bs_load_component(a, 0, g0, sm, t.b1);
-    bs_load_component(a, 1, g0, sm, t.b2);
-    bs_load_component(a, 2, g0, sm, t.b3);
-    transpose32(t.b1);
-    transpose32(t.b2);
-    transpose32(t.b3);
-}
 
 // Steps k of a 16-step block count only while k < valid (MASK; the masks fold into the
 // LOP3s that form them). Without MASK every step counts.
@@ -1114,24 +1123,17 @@ __global__ void __launch_bounds__(kBsBlock) k_tlp_walk_bs(RepArgs a) {
 // transposed once by k_bs_seeds; lane 31's finished counters collect in shared memory and
 // 32 groups are finalised at once (one per lane). Counts must stay below 2^16 (n < 65536).
 // ---------------------------------------------------------------------------------
-constexpr int kBsLive = 88;  // b1[1..31], b2[3..31], b3[4..31]
 
 __global__ void __launch_bounds__(kBsBlock) k_bs_seeds(RepArgs a, int64_t groups, uint32_t* __restrict__ out) {
     __shared__ uint32_t stage[kBsBlock * 33];
     const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     BsTaus t;
-    bs_load_group(a, static_cast<int64_t>(blockIdx.x) * blockDim.x, stage, t);
+    const int64_t g0 = static_cast<int64_t>(blockIdx.x) * blockDim.x;
+    bs_load_component(a, 0, g0, stage, t.b1);
+    bs_load_component(a, 1, g0, stage, t.b2);
+    bs_load_component(a, 2, g0, stage, t.b3);
     if (g >= groups) return;
-    uint32_t w[kBsLive];
-#pragma unroll
-    for (int i = 1; i < 32; ++i) w[i - 1] = t.b1[i];
-#pragma unroll
-    for (int i = 3; i < 32; ++i) w[31 + i - 3] = t.b2[i];
-#pragma unroll
-    for (int i = 4; i < 32; ++i) w[60 + i - 4] = t.b3[i];
-    uint4* o = reinterpret_cast<uint4*>(out + g * kBsLive);
-#pragma unroll
-    for (int k = 0; k < kBsLive / 4; ++k) o[k] = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+    bs_store_planes(t, out + g * kBsLive);
 }
 
 // A lane's chunk of its group: `blocks` 16-step carry-save blocks for every lane of the
@@ -1803,7 +1805,7 @@ cudaError_t launch_seed_per(const SeedArgs& a, cudaStream_t st) {
 cudaError_t launch_seed(const SeedArgs& a, cudaStream_t st) {
     if (a.count <= 0) return cudaSuccess;
     if (a.count >= (int64_t(1) << 22)) return launch_seed_per<128>(a, st);
-    if (a.count >= (int64_t(1) << 18)) return launch_seed_per<32>(a, st);
+    if (a.count >= (int64_t(1) << 18) || a.planes) return launch_seed_per<32>(a, st);  // planes: whole groups
     return launch_seed_per<8>(a, st);
 }
 
@@ -1939,10 +1941,12 @@ cudaError_t launch_tlp_walk_bs(const RepArgs& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_wlp_walk_bs_pipe(const RepArgs& a, uint32_t* bseeds, int64_t K, int grid, cudaStream_t st) {
+cudaError_t launch_wlp_walk_bs_pipe(const RepArgs& a, uint32_t* bseeds, int64_t K, int grid, cudaStream_t st,
+                                    bool planes_ready) {
     if (a.count <= 0) return cudaSuccess;
     const int64_t groups = (a.count + 31) / 32;
-    k_bs_seeds<<<static_cast<unsigned>((groups + kBsBlock - 1) / kBsBlock), kBsBlock, 0, st>>>(a, groups, bseeds);
+    if (!planes_ready)  // else the seeding kernel wrote them (SeedArgs::planes)
+        k_bs_seeds<<<static_cast<unsigned>((groups + kBsBlock - 1) / kBsBlock), kBsBlock, 0, st>>>(a, groups, bseeds);
     k_wlp_walk_bs_pipe<<<grid, kBsPipeBlock, 0, st>>>(a, bseeds, groups, K);
     return cudaGetLastError();
 }

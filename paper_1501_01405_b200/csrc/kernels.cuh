@@ -57,6 +57,9 @@ struct SeedArgs {
     unsigned long long* n_special;
     int64_t out_off = 0;
     int64_t stride = 0;  // 0: count
+    // optional: the walk's bit planes of each group of 32 slots (88 live words per group,
+    // the layout k_bs_seeds writes), so the bitsliced pipeline needs no separate pass
+    uint32_t* planes = nullptr;
 };
 
 // Experimental plan (BASELINE config 5): many factor-level sets in one launch.
@@ -128,7 +131,8 @@ cudaError_t launch_tlp(int model, const RepArgs& a, int tlp_block, cudaStream_t 
 cudaError_t launch_tlp_walk_bs(const RepArgs& a, cudaStream_t st);
 // Walk WLP, bitsliced warp pipeline (groups of 32 replications; n < 65536). bseeds:
 // scratch of 88 words per group; a.next zeroed, a.grab groups per grab.
-cudaError_t launch_wlp_walk_bs_pipe(const RepArgs& a, uint32_t* bseeds, int64_t K, int grid, cudaStream_t st);
+cudaError_t launch_wlp_walk_bs_pipe(const RepArgs& a, uint32_t* bseeds, int64_t K, int grid, cudaStream_t st,
+                                    bool planes_ready = false);
 int wlp_walk_bs_pipe_blocks_per_sm();
 // Walk WLP, bitsliced lane chunks: a warp per group of 32 replications (K < 65536; lane
 // jump table of stride 2K draws; a.next zeroed, a.grab groups per grab).

@@ -99,6 +99,8 @@ struct DevCtx {
     DevBuf<uint32_t> mm1_lane, mm1_skip;
     DevBuf<uint32_t> seeds, in_seeds;
     DevBuf<uint32_t> bseeds;  // walk bitsliced pipeline: group seed bit planes
+    const uint32_t* planes_of = nullptr;  // bseeds holds the planes of these seeds ...
+    int64_t planes_count = -1;            // ... (count), written by the last seed_async
     DevBuf<double> outs, partials, stats_in;
     DevBuf<SpecialRec> specials;
     DevBuf<unsigned long long> counter;
@@ -385,7 +387,7 @@ int spacing_rejections(std::vector<SpecialRec> sp, const std::vector<int64_t>& p
 
 // Seed slots [slot_begin, slot_begin+count) into d_out (SoA), async; specials counted.
 int seed_async(DevCtx& c, Taus master, int64_t slot_begin, int64_t count, const std::vector<int64_t>& rej,
-               uint32_t* d_out, cudaStream_t st) {
+               uint32_t* d_out, cudaStream_t st, bool planes = false) {
     if (!rej.empty()) {
         WLP_CUDA(c.rejected.ensure(static_cast<int64_t>(rej.size())));
         WLP_CUDA(cudaMemcpyAsync(c.rejected.p, rej.data(), rej.size() * 8, cudaMemcpyHostToDevice, st));
@@ -402,6 +404,14 @@ int seed_async(DevCtx& c, Taus master, int64_t slot_begin, int64_t count, const 
     a.specials = c.specials.p;
     a.special_cap = kSpecialCap;
     a.n_special = c.counter.p;
+    c.planes_of = nullptr;
+    c.planes_count = -1;
+    if (planes) {  // the walk's bitsliced pipeline follows: write its bit planes as well
+        WLP_CUDA(c.bseeds.ensure((count + 31) / 32 * 88));
+        a.planes = c.bseeds.p;
+        c.planes_of = d_out;
+        c.planes_count = count;
+    }
     WLP_CUDA(launch_seed(a, st));
     return WLP_OK;
 }
@@ -440,6 +450,12 @@ int walk_bs_choice(const DevCtx& c, int64_t count, int64_t n) {
     if (pipe_ok && groups >= 8 * static_cast<int64_t>(c.sms) * c.bs_pipe_bps * (kBsPipeBlock / 32)) return 3;
     if (lanes_ok && groups >= c.sms) return 4;
     return 0;
+}
+
+// Whether the seeding should also write the walk's bit planes (the bitsliced pipeline
+// will run, and then needs no separate transposition pass).
+bool walk_planes(const DevCtx& c, int model, int mode, const wlp_params& p, int64_t count) {
+    return model == WLP_MODEL_WALK && mode != WLP_MODE_TLP && !g_hw_counters && walk_bs_choice(c, count, p.steps) == 3;
 }
 
 // Launch the model over d_seeds (count replications). Async.
@@ -522,11 +538,12 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
         const int64_t cap = static_cast<int64_t>(c.sms) * c.bs_pipe_bps;
         grid_out = static_cast<int>(std::clamp<int64_t>((warps_want + 1) / 2, 1, cap));
         a.grab = static_cast<int>(std::clamp<int64_t>(groups / (2 * grid_out * 32), 1, 32));
-        WLP_CUDA(c.bseeds.ensure(groups * 88));
         // lane chunk: a multiple of 16 steps, so only a group's last chunk is partial
         const int64_t K = ((a.n + 31) / 32 + 15) / 16 * 16;
         g_last_kernel = "k_wlp_walk_bs_pipe";
-        WLP_CUDA(launch_wlp_walk_bs_pipe(a, c.bseeds.p, K, grid_out, st));
+        const bool ready = c.planes_of == d_seeds && c.planes_count == count;  // from the seeding
+        if (!ready) WLP_CUDA(c.bseeds.ensure(groups * 88));
+        WLP_CUDA(launch_wlp_walk_bs_pipe(a, c.bseeds.p, K, grid_out, st, ready));
     } else {
         const int64_t K = (a.n + 31) / 32;
         // Lane jumps cost ~80 instructions per lane per replication against K units of
@@ -934,7 +951,8 @@ int wlp_run_shard(int model, const wlp_params* p, int mode, uint64_t master_seed
         o2 = c->outs.p + 2 * r_count;
     }
     std::vector<int64_t> rej(rejected, rejected + n_rejected);
-    WLP_TRY(seed_async(*c, master_from_seed(master_seed), r_begin, r_count, rej, c->seeds.p, st));
+    WLP_TRY(seed_async(*c, master_from_seed(master_seed), r_begin, r_count, rej, c->seeds.p, st,
+                       walk_planes(*c, model, mode, *p, r_count)));
     int grid = 0;
     if (report) WLP_CUDA(cudaEventRecord(c->ev0, st));
     WLP_TRY(model_async(*c, model, *p, mode, tlp_block_size, c->seeds.p, r_count, o0, o1, o2, st, grid));
@@ -990,7 +1008,7 @@ int wlp_run(int model, const wlp_params* p, int mode, uint64_t master_seed, int 
     for (;;) {
         // Seeding and the model run back to back; the spacing check below only forces a
         // re-run when two special candidates actually share a key.
-        WLP_TRY(seed_async(*c, master, 0, R, rej, c->seeds.p, st));
+        WLP_TRY(seed_async(*c, master, 0, R, rej, c->seeds.p, st, walk_planes(*c, model, mode, *p, R)));
         if (report) WLP_CUDA(cudaEventRecord(c->ev0, st));
         WLP_TRY(model_async(*c, model, *p, mode, tlp_block_size, c->seeds.p, R, o0, o1, o2, st, grid));
         if (report) WLP_CUDA(cudaEventRecord(c->ev1, st));
