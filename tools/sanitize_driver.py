@@ -23,6 +23,14 @@ for model in (M.Pi, M.Mm1, M.Walk):
 # the warp pipelines at a size where auto selection picks them, and the instrumented kernels
 for model in (M.Pi, M.Mm1, M.Walk):
     w.run_model(model, w.ModelParams(replications=150_000, draws=40, clients=40, steps=40), E.Wlp, master_seed=5)
+# the walk's bitsliced kernels: lane chunks (auto), the pipeline with seeding-written planes
+# (auto at large R) and with its own plane pass (forced at small R), the bitsliced TLP
+w.run_model(M.Walk, w.ModelParams(replications=20_000, steps=100), E.Wlp, master_seed=5)
+w.run_model(M.Walk, w.ModelParams(replications=500_000, steps=20), E.Wlp, master_seed=5)
+with w.wlp_variant(3):
+    w.run_model(M.Walk, w.ModelParams(replications=3_000, steps=70), E.Wlp, master_seed=5)
+with w.tlp_variant(2):
+    w.run_model(M.Walk, w.ModelParams(replications=3_001, steps=70), E.Tlp, master_seed=5)
     with w.hw_counters():
         for mode in (E.Tlp, E.Wlp):
             w.run_model(model, w.ModelParams(replications=100, draws=300, clients=300, steps=300), mode, master_seed=5)
