@@ -1296,9 +1296,9 @@ __global__ void __launch_bounds__(kBsPipeBlock, 6) k_wlp_walk_bs_pipe(RepArgs a,
 // jumps the 32 seeds to its chunk (lane_jump, nibble tables in shared memory), transposes
 // them into bit planes, walks its chunk with the carry-save counters (all lanes run the
 // same ceil(K/16) blocks; steps past a lane's chunk are masked out of the counts and its
-// end state is never used), turns the counts into per-stream dx and the warp sums them
-// over lanes with a 31-shuffle transpose-reduce that leaves stream j's total in lane j,
-// which folds and stores it (coalesced). No drain: a warp per group from the first step,
+// end state is never used), and the warp sums the lanes' counts as bitsliced two's-
+// complement numbers by a butterfly of shuffles; lane j reads stream j's total, folds and
+// stores it (coalesced). No drain: a warp per group from the first step,
 // so it suits R too small for the pipeline (config 3). Chunk counts < 2^16: K < 65536.
 // ---------------------------------------------------------------------------------
 constexpr int kBsLanesBlock = 128;  // 2 blocks (8 warps) per SM at ~250 registers
@@ -1336,26 +1336,37 @@ __global__ void __launch_bounds__(kBsLanesBlock, 2) k_wlp_walk_bs_lanes(RepArgs 
             bs_count_init(P);
             bs_count_init(Q);
             bs_walk_units(t, P, Q, units, blocks);
-            uint32_t pv[32], qv[32];
-            bs_count_values(P, pv);
-            bs_count_values(Q, qv);
-            int32_t v[32];
+            // dx = P - Q summed over the lanes without leaving bit-plane form: D = P + ~Q + 1
+            // in 22-digit two's complement (|dx| <= n < 2^21), then a 5-round butterfly of
+            // bitsliced additions (every lane ends with the warp total of all 32 streams),
+            // then lane j reads stream j's digits: ~440 operations instead of two 32x32
+            // transposes and a transpose-reduce (~960).
+            constexpr int kD = 22;
+            uint32_t D[kD];
+            uint32_t carry = ~0u;  // the +1 of the negation, in every stream
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = static_cast<int32_t>(pv[j]) - static_cast<int32_t>(qv[j]);
-            // transpose-reduce: after the round with offset s, slot k of lane l stands for
-            // stream k + (the lane bits above s already folded in); lane j ends with stream j
+            for (int w = 0; w < kD; ++w) {
+                const uint32_t x = w < 16 ? P.c[w] : 0u, y = ~(w < 16 ? Q.c[w] : 0u);
+                D[w] = x ^ y ^ carry;
+                carry = (x & y) | (carry & (x ^ y));
+            }
 #pragma unroll
             for (int s = 16; s >= 1; s >>= 1) {
-                const bool up = (lane & s) != 0;
+                uint32_t c = 0u;
 #pragma unroll
-                for (int k = 0; k < s; ++k) {
-                    const int32_t send = up ? v[k] : v[k + s];
-                    const int32_t keep = up ? v[k + s] : v[k];
-                    v[k] = keep + __shfl_xor_sync(kFull, send, s);
+                for (int w = 0; w < kD; ++w) {
+                    const uint32_t o = __shfl_xor_sync(kFull, D[w], s);
+                    const uint32_t t = D[w] ^ o ^ c;
+                    c = (D[w] & o) | (c & (D[w] ^ o));
+                    D[w] = t;
                 }
             }
+            int32_t dx = 0;
+#pragma unroll
+            for (int w = 0; w < kD; ++w) dx |= static_cast<int32_t>((D[w] >> lane) & 1u) << w;
+            dx = (dx << (32 - kD)) >> (32 - kD);  // sign-extend from digit 21
             const int64_t r = g * 32 + lane;
-            if (r < a.count) a.out0[r] = walk_fold(v[0], a.chunks);
+            if (r < a.count) a.out0[r] = walk_fold(dx, a.chunks);
         }
         g = grab_take(ticket);
     }
