@@ -439,7 +439,7 @@ int wlp_grid(DevCtx& c, int model, int64_t count) {
 // lane chunks, 0 the per-replication kernels. Automatic: the pipeline once every resident
 // warp gets 8 or more groups of 32 replications (its 31-step drain is then small; R >=
 // ~3.8e5 on 148 SMs), lane chunks from one group per SM up to there (config 3, R = 1e5:
-// 0.053 ms against 0.143 per replication), per replication below that or when the
+// 0.051 ms against 0.143 per replication), per replication below that or when the
 // counts could pass 2^16 per chunk.
 int walk_bs_choice(const DevCtx& c, int64_t count, int64_t n) {
     const bool pipe_ok = n < 65536, lanes_ok = (n + 31) / 32 < 65536;
