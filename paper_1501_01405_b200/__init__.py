@@ -356,6 +356,11 @@ def plan_launch(replications: int, mode: ExecutionMode, prof: Optional[DevicePro
                 tlp_block_size: int = 256, grid_limit: int = 65535) -> LaunchPlan:
     """plan_launch (wlp.cpp:71-105), reference geometry and PlanError semantics."""
     prof = prof or DeviceProfile()
+    # the reference's check order (wlp.cpp:73-76); the C layer adds CUDA's 1024-thread limit
+    if replications < 1:
+        raise PlanError("plan_launch: need at least one replication")
+    if tlp_block_size < 1:
+        raise PlanError("plan_launch: tlp_block_size must be >= 1")
     if tlp_block_size > prof.maxThreadsPerBlock:
         raise PlanError("plan_launch: tlp_block_size exceeds maxThreadsPerBlock")
     cfg = _Cfg()

@@ -296,6 +296,10 @@ __device__ void run_ir_warp(const IrArgs& a, int64_t g, int lane, unsigned long 
                             ok = L.fault == 0;
                         }
                     }
+                    // the reference stores lane by lane in ascending order and throws at the
+                    // first faulting lane (warp_exec.cpp:255-265): lanes above it never store
+                    const uint32_t faulted = __ballot_sync(kFull, in && L.fault != 0);
+                    if (faulted && lane >= __ffs(static_cast<int>(faulted)) - 1) ok = false;
                     // lanes storing to one element: the highest lane's value lands last
                     // (the reference stores in ascending lane order)
                     const unsigned long long key = ok ? static_cast<unsigned long long>(idx)

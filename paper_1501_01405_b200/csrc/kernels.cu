@@ -1364,7 +1364,7 @@ __global__ void __launch_bounds__(kBsLanesBlock, 2) k_wlp_walk_bs_lanes(RepArgs 
             int32_t dx = 0;
 #pragma unroll
             for (int w = 0; w < kD; ++w) dx |= static_cast<int32_t>((D[w] >> lane) & 1u) << w;
-            dx = (dx << (32 - kD)) >> (32 - kD);  // sign-extend from digit 21
+            dx = static_cast<int32_t>(static_cast<uint32_t>(dx) << (32 - kD)) >> (32 - kD);  // sign-extend from digit 21
             const int64_t r = g * 32 + lane;
             if (r < a.count) a.out0[r] = walk_fold(dx, a.chunks);
         }

@@ -277,7 +277,10 @@ int validate(int model, const wlp_params* p, std::string* warning) {
 int plan(int64_t R, int mode, int tlp_block, int64_t grid_limit, wlp_launch_cfg* cfg, std::string* warning) {
     if (R < 1) return fail(WLP_EPLAN, "plan_launch: need at least one replication");
     if (tlp_block < 1) return fail(WLP_EPLAN, "plan_launch: tlp_block_size must be >= 1");
-    if (tlp_block > 1024) return fail(WLP_EPLAN, "plan_launch: tlp_block_size exceeds maxThreadsPerBlock");
+    // CUDA's hardware limit, checked after the reference's own checks (wlp.cpp:73-76); the
+    // profile's maxThreadsPerBlock is the C++ layer's (warpsim_api.cpp plan_launch)
+    if (tlp_block > 1024)
+        return fail(WLP_EPLAN, "plan_launch: tlp_block_size exceeds the device limit of 1024 threads per block");
     wlp_launch_cfg c{1, 1, 1, 1, 1, 32};
     if (mode == WLP_MODE_SEQUENTIAL) {
         c.warp_size = 1;
@@ -1274,6 +1277,26 @@ int ir_check(const wlp_ir_program& p) {
                 break;
             case WLP_IR_HALT: break;
             default: return bad("statement kind");
+        }
+    }
+    // The body ranges must form a tree: walked from the top range, every statement is
+    // reached at most once (a range containing its own IF/WHILE, or two overlapping
+    // ranges, reaches one twice) and nesting stays below kMaxNest, so the interpreter
+    // and the JIT generator's recursion (ir_jit.cu list()/stmt()) always terminate.
+    constexpr int kMaxNest = 1024;
+    std::vector<char> seen(p.n_stmts, 0);
+    struct Range { int b, e, depth; };
+    std::vector<Range> todo{{p.top_begin, p.top_end, 0}};
+    while (!todo.empty()) {
+        const Range r = todo.back();
+        todo.pop_back();
+        if (r.depth > kMaxNest) return bad("bodies nested deeper than " + std::to_string(kMaxNest));
+        for (int i = r.b; i < r.e; ++i) {
+            if (seen[i]) return bad("statement " + std::to_string(i) + " reached twice (body ranges overlap)");
+            seen[i] = 1;
+            const wlp_ir_stmt& st = p.stmts[i];
+            if (st.kind == WLP_IR_IF || st.kind == WLP_IR_WHILE) todo.push_back({st.b1_begin, st.b1_end, r.depth + 1});
+            if (st.kind == WLP_IR_IF) todo.push_back({st.b2_begin, st.b2_end, r.depth + 1});
         }
     }
     return WLP_OK;

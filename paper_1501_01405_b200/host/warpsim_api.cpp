@@ -143,7 +143,10 @@ std::vector<std::uint32_t> taus_stream(RngState& state, std::size_t n) {
 
 LaunchPlan plan_launch(std::int64_t replications, ExecutionMode mode, const DeviceProfile& prof, int tlp_block_size,
                        std::int64_t grid_limit) {
-    if (tlp_block_size > prof.maxThreadsPerBlock && tlp_block_size <= 1024)
+    // the reference's order (wlp.cpp:73-76); the C layer adds CUDA's 1024-thread limit
+    if (replications < 1) throw PlanError("plan_launch: need at least one replication");
+    if (tlp_block_size < 1) throw PlanError("plan_launch: tlp_block_size must be >= 1");
+    if (tlp_block_size > prof.maxThreadsPerBlock)
         throw PlanError("plan_launch: tlp_block_size exceeds maxThreadsPerBlock");
     wlp_launch_cfg c{};
     char warn[512];

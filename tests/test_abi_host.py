@@ -87,6 +87,19 @@ def test_plan_launch_matches_reference(ref, mode):
         w.plan_launch(0, w.ExecutionMode.Tlp)
 
 
+def test_plan_launch_check_order():
+    """wlp.cpp:73-76: replications, then the block's lower bound, then the profile limit."""
+    with pytest.raises(w.PlanError, match="at least one replication"):
+        w.plan_launch(0, w.ExecutionMode.Tlp, tlp_block_size=4096)
+    with pytest.raises(w.PlanError, match=">= 1"):
+        w.plan_launch(5, w.ExecutionMode.Tlp, w.DeviceProfile(maxThreadsPerBlock=16), tlp_block_size=0)
+    with pytest.raises(w.PlanError, match="maxThreadsPerBlock"):
+        w.plan_launch(5, w.ExecutionMode.Tlp, w.DeviceProfile(maxThreadsPerBlock=64), tlp_block_size=128)
+    # a profile above CUDA's limit: the device limit, reported as such
+    with pytest.raises(w.PlanError, match="device limit"):
+        w.plan_launch(5, w.ExecutionMode.Tlp, w.DeviceProfile(maxThreadsPerBlock=4096), tlp_block_size=2048)
+
+
 def test_master_from_seed_and_make_state(port):
     for seed in [0, 1, 42, 9001, 20260201, 2**64 - 1]:
         assert tuple(vars(w.rng_state_from_seed(seed)).values()) == port.master_from_seed(seed)

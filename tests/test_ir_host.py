@@ -141,6 +141,11 @@ def test_c_abi_rejects_malformed_flattened_programs():
         ([(3, -1, -1, 0, -1, 0, 5, 0, 0, 0)], [OP_CONST, 1, 0, OP_END]),          # body range past the end
         ([(2, 0, -1, 0, 0, 0, 0, 0, 0, 0)], [OP_CONST, 1, 0, OP_END]),            # store to a scalar param
         ([(7, 0, -1, 0, -1, 0, 0, 0, 0, 0)], [OP_CONST, 1, 0, OP_END]),           # unknown statement kind
+        ([(4, -1, -1, 0, -1, 0, 1, 0, 0, 0)], [OP_CONST, 1, 0, OP_END]),          # WHILE whose body holds itself
+        ([(3, -1, -1, 0, -1, 1, 2, 1, 2, 0), (5, -1, -1, -1, -1, 0, 0, 0, 0, 0)],  # then and else overlap
+         [OP_CONST, 1, 0, OP_END]),
+        ([(3, -1, -1, 0, -1, 1, 2, 0, 0, 0), (4, -1, -1, 0, -1, 0, 1, 0, 0, 0)],  # IF -> WHILE -> IF cycle
+         [OP_CONST, 1, 0, OP_END]),
     ]
     need = C.c_int(0)
     p, keep = prog(*good)
