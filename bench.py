@@ -1,46 +1,49 @@
 #!/usr/bin/env python3
 """Benchmark of the MRIP replication runner (BASELINE.json metric: replications/sec per
-model on 1/2/4/8 B200, with warp-exec efficiency / ALU-issue fraction from ncu).
+model on 1/2/4/8 B200, with the warp-exec / ALU-issue evidence).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
 
-Workload (a "step"): BASELINE config 2 — Monte-Carlo pi, 10^6 replications x 10^4 draws
+With --gpus N > 1 outside torchrun, bench.py re-launches itself under
+`torch.distributed.run` with N ranks (one per GPU, NCCL, 127.0.0.1); under torchrun it
+checks WORLD_SIZE == N. `--dry-run` brings the ranks up over gloo on CPU and exercises
+only that launch / barrier / max-over-ranks plumbing (tests/test_bench_launch.py).
+
+Headline (a "step"): BASELINE config 2 — Monte-Carlo pi, 10^6 replications x 10^4 draws
 per GPU (weak scaling: rank g runs slots [g*10^6, (g+1)*10^6) of one run of N*10^6
-replications), master seed 42, WLP mapping: exact random-spacing seeding on device +
-the WLP replication kernel + the two-pass device statistics of the outputs, merged
-across ranks (all_gather of sufficient statistics), -> mean / 95% CI.
+replications), master seed 42, WLP: exact random-spacing seeding on device + the WLP
+replication kernel + the two-pass device statistics, merged across ranks (all_gather of
+sufficient statistics) -> mean / 95% CI.
 
-  value  device-resident: outputs stay in HBM, CUDA events on the launching stream over
-         exactly K steps after W warm-ups, barrier + synchronize on both sides, max over
-         ranks. Inputs (the replications' 12-byte stream seeds) are generated in the step.
-         The 8 MB output per GPU and the 120 MB of seeds are far below L2 capacity
-         reuse distance: every step rewrites them (config "l2": "inputs regenerated").
+  value  device-resident: CUDA events on the launching stream over exactly K steps after
+         W warm-ups, barrier + synchronize on both sides, max over ranks. The step's
+         inputs (12-byte stream keys per replication) are generated in the step and its
+         outputs (8 B per replication) rewritten, every step.
   e2e    the same metric through the reference-facing call with HOST buffers: at N=1
-         wlp_run (run_model) writing per-replication outputs to pinned host memory + device
-         CI; at N>1 the sharded step plus the D2H of the shard's outputs. Wall clock
-         (perf_counter with synchronize), max over ranks.
+         wlp_run (run_model) writing per-replication outputs to pinned host memory plus the
+         device CI; at N>1 each rank's wlp_run_shard writing its slice to pinned host memory
+         plus the statistics exchange. Synchronised wall clock, max over ranks.
 
-Extras (N=1): WLP and TLP rates for every model/config of BASELINE (2, 3, 4, 5), the
-ALU-issue roofline of the dominant kernel, the IR path (interpreter and JIT), and the CPU
-baseline (the reference's own replication functions, oracle/_ref, on all host cores,
-bounded sample). Under torchrun (every N): "cfg4_sharded_1e7" — BASELINE config 4 as
-stated, all three models with 10^7 replications in total sharded over the N GPUs.
+"models" (every N): BASELINE config 4 as stated — each model with 10^7 replications in
+total sharded over the N GPUs (strong scaling), WLP, N = 1000 units: device value, e2e
+(host buffers), the roofline of the model's kernel (name taken from the run), and at
+N=1 the reference's own CPU path on all host cores (bounded sample).
+
+Extras (N=1): WLP vs TLP for configs 2-5, the walk's alternative kernels, the measured
+divergence counters, the IR path, and the CPU baselines.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
 import tempfile
 import time
 from pathlib import Path
-
-import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
@@ -50,8 +53,9 @@ UNIT = "replications/s"
 R_PER_GPU = 1_000_000
 DRAWS = 10_000
 SEED = 42
+R_CFG4 = 10_000_000
 
-# Algorithmic instruction counts per unit (issue slots of one lane), see DESIGN.md §roofline:
+# Algorithmic instruction counts per unit (issue slots of one lane), see DESIGN.md §6:
 # one taus88 draw = 16 SASS (6 IMAD.SHL, 3 shift-merge, 7 LOP3); pi point = 2 draws +
 # 2 exact u32->f64 + 2 DMUL + DADD + DSETP + count = 39; walk step = 2 draws + shift +
 # 2 compare/add = 35.
@@ -64,6 +68,8 @@ BS_LOP3_PER_STEP = 45.4
 # 15.7 average) + negate/scale (1), plus the Lindley step (6 DADD + 1 compare) = 42.
 FP64_PER_CLIENT = 42
 
+CFG4 = [("pi", 0, dict(draws=1000)), ("mm1", 1, dict(clients=1000)), ("walk", 2, dict(steps=1000, chunks=30))]
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -73,10 +79,90 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="launch plumbing only (gloo, CPU)")
     return ap.parse_args()
 
 
-# ---------------------------------------------------------------------------------------------
+# ---- launch ----------------------------------------------------------------------------------
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args) -> None:
+    """--gpus N > 1 outside torchrun: re-run this command as N torchrun ranks (returns
+    only when already under torchrun or N == 1)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    sys.stdout.flush()
+    r = subprocess.run(cmd)
+    sys.exit(r.returncode)
+
+
+def world_of(args) -> tuple[int, int, int]:
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but torchrun started {world} ranks")
+    return world, rank, local
+
+
+def dist_setup(args):
+    import torch
+
+    world, rank, local = world_of(args)
+    if "LOCAL_RANK" in os.environ:  # under torchrun: always the NCCL path (even at N = 1)
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        # NCCL's banner goes to stdout at communicator creation; keep stdout for the one
+        # JSON line by pointing fd 1 at stderr while the communicator comes up
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.barrier()
+            torch.cuda.synchronize()
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
+        assert dist.get_world_size() == args.gpus
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def dry_run(args) -> None:
+    """The launch plumbing without a GPU: gloo ranks, barrier, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank, _ = world_of(args)
+    if "LOCAL_RANK" in os.environ:
+        dist.init_process_group("gloo")
+        assert dist.get_world_size() == args.gpus
+    t = torch.tensor([float(rank + 1)])
+    if dist.is_initialized():
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "impl": args.impl, "n_gpus": world, "world": world,
+                          "backend": dist.get_backend() if dist.is_initialized() else None,
+                          "max_over_ranks": float(t.item())}), flush=True)
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
+# ---- timing ----------------------------------------------------------------------------------
 
 
 class Clocks:
@@ -94,7 +180,7 @@ class Clocks:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
                                          stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.proc = None
@@ -123,43 +209,14 @@ def measured_peaks() -> dict:
         return {}
 
 
-def ncu_traffic() -> dict:
-    """Per-launch DRAM bytes of the dominant kernel from the committed ncu summary."""
+def ncu_capture(kernel: str) -> dict:
+    """The latest committed ncu summary of `kernel` (profiles/ncu_summary.json, keyed by the
+    kernel's demangled name as wlp_last_kernel reports it)."""
     try:
-        return json.loads((ROOT / "profiles" / "ncu_summary.json").read_text())
+        caps = json.loads((ROOT / "profiles" / "ncu_summary.json").read_text()).get(kernel, {})
     except Exception:
         return {}
-
-
-# ---------------------------------------------------------------------------------------------
-
-
-def dist_setup():
-    import torch
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1 or "LOCAL_RANK" in os.environ:  # under torchrun: always the NCCL path
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local)
-        # NCCL's "NCCL version ..." banner goes to stdout at communicator creation; keep
-        # stdout for the one JSON line by pointing fd 1 at stderr while the comm comes up
-        sys.stdout.flush()
-        saved = os.dup(1)
-        os.dup2(2, 1)
-        try:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-            dist.barrier()
-            torch.cuda.synchronize()
-        finally:
-            sys.stdout.flush()
-            os.dup2(saved, 1)
-            os.close(saved)
-    else:
-        torch.cuda.set_device(0)
-    return world, rank, local
+    return caps[sorted(caps)[-1]] if caps else {}
 
 
 def barrier(world):
@@ -215,53 +272,60 @@ def wall_timed(step, steps: int, warmup: int, world: int):
     return max_over_ranks(t, world)
 
 
-# ---------------------------------------------------------------------------------------------
+# ---- CPU path of the reference ----------------------------------------------------------------
 
 
-def cpu_baseline(model: int, p, budget_s: float = 15.0, steps: int = 1):
-    """The reference's own host path (oracle/_ref = proj/src compiled unmodified):
-    random_spacing (sequential, as in the reference) + the replication functions on all
-    host threads (they are pure), on a bounded sample of the workload."""
+def cpu_sample(model: int, p, S: int):
+    """The reference's own host path (oracle/_ref = proj/src compiled unmodified) over the
+    first S replications of the run: random_spacing (sequential, as in the reference) +
+    the replication functions on all host threads (pure functions).
+    Returns (seconds spacing, seconds replications, kind, threads)."""
     import oracle
 
     ref = oracle.Oracle("reference") if oracle.available("reference") else oracle.Oracle("port")
     kind = "reference" if ref.kind == "reference" else "port"
-    nth = os.cpu_count() or 1
+    nth = (os.cpu_count() or 1) if kind == "reference" else 1
     op = oracle.params_from(p)
+    t0 = time.perf_counter()
+    keys = ref.random_spacing(SEED, S)
+    t1 = time.perf_counter()
+    if kind == "reference":
+        ref.replications(model, op, keys, nthreads=nth)
+    else:
+        ref.replications(model, op, keys)
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1, kind, nth
 
-    def run(S):
-        t0 = time.perf_counter()
-        keys = ref.random_spacing(SEED, S)
-        t1 = time.perf_counter()
-        if kind == "reference":
-            ref.replications(model, op, keys, nthreads=nth)
-        else:
-            ref.replications(model, op, keys)
-        t2 = time.perf_counter()
-        return t1 - t0, t2 - t1
 
-    S = 4 * nth
-    a, b = run(S)
-    per = (a + b) / S
+def cpu_baseline(model: int, p, budget_s: float = 10.0) -> dict:
+    """Replications/s of the reference's CPU path on a bounded sample (~budget_s seconds)
+    of the run, plus the single-core rate of the replication functions."""
+    nth = os.cpu_count() or 1
+    a, b, kind, used = cpu_sample(model, p, 4 * nth)
+    per = (a + b) / (4 * nth)
     S = int(max(4 * nth, min(p.replications, budget_s / max(per, 1e-9))))
     S = max(nth, (S // nth) * nth)
-    tot = [run(S) for _ in range(steps)]
-    tsp = sum(x for x, _ in tot) / steps
-    trep = sum(y for _, y in tot) / steps
-    # single-core rate of the same functions on a small slice (SURVEY §8d)
-    s1 = max(4, min(S, int(2.0 / max(per * nth, 1e-9))))
-    keys = ref.random_spacing(SEED, s1)
+    tsp, trep, kind, used = cpu_sample(model, p, S)
+    s1 = max(4, min(S, int(2.0 / max(trep / S * used, 1e-9))))
+    _, t1rep, _, _ = cpu_sample_single(model, p, s1)
+    return {"value": S / (tsp + trep), "unit": UNIT, "cores": used, "kind": kind,
+            "sample": f"first {S} of {p.replications} replications (seed {SEED}): random_spacing 1 thread "
+                      f"{tsp:.3f}s + replications on {used} threads {trep:.3f}s",
+            "single_core_value": s1 / (t1rep + tsp / S * s1), "single_core_sample": f"{s1} replications"}
+
+
+def cpu_sample_single(model: int, p, S: int):
+    import oracle
+
+    ref = oracle.Oracle("reference") if oracle.available("reference") else oracle.Oracle("port")
+    op = oracle.params_from(p)
+    keys = ref.random_spacing(SEED, S)
     t0 = time.perf_counter()
-    if kind == "reference":
+    if ref.kind == "reference":
         ref.replications(model, op, keys, nthreads=1)
     else:
         ref.replications(model, op, keys)
-    t1 = time.perf_counter()
-    return {"value": S / (tsp + trep), "unit": UNIT, "cores": nth if kind == "reference" else 1, "kind": kind,
-            "sample": f"{S} of {p.replications} replications (seed {SEED}): random_spacing 1 thread "
-                      f"{tsp:.3f}s + replications on {nth if kind == 'reference' else 1} threads {trep:.3f}s",
-            "single_core_value": s1 / (t1 - t0 + tsp / S * s1), "single_core_sample": f"{s1} replications",
-            "step_s": tsp + trep}
+    return 0.0, time.perf_counter() - t0, ref.kind, 1
 
 
 def ir_simulator_baseline() -> dict:
@@ -281,33 +345,76 @@ def ir_simulator_baseline() -> dict:
         return {"unavailable": str(e)}
 
 
+def headline_config(n: int) -> dict:
+    return {"workload": "BASELINE config 2: pi, 1e6 replications x 1e4 draws per GPU, WLP",
+            "replications": R_PER_GPU * n, "draws": DRAWS, "mode": "wlp", "parallelism": f"shard{n}",
+            "l2": "inputs regenerated every step (seeds 12 B/rep + outputs 8 B/rep)"}
+
+
 def run_reference_arm(args):
-    """--impl reference: the reference CPU path on this box's host cores."""
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
+    """--impl reference: the reference's CPU path (oracle/_ref) on this box's host cores, on
+    the headline workload (N*10^6 pi replications x 10^4 draws). Each timed step is one
+    measured pass over a bounded sample of it — the whole run when it fits — sized so the
+    arm ends within a few minutes; ms_per_step is that pass's measured time."""
+    world, rank, _ = world_of(args)
     if rank != 0:
         return
     import paper_1501_01405_b200 as w
 
-    p = w.ModelParams(replications=R_PER_GPU * world, draws=DRAWS)
-    # one calibration/warm-up step, then exactly K steps, each a bounded sample: ~6 s of CPU
-    # work, less when K is large, so the whole arm stays within ~2.5 minutes
-    budget = max(1.0, min(6.0, 150.0 / (args.steps + 1)))
-    cal = cpu_baseline(0, p, budget_s=budget)
-    rates = [cpu_baseline(0, p, budget_s=budget)["value"] for _ in range(args.steps)]
-    v = statistics.mean(rates)
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * p.replications / v,
+    n = args.gpus
+    p = w.ModelParams(replications=R_PER_GPU * n, draws=DRAWS)
+    nth = os.cpu_count() or 1
+    a, b, kind, used = cpu_sample(0, p, 4 * nth)  # calibration (not a step)
+    per = (a + b) / (4 * nth)
+    budget = max(2.0, 150.0 / max(args.steps, 1))
+    S = int(min(p.replications, max(nth, budget / max(per, 1e-9))))
+    S = max(nth, (S // nth) * nth) if S < p.replications else S
+    for _ in range(args.warmup):
+        cpu_sample(0, p, max(nth, S // 50))  # short warm-up passes (page-in, threads)
+    times = []
+    for _ in range(args.steps):
+        tsp, trep, kind, used = cpu_sample(0, p, S)
+        times.append(tsp + trep)
+    step_s = sum(times) / len(times)
+    v = S / step_s
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": n,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * step_s,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32+f64",
-            "data": "synthetic (taus88 streams from master seed 42)",
-            "config": {"workload": "BASELINE config 2: pi, 1e6 replications x 1e4 draws per GPU",
-                       "replications": p.replications, "draws": DRAWS},
-            "cpu_baseline": {k: cal[k] for k in ("kind", "cores", "sample")} | {"value": v, "unit": UNIT},
+            "data": "synthetic (taus88 streams by random spacing from master seed 42)",
+            "config": headline_config(n),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": used, "kind": kind,
+                             "sample": f"each step: the first {S} of {p.replications} replications "
+                                       f"(random_spacing on 1 thread + pi_replication on {used} threads)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-# ---------------------------------------------------------------------------------------------
+# ---- GPU arm -----------------------------------------------------------------------------------
+
+
+def roofline_of(model: int, kernel: str, units: int, kernel_ms: float, sms: int, fmax: float) -> dict:
+    """The roofline that bounds `kernel`: issue slots (pi, per-replication
+    walk), the ALU pipe (bitsliced walk: LOP3) or the FP64 pipe (mm1). No tensor-core or
+    HBM roofline applies (integer / FP64 ALU work, ~20 B of HBM per replication)."""
+    t = kernel_ms * 1e-3
+    if "walk_bs" in kernel:
+        achieved = units * BS_LOP3_PER_STEP / 32 / 32 / t / 1e9
+        peak, bound = 2 * sms * fmax * 1e-3, "alu_pipe"
+        algo = f"{BS_LOP3_PER_STEP} LOP3 per step per 32 replications x {units:.0e} steps / 32 lanes"
+    elif model == 1:
+        achieved = units * FP64_PER_CLIENT / 32 / t / 1e9
+        peak, bound = 2 * sms * fmax * 1e-3, "fp64_pipe"
+        algo = f"{FP64_PER_CLIENT} FP64 lane-ops per client x {units:.0e} clients / 32"
+    else:
+        achieved = units * INSTR_PER_UNIT[model] / 32 / t / 1e9
+        peak, bound = 4 * sms * fmax * 1e-3, "issue"
+        algo = f"{INSTR_PER_UNIT[model]} lane-instr per unit x {units:.0e} units / 32"
+    cap = ncu_capture(kernel)
+    return {"bound": bound, "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s",
+            "frac": achieved / peak, "traffic": cap.get("dram_bytes_per_launch"), "algorithmic": algo,
+            "kernel_ms": kernel_ms,
+            "peak_source": f"{'4 issue' if bound == 'issue' else '2 warp-instr'}/clk/SM x {sms} SMs x "
+                           f"sm_max_mhz {fmax:.0f} (MEASURED_PEAKS.json; pipe rates profiles/round1_microbench.txt)"}
 
 
 def model_rate(w, model, p, mode, steps=5, warmup=3):
@@ -330,17 +437,143 @@ def model_rate(w, model, p, mode, steps=5, warmup=3):
             "kernel": w.last_kernel()}
 
 
+def sharded_record(w, D, model: int, p, world: int, comm, stats, stream, steps: int, warmup: int, sms, fmax,
+                   e2e_single_call: bool) -> dict:
+    """One run of p.replications sharded over the ranks: device value, e2e with host
+    buffers, and the roofline of the model kernel that ran."""
+    import torch
+
+    R = p.replications
+    kernel_ms: list = []
+    runner = D.gpu_runner(model, p, w.ExecutionMode.Wlp, SEED, stream=stream, kernel_ms=kernel_ms)
+    res = {}
+
+    def step():
+        res["r"] = D.run_sharded(model, R, runner, stats, comm=comm)
+
+    ms = device_timed(step, steps, warmup, world)
+    kernel = w.last_kernel()
+    k_ms = kernel_ms[warmup:]
+    kernel_avg = max_over_ranks(sum(k_ms) / len(k_ms), world)
+    r = res["r"]
+    nout = len(w.OUTPUT_NAMES[w.ModelKind(model)])
+    host = [torch.empty(max(r.count, 1), dtype=torch.float64, pin_memory=True) for _ in range(nout)]
+    if e2e_single_call:  # N = 1: the reference-facing run_model (wlp_run) into host buffers
+        def e2e_step():
+            w.run_model_into(model, p, w.ExecutionMode.Wlp, SEED, [h.numpy() for h in host], on_device=False,
+                             ci_level=0.95)
+    else:  # each rank: its shard written to host memory + the statistics exchange
+        def e2e_step():
+            rr = D.run_sharded(model, R, runner, stats, comm=comm)
+            for h, o in zip(host, rr.outputs):
+                h[: rr.count].copy_(o[: rr.count])
+
+    e2e_ms = wall_timed(e2e_step, steps, min(warmup, 3), world)
+    units = r.count * p.units(w.ModelKind(model))  # this rank's units per launch
+    ci = r.cis[w.OUTPUT_NAMES[w.ModelKind(model)].index(w.PRIMARY[w.ModelKind(model)])]
+    return {"value": R / (ms * 1e-3), "unit": UNIT, "ms_per_run": ms, "kernel": kernel,
+            "e2e": {"value": R / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_run": e2e_ms,
+                    "h2d_bytes_per_step": 64 * world, "d2h_bytes_per_step": 8 * nout * R,
+                    "call": "wlp_run (run_model) into pinned host arrays" if e2e_single_call
+                    else "wlp_run_shard per rank into pinned host arrays + statistics exchange"},
+            "roofline": roofline_of(model, kernel, units, kernel_avg, sms, fmax),
+            "result": {"mean": ci.mean, "half_width": ci.halfWidth, "n": ci.n},
+            "gpu_launches_per_step": 2 + 2 * nout}
+
+
+def extras_single_gpu(w, sms, fmax, peak_issue) -> dict:
+    import torch
+
+    extras = {}
+    cfgs = [("cfg2_pi_1e6x1e4", w.ModelKind.Pi, dict(replications=1_000_000, draws=10_000)),
+            ("cfg3_walk_1e5x1e3", w.ModelKind.Walk, dict(replications=100_000, steps=1000, chunks=30)),
+            ("cfg4_pi_1e7x1e3", w.ModelKind.Pi, dict(replications=R_CFG4, draws=1000)),
+            ("cfg4_mm1_1e7x1e3", w.ModelKind.Mm1, dict(replications=R_CFG4, clients=1000)),
+            ("cfg4_walk_1e7x1e3", w.ModelKind.Walk, dict(replications=R_CFG4, steps=1000, chunks=30))]
+    for name, m, kw in cfgs:
+        pp = w.ModelParams(**kw)
+        extras[name] = {}
+        variants = [("wlp", w.ExecutionMode.Wlp, 0, 0), ("tlp", w.ExecutionMode.Tlp, 0, 0)]
+        if m == w.ModelKind.Walk:
+            # the walk's other kernels (DESIGN.md §4): per-replication WLP (lane jumps /
+            # pipeline) and the bitsliced TLP (thread per 32 replications)
+            variants += [("wlp_per_replication", w.ExecutionMode.Wlp, 2 if pp.replications >= 1_000_000 else 1, 0),
+                         ("tlp_bitsliced", w.ExecutionMode.Tlp, 0, 2)]
+        for label, md, wv, tv in variants:
+            with w.wlp_variant(wv), w.tlp_variant(tv):
+                r = model_rate(w, m, pp, md)
+            units_ = pp.replications * pp.units(m)
+            rl = roofline_of(int(m), r["kernel"], units_, r["kernel_ms"], sms, fmax)
+            r[{"issue": "issue_frac", "alu_pipe": "alu_frac", "fp64_pipe": "fp64_frac"}[rl["bound"]]] = rl["frac"]
+            extras[name][label] = r
+    # measured warp-execution evidence (paper Table 1 / Fig. 7 analogue): divergence events
+    # with the reference's definition and global memory warp-instructions, from the
+    # instrumented kernels (outputs identical; counters cost a little speed)
+    for name, m, kw in [("cfg3_walk_1e5x1e3", w.ModelKind.Walk, dict(replications=100_000, steps=1000, chunks=30)),
+                        ("cfg4_mm1_1e7x1e3", w.ModelKind.Mm1, dict(replications=1_000_000, clients=1000))]:
+        table1 = {}
+        with w.hw_counters():
+            for md in (w.ExecutionMode.Wlp, w.ExecutionMode.Tlp):
+                rr = w.run_model(m, w.ModelParams(**kw), md, master_seed=SEED)
+                rep = rr.report
+                table1[w.mode_name(md)] = {"kernel": w.last_kernel(), "divergence_events": rep.divergenceEvents,
+                                           "mem_reads": rep.memReads, "mem_writes": rep.memWrites,
+                                           "total_cycles": rep.totalCycles}
+        table1["replications"] = kw["replications"]
+        extras[name]["counters"] = table1
+    # config 5: experimental plan, 64 factor-level sets x 30 replications, one launch
+    sets = [w.ModelParams(replications=30, clients=10_000, lambda_=0.1 + 0.8 * k / 63, mu=1.0) for k in range(64)]
+    seeds = [SEED + k for k in range(64)]
+    hsets = [w.ModelParams(replications=30, steps=100 + 30 * k, chunks=30) for k in range(64)]
+    for label, m, ss, nout in (("cfg5_plan_mm1_64x30x1e4", w.ModelKind.Mm1, sets, 3),
+                               ("cfg5_plan_walk_hetero_64x30", w.ModelKind.Walk, hsets, 1)):
+        extras[label] = {}
+        for md in (w.ExecutionMode.Wlp, w.ExecutionMode.Tlp):
+            outs = [torch.empty(64 * 30, dtype=torch.float64, device="cuda") for _ in range(nout)]
+            kms = []
+
+            def pstep():
+                rep = w.SimReport()
+                w.run_plan(m, ss, seeds, md, outs, on_device=True, report=rep)
+                kms.append(rep.kernel_ms)
+
+            pms = device_timed(pstep, 5, 3, 1)
+            extras[label][w.mode_name(md)] = {"reps_per_s": 1920 / (pms * 1e-3), "ms_per_run": pms,
+                                              "kernel_ms": sum(kms[3:]) / len(kms[3:])}
+    # the reference's own IR kernel (TLP walk) on the GPU IR interpreter (DESIGN.md §11):
+    # statements issued per second, counters exact; then compiled (IR -> CUDA C++ -> NVRTC)
+    from paper_1501_01405_b200 import ir
+
+    pir = w.ModelParams(replications=20_000, steps=1000, chunks=30)
+    runs = [ir.run_model(w.ModelKind.Walk, pir, w.ExecutionMode.Tlp, SEED) for _ in range(3)]
+    kms = min(r.report.kernel_ms for r in runs)
+    extras["ir_walk_tlp_2e4x1e3"] = {"kernel_ms": kms, "issues": runs[-1].report.issues,
+                                     "divergence_events": runs[-1].report.divergenceEvents,
+                                     "issues_per_s": runs[-1].report.issues / (kms * 1e-3)}
+    jruns = [ir.run_model(w.ModelKind.Walk, pir, w.ExecutionMode.Tlp, SEED, jit=True) for _ in range(4)]
+    jms = min(r.report.kernel_ms for r in jruns[1:])
+    assert all((r.primary == runs[-1].primary).all() for r in jruns)
+    extras["ir_walk_tlp_2e4x1e3"]["jit"] = {"kernel_ms": jms, "speedup_vs_interpreter": kms / jms}
+    return extras
+
+
 def main():
     args = parse()
+    if args.dry_run:
+        self_launch(args)
+        dry_run(args)
+        return
     if args.impl == "reference":
+        # rank 0 alone times the CPU path; no GPU and no re-launch needed
         run_reference_arm(args)
         return
+    self_launch(args)
     import torch
 
     import paper_1501_01405_b200 as w
     from paper_1501_01405_b200 import distributed as D
 
-    world, rank, local = dist_setup()
+    world, rank, local = dist_setup(args)
     model, mode = w.ModelKind.Pi, w.ExecutionMode.Wlp
     R = R_PER_GPU * world
     p = w.ModelParams(replications=R, draws=DRAWS)
@@ -358,12 +591,11 @@ def main():
     clocks.start()
     ms = device_timed(step, args.steps, args.warmup, world)
     clk = clocks.stop()
+    kernel = w.last_kernel()
     k_ms = kernel_ms[args.warmup:]
-    kernel_avg = sum(k_ms) / len(k_ms)
-    kernel_avg = max_over_ranks(kernel_avg, world)
+    kernel_avg = max_over_ranks(sum(k_ms) / len(k_ms), world)
     value = R / (ms * 1e-3)
-    # launches of our kernels per step: seed + model + 2 statistics passes (1 output)
-    launches = args.steps * 4
+    launches = args.steps * 4  # per step: seeding + model + the two statistics passes
     ci = result["r"].cis[0]
 
     # ---- e2e through the reference-facing call with host buffers
@@ -378,152 +610,43 @@ def main():
             host[0].copy_(r.outputs[0][:count], non_blocking=False)
     e2e_ms = wall_timed(e2e_step, args.steps, min(args.warmup, 3), world)
 
-    # ---- roofline of the dominant kernel (ALU issue; no tensor cores on this path)
+    # ---- roofline of the dominant kernel, named by the run itself
     peaks = measured_peaks()
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     fmax = float(peaks.get("sm_max_mhz", 1965.0))
-    units = R_PER_GPU * DRAWS
-    achieved = units * INSTR_PER_UNIT[0] / 32 / (kernel_avg * 1e-3) / 1e9  # G warp-instr/s
-    peak = 4 * sms * fmax * 1e6 / 1e9
-    # latest committed capture of this kernel at this workload (the capture names end in R)
-    caps = {k: v for name in ("k_wlp_lanes<0>", "k_wlp_lanes<0, 0>")
-            for k, v in ncu_traffic().get(name, {}).items() if k.endswith(f"_{R_PER_GPU}")}
-    nc = caps[sorted(caps)[-1]] if caps else {}
-    roofline = {"bound": "issue", "kernel": "k_wlp_lanes<0> (pi WLP)", "achieved": achieved, "peak": peak,
-                "unit": "Gwarp-inst/s", "frac": achieved / peak, "traffic": nc.get("dram_bytes_per_launch"),
-                "algorithmic": f"{INSTR_PER_UNIT[0]} lane-instr/point x {units:.0e} points per launch / 32",
-                "peak_source": f"4 issue/clk x {sms} SMs x sm_max_mhz {fmax:.0f} (MEASURED_PEAKS.json); "
-                               "no tensor/HBM roofline applies (integer/fp64 ALU work)",
-                "kernel_ms": kernel_avg,
-                "frac_at_measured_clock": (achieved / (4 * sms * clk["sm_mhz"] * 1e-3)) if clk.get("sm_mhz") else None,
-                "hbm_gbs_output_writeout": (R_PER_GPU * 8 + 3 * 4 * R_PER_GPU) / (kernel_avg * 1e-3) / 1e9}
+    roofline = roofline_of(0, kernel, R_PER_GPU * DRAWS, kernel_avg, sms, fmax)
+    roofline["frac_at_measured_clock"] = (roofline["achieved"] / (4 * sms * clk["sm_mhz"] * 1e-3)
+                                          if clk.get("sm_mhz") else None)
+    roofline["hbm_gbs_output_writeout"] = (R_PER_GPU * 8 + 3 * 4 * R_PER_GPU) / (kernel_avg * 1e-3) / 1e9
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32+f64",
             "data": "synthetic (taus88 streams by random spacing from master seed 42)",
-            "config": {"workload": "BASELINE config 2: pi, 1e6 replications x 1e4 draws per GPU, WLP",
-                       "replications": R, "draws": DRAWS, "mode": "wlp", "parallelism": f"shard{world}",
-                       "l2": "inputs regenerated every step (seeds 12 B/rep + outputs 8 B/rep)"},
+            "config": headline_config(world),
             "e2e": {"value": R / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 64 * world,
                     "d2h_bytes_per_step": R * 8, "ms_per_step": e2e_ms,
                     "note": "inputs are (master seed, params) by value; outputs D2H to pinned host"},
             "gpu_launches": launches, "clocks": clk, "roofline": roofline,
             "result": {"mean": ci.mean, "half_width": ci.halfWidth, "n": ci.n}}
 
-    if (world > 1 or "LOCAL_RANK" in os.environ) and not args.no_extras:
-        # BASELINE config 4 as stated (every torchrun launch, N >= 1): all models, 10^7
-        # replications in total sharded over the N GPUs (strong scaling), WLP, the two
-        # statistics exchanges included; time is the max over ranks of the device time
-        sharded = {}
-        for name, m, kw in [("pi", w.ModelKind.Pi, dict(draws=1000)), ("mm1", w.ModelKind.Mm1, dict(clients=1000)),
-                            ("walk", w.ModelKind.Walk, dict(steps=1000, chunks=30))]:
-            p4 = w.ModelParams(replications=10_000_000, **kw)
-            run4 = D.gpu_runner(m, p4, w.ExecutionMode.Wlp, SEED, stream=stream)
+    # ---- BASELINE config 4 per model: 10^7 replications sharded over the N GPUs
+    models = {}
+    for name, m, kw in CFG4:
+        p4 = w.ModelParams(replications=R_CFG4, **kw)
+        models[name] = sharded_record(w, D, m, p4, world, comm, stats, stream, args.steps, args.warmup, sms, fmax,
+                                      e2e_single_call=(world == 1 and "LOCAL_RANK" not in os.environ))
+        models[name]["config"] = {"workload": f"BASELINE config 4: {name}, 1e7 replications sharded over "
+                                              f"{world} GPU(s), WLP", "replications": R_CFG4, **kw,
+                                  "parallelism": f"shard{world}", "scaling": "strong"}
+    line["models"] = models
 
-            def step4():
-                D.run_sharded(m, p4.replications, run4, stats, comm=comm)
-
-            ms4 = device_timed(step4, 3, 3, world)
-            sharded[name] = {"reps_per_s": p4.replications / (ms4 * 1e-3), "ms_per_run": ms4}
-        line["cfg4_sharded_1e7"] = sharded
     if world == 1 and not args.no_extras:
-        extras = {}
-        cfgs = [("cfg2_pi_1e6x1e4", w.ModelKind.Pi, dict(replications=1_000_000, draws=10_000)),
-                ("cfg3_walk_1e5x1e3", w.ModelKind.Walk, dict(replications=100_000, steps=1000, chunks=30)),
-                ("cfg4_pi_1e7x1e3", w.ModelKind.Pi, dict(replications=10_000_000, draws=1000)),
-                ("cfg4_mm1_1e7x1e3", w.ModelKind.Mm1, dict(replications=10_000_000, clients=1000)),
-                ("cfg4_walk_1e7x1e3", w.ModelKind.Walk, dict(replications=10_000_000, steps=1000, chunks=30))]
-        for name, m, kw in cfgs:
-            pp = w.ModelParams(**kw)
-            extras[name] = {}
-            for md in (w.ExecutionMode.Wlp, w.ExecutionMode.Tlp):
-                r = model_rate(w, m, pp, md)
-                units_ = pp.replications * pp.units(m)
-                if "walk_bs" in r["kernel"]:  # bitsliced: ALU pipe against its own LOP3 count
-                    r["alu_frac"] = units_ * BS_LOP3_PER_STEP / 32 / 32 / (r["kernel_ms"] * 1e-3) / (2 * sms * fmax * 1e6)
-                elif m in INSTR_PER_UNIT:
-                    r["issue_frac"] = units_ * INSTR_PER_UNIT[int(m)] / 32 / (r["kernel_ms"] * 1e-3) / (peak * 1e9)
-                else:  # FP64 pipe: 64 lanes/clk/SM (measured, profiles/round1_microbench.txt)
-                    r["fp64_frac"] = units_ * FP64_PER_CLIENT / (r["kernel_ms"] * 1e-3) / (64 * sms * fmax * 1e6)
-                extras[name][w.mode_name(md)] = r
-            if m == w.ModelKind.Walk:
-                # the walk's other kernels (DESIGN.md §4 bitsliced walk): per-replication
-                # WLP pipeline / lane jumps, and the bitsliced TLP (thread per 32 replications).
-                # Bitsliced work is ~45 LOP3 per step per 32 replications, ALU pipe 2/clk/SM.
-                units_ = pp.replications * pp.steps
-                for label, wv, tv, md in (("wlp_per_replication", 2 if pp.replications >= 1_000_000 else 1, 0,
-                                           w.ExecutionMode.Wlp),
-                                          ("tlp_bitsliced", 0, 2, w.ExecutionMode.Tlp)):
-                    with w.wlp_variant(wv), w.tlp_variant(tv):
-                        r = model_rate(w, m, pp, md)
-                    if "walk_bs" in r["kernel"]:
-                        r["alu_frac"] = units_ * BS_LOP3_PER_STEP / 32 / 32 / (r["kernel_ms"] * 1e-3) / (2 * sms * fmax * 1e6)
-                    else:
-                        r["issue_frac"] = units_ * INSTR_PER_UNIT[2] / 32 / (r["kernel_ms"] * 1e-3) / (peak * 1e9)
-                    extras[name][label] = r
-        # config 3's warp-execution evidence (paper Table 1 / Fig. 7 analogue): divergence
-        # events with the reference's definition and global memory warp-instructions, from
-        # the instrumented kernels (outputs identical; counters cost a little speed)
-        pw = w.ModelParams(replications=100_000, steps=1000, chunks=30)
-        table1 = {}
-        with w.hw_counters():
-            for md in (w.ExecutionMode.Wlp, w.ExecutionMode.Tlp):
-                rr = w.run_model(w.ModelKind.Walk, pw, md, master_seed=SEED).report
-                table1[w.mode_name(md)] = {"divergence_events": rr.divergenceEvents, "mem_reads": rr.memReads,
-                                           "mem_writes": rr.memWrites}
-        extras["cfg3_walk_1e5x1e3"]["counters"] = table1
-        # config 5: experimental plan, 64 factor-level sets x 30 replications, one launch
-        sets = [w.ModelParams(replications=30, clients=10_000, lambda_=0.1 + 0.8 * k / 63, mu=1.0) for k in range(64)]
-        seeds = [SEED + k for k in range(64)]
-        extras["cfg5_plan_mm1_64x30x1e4"] = {}
-        for md in (w.ExecutionMode.Wlp, w.ExecutionMode.Tlp):
-            outs = [torch.empty(64 * 30, dtype=torch.float64, device="cuda") for _ in range(3)]
-            kms = []
-
-            def pstep():
-                rep = w.SimReport()
-                w.run_plan(w.ModelKind.Mm1, sets, seeds, md, outs, on_device=True, report=rep)
-                kms.append(rep.kernel_ms)
-
-            pms = device_timed(pstep, 5, 3, 1)
-            extras["cfg5_plan_mm1_64x30x1e4"][w.mode_name(md)] = {
-                "reps_per_s": 1920 / (pms * 1e-3), "ms_per_run": pms, "kernel_ms": sum(kms[3:]) / len(kms[3:])}
-        # config 5's trip-count-heterogeneous variant: walk sets with
-        # steps_k = 100 + 30k, so a TLP warp spanning two sets idles lanes; one launch each
-        hsets = [w.ModelParams(replications=30, steps=100 + 30 * k, chunks=30) for k in range(64)]
-        extras["cfg5_plan_walk_hetero_64x30"] = {}
-        for md in (w.ExecutionMode.Wlp, w.ExecutionMode.Tlp):
-            hout = [torch.empty(64 * 30, dtype=torch.float64, device="cuda")]
-            hk = []
-
-            def hstep():
-                rep = w.SimReport()
-                w.run_plan(w.ModelKind.Walk, hsets, seeds, md, hout, on_device=True, report=rep)
-                hk.append(rep.kernel_ms)
-
-            hms = device_timed(hstep, 5, 3, 1)
-            extras["cfg5_plan_walk_hetero_64x30"][w.mode_name(md)] = {
-                "reps_per_s": 1920 / (hms * 1e-3), "ms_per_run": hms, "kernel_ms": sum(hk[3:]) / len(hk[3:])}
-        # the reference's own IR kernel (TLP walk) on the GPU IR interpreter:
-        # statements issued per second, counters exact; the reference's host simulator on
-        # a 10x smaller sample beside it when the CPU legs run
-        from paper_1501_01405_b200 import ir
-
-        pir = w.ModelParams(replications=20_000, steps=1000, chunks=30)
-        runs = [ir.run_model(w.ModelKind.Walk, pir, w.ExecutionMode.Tlp, SEED) for _ in range(3)]
-        kms = min(r.report.kernel_ms for r in runs)
-        extras["ir_walk_tlp_2e4x1e3"] = {"kernel_ms": kms, "issues": runs[-1].report.issues,
-                                         "divergence_events": runs[-1].report.divergenceEvents,
-                                         "issues_per_s": runs[-1].report.issues / (kms * 1e-3)}
-        # the same IR kernel compiled (IR -> CUDA C++ -> NVRTC), first call compiles
-        jruns = [ir.run_model(w.ModelKind.Walk, pir, w.ExecutionMode.Tlp, SEED, jit=True) for _ in range(4)]
-        jms = min(r.report.kernel_ms for r in jruns[1:])
-        assert all((r.primary == runs[-1].primary).all() for r in jruns)
-        extras["ir_walk_tlp_2e4x1e3"]["jit"] = {"kernel_ms": jms, "speedup_vs_interpreter": kms / jms}
-        line["extras"] = extras
+        line["extras"] = extras_single_gpu(w, sms, fmax, 4 * sms * fmax * 1e-3)
     if world == 1 and rank == 0 and not args.no_cpu:
-        line["cpu_baseline"] = {k: v for k, v in cpu_baseline(0, p).items() if k != "step_s"}
+        line["cpu_baseline"] = cpu_baseline(0, p)
+        for name, m, kw in CFG4:
+            models[name]["cpu_baseline"] = cpu_baseline(m, w.ModelParams(replications=R_CFG4, **kw), budget_s=5.0)
         if "extras" in line:  # the reference's host simulator beside the GPU IR interpreter
             line["cpu_baseline"]["ir_reference_simulator"] = ir_simulator_baseline()
     if rank == 0:

@@ -50,7 +50,7 @@ struct AnalysisError : Error {
     using Error::Error;
 };
 
-// ---- rng.hpp:11-45 ----------------------------------------------------------------
+// ---- rng.hpp:11-45 (all of it) ----------------------------------------------------------------
 struct RngState {
     std::uint32_t s1 = 2;
     std::uint32_t s2 = 8;
@@ -65,6 +65,20 @@ RngState rng_state_from_seed(std::uint64_t seed);
 std::vector<RngState> random_spacing(RngState& master, std::size_t count);
 // Raw stream: n consecutive taus_next outputs from `state` (GPU), and the state after them.
 std::vector<std::uint32_t> taus_stream(RngState& state, std::size_t n);
+
+// Scalar draws (rng.hpp:22-33). These are host utilities (one value per call, the
+// reference's own arithmetic: taus88 step, * 2^-32, and -log(1-u)/rate through the same
+// glibc-log port the mm1 kernels run); bulk draws go through taus_stream / the kernels.
+std::uint32_t taus_next(RngState& state);
+double uniform01(RngState& state);
+double exponential_from_u(double u, double rate);  // DomainError: rate <= 0, u outside [0,1)
+double exponential(RngState& state, double rate);
+
+// Callable uniform source over an owned state (rng.hpp:42-45).
+struct TausStream {
+    RngState state;
+    double operator()() { return uniform01(state); }
+};
 
 // ---- kernel_ir.hpp / device.hpp records used by the API ------------------------------
 struct Dim3 {
@@ -108,7 +122,13 @@ struct SimOptions {
     // B200 extension: simulate() compiles the IR kernel (CUDA C++ via NVRTC) instead of
     // interpreting it. Same memory results; the report has measured time only.
     bool irJit = false;
+    // B200 extension: run_model shards the replications over GPUs 0..devices-1 of this
+    // process (wlp_run_devices: contiguous slices, one host thread per GPU, global
+    // spacing check, statistics merged in device order). Outputs are identical.
+    int devices = 1;
 };
+// CUDA devices visible to this process.
+int device_count();
 struct SimReport {
     std::int64_t totalCycles = 0;
     std::int64_t wavesExecuted = 0;
@@ -156,6 +176,42 @@ struct MM1Result {
     double avgWaitQueue = 0.0;
     double avgSystem = 0.0;
 };
+
+namespace detail {
+// The model body over 2 * units uniforms on the GPU (wlp_run_uniforms); checks the
+// template's parameters first (check_u), as the reference throws before drawing.
+void check_u(ModelKind model, std::int64_t units, std::int64_t chunks, double lambda, double mu);
+std::vector<double> run_u(ModelKind model, std::int64_t units, std::int64_t chunks, double lambda, double mu,
+                          const std::vector<double>& u);
+template <class U>
+std::vector<double> draw_u(std::int64_t units, U& next) {
+    std::vector<double> u(static_cast<std::size_t>(2 * units));
+    for (double& x : u) x = next();
+    return u;
+}
+}  // namespace detail
+
+// One replication over any uniform source (models.hpp:49-108): the source is called
+// 2 * units times in the reference's order on the host, the model body runs on the GPU
+// over those values (same operations, so the same result as the reference's template).
+template <class U>
+double pi_replication_u(std::int64_t draws, U&& next) {
+    detail::check_u(ModelKind::Pi, draws, 0, 0.0, 0.0);
+    return detail::run_u(ModelKind::Pi, draws, 0, 0.0, 0.0, detail::draw_u(draws, next))[0];
+}
+
+template <class U>
+MM1Result mm1_replication_u(std::int64_t clients, double lambda, double mu, U&& next) {
+    detail::check_u(ModelKind::Mm1, clients, 0, lambda, mu);
+    const auto o = detail::run_u(ModelKind::Mm1, clients, 0, lambda, mu, detail::draw_u(clients, next));
+    return MM1Result{o[0], o[1], o[2]};
+}
+
+template <class U>
+double walk_replication_u(std::int64_t steps, std::int64_t chunks, U&& next) {
+    detail::check_u(ModelKind::Walk, steps, chunks, 0.0, 0.0);
+    return detail::run_u(ModelKind::Walk, steps, chunks, 0.0, 0.0, detail::draw_u(steps, next))[0];
+}
 
 // One replication over a given stream, computed on the GPU (models.hpp:110-112).
 double pi_replication(std::int64_t draws, RngState stream);

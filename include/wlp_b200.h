@@ -162,6 +162,16 @@ int wlp_jump_host(const uint32_t state[3], uint64_t n, uint32_t state_out[3]);
 /* inverse_normal_cdf (models.cpp:61-97). */
 int wlp_inverse_normal_cdf(double p, double* z);
 
+/* The reference's scalar rng utilities (rng.hpp:22-33), on the host: taus_next
+ * (rng.cpp:42-51) advancing state[3] in place, uniform01 = taus_next * 2^-32
+ * (rng.cpp:53-55), and exponential_from_u = -log(1-u)/rate (rng.cpp:58-61; WLP_EDOMAIN for
+ * rate <= 0 or u outside [0,1), the reference's messages) through the same glibc-log port
+ * the mm1 kernels run (bit-identical to libm's on the FMA path). Bulk forms on the
+ * device: wlp_taus_stream, wlp_exponentials. */
+int wlp_taus_next(uint32_t state[3], uint32_t* out);
+int wlp_uniform01(uint32_t state[3], double* out);
+int wlp_exponential_from_u(double u, double rate, double* out);
+
 /* Exact rejection bookkeeping of random_spacing (rng.cpp:67-87) from the special
  * candidates of all shards: sorts them by index, marks every candidate whose key equals
  * an earlier accepted one, and merges with `prev`. Returns WLP_ESPACING if one stream
@@ -235,6 +245,34 @@ int wlp_run_shard(int model, const wlp_params* p, int mode, uint64_t master_seed
 int wlp_run(int model, const wlp_params* p, int mode, uint64_t master_seed, int tlp_block_size,
             double* out0, double* out1, double* out2, int out_on_device, void* stream,
             wlp_report* report, wlp_ci* ci, double level, char* warn, int warn_cap);
+
+/* run_model over several GPUs of this process (SURVEY §8b device_count): the run's
+ * replications are split into contiguous slices, device k = devices[k] runs
+ * [k*R/n, (k+1)*R/n) with one host thread per device, the random-spacing check is global
+ * (every slice's special candidates, as wlp_run_shard), and the confidence intervals
+ * come from the slices' statistics merged in device order (two passes about the merged
+ * mean; within 1e-12 of the single-device sums). Outputs are HOST arrays of R entries
+ * (each device writes its slice), bit-identical to wlp_run. Runs below 2^15
+ * replications per device use fewer devices (R < 2^16: devices[0] alone, exactly
+ * wlp_run). report: kernel_ms / cycles / waves the maximum over devices, counters summed.
+ * The calling thread's wlp_set_* settings apply to every device. */
+int wlp_run_devices(int model, const wlp_params* p, int mode, uint64_t master_seed, int tlp_block_size,
+                    const int* devices, int n_devices, double* out0, double* out1, double* out2,
+                    wlp_report* report, wlp_ci* ci, double level, char* warn, int warn_cap);
+
+/* The reference's *_replication_u templates (models.hpp:49-108) on the device: replication
+ * r runs the model body over the caller's uniforms u[r*2n .. r*2n + 2n), n = draws /
+ * clients / steps of p (p->replications is ignored; `count` replications), consuming them
+ * in the reference's order (pi: x then y; mm1: arrival then service; walk: direction then
+ * the discarded draw). Any double values, as the templates accept. One thread per
+ * replication; outputs as wlp_run_streams. Synchronous. */
+int wlp_run_uniforms(int model, const wlp_params* p, const double* u, int64_t count, int u_on_device,
+                     double* out0, double* out1, double* out2, int out_on_device, void* stream);
+
+/* exponential_from_u (rng.cpp:58-61) over n uniforms on the device (glibc-log port):
+ * out[i] = -log(1 - u[i]) / rate. WLP_EDOMAIN if rate <= 0 or any u outside [0,1).
+ * Synchronous. */
+int wlp_exponentials(const double* u, int64_t n, double rate, double* out, int on_device, void* stream);
 
 /* Experimental plan (BASELINE config 5): n_sets factor-level sets of one model, set k
  * being run_model(model, sets[k], mode, master_seeds[k]) — its own parameters, replication

@@ -143,6 +143,8 @@ class SimOptions:  # device.hpp:53-60
     irInterpreter: bool = False
     maxIssuesPerWarp: int = 1 << 50
     irJit: bool = False  # with irInterpreter: compile the IR kernel (NVRTC) instead
+    # B200 extension: shard run_model over GPUs 0..devices-1 of this process (wlp_run_devices)
+    devices: int = 1
 
 
 @dataclass
@@ -274,6 +276,13 @@ _SIGS = {
                                       C.POINTER(_Report)]),
     "wlp_ir_jit_source": (C.c_int, [_P, C.c_char_p, C.c_int, C.POINTER(C.c_int)]),
     "wlp_shutdown": (C.c_int, []),
+    "wlp_taus_next": (C.c_int, [_P, C.POINTER(C.c_uint32)]),
+    "wlp_uniform01": (C.c_int, [_P, C.POINTER(C.c_double)]),
+    "wlp_exponential_from_u": (C.c_int, [C.c_double, C.c_double, C.POINTER(C.c_double)]),
+    "wlp_run_devices": (C.c_int, [C.c_int, C.POINTER(_Params), C.c_int, C.c_uint64, C.c_int, _P, C.c_int, _P, _P,
+                                  _P, C.POINTER(_Report), C.POINTER(_CI), C.c_double, C.c_char_p, C.c_int]),
+    "wlp_run_uniforms": (C.c_int, [C.c_int, C.POINTER(_Params), _P, _I64, C.c_int, _P, _P, _P, C.c_int, _P]),
+    "wlp_exponentials": (C.c_int, [_P, _I64, C.c_double, _P, C.c_int, _P]),
 }
 EXPORTS = tuple(_SIGS)
 
@@ -495,6 +504,96 @@ def mm1_replication(clients: int, lambda_: float, mu: float, stream: RngState):
     return float(o["outIdle"][0]), float(o["outWait"][0]), float(o["outSys"][0])
 
 
+def taus_next(state: RngState) -> int:
+    """taus_next (rng.cpp:42-51): advances `state` in place, returns the output (host utility)."""
+    s = (C.c_uint32 * 3)(state.s1, state.s2, state.s3)
+    out = C.c_uint32()
+    _check(_lib.wlp_taus_next(s, C.byref(out)))
+    state.s1, state.s2, state.s3 = s
+    return out.value
+
+
+def uniform01(state: RngState) -> float:
+    """uniform01 (rng.cpp:53-55) = taus_next * 2^-32."""
+    return taus_next(state) * 2.0**-32
+
+
+def exponential_from_u(u: float, rate: float) -> float:
+    """exponential_from_u (rng.cpp:58-61): -log(1-u)/rate through the glibc-log port."""
+    out = C.c_double()
+    _check(_lib.wlp_exponential_from_u(float(u), float(rate), C.byref(out)))
+    return out.value
+
+
+def exponential(state: RngState, rate: float) -> float:
+    """exponential (rng.cpp:63-65)."""
+    return exponential_from_u(uniform01(state), rate)
+
+
+class TausStream:
+    """Callable uniform source over an owned state (rng.hpp:42-45)."""
+
+    def __init__(self, state: RngState):
+        self.state = RngState(state.s1, state.s2, state.s3)
+
+    def __call__(self) -> float:
+        return uniform01(self.state)
+
+
+def exponentials(u, rate: float) -> np.ndarray:
+    """exponential_from_u over an array, on the GPU (glibc-log port)."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    out = np.empty(len(u))
+    _check(_lib.wlp_exponentials(_ptr(u) if len(u) else None, len(u), float(rate), _ptr(out) if len(u) else None, 0,
+                                 None))
+    return out
+
+
+def run_uniforms(model: ModelKind, p: ModelParams, u) -> dict:
+    """The reference's *_replication_u bodies (models.hpp:49-108) on the GPU over explicit
+    uniforms: u is (count, 2*units) — row r is replication r's source, consumed in order."""
+    model = ModelKind(model)
+    n = p.units(model)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    if u.ndim == 1:
+        u = u.reshape(1, -1)
+    count = u.shape[0]
+    if count and u.shape[1] != 2 * n:
+        raise DomainError(f"run_uniforms: need {2 * n} uniforms per replication, got {u.shape[1]}")
+    outs = [np.empty(count) for _ in OUTPUT_NAMES[model]]
+    o = [_ptr(x) if count else None for x in outs] + [None] * (3 - len(outs))
+    _check(_lib.wlp_run_uniforms(int(model), C.byref(_params(p)), _ptr(u) if count else None, count, 0, o[0], o[1],
+                                 o[2], 0, None))
+    return dict(zip(OUTPUT_NAMES[model], outs))
+
+
+def _draw(units: int, nxt) -> np.ndarray:
+    return np.array([nxt() for _ in range(2 * units)], dtype=np.float64)
+
+
+def pi_replication_u(draws: int, nxt) -> float:
+    """pi_replication_u (models.hpp:49-59): `nxt` is called 2*draws times on the host, the
+    body runs on the GPU."""
+    p = ModelParams(draws=draws)
+    validate_params(ModelKind.Pi, p)
+    return float(run_uniforms(ModelKind.Pi, p, _draw(draws, nxt))["out"][0])
+
+
+def mm1_replication_u(clients: int, lambda_: float, mu: float, nxt):
+    """mm1_replication_u (models.hpp:61-84) -> (avgIdle, avgWaitQueue, avgSystem)."""
+    p = ModelParams(clients=clients, lambda_=lambda_, mu=mu)
+    validate_params(ModelKind.Mm1, p)
+    o = run_uniforms(ModelKind.Mm1, p, _draw(clients, nxt))
+    return float(o["outIdle"][0]), float(o["outWait"][0]), float(o["outSys"][0])
+
+
+def walk_replication_u(steps: int, chunks: int, nxt) -> float:
+    """walk_replication_u (models.hpp:86-108)."""
+    p = ModelParams(steps=steps, chunks=chunks)
+    validate_params(ModelKind.Walk, p)
+    return float(run_uniforms(ModelKind.Walk, p, _draw(steps, nxt))["out"][0])
+
+
 def walk_replication(steps: int, chunks: int, stream: RngState) -> float:
     """walk_replication (models.cpp:56-59)."""
     s = np.array([[stream.s1], [stream.s2], [stream.s3]], dtype=np.uint32)
@@ -575,10 +674,41 @@ def run_model(model: ModelKind, p: ModelParams, mode: ExecutionMode, prof: Optio
     o = [_ptr(x) for x in outs] + [None] * (3 - len(outs))
     rep = _Report()
     warn = C.create_string_buffer(512)
+    devices = opts.devices if opts is not None else 1
+    if devices > 1:  # contiguous slices over GPUs 0..devices-1, one host thread each
+        devs = (C.c_int * devices)(*range(devices))
+        _check(_lib.wlp_run_devices(int(model), C.byref(_params(p)), int(mode), master_seed & (2**64 - 1),
+                                    int(tlp_block_size), devs, devices, o[0], o[1], o[2],
+                                    C.byref(rep) if timed else None, None, 0.95, warn, 512))
+        outputs = dict(zip(names, outs))
+        return ModelRun(outputs, outputs[PRIMARY[model]], _report(rep), plan.cfg, mode, warn.value.decode() or None)
     _check(_lib.wlp_run(int(model), C.byref(_params(p)), int(mode), master_seed & (2**64 - 1), int(tlp_block_size),
                         o[0], o[1], o[2], 0, None, C.byref(rep) if timed else None, None, 0.95, warn, 512))
     outputs = dict(zip(names, outs))
     return ModelRun(outputs, outputs[PRIMARY[model]], _report(rep), plan.cfg, mode, warn.value.decode() or None)
+
+
+def run_devices(model: ModelKind, p: ModelParams, mode: ExecutionMode, master_seed: int, devices: Sequence[int],
+                outs=None, *, ci_level: Optional[float] = None, tlp_block_size: int = 256,
+                report: Optional[SimReport] = None):
+    """run_model over several GPUs of this process (wlp_run_devices): host output arrays
+    (allocated when outs is None), bit-identical to run_model; returns (outs, CIs or None)."""
+    model = ModelKind(model)
+    names = OUTPUT_NAMES[model]
+    if outs is None:
+        outs = [np.empty(int(p.replications)) for _ in names]
+    o = [_ptr(x) for x in outs] + [None] * (3 - len(outs))
+    devs = (C.c_int * max(len(devices), 1))(*devices)
+    cis = (_CI * len(names))() if ci_level is not None else None
+    rep = _Report() if report is not None else None
+    _check(_lib.wlp_run_devices(int(model), C.byref(_params(p)), int(mode), master_seed & (2**64 - 1),
+                                int(tlp_block_size), devs, len(devices), o[0], o[1], o[2],
+                                C.byref(rep) if rep is not None else None, cis, float(ci_level or 0.95), None, 0))
+    if rep is not None:
+        report.__dict__.update(vars(_report(rep)))
+    ci = None if cis is None else [ConfidenceInterval(c.mean, c.half_width, c.level, c.n,
+                                                      bool(c.warn_small_sample)) for c in cis]
+    return outs, ci
 
 
 def run_model_into(model: ModelKind, p: ModelParams, mode: ExecutionMode, master_seed: int, outs, *,

@@ -148,6 +148,23 @@ cudaError_t launch_plan(int model, int mode, const PlanArgs& a, const uint32_t* 
                         cudaStream_t st);
 int plan_blocks_per_sm(int model);
 
+// The reference's *_replication_u bodies over caller-given uniforms (uniforms.cu):
+// replication r reads u[r*2n, r*2n + 2n), one thread per replication.
+struct UniArgs {
+    int model;
+    const double* u;
+    int64_t count, n, chunks;
+    double lambda, mu;
+    double* out0;
+    double* out1;
+    double* out2;
+};
+cudaError_t launch_uniform_reps(const UniArgs& a, cudaStream_t st);
+// exponential_from_u (rng.cpp:58-61) over u[n]; *bad (init ~0) gets the lowest index
+// with u outside [0, 1).
+cudaError_t launch_exponentials(const double* u, int64_t n, double rate, double* out, unsigned long long* bad,
+                                cudaStream_t st);
+
 // Stats: per-block partials [grid][4] (sum_hi, sum_lo or ss_hi, ss_lo) of x (pass 1
 // about 0, pass 2 about `center`).
 cudaError_t launch_stats(const double* x, int64_t n, int pass, double center, double* partials,

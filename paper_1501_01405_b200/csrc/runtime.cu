@@ -8,16 +8,19 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <condition_variable>
 #include <cstring>
 #include <map>
 #include <memory>
 #include <mutex>
 #include <set>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
 #include "../../include/wlp_b200.h"
+#include "glibc_log.cuh"
 #include "jump.hpp"
 #include "ir_interp.cuh"
 #include "kernels.cuh"
@@ -734,6 +737,30 @@ int wlp_jump_host(const uint32_t s[3], uint64_t n, uint32_t out[3]) {
 
 int wlp_inverse_normal_cdf(double p, double* z) { return inv_normal(p, z); }
 
+int wlp_taus_next(uint32_t state[3], uint32_t* out) {
+    Taus t{state[0], state[1], state[2]};
+    const uint32_t o = taus_next(t);
+    state[0] = t.s1;
+    state[1] = t.s2;
+    state[2] = t.s3;
+    if (out) *out = o;
+    return WLP_OK;
+}
+
+int wlp_uniform01(uint32_t state[3], double* out) {
+    uint32_t o = 0;
+    wlp_taus_next(state, &o);
+    *out = static_cast<double>(o) * 0x1p-32;
+    return WLP_OK;
+}
+
+int wlp_exponential_from_u(double u, double rate, double* out) {
+    if (!(rate > 0.0)) return fail(WLP_EDOMAIN, "exponential: rate must be > 0");
+    if (!(u >= 0.0 && u < 1.0)) return fail(WLP_EDOMAIN, "exponential: u outside [0,1)");
+    *out = -glibc_log_tab(1.0 - u, kLogTabHost) / rate;
+    return WLP_OK;
+}
+
 int wlp_spacing_rejections(const wlp_special* specials, int64_t n_special, const int64_t* prev, int64_t n_prev,
                            int64_t* out, int64_t out_cap, int64_t* n_out) {
     std::vector<SpecialRec> sp(n_special);
@@ -1042,6 +1069,305 @@ int wlp_run(int model, const wlp_params* p, int mode, uint64_t master_seed, int 
         float ms = 0.f;
         WLP_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
         fill_report(*c, model, mode, tlp_block_size, R, grid, ms, report);
+    }
+    return WLP_OK;
+}
+
+// ---- the reference's *_replication_u bodies and exponential_from_u on the device ----
+
+int wlp_run_uniforms(int model, const wlp_params* p, const double* u, int64_t count, int u_on_device,
+                     double* out0, double* out1, double* out2, int out_on_device, void* stream) {
+    if (model < 0 || model > 2) return fail(WLP_EDOMAIN, "unknown model id");
+    if (count < 0) return fail(WLP_EDOMAIN, "run_uniforms: negative count");
+    wlp_params q = *p;
+    q.replications = 1;
+    WLP_TRY(validate(model, &q, nullptr));  // the templates' DomainErrors (models.hpp:51, 63-64, 88-89)
+    if (count == 0) return WLP_OK;
+    const int64_t n = units_of(model, q);
+    if (n > (int64_t(1) << 40) / std::max<int64_t>(count, 1)) return fail(WLP_EPLAN, "run_uniforms: too many uniforms");
+    DevCtx* c;
+    std::unique_lock<std::mutex> lk;
+    WLP_TRY(acquire(c, lk));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamOrder so(*c, st);
+    const int64_t nu = 2 * n * count;
+    const double* du = u;
+    DevBuf<double> ubuf, obuf;
+    if (!u_on_device) {
+        WLP_CUDA(ubuf.ensure(nu));
+        WLP_CUDA(cudaMemcpyAsync(ubuf.p, u, nu * 8, cudaMemcpyHostToDevice, st));
+        du = ubuf.p;
+    }
+    const int nout = n_outputs(model);
+    UniArgs a{model, du, count, n, q.chunks, q.lambda, q.mu, out0, out1, out2};
+    if (!out_on_device) {
+        WLP_CUDA(obuf.ensure(nout * count));
+        a.out0 = obuf.p;
+        a.out1 = obuf.p + count;
+        a.out2 = obuf.p + 2 * count;
+    }
+    WLP_CUDA(launch_uniform_reps(a, st));
+    g_last_kernel = "k_uniform_reps";
+    if (!out_on_device) {
+        double* host[3] = {out0, out1, out2};
+        double* dev[3] = {a.out0, a.out1, a.out2};
+        for (int k = 0; k < nout; ++k) WLP_CUDA(cudaMemcpyAsync(host[k], dev[k], count * 8, cudaMemcpyDeviceToHost, st));
+    }
+    WLP_CUDA(cudaStreamSynchronize(st));  // the scratch buffers are released on return
+    ubuf.release();
+    obuf.release();
+    return WLP_OK;
+}
+
+int wlp_exponentials(const double* u, int64_t n, double rate, double* out, int on_device, void* stream) {
+    if (!(rate > 0.0)) return fail(WLP_EDOMAIN, "exponential: rate must be > 0");
+    if (n < 0) return fail(WLP_EDOMAIN, "exponentials: negative count");
+    if (n == 0) return WLP_OK;
+    DevCtx* c;
+    std::unique_lock<std::mutex> lk;
+    WLP_TRY(acquire(c, lk));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamOrder so(*c, st);
+    DevBuf<double> buf;
+    const double* du = u;
+    double* dout = out;
+    if (!on_device) {
+        WLP_CUDA(buf.ensure(2 * n));
+        WLP_CUDA(cudaMemcpyAsync(buf.p, u, n * 8, cudaMemcpyHostToDevice, st));
+        du = buf.p;
+        dout = buf.p + n;
+    }
+    WLP_CUDA(cudaMemsetAsync(c->work.p, 0xFF, 8, st));
+    WLP_CUDA(launch_exponentials(du, n, rate, dout, c->work.p, st));
+    unsigned long long bad = 0;
+    WLP_CUDA(cudaMemcpyAsync(&bad, c->work.p, 8, cudaMemcpyDeviceToHost, st));
+    if (!on_device) WLP_CUDA(cudaMemcpyAsync(out, dout, n * 8, cudaMemcpyDeviceToHost, st));
+    WLP_CUDA(cudaStreamSynchronize(st));
+    buf.release();
+    if (bad != ~0ull) return fail(WLP_EDOMAIN, "exponential: u outside [0,1)");
+    return WLP_OK;
+}
+
+// ---- run_model over several GPUs of this process ----------------------------------
+
+}  // extern "C"
+
+namespace wlp {
+namespace {
+
+// Host barrier for the per-device worker threads; abort() releases every waiter (a
+// worker failed) and later waits return false.
+class Barrier {
+public:
+    explicit Barrier(int n) : n_(n) {}
+    bool wait() {
+        std::unique_lock<std::mutex> l(m_);
+        if (aborted_) return false;
+        const int64_t gen = gen_;
+        if (++arrived_ == n_) {
+            arrived_ = 0;
+            ++gen_;
+            cv_.notify_all();
+            return true;
+        }
+        cv_.wait(l, [&] { return gen_ != gen || aborted_; });
+        return !aborted_;
+    }
+    void abort() {
+        std::lock_guard<std::mutex> l(m_);
+        aborted_ = true;
+        cv_.notify_all();
+    }
+
+private:
+    std::mutex m_;
+    std::condition_variable cv_;
+    int n_, arrived_ = 0;
+    int64_t gen_ = 0;
+    bool aborted_ = false;
+};
+
+struct DevShard {
+    int dev = 0;
+    int64_t begin = 0, count = 0;
+    std::vector<SpecialRec> specials;
+    wlp_stats first[3]{}, second[3]{};
+    wlp_report rep{};
+    int rc = WLP_OK;
+    std::string err;
+};
+
+// The calling thread's settings, applied in each worker (they are thread-local).
+struct ThreadSettings {
+    bool hw;
+    int wv, tv;
+    void apply() const {
+        g_hw_counters = hw;
+        g_wlp_variant = wv;
+        g_tlp_variant = tv;
+    }
+};
+
+wlp_stats merged(const std::vector<DevShard>& sh, int k, bool second) {
+    wlp_stats acc{};
+    for (const DevShard& s : sh) {  // device order: every worker computes the same numbers
+        const wlp_stats& b = second ? s.second[k] : s.first[k];
+        acc.n += b.n;
+        dd_add(acc.sum_hi, acc.sum_lo, b.sum_hi);
+        acc.sum_lo += b.sum_lo;
+        dd_add(acc.ss_hi, acc.ss_lo, b.ss_hi);
+        acc.ss_lo += b.ss_lo;
+    }
+    return acc;
+}
+
+// One device's part of wlp_run_devices: seed + model for its contiguous slice, the
+// global spacing check (every worker reads every slice's specials after a barrier), the
+// two statistics passes about the merged mean, and the slice's outputs to the host.
+int run_device_shard(int model, const wlp_params& p, int mode, Taus master, int tlp_block, std::vector<DevShard>& sh,
+                     int k, Barrier& bar, double* const host[3], std::vector<int64_t>& rej_out) {
+    DevShard& me = sh[k];
+    WLP_CUDA(cudaSetDevice(me.dev));
+    DevCtx* c;
+    std::unique_lock<std::mutex> lk;
+    WLP_TRY(acquire(c, lk));
+    cudaStream_t st = nullptr;
+    WLP_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() { cudaStreamDestroy(s); }
+    } guard{st};
+    StreamOrder so(*c, st);
+    const int64_t n = me.count;
+    const int nout = n_outputs(model);
+    WLP_CUDA(c->seeds.ensure(3 * n));
+    WLP_CUDA(c->outs.ensure(3 * n));
+    double* o[3] = {c->outs.p, c->outs.p + n, c->outs.p + 2 * n};
+    std::vector<int64_t> rej;
+    int grid = 0;
+    for (;;) {
+        WLP_TRY(seed_async(*c, master, me.begin, n, rej, c->seeds.p, st, walk_planes(*c, model, mode, p, n)));
+        WLP_CUDA(cudaEventRecord(c->ev0, st));
+        WLP_TRY(model_async(*c, model, p, mode, tlp_block, c->seeds.p, n, o[0], o[1], o[2], st, grid));
+        WLP_CUDA(cudaEventRecord(c->ev1, st));
+        int64_t nt = 0;
+        WLP_TRY(read_specials(*c, st, me.specials, nt));
+        if (!bar.wait()) return fail(WLP_EINTERNAL, "another device failed");
+        std::vector<SpecialRec> all;
+        for (const DevShard& s : sh) all.insert(all.end(), s.specials.begin(), s.specials.end());
+        std::vector<int64_t> next = rej;
+        if (all.size() >= 2) WLP_TRY(spacing_rejections(all, rej, next));
+        if (!bar.wait()) return fail(WLP_EINTERNAL, "another device failed");  // specials read by all
+        if (next == rej) break;
+        rej.swap(next);
+    }
+    for (int j = 0; j < nout; ++j) WLP_TRY(stats_device(*c, o[j], n, 1, &me.first[j], st));
+    if (!bar.wait()) return fail(WLP_EINTERNAL, "another device failed");
+    for (int j = 0; j < nout; ++j) {
+        const wlp_stats tot = merged(sh, j, false);
+        me.second[j].center = (tot.sum_hi + tot.sum_lo) / static_cast<double>(tot.n);
+        WLP_TRY(stats_device(*c, o[j], n, 2, &me.second[j], st));
+    }
+    for (int j = 0; j < nout; ++j)
+        WLP_CUDA(cudaMemcpyAsync(host[j] + me.begin, o[j], n * 8, cudaMemcpyDeviceToHost, st));
+    WLP_CUDA(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    WLP_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    fill_report(*c, model, mode, tlp_block, n, grid, ms, &me.rep);
+    if (k == 0) rej_out = rej;
+    return WLP_OK;
+}
+
+}  // namespace
+}  // namespace wlp
+
+extern "C" {
+
+int wlp_run_devices(int model, const wlp_params* p, int mode, uint64_t master_seed, int tlp_block_size,
+                    const int* devices, int n_devices, double* out0, double* out1, double* out2, wlp_report* report,
+                    wlp_ci* ci, double level, char* warn, int warn_cap) {
+    WLP_TRY(check_model_mode(model, mode));
+    std::string pw, lw;
+    WLP_TRY(validate(model, p, &pw));
+    WLP_TRY(plan(p->replications, mode, tlp_block_size, 0x7FFFFFFF, nullptr, &lw));
+    if (n_devices < 1 || !devices) return fail(WLP_EDOMAIN, "run_devices: need at least one device");
+    int have = 0;
+    WLP_CUDA(cudaGetDeviceCount(&have));
+    std::set<int> distinct;
+    for (int k = 0; k < n_devices; ++k) {
+        if (devices[k] < 0 || devices[k] >= have)
+            return fail(WLP_EDOMAIN, "run_devices: device " + std::to_string(devices[k]) + " does not exist (" +
+                                         std::to_string(have) + " visible)");
+        distinct.insert(devices[k]);
+    }
+    if (static_cast<int>(distinct.size()) != n_devices) return fail(WLP_EDOMAIN, "run_devices: a device is listed twice");
+    if (!out0 || (model == WLP_MODEL_MM1 && (!out1 || !out2))) return fail(WLP_EDOMAIN, "run_devices: null output");
+    if (ci && !(level > 0.0 && level < 1.0)) return fail(WLP_EDOMAIN, "confidence_interval: level outside (0,1)");
+    const int64_t R = p->replications;
+    // A run below 2^15 replications per device stays on the first device (the sums are
+    // then wlp_run's, bit for bit, and sharding would only add launch latency).
+    const int nd = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(n_devices, R >> 15)));
+    std::vector<DevShard> sh(nd);
+    for (int k = 0; k < nd; ++k) {
+        sh[k].dev = devices[k];
+        sh[k].begin = R * k / nd;
+        sh[k].count = R * (k + 1) / nd - sh[k].begin;
+    }
+    int prev_dev = 0;
+    WLP_CUDA(cudaGetDevice(&prev_dev));
+    if (nd == 1) {
+        WLP_CUDA(cudaSetDevice(devices[0]));
+        const int rc = wlp_run(model, p, mode, master_seed, tlp_block_size, out0, out1, out2, 0, nullptr, report, ci,
+                               level, warn, warn_cap);
+        cudaSetDevice(prev_dev);
+        return rc;
+    }
+    copy_warning(!pw.empty() && !lw.empty() ? pw + "; " + lw : (!pw.empty() ? pw : lw), warn, warn_cap);
+    const ThreadSettings ts{g_hw_counters, g_wlp_variant, g_tlp_variant};
+    const Taus master = master_from_seed(master_seed);
+    double* const host[3] = {out0, out1, out2};
+    Barrier bar(nd);
+    std::vector<int64_t> rej;
+    std::vector<std::thread> th;
+    const char* kernel = "";
+    for (int k = 0; k < nd; ++k)
+        th.emplace_back([&, k] {
+            ts.apply();
+            sh[k].rc = run_device_shard(model, *p, mode, master, tlp_block_size, sh, k, bar, host, rej);
+            if (sh[k].rc != WLP_OK) {
+                sh[k].err = g_err;
+                bar.abort();
+            }
+            if (k == 0) kernel = g_last_kernel;
+        });
+    for (auto& t : th) t.join();
+    cudaSetDevice(prev_dev);
+    for (const DevShard& s : sh)  // the first real failure (not "another device failed")
+        if (s.rc != WLP_OK && s.err != "another device failed") return fail(s.rc, s.err);
+    for (const DevShard& s : sh)
+        if (s.rc != WLP_OK) return fail(s.rc, s.err);
+    g_last_kernel = kernel;
+    if (ci) {
+        for (int j = 0; j < n_outputs(model); ++j) {
+            wlp_stats s = merged(sh, j, false);
+            const wlp_stats s2 = merged(sh, j, true);
+            s.center = (s.sum_hi + s.sum_lo) / static_cast<double>(s.n);
+            s.ss_hi = s2.ss_hi;
+            s.ss_lo = s2.ss_lo;
+            WLP_TRY(ci_from_stats(&s, level, &ci[j]));
+        }
+    }
+    if (report) {
+        std::memset(report, 0, sizeof *report);
+        for (const DevShard& s : sh) {
+            report->kernel_ms = std::max(report->kernel_ms, s.rep.kernel_ms);
+            report->total_cycles = std::max(report->total_cycles, s.rep.total_cycles);
+            report->waves_executed = std::max(report->waves_executed, s.rep.waves_executed);
+            report->peak_resident_warps += s.rep.peak_resident_warps;
+            report->divergence_events += s.rep.divergence_events;
+            report->mem_reads += s.rep.mem_reads;
+            report->mem_writes += s.rep.mem_writes;
+        }
     }
     return WLP_OK;
 }

@@ -141,6 +141,57 @@ std::vector<std::uint32_t> taus_stream(RngState& state, std::size_t n) {
     return out;
 }
 
+std::uint32_t taus_next(RngState& state) {
+    std::uint32_t s[3] = {state.s1, state.s2, state.s3}, out = 0;
+    check(wlp_taus_next(s, &out));
+    state = RngState{s[0], s[1], s[2]};
+    return out;
+}
+
+double uniform01(RngState& state) { return taus_next(state) * 0x1p-32; }
+
+double exponential_from_u(double u, double rate) {
+    double out = 0.0;
+    check(wlp_exponential_from_u(u, rate, &out));
+    return out;
+}
+
+double exponential(RngState& state, double rate) { return exponential_from_u(uniform01(state), rate); }
+
+int device_count() {
+    int n = 0;
+    check(wlp_device_count(&n));
+    return n;
+}
+
+namespace detail {
+
+void check_u(ModelKind model, std::int64_t units, std::int64_t chunks, double lambda, double mu) {
+    ModelParams p;
+    p.replications = 1;
+    p.draws = p.clients = p.steps = units;
+    p.chunks = model == ModelKind::Walk ? chunks : 2;
+    p.lambda = model == ModelKind::Mm1 ? lambda : 0.5;
+    p.mu = model == ModelKind::Mm1 ? mu : 1.0;
+    const wlp_params c = to_c(p);
+    check(wlp_validate_params(model_id(model), &c, nullptr, 0));
+}
+
+std::vector<double> run_u(ModelKind model, std::int64_t units, std::int64_t chunks, double lambda, double mu,
+                          const std::vector<double>& u) {
+    ModelParams p;
+    p.draws = p.clients = p.steps = units;
+    p.chunks = model == ModelKind::Walk ? chunks : 2;
+    p.lambda = model == ModelKind::Mm1 ? lambda : 0.5;
+    p.mu = model == ModelKind::Mm1 ? mu : 1.0;
+    const wlp_params c = to_c(p);
+    std::vector<double> o(3, 0.0);
+    check(wlp_run_uniforms(model_id(model), &c, u.data(), 1, 0, &o[0], &o[1], &o[2], 0, nullptr));
+    return o;
+}
+
+}  // namespace detail
+
 LaunchPlan plan_launch(std::int64_t replications, ExecutionMode mode, const DeviceProfile& prof, int tlp_block_size,
                        std::int64_t grid_limit) {
     // the reference's order (wlp.cpp:73-76); the C layer adds CUDA's 1024-thread limit
@@ -239,9 +290,17 @@ ModelRun run_model(ModelKind model, const ModelParams& p, ExecutionMode mode, co
     std::vector<double> o0(R), o1(mm1 ? R : 0), o2(mm1 ? R : 0);
     wlp_report rep{};
     char warn[512];
-    check(wlp_run(model_id(model), &c, mode_id(mode), master_seed, tlp_block_size, o0.data(),
-                  mm1 ? o1.data() : nullptr, mm1 ? o2.data() : nullptr, 0, nullptr, &rep, nullptr, 0.95, warn,
-                  sizeof warn));
+    if (opts.devices > 1) {  // contiguous slices over GPUs 0..devices-1 (wlp_run_devices)
+        std::vector<int> devs(static_cast<std::size_t>(opts.devices));
+        for (int k = 0; k < opts.devices; ++k) devs[static_cast<std::size_t>(k)] = k;
+        check(wlp_run_devices(model_id(model), &c, mode_id(mode), master_seed, tlp_block_size, devs.data(),
+                              opts.devices, o0.data(), mm1 ? o1.data() : nullptr, mm1 ? o2.data() : nullptr, &rep,
+                              nullptr, 0.95, warn, sizeof warn));
+    } else {
+        check(wlp_run(model_id(model), &c, mode_id(mode), master_seed, tlp_block_size, o0.data(),
+                      mm1 ? o1.data() : nullptr, mm1 ? o2.data() : nullptr, 0, nullptr, &rep, nullptr, 0.95, warn,
+                      sizeof warn));
+    }
     if (warn[0]) run.warning = std::string(warn);
     run.report = from_c(rep);
     if (mm1) {
