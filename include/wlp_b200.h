@@ -255,7 +255,9 @@ int wlp_run(int model, const wlp_params* p, int mode, uint64_t master_seed, int 
  * (each device writes its slice), bit-identical to wlp_run. Runs below 2^15
  * replications per device use fewer devices (R < 2^16: devices[0] alone, exactly
  * wlp_run). report: kernel_ms / cycles / waves the maximum over devices, counters summed.
- * The calling thread's wlp_set_* settings apply to every device. */
+ * The calling thread's wlp_set_* settings apply to every device. A device may be listed
+ * more than once: its slices then take turns on it (phase by phase; this is how the
+ * multi-device path is exercised on a one-GPU box). */
 int wlp_run_devices(int model, const wlp_params* p, int mode, uint64_t master_seed, int tlp_block_size,
                     const int* devices, int n_devices, double* out0, double* out1, double* out2,
                     wlp_report* report, wlp_ci* ci, double level, char* warn, int warn_cap);

@@ -163,6 +163,18 @@ class Oracle:
         self._check(f(p, C.byref(z)))
         return z.value
 
+    def replications_u(self, model: int, p: _Params, u) -> dict:
+        """The reference's *_replication_u templates over rows of explicit uniforms
+        (reference only)."""
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        R = u.shape[0]
+        outs = [np.empty(R) for _ in OUTPUTS[model]]
+        ptrs = [o.ctypes.data for o in outs] + [None] * (3 - len(outs))
+        f = self._fn("replications_u")
+        f.argtypes = [C.c_int, C.POINTER(_Params), C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
+        self._check(f(model, C.byref(p), u.ctypes.data, R, *ptrs))
+        return dict(zip(OUTPUTS[model], outs))
+
     def exponential_from_u(self, u, rate: float) -> np.ndarray:
         u = np.ascontiguousarray(u, dtype=np.float64)
         out = np.empty_like(u)

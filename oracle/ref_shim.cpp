@@ -238,6 +238,33 @@ int ref_replications(int model, const RefParams* p, const std::uint32_t* s1,
     });
 }
 
+// The reference's *_replication_u templates (models.hpp:49-108) over explicit uniforms:
+// replication r's source yields u[r*2n ...] in order (pins wlp_run_uniforms).
+int ref_replications_u(int model, const RefParams* p, const double* u, std::int64_t count, double* o0,
+                       double* o1, double* o2) {
+    return guarded([&] {
+        warpsim::ModelKind mk = to_model(model);
+        const std::int64_t n = mk == warpsim::ModelKind::Pi ? p->draws
+                               : mk == warpsim::ModelKind::Mm1 ? p->clients : p->steps;
+        for (std::int64_t r = 0; r < count; ++r) {
+            const double* src = u + r * 2 * n;
+            std::int64_t i = 0;
+            auto next = [&] { return src[i++]; };
+            switch (mk) {
+                case warpsim::ModelKind::Pi: o0[r] = warpsim::pi_replication_u(p->draws, next); break;
+                case warpsim::ModelKind::Mm1: {
+                    warpsim::MM1Result m = warpsim::mm1_replication_u(p->clients, p->lambda, p->mu, next);
+                    o0[r] = m.avgIdle;
+                    o1[r] = m.avgWaitQueue;
+                    o2[r] = m.avgSystem;
+                    break;
+                }
+                case warpsim::ModelKind::Walk: o0[r] = warpsim::walk_replication_u(p->steps, p->chunks, next); break;
+            }
+        }
+    });
+}
+
 // confidence_interval (models.cpp:99-119).
 int ref_confidence_interval(const double* x, std::int64_t n, double level, double* mean,
                             double* half_width, std::int64_t* n_out, int* warn_small) {

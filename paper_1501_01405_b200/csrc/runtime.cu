@@ -1193,6 +1193,7 @@ struct DevShard {
     std::vector<SpecialRec> specials;
     wlp_stats first[3]{}, second[3]{};
     wlp_report rep{};
+    const char* kernel = "";
     int rc = WLP_OK;
     std::string err;
 };
@@ -1221,59 +1222,84 @@ wlp_stats merged(const std::vector<DevShard>& sh, int k, bool second) {
     return acc;
 }
 
-// One device's part of wlp_run_devices: seed + model for its contiguous slice, the
-// global spacing check (every worker reads every slice's specials after a barrier), the
-// two statistics passes about the merged mean, and the slice's outputs to the host.
+// One slice of wlp_run_devices, on its worker thread: seed + model into the slice's own
+// buffers, the global spacing check (every worker reads every slice's specials after a
+// barrier), the two statistics passes about the merged mean, and the slice's outputs to
+// the host. The device context is locked per phase only, never across a barrier, so a
+// device listed twice runs its slices one phase after another.
 int run_device_shard(int model, const wlp_params& p, int mode, Taus master, int tlp_block, std::vector<DevShard>& sh,
                      int k, Barrier& bar, double* const host[3], std::vector<int64_t>& rej_out) {
     DevShard& me = sh[k];
     WLP_CUDA(cudaSetDevice(me.dev));
-    DevCtx* c;
-    std::unique_lock<std::mutex> lk;
-    WLP_TRY(acquire(c, lk));
     cudaStream_t st = nullptr;
     WLP_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    struct StreamGuard {
+    struct Local {
         cudaStream_t s;
-        ~StreamGuard() { cudaStreamDestroy(s); }
-    } guard{st};
-    StreamOrder so(*c, st);
+        DevBuf<uint32_t> seeds;
+        DevBuf<double> outs;
+        ~Local() {
+            cudaStreamSynchronize(s);
+            seeds.release();
+            outs.release();
+            cudaStreamDestroy(s);
+        }
+    } loc{st};
     const int64_t n = me.count;
     const int nout = n_outputs(model);
-    WLP_CUDA(c->seeds.ensure(3 * n));
-    WLP_CUDA(c->outs.ensure(3 * n));
-    double* o[3] = {c->outs.p, c->outs.p + n, c->outs.p + 2 * n};
+    WLP_CUDA(loc.seeds.ensure(3 * n));
+    WLP_CUDA(loc.outs.ensure(3 * n));
+    double* o[3] = {loc.outs.p, loc.outs.p + n, loc.outs.p + 2 * n};
+    const std::string peer_failed = "another device failed";
     std::vector<int64_t> rej;
-    int grid = 0;
     for (;;) {
-        WLP_TRY(seed_async(*c, master, me.begin, n, rej, c->seeds.p, st, walk_planes(*c, model, mode, p, n)));
-        WLP_CUDA(cudaEventRecord(c->ev0, st));
-        WLP_TRY(model_async(*c, model, p, mode, tlp_block, c->seeds.p, n, o[0], o[1], o[2], st, grid));
-        WLP_CUDA(cudaEventRecord(c->ev1, st));
-        int64_t nt = 0;
-        WLP_TRY(read_specials(*c, st, me.specials, nt));
-        if (!bar.wait()) return fail(WLP_EINTERNAL, "another device failed");
+        {
+            DevCtx* c;
+            std::unique_lock<std::mutex> lk;
+            WLP_TRY(acquire(c, lk));
+            StreamOrder so(*c, st);
+            int grid = 0;
+            WLP_TRY(seed_async(*c, master, me.begin, n, rej, loc.seeds.p, st, walk_planes(*c, model, mode, p, n)));
+            WLP_CUDA(cudaEventRecord(c->ev0, st));
+            WLP_TRY(model_async(*c, model, p, mode, tlp_block, loc.seeds.p, n, o[0], o[1], o[2], st, grid));
+            WLP_CUDA(cudaEventRecord(c->ev1, st));
+            int64_t nt = 0;
+            WLP_TRY(read_specials(*c, st, me.specials, nt));  // synchronises the stream
+            float ms = 0.f;
+            WLP_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+            fill_report(*c, model, mode, tlp_block, n, grid, ms, &me.rep);
+            me.kernel = g_last_kernel;
+        }
+        if (!bar.wait()) return fail(WLP_EINTERNAL, peer_failed);
         std::vector<SpecialRec> all;
         for (const DevShard& s : sh) all.insert(all.end(), s.specials.begin(), s.specials.end());
         std::vector<int64_t> next = rej;
         if (all.size() >= 2) WLP_TRY(spacing_rejections(all, rej, next));
-        if (!bar.wait()) return fail(WLP_EINTERNAL, "another device failed");  // specials read by all
+        if (!bar.wait()) return fail(WLP_EINTERNAL, peer_failed);  // every slice's specials read
         if (next == rej) break;
         rej.swap(next);
     }
-    for (int j = 0; j < nout; ++j) WLP_TRY(stats_device(*c, o[j], n, 1, &me.first[j], st));
-    if (!bar.wait()) return fail(WLP_EINTERNAL, "another device failed");
-    for (int j = 0; j < nout; ++j) {
-        const wlp_stats tot = merged(sh, j, false);
-        me.second[j].center = (tot.sum_hi + tot.sum_lo) / static_cast<double>(tot.n);
-        WLP_TRY(stats_device(*c, o[j], n, 2, &me.second[j], st));
+    {
+        DevCtx* c;
+        std::unique_lock<std::mutex> lk;
+        WLP_TRY(acquire(c, lk));
+        StreamOrder so(*c, st);
+        for (int j = 0; j < nout; ++j) WLP_TRY(stats_device(*c, o[j], n, 1, &me.first[j], st));
+    }
+    if (!bar.wait()) return fail(WLP_EINTERNAL, peer_failed);
+    {
+        DevCtx* c;
+        std::unique_lock<std::mutex> lk;
+        WLP_TRY(acquire(c, lk));
+        StreamOrder so(*c, st);
+        for (int j = 0; j < nout; ++j) {
+            const wlp_stats tot = merged(sh, j, false);
+            me.second[j].center = (tot.sum_hi + tot.sum_lo) / static_cast<double>(tot.n);
+            WLP_TRY(stats_device(*c, o[j], n, 2, &me.second[j], st));
+        }
     }
     for (int j = 0; j < nout; ++j)
         WLP_CUDA(cudaMemcpyAsync(host[j] + me.begin, o[j], n * 8, cudaMemcpyDeviceToHost, st));
     WLP_CUDA(cudaStreamSynchronize(st));
-    float ms = 0.f;
-    WLP_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
-    fill_report(*c, model, mode, tlp_block, n, grid, ms, &me.rep);
     if (k == 0) rej_out = rej;
     return WLP_OK;
 }
@@ -1293,14 +1319,10 @@ int wlp_run_devices(int model, const wlp_params* p, int mode, uint64_t master_se
     if (n_devices < 1 || !devices) return fail(WLP_EDOMAIN, "run_devices: need at least one device");
     int have = 0;
     WLP_CUDA(cudaGetDeviceCount(&have));
-    std::set<int> distinct;
-    for (int k = 0; k < n_devices; ++k) {
+    for (int k = 0; k < n_devices; ++k)
         if (devices[k] < 0 || devices[k] >= have)
             return fail(WLP_EDOMAIN, "run_devices: device " + std::to_string(devices[k]) + " does not exist (" +
                                          std::to_string(have) + " visible)");
-        distinct.insert(devices[k]);
-    }
-    if (static_cast<int>(distinct.size()) != n_devices) return fail(WLP_EDOMAIN, "run_devices: a device is listed twice");
     if (!out0 || (model == WLP_MODEL_MM1 && (!out1 || !out2))) return fail(WLP_EDOMAIN, "run_devices: null output");
     if (ci && !(level > 0.0 && level < 1.0)) return fail(WLP_EDOMAIN, "confidence_interval: level outside (0,1)");
     const int64_t R = p->replications;
@@ -1329,7 +1351,6 @@ int wlp_run_devices(int model, const wlp_params* p, int mode, uint64_t master_se
     Barrier bar(nd);
     std::vector<int64_t> rej;
     std::vector<std::thread> th;
-    const char* kernel = "";
     for (int k = 0; k < nd; ++k)
         th.emplace_back([&, k] {
             ts.apply();
@@ -1338,7 +1359,6 @@ int wlp_run_devices(int model, const wlp_params* p, int mode, uint64_t master_se
                 sh[k].err = g_err;
                 bar.abort();
             }
-            if (k == 0) kernel = g_last_kernel;
         });
     for (auto& t : th) t.join();
     cudaSetDevice(prev_dev);
@@ -1346,7 +1366,7 @@ int wlp_run_devices(int model, const wlp_params* p, int mode, uint64_t master_se
         if (s.rc != WLP_OK && s.err != "another device failed") return fail(s.rc, s.err);
     for (const DevShard& s : sh)
         if (s.rc != WLP_OK) return fail(s.rc, s.err);
-    g_last_kernel = kernel;
+    g_last_kernel = sh[0].kernel;
     if (ci) {
         for (int j = 0; j < n_outputs(model); ++j) {
             wlp_stats s = merged(sh, j, false);

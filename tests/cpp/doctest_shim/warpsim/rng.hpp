@@ -1,0 +1,5 @@
+// TEST INFRASTRUCTURE: maps the reference test files' #include "warpsim/rng.hpp" onto the
+// drop-in headers (include/warpsim_b200.hpp, include/warpsim_ir_b200.hpp).
+#pragma once
+#include "warpsim_b200.hpp"
+#include "warpsim_ir_b200.hpp"
