@@ -137,6 +137,15 @@ int wlp_set_wlp_variant(int variant);
  * word (pi / mm1 keep the per-replication kernel). Outputs are identical. */
 int wlp_set_tlp_variant(int variant);
 
+/* Summation order of the device statistics (confidence intervals, wlp_stats_device) for
+ * later calls on this thread. 0 (default): accurate — a parallel double-double sum, within
+ * a few ulps of the exact sums (the reference's naive loop, models.cpp:104-109, drifts by up
+ * to ~n*2^-53 relative; 9e-12 at pi 10^7 x 10^3). 1: the reference's order — one
+ * sequential fp64 sum in index order, bit-identical to confidence_interval's at any n, at
+ * ~4 ns per sample (n <= 256 always sums this way). Multi-slice runs (wlp_run_devices,
+ * sharded statistics) merge slice sums, so their sums are the accurate kind either way. */
+int wlp_set_stats_order(int order);
+
 /* Name of the model kernel the last run on this thread launched (e.g. "k_wlp_pipe<pi>",
  * "k_wlp_walk_bs_pipe", "k_tlp_mm1"); "" before any run. Static storage. */
 const char* wlp_last_kernel(void);

@@ -277,6 +277,7 @@ _SIGS = {
     "wlp_ir_jit_source": (C.c_int, [_P, C.c_char_p, C.c_int, C.POINTER(C.c_int)]),
     "wlp_shutdown": (C.c_int, []),
     "wlp_taus_next": (C.c_int, [_P, C.POINTER(C.c_uint32)]),
+    "wlp_set_stats_order": (C.c_int, [C.c_int]),
     "wlp_uniform01": (C.c_int, [_P, C.POINTER(C.c_double)]),
     "wlp_exponential_from_u": (C.c_int, [C.c_double, C.c_double, C.POINTER(C.c_double)]),
     "wlp_run_devices": (C.c_int, [C.c_int, C.POINTER(_Params), C.c_int, C.c_uint64, C.c_int, _P, C.c_int, _P, _P,
@@ -635,6 +636,22 @@ class tlp_variant:
 
     def __exit__(self, *exc):
         _check(_lib.wlp_set_tlp_variant(0))
+
+
+class stats_order:
+    """Context manager: summation order of the device statistics on this thread
+    (wlp_set_stats_order): 0 accurate double-double (default), 1 the reference's
+    sequential order (confidence_interval bit for bit at any n)."""
+
+    def __init__(self, order: int):
+        self.order = order
+
+    def __enter__(self):
+        _check(_lib.wlp_set_stats_order(self.order))
+        return self
+
+    def __exit__(self, *exc):
+        _lib.wlp_set_stats_order(0)
 
 
 class hw_counters:

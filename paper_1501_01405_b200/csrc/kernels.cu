@@ -1744,6 +1744,54 @@ __global__ void __launch_bounds__(kStatsBlock) k_stats(const double* __restrict_
     }
 }
 
+// The reference's naive loop (models.cpp:104-109) for any n, bit for bit: the block stages
+// tiles of terms (x, or (x - center)^2) in shared memory, double buffered, and thread 0
+// adds them in order while the other threads load the next tile. The dependent DADD
+// chain (~8 cycles per sample) is the cost: ~4 ns per sample (opt-in, wlp_set_stats_order).
+constexpr int kSeqTile = 2048;
+__global__ void __launch_bounds__(kStatsBlock) k_stats_seq(const double* __restrict__ x, int64_t n, int pass,
+                                                           double center, double* __restrict__ partials) {
+    __shared__ double tile[2][kSeqTile];
+    const int64_t tiles = (n + kSeqTile - 1) / kSeqTile;
+    double s = 0.0;
+    auto load = [&](int64_t t, int buf) {
+        for (int j = threadIdx.x; j < kSeqTile; j += kStatsBlock) {
+            const int64_t i = t * kSeqTile + j;
+            if (i < n) tile[buf][j] = stat_term(__ldg(x + i), pass, center);
+        }
+    };
+    load(0, 0);
+    __syncthreads();
+    for (int64_t t = 0; t < tiles; ++t) {
+        const int buf = static_cast<int>(t & 1);
+        if (threadIdx.x == 0) {
+            const int64_t left = n - t * kSeqTile;
+            const int m = left < kSeqTile ? static_cast<int>(left) : kSeqTile;
+            const double* v = tile[buf];
+            int j = 0;
+            for (; j + 8 <= m; j += 8) {
+                double r[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) r[k] = v[j + k];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) s = __dadd_rn(s, r[k]);
+            }
+            for (; j < m; ++j) s = __dadd_rn(s, v[j]);
+        } else if (t + 1 < tiles) {
+            // threads 1.. load the next tile (thread 0's share goes to thread 1)
+            for (int j = threadIdx.x - 1; j < kSeqTile; j += kStatsBlock - 1) {
+                const int64_t i = (t + 1) * kSeqTile + j;
+                if (i < n) tile[buf ^ 1][j] = stat_term(__ldg(x + i), pass, center);
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        partials[0] = s;
+        partials[1] = 0.0;
+    }
+}
+
 size_t tlp_mm1_smem(int block) { return 256 * 8 + static_cast<size_t>((block + 31) / 32) * sizeof(TlpMm1Warp); }
 
 template <class K>
@@ -2032,7 +2080,11 @@ cudaError_t launch_plan(int model, int mode, const PlanArgs& a, const uint32_t* 
 }
 
 cudaError_t launch_stats(const double* x, int64_t n, int pass, double center, double* partials, int grid,
-                         cudaStream_t st) {
+                         cudaStream_t st, bool reference_order) {
+    if (reference_order && n > kStatsSeqMax) {
+        k_stats_seq<<<1, kStatsBlock, 0, st>>>(x, n, pass, center, partials);
+        return cudaGetLastError();
+    }
     if (n <= kStatsSeqMax) grid = 1;
     k_stats<<<grid, kStatsBlock, 0, st>>>(x, n, pass, center, partials);
     return cudaGetLastError();

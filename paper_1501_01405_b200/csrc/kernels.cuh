@@ -165,9 +165,10 @@ cudaError_t launch_uniform_reps(const UniArgs& a, cudaStream_t st);
 cudaError_t launch_exponentials(const double* u, int64_t n, double rate, double* out, unsigned long long* bad,
                                 cudaStream_t st);
 
-// Stats: per-block partials [grid][4] (sum_hi, sum_lo or ss_hi, ss_lo) of x (pass 1
-// about 0, pass 2 about `center`).
+// Stats: per-block partials [grid][2] (sum_hi, sum_lo or ss_hi, ss_lo) of x (pass 1
+// about 0, pass 2 about `center`). n <= 256 or reference_order: one partial, the
+// reference's sequential sum (models.cpp:104-109) bit for bit.
 cudaError_t launch_stats(const double* x, int64_t n, int pass, double center, double* partials,
-                         int grid, cudaStream_t st);
+                         int grid, cudaStream_t st, bool reference_order = false);
 
 }  // namespace wlp

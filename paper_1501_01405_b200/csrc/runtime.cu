@@ -35,6 +35,7 @@ thread_local bool g_hw_counters = false;  // wlp_set_hw_counters
 thread_local int g_wlp_variant = 0;       // wlp_set_wlp_variant: 0 auto, 1 lane jumps, 2 pipeline
 thread_local const char* g_last_kernel = "";  // wlp_last_kernel
 thread_local int g_tlp_variant = 0;       // wlp_set_tlp_variant: 0 auto, 1 per replication, 2 bitsliced walk
+thread_local int g_stats_order = 0;       // wlp_set_stats_order: 0 accurate (double-double), 1 reference
 
 // mm1 WLP segment chaining hands replications with lambda >= rho * mu to the serial
 // heavy-traffic loop; WLP_MM1_SERIAL_RHO overrides the measured default.
@@ -607,8 +608,9 @@ int stats_device(DevCtx& c, const double* x, int64_t n, int pass, wlp_stats* s, 
     const int grid = std::max(1, std::min<int>(c.sms * 4, static_cast<int>((n + 255) / 256)));
     WLP_CUDA(c.partials.ensure(2 * grid));
     const double center = pass == 1 ? 0.0 : s->center;
-    WLP_CUDA(launch_stats(x, n, pass, center, c.partials.p, grid, st));
-    const int used = n <= 256 ? 1 : grid;
+    const bool seq = g_stats_order == 1;
+    WLP_CUDA(launch_stats(x, n, pass, center, c.partials.p, grid, st, seq));
+    const int used = n <= 256 || seq ? 1 : grid;
     std::vector<double> h(2 * used);
     WLP_CUDA(cudaMemcpyAsync(h.data(), c.partials.p, h.size() * 8, cudaMemcpyDeviceToHost, st));
     WLP_CUDA(cudaStreamSynchronize(st));
@@ -688,6 +690,12 @@ const char* wlp_last_kernel(void) { return g_last_kernel; }
 int wlp_set_tlp_variant(int variant) {
     if (variant < 0 || variant > 2) return fail(WLP_EDOMAIN, "tlp variant must be 0 (auto), 1 or 2");
     g_tlp_variant = variant;
+    return WLP_OK;
+}
+
+int wlp_set_stats_order(int order) {
+    if (order < 0 || order > 1) return fail(WLP_EDOMAIN, "stats order must be 0 or 1");
+    g_stats_order = order;
     return WLP_OK;
 }
 
@@ -1201,11 +1209,12 @@ struct DevShard {
 // The calling thread's settings, applied in each worker (they are thread-local).
 struct ThreadSettings {
     bool hw;
-    int wv, tv;
+    int wv, tv, so;
     void apply() const {
         g_hw_counters = hw;
         g_wlp_variant = wv;
         g_tlp_variant = tv;
+        g_stats_order = so;
     }
 };
 
@@ -1345,7 +1354,7 @@ int wlp_run_devices(int model, const wlp_params* p, int mode, uint64_t master_se
         return rc;
     }
     copy_warning(!pw.empty() && !lw.empty() ? pw + "; " + lw : (!pw.empty() ? pw : lw), warn, warn_cap);
-    const ThreadSettings ts{g_hw_counters, g_wlp_variant, g_tlp_variant};
+    const ThreadSettings ts{g_hw_counters, g_wlp_variant, g_tlp_variant, g_stats_order};
     const Taus master = master_from_seed(master_seed);
     double* const host[3] = {out0, out1, out2};
     Barrier bar(nd);
