@@ -1,11 +1,8 @@
 // C++ drop-in API (include/warpsim_b200.hpp) over the C ABI of libwlp_b200.so.
 // Every model computation is a C-ABI call into the sm_100a kernels; this file holds only
-// argument plumbing, the reference's error mapping and the sweep/CSV bookkeeping
-// (reference proj/src/sweep.cpp:57-186 semantics, re-implemented).
-#include <charconv>
+// argument plumbing and the reference's error mapping (the sweep and its CSV form are in
+// sweep.cpp).
 #include <cstring>
-#include <fstream>
-#include <sstream>
 
 #include "warpsim_b200.hpp"
 #include "warpsim_ir_b200.hpp"
@@ -52,24 +49,6 @@ SimReport from_c(const wlp_report& r) {
 }
 
 std::vector<std::uint32_t> soa(const RngState& s) { return {s.s1, s.s2, s.s3}; }
-
-constexpr const char* kHeader =
-    "replications,mode,model,total_cycles,mem_reads,mem_writes,divergence_events,waves,mean,ci_low,ci_high";
-
-std::string fmt_double(double v) {
-    char buf[64];
-    auto res = std::to_chars(buf, buf + sizeof buf, v);  // shortest round trip, as sweep.cpp:18-22
-    return std::string(buf, res.ptr);
-}
-
-template <class T>
-T parse_num(const std::string& f, std::size_t line, const char* what) {
-    T v{};
-    auto res = std::from_chars(f.data(), f.data() + f.size(), v);
-    if (res.ec != std::errc{} || res.ptr != f.data() + f.size())
-        throw ParseError("csv line " + std::to_string(line) + ": bad " + what + " '" + f + "'");
-    return v;
-}
 
 }  // namespace
 
@@ -313,138 +292,6 @@ ModelRun run_model(ModelKind model, const ModelParams& p, ExecutionMode mode, co
         run.primary = run.outputs["out"];
     }
     return run;
-}
-
-// ---- sweep (reference sweep.hpp:42-60 semantics) ---------------------------------------
-
-std::vector<SweepRow> run_sweep(const SweepSpec& spec, const DeviceProfile& prof) {
-    if (spec.rMin < 1 || spec.rMin > spec.rMax) throw DomainError("sweep: need 1 <= rMin <= rMax");
-    if (spec.rStep < 1) throw DomainError("sweep: rStep must be >= 1");
-    if (spec.modes.empty()) throw DomainError("sweep: no execution modes selected");
-    std::vector<SweepRow> rows;
-    for (ExecutionMode mode : {ExecutionMode::Sequential, ExecutionMode::Tlp, ExecutionMode::Wlp}) {
-        bool on = false;
-        for (ExecutionMode m : spec.modes) on = on || m == mode;
-        if (!on) continue;
-        for (std::int64_t R = spec.rMin; R <= spec.rMax; R += spec.rStep) {
-            ModelParams params = spec.params;
-            params.replications = R;
-            SimOptions opts;
-            opts.irInterpreter = spec.irCounters;
-            const ModelRun run = run_model(spec.model, params, mode, prof, spec.masterSeed, spec.tlpBlockSize, opts);
-            SweepRow row;
-            row.replications = R;
-            row.mode = mode;
-            row.model = spec.model;
-            row.totalCycles = run.report.totalCycles;  // measured on the GPU
-            row.memReads = run.report.memReads;
-            row.memWrites = run.report.memWrites;
-            row.divergenceEvents = run.report.divergenceEvents;
-            row.waves = run.report.wavesExecuted;
-            if (run.primary.size() >= 2) {
-                const ConfidenceInterval ci = confidence_interval(run.primary);
-                row.mean = ci.mean;
-                row.ciLow = ci.low();
-                row.ciHigh = ci.high();
-            } else {
-                row.mean = row.ciLow = row.ciHigh = run.primary.at(0);
-            }
-            rows.push_back(row);
-        }
-    }
-    return rows;
-}
-
-std::vector<std::int64_t> detect_steps(const std::vector<std::pair<std::int64_t, std::int64_t>>& curve) {
-    std::vector<std::int64_t> steps;
-    for (std::size_t i = 1; i < curve.size(); ++i) {
-        if (curve[i].first <= curve[i - 1].first)
-            throw AnalysisError("step detection: curve not sorted by ascending R");
-        if (curve[i].second < curve[i - 1].second)
-            throw AnalysisError("step detection: cycles decreased at R=" + std::to_string(curve[i].first) +
-                                " — cost curves must be non-decreasing");
-        if (curve[i].second > curve[i - 1].second) steps.push_back(curve[i].first);
-    }
-    return steps;
-}
-
-std::vector<std::pair<std::int64_t, std::int64_t>> curve_of(const std::vector<SweepRow>& rows, ExecutionMode mode) {
-    std::vector<std::pair<std::int64_t, std::int64_t>> c;
-    for (const SweepRow& r : rows)
-        if (r.mode == mode) c.emplace_back(r.replications, r.totalCycles);
-    return c;
-}
-
-std::string csv_string(const std::vector<SweepRow>& rows) {
-    std::ostringstream out;
-    out << kHeader << '\n';
-    for (const SweepRow& r : rows)
-        out << r.replications << ',' << mode_name(r.mode) << ',' << model_name(r.model) << ',' << r.totalCycles << ','
-            << r.memReads << ',' << r.memWrites << ',' << r.divergenceEvents << ',' << r.waves << ','
-            << fmt_double(r.mean) << ',' << fmt_double(r.ciLow) << ',' << fmt_double(r.ciHigh) << '\n';
-    return out.str();
-}
-
-void emit_csv(const std::vector<SweepRow>& rows, const std::string& path) {
-    if (rows.empty()) throw DomainError("emit_csv: no rows");
-    std::ofstream out(path);
-    if (!out) throw Error("cannot write csv: " + path);
-    out << csv_string(rows);
-    if (!out.flush()) throw Error("write failed: " + path);
-}
-
-std::vector<SweepRow> parse_csv_string(const std::string& text) {
-    std::istringstream in(text);
-    std::string line;
-    std::size_t lineno = 0;
-    std::vector<SweepRow> rows;
-    while (std::getline(in, line)) {
-        ++lineno;
-        if (!line.empty() && line.back() == '\r') line.pop_back();
-        if (lineno == 1) {
-            if (line != kHeader) throw ParseError("csv line 1: unexpected header");
-            continue;
-        }
-        if (line.empty()) continue;
-        std::vector<std::string> f;
-        std::size_t start = 0;
-        for (;;) {
-            const std::size_t comma = line.find(',', start);
-            f.push_back(line.substr(start, comma == std::string::npos ? std::string::npos : comma - start));
-            if (comma == std::string::npos) break;
-            start = comma + 1;
-        }
-        if (f.size() != 11)
-            throw ParseError("csv line " + std::to_string(lineno) + ": expected 11 fields, got " +
-                             std::to_string(f.size()));
-        SweepRow r;
-        r.replications = parse_num<std::int64_t>(f[0], lineno, "integer");
-        try {
-            r.mode = mode_from_name(f[1]);
-            r.model = model_from_name(f[2]);
-        } catch (const DomainError& e) {
-            throw ParseError("csv line " + std::to_string(lineno) + ": " + e.what());
-        }
-        r.totalCycles = parse_num<std::int64_t>(f[3], lineno, "integer");
-        r.memReads = parse_num<std::uint64_t>(f[4], lineno, "integer");
-        r.memWrites = parse_num<std::uint64_t>(f[5], lineno, "integer");
-        r.divergenceEvents = parse_num<std::uint64_t>(f[6], lineno, "integer");
-        r.waves = parse_num<std::int64_t>(f[7], lineno, "integer");
-        r.mean = parse_num<double>(f[8], lineno, "real");
-        r.ciLow = parse_num<double>(f[9], lineno, "real");
-        r.ciHigh = parse_num<double>(f[10], lineno, "real");
-        rows.push_back(r);
-    }
-    if (rows.empty()) throw ParseError("csv: no data rows");
-    return rows;
-}
-
-std::vector<SweepRow> parse_csv(const std::string& path) {
-    std::ifstream in(path);
-    if (!in) throw Error("cannot open csv: " + path);
-    std::ostringstream buf;
-    buf << in.rdbuf();
-    return parse_csv_string(buf.str());
 }
 
 }  // namespace warpsim
