@@ -745,6 +745,18 @@ def run_model_into(model: ModelKind, p: ModelParams, mode: ExecutionMode, master
     return [ConfidenceInterval(c.mean, c.half_width, c.level, c.n, bool(c.warn_small_sample)) for c in cis]
 
 
+_SPECIAL_BUFS: dict = {}
+
+
+def _special_buffer(cap: int):
+    """A reused ctypes array for the specials a shard run reports (allocating and zeroing
+    ~100 KB per call showed up in small runs' host time)."""
+    b = _SPECIAL_BUFS.get(cap)
+    if b is None:
+        b = _SPECIAL_BUFS[cap] = (Special * cap)()
+    return b
+
+
 def run_shard(model: ModelKind, p: ModelParams, mode: ExecutionMode, master_seed: int, r_begin: int, r_count: int,
               outs, *, on_device: bool, rejected: Sequence[int] = (), stream: Optional[int] = None,
               tlp_block_size: int = 256, special_cap: int = 4096, report: Optional[SimReport] = None):
@@ -753,7 +765,7 @@ def run_shard(model: ModelKind, p: ModelParams, mode: ExecutionMode, master_seed
     with the model kernel's measured time (CUDA events on the launching stream)."""
     o = [_ptr(x) for x in outs] + [None] * (3 - len(outs))
     rej = np.asarray(sorted(rejected), dtype=np.int64)
-    sp = (Special * special_cap)()
+    sp = _special_buffer(special_cap)
     nsp = C.c_int64()
     rep = _Report() if report is not None else None
     _check(_lib.wlp_run_shard(int(model), C.byref(_params(p)), int(mode), master_seed & (2**64 - 1),
@@ -764,22 +776,40 @@ def run_shard(model: ModelKind, p: ModelParams, mode: ExecutionMode, master_seed
         report.__dict__.update(vars(_report(rep)))
     if nsp.value > special_cap:
         raise Error("too many special seeding candidates")
-    return list(sp[: nsp.value])
+    return [Special.from_buffer_copy(x) for x in sp[: nsp.value]]  # (the buffer is reused)
 
 
-def run_plan(model: ModelKind, sets: Sequence[ModelParams], master_seeds: Sequence[int], mode: ExecutionMode,
+class PlanSets:
+    """A plan's factor-level sets and master seeds marshalled once for the C ABI (the
+    per-set ctypes conversion costs ~2 us a set, 150 us for BASELINE config 5's 64 sets —
+    more than a third of the run). Pass it to run_plan in place of (sets, master_seeds)."""
+
+    def __init__(self, sets: Sequence[ModelParams], master_seeds: Sequence[int]):
+        if len(sets) != len(master_seeds):
+            raise DomainError("plan: one master seed per set")
+        n = len(sets)
+        self.sets = list(sets)
+        self.params = (_Params * max(n, 1))(*[_params(p) for p in sets])
+        self.seeds = (C.c_uint64 * max(n, 1))(*[s & (2**64 - 1) for s in master_seeds])
+        self.replications = [int(p.replications) for p in sets]
+        self.total = sum(self.replications)
+
+    def __len__(self) -> int:
+        return len(self.sets)
+
+
+def run_plan(model: ModelKind, sets, master_seeds: Optional[Sequence[int]], mode: ExecutionMode,
              outs=None, *, on_device: bool = False, stream: Optional[int] = None, tlp_block_size: int = 256,
              report: Optional[SimReport] = None):
     """Experimental plan (BASELINE config 5): every factor-level set k is
-    run_model(model, sets[k], mode, master_seeds[k]), all in one launch. Returns a list (per
+    run_model(model, sets[k], mode, master_seeds[k]), all in one launch. `sets` is a list of
+    ModelParams (with `master_seeds`) or a PlanSets (master_seeds None). Returns a list (per
     set) of output dicts when outs is None (host), else fills `outs` (concatenated)."""
     model = ModelKind(model)
-    n = len(sets)
-    if n != len(master_seeds):
-        raise DomainError("plan: one master seed per set")
-    arr = (_Params * max(n, 1))(*[_params(p) for p in sets])
-    seeds = (C.c_uint64 * max(n, 1))(*[s & (2**64 - 1) for s in master_seeds])
-    R = sum(int(p.replications) for p in sets)
+    ps = sets if isinstance(sets, PlanSets) else PlanSets(sets, master_seeds)
+    n = len(ps)
+    arr, seeds, R = ps.params, ps.seeds, ps.total
+    sets = ps.sets
     names = OUTPUT_NAMES[model]
     host = outs is None
     if host:

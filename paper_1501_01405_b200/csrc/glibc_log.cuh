@@ -219,23 +219,46 @@ __device__ __forceinline__ double log_table_dev(double x, const double* tab) {
 // * the result is negated in the final add (-(y + hi) == (-y) + (-hi) in round-to-nearest;
 //   y + hi is never an exact zero here since x != 1).
 // tools/log_check.cu compares it with the two-step form for every n.
+// The polynomial and ln2 constants as constant-bank operands: a DFMA takes one c[][]
+// operand directly, where immediates would be rebuilt in registers (two moves per
+// double) wherever the compiler does not keep them live across a loop.
+__constant__ double kLogTabConstDev[7] = {WLP_LOG_LN2HI, WLP_LOG_LN2LO, -0x1.0000000000001p-1, 0x1.555555551305bp-2,
+                                          -0x1.fffffffeb4590p-3, 0x1.999b324f10111p-3, -0x1.55575e506c89fp-3};
+
+constexpr double kLogPolyCheck[5] = WLP_LOG_POLY_INIT;
+static_assert(kLogPolyCheck[0] == -0x1.0000000000001p-1 && kLogPolyCheck[1] == 0x1.555555551305bp-2 &&
+                  kLogPolyCheck[2] == -0x1.fffffffeb4590p-3 && kLogPolyCheck[3] == 0x1.999b324f10111p-3 &&
+                  kLogPolyCheck[4] == -0x1.55575e506c89fp-3,
+              "kLogTabConstDev follows WLP_LOG_POLY_INIT");
+
+#ifndef WLP_LOG_NOI2F
+#define WLP_LOG_NOI2F 0
+#endif
 __device__ __forceinline__ double neg_log1m_table_dev(uint32_t n, const double* tab) {
+#if WLP_LOG_NOI2F & 1
+    const double dm = __dsub_rn(__hiloint2double(0x43300000, static_cast<int>(0u - n)), 0x1p52);
+#else
     const double dm = __uint2double_rn(0u - n);
+#endif
     const uint32_t hm = static_cast<uint32_t>(__double2hiint(dm));
     const uint32_t thi = hm - (0x3fe60000u + (32u << 20));  // == hi(x) - hi(OFF)
     const int i = static_cast<int>((thi >> 13) & 127u);
     const int k = static_cast<int>(thi) >> 20;
     const double z = __hiloint2double(static_cast<int>(hm - (thi & 0xfff00000u) - (32u << 20)), __double2loint(dm));
     const double2 c = reinterpret_cast<const double2*>(tab)[i];  // {invc, logc}
+#if WLP_LOG_NOI2F & 2
+    const double kd = __dsub_rn(__hiloint2double(0x43380000 + (k >> 31), k), 0x1.8p52);
+#else
     const double kd = static_cast<double>(k);
-    constexpr double A[5] = WLP_LOG_POLY_INIT;
+#endif
+    const double* K = kLogTabConstDev;  // ln2hi, ln2lo, A[0..4] (WLP_LOG_POLY_INIT)
     const double r = __fma_rn(z, c.x, -1.0);
-    const double w = __fma_rn(kd, WLP_LOG_LN2HI, c.y);
+    const double w = __fma_rn(kd, K[0], c.y);
     const double hi = __dadd_rn(r, w);
-    const double lo = __fma_rn(kd, WLP_LOG_LN2LO, __dadd_rn(__dsub_rn(w, hi), r));
+    const double lo = __fma_rn(kd, K[1], __dadd_rn(__dsub_rn(w, hi), r));
     const double r2 = __dmul_rn(r, r);
-    const double q = __fma_rn(__fma_rn(r, A[4], A[3]), r2, __fma_rn(r, A[2], A[1]));
-    const double y = __fma_rn(__dmul_rn(r, r2), q, __fma_rn(r2, A[0], lo));
+    const double q = __fma_rn(__fma_rn(r, K[6], K[5]), r2, __fma_rn(r, K[4], K[3]));
+    const double y = __fma_rn(__dmul_rn(r, r2), q, __fma_rn(r2, K[2], lo));
     return __dadd_rn(-y, -hi);
 }
 #endif

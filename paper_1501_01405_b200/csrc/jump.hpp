@@ -116,6 +116,20 @@ inline std::vector<uint32_t> uniform_table(uint64_t n) {
     return out;
 }
 
+// Binary powers as nibble tables [k][comp][p][v] (96 KB) for the device jumps: applying
+// M^(2^k) to a word is 8 independent lookups and an XOR tree, not 32 masked columns in a
+// dependent chain (jump-ahead latency is what bounds the seeding of small runs).
+inline std::vector<uint32_t> flat_nibble_powers() {
+    std::vector<uint32_t> out(64 * kUniTabWords);
+    const auto& pw = binary_powers();
+    for (int k = 0; k < 64; ++k)
+        for (int c = 0; c < 3; ++c)
+            for (int p = 0; p < 8; ++p)
+                for (uint32_t v = 0; v < 16; ++v)
+                    out[k * kUniTabWords + (c * 8 + p) * 16 + v] = nibble_entry(pw[k].m[c], p, v);
+    return out;
+}
+
 // Binary powers flattened as [k][comp][col] for the device seeding kernel.
 inline std::vector<uint32_t> flat_binary_powers() {
     std::vector<uint32_t> out(64 * 3 * 32);

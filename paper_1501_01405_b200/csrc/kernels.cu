@@ -22,7 +22,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
 #include <type_traits>
+#include <utility>
 
 #include "bitslice.cuh"
 #include "glibc_log.cuh"
@@ -34,23 +37,26 @@ namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
-// x -> M x for a matrix given by 32 columns in global memory.
-__device__ __forceinline__ uint32_t mat_apply_g(const uint32_t* __restrict__ col, uint32_t x) {
-    uint32_t y = 0;
+
+// Nibble-table application from global memory (L1-resident tables): 8 independent loads
+// and an XOR tree.
+__device__ __forceinline__ uint32_t nib_apply_g(const uint32_t* __restrict__ t, uint32_t x) {
+    uint32_t y[8];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) y ^= (0u - ((x >> j) & 1u)) & __ldg(col + j);
-    return y;
+    for (int p = 0; p < 8; ++p) y[p] = __ldg(t + p * 16 + ((x >> (4 * p)) & 15u));
+    return ((y[0] ^ y[1]) ^ (y[2] ^ y[3])) ^ ((y[4] ^ y[5]) ^ (y[6] ^ y[7]));
 }
 
-// Jump n draws with the binary powers M^(2^k) ([k][comp][32]).
-__device__ Taus jump_pow(const uint32_t* __restrict__ pw, Taus t, uint64_t n) {
+// Jump n draws with the binary powers M^(2^k) as nibble tables ([k][comp][p][v], jump.hpp
+// flat_nibble_powers): per set bit of n one nibble application per component.
+__device__ Taus jump_pow(const uint32_t* __restrict__ pn, Taus t, uint64_t n) {
     while (n) {
         const int k = __ffsll(static_cast<long long>(n)) - 1;
         n &= n - 1;
-        const uint32_t* m = pw + k * 96;
-        t.s1 = mat_apply_g(m, t.s1);
-        t.s2 = mat_apply_g(m + 32, t.s2);
-        t.s3 = mat_apply_g(m + 64, t.s3);
+        const uint32_t* m = pn + k * kUniTabWords;
+        t.s1 = nib_apply_g(m, t.s1);
+        t.s2 = nib_apply_g(m + 128, t.s2);
+        t.s3 = nib_apply_g(m + 256, t.s3);
     }
     return t;
 }
@@ -1414,39 +1420,188 @@ __device__ __forceinline__ Queue mm1_thread_rep(Taus st, int64_t n, int64_t n_wa
 // work every step (each on a different replication's segment); the exponentials go
 // through the warp-cooperative log batches as in TLP. Draws of a segment's last, partial
 // batch are predicated so each lane hands over the state exactly at its segment's end.
-// EXACT = false: every lane whose hand-over state matters (lanes 0-30) has whole batches
-// (31*K <= n and K % 4 == 0), so draws need no predication (lane 31, and lanes between
+// EXACT = false: every lane whose hand-over state matters (lanes 0-30) has whole panels
+// (31*K <= n and K % kPanT == 0), so draws need no predication (lane 31, and lanes between
 // replications, may overdraw: their stream state is never handed over).
+// ---------------------------------------------------------------------------------
+// mm1 exponential panels. A lane's next kPanT clients take 2*kPanT draws; their scaled
+// exponentials (a, s) go to the lane's row of a shared-memory panel as 16-byte pairs,
+// and the recursion then reads the pairs back in client order. The near-one inputs of
+// the whole warp's panel (1 in 16, ~32 of 512) are listed once — their places in the
+// list come from one lane scan of the per-lane counts, done before any log — and the
+// warp evaluates them in one (rarely two) full passes that write straight into the
+// panel slots: no per-batch compaction, no predicated patch-back into registers.
+// ---------------------------------------------------------------------------------
+constexpr int kPanT = 8;            // clients per lane per panel
+constexpr int kPanD = 2 * kPanT;    // draws per lane per panel
+constexpr int kPanRow = kPanD + 2;  // doubles per lane row: an odd number of 16-byte pairs,
+                                    // so 8 lanes' STS.128 / LDS.128 of one column hit all 32 banks
+constexpr int kDrRow = kPanD + 4;   // u32 per lane row of the draw buffer (5 x 16 B: odd, as above)
+constexpr int kNearCap = 128;       // near list entries (expected 32 per panel; more: lane-local path)
+constexpr uint32_t kNearMax = 0x10000000u;  // draw n is near one (1 - n 2^-32 >= 1 - 2^-4) iff n <= 2^28
+
+struct PanelWarp {
+    double v[32 * kPanRow];    // lane l, client c: v[l*kPanRow + 2c] = a, + 1 = s
+    uint32_t dr[32 * kDrRow];  // the panel's draws, lane rows
+    uint2 nl[kNearCap];        // near list: {draw, panel slot}
+};
+
+// e / rate for panel slot parity `odd` (odd slots are services: mu; even arrivals: lambda)
+template <int DIV>
+__device__ __forceinline__ double scale_slot(double e, bool odd, double lambda, double mu, double inv_l, double inv_m) {
+    return scale<DIV>(e, odd ? mu : lambda, odd ? inv_m : inv_l);
+}
+
+#ifndef WLP_PAN_UNROLL
+#define WLP_PAN_UNROLL 4
+#endif
+#ifndef WLP_PAN_MASK
+#define WLP_PAN_MASK 1
+#endif
+constexpr int kPanUnroll = WLP_PAN_UNROLL;
+
+// Near-one flag of draw n shifted into m: m = 2m + [n <= 2^28] (a subtract's borrow-out
+// carried into an add: two integer ops, no predicate-to-register select).
+__device__ __forceinline__ void near_bit(uint32_t& m, uint32_t n) {
+#if WLP_PAN_MASK
+    // the borrow-out of n - (2^28 + 1) is a carry flag of 0 (PTX sub.cc records a - b as
+    // a + ~b + 1): the carry is 1 exactly when n > 2^28, so shift in its complement via
+    // 2^28 - n, whose carry is 1 exactly when n <= 2^28
+    asm("{\n\t.reg .u32 t;\n\tsub.cc.u32 t, %1, %2;\n\taddc.u32 %0, %0, %0;\n\t}"
+        : "+r"(m)
+        : "r"(kNearMax), "r"(n));
+#else
+    m = 2u * m + (n <= kNearMax ? 1u : 0u);
+#endif
+}
+
+// List append of draw j (near iff bit kPanD-1-j of the lane's mask is set).
+__device__ __forceinline__ void near_append_m(uint32_t& sp, uint32_t m, int j, uint32_t n, uint32_t slot) {
+    const uint32_t bit = m & (1u << (kPanD - 1 - j));
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t"
+                 "@p st.shared.v2.u32 [%0], {%2, %3};\n\t@p add.u32 %0, %0, 8;\n\t}"
+                 : "+r"(sp)
+                 : "r"(bit), "r"(n), "r"(slot)
+                 : "memory");
+}
+
+// Fills the lane's panel row with the next `ndraw` draws' exponentials (EXACT: draws past
+// ndraw are not taken, so the stream state ends exactly there; else all kPanD are taken).
+// All lanes of `mask` (contiguous low lanes) take part. On return the row is final.
+// Pass 1 draws into the lane's draw row and builds its near-one bit mask; one lane scan
+// of the popcounts places each lane's near-ones in the list; pass 2 evaluates the table
+// path for every draw and lists the near ones; then the warp evaluates the list into the
+// panel.
 template <int DIV, bool EXACT>
-__device__ __forceinline__ void mm1_segment(Taus& st, Queue& q, uint32_t units, uint32_t units_max, double lambda,
-                                            double mu, double inv_l, double inv_m, const double* logtab,
-                                            TlpMm1Warp& W, int lane) {
-    for (uint32_t done = 0; done < units_max; done += kExpoB / 2) {
-        const int cnt = units <= done ? 0 : (units - done < kExpoB / 2 ? static_cast<int>(units - done) : kExpoB / 2);
-        uint32_t d[kExpoB];
-        double e[kExpoB];
+__device__ __forceinline__ void panel_fill(Taus& st, int ndraw, double lambda, double mu, double inv_l,
+                                           double inv_m, const double* tab, PanelWarp& P, unsigned mask,
+                                           int lane) {
+    uint32_t* drow = P.dr + lane * kDrRow;
+    uint32_t m = 0;
+#pragma unroll
+    for (int j = 0; j < kPanD; j += 4) {
+        uint4 q4;
         if (EXACT) {
-#pragma unroll
-            for (int j = 0; j < kExpoB; ++j) d[j] = j < 2 * cnt ? taus_next(st) : 0u;
+            // filler past ndraw: a table-path value (never listed, never read)
+            q4.x = j < ndraw ? taus_next(st) : 0x80000000u;
+            q4.y = j + 1 < ndraw ? taus_next(st) : 0x80000000u;
+            q4.z = j + 2 < ndraw ? taus_next(st) : 0x80000000u;
+            q4.w = j + 3 < ndraw ? taus_next(st) : 0x80000000u;
         } else {
-#pragma unroll
-            for (int j = 0; j < kExpoB; j += 2) taus_next2(st, d[j], d[j + 1]);
+            taus_next2(st, q4.x, q4.y);
+            taus_next2(st, q4.z, q4.w);
         }
-        neg_log1m_batch<kExpoB, true>(d, e, logtab, W.nl, W.res, kFull, lane);
+        near_bit(m, q4.x);
+        near_bit(m, q4.y);
+        near_bit(m, q4.z);
+        near_bit(m, q4.w);
+        *reinterpret_cast<uint4*>(drow + j) = q4;
+    }
+    const int c = __popc(m);
+    int incl = c;
 #pragma unroll
-        for (int c = 0; c < kExpoB / 2; ++c)
-            if (c < cnt) q.client(scale<DIV>(e[2 * c], lambda, inv_l), scale<DIV>(e[2 * c + 1], mu, inv_m));
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(mask, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const int width = mask == kFull ? 32 : __popc(mask);
+    const int total = __shfl_sync(mask, incl, width - 1);
+    const bool listed = total <= kNearCap;  // warp-uniform
+    double* row = P.v + lane * kPanRow;
+    const uint32_t slot0 = static_cast<uint32_t>(lane * kPanRow);
+    uint32_t sp = static_cast<uint32_t>(__cvta_generic_to_shared(P.nl + (incl - c)));
+#pragma unroll kPanUnroll
+    for (int j = 0; j < kPanD; j += 4) {
+        const uint4 q4 = *reinterpret_cast<const uint4*>(drow + j);
+        const double a0 = scale<DIV>(neg_log1m_table_dev(q4.x, tab), lambda, inv_l);
+        const double s0 = scale<DIV>(neg_log1m_table_dev(q4.y, tab), mu, inv_m);
+        const double a1 = scale<DIV>(neg_log1m_table_dev(q4.z, tab), lambda, inv_l);
+        const double s1 = scale<DIV>(neg_log1m_table_dev(q4.w, tab), mu, inv_m);
+        *reinterpret_cast<double2*>(row + j) = make_double2(a0, s0);
+        *reinterpret_cast<double2*>(row + j + 2) = make_double2(a1, s1);
+        if (listed) {
+            near_append_m(sp, m, j, q4.x, slot0 + j);
+            near_append_m(sp, m, j + 1, q4.y, slot0 + j + 1);
+            near_append_m(sp, m, j + 2, q4.z, slot0 + j + 2);
+            near_append_m(sp, m, j + 3, q4.w, slot0 + j + 3);
+        }
+    }
+    if (listed) {
+        __syncwarp(mask);
+        for (int k = lane; k < total; k += width) {
+            const uint2 it = P.nl[k];
+            const double e = it.x == 0u ? -0.0 : -log_near_one_dev(one_minus_u32_dev(it.x));
+            P.v[it.y] = scale_slot<DIV>(e, it.y & 1u, lambda, mu, inv_l, inv_m);
+        }
+    } else {  // (never at random draws) each lane fixes its own row
+        for (int j = 0; j < kPanD; ++j) {
+            const uint32_t n = drow[j];
+            if (n <= kNearMax) {
+                const double e = n == 0u ? -0.0 : -log_near_one_dev(one_minus_u32_dev(n));
+                row[j] = scale_slot<DIV>(e, j & 1, lambda, mu, inv_l, inv_m);
+            }
+        }
+    }
+    __syncwarp(mask);
+}
+
+// The recursion over `cnt` clients of the lane's panel row (cnt == kPanT: unpredicated).
+// COUNT: warp-level splits of the `t < 0` branch (models.cpp:199-201) over lanes `act`.
+template <bool COUNT = false>
+__device__ __forceinline__ void panel_clients(Queue& q, const PanelWarp& P, int cnt, int lane, unsigned act = 0u,
+                                              unsigned sync = 0u, unsigned* events = nullptr) {
+    const double2* row = reinterpret_cast<const double2*>(P.v + lane * kPanRow);
+    if (!COUNT && cnt == kPanT) {
+#pragma unroll
+        for (int c = 0; c < kPanT; ++c) {
+            const double2 v = row[c];
+            q.client(v.x, v.y);
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < kPanT; ++c) {
+            const bool on = c < cnt;
+            bool dry = false;
+            if (on) {
+                const double2 v = row[c];
+                dry = q.client(v.x, v.y);
+            }
+            if (COUNT && act && on) split_if(act, dry, *events, sync);  // (cnt is warp-uniform in TLP)
+        }
     }
 }
 
 struct Mm1PipeWarp {
-    TlpMm1Warp tw;
+    PanelWarp pw;
     long long rep[32];
     double sums[32][3];  // idle, sumw, sums
 };
 
 template <int DIV, bool EXACT>
-__global__ void __launch_bounds__(kMm1Block, 3) k_wlp_mm1_pipe(RepArgs a, int64_t K) {
+#ifndef WLP_MM1_MINB
+#define WLP_MM1_MINB 3
+#endif
+__global__ void __launch_bounds__(kMm1Block, WLP_MM1_MINB) k_wlp_mm1_pipe(RepArgs a, int64_t K) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double* logtab = reinterpret_cast<double*>(smraw);
     Mm1PipeWarp& P = reinterpret_cast<Mm1PipeWarp*>(logtab + 256)[threadIdx.x >> 5];
@@ -1492,8 +1647,12 @@ __global__ void __launch_bounds__(kMm1Block, 3) k_wlp_mm1_pipe(RepArgs a, int64_
         }
         if (more) ++cur;
         if (!__any_sync(kFull, rep >= 0)) break;
-        mm1_segment<DIV, EXACT>(st, q, rep >= 0 ? seg : 0u, seg_max, a.lambda, a.mu, a.inv_lambda, a.inv_mu, logtab,
-                                P.tw, lane);
+        const uint32_t units = rep >= 0 ? seg : 0u;
+        for (uint32_t done = 0; done < seg_max; done += kPanT) {
+            const int cnt = units <= done ? 0 : (units - done < kPanT ? static_cast<int>(units - done) : kPanT);
+            panel_fill<DIV, EXACT>(st, 2 * cnt, a.lambda, a.mu, a.inv_lambda, a.inv_mu, logtab, P.pw, kFull, lane);
+            panel_clients(q, P.pw, cnt, lane);
+        }
         if (__shfl_sync(kFull, rep, 31) >= 0) {  // lane 31 finished a replication
             if (lane == 31) {
                 P.rep[nemit] = rep;
@@ -1525,24 +1684,31 @@ __device__ __forceinline__ unsigned block_lane_mask() {  // partial last warp of
     return in_warp >= 32 ? kFull : ((1u << in_warp) - 1u);
 }
 
-template <int DIV, bool COUNT>
-__global__ void k_tlp_mm1(RepArgs a) {
+#ifndef WLP_TLP_MM1_MINB
+#define WLP_TLP_MM1_MINB 3
+#endif
+// SMALL: blocks of at most 256 threads (the default TLP block), register budget for
+// WLP_TLP_MM1_MINB blocks per SM; else any block size up to 1024.
+template <int DIV, bool COUNT, bool SMALL>
+__global__ void __launch_bounds__(SMALL ? 256 : 1024, SMALL ? WLP_TLP_MM1_MINB : 1) k_tlp_mm1(RepArgs a) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double* logtab = reinterpret_cast<double*>(smraw);
-    TlpMm1Warp& W = reinterpret_cast<TlpMm1Warp*>(logtab + 256)[threadIdx.x >> 5];
+    PanelWarp& W = reinterpret_cast<PanelWarp*>(logtab + 256)[threadIdx.x >> 5];
     stage_log_table(logtab);
     __syncthreads();
     const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const bool live = r < a.count;
-    const Taus st = live ? load_seed(a, r) : Taus{2u, 8u, 16u};  // tail threads: dummy stream
+    Taus st = live ? load_seed(a, r) : Taus{2u, 8u, 16u};  // tail threads: dummy stream
     const unsigned mask = block_lane_mask();
     unsigned events = 0;
-    const Queue q = mask == kFull
-                        ? mm1_thread_rep<DIV, true, COUNT>(st, a.n, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu,
-                                                           logtab, W, mask, lane, live, &events)
-                        : mm1_thread_rep<DIV, false, COUNT>(st, a.n, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu,
-                                                            logtab, W, mask, lane, live, &events);
+    const unsigned act = COUNT ? __ballot_sync(mask, live) : 0u;  // lanes of real replications
+    Queue q;
+    for (int64_t done = 0; done < a.n; done += kPanT) {  // every replication of the launch has a.n clients
+        const int cnt = a.n - done < kPanT ? static_cast<int>(a.n - done) : kPanT;
+        panel_fill<DIV, false>(st, 2 * kPanT, a.lambda, a.mu, a.inv_lambda, a.inv_mu, logtab, W, mask, lane);
+        panel_clients<COUNT>(q, W, cnt, lane, act, mask, &events);
+    }
     if (COUNT) {
         HwTally hw;
         hw.div = events;
@@ -1793,13 +1959,24 @@ __global__ void __launch_bounds__(kStatsBlock) k_stats_seq(const double* __restr
 }
 
 size_t tlp_mm1_smem(int block) { return 256 * 8 + static_cast<size_t>((block + 31) / 32) * sizeof(TlpMm1Warp); }
+size_t tlp_mm1_panel_smem(int block) { return 256 * 8 + static_cast<size_t>((block + 31) / 32) * sizeof(PanelWarp); }
 
+// Once per (device, kernel, size): the attribute calls cost ~1 us of host time each, which
+// showed in small runs when they were repeated at every launch.
 template <class K>
 void allow_smem(K kernel, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    size_t& have = done[{dev, reinterpret_cast<const void*>(kernel)}];
+    if (have != 0 && have >= bytes) return;
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
     // the persistent grids are sized by the occupancy API, which assumes the largest
     // shared-memory carveout; ask for it so every planned block is resident at once
     cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    have = bytes;
 }
 
 }  // namespace
@@ -1837,9 +2014,14 @@ int tlp_blocks_per_sm(int model, int block) {
     switch (model) {
         case 0: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tlp<0, false>, block, 0); break;
         case 1: {
-            const size_t smem = tlp_mm1_smem(block);
-            allow_smem(k_tlp_mm1<kDivIeee, false>, smem);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tlp_mm1<kDivIeee, false>, block, smem);
+            const size_t smem = tlp_mm1_panel_smem(block);
+            if (block <= 256) {
+                allow_smem(k_tlp_mm1<kDivIeee, false, true>, smem);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tlp_mm1<kDivIeee, false, true>, block, smem);
+            } else {
+                allow_smem(k_tlp_mm1<kDivIeee, false, false>, smem);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tlp_mm1<kDivIeee, false, false>, block, smem);
+            }
             break;
         }
         default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tlp<2, false>, block, 0); break;
@@ -1929,7 +2111,7 @@ cudaError_t launch_wlp_pipe(int model, const RepArgs& a, int64_t lane_units, int
 
 cudaError_t launch_wlp_mm1_pipe(const RepArgs& a, int64_t lane_units, int grid, cudaStream_t st) {
     if (a.count <= 0) return cudaSuccess;
-    const bool exact = 31 * lane_units > a.n || lane_units % (kExpoB / 2) != 0;
+    const bool exact = 31 * lane_units > a.n || lane_units % kPanT != 0;
     auto go = [&](auto kernel) { kernel<<<grid, kMm1Block, kMm1PipeSmem, st>>>(a, lane_units); };
     by_div(a.div, [&](auto d) {
         constexpr int D = decltype(d)::value;
@@ -1970,14 +2152,17 @@ cudaError_t launch_tlp(int model, const RepArgs& a, int tlp_block, cudaStream_t 
                 k_tlp<0, false><<<g, b, 0, st>>>(a);
             break;
         case 1: {
-            const size_t smem = tlp_mm1_smem(static_cast<int>(block));
+            const size_t smem = tlp_mm1_panel_smem(static_cast<int>(block));
             auto go = [&](auto kernel) {
                 allow_smem(kernel, smem);
                 kernel<<<g, b, smem, st>>>(a);
             };
             by_div(a.div, [&](auto d) {
                 constexpr int D = decltype(d)::value;
-                count ? go(k_tlp_mm1<D, true>) : go(k_tlp_mm1<D, false>);
+                if (block <= 256)
+                    count ? go(k_tlp_mm1<D, true, true>) : go(k_tlp_mm1<D, false, true>);
+                else
+                    count ? go(k_tlp_mm1<D, true, false>) : go(k_tlp_mm1<D, false, false>);
             });
             break;
         }

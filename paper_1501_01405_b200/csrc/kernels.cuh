@@ -46,7 +46,7 @@ struct HwTally {
 
 // Seeding: stream slots [slot_begin, slot_begin+count) of a run.
 struct SeedArgs {
-    const uint32_t* powers;  // [64][3][32] binary powers of the taus88 step
+    const uint32_t* powers;  // [64][3][8][16] binary powers of the taus88 step as nibble tables
     Taus master;
     int64_t slot_begin, count;
     const int64_t* rejected;  // sorted global candidate indices

@@ -107,7 +107,12 @@ struct DevCtx {
     int64_t planes_count = -1;            // ... (count), written by the last seed_async
     DevBuf<double> outs, partials, stats_in;
     DevBuf<SpecialRec> specials;
-    DevBuf<unsigned long long> counter;
+    DevBuf<unsigned long long> counter;  // [0] special candidates of the last seeding, [1] its grab counter
+    bool work_zeroed = false;            // counter[1] was cleared with counter[0] by seed_async
+    unsigned long long* h_counter = nullptr;  // pinned host word for the specials count readback
+    unsigned char* h_stage = nullptr;         // pinned staging of small uploads (plan tables)
+    size_t h_stage_cap = 0;
+    DevBuf<unsigned char> plan_blob;          // the plan's SeedJob[] then SetParam[]
     DevBuf<int64_t> rejected;
     DevBuf<unsigned long long> work;
     DevBuf<unsigned long long> hw;  // instrumentation tallies [div, ld, st]
@@ -134,7 +139,7 @@ int ctx_init(DevCtx& c) {
     if (c.ready) return WLP_OK;
     WLP_CUDA(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, c.dev));
     if (cudaDeviceGetAttribute(&c.clock_khz, cudaDevAttrClockRate, c.dev) != cudaSuccess) c.clock_khz = 0;
-    WLP_TRY(upload_u32(c.powers, flat_binary_powers()));
+    WLP_TRY(upload_u32(c.powers, flat_nibble_powers()));
     WLP_TRY(upload_u32(c.mm1_lane, lane_tables(2ull * kMm1PanelT)));
     WLP_TRY(upload_u32(c.mm1_skip, uniform_table(2ull * 31 * kMm1PanelT)));
     WLP_TRY(upload_u32(c.plan_lane, lane_tables(2ull * kPlanT)));
@@ -147,8 +152,9 @@ int ctx_init(DevCtx& c) {
         c.plan_bps[m] = plan_blocks_per_sm(m);
     }
     WLP_CUDA(c.specials.ensure(kSpecialCap));
-    WLP_CUDA(c.counter.ensure(1));
+    WLP_CUDA(c.counter.ensure(2));
     WLP_CUDA(c.work.ensure(1));
+    WLP_CUDA(cudaMallocHost(&c.h_counter, sizeof(unsigned long long)));
     WLP_CUDA(c.hw.ensure(3));
     WLP_CUDA(cudaEventCreate(&c.ev0));
     WLP_CUDA(cudaEventCreate(&c.ev1));
@@ -399,7 +405,9 @@ int seed_async(DevCtx& c, Taus master, int64_t slot_begin, int64_t count, const 
         WLP_CUDA(c.rejected.ensure(static_cast<int64_t>(rej.size())));
         WLP_CUDA(cudaMemcpyAsync(c.rejected.p, rej.data(), rej.size() * 8, cudaMemcpyHostToDevice, st));
     }
-    WLP_CUDA(cudaMemsetAsync(c.counter.p, 0, 8, st));
+    // the specials count and the model launch's grab counter (counter[1]) in one memset
+    WLP_CUDA(cudaMemsetAsync(c.counter.p, 0, 16, st));
+    c.work_zeroed = true;
     SeedArgs a;
     a.powers = c.powers.p;
     a.master = master;
@@ -425,9 +433,10 @@ int seed_async(DevCtx& c, Taus master, int64_t slot_begin, int64_t count, const 
 
 // Specials of the last seed_async (synchronises the stream).
 int read_specials(DevCtx& c, cudaStream_t st, std::vector<SpecialRec>& sp, int64_t& n_total) {
-    unsigned long long n = 0;
-    WLP_CUDA(cudaMemcpyAsync(&n, c.counter.p, 8, cudaMemcpyDeviceToHost, st));
+    c.work_zeroed = false;
+    WLP_CUDA(cudaMemcpyAsync(c.h_counter, c.counter.p, 8, cudaMemcpyDeviceToHost, st));
     WLP_CUDA(cudaStreamSynchronize(st));
+    const unsigned long long n = *c.h_counter;
     n_total = static_cast<int64_t>(n);
     if (n_total > kSpecialCap) return fail(WLP_EINTERNAL, "random_spacing: too many special candidates");
     sp.resize(static_cast<size_t>(n_total));
@@ -468,6 +477,8 @@ bool walk_planes(const DevCtx& c, int model, int mode, const wlp_params& p, int6
 // Launch the model over d_seeds (count replications). Async.
 int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_block, const uint32_t* d_seeds,
                 int64_t count, double* o0, double* o1, double* o2, cudaStream_t st, int& grid_out) {
+    const bool zeroed = c.work_zeroed;  // valid only for the launch right after seed_async
+    c.work_zeroed = false;
     RepArgs a;
     a.seeds = d_seeds;
     a.count = count;
@@ -509,8 +520,12 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
     grid_out = wlp_grid(c, model, count);
     const int64_t warps = static_cast<int64_t>(grid_out) * ((model == WLP_MODEL_MM1 ? kMm1Block : kWlpBlock) / 32);
     a.grab = static_cast<int>(std::clamp<int64_t>(count / (warps * 32), 1, 32));  // ~32 grabs per warp
-    a.next = c.work.p;
-    WLP_CUDA(cudaMemsetAsync(c.work.p, 0, sizeof(unsigned long long), st));
+    if (zeroed) {  // seed_async just cleared counter[1] on this stream
+        a.next = c.counter.p + 1;
+    } else {
+        a.next = c.work.p;
+        WLP_CUDA(cudaMemsetAsync(c.work.p, 0, sizeof(unsigned long long), st));
+    }
     if (model == WLP_MODEL_MM1) {
         // The pipeline runs each segment's recursion and sums in order on one lane (TLP's
         // per-client cost) but drains 31 steps per warp; segment chaining pays ~1.8x per
@@ -880,6 +895,7 @@ int seed_exact(Taus master, int64_t count, uint32_t* s_out, int out_on_device, v
     std::vector<int64_t> rej;
     for (;;) {
         WLP_TRY(seed_async(*c, master, 0, count, rej, d, st));
+        c->work_zeroed = false;  // no model launch follows
         std::vector<SpecialRec> sp;
         int64_t nt = 0;
         WLP_TRY(read_specials(*c, st, sp, nt));
@@ -1429,10 +1445,24 @@ int wlp_run_plan(int model, const wlp_params* sets, const uint64_t* master_seeds
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     StreamOrder so(*c, st);
     WLP_CUDA(c->seeds.ensure(3 * R));
-    WLP_CUDA(c->jobs.ensure(n_sets));
-    WLP_CUDA(c->setp.ensure(n_sets));
-    WLP_CUDA(cudaMemcpyAsync(c->jobs.p, jobs.data(), n_sets * sizeof(SeedJob), cudaMemcpyHostToDevice, st));
-    WLP_CUDA(cudaMemcpyAsync(c->setp.p, sp.data(), n_sets * sizeof(SetParam), cudaMemcpyHostToDevice, st));
+    // both tables in one upload from pinned staging (a pageable copy is a synchronous
+    // staging round trip per call); the stream is synchronised before this call returns,
+    // so the staging buffer is free again by the next call
+    const size_t jobs_bytes = (n_sets * sizeof(SeedJob) + 255) / 256 * 256;
+    const size_t blob = jobs_bytes + n_sets * sizeof(SetParam);
+    if (c->h_stage_cap < blob) {
+        if (c->h_stage) cudaFreeHost(c->h_stage);
+        c->h_stage = nullptr;
+        c->h_stage_cap = 0;
+        WLP_CUDA(cudaMallocHost(&c->h_stage, blob));
+        c->h_stage_cap = blob;
+    }
+    std::memcpy(c->h_stage, jobs.data(), n_sets * sizeof(SeedJob));
+    std::memcpy(c->h_stage + jobs_bytes, sp.data(), n_sets * sizeof(SetParam));
+    WLP_CUDA(c->plan_blob.ensure(static_cast<int64_t>(blob)));
+    WLP_CUDA(cudaMemcpyAsync(c->plan_blob.p, c->h_stage, blob, cudaMemcpyHostToDevice, st));
+    const SeedJob* d_jobs = reinterpret_cast<const SeedJob*>(c->plan_blob.p);
+    const SetParam* d_setp = reinterpret_cast<const SetParam*>(c->plan_blob.p + jobs_bytes);
     double *o0 = out0, *o1 = out1, *o2 = out2;
     if (!out_on_device) {
         WLP_CUDA(c->outs.ensure(3 * R));
@@ -1442,25 +1472,27 @@ int wlp_run_plan(int model, const wlp_params* sets, const uint64_t* master_seeds
     }
     // one batched seeding launch for all sets, and the model right behind it; the spacing
     // check below re-runs the model only when two special candidates share a key
-    WLP_CUDA(cudaMemsetAsync(c->counter.p, 0, 8, st));
-    WLP_CUDA(launch_seed_jobs(c->powers.p, c->jobs.p, n_sets, blocks, R, c->seeds.p, c->specials.p, kSpecialCap,
+    WLP_CUDA(cudaMemsetAsync(c->counter.p, 0, 16, st));  // specials count and the grab counter
+    WLP_CUDA(launch_seed_jobs(c->powers.p, d_jobs, n_sets, blocks, R, c->seeds.p, c->specials.p, kSpecialCap,
                               c->counter.p, st));
     PlanArgs pa;
     pa.serial_rho = mm1_serial_rho();
     pa.tlp_div = all_rcp ? kDivRcp : kDivIeee;
     pa.seeds = c->seeds.p;
     pa.count = R;
-    pa.sets = c->setp.p;
+    pa.sets = d_setp;
     pa.n_sets = n_sets;
     pa.out0 = o0;
     pa.out1 = o1;
     pa.out2 = o2;
-    pa.next = c->work.p;
+    pa.next = c->counter.p + 1;
     const int wpb = (model == WLP_MODEL_MM1 ? kMm1Block : kWlpBlock) / 32;
     const int grid = static_cast<int>(
         std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(c->sms) * c->plan_bps[model], (R + wpb - 1) / wpb)));
+    bool first = true;
     auto run_model_launch = [&]() -> int {
-        WLP_CUDA(cudaMemsetAsync(c->work.p, 0, 8, st));
+        if (!first) WLP_CUDA(cudaMemsetAsync(pa.next, 0, 8, st));  // (the first was cleared with the count)
+        first = false;
         if (report) WLP_CUDA(cudaEventRecord(c->ev0, st));
         WLP_CUDA(launch_plan(model, mode, pa, c->plan_lane.p, c->plan_skip.p, c->mm1_lane.p, c->mm1_skip.p, grid,
                              tlp_block_size, st));
@@ -1922,6 +1954,12 @@ int wlp_shutdown(void) {
     c.ev0 = c.ev1 = c.done = nullptr;
     c.last_used = false;
     c.work.release();
+    if (c.h_counter) cudaFreeHost(c.h_counter);
+    c.h_counter = nullptr;
+    if (c.h_stage) cudaFreeHost(c.h_stage);
+    c.h_stage = nullptr;
+    c.h_stage_cap = 0;
+    c.plan_blob.release();
     c.hw.release();
     c.jobs.release();
     c.setp.release();
