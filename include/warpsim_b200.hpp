@@ -139,6 +139,7 @@ struct SimReport {
     std::uint64_t memWrites = 0;
     std::uint64_t divergenceEvents = 0;
     double kernelMs = 0.0;  // measured model-kernel time (B200 extension)
+    std::uint64_t warpSplits = 0;  // instrumented runs: all warp splits of the kernel (B200 extension)
 };
 
 // ---- wlp.hpp:16-59 ----------------------------------------------------------------

@@ -75,6 +75,7 @@ typedef struct wlp_report {
     int64_t peak_resident_warps;
     uint64_t issues, alu_issues, mem_reads, mem_writes, divergence_events;
     double kernel_ms; /* model-kernel time from CUDA events (0 when not timed) */
+    uint64_t warp_splits; /* instrumented runs: every warp split of the kernel (see below) */
 } wlp_report;
 
 /* ConfidenceInterval (models.hpp:118-127). */
@@ -116,7 +117,14 @@ int wlp_version(void);              /* ABI version (1)                          
  *                       the TLP walk's 3 nested direction ifs, the TLP mm1 `t < 0`;
  *                       WLP has none (no lane runs a model branch against another);
  *   mem_reads / mem_writes — global load / store warp-instructions of the model kernel
- *                       (the analogue of the paper's Table 1 counts; atomics excluded).
+ *                       (the analogue of the paper's Table 1 counts; atomics excluded);
+ *   warp_splits       — every warp split the kernel itself executes, by the same event
+ *                       definition: the model's ifs above plus the implementation's
+ *                       lane-divergent loops (WLP: lane chunk tails of unequal length,
+ *                       the warp's near-one log list; TLP mm1: its near-one list);
+ *   total_cycles      — the kernel's makespan in SM cycles from clock64 (per SM, latest
+ *                       warp end minus earliest warp start, max over SMs); uninstrumented
+ *                       runs report kernel_ms x the SM clock instead.
  * Costs some speed; off by default. */
 int wlp_set_hw_counters(int enable);
 

@@ -158,6 +158,7 @@ class SimReport:  # device.hpp:62-71; measured on the GPU (see wlp_report in wlp
     memWrites: int = 0
     divergenceEvents: int = 0
     kernel_ms: float = 0.0
+    warpSplits: int = 0  # instrumented runs: every warp split of the kernel (wlp_report.warp_splits)
 
 
 @dataclass
@@ -216,7 +217,8 @@ class _Cfg(C.Structure):
 class _Report(C.Structure):
     _fields_ = [("total_cycles", C.c_int64), ("waves_executed", C.c_int64), ("peak_resident_warps", C.c_int64),
                 ("issues", C.c_uint64), ("alu_issues", C.c_uint64), ("mem_reads", C.c_uint64),
-                ("mem_writes", C.c_uint64), ("divergence_events", C.c_uint64), ("kernel_ms", C.c_double)]
+                ("mem_writes", C.c_uint64), ("divergence_events", C.c_uint64), ("kernel_ms", C.c_double),
+                ("warp_splits", C.c_uint64)]
 
 
 class _CI(C.Structure):
@@ -349,7 +351,7 @@ def _ptr(a) -> Optional[int]:
 
 def _report(r: _Report) -> SimReport:
     return SimReport(r.total_cycles, r.waves_executed, r.peak_resident_warps, r.issues, r.alu_issues, r.mem_reads,
-                     r.mem_writes, r.divergence_events, r.kernel_ms)
+                     r.mem_writes, r.divergence_events, r.kernel_ms, r.warp_splits)
 
 
 # ---- host utilities (reference host functions) ----------------------------------------------

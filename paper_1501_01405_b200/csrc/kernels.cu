@@ -109,13 +109,39 @@ __device__ __forceinline__ unsigned staged_loads(int total) {
     return first < total ? static_cast<unsigned>((total - first + blockDim.x - 1) / blockDim.x) : 0u;
 }
 
+__device__ __forceinline__ unsigned smid() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ long long hw_clock() { return clock64(); }
+
 __device__ __forceinline__ void flush_tally(const HwTally& h, unsigned long long* hw) {
     const unsigned act = __activemask();
     if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(act) - 1)) {
         if (h.div) atomicAdd(hw, static_cast<unsigned long long>(h.div));
         if (h.ld) atomicAdd(hw + 1, static_cast<unsigned long long>(h.ld));
         if (h.st) atomicAdd(hw + 2, static_cast<unsigned long long>(h.st));
+        if (h.splits) atomicAdd(hw + 3, static_cast<unsigned long long>(h.splits));
+        const unsigned sm = smid();
+        if (sm < static_cast<unsigned>(kHwMaxSms)) {
+            atomicMin(hw + kHwClk + sm, static_cast<unsigned long long>(h.t0));
+            atomicMax(hw + kHwClk + kHwMaxSms + sm, static_cast<unsigned long long>(hw_clock()));
+        }
     }
+}
+
+// Divergence events of one execution of a loop whose trip count `trips` differs per lane
+// (the reference's While event, warp_exec.cpp:286-293: an evaluation of the condition
+// where some active lanes enter and some skip). The lanes leave in groups of equal trip
+// count, and every group but the last leaves while others stay: events = the number of
+// distinct trip counts among the `mask` lanes, minus one. (All lanes call it.)
+__device__ __forceinline__ unsigned loop_split_events(unsigned mask, unsigned trips) {
+    const unsigned same = __match_any_sync(mask, trips);
+    const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
+    const unsigned firsts = __ballot_sync(mask, (same & lt & mask) == 0u);
+    return static_cast<unsigned>(__popc(firsts)) - 1u;
 }
 
 // Inside test of one pi point, x*x + y*y <= 1.0 in unfused fp64 (models.hpp:54-56),
@@ -245,9 +271,12 @@ struct NearList {  // per-warp compaction scratch
 // batch, instead of a ballot and popcounts per input) places them in nl, each is
 // evaluated by one lane into res[pos], and picked up by its owner. FULL: all 32 lanes take
 // part; else `mask_` names the (contiguous, low) lanes of a partial warp.
+// ev (instrumented kernels): add the near-one loop's divergence events (its lanes run
+// different trip counts whenever the list is not a multiple of the warp width).
 template <int B, bool FULL>
 __device__ __forceinline__ void neg_log1m_batch(const uint32_t (&n)[B], double (&e)[B], const double* tab,
-                                                NearList& nl, double* res, unsigned mask_, int lane) {
+                                                NearList& nl, double* res, unsigned mask_, int lane,
+                                                unsigned* ev = nullptr) {
     static_assert(B <= 32, "near flags fit one word");
     const unsigned mask = FULL ? kFull : mask_;
     unsigned near = 0;
@@ -282,6 +311,7 @@ __device__ __forceinline__ void neg_log1m_batch(const uint32_t (&n)[B], double (
                      : "r"(n[j]), "r"(static_cast<uint32_t>(nr[j]))
                      : "memory");
     __syncwarp(mask);
+    if (ev) *ev += loop_split_events(mask, lane < total ? static_cast<unsigned>((total - lane + width - 1) / width) : 0u);
     for (int p = lane; p < total; p += width) {
         const uint32_t v = nl.n[p];
         res[p] = v == 0u ? -0.0 : -log_near_one_dev(one_minus_u32_dev(v));
@@ -509,12 +539,31 @@ __global__ void __launch_bounds__(kWlpBlock, 4) k_wlp_lanes(RepArgs a, const uin
     stage_u32<kLaneTabWords>(tab, gtab);
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    HwTally hw;  // WLP: no lane runs a model branch against another, so hw.div stays 0
-    if (COUNT) hw.ld = staged_loads(kLaneTabWords / 4);
+    HwTally hw;
+    if (COUNT) {
+        hw.t0 = hw_clock();
+        hw.ld = staged_loads(kLaneTabWords / 4);
+    }
     int64_t mine = a.n - static_cast<int64_t>(lane) * K;
     mine = mine < 0 ? 0 : (mine > K ? K : mine);
     const uint32_t units = static_cast<uint32_t>(mine);
     const bool wide = a.n >= (int64_t(1) << 31);
+    // The model's branches are arithmetic here (pi's count is a predicated add, the walk's
+    // direction a polynomial), so a warp splits only where its lanes' unit loops end at
+    // different trips (pi_hits: 8-point main loop and tail; walk_dx: 2^24-step blocks, 4-step
+    // main loop, tail). The lanes' units are fixed for the launch, so every replication
+    // splits the same way: count it once per warp.
+    unsigned ev_rep = 0;
+    if (COUNT) {
+        if (MODEL == 0) {
+            ev_rep = loop_split_events(kFull, units / 8) + loop_split_events(kFull, units % 8);
+        } else {
+            const unsigned blocks = units > (1u << 24) ? (units - 1u) >> 24 : 0u;  // walk_dx's while
+            const unsigned last = units - (blocks << 24);
+            ev_rep = loop_split_events(kFull, blocks) + loop_split_events(kFull, last / 4) +
+                     loop_split_events(kFull, last % 4);
+        }
+    }
     for (int64_t base = grab_take(grab_issue(a, lane)); base < a.count;) {
         const unsigned long long ticket = grab_issue(a, lane);  // next group, in flight
         const int64_t end = base + a.grab < a.count ? base + a.grab : a.count;
@@ -539,6 +588,7 @@ __global__ void __launch_bounds__(kWlpBlock, 4) k_wlp_lanes(RepArgs a, const uin
         if (COUNT) {
             hw.ld += 3 * static_cast<unsigned>(end - base);
             hw.st += 1;
+            hw.splits += ev_rep * static_cast<unsigned>(end - base);
         }
         base = grab_take(ticket);
     }
@@ -670,7 +720,7 @@ __device__ __forceinline__ void lindley(double& w, double& u, double a, double s
 template <int DIV>
 __device__ __forceinline__ double mm1_warp_rep(Taus st, int64_t n, double lambda, double mu, double inv_l,
                                                double inv_m, const double* logtab, const uint32_t* skip, Mm1Warp& W,
-                                               int lane) {
+                                               int lane, unsigned* ev = nullptr) {
     constexpr int T = kMm1PanelT;
     constexpr int P = kMm1P;
     static_assert(2 * T % kExpoB == 0 && T % 2 == 0, "panel draws per lane must be whole batches");
@@ -685,7 +735,7 @@ __device__ __forceinline__ double mm1_warp_rep(Taus st, int64_t n, double lambda
             double e[kExpoB];
 #pragma unroll
             for (int j = 0; j < kExpoB; j += 2) taus_next2(st, d[j], d[j + 1]);
-            neg_log1m_batch<kExpoB, true>(d, e, logtab, W.nl, W.term, kFull, lane);
+            neg_log1m_batch<kExpoB, true>(d, e, logtab, W.nl, W.term, kFull, lane, ev);
 #pragma unroll
             for (int j = 0; j < kExpoB; j += 2) {
                 ea[(h + j) / 2] = scale<DIV>(e[j], lambda, inv_l);
@@ -775,7 +825,7 @@ __device__ __forceinline__ double mm1_warp_rep(Taus st, int64_t n, double lambda
 template <int DIV>
 __device__ __forceinline__ double mm1_warp_rep_serial(Taus st, int64_t n, double lambda, double mu, double inv_l,
                                                       double inv_m, const double* logtab, const uint32_t* skip,
-                                                      Mm1Warp& W, int lane) {
+                                                      Mm1Warp& W, int lane, unsigned* ev = nullptr) {
     constexpr int T = kMm1PanelT;
     constexpr int P = kMm1P;
     static_assert(sizeof(double2) * 32 * (T + 1) <= sizeof(W.term), "pair panel fits the term arrays");
@@ -789,7 +839,7 @@ __device__ __forceinline__ double mm1_warp_rep_serial(Taus st, int64_t n, double
             double e[kExpoB];
 #pragma unroll
             for (int j = 0; j < kExpoB; j += 2) taus_next2(st, d[j], d[j + 1]);
-            neg_log1m_batch<kExpoB, true>(d, e, logtab, W.nl, W.term, kFull, lane);
+            neg_log1m_batch<kExpoB, true>(d, e, logtab, W.nl, W.term, kFull, lane, ev);
 #pragma unroll
             for (int j = 0; j < kExpoB; j += 2) {
                 ea[(h + j) / 2] = scale<DIV>(e[j], lambda, inv_l);
@@ -852,8 +902,14 @@ __global__ void __launch_bounds__(kMm1Block, 3) k_wlp_mm1(RepArgs a, const uint3
                                                         const uint32_t* __restrict__ gskip) {
     const Mm1Smem m = mm1_stage(gtab, gskip);
     const int lane = threadIdx.x & 31;
-    HwTally hw;  // the `t < 0` decision is a per-lane select, never a warp branch: hw.div stays 0
-    if (COUNT) hw.ld = staged_loads(kUniTabWords) + staged_loads(256);
+    // the `t < 0` decision is a per-lane select, never a warp branch; the warp splits in
+    // the near-one loops of the exponential batches (counted there)
+    HwTally hw;
+    if (COUNT) {
+        hw.t0 = hw_clock();
+        hw.ld = staged_loads(kUniTabWords) + staged_loads(256);
+    }
+    unsigned* const ev = COUNT ? &hw.splits : nullptr;
     for (int64_t base = grab_take(grab_issue(a, lane)); base < a.count;) {
         const unsigned long long ticket = grab_issue(a, lane);
         const int64_t end = base + a.grab < a.count ? base + a.grab : a.count;
@@ -863,8 +919,9 @@ __global__ void __launch_bounds__(kMm1Block, 3) k_wlp_mm1(RepArgs a, const uint3
             const double acc =
                 a.lambda >= a.serial_rho * a.mu
                     ? mm1_warp_rep_serial<DIV>(st, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu, m.logtab, m.skip,
-                                               *m.W, lane)
-                    : mm1_warp_rep<DIV>(st, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu, m.logtab, m.skip, *m.W, lane);
+                                               *m.W, lane, ev)
+                    : mm1_warp_rep<DIV>(st, a.n, a.lambda, a.mu, a.inv_lambda, a.inv_mu, m.logtab, m.skip, *m.W, lane,
+                                        ev);
             const double avg = __ddiv_rn(acc, static_cast<double>(a.n));  // lanes 0/1/2: wait/sys/idle
             const double v0 = __shfl_sync(kFull, avg, 2);
             const double v1 = __shfl_sync(kFull, avg, 0);
@@ -960,6 +1017,7 @@ __global__ void k_tlp(RepArgs a) {
     if (r >= a.count) return;  // tail threads of the last block stay inert (wlp.cpp:125-138)
     const Taus st = load_seed(a, r);
     HwTally hw;
+    if (COUNT) hw.t0 = hw_clock();
     if (MODEL == 0) {
         a.out0[r] = pi_rep_tlp(st, a.n);  // no data-dependent branch: no events
     } else if (COUNT) {
@@ -1495,7 +1553,7 @@ __device__ __forceinline__ void near_append_m(uint32_t& sp, uint32_t m, int j, u
 template <int DIV, bool EXACT>
 __device__ __forceinline__ void panel_fill(Taus& st, int ndraw, double lambda, double mu, double inv_l,
                                            double inv_m, const double* tab, PanelWarp& P, unsigned mask,
-                                           int lane) {
+                                           int lane, unsigned* ev = nullptr) {
     uint32_t* drow = P.dr + lane * kDrRow;
     uint32_t m = 0;
 #pragma unroll
@@ -1548,6 +1606,7 @@ __device__ __forceinline__ void panel_fill(Taus& st, int ndraw, double lambda, d
     }
     if (listed) {
         __syncwarp(mask);
+        if (ev) *ev += loop_split_events(mask, lane < total ? static_cast<unsigned>((total - lane + width - 1) / width) : 0u);
         for (int k = lane; k < total; k += width) {
             const uint2 it = P.nl[k];
             const double e = it.x == 0u ? -0.0 : -log_near_one_dev(one_minus_u32_dev(it.x));
@@ -1701,17 +1760,21 @@ __global__ void __launch_bounds__(SMALL ? 256 : 1024, SMALL ? WLP_TLP_MM1_MINB :
     const bool live = r < a.count;
     Taus st = live ? load_seed(a, r) : Taus{2u, 8u, 16u};  // tail threads: dummy stream
     const unsigned mask = block_lane_mask();
-    unsigned events = 0;
+    unsigned events = 0, splits = 0;
     const unsigned act = COUNT ? __ballot_sync(mask, live) : 0u;  // lanes of real replications
+    const long long t0 = COUNT ? hw_clock() : 0;
     Queue q;
     for (int64_t done = 0; done < a.n; done += kPanT) {  // every replication of the launch has a.n clients
         const int cnt = a.n - done < kPanT ? static_cast<int>(a.n - done) : kPanT;
-        panel_fill<DIV, false>(st, 2 * kPanT, a.lambda, a.mu, a.inv_lambda, a.inv_mu, logtab, W, mask, lane);
+        panel_fill<DIV, false>(st, 2 * kPanT, a.lambda, a.mu, a.inv_lambda, a.inv_mu, logtab, W, mask, lane,
+                               COUNT ? &splits : nullptr);
         panel_clients<COUNT>(q, W, cnt, lane, act, mask, &events);
     }
     if (COUNT) {
         HwTally hw;
+        hw.t0 = t0;
         hw.div = events;
+        hw.splits = splits;
         const bool any_live = __any_sync(mask, live);
         // the seed loads are predicated, so a warp of dummy lanes still issues them
         hw.ld = staged_loads(256) + 3u;

@@ -39,10 +39,20 @@ struct RepArgs {
     double serial_rho = 2.0;
 };
 
-// Per-warp instrumentation tally (identical in every lane; the leader flushes it).
+// Per-warp instrumentation tally (identical in every lane; the leader flushes it), and the
+// warp's clock64 at kernel entry (set by the instrumented kernels).
 struct HwTally {
     unsigned div = 0, ld = 0, st = 0;
+    unsigned splits = 0;  // implementation splits (lane-divergent loops), beyond the model's `div`
+    long long t0 = 0;
 };
+
+// Layout of RepArgs::hw: [0] model-branch events, [1] loads, [2] stores, [3] implementation
+// splits, then per SM the earliest warp start and the latest warp end in that SM's clock64
+// (the host takes max over SMs of end - start: the kernel's makespan in SM cycles).
+constexpr int kHwMaxSms = 256;
+constexpr int kHwClk = 4;
+constexpr int kHwWords = kHwClk + 2 * kHwMaxSms;
 
 // Seeding: stream slots [slot_begin, slot_begin+count) of a run.
 struct SeedArgs {

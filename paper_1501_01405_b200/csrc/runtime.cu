@@ -109,6 +109,7 @@ struct DevCtx {
     DevBuf<SpecialRec> specials;
     DevBuf<unsigned long long> counter;  // [0] special candidates of the last seeding, [1] its grab counter
     bool work_zeroed = false;            // counter[1] was cleared with counter[0] by seed_async
+    bool time_model = false;  // model_async records ev0 right before its launch
     unsigned long long* h_counter = nullptr;  // pinned host word for the specials count readback
     unsigned char* h_stage = nullptr;         // pinned staging of small uploads (plan tables)
     size_t h_stage_cap = 0;
@@ -155,7 +156,7 @@ int ctx_init(DevCtx& c) {
     WLP_CUDA(c.counter.ensure(2));
     WLP_CUDA(c.work.ensure(1));
     WLP_CUDA(cudaMallocHost(&c.h_counter, sizeof(unsigned long long)));
-    WLP_CUDA(c.hw.ensure(3));
+    WLP_CUDA(c.hw.ensure(kHwWords));
     WLP_CUDA(cudaEventCreate(&c.ev0));
     WLP_CUDA(cudaEventCreate(&c.ev1));
     WLP_CUDA(cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming));
@@ -474,7 +475,15 @@ bool walk_planes(const DevCtx& c, int model, int mode, const wlp_params& p, int6
     return model == WLP_MODEL_WALK && mode != WLP_MODE_TLP && !g_hw_counters && walk_bs_choice(c, count, p.steps) == 3;
 }
 
-// Launch the model over d_seeds (count replications). Async.
+// The model kernel's start event: recorded by model_async right before its launch, after
+// any host-side preparation (lane tables are built on first use), when c.time_model is set.
+int mark_model_start(DevCtx& c, cudaStream_t st) {
+    if (c.time_model) WLP_CUDA(cudaEventRecord(c.ev0, st));
+    return WLP_OK;
+}
+
+// Launch the model over d_seeds (count replications). Async. With c.time_model the caller
+// records c.ev1 after it (c.ev0 is recorded here).
 int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_block, const uint32_t* d_seeds,
                 int64_t count, double* o0, double* o1, double* o2, cudaStream_t st, int& grid_out) {
     const bool zeroed = c.work_zeroed;  // valid only for the launch right after seed_async
@@ -499,19 +508,23 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
     a.out2 = o2;
     a.serial_rho = mm1_serial_rho();
     if (g_hw_counters) {
-        WLP_CUDA(cudaMemsetAsync(c.hw.p, 0, 3 * sizeof(unsigned long long), st));
+        WLP_CUDA(cudaMemsetAsync(c.hw.p, 0, kHwClk * sizeof(unsigned long long), st));
+        WLP_CUDA(cudaMemsetAsync(c.hw.p + kHwClk, 0xFF, kHwMaxSms * sizeof(unsigned long long), st));  // starts: min
+        WLP_CUDA(cudaMemsetAsync(c.hw.p + kHwClk + kHwMaxSms, 0, kHwMaxSms * sizeof(unsigned long long), st));
         a.hw = c.hw.p;
     }
     if (mode == WLP_MODE_TLP) {
         if (model == WLP_MODEL_WALK && g_tlp_variant == 2 && !g_hw_counters && a.n < (int64_t(1) << 31)) {
             grid_out = static_cast<int>((count + 32 * 128 - 1) / (32 * 128));
             g_last_kernel = "k_tlp_walk_bs";
+            WLP_TRY(mark_model_start(c, st));
             WLP_CUDA(launch_tlp_walk_bs(a, st));
             return WLP_OK;
         }
         const int64_t block = std::min<int64_t>(count, tlp_block);
         grid_out = static_cast<int>((count + block - 1) / block);
         g_last_kernel = model == WLP_MODEL_PI ? "k_tlp<pi>" : (model == WLP_MODEL_MM1 ? "k_tlp_mm1" : "k_tlp<walk>");
+        WLP_TRY(mark_model_start(c, st));
         WLP_CUDA(launch_tlp(model, a, tlp_block, st));
         return WLP_OK;
     }
@@ -536,9 +549,11 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
             const int64_t cap = static_cast<int64_t>(c.sms) * c.mm1_pipe_bps;
             grid_out = static_cast<int>(std::min<int64_t>(grid_out, cap));
             g_last_kernel = "k_wlp_mm1_pipe";
+            WLP_TRY(mark_model_start(c, st));
             WLP_CUDA(launch_wlp_mm1_pipe(a, (a.n + 31) / 32, grid_out, st));
         } else {
             g_last_kernel = "k_wlp_mm1";
+            WLP_TRY(mark_model_start(c, st));
             WLP_CUDA(launch_wlp(model, a, c.mm1_lane.p, c.mm1_skip.p, 0, grid_out, st));
         }
     } else if (model == WLP_MODEL_WALK && !g_hw_counters && walk_bs_choice(c, count, a.n) == 4) {
@@ -551,6 +566,7 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
         const uint32_t* tab = nullptr;
         WLP_TRY(lane_table(c, 2ull * static_cast<uint64_t>(K), tab));
         g_last_kernel = "k_wlp_walk_bs_lanes";
+        WLP_TRY(mark_model_start(c, st));
         WLP_CUDA(launch_wlp_walk_bs_lanes(a, tab, K, grid_out, st));
     } else if (model == WLP_MODEL_WALK && !g_hw_counters && walk_bs_choice(c, count, a.n) == 3) {
         // bitsliced pipeline: groups of 32 replications; at least ~64 groups per warp so
@@ -565,6 +581,7 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
         g_last_kernel = "k_wlp_walk_bs_pipe";
         const bool ready = c.planes_of == d_seeds && c.planes_count == count;  // from the seeding
         if (!ready) WLP_CUDA(c.bseeds.ensure(groups * 88));
+        WLP_TRY(mark_model_start(c, st));
         WLP_CUDA(launch_wlp_walk_bs_pipe(a, c.bseeds.p, K, grid_out, st, ready));
     } else {
         const int64_t K = (a.n + 31) / 32;
@@ -578,6 +595,7 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
             const int64_t cap = static_cast<int64_t>(c.sms) * c.pipe_bps;
             grid_out = static_cast<int>(std::min<int64_t>(grid_out, cap));
             g_last_kernel = model == WLP_MODEL_PI ? "k_wlp_pipe<pi>" : "k_wlp_pipe<walk>";
+            WLP_TRY(mark_model_start(c, st));
             WLP_CUDA(launch_wlp_pipe(model, a, K, grid_out, st));
         } else {
             // With few replications per warp the last groups leave a tail: 3 of the 4
@@ -586,6 +604,7 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
             const uint32_t* tab = nullptr;
             WLP_TRY(lane_table(c, 2ull * static_cast<uint64_t>(K), tab));
             g_last_kernel = model == WLP_MODEL_PI ? "k_wlp_lanes<pi>" : "k_wlp_lanes<walk>";
+            WLP_TRY(mark_model_start(c, st));
             WLP_CUDA(launch_wlp(model, a, tab, nullptr, K, grid_out, st));
         }
     }
@@ -610,11 +629,20 @@ void fill_report(DevCtx& c, int model, int mode, int tlp_block, int64_t count, i
     rep->waves_executed = (grid + resident - 1) / resident;
     rep->peak_resident_warps = std::min<int64_t>(grid, resident) * warps_per_block;
     if (g_hw_counters) {  // tallies of the instrumented kernels (the stream is synchronised)
-        unsigned long long h[3] = {0, 0, 0};
-        if (cudaMemcpy(h, c.hw.p, sizeof h, cudaMemcpyDeviceToHost) == cudaSuccess) {
+        std::vector<unsigned long long> h(kHwWords, 0ull);
+        if (cudaMemcpy(h.data(), c.hw.p, kHwWords * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
+            cudaSuccess) {
             rep->divergence_events = h[0];
             rep->mem_reads = h[1];
             rep->mem_writes = h[2];
+            rep->warp_splits = h[0] + h[3];
+            // makespan in SM cycles: per SM its own clock64, latest end - earliest start
+            unsigned long long span = 0;
+            for (int sm = 0; sm < kHwMaxSms; ++sm) {
+                const unsigned long long t0 = h[kHwClk + sm], t1 = h[kHwClk + kHwMaxSms + sm];
+                if (t0 != ~0ull && t1 >= t0) span = std::max(span, t1 - t0);
+            }
+            if (span) rep->total_cycles = static_cast<int64_t>(span);
         }
     }
 }
@@ -959,8 +987,9 @@ int wlp_run_streams(int model, const wlp_params* p, int mode, const uint32_t* s,
         o2 = c->outs.p + 2 * count;
     }
     int grid = 0;
-    if (report) WLP_CUDA(cudaEventRecord(c->ev0, st));
+    c->time_model = report != nullptr;
     WLP_TRY(model_async(*c, model, q, mode, 256, ds, count, o0, o1, o2, st, grid));
+    c->time_model = false;
     if (report) WLP_CUDA(cudaEventRecord(c->ev1, st));
     if (!out_on_device) {
         WLP_CUDA(cudaMemcpyAsync(out0, o0, count * 8, cudaMemcpyDeviceToHost, st));
@@ -1008,8 +1037,9 @@ int wlp_run_shard(int model, const wlp_params* p, int mode, uint64_t master_seed
     WLP_TRY(seed_async(*c, master_from_seed(master_seed), r_begin, r_count, rej, c->seeds.p, st,
                        walk_planes(*c, model, mode, *p, r_count)));
     int grid = 0;
-    if (report) WLP_CUDA(cudaEventRecord(c->ev0, st));
+    c->time_model = report != nullptr;
     WLP_TRY(model_async(*c, model, *p, mode, tlp_block_size, c->seeds.p, r_count, o0, o1, o2, st, grid));
+    c->time_model = false;
     if (report) WLP_CUDA(cudaEventRecord(c->ev1, st));
     if (!out_on_device) {
         WLP_CUDA(cudaMemcpyAsync(out0, o0, r_count * 8, cudaMemcpyDeviceToHost, st));
@@ -1063,8 +1093,9 @@ int wlp_run(int model, const wlp_params* p, int mode, uint64_t master_seed, int 
         // Seeding and the model run back to back; the spacing check below only forces a
         // re-run when two special candidates actually share a key.
         WLP_TRY(seed_async(*c, master, 0, R, rej, c->seeds.p, st, walk_planes(*c, model, mode, *p, R)));
-        if (report) WLP_CUDA(cudaEventRecord(c->ev0, st));
+        c->time_model = report != nullptr;
         WLP_TRY(model_async(*c, model, *p, mode, tlp_block_size, c->seeds.p, R, o0, o1, o2, st, grid));
+        c->time_model = false;
         if (report) WLP_CUDA(cudaEventRecord(c->ev1, st));
         std::vector<SpecialRec> sp;
         int64_t nt = 0;
@@ -1284,8 +1315,9 @@ int run_device_shard(int model, const wlp_params& p, int mode, Taus master, int 
             StreamOrder so(*c, st);
             int grid = 0;
             WLP_TRY(seed_async(*c, master, me.begin, n, rej, loc.seeds.p, st, walk_planes(*c, model, mode, p, n)));
-            WLP_CUDA(cudaEventRecord(c->ev0, st));
+            c->time_model = true;
             WLP_TRY(model_async(*c, model, p, mode, tlp_block, loc.seeds.p, n, o[0], o[1], o[2], st, grid));
+            c->time_model = false;
             WLP_CUDA(cudaEventRecord(c->ev1, st));
             int64_t nt = 0;
             WLP_TRY(read_specials(*c, st, me.specials, nt));  // synchronises the stream

@@ -45,6 +45,7 @@ SimReport from_c(const wlp_report& r) {
     s.memWrites = r.mem_writes;
     s.divergenceEvents = r.divergence_events;
     s.kernelMs = r.kernel_ms;
+    s.warpSplits = r.warp_splits;
     return s;
 }
 

@@ -60,3 +60,40 @@ def test_walk_table1_direction(gpu):
         tlp = gpu.run_model(gpu.ModelKind.Walk, p, gpu.ExecutionMode.Tlp, master_seed=42)
         wlp = gpu.run_model(gpu.ModelKind.Walk, p, gpu.ExecutionMode.Wlp, master_seed=42)
     assert tlp.report.divergenceEvents > 1000 and wlp.report.divergenceEvents == 0
+
+
+@pytest.mark.parametrize("model,expect", [(0, 128), (2, 128), (1, None)])
+def test_wlp_warp_splits_measured(gpu, model, expect):
+    # The WLP kernels run the model's ifs as arithmetic (divergenceEvents 0, as the
+    # reference), but their own lane-divergent loops are counted: 200 units over 32 lanes
+    # (K = 7) leave lanes 0-27 with 7, lane 28 with 4 and lanes 29-31 with none, so pi's
+    # tail loop (7 / 4 / 0 trips) and the walk's 4-step loop (1 / 1 / 0) and tail (3 / 0 / 0)
+    # split twice per replication; mm1 splits in its near-one log lists.
+    kw = dict(replications=64, draws=200, clients=200, steps=200, chunks=7)
+    with gpu.hw_counters():
+        run = gpu.run_model(gpu.ModelKind(model), gpu.ModelParams(**kw), gpu.ExecutionMode.Wlp, master_seed=7)
+    assert run.report.divergenceEvents == 0
+    if expect is not None:
+        assert run.report.warpSplits == expect
+    else:
+        assert run.report.warpSplits > 0
+
+
+def test_tlp_warp_splits_include_model_events(gpu):
+    p = gpu.ModelParams(replications=256, clients=300)
+    with gpu.hw_counters():
+        run = gpu.run_model(gpu.ModelKind.Mm1, p, gpu.ExecutionMode.Tlp, master_seed=3)
+    assert run.report.divergenceEvents > 0
+    assert run.report.warpSplits > run.report.divergenceEvents  # + the near-one list loops
+
+
+@pytest.mark.parametrize("mode", ["wlp", "tlp"])
+def test_total_cycles_from_clock64(gpu, mode):
+    p = gpu.ModelParams(replications=20000, steps=2000, chunks=30)
+    with gpu.hw_counters():
+        run = gpu.run_model(gpu.ModelKind.Walk, p, gpu.mode_from_name(mode), master_seed=1)
+    rep = run.report
+    assert rep.kernel_ms > 0 and rep.totalCycles > 0
+    # the makespan on one SM's clock fits inside the event-timed launch (<= ~2.1 GHz)
+    assert rep.totalCycles <= rep.kernel_ms * 2.2e6
+    assert rep.totalCycles >= rep.kernel_ms * 0.3e6

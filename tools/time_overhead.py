@@ -48,3 +48,16 @@ timed("run_streams only (device seeds)", lambda: w._lib.wlp_run_streams(int(mode
                                                                         seeds.data_ptr(), R, 1,
                                                                         *[o.data_ptr() for o in outs],
                                                                         *([None] * (3 - len(outs))), 1, None, None))
+
+# the same call with every argument marshalled once (Python's share of the run)
+pp = w._params(p)
+o = [x.data_ptr() for x in outs] + [None] * (3 - len(outs))
+sp = w._special_buffer(4096)
+nsp = w.C.c_int64()
+rr = w._Report()
+timed("wlp_run_shard, args pre-marshalled (report)", lambda: w._lib.wlp_run_shard(
+    int(model), w.C.byref(pp), 2, 42, 256, 0, R, None, 0, o[0], o[1], o[2], 1, None, sp, 4096, w.C.byref(nsp),
+    w.C.byref(rr)))
+timed("wlp_run_shard, args pre-marshalled (no report)", lambda: w._lib.wlp_run_shard(
+    int(model), w.C.byref(pp), 2, 42, 256, 0, R, None, 0, o[0], o[1], o[2], 1, None, sp, 4096, w.C.byref(nsp),
+    None))
