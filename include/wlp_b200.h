@@ -139,6 +139,13 @@ int wlp_set_hw_counters(int enable);
  * identical; only speed differs. */
 int wlp_set_wlp_variant(int variant);
 
+/* Tuning / test hook for later calls on this thread: lanes per replication of the pi /
+ * walk warp pipeline (wlp variant 2, automatic at large R). 32 = the whole warp is one
+ * pipeline; 16 or 8 = 32/S pipelines side by side in the warp, each replication split into
+ * S chunks (longer steps for the same hand-over work); 0 = automatic (32 when n >= 3840,
+ * else 16 when n >= 1920, else 8). Outputs are identical. */
+int wlp_set_pipe_lanes(int lanes);
+
 /* The same for the TLP (thread-level) mapping: 0 = automatic (default: one thread per
  * replication, the paper's comparison mapping); 1 = one thread per replication; 2 = walk
  * bitsliced, one thread per 32 replications, each state bit of the 32 streams in one

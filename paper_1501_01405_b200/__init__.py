@@ -246,6 +246,7 @@ _SIGS = {
     "wlp_set_hw_counters": (C.c_int, [C.c_int]),
     "wlp_set_wlp_variant": (C.c_int, [C.c_int]),
     "wlp_set_tlp_variant": (C.c_int, [C.c_int]),
+    "wlp_set_pipe_lanes": (C.c_int, [C.c_int]),
     "wlp_last_kernel": (C.c_char_p, []),
     "wlp_validate_params": (C.c_int, [C.c_int, C.POINTER(_Params), C.c_char_p, C.c_int]),
     "wlp_plan_launch": (C.c_int, [_I64, C.c_int, C.c_int, _I64, C.POINTER(_Cfg), C.c_char_p, C.c_int]),
@@ -617,6 +618,21 @@ class wlp_variant:
 
     def __exit__(self, *exc):
         _check(_lib.wlp_set_wlp_variant(0))
+
+
+class pipe_lanes:
+    """Context manager: lanes per replication of the pi / walk warp pipeline (8, 16, 32;
+    0 automatic) for calls on this thread (wlp_set_pipe_lanes)."""
+
+    def __init__(self, lanes: int):
+        self.lanes = int(lanes)
+
+    def __enter__(self):
+        _check(_lib.wlp_set_pipe_lanes(self.lanes))
+        return self
+
+    def __exit__(self, *exc):
+        _check(_lib.wlp_set_pipe_lanes(0))
 
 
 def last_kernel() -> str:

@@ -91,18 +91,29 @@ inline uint32_t nibble_entry(const Mat32& m, int p, uint32_t v) {
 constexpr int kLaneTabWords = 3 * 8 * 16 * 32;  // [comp][p][v][lane], 48 KB
 constexpr int kUniTabWords = 3 * 8 * 16;         // [comp][p][v], 1.5 KB
 
+inline void put_lane(std::vector<uint32_t>& out, int l, const Jump3& j) {
+    for (int c = 0; c < 3; ++c)
+        for (int p = 0; p < 8; ++p)
+            for (uint32_t v = 0; v < 16; ++v) out[((c * 8 + p) * 16 + v) * 32 + l] = nibble_entry(j.m[c], p, v);
+}
+
 // Lane-start tables: lane l jumps by l * stride draws.
 inline std::vector<uint32_t> lane_tables(uint64_t stride) {
     std::vector<uint32_t> out(kLaneTabWords);
     Jump3 step = jump_matrix(stride), cur;
     for (int c = 0; c < 3; ++c) cur.m[c] = mat_identity();
     for (int l = 0; l < 32; ++l) {
-        for (int c = 0; c < 3; ++c)
-            for (int p = 0; p < 8; ++p)
-                for (uint32_t v = 0; v < 16; ++v)
-                    out[((c * 8 + p) * 16 + v) * 32 + l] = nibble_entry(cur.m[c], p, v);
+        put_lane(out, l, cur);
         for (int c = 0; c < 3; ++c) cur.m[c] = mat_mul(step.m[c], cur.m[c]);
     }
+    return out;
+}
+
+// Lane tables for arbitrary per-lane distances: lane l jumps dist[l] draws (the wrapped
+// warp pipelines start lane l of their first step at a replication's chunk l).
+inline std::vector<uint32_t> lane_tables_dist(const std::array<uint64_t, 32>& dist) {
+    std::vector<uint32_t> out(kLaneTabWords);
+    for (int l = 0; l < 32; ++l) put_lane(out, l, jump_matrix(dist[l]));
     return out;
 }
 

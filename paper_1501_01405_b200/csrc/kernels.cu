@@ -47,6 +47,14 @@ __device__ __forceinline__ uint32_t nib_apply_g(const uint32_t* __restrict__ t, 
     return ((y[0] ^ y[1]) ^ (y[2] ^ y[3])) ^ ((y[4] ^ y[5]) ^ (y[6] ^ y[7]));
 }
 
+// The same for a lane-major table ([p][v][lane], row stride 32 words) in global memory.
+__device__ __forceinline__ uint32_t nib_apply_g32(const uint32_t* __restrict__ t, uint32_t x) {
+    uint32_t y[8];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) y[p] = __ldg(t + (p * 16 + ((x >> (4 * p)) & 15u)) * 32);
+    return ((y[0] ^ y[1]) ^ (y[2] ^ y[3])) ^ ((y[4] ^ y[5]) ^ (y[6] ^ y[7]));
+}
+
 // Jump n draws with the binary powers M^(2^k) as nibble tables ([k][comp][p][v], jump.hpp
 // flat_nibble_powers): per set bit of n one nibble application per component.
 __device__ Taus jump_pow(const uint32_t* __restrict__ pn, Taus t, uint64_t n) {
@@ -596,43 +604,81 @@ __global__ void __launch_bounds__(kWlpBlock, 4) k_wlp_lanes(RepArgs a, const uin
 }
 
 // WLP as a systolic warp pipeline (pi / walk, many short replications per warp). Lane l
-// still owns units [l*K, (l+1)*K) of every replication, but instead of each lane jumping
-// its stream ahead (lane_jump: ~24 table reads per lane per replication), replication r
-// enters at lane 0 and moves one lane per step: at step t lane l runs its chunk of the
-// replication that entered at step t - l, starting from the stream state lane l-1 ended
-// with (its chunk ends exactly where chunk l begins), and passes (state, partial sum,
-// index) up with __shfl_up_sync. Lane 31 completes a replication every step; finished
-// sums collect in shared memory and 32 of them are finalised and stored by the 32 lanes
-// at once. No jump tables at all; the cost is the 31-step drain per warp, so the launcher
-// picks this kernel when replications per warp are many and units per replication few
-// (config 4: 1400 replications of 32 units per lane).
+// owns chunk l of every replication, but instead of each lane jumping its stream ahead
+// (lane_jump: ~24 table reads per lane per replication), replication r enters at lane 0
+// and moves one lane per step: at step t lane l runs its chunk of the replication that
+// entered at step t - l, starting from the stream state lane l-1 ended with (chunk l-1
+// ends exactly where chunk l begins), and passes (state, partial sum, index) up with
+// __shfl_up_sync. The last lane completes a replication every step; finished sums collect
+// in shared memory and 32 of them are finalised and stored by the 32 lanes at once.
+//
+// * Rotating schedule (PipeSched): every lane runs L(t) units at step t, and any S
+//   consecutive L sum to n, so no lane idles behind a longer chunk.
+// * S lanes per replication: S = 32 is the whole warp; S = 16 or 8 runs 32/S such
+//   pipelines side by side in the warp (every replication still passes through lanes of
+//   one warp only, split into S chunks), so a step carries 32/S times the units per
+//   lane for the same hand-over and bookkeeping instructions (config 4, 1,000 points:
+//   31 units per step at S = 32, 125 at S = 8).
+// * Wrap (WRAP): a straight pipeline idles a triangle of (S-1) x S lane-steps per
+//   pipeline (lanes p > t while it fills, lanes p < s while it drains). Each S-lane
+//   pipeline owns S - 1 "wrap" replications besides the ones its warp grabs: at step 0
+//   its lane p >= 1 starts wrap replication p at chunk p (the seed jumped by the units of
+//   chunks 0..p-1: one lane-table jump per lane and warp), and these late chunks fill the
+//   fill triangle; once the grabbed replications run out, its lane 0 is fed the wrap
+//   replications S-1, .., 1, whose early chunks 0..k-1 fill the drain triangle exactly
+//   and all end at the pipeline's last step. Late and early partial sums are integers,
+//   added exactly. A pipeline fed N grabbed replications runs N + S - 1 steps for
+//   N + S - 1 replications.
 // WIDE: 64-bit sums and indices (n >= 2^27 or count >= 2^31); else 32-bit, fewer shuffles.
-template <int MODEL, bool WIDE>
-__global__ void __launch_bounds__(kWlpBlock, 3) k_wlp_pipe(RepArgs a, int64_t K) {
+__device__ __forceinline__ Taus lane_jump_g(const uint32_t* __restrict__ tab, int lane, Taus t) {
+    t.s1 = nib_apply_g32(tab + lane, t.s1);
+    t.s2 = nib_apply_g32(tab + 4096 + lane, t.s2);
+    t.s3 = nib_apply_g32(tab + 8192 + lane, t.s3);
+    return t;
+}
+
+#ifndef WLP_PIPE_MINB
+#define WLP_PIPE_MINB 4
+#endif
+template <int MODEL, bool WIDE, int S, bool WRAP>
+__global__ void __launch_bounds__(kWlpBlock, WLP_PIPE_MINB) k_wlp_pipe(RepArgs a, PipeSched ps,
+                                                           const uint32_t* __restrict__ wtab) {
+    static_assert(S == 32 || WRAP, "S < 32 pipelines always wrap");
     using I = typename std::conditional<WIDE, long long, int>::type;
-    __shared__ I emit_rep[kWlpBlock / 32][32];
-    __shared__ I emit_sum[kWlpBlock / 32][32];
+    constexpr int kW = kWlpBlock / 32, P = 32 / S, kWr = S - 1;
+    __shared__ I emit_rep[kW][32];
+    __shared__ I emit_sum[kW][32];
+    __shared__ I late_sum[kW][32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int64_t mine = a.n - static_cast<int64_t>(lane) * K;
-    mine = mine < 0 ? 0 : (mine > K ? K : mine);
-    const uint32_t units = static_cast<uint32_t>(mine);
+    const int g = lane / S, pos = lane % S;  // pipeline of the lane, stage in it
+    const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * kW + wid;
+    // wrap replication k (1..S-1) of pipeline g: wrap0 + g*(S-1) + k - 1
+    const int64_t wrap0 = gwarp * (P * kWr) + g * kWr;
+    const int64_t pool0 = WRAP ? static_cast<int64_t>(gridDim.x) * kW * (P * kWr) : 0;
+    // item codes: r >= 0 a grabbed replication, -1 idle, -1-k the late chunks of wrap k,
+    // -33-k its early chunks
     Taus st{kMin1, kMin2, kMin3};
-    I sum = 0, rep = -1;
-    int64_t cur = 0, cend = 0;  // lane 0's current group of replications (warp-uniform)
-    bool more = true;
-    int nemit = 0;
+    I sum = 0, rep = -1, left = 0;
+    if (WRAP && pos > 0) {
+        st = lane_jump_g(wtab, lane, load_seed(a, wrap0 + pos - 1));
+        rep = static_cast<I>(-1 - pos);
+    }
+    int64_t cur = 0, cend = 0;  // the warp's current group of replications (warp-uniform)
+    bool more = true;           // the warp still grabs
+    bool drain = false;         // this lane's pipeline takes no more grabbed replications
+    int wraps = kWr, nemit = 0, phase = 0;
+    auto value = [&](I c) {  // pi: hits; walk: the raw q sum, dx = (sum + 6n) / 6
+        return MODEL == 0 ? __ddiv_rn(__dmul_rn(4.0, static_cast<double>(c)), static_cast<double>(a.n))
+                          : walk_fold((static_cast<int64_t>(c) + 6 * a.n) / 6, a.chunks);
+    };
     auto flush = [&](int cnt) {
         __syncwarp();
-        if (lane < cnt) {  // pi: hits; walk: the raw q sum, dx = (sum + 6n) / 6
-            const I r = emit_rep[wid][lane], c = emit_sum[wid][lane];
-            a.out0[r] = MODEL == 0 ? __ddiv_rn(__dmul_rn(4.0, static_cast<double>(c)), static_cast<double>(a.n))
-                                   : walk_fold((static_cast<int64_t>(c) + 6 * a.n) / 6, a.chunks);
-        }
+        if (lane < cnt) a.out0[emit_rep[wid][lane]] = value(emit_sum[wid][lane]);
         __syncwarp();
     };
     for (;;) {
-        if (more && cur >= cend) {  // next group from the global counter
-            const int64_t base = grab_take(grab_issue(a, lane));
+        if (more && cur >= cend) {  // next group (a multiple of P replications)
+            const int64_t base = pool0 + grab_take(grab_issue(a, lane));
             if (base >= a.count) {
                 more = false;
             } else {
@@ -640,31 +686,88 @@ __global__ void __launch_bounds__(kWlpBlock, 3) k_wlp_pipe(RepArgs a, int64_t K)
                 cend = base + a.grab < a.count ? base + a.grab : a.count;
             }
         }
-        if (lane == 0) {  // feed
-            rep = more ? static_cast<I>(cur) : I(-1);
-            if (more) {
-                st = load_seed(a, cur);
-                sum = 0;
+        bool last = false;  // this lane's pipeline runs its last step
+        if (!drain) {
+            const int64_t r = cur + g;
+            if (more && r < cend) {  // feed a grabbed replication
+                if (pos == 0) {
+                    rep = static_cast<I>(r);
+                    st = load_seed(a, r);
+                    sum = 0;
+                }
+            } else {
+                drain = true;
             }
         }
-        if (more) ++cur;
-        if (!__any_sync(kFull, rep >= 0)) break;
-        if (rep >= 0) sum += MODEL == 0 ? static_cast<I>(pi_hits(st, units)) : static_cast<I>(walk_q(st, units));
-        if (__shfl_sync(kFull, rep, 31) >= 0) {  // lane 31 finished a replication
-            if (lane == 31) {
-                emit_rep[wid][nemit] = rep;
-                emit_sum[wid][nemit] = sum;
+        if (more) cur += P;
+        if (drain) {
+            if (WRAP && wraps > 0) {  // the early chunks of wrap replication `wraps`
+                if (pos == 0) {
+                    rep = static_cast<I>(-33 - wraps);
+                    st = load_seed(a, wrap0 + wraps - 1);
+                    sum = 0;
+                    left = static_cast<I>(pipe_wrap_units(ps, wraps));
+                }
+                last = wraps == 1;
+                --wraps;
+            } else if (!WRAP) {
+                if (pos == 0) rep = -1;
+            } else {
+                rep = -1;  // finished pipeline
             }
-            if (++nemit == 32) {
-                flush(32);
+        }
+        if (!more && !__any_sync(kFull, rep != -1)) break;
+        uint32_t units = static_cast<uint32_t>(pipe_units(ps, phase));
+        if (WRAP && rep <= -34) {  // early chunk pos of wrap k: stop exactly at its late part
+            const I k = -33 - rep;
+            const I u = pos == k - 1 ? left : (left < static_cast<I>(units) ? left : static_cast<I>(units));
+            left -= u;
+            units = static_cast<uint32_t>(u);
+        }
+        if (rep != -1) sum += MODEL == 0 ? static_cast<I>(pi_hits(st, units)) : static_cast<I>(walk_q(st, units));
+        if (S == 32) {
+            const I r31 = __shfl_sync(kFull, rep, 31);
+            if (r31 >= 0) {  // lane 31 finished a replication
+                if (lane == 31) {
+                    emit_rep[wid][nemit] = rep;
+                    emit_sum[wid][nemit] = sum;
+                }
+                if (++nemit == 32) {
+                    flush(32);
+                    nemit = 0;
+                }
+            } else if (WRAP && r31 < -1 && lane == 31) {  // the late chunks of a wrap replication
+                late_sum[wid][-1 - r31] = sum;
+            }
+        } else {
+            const bool fin = pos == S - 1 && rep >= 0;
+            const unsigned m = __ballot_sync(kFull, fin);
+            if (fin) {
+                const int slot = nemit + __popc(m & ((1u << lane) - 1u));
+                emit_rep[wid][slot] = rep;
+                emit_sum[wid][slot] = sum;
+            } else if (pos == S - 1 && rep < -1 && rep >= -32) {
+                late_sum[wid][g * S - 1 - static_cast<int>(rep)] = sum;
+            }
+            nemit += __popc(m);
+            if (nemit > 32 - P) {
+                flush(nemit);
                 nemit = 0;
             }
         }
-        st.s1 = __shfl_up_sync(kFull, st.s1, 1);
-        st.s2 = __shfl_up_sync(kFull, st.s2, 1);
-        st.s3 = __shfl_up_sync(kFull, st.s3, 1);
-        sum = __shfl_up_sync(kFull, sum, 1);
-        rep = __shfl_up_sync(kFull, rep, 1);
+        if (WRAP && __any_sync(kFull, last)) {  // early chunks of wraps 1..S-1 end here
+            __syncwarp();
+            if (last && pos < S - 1) a.out0[wrap0 + pos] = value(sum + late_sum[wid][g * S + pos + 1]);
+            if (last) rep = -1;
+            if (S == 32) break;
+        }
+        st.s1 = __shfl_up_sync(kFull, st.s1, 1, S);
+        st.s2 = __shfl_up_sync(kFull, st.s2, 1, S);
+        st.s3 = __shfl_up_sync(kFull, st.s3, 1, S);
+        sum = __shfl_up_sync(kFull, sum, 1, S);
+        rep = __shfl_up_sync(kFull, rep, 1, S);
+        if (WRAP) left = __shfl_up_sync(kFull, left, 1, S);
+        phase = phase == S - 1 ? 0 : phase + 1;
     }
     flush(nemit);
 }
@@ -2159,16 +2262,29 @@ cudaError_t launch_wlp(int model, const RepArgs& a, const uint32_t* lane_tab, co
     return cudaGetLastError();
 }
 
-cudaError_t launch_wlp_pipe(int model, const RepArgs& a, int64_t lane_units, int grid, cudaStream_t st) {
+template <int MODEL, bool WIDE>
+void launch_wlp_pipe_m(const RepArgs& a, const PipeSched& s, const uint32_t* wrap_tab, int grid, cudaStream_t st) {
+    auto go = [&](auto kernel) { kernel<<<grid, kWlpBlock, 0, st>>>(a, s, wrap_tab); };
+    if (s.S == 8)
+        go(k_wlp_pipe<MODEL, WIDE, 8, true>);
+    else if (s.S == 16)
+        go(k_wlp_pipe<MODEL, WIDE, 16, true>);
+    else if (wrap_tab)
+        go(k_wlp_pipe<MODEL, WIDE, 32, true>);
+    else
+        go(k_wlp_pipe<MODEL, WIDE, 32, false>);
+}
+
+cudaError_t launch_wlp_pipe(int model, const RepArgs& a, const PipeSched& s, const uint32_t* wrap_tab, int grid,
+                            cudaStream_t st) {
     if (a.count <= 0) return cudaSuccess;
+    if (s.S != 32 && (!wrap_tab || (s.S != 16 && s.S != 8))) return cudaErrorInvalidValue;
     // 32-bit sums hold pi's hits (< n) and the walk's raw q sum (|sum| <= 12 n)
     const bool wide = a.n >= (int64_t(1) << 27) || a.count >= (int64_t(1) << 31);
     if (model == 0)
-        wide ? k_wlp_pipe<0, true><<<grid, kWlpBlock, 0, st>>>(a, lane_units)
-             : k_wlp_pipe<0, false><<<grid, kWlpBlock, 0, st>>>(a, lane_units);
+        wide ? launch_wlp_pipe_m<0, true>(a, s, wrap_tab, grid, st) : launch_wlp_pipe_m<0, false>(a, s, wrap_tab, grid, st);
     else
-        wide ? k_wlp_pipe<2, true><<<grid, kWlpBlock, 0, st>>>(a, lane_units)
-             : k_wlp_pipe<2, false><<<grid, kWlpBlock, 0, st>>>(a, lane_units);
+        wide ? launch_wlp_pipe_m<2, true>(a, s, wrap_tab, grid, st) : launch_wlp_pipe_m<2, false>(a, s, wrap_tab, grid, st);
     return cudaGetLastError();
 }
 
@@ -2197,7 +2313,7 @@ int wlp_mm1_pipe_blocks_per_sm() {
 
 int wlp_pipe_blocks_per_sm() {
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_pipe<0, true>, kWlpBlock, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_pipe<0, true, 32, true>, kWlpBlock, 0);
     return nb < 1 ? 1 : nb;
 }
 

@@ -54,6 +54,43 @@ constexpr int kHwMaxSms = 256;
 constexpr int kHwClk = 4;
 constexpr int kHwWords = kHwClk + 2 * kHwMaxSms;
 
+// Rotating schedule of the warp pipelines (k_wlp_pipe, k_wlp_walk_bs_pipe,
+// k_wlp_mm1_pipe). A replication's units are split into S chunks, one per lane of an
+// S-lane pipeline (S = 32: the whole warp). At pipeline step t every lane runs the same
+// number of units,
+//   L(t) = G * (qb + [t % S < rb]) + [t % S == S-1] * tail,   n = G * (S qb + rb) + tail,
+// so any S consecutive steps sum to n: a replication entering at lane 0 at any step is
+// covered exactly by its S chunks, and no lane waits on a longer chunk of another (a
+// fixed split ceil(n/32) leaves lane 31 short: 1000 units = 31 x 32 + 8 idles 2.3 %).
+// G is the kernel's unrolled block (8 units, 8 walk steps for the bitsliced counters).
+struct PipeSched {
+    int G = 1, S = 32, qb = 0, rb = 0, tail = 0;
+};
+__host__ __device__ inline PipeSched pipe_sched(int64_t n, int G, int S = 32) {
+    PipeSched s;
+    s.G = G;
+    s.S = S;
+    const int64_t nb = n / G;
+    s.qb = static_cast<int>(nb / S);
+    s.rb = static_cast<int>(nb % S);
+    s.tail = static_cast<int>(n % G);
+    return s;
+}
+__host__ __device__ inline int pipe_units(const PipeSched& s, int phase) {
+    return s.G * (s.qb + (phase < s.rb ? 1 : 0)) + (phase == s.S - 1 ? s.tail : 0);
+}
+// Units of chunks 0..k-1 of a replication that would have entered at step -k (the steps
+// -k..-1, i.e. phases S-k..S-1): where the wrapped pipelines start chunk k at step 0.
+__host__ __device__ inline int64_t pipe_wrap_units(const PipeSched& s, int k) {
+    const int extra = s.rb - (s.S - k);
+    return static_cast<int64_t>(s.G) * (static_cast<int64_t>(k) * s.qb + (extra > 0 ? extra : 0)) +
+           (k > 0 ? s.tail : 0);
+}
+// Replications per warp reserved for the wrap: S - 1 per S-lane pipeline (lanes 1..S-1
+// of the first step).
+__host__ __device__ constexpr int pipe_wrap_per_warp(int S) { return 32 - 32 / S; }
+constexpr int kWrap = 31;  // S = 32
+
 // Seeding: stream slots [slot_begin, slot_begin+count) of a run.
 struct SeedArgs {
     const uint32_t* powers;  // [64][3][8][16] binary powers of the taus88 step as nibble tables
@@ -129,8 +166,12 @@ cudaError_t launch_taus_stream(const uint32_t* powers, Taus seed, int64_t n, uin
 // uni_tab = panel-skip table (mm1 only).
 cudaError_t launch_wlp(int model, const RepArgs& a, const uint32_t* lane_tab,
                        const uint32_t* uni_tab, int64_t lane_units, int grid, cudaStream_t st);
-// WLP as a warp pipeline (pi / walk): no lane jumps; lane_units = ceil(n / 32).
-cudaError_t launch_wlp_pipe(int model, const RepArgs& a, int64_t lane_units, int grid, cudaStream_t st);
+// WLP as a warp pipeline (pi / walk): no per-replication lane jumps; s.S lanes per
+// replication (32, 16 or 8). wrap_tab: lane tables of the distances
+// 2 * pipe_wrap_units(s, lane % S) draws (null: no wrap, S = 32 only; with it a.count >=
+// pipe_wrap_per_warp(S) * warps).
+cudaError_t launch_wlp_pipe(int model, const RepArgs& a, const PipeSched& s, const uint32_t* wrap_tab, int grid,
+                            cudaStream_t st);
 int wlp_pipe_blocks_per_sm();
 // mm1 WLP as a warp pipeline: lane_units = ceil(clients / 32).
 cudaError_t launch_wlp_mm1_pipe(const RepArgs& a, int64_t lane_units, int grid, cudaStream_t st);

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -34,6 +35,7 @@ thread_local std::string g_err;
 thread_local bool g_hw_counters = false;  // wlp_set_hw_counters
 thread_local int g_wlp_variant = 0;       // wlp_set_wlp_variant: 0 auto, 1 lane jumps, 2 pipeline
 thread_local const char* g_last_kernel = "";  // wlp_last_kernel
+thread_local int g_pipe_lanes = 0;       // wlp_set_pipe_lanes: 0 auto, else 8 / 16 / 32
 thread_local int g_tlp_variant = 0;       // wlp_set_tlp_variant: 0 auto, 1 per replication, 2 bitsliced walk
 thread_local int g_stats_order = 0;       // wlp_set_stats_order: 0 accurate (double-double), 1 reference
 
@@ -100,6 +102,7 @@ struct DevCtx {
     bool ready = false;
     DevBuf<uint32_t> powers;
     std::map<uint64_t, DevBuf<uint32_t>> lane_tabs;  // by lane jump stride (draws)
+    std::map<std::tuple<int, int, int, int>, DevBuf<uint32_t>> wrap_tabs;  // by pipeline schedule
     DevBuf<uint32_t> mm1_lane, mm1_skip;
     DevBuf<uint32_t> seeds, in_seeds;
     DevBuf<uint32_t> bseeds;  // walk bitsliced pipeline: group seed bit planes
@@ -249,6 +252,28 @@ int lane_table(DevCtx& c, uint64_t stride, const uint32_t*& out) {
     return WLP_OK;
 }
 
+
+// Lane tables of the wrapped pipelines: lane l jumps 2 * pipe_wrap_units(s, l) draws (every
+// model here takes two draws per unit), cached per schedule.
+int wrap_table(DevCtx& c, const PipeSched& s, const uint32_t*& out) {
+    const auto key = std::make_tuple(s.G * 64 + s.S, s.qb, s.rb, s.tail);
+    auto it = c.wrap_tabs.find(key);
+    if (it != c.wrap_tabs.end()) {
+        out = it->second.p;
+        return WLP_OK;
+    }
+    if (static_cast<int>(c.wrap_tabs.size()) >= kMaxLaneTabs) {
+        WLP_CUDA(cudaDeviceSynchronize());
+        for (auto& kv : c.wrap_tabs) kv.second.release();
+        c.wrap_tabs.clear();
+    }
+    std::array<uint64_t, 32> dist{};
+    for (int l = 0; l < 32; ++l) dist[l] = 2ull * static_cast<uint64_t>(pipe_wrap_units(s, l % s.S));
+    DevBuf<uint32_t>& b = c.wrap_tabs[key];
+    WLP_TRY(upload_u32(b, lane_tables_dist(dist)));
+    out = b.p;
+    return WLP_OK;
+}
 
 int check_model_mode(int model, int mode) {
     if (model < 0 || model > 2) return fail(WLP_EDOMAIN, "unknown model id");
@@ -586,17 +611,37 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
     } else {
         const int64_t K = (a.n + 31) / 32;
         // Lane jumps cost ~80 instructions per lane per replication against K units of
-        // ~35-39; the pipeline costs a 31-step drain per warp against its replications.
-        const double per_warp = static_cast<double>(count) / static_cast<double>(warps);
+        // ~31-39. The pipeline has none; with the wrap (every S-lane pipeline owns S - 1
+        // replications beyond the ones its warp grabs) it has no fill or drain either;
+        // without it a 31-step triangle per warp idles.
+        int S = g_pipe_lanes;
+        if (S == 0) S = a.n >= 32 * 120 ? 32 : (a.n >= 16 * 120 ? 16 : 8);
+        const int64_t wpw = pipe_wrap_per_warp(S);
+        int pgrid = static_cast<int>(std::min<int64_t>(grid_out, static_cast<int64_t>(c.sms) * c.pipe_bps));
+        bool wrap = count >= 2 * wpw * static_cast<int64_t>(pgrid) * (kWlpBlock / 32);
+        if (!wrap && (g_wlp_variant == 2 || S < 32) && count >= 2 * wpw * (kWlpBlock / 32)) {
+            // fewer warps, each with its wrap replications (a forced pipeline on a small run)
+            pgrid = static_cast<int>(count / (2 * wpw * (kWlpBlock / 32)));
+            wrap = true;
+        }
+        if (!wrap) S = 32;  // only the whole-warp pipeline runs without the wrap
+        const int64_t pwarps = static_cast<int64_t>(pgrid) * (kWlpBlock / 32);
+        const double per_warp = static_cast<double>(count) / static_cast<double>(pwarps);
         const bool pipe = !g_hw_counters &&
                           (g_wlp_variant == 2 ||
-                           (g_wlp_variant == 0 && 31.0 / (per_warp + 31.0) < 80.0 / (35.0 * K + 80.0)));
+                           (g_wlp_variant == 0 && ((wrap && pgrid >= c.sms) ||
+                                                   31.0 / (per_warp + 31.0) < 80.0 / (35.0 * K + 80.0))));
         if (pipe) {
-            const int64_t cap = static_cast<int64_t>(c.sms) * c.pipe_bps;
-            grid_out = static_cast<int>(std::min<int64_t>(grid_out, cap));
+            grid_out = pgrid;
+            const int P = 32 / S;
+            const int64_t pool = count - (wrap ? wpw * pwarps : 0);
+            a.grab = P * static_cast<int>(std::clamp<int64_t>(pool / (pwarps * 32 * P), 1, 32));
+            const PipeSched ps = pipe_sched(a.n, a.n >= 8 * S ? 8 : 1, S);
+            const uint32_t* wtab = nullptr;
+            if (wrap) WLP_TRY(wrap_table(c, ps, wtab));
             g_last_kernel = model == WLP_MODEL_PI ? "k_wlp_pipe<pi>" : "k_wlp_pipe<walk>";
             WLP_TRY(mark_model_start(c, st));
-            WLP_CUDA(launch_wlp_pipe(model, a, K, grid_out, st));
+            WLP_CUDA(launch_wlp_pipe(model, a, ps, wtab, grid_out, st));
         } else {
             // With few replications per warp the last groups leave a tail: 3 of the 4
             // resident blocks per SM then do better (config 3: 0.143 vs 0.148 ms).
@@ -729,6 +774,13 @@ int wlp_set_wlp_variant(int variant) {
 }
 
 const char* wlp_last_kernel(void) { return g_last_kernel; }
+
+int wlp_set_pipe_lanes(int lanes) {
+    if (lanes != 0 && lanes != 8 && lanes != 16 && lanes != 32)
+        return fail(WLP_EDOMAIN, "pipeline lanes per replication must be 0 (auto), 8, 16 or 32");
+    g_pipe_lanes = lanes;
+    return WLP_OK;
+}
 
 int wlp_set_tlp_variant(int variant) {
     if (variant < 0 || variant > 2) return fail(WLP_EDOMAIN, "tlp variant must be 0 (auto), 1 or 2");
@@ -1256,10 +1308,11 @@ struct DevShard {
 // The calling thread's settings, applied in each worker (they are thread-local).
 struct ThreadSettings {
     bool hw;
-    int wv, tv, so;
+    int wv, tv, so, pl;
     void apply() const {
         g_hw_counters = hw;
         g_wlp_variant = wv;
+        g_pipe_lanes = pl;
         g_tlp_variant = tv;
         g_stats_order = so;
     }
@@ -1402,7 +1455,7 @@ int wlp_run_devices(int model, const wlp_params* p, int mode, uint64_t master_se
         return rc;
     }
     copy_warning(!pw.empty() && !lw.empty() ? pw + "; " + lw : (!pw.empty() ? pw : lw), warn, warn_cap);
-    const ThreadSettings ts{g_hw_counters, g_wlp_variant, g_tlp_variant, g_stats_order};
+    const ThreadSettings ts{g_hw_counters, g_wlp_variant, g_tlp_variant, g_stats_order, g_pipe_lanes};
     const Taus master = master_from_seed(master_seed);
     double* const host[3] = {out0, out1, out2};
     Barrier bar(nd);

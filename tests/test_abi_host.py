@@ -54,7 +54,11 @@ def test_kernel_variant_knobs_and_last_kernel():
         with pytest.raises(w.DomainError):
             with w.tlp_variant(bad):
                 pass
-    with w.wlp_variant(4), w.tlp_variant(2):
+    for bad in (-1, 4, 12, 64):
+        with pytest.raises(w.DomainError):
+            with w.pipe_lanes(bad):
+                pass
+    with w.wlp_variant(4), w.tlp_variant(2), w.pipe_lanes(8):
         pass
     assert isinstance(w.last_kernel(), str)
 

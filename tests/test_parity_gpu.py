@@ -359,6 +359,27 @@ def test_wlp_lane_jump_and_pipeline_kernels_agree_with_oracle(gpu, port, variant
         assert np.array_equal(run.outputs[name], want[name]), name
 
 
+@pytest.mark.parametrize("model", [0, 2])
+@pytest.mark.parametrize("R,n", [(992, 1), (1000, 5), (2500, 257), (2500, 999), (3001, 1000), (1500, 10_000),
+                                 (4000, 63), (993, 2049)])
+@pytest.mark.parametrize("lanes", [32, 16, 8])
+def test_wrapped_pipeline_rotating_chunks_vs_oracle(gpu, port, model, R, n, lanes):
+    # the pi / walk warp pipeline with rotating chunk lengths (PipeSched: G-unit blocks, a
+    # remainder of blocks spread over the phases, a sub-block tail at phase 31) and the wrap
+    # (lanes 1..31 start kWrap replications per warp at their chunk by a lane-table jump,
+    # whose early chunks then run in the drain): every replication bit-exact, including the
+    # wrap ones, which sit at the front of the array (warp w owns [31w, 31w + 31)); with
+    # 16 or 8 lanes per replication, 2 or 4 pipelines per warp, each with its own wrap set
+    kw = dict(replications=R, draws=n) if model == 0 else dict(replications=R, steps=n, chunks=5 + R % 17)
+    p = gpu.ModelParams(**kw)
+    want = port.run_model(model, oracle.params_from(p), 2024 + R)
+    with gpu.wlp_variant(2), gpu.pipe_lanes(lanes):
+        run = gpu.run_model(gpu.ModelKind(model), p, gpu.ExecutionMode.Wlp, master_seed=2024 + R)
+    assert gpu.last_kernel().startswith("k_wlp_pipe")
+    for name in oracle.OUTPUTS[model]:
+        assert np.array_equal(run.outputs[name], want[name]), name
+
+
 @pytest.mark.parametrize("model,kw", [(0, dict(replications=10_000_000, draws=1000)),
                                       (2, dict(replications=10_000_000, steps=1000, chunks=30)),
                                       (1, dict(replications=2_000_000, clients=1000))])

@@ -118,20 +118,27 @@ __global__ void k_dfma(double* out, double seed) {
     if (s == 1.2345) out[0] = s;
 }
 
+// Eight independent conversion chains: each conversion's input is the high word of the
+// previous result (a register half, no extra instruction), so no conversion is loop
+// invariant. (The round-1 version converted the same v + i every iteration; the compiler
+// hoisted it out of the loop and the row reported an impossible 124 warp-instr/clk/SM.)
+template <bool SIGNED>
 __global__ void k_i2f64(double* out, uint32_t seed) {
-    double acc[8];
-    uint32_t v = seed + threadIdx.x;
-    for (int i = 0; i < 8; ++i) acc[i] = 0;
+    uint32_t v[8];
+    for (int i = 0; i < 8; ++i) v[i] = seed + threadIdx.x * 8 + i;
     for (int it = 0; it < ITERS; ++it)
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             double d;
-            asm volatile("cvt.rn.f64.u32 %0, %1;" : "=d"(d) : "r"(v + i));
-            acc[i] = d;  // keep one conversion per instruction slot
+            if (SIGNED)
+                asm volatile("cvt.rn.f64.s32 %0, %1;" : "=d"(d) : "r"(v[i]));
+            else
+                asm volatile("cvt.rn.f64.u32 %0, %1;" : "=d"(d) : "r"(v[i]));
+            v[i] = static_cast<uint32_t>(__double2hiint(d));
         }
-    double s = 0;
-    for (int i = 0; i < 8; ++i) s += acc[i];
-    if (s == 1.2345) out[0] = s;
+    uint32_t s = 0;
+    for (int i = 0; i < 8; ++i) s += v[i];
+    if (s == 12345u) out[0] = s;
 }
 
 __global__ void k_imadhi(uint32_t* out, uint32_t seed) {
@@ -140,6 +147,17 @@ __global__ void k_imadhi(uint32_t* out, uint32_t seed) {
     for (int it = 0; it < ITERS; ++it)
 #pragma unroll
         for (int i = 0; i < 8; ++i) asm volatile("mul.hi.u32 %0, %0, %1;" : "+r"(a[i]) : "r"(a[(i + 5) & 7] | 0x80000001u));
+    uint32_t s = 0;
+    for (int i = 0; i < 8; ++i) s ^= a[i];
+    if (s == 0x12345) out[0] = s;
+}
+
+__global__ void k_shfl(uint32_t* out, uint32_t seed) {  // SHFL.UP (the pipelines' hand-over)
+    uint32_t a[8];
+    for (int i = 0; i < 8; ++i) a[i] = seed + threadIdx.x * 8 + i;
+    for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = __shfl_up_sync(0xffffffffu, a[i], 1);
     uint32_t s = 0;
     for (int i = 0; i < 8; ++i) s ^= a[i];
     if (s == 0x12345) out[0] = s;
@@ -200,7 +218,9 @@ int main() {
     report("IMAD.HI", time_it([&] { k_imadhi<<<blocks, threads>>>(du, 1); }), 8);
     report("DADD", time_it([&] { k_dadd<<<blocks, threads>>>(dd, 1.0); }), 8);
     report("DFMA", time_it([&] { k_dfma<<<blocks, threads>>>(dd, 1.0); }), 8);
-    report("I2F.F64.U32", time_it([&] { k_i2f64<<<blocks, threads>>>(dd, 1); }), 8);
+    report("I2F.F64.U32 (chained)", time_it([&] { k_i2f64<false><<<blocks, threads>>>(dd, 1); }), 8);
+    report("SHFL.UP", time_it([&] { k_shfl<<<blocks, threads>>>(du, 1); }), 8);
+    report("I2F.F64.S32 (chained)", time_it([&] { k_i2f64<true><<<blocks, threads>>>(dd, 1); }), 8);
     // taus88: 4 streams x (16 SASS per draw) + acc add per draw
     report("taus88 draw (16 SASS+1)", time_it([&] { k_mixed_taus<<<blocks, threads>>>(du, 7); }), 4 * 17);
     Mul mm{{1u << 13, 1u << 7, 1u << 21}, {1u << 12, 1u << 4, 1u << 17}};

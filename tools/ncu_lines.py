@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Per-source-line instruction counts and stall samples of an ncu report (run here).
 
-    python tools/ncu_lines.py report.ncu-rep [top]
+    python tools/ncu_lines.py report.ncu-rep|page.csv[.gz] [top]
 """
 import csv
 import io
@@ -10,8 +10,15 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                     capture_output=True, text=True).stdout
+if rep.endswith(".csv.gz"):  # a source page exported on the GPU box (tools/_prof*.sh)
+    import gzip
+
+    out = gzip.open(rep, "rt").read()
+elif rep.endswith(".csv"):
+    out = open(rep).read()
+else:
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                         capture_output=True, text=True).stdout
 rows = []
 fname = ""
 total_i = total_s = 0

@@ -26,6 +26,7 @@ ap.add_argument("--ir", action="store_true", help="run the reference's IR kernel
 ap.add_argument("--lambda", dest="lam", type=float, default=0.5)
 ap.add_argument("--wlp-variant", type=int, default=0)
 ap.add_argument("--tlp-variant", type=int, default=0)
+ap.add_argument("--pipe-lanes", type=int, default=0)
 a = ap.parse_args()
 m = w.model_from_name(a.model)
 p = w.ModelParams(replications=a.R, draws=a.N, clients=a.N, steps=a.N, lambda_=a.lam)
@@ -41,7 +42,7 @@ rep = w.SimReport()
 ctx = w.hw_counters() if a.counters else None
 if ctx:
     ctx.__enter__()
-with w.wlp_variant(a.wlp_variant), w.tlp_variant(a.tlp_variant):
+with w.wlp_variant(a.wlp_variant), w.tlp_variant(a.tlp_variant), w.pipe_lanes(a.pipe_lanes):
     for _ in range(a.repeat):
         w.run_shard(m, p, w.mode_from_name(a.mode), 42, 0, a.R, outs, on_device=True, report=rep)
 if ctx:
