@@ -345,7 +345,7 @@ __device__ __forceinline__ void neg_log1m_batch(const uint32_t (&n)[B], double (
 // the host picks kDivIeee for rates outside [2^-900, 2^900].
 template <int DIV>
 __device__ __forceinline__ double scale(double e, double rate, double inv) {
-    if constexpr (DIV == kDivPow2) {
+    if constexpr (DIV == kDivPow2 || DIV == kDivPow2One) {  // (kDivPow2One: arrivals; services below)
         return __dmul_rn(e, inv);
     } else if constexpr (DIV == kDivRcp) {
         const double q = __dmul_rn(e, inv);
@@ -1594,23 +1594,39 @@ __device__ __forceinline__ Queue mm1_thread_rep(Taus st, int64_t n, int64_t n_wa
 // panel slots: no per-batch compaction, no predicated patch-back into registers.
 // ---------------------------------------------------------------------------------
 constexpr int kPanT = 8;            // clients per lane per panel
+static_assert(kPanT == kMm1PanelT, "the mm1 pipeline schedule counts panels of kMm1PanelT clients");
 constexpr int kPanD = 2 * kPanT;    // draws per lane per panel
-constexpr int kPanRow = kPanD + 2;  // doubles per lane row: an odd number of 16-byte pairs,
-                                    // so 8 lanes' STS.128 / LDS.128 of one column hit all 32 banks
-constexpr int kDrRow = kPanD + 4;   // u32 per lane row of the draw buffer (5 x 16 B: odd, as above)
-constexpr int kNearCap = 128;       // near list entries (expected 32 per panel; more: lane-local path)
+constexpr int kNearCap = 64;        // near list entries (expected 32 per panel; more: lane-local path)
 constexpr uint32_t kNearMax = 0x10000000u;  // draw n is near one (1 - n 2^-32 >= 1 - 2^-4) iff n <= 2^28
 
+// Column-major panel: client c of lane l is the 16-byte pair v[(c * 32 + l) * 2 ..], draw
+// quad q of lane l is dr[(q * 32 + l) * 4 ..]. A quarter warp's STS.128 / LDS.128 of one
+// column covers 128 consecutive bytes (all 32 banks), every offset is a compile-time
+// immediate, and nothing is padded: 6.5 KB per warp, so 4 blocks of 8 warps fit an SM.
 struct PanelWarp {
-    double v[32 * kPanRow];    // lane l, client c: v[l*kPanRow + 2c] = a, + 1 = s
-    uint32_t dr[32 * kDrRow];  // the panel's draws, lane rows
-    uint2 nl[kNearCap];        // near list: {draw, panel slot}
+    double v[kPanT * 32 * 2];  // (a, s) of client c, lane l at [(c*32 + l)*2]
+    uint32_t dr[kPanD * 32];   // draws 4q..4q+3 of lane l at [(q*32 + l)*4]
+    uint2 nl[kNearCap];        // near list: {draw, panel slot (double index into v)}
 };
+// Slot (double index into PanelWarp::v) of draw j of lane l: client j/2, a (even j) or s.
+__host__ __device__ constexpr int pan_slot(int j, int l) { return ((j >> 1) * 32 + l) * 2 + (j & 1); }
+
+// e / mu for a service time (kDivPow2One: mu = 1, the identity)
+template <int DIV>
+__device__ __forceinline__ double scale_mu(double e, double mu, double inv_m) {
+    if constexpr (DIV == kDivPow2One)
+        return e;
+    else
+        return scale<DIV>(e, mu, inv_m);
+}
 
 // e / rate for panel slot parity `odd` (odd slots are services: mu; even arrivals: lambda)
 template <int DIV>
 __device__ __forceinline__ double scale_slot(double e, bool odd, double lambda, double mu, double inv_l, double inv_m) {
-    return scale<DIV>(e, odd ? mu : lambda, odd ? inv_m : inv_l);
+    if constexpr (DIV == kDivPow2One)
+        return odd ? e : scale<DIV>(e, lambda, inv_l);
+    else
+        return scale<DIV>(e, odd ? mu : lambda, odd ? inv_m : inv_l);
 }
 
 #ifndef WLP_PAN_UNROLL
@@ -1657,7 +1673,7 @@ template <int DIV, bool EXACT>
 __device__ __forceinline__ void panel_fill(Taus& st, int ndraw, double lambda, double mu, double inv_l,
                                            double inv_m, const double* tab, PanelWarp& P, unsigned mask,
                                            int lane, unsigned* ev = nullptr) {
-    uint32_t* drow = P.dr + lane * kDrRow;
+    uint4* dq = reinterpret_cast<uint4*>(P.dr) + lane;  // quad q at dq[q * 32]
     uint32_t m = 0;
 #pragma unroll
     for (int j = 0; j < kPanD; j += 4) {
@@ -1676,7 +1692,7 @@ __device__ __forceinline__ void panel_fill(Taus& st, int ndraw, double lambda, d
         near_bit(m, q4.y);
         near_bit(m, q4.z);
         near_bit(m, q4.w);
-        *reinterpret_cast<uint4*>(drow + j) = q4;
+        dq[(j / 4) * 32] = q4;
     }
     const int c = __popc(m);
     int incl = c;
@@ -1688,23 +1704,23 @@ __device__ __forceinline__ void panel_fill(Taus& st, int ndraw, double lambda, d
     const int width = mask == kFull ? 32 : __popc(mask);
     const int total = __shfl_sync(mask, incl, width - 1);
     const bool listed = total <= kNearCap;  // warp-uniform
-    double* row = P.v + lane * kPanRow;
-    const uint32_t slot0 = static_cast<uint32_t>(lane * kPanRow);
+    double2* vq = reinterpret_cast<double2*>(P.v) + lane;  // client c at vq[c * 32]
+    const uint32_t slot0 = static_cast<uint32_t>(pan_slot(0, lane));
     uint32_t sp = static_cast<uint32_t>(__cvta_generic_to_shared(P.nl + (incl - c)));
 #pragma unroll kPanUnroll
     for (int j = 0; j < kPanD; j += 4) {
-        const uint4 q4 = *reinterpret_cast<const uint4*>(drow + j);
+        const uint4 q4 = dq[(j / 4) * 32];
         const double a0 = scale<DIV>(neg_log1m_table_dev(q4.x, tab), lambda, inv_l);
         const double s0 = scale<DIV>(neg_log1m_table_dev(q4.y, tab), mu, inv_m);
         const double a1 = scale<DIV>(neg_log1m_table_dev(q4.z, tab), lambda, inv_l);
         const double s1 = scale<DIV>(neg_log1m_table_dev(q4.w, tab), mu, inv_m);
-        *reinterpret_cast<double2*>(row + j) = make_double2(a0, s0);
-        *reinterpret_cast<double2*>(row + j + 2) = make_double2(a1, s1);
+        vq[(j / 2) * 32] = make_double2(a0, s0);
+        vq[(j / 2 + 1) * 32] = make_double2(a1, s1);
         if (listed) {
-            near_append_m(sp, m, j, q4.x, slot0 + j);
-            near_append_m(sp, m, j + 1, q4.y, slot0 + j + 1);
-            near_append_m(sp, m, j + 2, q4.z, slot0 + j + 2);
-            near_append_m(sp, m, j + 3, q4.w, slot0 + j + 3);
+            near_append_m(sp, m, j, q4.x, slot0 + pan_slot(j, 0));
+            near_append_m(sp, m, j + 1, q4.y, slot0 + pan_slot(j + 1, 0));
+            near_append_m(sp, m, j + 2, q4.z, slot0 + pan_slot(j + 2, 0));
+            near_append_m(sp, m, j + 3, q4.w, slot0 + pan_slot(j + 3, 0));
         }
     }
     if (listed) {
@@ -1715,12 +1731,13 @@ __device__ __forceinline__ void panel_fill(Taus& st, int ndraw, double lambda, d
             const double e = it.x == 0u ? -0.0 : -log_near_one_dev(one_minus_u32_dev(it.x));
             P.v[it.y] = scale_slot<DIV>(e, it.y & 1u, lambda, mu, inv_l, inv_m);
         }
-    } else {  // (never at random draws) each lane fixes its own row
+    } else {  // (rare: > kNearCap near draws in the panel) each lane fixes its own clients
+        const uint32_t* dr = P.dr + lane * 4;
         for (int j = 0; j < kPanD; ++j) {
-            const uint32_t n = drow[j];
+            const uint32_t n = dr[(j >> 2) * 128 + (j & 3)];
             if (n <= kNearMax) {
                 const double e = n == 0u ? -0.0 : -log_near_one_dev(one_minus_u32_dev(n));
-                row[j] = scale_slot<DIV>(e, j & 1, lambda, mu, inv_l, inv_m);
+                P.v[pan_slot(j, lane)] = scale_slot<DIV>(e, j & 1, lambda, mu, inv_l, inv_m);
             }
         }
     }
@@ -1732,11 +1749,11 @@ __device__ __forceinline__ void panel_fill(Taus& st, int ndraw, double lambda, d
 template <bool COUNT = false>
 __device__ __forceinline__ void panel_clients(Queue& q, const PanelWarp& P, int cnt, int lane, unsigned act = 0u,
                                               unsigned sync = 0u, unsigned* events = nullptr) {
-    const double2* row = reinterpret_cast<const double2*>(P.v + lane * kPanRow);
+    const double2* row = reinterpret_cast<const double2*>(P.v) + lane;  // client c at row[c * 32]
     if (!COUNT && cnt == kPanT) {
 #pragma unroll
         for (int c = 0; c < kPanT; ++c) {
-            const double2 v = row[c];
+            const double2 v = row[c * 32];
             q.client(v.x, v.y);
         }
     } else {
@@ -1745,7 +1762,7 @@ __device__ __forceinline__ void panel_clients(Queue& q, const PanelWarp& P, int 
             const bool on = c < cnt;
             bool dry = false;
             if (on) {
-                const double2 v = row[c];
+                const double2 v = row[c * 32];
                 dry = q.client(v.x, v.y);
             }
             if (COUNT && act && on) split_if(act, dry, *events, sync);  // (cnt is warp-uniform in TLP)
@@ -1753,43 +1770,32 @@ __device__ __forceinline__ void panel_clients(Queue& q, const PanelWarp& P, int 
     }
 }
 
-struct Mm1PipeWarp {
-    PanelWarp pw;
-    long long rep[32];
-    double sums[32][3];  // idle, sumw, sums
-};
-
+// mm1 WLP as a warp pipeline, rotating schedule (PipeSched with G = kPanT clients: every
+// lane runs the same number of whole panels per step, and any 32 consecutive steps cover
+// a replication's n clients; with a fixed split ceil(n/32) lane 31 idled through 3 of 4
+// panels at 1,000 clients). Lane 31 stores each finished replication's three outputs
+// itself (three one-lane stores per step, ~1 % of a step's instructions), which frees the
+// shared memory of a result buffer: with the column-major panel, 4 blocks of 8 warps fit.
+// EXACT: some chunk has a partial panel (n % kPanT != 0), whose draws are predicated so
+// the hand-over state is exact; otherwise lanes draw whole panels unpredicated.
 template <int DIV, bool EXACT>
 #ifndef WLP_MM1_MINB
 #define WLP_MM1_MINB 3
 #endif
-__global__ void __launch_bounds__(kMm1Block, WLP_MM1_MINB) k_wlp_mm1_pipe(RepArgs a, int64_t K) {
+__global__ void __launch_bounds__(kMm1Block, WLP_MM1_MINB) k_wlp_mm1_pipe_ragged(RepArgs a, PipeSched ps) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double* logtab = reinterpret_cast<double*>(smraw);
-    Mm1PipeWarp& P = reinterpret_cast<Mm1PipeWarp*>(logtab + 256)[threadIdx.x >> 5];
+    PanelWarp& P = reinterpret_cast<PanelWarp*>(logtab + 256)[threadIdx.x >> 5];
     stage_log_table(logtab);
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    int64_t mine = a.n - static_cast<int64_t>(lane) * K;
-    mine = mine < 0 ? 0 : (mine > K ? K : mine);
-    const uint32_t seg = static_cast<uint32_t>(mine), seg_max = static_cast<uint32_t>(K);
     const double nd = static_cast<double>(a.n);
     Taus st{kMin1, kMin2, kMin3};
     Queue q;
     long long rep = -1;
     int64_t cur = 0, cend = 0;
     bool more = true;
-    int nemit = 0;
-    auto flush = [&](int cnt) {
-        __syncwarp();
-        if (lane < cnt) {
-            const long long r = P.rep[lane];
-            a.out0[r] = __ddiv_rn(P.sums[lane][0], nd);
-            a.out1[r] = __ddiv_rn(P.sums[lane][1], nd);
-            a.out2[r] = __ddiv_rn(P.sums[lane][2], nd);
-        }
-        __syncwarp();
-    };
+    int phase = 0;
     for (;;) {
         if (more && cur >= cend) {
             const int64_t base = grab_take(grab_issue(a, lane));
@@ -1809,23 +1815,18 @@ __global__ void __launch_bounds__(kMm1Block, WLP_MM1_MINB) k_wlp_mm1_pipe(RepArg
         }
         if (more) ++cur;
         if (!__any_sync(kFull, rep >= 0)) break;
-        const uint32_t units = rep >= 0 ? seg : 0u;
-        for (uint32_t done = 0; done < seg_max; done += kPanT) {
-            const int cnt = units <= done ? 0 : (units - done < kPanT ? static_cast<int>(units - done) : kPanT);
-            panel_fill<DIV, EXACT>(st, 2 * cnt, a.lambda, a.mu, a.inv_lambda, a.inv_mu, logtab, P.pw, kFull, lane);
-            panel_clients(q, P.pw, cnt, lane);
+        const int units = rep >= 0 ? pipe_units(ps, phase) : 0;
+        const int steps = (pipe_units(ps, phase) + kPanT - 1) / kPanT;  // warp-uniform
+        for (int p = 0; p < steps; ++p) {
+            const int left = units - p * kPanT;
+            const int cnt = left <= 0 ? 0 : (left < kPanT ? left : kPanT);
+            panel_fill<DIV, EXACT>(st, 2 * cnt, a.lambda, a.mu, a.inv_lambda, a.inv_mu, logtab, P, kFull, lane);
+            panel_clients(q, P, cnt, lane);
         }
-        if (__shfl_sync(kFull, rep, 31) >= 0) {  // lane 31 finished a replication
-            if (lane == 31) {
-                P.rep[nemit] = rep;
-                P.sums[nemit][0] = q.idle;
-                P.sums[nemit][1] = q.sumw;
-                P.sums[nemit][2] = q.sums;
-            }
-            if (++nemit == 32) {
-                flush(32);
-                nemit = 0;
-            }
+        if (lane == 31 && rep >= 0) {  // lane 31 finished a replication
+            a.out0[rep] = __ddiv_rn(q.idle, nd);
+            a.out1[rep] = __ddiv_rn(q.sumw, nd);
+            a.out2[rep] = __ddiv_rn(q.sums, nd);
         }
         st.s1 = __shfl_up_sync(kFull, st.s1, 1);
         st.s2 = __shfl_up_sync(kFull, st.s2, 1);
@@ -1835,11 +1836,175 @@ __global__ void __launch_bounds__(kMm1Block, WLP_MM1_MINB) k_wlp_mm1_pipe(RepArg
         q.sumw = __shfl_up_sync(kFull, q.sumw, 1);
         q.sums = __shfl_up_sync(kFull, q.sums, 1);
         rep = __shfl_up_sync(kFull, rep, 1);
+        phase = (phase + 1) & 31;
     }
-    flush(nemit);
 }
 
-constexpr size_t kMm1PipeSmem = 256 * 8 + (kMm1Block / 32) * sizeof(Mm1PipeWarp);
+constexpr size_t kMm1PipeSmem = 256 * 8 + (kMm1Block / 32) * sizeof(PanelWarp);
+
+// ---------------------------------------------------------------------------------
+// mm1 WLP warp pipeline, single-pass panels with the recursion interleaved (the default
+// for n % 8 == 0). Per lane and panel of kPanT clients:
+// * one pass draws, evaluates the branch-free table path of every exponential and stores
+//   the (a, s) pairs column-major; a near-one draw (1 in 16) also claims a list entry
+//   with a shared-memory atomic (ATOMS) and records {draw, slot}. No per-lane flag masks,
+//   no lane scan, no draw staging: ~4 instructions per draw of bookkeeping instead of ~8;
+// * the warp then evaluates the list (one pass of the near-one polynomial across the
+//   lanes, straight into the slots). More than kNearCap near-ones (never at random draws)
+//   redo the panel from the stream state saved before it, each lane fixing its own;
+// * the Lindley recursion of panel p runs client by client interleaved with the fill of
+//   panel p + 1 into the same slots (each slot is read by the recursion before its own
+//   lane overwrites it), so the recursion's dependent DADD chain overlaps independent
+//   draw / log work instead of idling the warp.
+// S lanes per replication (32, or 8: four pipelines per warp, 4x longer steps; mm1 has
+// no wrap, its queue state is sequential, so the S-1 step drain remains: ~1 % at config 4).
+// ---------------------------------------------------------------------------------
+constexpr int kNearCap2 = 128;  // list entries per panel (expected 32 of 512 draws)
+static_assert((kNearCap2 & (kNearCap2 - 1)) == 0, "the list index wraps with a mask");
+
+struct Mm1Pan {
+    double2 v[kPanT][32];  // (a, s) of client c of lane l
+    uint2 nl[kNearCap2];   // near list: {draw, slot (double index into v)}
+    Taus save[32];         // each lane's stream state before the panel being filled
+    uint32_t cnt;          // near-list claims of the panel
+    uint32_t pad[3];
+};
+constexpr size_t kMm1Pipe2Smem = 256 * 8 + (kMm1Block / 32) * sizeof(Mm1Pan);
+
+// Client c of a panel: two draws, their table-path exponentials, near-ones listed (a
+// shared-memory atomic claims the list entry; the claim counter runs past the capacity on
+// overflow, the index wraps, and fix_near redoes such a panel).
+template <int DIV>
+__device__ __forceinline__ void fill_client(Taus& st, int c, int lane, bool on, double lambda, double mu, double inv_l,
+                                            double inv_m, const double* tab, Mm1Pan& W) {
+    uint32_t x, y;
+    taus_next2(st, x, y);
+    const double a = scale<DIV>(neg_log1m_table_dev(x, tab), lambda, inv_l);
+    const double sv = scale_mu<DIV>(neg_log1m_table_dev(y, tab), mu, inv_m);
+    W.v[c][lane] = make_double2(a, sv);
+    const uint32_t slot = static_cast<uint32_t>(pan_slot(2 * c, lane));
+    if (on && x <= kNearMax) W.nl[atomicAdd(&W.cnt, 1u) & (kNearCap2 - 1)] = make_uint2(x, slot);
+    if (on && y <= kNearMax) W.nl[atomicAdd(&W.cnt, 1u) & (kNearCap2 - 1)] = make_uint2(y, slot + 1);
+}
+
+// The listed near-ones of the panel just filled, into their slots; on overflow every lane
+// redraws its panel from the saved state and fixes its own near-ones.
+template <int DIV>
+__device__ __forceinline__ void fix_near(Mm1Pan& W, int lane, bool on, double lambda, double mu, double inv_l,
+                                         double inv_m) {
+    __syncwarp();
+    const uint32_t total = W.cnt;
+    __syncwarp();
+    if (lane == 0) W.cnt = 0;
+    double* v = reinterpret_cast<double*>(&W.v[0][0]);
+    if (total <= kNearCap2) {
+        for (uint32_t k = lane; k < total; k += 32) {
+            const uint2 it = W.nl[k];
+            const double e = it.x == 0u ? -0.0 : -log_near_one_dev(one_minus_u32_dev(it.x));
+            v[it.y] = scale_slot<DIV>(e, it.y & 1u, lambda, mu, inv_l, inv_m);
+        }
+    } else if (on) {
+        Taus t = W.save[lane];
+        for (int j = 0; j < kPanD; ++j) {
+            const uint32_t n = taus_next(t);
+            if (n <= kNearMax) {
+                const double e = n == 0u ? -0.0 : -log_near_one_dev(one_minus_u32_dev(n));
+                v[pan_slot(j, lane)] = scale_slot<DIV>(e, j & 1, lambda, mu, inv_l, inv_m);
+            }
+        }
+    }
+    __syncwarp();
+}
+
+template <int DIV>
+__device__ __forceinline__ void fill_panel(Taus& st, int lane, bool on, double lambda, double mu, double inv_l,
+                                           double inv_m, const double* tab, Mm1Pan& W) {
+    W.save[lane] = st;
+#pragma unroll
+    for (int c = 0; c < kPanT; ++c) fill_client<DIV>(st, c, lane, on, lambda, mu, inv_l, inv_m, tab, W);
+    fix_near<DIV>(W, lane, on, lambda, mu, inv_l, inv_m);
+}
+
+// One pipeline step of a lane: np panels of its chunk (np >= 1, warp-uniform). Panel p's
+// recursion runs client by client interleaved with the fill of panel p + 1.
+template <int DIV>
+__device__ __forceinline__ void mm1_chunk(Taus& st, Queue& q, int np, int lane, bool on, double lambda, double mu,
+                                          double inv_l, double inv_m, const double* tab, Mm1Pan& W) {
+    fill_panel<DIV>(st, lane, on, lambda, mu, inv_l, inv_m, tab, W);
+    for (int p = 1; p < np; ++p) {
+        W.save[lane] = st;
+#pragma unroll
+        for (int c = 0; c < kPanT; ++c) {
+            const double2 v = W.v[c][lane];  // panel p-1's client c, then its slot is refilled
+            q.client(v.x, v.y);
+            fill_client<DIV>(st, c, lane, on, lambda, mu, inv_l, inv_m, tab, W);
+        }
+        fix_near<DIV>(W, lane, on, lambda, mu, inv_l, inv_m);
+    }
+#pragma unroll
+    for (int c = 0; c < kPanT; ++c) {
+        const double2 v = W.v[c][lane];
+        q.client(v.x, v.y);
+    }
+}
+
+template <int DIV, int S>
+__global__ void __launch_bounds__(kMm1Block, WLP_MM1_MINB) k_wlp_mm1_pipe(RepArgs a, PipeSched ps) {
+    constexpr int P = 32 / S;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double* logtab = reinterpret_cast<double*>(smraw);
+    Mm1Pan& W = reinterpret_cast<Mm1Pan*>(logtab + 256)[threadIdx.x >> 5];
+    stage_log_table(logtab);
+    if ((threadIdx.x & 31) == 0) W.cnt = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, g = lane / S, pos = lane % S;
+    const double nd = static_cast<double>(a.n);
+    Taus st{kMin1, kMin2, kMin3};
+    Queue q;
+    long long rep = -1;
+    int64_t cur = 0, cend = 0;
+    bool more = true;
+    int phase = 0;
+    for (;;) {
+        if (more && cur >= cend) {  // next group (a multiple of P replications)
+            const int64_t base = grab_take(grab_issue(a, lane));
+            if (base >= a.count) {
+                more = false;
+            } else {
+                cur = base;
+                cend = base + a.grab < a.count ? base + a.grab : a.count;
+            }
+        }
+        if (pos == 0) {  // feed each pipeline a fresh queue on its next replication's stream
+            const int64_t r = cur + g;
+            rep = more && r < cend ? r : -1;
+            if (rep >= 0) {
+                st = load_seed(a, r);
+                q = Queue();
+            }
+        }
+        if (more) cur += P;
+        if (!more && !__any_sync(kFull, rep >= 0)) break;
+        const int np = pipe_units(ps, phase) / kPanT;
+        if (np > 0)
+            mm1_chunk<DIV>(st, q, np, lane, rep >= 0, a.lambda, a.mu, a.inv_lambda, a.inv_mu, logtab, W);
+        if (pos == S - 1 && rep >= 0) {  // the pipeline's last lane finished a replication
+            a.out0[rep] = __ddiv_rn(q.idle, nd);
+            a.out1[rep] = __ddiv_rn(q.sumw, nd);
+            a.out2[rep] = __ddiv_rn(q.sums, nd);
+        }
+        st.s1 = __shfl_up_sync(kFull, st.s1, 1, S);
+        st.s2 = __shfl_up_sync(kFull, st.s2, 1, S);
+        st.s3 = __shfl_up_sync(kFull, st.s3, 1, S);
+        q.u = __shfl_up_sync(kFull, q.u, 1, S);
+        q.idle = __shfl_up_sync(kFull, q.idle, 1, S);
+        q.sumw = __shfl_up_sync(kFull, q.sumw, 1, S);
+        q.sums = __shfl_up_sync(kFull, q.sums, 1, S);
+        rep = __shfl_up_sync(kFull, rep, 1, S);
+        phase = phase == S - 1 ? 0 : phase + 1;
+    }
+}
+
 
 __device__ __forceinline__ unsigned block_lane_mask() {  // partial last warp of odd-sized blocks
     const int in_warp = static_cast<int>(blockDim.x) - (static_cast<int>(threadIdx.x) & ~31);
@@ -1847,7 +2012,7 @@ __device__ __forceinline__ unsigned block_lane_mask() {  // partial last warp of
 }
 
 #ifndef WLP_TLP_MM1_MINB
-#define WLP_TLP_MM1_MINB 3
+#define WLP_TLP_MM1_MINB 4
 #endif
 // SMALL: blocks of at most 256 threads (the default TLP block), register budget for
 // WLP_TLP_MM1_MINB blocks per SM; else any block size up to 1024.
@@ -2288,26 +2453,52 @@ cudaError_t launch_wlp_pipe(int model, const RepArgs& a, const PipeSched& s, con
     return cudaGetLastError();
 }
 
-cudaError_t launch_wlp_mm1_pipe(const RepArgs& a, int64_t lane_units, int grid, cudaStream_t st) {
+cudaError_t launch_wlp_mm1_pipe(const RepArgs& a, const PipeSched& ps, int grid, cudaStream_t st) {
     if (a.count <= 0) return cudaSuccess;
-    const bool exact = 31 * lane_units > a.n || lane_units % kPanT != 0;
-    auto go = [&](auto kernel) { kernel<<<grid, kMm1Block, kMm1PipeSmem, st>>>(a, lane_units); };
+    if (ps.G == kPanT && ps.tail == 0 && ps.qb > 0) {  // whole panels at every step
+        const bool mu_one = a.div == kDivPow2 && a.mu == 1.0;
+        auto go = [&](auto kernel) {
+            allow_smem(kernel, kMm1Pipe2Smem);
+            kernel<<<grid, kMm1Block, kMm1Pipe2Smem, st>>>(a, ps);
+        };
+        auto by_s = [&](auto d) {
+            constexpr int D = decltype(d)::value;
+            if (ps.S == 8)
+                go(k_wlp_mm1_pipe<D, 8>);
+            else if (ps.S == 16)
+                go(k_wlp_mm1_pipe<D, 16>);
+            else
+                go(k_wlp_mm1_pipe<D, 32>);
+        };
+        if (mu_one)
+            by_s(std::integral_constant<int, kDivPow2One>{});
+        else
+            by_div(a.div, by_s);
+        return cudaGetLastError();
+    }
+    if (ps.S != 32) return cudaErrorInvalidValue;
+    const bool exact = !(ps.G == kPanT && ps.tail == 0);  // some chunk ends inside a panel
+    auto go = [&](auto kernel) { kernel<<<grid, kMm1Block, kMm1PipeSmem, st>>>(a, ps); };
     by_div(a.div, [&](auto d) {
         constexpr int D = decltype(d)::value;
-        exact ? go(k_wlp_mm1_pipe<D, true>) : go(k_wlp_mm1_pipe<D, false>);
+        exact ? go(k_wlp_mm1_pipe_ragged<D, true>) : go(k_wlp_mm1_pipe_ragged<D, false>);
     });
     return cudaGetLastError();
 }
 
 int wlp_mm1_pipe_blocks_per_sm() {
     int nb = 0;
-    allow_smem(k_wlp_mm1_pipe<kDivIeee, true>, kMm1PipeSmem);
-    allow_smem(k_wlp_mm1_pipe<kDivIeee, false>, kMm1PipeSmem);
-    allow_smem(k_wlp_mm1_pipe<kDivPow2, true>, kMm1PipeSmem);
-    allow_smem(k_wlp_mm1_pipe<kDivPow2, false>, kMm1PipeSmem);
-    allow_smem(k_wlp_mm1_pipe<kDivRcp, true>, kMm1PipeSmem);
-    allow_smem(k_wlp_mm1_pipe<kDivRcp, false>, kMm1PipeSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_mm1_pipe<kDivIeee, true>, kMm1Block, kMm1PipeSmem);
+    allow_smem(k_wlp_mm1_pipe_ragged<kDivIeee, true>, kMm1PipeSmem);
+    allow_smem(k_wlp_mm1_pipe_ragged<kDivIeee, false>, kMm1PipeSmem);
+    allow_smem(k_wlp_mm1_pipe_ragged<kDivPow2, true>, kMm1PipeSmem);
+    allow_smem(k_wlp_mm1_pipe_ragged<kDivPow2, false>, kMm1PipeSmem);
+    allow_smem(k_wlp_mm1_pipe_ragged<kDivRcp, true>, kMm1PipeSmem);
+    allow_smem(k_wlp_mm1_pipe_ragged<kDivRcp, false>, kMm1PipeSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_mm1_pipe_ragged<kDivIeee, true>, kMm1Block, kMm1PipeSmem);
+    int nb2 = 0;
+    allow_smem(k_wlp_mm1_pipe<kDivIeee, 32>, kMm1Pipe2Smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, k_wlp_mm1_pipe<kDivIeee, 32>, kMm1Block, kMm1Pipe2Smem);
+    nb = nb2 < nb ? nb2 : nb;  // one grid size serves both
     return nb < 1 ? 1 : nb;
 }
 

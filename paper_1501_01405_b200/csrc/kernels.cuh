@@ -11,7 +11,9 @@ namespace wlp {
 // How the mm1 kernels divide a log by a rate (models.hpp:67,75); all three give IEEE
 // e / rate bit for bit (kernels.cu scale()). kDivPow2: rate = 2^k, inv = 1/rate exactly;
 // kDivRcp: inv = RN(1/rate), rate in [2^-900, 2^900]; kDivIeee: anything else.
-enum : int { kDivIeee = 0, kDivPow2 = 1, kDivRcp = 2 };
+// kDivPow2One: lambda = 2^k and mu = 1 (the reference's default service rate): the
+// services' division is the identity, one FP64 operation fewer per client.
+enum : int { kDivIeee = 0, kDivPow2 = 1, kDivRcp = 2, kDivPow2One = 3 };
 
 // Replication-kernel arguments shared by every model/mapping.
 struct RepArgs {
@@ -173,8 +175,8 @@ cudaError_t launch_wlp(int model, const RepArgs& a, const uint32_t* lane_tab,
 cudaError_t launch_wlp_pipe(int model, const RepArgs& a, const PipeSched& s, const uint32_t* wrap_tab, int grid,
                             cudaStream_t st);
 int wlp_pipe_blocks_per_sm();
-// mm1 WLP as a warp pipeline: lane_units = ceil(clients / 32).
-cudaError_t launch_wlp_mm1_pipe(const RepArgs& a, int64_t lane_units, int grid, cudaStream_t st);
+// mm1 WLP as a warp pipeline on a rotating schedule (s.S = 32; G = 8 clients, a panel, or 1).
+cudaError_t launch_wlp_mm1_pipe(const RepArgs& a, const PipeSched& s, int grid, cudaStream_t st);
 int wlp_mm1_pipe_blocks_per_sm();
 // TLP: thread per replication, block = tlp_block, grid = ceil(count / tlp_block).
 cudaError_t launch_tlp(int model, const RepArgs& a, int tlp_block, cudaStream_t st);

@@ -571,11 +571,26 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
         const double per_warp = static_cast<double>(count) / static_cast<double>(warps);
         const bool pipe = !g_hw_counters && (g_wlp_variant == 2 || (g_wlp_variant == 0 && per_warp > 30.0));
         if (pipe) {
+            // its own occupancy (4 blocks of 8 warps), not the segment-chaining kernel's
             const int64_t cap = static_cast<int64_t>(c.sms) * c.mm1_pipe_bps;
-            grid_out = static_cast<int>(std::min<int64_t>(grid_out, cap));
+            grid_out = static_cast<int>(std::clamp<int64_t>((count + kMm1Block / 32 - 1) / (kMm1Block / 32), 1, cap));
+            a.grab = static_cast<int>(
+                std::clamp<int64_t>(count / (static_cast<int64_t>(grid_out) * (kMm1Block / 32) * 32), 1, 32));
             g_last_kernel = "k_wlp_mm1_pipe";
             WLP_TRY(mark_model_start(c, st));
-            WLP_CUDA(launch_wlp_mm1_pipe(a, (a.n + 31) / 32, grid_out, st));
+            // whole panels at every step (n % 8 == 0): S lanes per replication, 8 unless a
+            // lane's chunk is long at 32 (each step then interleaves more panels)
+            int S = g_pipe_lanes;
+            if (S == 0) S = a.n >= 32 * kMm1PanelT * 8 ? 32 : 8;
+            int G = kMm1PanelT;
+            if (a.n % kMm1PanelT != 0 || a.n < static_cast<int64_t>(S) * kMm1PanelT) {  // the ragged kernel
+                S = 32;
+                G = a.n >= 32 * kMm1PanelT ? kMm1PanelT : 1;
+            }
+            const int64_t P = 32 / S;
+            a.grab = static_cast<int>(P * std::clamp<int64_t>(a.grab / P, 1, 32));
+            const PipeSched ps = pipe_sched(a.n, G, S);
+            WLP_CUDA(launch_wlp_mm1_pipe(a, ps, grid_out, st));
         } else {
             g_last_kernel = "k_wlp_mm1";
             WLP_TRY(mark_model_start(c, st));

@@ -152,6 +152,29 @@ __global__ void k_imadhi(uint32_t* out, uint32_t seed) {
     if (s == 0x12345) out[0] = s;
 }
 
+// DFMA interleaved with R independent IMAD chains per DFMA (FMA pipe, full rate): if an
+// FP64 warp-instruction held the SMSP's dispatch for two cycles, R = 1 would reach 2
+// instructions per 3 cycles (2.67 warp-instr/clk/SM) instead of 1 per cycle (4.0).
+template <int R>
+__global__ void k_dfma_mix(double* out, double seed) {
+    double a[4];
+    uint32_t b[4 * R];
+    for (int i = 0; i < 4; ++i) a[i] = seed + threadIdx.x + i;
+    for (int i = 0; i < 4 * R; ++i) b[i] = threadIdx.x * 7 + i;
+    for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            a[i] = __fma_rn(a[i], 0.999999, 1e-300);
+#pragma unroll
+            for (int k = 0; k < R; ++k) asm volatile("mad.lo.u32 %0, %0, 8193, %1;" : "+r"(b[i * R + k]) : "r"(b[(i * R + k + 1) % (4 * R)]));
+        }
+    double s = 0;
+    for (int i = 0; i < 4; ++i) s += a[i];
+    uint32_t t = 0;
+    for (int i = 0; i < 4 * R; ++i) t ^= b[i];
+    if (s == 1.2345 || t == 12345u) out[0] = s + t;
+}
+
 __global__ void k_shfl(uint32_t* out, uint32_t seed) {  // SHFL.UP (the pipelines' hand-over)
     uint32_t a[8];
     for (int i = 0; i < 8; ++i) a[i] = seed + threadIdx.x * 8 + i;
@@ -219,6 +242,9 @@ int main() {
     report("DADD", time_it([&] { k_dadd<<<blocks, threads>>>(dd, 1.0); }), 8);
     report("DFMA", time_it([&] { k_dfma<<<blocks, threads>>>(dd, 1.0); }), 8);
     report("I2F.F64.U32 (chained)", time_it([&] { k_i2f64<false><<<blocks, threads>>>(dd, 1); }), 8);
+    report("DFMA + 1 IMAD (mixed)", time_it([&] { k_dfma_mix<1><<<blocks, threads>>>(dd, 1.0); }), 8);
+    report("DFMA + 2 IMAD (mixed)", time_it([&] { k_dfma_mix<2><<<blocks, threads>>>(dd, 1.0); }), 12);
+    report("DFMA + 3 IMAD (mixed)", time_it([&] { k_dfma_mix<3><<<blocks, threads>>>(dd, 1.0); }), 16);
     report("SHFL.UP", time_it([&] { k_shfl<<<blocks, threads>>>(du, 1); }), 8);
     report("I2F.F64.S32 (chained)", time_it([&] { k_i2f64<true><<<blocks, threads>>>(dd, 1); }), 8);
     // taus88: 4 streams x (16 SASS per draw) + acc add per draw
