@@ -146,6 +146,11 @@ int wlp_set_wlp_variant(int variant);
  * else 16 when n >= 1920, else 8). Outputs are identical. */
 int wlp_set_pipe_lanes(int lanes);
 
+/* Test hook (this thread): near-one list entries per panel of the mm1 warp pipeline, a
+ * power of two in [1, 128] (default 128). Small values force the rare overflow path (the
+ * panel is redrawn and every lane fixes its own near-one draws); outputs are identical. */
+int wlp_debug_set_near_cap(int cap);
+
 /* The same for the TLP (thread-level) mapping: 0 = automatic (default: one thread per
  * replication, the paper's comparison mapping); 1 = one thread per replication; 2 = walk
  * bitsliced, one thread per 32 replications, each state bit of the 32 streams in one

@@ -247,6 +247,7 @@ _SIGS = {
     "wlp_set_wlp_variant": (C.c_int, [C.c_int]),
     "wlp_set_tlp_variant": (C.c_int, [C.c_int]),
     "wlp_set_pipe_lanes": (C.c_int, [C.c_int]),
+    "wlp_debug_set_near_cap": (C.c_int, [C.c_int]),
     "wlp_last_kernel": (C.c_char_p, []),
     "wlp_validate_params": (C.c_int, [C.c_int, C.POINTER(_Params), C.c_char_p, C.c_int]),
     "wlp_plan_launch": (C.c_int, [_I64, C.c_int, C.c_int, _I64, C.POINTER(_Cfg), C.c_char_p, C.c_int]),
@@ -633,6 +634,21 @@ class pipe_lanes:
 
     def __exit__(self, *exc):
         _check(_lib.wlp_set_pipe_lanes(0))
+
+
+class near_cap:
+    """Test hook: near-one list capacity of the mm1 warp pipeline (power of two <= 128) for
+    calls on this thread (wlp_debug_set_near_cap); small values exercise the overflow redo."""
+
+    def __init__(self, cap: int):
+        self.cap = int(cap)
+
+    def __enter__(self):
+        _check(_lib.wlp_debug_set_near_cap(self.cap))
+        return self
+
+    def __exit__(self, *exc):
+        _check(_lib.wlp_debug_set_near_cap(128))
 
 
 def last_kernel() -> str:

@@ -1876,28 +1876,28 @@ constexpr size_t kMm1Pipe2Smem = 256 * 8 + (kMm1Block / 32) * sizeof(Mm1Pan);
 // overflow, the index wraps, and fix_near redoes such a panel).
 template <int DIV>
 __device__ __forceinline__ void fill_client(Taus& st, int c, int lane, bool on, double lambda, double mu, double inv_l,
-                                            double inv_m, const double* tab, Mm1Pan& W) {
+                                            double inv_m, const double* tab, Mm1Pan& W, uint32_t cap) {
     uint32_t x, y;
     taus_next2(st, x, y);
     const double a = scale<DIV>(neg_log1m_table_dev(x, tab), lambda, inv_l);
     const double sv = scale_mu<DIV>(neg_log1m_table_dev(y, tab), mu, inv_m);
     W.v[c][lane] = make_double2(a, sv);
     const uint32_t slot = static_cast<uint32_t>(pan_slot(2 * c, lane));
-    if (on && x <= kNearMax) W.nl[atomicAdd(&W.cnt, 1u) & (kNearCap2 - 1)] = make_uint2(x, slot);
-    if (on && y <= kNearMax) W.nl[atomicAdd(&W.cnt, 1u) & (kNearCap2 - 1)] = make_uint2(y, slot + 1);
+    if (on && x <= kNearMax) W.nl[atomicAdd(&W.cnt, 1u) & (cap - 1)] = make_uint2(x, slot);
+    if (on && y <= kNearMax) W.nl[atomicAdd(&W.cnt, 1u) & (cap - 1)] = make_uint2(y, slot + 1);
 }
 
 // The listed near-ones of the panel just filled, into their slots; on overflow every lane
 // redraws its panel from the saved state and fixes its own near-ones.
 template <int DIV>
 __device__ __forceinline__ void fix_near(Mm1Pan& W, int lane, bool on, double lambda, double mu, double inv_l,
-                                         double inv_m) {
+                                         double inv_m, uint32_t cap) {
     __syncwarp();
     const uint32_t total = W.cnt;
     __syncwarp();
     if (lane == 0) W.cnt = 0;
     double* v = reinterpret_cast<double*>(&W.v[0][0]);
-    if (total <= kNearCap2) {
+    if (total <= cap) {
         for (uint32_t k = lane; k < total; k += 32) {
             const uint2 it = W.nl[k];
             const double e = it.x == 0u ? -0.0 : -log_near_one_dev(one_minus_u32_dev(it.x));
@@ -1918,28 +1918,28 @@ __device__ __forceinline__ void fix_near(Mm1Pan& W, int lane, bool on, double la
 
 template <int DIV>
 __device__ __forceinline__ void fill_panel(Taus& st, int lane, bool on, double lambda, double mu, double inv_l,
-                                           double inv_m, const double* tab, Mm1Pan& W) {
+                                           double inv_m, const double* tab, Mm1Pan& W, uint32_t cap) {
     W.save[lane] = st;
 #pragma unroll
-    for (int c = 0; c < kPanT; ++c) fill_client<DIV>(st, c, lane, on, lambda, mu, inv_l, inv_m, tab, W);
-    fix_near<DIV>(W, lane, on, lambda, mu, inv_l, inv_m);
+    for (int c = 0; c < kPanT; ++c) fill_client<DIV>(st, c, lane, on, lambda, mu, inv_l, inv_m, tab, W, cap);
+    fix_near<DIV>(W, lane, on, lambda, mu, inv_l, inv_m, cap);
 }
 
 // One pipeline step of a lane: np panels of its chunk (np >= 1, warp-uniform). Panel p's
 // recursion runs client by client interleaved with the fill of panel p + 1.
 template <int DIV>
 __device__ __forceinline__ void mm1_chunk(Taus& st, Queue& q, int np, int lane, bool on, double lambda, double mu,
-                                          double inv_l, double inv_m, const double* tab, Mm1Pan& W) {
-    fill_panel<DIV>(st, lane, on, lambda, mu, inv_l, inv_m, tab, W);
+                                          double inv_l, double inv_m, const double* tab, Mm1Pan& W, uint32_t cap) {
+    fill_panel<DIV>(st, lane, on, lambda, mu, inv_l, inv_m, tab, W, cap);
     for (int p = 1; p < np; ++p) {
         W.save[lane] = st;
 #pragma unroll
         for (int c = 0; c < kPanT; ++c) {
             const double2 v = W.v[c][lane];  // panel p-1's client c, then its slot is refilled
             q.client(v.x, v.y);
-            fill_client<DIV>(st, c, lane, on, lambda, mu, inv_l, inv_m, tab, W);
+            fill_client<DIV>(st, c, lane, on, lambda, mu, inv_l, inv_m, tab, W, cap);
         }
-        fix_near<DIV>(W, lane, on, lambda, mu, inv_l, inv_m);
+        fix_near<DIV>(W, lane, on, lambda, mu, inv_l, inv_m, cap);
     }
 #pragma unroll
     for (int c = 0; c < kPanT; ++c) {
@@ -1987,7 +1987,7 @@ __global__ void __launch_bounds__(kMm1Block, WLP_MM1_MINB) k_wlp_mm1_pipe(RepArg
         if (!more && !__any_sync(kFull, rep >= 0)) break;
         const int np = pipe_units(ps, phase) / kPanT;
         if (np > 0)
-            mm1_chunk<DIV>(st, q, np, lane, rep >= 0, a.lambda, a.mu, a.inv_lambda, a.inv_mu, logtab, W);
+            mm1_chunk<DIV>(st, q, np, lane, rep >= 0, a.lambda, a.mu, a.inv_lambda, a.inv_mu, logtab, W, a.near_cap);
         if (pos == S - 1 && rep >= 0) {  // the pipeline's last lane finished a replication
             a.out0[rep] = __ddiv_rn(q.idle, nd);
             a.out1[rep] = __ddiv_rn(q.sumw, nd);

@@ -39,6 +39,9 @@ struct RepArgs {
     // mm1 WLP with segment chaining: replications with lambda >= serial_rho * mu run the
     // heavy-traffic ordered loop on lane 0 instead (0.75 by default, runtime.cu)
     double serial_rho = 2.0;
+    // mm1 pipeline: near-one list entries used per panel (a power of two <= the 128 the
+    // shared memory holds; smaller only as a test hook, to exercise the overflow redo)
+    uint32_t near_cap = 128;
 };
 
 // Per-warp instrumentation tally (identical in every lane; the leader flushes it), and the

@@ -36,6 +36,7 @@ thread_local bool g_hw_counters = false;  // wlp_set_hw_counters
 thread_local int g_wlp_variant = 0;       // wlp_set_wlp_variant: 0 auto, 1 lane jumps, 2 pipeline
 thread_local const char* g_last_kernel = "";  // wlp_last_kernel
 thread_local int g_pipe_lanes = 0;       // wlp_set_pipe_lanes: 0 auto, else 8 / 16 / 32
+thread_local uint32_t g_near_cap = 128;  // wlp_debug_set_near_cap (test hook)
 thread_local int g_tlp_variant = 0;       // wlp_set_tlp_variant: 0 auto, 1 per replication, 2 bitsliced walk
 thread_local int g_stats_order = 0;       // wlp_set_stats_order: 0 accurate (double-double), 1 reference
 
@@ -532,6 +533,7 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
     a.out1 = o1;
     a.out2 = o2;
     a.serial_rho = mm1_serial_rho();
+    a.near_cap = g_near_cap;
     if (g_hw_counters) {
         WLP_CUDA(cudaMemsetAsync(c.hw.p, 0, kHwClk * sizeof(unsigned long long), st));
         WLP_CUDA(cudaMemsetAsync(c.hw.p + kHwClk, 0xFF, kHwMaxSms * sizeof(unsigned long long), st));  // starts: min
@@ -789,6 +791,13 @@ int wlp_set_wlp_variant(int variant) {
 }
 
 const char* wlp_last_kernel(void) { return g_last_kernel; }
+
+int wlp_debug_set_near_cap(int cap) {
+    if (cap < 1 || cap > 128 || (cap & (cap - 1)) != 0)
+        return fail(WLP_EDOMAIN, "near-one list capacity must be a power of two in [1, 128]");
+    g_near_cap = static_cast<uint32_t>(cap);
+    return WLP_OK;
+}
 
 int wlp_set_pipe_lanes(int lanes) {
     if (lanes != 0 && lanes != 8 && lanes != 16 && lanes != 32)

@@ -58,7 +58,11 @@ def test_kernel_variant_knobs_and_last_kernel():
         with pytest.raises(w.DomainError):
             with w.pipe_lanes(bad):
                 pass
-    with w.wlp_variant(4), w.tlp_variant(2), w.pipe_lanes(8):
+    for bad in (0, 3, 256):
+        with pytest.raises(w.DomainError):
+            with w.near_cap(bad):
+                pass
+    with w.wlp_variant(4), w.tlp_variant(2), w.pipe_lanes(8), w.near_cap(16):
         pass
     assert isinstance(w.last_kernel(), str)
 

@@ -359,6 +359,35 @@ def test_wlp_lane_jump_and_pipeline_kernels_agree_with_oracle(gpu, port, variant
         assert np.array_equal(run.outputs[name], want[name]), name
 
 
+@pytest.mark.parametrize("cap", [1, 4, 16, 32, 128])
+@pytest.mark.parametrize("lanes", [8, 32])
+def test_mm1_pipeline_near_list_overflow_redo(gpu, port, cap, lanes):
+    # the single-pass mm1 pipeline lists a panel's near-one draws (~32 of 512) with a
+    # shared-memory atomic; more than `cap` entries (never at the real cap of 128 with
+    # random draws) redo the panel from the saved stream state: force it with small caps
+    p = gpu.ModelParams(replications=3000, clients=1024, lambda_=0.5, mu=1.0)
+    want = port.run_model(1, oracle.params_from(p), 555)
+    with gpu.wlp_variant(2), gpu.pipe_lanes(lanes), gpu.near_cap(cap):
+        run = gpu.run_model(gpu.ModelKind.Mm1, p, gpu.ExecutionMode.Wlp, master_seed=555)
+    assert gpu.last_kernel() == "k_wlp_mm1_pipe"
+    for name in oracle.OUTPUTS[1]:
+        assert np.array_equal(run.outputs[name], want[name]), name
+
+
+@pytest.mark.parametrize("lanes", [8, 16, 32])
+@pytest.mark.parametrize("lam,mu,n", [(0.5, 1.0, 1000), (0.3, 0.9, 512), (0.9, 1.0, 2048), (1.7, 1.0, 64),
+                                      (0.4, 0.4, 800), (0.1, 1e-3, 96)])
+def test_mm1_pipeline_lanes_and_division_modes(gpu, port, lanes, lam, mu, n):
+    # S = 8 / 16 / 32 lanes per replication, rotating whole-panel chunks, the interleaved
+    # recursion, every division mode (mu = 1 services skip the division)
+    p = gpu.ModelParams(replications=2500, clients=n, lambda_=lam, mu=mu)
+    want = port.run_model(1, oracle.params_from(p), 8080 + n)
+    with gpu.wlp_variant(2), gpu.pipe_lanes(lanes):
+        run = gpu.run_model(gpu.ModelKind.Mm1, p, gpu.ExecutionMode.Wlp, master_seed=8080 + n)
+    for name in oracle.OUTPUTS[1]:
+        assert np.array_equal(run.outputs[name], want[name]), name
+
+
 @pytest.mark.parametrize("model", [0, 2])
 @pytest.mark.parametrize("R,n", [(992, 1), (1000, 5), (2500, 257), (2500, 999), (3001, 1000), (1500, 10_000),
                                  (4000, 63), (993, 2049)])
