@@ -1306,7 +1306,7 @@ __global__ void __launch_bounds__(kBsBlock) k_bs_seeds(RepArgs a, int64_t groups
 // A lane's chunk of its group: `blocks` 16-step carry-save blocks for every lane of the
 // warp alike (no lane runs a tail the others wait for); steps past the lane's `units`
 // do not count. Only a group's last chunk is partial (the lane chunk is a multiple of
-// 16), and the state it ends with is never used.
+// 16), and the state it ends with is never used. (The bitsliced lane-chunk kernel.)
 __device__ __forceinline__ void bs_walk_units(BsTaus& t, BsCount& P, BsCount& Q, uint32_t units, uint32_t blocks) {
     for (uint32_t b = 0; b < blocks; ++b) {
         const int valid = static_cast<int>(units > 16 * b ? (units - 16 * b < 16 ? units - 16 * b : 16) : 0);
@@ -1320,9 +1320,48 @@ __device__ __forceinline__ void bs_walk_units(BsTaus& t, BsCount& P, BsCount& Q,
     }
 }
 
+// Adds mask m at weight 2^W0 (a carry out of the carry-save tree's digit W0 - 1).
+template <int W0>
+__device__ __forceinline__ void bs_ripple_from(BsCount& k, uint32_t m) {
+#pragma unroll
+    for (int w = W0; w < 16; ++w) {
+        const uint32_t carry = k.c[w] & m;
+        k.c[w] ^= m;
+        m = carry;
+    }
+}
+
+// Exactly `units` walk steps of the 32 streams (the state ends exactly there): 16-step
+// blocks, an 8-step sub-tree whose carry ripples in at weight 8, then single steps. The
+// counters stay exact binary counts.
+__device__ __forceinline__ void bs_walk_exact(BsTaus& t, BsCount& P, BsCount& Q, uint32_t units) {
+    for (uint32_t b = units >> 4; b; --b) {
+        uint32_t pa, qa, pb, qb, p16, q16;
+        bs_oct<false>(t, P, Q, pa, qa, 0, 16);
+        bs_oct<false>(t, P, Q, pb, qb, 8, 16);
+        bs_csa(p16, P.c[3], P.c[3], pa, pb);
+        bs_csa(q16, Q.c[3], Q.c[3], qa, qb);
+        bs_ripple16(P, p16);
+        bs_ripple16(Q, q16);
+    }
+    if (units & 8) {
+        uint32_t p8, q8;
+        bs_oct<false>(t, P, Q, p8, q8, 0, 16);
+        bs_ripple_from<3>(P, p8);
+        bs_ripple_from<3>(Q, q8);
+    }
+    for (uint32_t r = units & 7; r; --r) {  // (one copy of the step: the code stays in the I-cache)
+        uint32_t pl, mi;
+        bs_walk_step(t, pl, mi);
+        bs_count_add1(P, pl);
+        bs_count_add1(Q, mi);
+    }
+}
+
 struct BsPipeWarp {
-    uint32_t cnt[32][33];  // finished groups: P digits 0..15, Q digits 16..31 (+1 pad)
+    uint32_t cnt[32][33];   // finished groups: P digits 0..15, Q digits 16..31 (+1 pad)
     long long grp[32];
+    uint32_t late[32][33];  // wrap groups' late-chunk counters, by wrap index k (P 0..15, Q 16..31)
     __align__(16) uint32_t seed[2][kBsLive];  // next groups' bit planes, fetched a step ahead
 };
 
@@ -1336,16 +1375,57 @@ __device__ __forceinline__ void bs_prefetch(uint32_t* dst, const uint32_t* src, 
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-// 6 blocks (12 warps) per SM: more warps hide the XOR chains' latency better than the
-// longer drain costs (4 blocks: 1.374 ms, 6: 1.348 ms at config 4; a few spilled bytes)
+// Per-stream dx of 32 streams from bitsliced counters (d[0..15] the +x digits P, d[16..31]
+// the -x digits Q) plus, optionally, a second pair of counters d2 (the late chunks of a
+// wrap group), written to out[0..31] (shared memory; out may alias d2, which is read
+// first).
+__device__ __forceinline__ void bs_dx_store(const uint32_t (&d)[32], const uint32_t* d2, int32_t* out) {
+    uint32_t pv[32], qv[32];
+#pragma unroll
+    for (int w = 0; w < 32; ++w) {
+        pv[w] = w < 16 ? d[w] : 0u;
+        qv[w] = w < 16 ? d[16 + w] : 0u;
+    }
+    transpose32(pv);
+    transpose32(qv);
+    int32_t dx[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) dx[j] = static_cast<int32_t>(pv[j]) - static_cast<int32_t>(qv[j]);
+    if (d2) {
+#pragma unroll
+        for (int w = 0; w < 32; ++w) {
+            pv[w] = w < 16 ? d2[w] : 0u;
+            qv[w] = w < 16 ? d2[16 + w] : 0u;
+        }
+        transpose32(pv);
+        transpose32(qv);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) dx[j] += static_cast<int32_t>(pv[j]) - static_cast<int32_t>(qv[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) out[j] = dx[j];
+}
+
+// Walk WLP, bitsliced warp pipeline on the rotating schedule (PipeSched, S = 32: L(t)
+// steps per lane per pipeline step, any 32 consecutive L summing to n, chunk lengths not
+// tied to 16-step blocks: bs_walk_exact advances the planes exactly) with the wrap of
+// k_wlp_pipe: warp w owns groups [31w, 31w + 31) besides the ones it grabs; at step 0
+// lane l >= 1 starts wrap group l at its chunk l (its 32 seeds jumped by a lane table and
+// transposed into planes), and after the grabbed groups lane 0 is fed wrap groups 31..1,
+// whose early chunks end at the warp's last step; each wrap group's dx is the sum of its
+// early and late counters. (WRAP = false: a straight pipeline, for runs too small to give
+// every warp its wrap groups.)
+template <bool WRAP>
 __global__ void __launch_bounds__(kBsPipeBlock, 6) k_wlp_walk_bs_pipe(RepArgs a, const uint32_t* __restrict__ bseeds,
-                                                                    int64_t groups, int64_t K) {
-    __shared__ BsPipeWarp sh[kBsPipeBlock / 32];
+                                                                    int64_t groups, PipeSched ps,
+                                                                    const uint32_t* __restrict__ wtab) {
+    constexpr int kW = kBsPipeBlock / 32;
+    __shared__ BsPipeWarp sh[kW];
     BsPipeWarp& E = sh[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
-    int64_t mine = a.n - static_cast<int64_t>(lane) * K;
-    mine = mine < 0 ? 0 : (mine > K ? K : mine);
-    const uint32_t units = static_cast<uint32_t>(mine);
+    const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * kW + (threadIdx.x >> 5);
+    const int64_t wrap0 = gwarp * kWrap;  // wrap group k is wrap0 + k - 1
+    const int64_t pool0 = WRAP ? static_cast<int64_t>(gridDim.x) * kW * kWrap : 0;
     RepArgs ga = a;  // the grab scheduler hands out groups
     ga.count = groups;
     BsTaus t;
@@ -1354,25 +1434,58 @@ __global__ void __launch_bounds__(kBsPipeBlock, 6) k_wlp_walk_bs_pipe(RepArgs a,
     for (int i = 0; i < 32; ++i) t.b1[i] = t.b2[i] = t.b3[i] = 0u;
     bs_count_init(P);
     bs_count_init(Q);
+    // item codes: g >= 0 a grabbed group, -1 idle, -1-k the late chunks of wrap group k,
+    // -33-k its early chunks
     long long grp = -1;
+    int left = 0;
+    if (WRAP) {  // lane l >= 1: wrap group l's 32 seeds jumped to chunk l, as bit planes
+        // one component at a time through the lane's row of the (still unused) result
+        // buffer, in loops that are not unrolled: the prologue stays small
+        const int64_t r0 = (wrap0 + lane - 1) * 32;
+        uint32_t* row = E.cnt[lane];
+        const uint32_t fill[3] = {kMin1, kMin2, kMin3};
+#pragma unroll 1
+        for (int comp = 0; comp < 3; ++comp) {
+            if (lane > 0) {
+                const uint32_t* tab = wtab + comp * 4096 + lane;
+#pragma unroll 1
+                for (int j = 0; j < 32; ++j) {
+                    const int64_t r = r0 + j;
+                    row[j] = nib_apply_g32(tab, r < a.count ? __ldg(a.seeds + comp * a.count + r) : fill[comp]);
+                }
+            }
+            __syncwarp();
+            uint32_t w[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) w[j] = row[j];
+            transpose32(w);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                if (comp == 0) t.b1[i] = w[i];
+                if (comp == 1) t.b2[i] = w[i];
+                if (comp == 2) t.b3[i] = w[i];
+            }
+            __syncwarp();
+        }
+        if (lane > 0) {
+            grp = -1 - lane;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) t.b1[i] = t.b2[i] = t.b3[i] = 0u;
+        }
+    }
     int64_t cur = 0, cend = 0;
     bool more = true;
-    int nemit = 0;
+    int wraps = kWrap, nemit = 0, phase = 0;
     auto flush = [&](int cnt) {
         __syncwarp();
         if (lane < cnt) {
             const long long g = E.grp[lane];
-            uint32_t pv[32], qv[32];
+            uint32_t d[32];
 #pragma unroll
-            for (int w = 0; w < 32; ++w) {
-                pv[w] = w < 16 ? E.cnt[lane][w] : 0u;
-                qv[w] = w < 16 ? E.cnt[lane][16 + w] : 0u;
-            }
-            transpose32(pv);
-            transpose32(qv);
+            for (int w = 0; w < 32; ++w) d[w] = E.cnt[lane][w];
             int32_t* dx = reinterpret_cast<int32_t*>(E.cnt[lane]);  // the slot's own row
-#pragma unroll
-            for (int j = 0; j < 32; ++j) dx[j] = static_cast<int32_t>(pv[j]) - static_cast<int32_t>(qv[j]);
+            bs_dx_store(d, nullptr, dx);
             for (int j = 0; j < 32; ++j) {  // not unrolled: one copy of fmod's code
                 const int64_t r = g * 32 + j;
                 if (r < a.count) a.out0[r] = walk_fold(dx[j], a.chunks);
@@ -1380,9 +1493,11 @@ __global__ void __launch_bounds__(kBsPipeBlock, 6) k_wlp_walk_bs_pipe(RepArgs a,
         }
         __syncwarp();
     };
-    auto next_group = [&]() -> long long {  // warp-uniform
+    // the item lane 0 takes next, decided a step ahead so its planes can be prefetched:
+    // a grabbed group, then (WRAP) the early chunks of wrap groups 31..1, then idle
+    auto next_item = [&](long long& code, int64_t& gidx) {  // warp-uniform
         if (more && cur >= cend) {
-            const int64_t base = grab_take(grab_issue(ga, lane));
+            const int64_t base = pool0 + grab_take(grab_issue(ga, lane));
             if (base >= groups) {
                 more = false;
             } else {
@@ -1390,17 +1505,28 @@ __global__ void __launch_bounds__(kBsPipeBlock, 6) k_wlp_walk_bs_pipe(RepArgs a,
                 cend = base + a.grab < groups ? base + a.grab : groups;
             }
         }
-        return more ? cur++ : -1;
+        if (more) {
+            code = gidx = cur++;
+        } else if (WRAP && wraps > 0) {
+            code = -33 - wraps;
+            gidx = wrap0 + wraps - 1;
+            --wraps;
+        } else {
+            code = gidx = -1;
+        }
     };
-    long long feed = next_group();
+    long long feed;
+    int64_t fidx;
+    next_item(feed, fidx);
     int buf = 0;
-    if (feed >= 0) bs_prefetch(E.seed[buf], bseeds + feed * kBsLive, lane);
+    if (fidx >= 0) bs_prefetch(E.seed[buf], bseeds + fidx * kBsLive, lane);
     for (;;) {
         asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
-        if (lane == 0) {  // feed the group fetched last step
+        const bool last = WRAP && feed == -34;  // lane 0 takes wrap group 1: the warp's last step
+        if (lane == 0) {  // feed the item fetched last step
             grp = feed;
-            if (feed >= 0) {
+            if (fidx >= 0) {
                 const uint4* src = reinterpret_cast<const uint4*>(E.seed[buf]);
                 uint32_t w[kBsLive];
 #pragma unroll
@@ -1419,15 +1545,26 @@ __global__ void __launch_bounds__(kBsPipeBlock, 6) k_wlp_walk_bs_pipe(RepArgs a,
                 for (int i = 4; i < 32; ++i) t.b3[i] = w[60 + i - 4];
                 bs_count_init(P);
                 bs_count_init(Q);
+                if (WRAP && feed < -1) left = static_cast<int>(pipe_wrap_units(ps, static_cast<int>(-33 - feed)));
             }
         }
         __syncwarp();
-        feed = next_group();
-        buf ^= 1;
-        if (feed >= 0) bs_prefetch(E.seed[buf], bseeds + feed * kBsLive, lane);
-        if (!__any_sync(kFull, grp >= 0)) break;
-        if (grp >= 0) bs_walk_units(t, P, Q, units, static_cast<uint32_t>(K / 16));
-        if (__shfl_sync(kFull, grp, 31) >= 0) {  // lane 31 finished a group
+        if (!last) {
+            next_item(feed, fidx);
+            buf ^= 1;
+            if (fidx >= 0) bs_prefetch(E.seed[buf], bseeds + fidx * kBsLive, lane);
+        }
+        if (!WRAP && !__any_sync(kFull, grp != -1)) break;
+        uint32_t units = static_cast<uint32_t>(pipe_units(ps, phase));
+        if (WRAP && grp <= -34) {  // early chunk `lane` of wrap group k: stop exactly at its late part
+            const int k = static_cast<int>(-33 - grp);
+            const int u = lane == k - 1 ? left : (left < static_cast<int>(units) ? left : static_cast<int>(units));
+            left -= u;
+            units = static_cast<uint32_t>(u);
+        }
+        if (grp != -1) bs_walk_exact(t, P, Q, units);
+        const long long g31 = __shfl_sync(kFull, grp, 31);
+        if (g31 >= 0) {  // lane 31 finished a group
             if (lane == 31) {
 #pragma unroll
                 for (int w = 0; w < 16; ++w) {
@@ -1440,7 +1577,15 @@ __global__ void __launch_bounds__(kBsPipeBlock, 6) k_wlp_walk_bs_pipe(RepArgs a,
                 flush(32);
                 nemit = 0;
             }
+        } else if (WRAP && g31 < -1 && lane == 31) {  // the late chunks of wrap group -1-g31
+            const int k = static_cast<int>(-1 - g31);
+#pragma unroll
+            for (int w = 0; w < 16; ++w) {
+                E.late[k][w] = P.c[w];
+                E.late[k][16 + w] = Q.c[w];
+            }
         }
+        if (last) break;  // lanes 0..30 hold the early chunks of wrap groups 1..31
 #pragma unroll
         for (int i = 1; i < 32; ++i) t.b1[i] = __shfl_up_sync(kFull, t.b1[i], 1);
 #pragma unroll
@@ -1453,8 +1598,28 @@ __global__ void __launch_bounds__(kBsPipeBlock, 6) k_wlp_walk_bs_pipe(RepArgs a,
             Q.c[w] = __shfl_up_sync(kFull, Q.c[w], 1);
         }
         grp = __shfl_up_sync(kFull, grp, 1);
+        if (WRAP) left = __shfl_up_sync(kFull, left, 1);
+        phase = (phase + 1) & 31;
     }
     flush(nemit);
+    if (WRAP) {  // the wrap groups: early counters (registers) + late counters (shared)
+        __syncwarp();
+        if (lane < kWrap) {
+            uint32_t d[32];
+#pragma unroll
+            for (int w = 0; w < 16; ++w) {
+                d[w] = P.c[w];
+                d[16 + w] = Q.c[w];
+            }
+            int32_t* dx = reinterpret_cast<int32_t*>(E.late[lane + 1]);
+            bs_dx_store(d, E.late[lane + 1], dx);
+            const int64_t g = wrap0 + lane;
+            for (int j = 0; j < 32; ++j) {
+                const int64_t r = g * 32 + j;
+                if (r < a.count) a.out0[r] = walk_fold(dx[j], a.chunks);
+            }
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------------
@@ -2555,13 +2720,16 @@ cudaError_t launch_tlp_walk_bs(const RepArgs& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_wlp_walk_bs_pipe(const RepArgs& a, uint32_t* bseeds, int64_t K, int grid, cudaStream_t st,
-                                    bool planes_ready) {
+cudaError_t launch_wlp_walk_bs_pipe(const RepArgs& a, uint32_t* bseeds, const PipeSched& s, const uint32_t* wrap_tab,
+                                    int grid, cudaStream_t st, bool planes_ready) {
     if (a.count <= 0) return cudaSuccess;
     const int64_t groups = (a.count + 31) / 32;
     if (!planes_ready)  // else the seeding kernel wrote them (SeedArgs::planes)
         k_bs_seeds<<<static_cast<unsigned>((groups + kBsBlock - 1) / kBsBlock), kBsBlock, 0, st>>>(a, groups, bseeds);
-    k_wlp_walk_bs_pipe<<<grid, kBsPipeBlock, 0, st>>>(a, bseeds, groups, K);
+    if (wrap_tab)
+        k_wlp_walk_bs_pipe<true><<<grid, kBsPipeBlock, 0, st>>>(a, bseeds, groups, s, wrap_tab);
+    else
+        k_wlp_walk_bs_pipe<false><<<grid, kBsPipeBlock, 0, st>>>(a, bseeds, groups, s, wrap_tab);
     return cudaGetLastError();
 }
 
@@ -2575,7 +2743,7 @@ cudaError_t launch_wlp_walk_bs_lanes(const RepArgs& a, const uint32_t* lane_tab,
 
 int wlp_walk_bs_pipe_blocks_per_sm() {
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_walk_bs_pipe, kBsPipeBlock, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_walk_bs_pipe<true>, kBsPipeBlock, 0);
     return nb < 1 ? 1 : nb;
 }
 

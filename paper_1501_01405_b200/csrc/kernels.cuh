@@ -185,10 +185,12 @@ int wlp_mm1_pipe_blocks_per_sm();
 cudaError_t launch_tlp(int model, const RepArgs& a, int tlp_block, cudaStream_t st);
 // Walk, bitsliced thread per 32 replications (needs n < 2^31).
 cudaError_t launch_tlp_walk_bs(const RepArgs& a, cudaStream_t st);
-// Walk WLP, bitsliced warp pipeline (groups of 32 replications; n < 65536). bseeds:
-// scratch of 88 words per group; a.next zeroed, a.grab groups per grab.
-cudaError_t launch_wlp_walk_bs_pipe(const RepArgs& a, uint32_t* bseeds, int64_t K, int grid, cudaStream_t st,
-                                    bool planes_ready = false);
+// Walk WLP, bitsliced warp pipeline (groups of 32 replications; n < 65536) on the
+// rotating schedule s (S = 32). bseeds: scratch of 88 words per group; a.next zeroed,
+// a.grab groups per grab. wrap_tab: lane tables of 2 * pipe_wrap_units(s, lane) draws
+// (null: no wrap; with it groups >= kWrap * warps).
+cudaError_t launch_wlp_walk_bs_pipe(const RepArgs& a, uint32_t* bseeds, const PipeSched& s, const uint32_t* wrap_tab,
+                                    int grid, cudaStream_t st, bool planes_ready = false);
 int wlp_walk_bs_pipe_blocks_per_sm();
 // Walk WLP, bitsliced lane chunks: a warp per group of 32 replications (K < 65536; lane
 // jump table of stride 2K draws; a.next zeroed, a.grab groups per grab).

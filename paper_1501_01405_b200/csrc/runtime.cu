@@ -611,20 +611,24 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
         WLP_TRY(mark_model_start(c, st));
         WLP_CUDA(launch_wlp_walk_bs_lanes(a, tab, K, grid_out, st));
     } else if (model == WLP_MODEL_WALK && !g_hw_counters && walk_bs_choice(c, count, a.n) == 3) {
-        // bitsliced pipeline: groups of 32 replications; at least ~64 groups per warp so
-        // the 31-step drain stays small (walk_bs_choice)
+        // bitsliced pipeline: groups of 32 replications, rotating schedule; each warp owns
+        // kWrap wrap groups (no fill or drain) when there are at least 2 * kWrap per warp
         const int64_t groups = (count + 31) / 32;
-        const int64_t warps_want = std::max<int64_t>(1, groups / 64);
         const int64_t cap = static_cast<int64_t>(c.sms) * c.bs_pipe_bps;
-        grid_out = static_cast<int>(std::clamp<int64_t>((warps_want + 1) / 2, 1, cap));
-        a.grab = static_cast<int>(std::clamp<int64_t>(groups / (2 * grid_out * 32), 1, 32));
-        // lane chunk: a multiple of 16 steps, so only a group's last chunk is partial
-        const int64_t K = ((a.n + 31) / 32 + 15) / 16 * 16;
+        constexpr int64_t kBsW = kBsPipeBlock / 32;
+        const int64_t blocks = std::clamp<int64_t>((std::max<int64_t>(1, groups / 64) + 1) / 2, 1, cap);
+        const bool wrap = groups >= kWrap * kBsW * blocks;
+        grid_out = static_cast<int>(blocks);
+        const int64_t pool = groups - (wrap ? kWrap * kBsW * blocks : 0);
+        a.grab = static_cast<int>(std::clamp<int64_t>(pool / (kBsW * blocks * 32), 1, 32));
+        const PipeSched ps = pipe_sched(a.n, a.n >= 512 ? 16 : 1);
+        const uint32_t* wtab = nullptr;
+        if (wrap) WLP_TRY(wrap_table(c, ps, wtab));
         g_last_kernel = "k_wlp_walk_bs_pipe";
         const bool ready = c.planes_of == d_seeds && c.planes_count == count;  // from the seeding
         if (!ready) WLP_CUDA(c.bseeds.ensure(groups * 88));
         WLP_TRY(mark_model_start(c, st));
-        WLP_CUDA(launch_wlp_walk_bs_pipe(a, c.bseeds.p, K, grid_out, st, ready));
+        WLP_CUDA(launch_wlp_walk_bs_pipe(a, c.bseeds.p, ps, wtab, grid_out, st, ready));
     } else {
         const int64_t K = (a.n + 31) / 32;
         // Lane jumps cost ~80 instructions per lane per replication against K units of
