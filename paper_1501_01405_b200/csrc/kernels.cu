@@ -37,6 +37,15 @@ namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
+// Programmatic dependent launch (sm_90+): a model kernel launched with the programmatic
+// stream-serialization attribute right after the seeding kernel may start while the
+// seeding drains; pdl_wait() (griddepcontrol.wait) then holds it until the seeding grid
+// has completed and its writes are visible. Each model kernel waits after its own
+// prologue (shared-memory table staging) and before its first read of the seeds or the
+// work counter; launched without the attribute, the wait is a no-op.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 
 // Nibble-table application from global memory (L1-resident tables): 8 independent loads
 // and an XOR tree.
@@ -65,6 +74,26 @@ __device__ Taus jump_pow(const uint32_t* __restrict__ pn, Taus t, uint64_t n) {
         t.s1 = nib_apply_g(m, t.s1);
         t.s2 = nib_apply_g(m + 128, t.s2);
         t.s3 = nib_apply_g(m + 256, t.s3);
+    }
+    return t;
+}
+
+// jump_pow with the binary-power tables staged in shared memory (k powers, k >= bits of n).
+__device__ Taus jump_pow_s(const uint32_t* pn, Taus t, uint64_t n) {
+    while (n) {
+        const int k = __ffsll(static_cast<long long>(n)) - 1;
+        n &= n - 1;
+        const uint32_t* m = pn + k * kUniTabWords;
+        uint32_t y1[8], y2[8], y3[8];
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+            y1[p] = m[p * 16 + ((t.s1 >> (4 * p)) & 15u)];
+            y2[p] = m[128 + p * 16 + ((t.s2 >> (4 * p)) & 15u)];
+            y3[p] = m[256 + p * 16 + ((t.s3 >> (4 * p)) & 15u)];
+        }
+        t.s1 = ((y1[0] ^ y1[1]) ^ (y1[2] ^ y1[3])) ^ ((y1[4] ^ y1[5]) ^ (y1[6] ^ y1[7]));
+        t.s2 = ((y2[0] ^ y2[1]) ^ (y2[2] ^ y2[3])) ^ ((y2[4] ^ y2[5]) ^ (y2[6] ^ y2[7]));
+        t.s3 = ((y3[0] ^ y3[1]) ^ (y3[2] ^ y3[3])) ^ ((y3[4] ^ y3[5]) ^ (y3[6] ^ y3[7]));
     }
     return t;
 }
@@ -386,13 +415,13 @@ struct Queue {
 // One block of stream slots of one random_spacing run: slots [blk*B, (blk+1)*B) of
 // `count` (B = kSeedBlock * PER), slot i = candidate c(slot_begin + i) after
 // the sorted rejection list; keys land SoA at out[plane*stride + out_off + i].
-template <int PER>
+template <int PER, bool STAGED = false>
 __device__ __forceinline__ void seed_block(const uint32_t* __restrict__ pw, Taus master, int64_t slot_begin,
                                            int64_t count, int64_t blk, const int64_t* __restrict__ rejected,
                                            int64_t n_rejected, uint32_t* __restrict__ out, int64_t out_off,
                                            int64_t stride, SpecialRec* specials, int64_t special_cap,
                                            unsigned long long* n_special, uint32_t job,
-                                           uint32_t* __restrict__ planes = nullptr) {
+                                           uint32_t* __restrict__ planes = nullptr, const uint32_t* spw = nullptr) {
     extern __shared__ uint32_t sh[];  // 3 x [kSeedBlock][PER + 1] (padded: conflict-free)
     constexpr int kRow = PER + 1;
     constexpr int kPlane = kSeedBlock * kRow;
@@ -408,7 +437,8 @@ __device__ __forceinline__ void seed_block(const uint32_t* __restrict__ pw, Taus
             ++c;
             ++ri;
         }
-        Taus m = jump_pow(pw, master, 3ull * static_cast<uint64_t>(c));
+        Taus m = STAGED ? jump_pow_s(spw, master, 3ull * static_cast<uint64_t>(c))
+                        : jump_pow(pw, master, 3ull * static_cast<uint64_t>(c));
         for (int j = 0; j < nmine; ++j) {
             Taus key;
             for (;;) {
@@ -467,9 +497,57 @@ __device__ __forceinline__ void seed_block(const uint32_t* __restrict__ pw, Taus
 
 template <int PER>
 __global__ void __launch_bounds__(kSeedBlock) k_seed(SeedArgs a) {
-    seed_block<PER>(a.powers, a.master, a.slot_begin, a.count, blockIdx.x, a.rejected, a.n_rejected, a.out, a.out_off,
-               a.stride ? a.stride : a.count,
-               static_cast<SpecialRec*>(a.specials), a.special_cap, a.n_special, 0u, a.planes);
+    pdl_wait();     // (launched early behind the previous run's kernels: they read what this writes)
+    pdl_trigger();  // the model kernel may launch now; it waits for this grid to complete
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (a.zero_a) *a.zero_a = 0ull;
+        if (a.zero_b) *a.zero_b = 0ull;
+    }
+    if constexpr (PER == 8) {
+        // small runs: a thread's jump is a chain of ~10 dependent table steps, each an L2
+        // round trip from global memory; staged in shared memory (the powers up to the
+        // run's largest candidate, 29 KB at R = 1e5), the chain runs at shared-memory latency.
+        // The copy is one TMA bulk transfer (cp.async.bulk, completion counted on an
+        // mbarrier): a plain load/store loop kept one L2 round trip per iteration in
+        // flight and cost ~10 us of this ~10 us kernel.
+        extern __shared__ __align__(16) uint32_t sh[];
+        __shared__ __align__(8) uint64_t bar;
+        uint32_t* spw = sh + 3 * kSeedBlock * (PER + 1);
+        const uint32_t bytes = static_cast<uint32_t>(a.stage_powers) * kUniTabWords * 4;
+        const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bar));
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             static_cast<uint32_t>(__cvta_generic_to_shared(spw))),
+                         "l"(a.powers), "r"(bytes), "r"(b)
+                         : "memory");
+        }
+        __syncthreads();  // (the barrier is initialised before anyone waits on it)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t@!p bra WAIT_%=;\n\t}" ::"r"(b)
+            : "memory");
+        seed_block<PER, true>(a.powers, a.master, a.slot_begin, a.count, blockIdx.x, a.rejected, a.n_rejected, a.out,
+                              a.out_off, a.stride ? a.stride : a.count, static_cast<SpecialRec*>(a.specials),
+                              a.special_cap, a.n_special, 0u, a.planes, spw);
+    } else {
+        seed_block<PER>(a.powers, a.master, a.slot_begin, a.count, blockIdx.x, a.rejected, a.n_rejected, a.out,
+                        a.out_off, a.stride ? a.stride : a.count, static_cast<SpecialRec*>(a.specials),
+                        a.special_cap, a.n_special, 0u, a.planes);
+    }
+    if (a.report) {  // the last block reports the specials count to the host
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(a.done, 1u) == gridDim.x - 1) {
+                __threadfence();
+                *reinterpret_cast<volatile unsigned long long*>(a.report) = atomicAdd(a.n_special, 0ull);
+                *a.done = 0u;
+            }
+        }
+    }
 }
 
 // Many independent runs (one per plan set) in one launch; block -> job by binary search.
@@ -546,6 +624,7 @@ __global__ void __launch_bounds__(kWlpBlock, 4) k_wlp_lanes(RepArgs a, const uin
     extern __shared__ uint32_t tab[];  // kLaneTabWords
     stage_u32<kLaneTabWords>(tab, gtab);
     __syncthreads();
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     HwTally hw;
     if (COUNT) {
@@ -644,6 +723,7 @@ template <int MODEL, bool WIDE, int S, bool WRAP>
 __global__ void __launch_bounds__(kWlpBlock, WLP_PIPE_MINB) k_wlp_pipe(RepArgs a, PipeSched ps,
                                                            const uint32_t* __restrict__ wtab) {
     static_assert(S == 32 || WRAP, "S < 32 pipelines always wrap");
+    pdl_wait();
     using I = typename std::conditional<WIDE, long long, int>::type;
     constexpr int kW = kWlpBlock / 32, P = 32 / S, kWr = S - 1;
     __shared__ I emit_rep[kW][32];
@@ -1004,6 +1084,7 @@ template <int DIV, bool COUNT>
 __global__ void __launch_bounds__(kMm1Block, 3) k_wlp_mm1(RepArgs a, const uint32_t* __restrict__ gtab,
                                                         const uint32_t* __restrict__ gskip) {
     const Mm1Smem m = mm1_stage(gtab, gskip);
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     // the `t < 0` decision is a per-lane select, never a warp branch; the warp splits in
     // the near-one loops of the exponential batches (counted there)
@@ -1116,6 +1197,7 @@ __device__ __forceinline__ double walk_rep_tlp_counted(Taus st, int64_t n, int64
 
 template <int MODEL, bool COUNT>
 __global__ void k_tlp(RepArgs a) {
+    pdl_wait();
     const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (r >= a.count) return;  // tail threads of the last block stay inert (wlp.cpp:125-138)
     const Taus st = load_seed(a, r);
@@ -1223,6 +1305,7 @@ __global__ void __launch_bounds__(kBsBlock) k_tlp_walk_bs(RepArgs a) {
     extern __shared__ int32_t bs_acc[];  // [kBsBlock][33] when n > 65520 steps
     const int64_t r0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 32;
     if (r0 >= a.count) return;
+    pdl_wait();
     // (direct loads: staging them through shared memory as k_bs_seeds does measured
     // 0.899 vs 0.884 ms here, where the seeds are read once per 1,000 steps)
     BsTaus t;
@@ -1293,6 +1376,7 @@ __global__ void __launch_bounds__(kBsBlock) k_tlp_walk_bs(RepArgs a) {
 
 __global__ void __launch_bounds__(kBsBlock) k_bs_seeds(RepArgs a, int64_t groups, uint32_t* __restrict__ out) {
     __shared__ uint32_t stage[kBsBlock * 33];
+    pdl_wait();
     const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     BsTaus t;
     const int64_t g0 = static_cast<int64_t>(blockIdx.x) * blockDim.x;
@@ -1422,6 +1506,7 @@ __global__ void __launch_bounds__(kBsPipeBlock, 6) k_wlp_walk_bs_pipe(RepArgs a,
     constexpr int kW = kBsPipeBlock / 32;
     __shared__ BsPipeWarp sh[kW];
     BsPipeWarp& E = sh[threadIdx.x >> 5];
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * kW + (threadIdx.x >> 5);
     const int64_t wrap0 = gwarp * kWrap;  // wrap group k is wrap0 + k - 1
@@ -1640,6 +1725,7 @@ __global__ void __launch_bounds__(kBsLanesBlock, 2) k_wlp_walk_bs_lanes(RepArgs 
     extern __shared__ uint32_t tab[];  // kLaneTabWords
     stage_u32<kLaneTabWords>(tab, gtab);
     __syncthreads();
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     int64_t mine = a.n - static_cast<int64_t>(lane) * K;
     mine = mine < 0 ? 0 : (mine > K ? K : mine);
@@ -1953,6 +2039,7 @@ __global__ void __launch_bounds__(kMm1Block, WLP_MM1_MINB) k_wlp_mm1_pipe_ragged
     PanelWarp& P = reinterpret_cast<PanelWarp*>(logtab + 256)[threadIdx.x >> 5];
     stage_log_table(logtab);
     __syncthreads();
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const double nd = static_cast<double>(a.n);
     Taus st{kMin1, kMin2, kMin3};
@@ -2122,6 +2209,7 @@ __global__ void __launch_bounds__(kMm1Block, WLP_MM1_MINB) k_wlp_mm1_pipe(RepArg
     stage_log_table(logtab);
     if ((threadIdx.x & 31) == 0) W.cnt = 0;
     __syncthreads();
+    pdl_wait();
     const int lane = threadIdx.x & 31, g = lane / S, pos = lane % S;
     const double nd = static_cast<double>(a.n);
     Taus st{kMin1, kMin2, kMin3};
@@ -2188,6 +2276,7 @@ __global__ void __launch_bounds__(SMALL ? 256 : 1024, SMALL ? WLP_TLP_MM1_MINB :
     PanelWarp& W = reinterpret_cast<PanelWarp*>(logtab + 256)[threadIdx.x >> 5];
     stage_log_table(logtab);
     __syncthreads();
+    pdl_wait();
     const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const bool live = r < a.count;
@@ -2475,7 +2564,29 @@ void allow_smem(K kernel, size_t bytes) {
     have = bytes;
 }
 
+// Launch with the programmatic stream-serialization attribute when t_pdl is set (the
+// runtime sets it for model launches that directly follow the seeding kernel and are not
+// bracketed by timing events): the kernel's prologue overlaps the seeding's tail.
+thread_local bool t_pdl = false;
+
+template <class... KP, class... Args>
+cudaError_t launch_ex(void (*kernel)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = t_pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KP>(args)...);
+}
+
 }  // namespace
+
+void set_pdl_launch(bool on) { t_pdl = on; }
 
 // ---------------------------------------------------------------------------------
 // launchers
@@ -2533,9 +2644,21 @@ template <int PER>
 cudaError_t launch_seed_per(const SeedArgs& a, cudaStream_t st) {
     const int64_t per_block = static_cast<int64_t>(kSeedBlock) * PER;
     const int64_t grid = (a.count + per_block - 1) / per_block;
-    const size_t smem = 3 * kSeedBlock * (PER + 1) * 4;
-    allow_smem(k_seed<PER>, smem);
-    k_seed<PER><<<static_cast<unsigned>(grid), kSeedBlock, smem, st>>>(a);
+    SeedArgs b = a;
+    size_t smem = 3 * kSeedBlock * (PER + 1) * 4;
+    if (PER == 8) {  // stage the binary powers up to the largest jump (3 x the last candidate)
+        const uint64_t last = 3ull * static_cast<uint64_t>(a.slot_begin + a.count + a.n_rejected);
+        b.stage_powers = 64 - __builtin_clzll(last | 1ull);
+        smem += static_cast<size_t>(b.stage_powers) * kUniTabWords * 4;
+    }
+    allow_smem(k_seed<PER>, 3 * kSeedBlock * (PER + 1) * 4 + 64 * kUniTabWords * 4);
+    // PDL: the seeding may launch while the previous run's kernels drain (it waits for them
+    // before touching memory), so the launch latency overlaps their tail
+    const bool prev = t_pdl;
+    t_pdl = true;
+    const cudaError_t e = launch_ex(k_seed<PER>, static_cast<unsigned>(grid), kSeedBlock, smem, st, b);
+    t_pdl = prev;
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
@@ -2577,13 +2700,13 @@ cudaError_t launch_wlp(int model, const RepArgs& a, const uint32_t* lane_tab, co
     if (a.count <= 0) return cudaSuccess;
     const bool count = a.hw != nullptr;
     if (model == 1) {
-        auto go = [&](auto kernel) { kernel<<<grid, kMm1Block, kMm1Smem, st>>>(a, lane_tab, uni_tab); };
+        auto go = [&](auto kernel) { launch_ex(kernel, grid, kMm1Block, kMm1Smem, st, a, lane_tab, uni_tab); };
         by_div(a.div, [&](auto d) {
             constexpr int D = decltype(d)::value;
             count ? go(k_wlp_mm1<D, true>) : go(k_wlp_mm1<D, false>);
         });
     } else {
-        auto go = [&](auto kernel) { kernel<<<grid, kWlpBlock, kLaneTabWords * 4, st>>>(a, lane_tab, lane_units); };
+        auto go = [&](auto kernel) { launch_ex(kernel, grid, kWlpBlock, kLaneTabWords * 4, st, a, lane_tab, lane_units); };
         if (model == 0)
             count ? go(k_wlp_lanes<0, true>) : go(k_wlp_lanes<0, false>);
         else
@@ -2594,7 +2717,7 @@ cudaError_t launch_wlp(int model, const RepArgs& a, const uint32_t* lane_tab, co
 
 template <int MODEL, bool WIDE>
 void launch_wlp_pipe_m(const RepArgs& a, const PipeSched& s, const uint32_t* wrap_tab, int grid, cudaStream_t st) {
-    auto go = [&](auto kernel) { kernel<<<grid, kWlpBlock, 0, st>>>(a, s, wrap_tab); };
+    auto go = [&](auto kernel) { launch_ex(kernel, grid, kWlpBlock, 0, st, a, s, wrap_tab); };
     if (s.S == 8)
         go(k_wlp_pipe<MODEL, WIDE, 8, true>);
     else if (s.S == 16)
@@ -2624,7 +2747,7 @@ cudaError_t launch_wlp_mm1_pipe(const RepArgs& a, const PipeSched& ps, int grid,
         const bool mu_one = a.div == kDivPow2 && a.mu == 1.0;
         auto go = [&](auto kernel) {
             allow_smem(kernel, kMm1Pipe2Smem);
-            kernel<<<grid, kMm1Block, kMm1Pipe2Smem, st>>>(a, ps);
+            launch_ex(kernel, grid, kMm1Block, kMm1Pipe2Smem, st, a, ps);
         };
         auto by_s = [&](auto d) {
             constexpr int D = decltype(d)::value;
@@ -2643,7 +2766,7 @@ cudaError_t launch_wlp_mm1_pipe(const RepArgs& a, const PipeSched& ps, int grid,
     }
     if (ps.S != 32) return cudaErrorInvalidValue;
     const bool exact = !(ps.G == kPanT && ps.tail == 0);  // some chunk ends inside a panel
-    auto go = [&](auto kernel) { kernel<<<grid, kMm1Block, kMm1PipeSmem, st>>>(a, ps); };
+    auto go = [&](auto kernel) { launch_ex(kernel, grid, kMm1Block, kMm1PipeSmem, st, a, ps); };
     by_div(a.div, [&](auto d) {
         constexpr int D = decltype(d)::value;
         exact ? go(k_wlp_mm1_pipe_ragged<D, true>) : go(k_wlp_mm1_pipe_ragged<D, false>);
@@ -2682,15 +2805,15 @@ cudaError_t launch_tlp(int model, const RepArgs& a, int tlp_block, cudaStream_t 
     switch (model) {
         case 0:
             if (count)
-                k_tlp<0, true><<<g, b, 0, st>>>(a);
+                launch_ex(k_tlp<0, true>, g, b, 0, st, a);
             else
-                k_tlp<0, false><<<g, b, 0, st>>>(a);
+                launch_ex(k_tlp<0, false>, g, b, 0, st, a);
             break;
         case 1: {
             const size_t smem = tlp_mm1_panel_smem(static_cast<int>(block));
             auto go = [&](auto kernel) {
                 allow_smem(kernel, smem);
-                kernel<<<g, b, smem, st>>>(a);
+                launch_ex(kernel, g, b, smem, st, a);
             };
             by_div(a.div, [&](auto d) {
                 constexpr int D = decltype(d)::value;
@@ -2703,9 +2826,9 @@ cudaError_t launch_tlp(int model, const RepArgs& a, int tlp_block, cudaStream_t 
         }
         default:
             if (count)
-                k_tlp<2, true><<<g, b, 0, st>>>(a);
+                launch_ex(k_tlp<2, true>, g, b, 0, st, a);
             else
-                k_tlp<2, false><<<g, b, 0, st>>>(a);
+                launch_ex(k_tlp<2, false>, g, b, 0, st, a);
             break;
     }
     return cudaGetLastError();
@@ -2716,7 +2839,7 @@ cudaError_t launch_tlp_walk_bs(const RepArgs& a, cudaStream_t st) {
     const int64_t threads = (a.count + 31) / 32;
     const int64_t grid = (threads + kBsBlock - 1) / kBsBlock;
     const size_t smem = a.n > kBsFlushBlocks * 16 ? kBsBlock * 33 * sizeof(int32_t) : 0;
-    k_tlp_walk_bs<<<static_cast<unsigned>(grid), kBsBlock, smem, st>>>(a);
+    launch_ex(k_tlp_walk_bs, static_cast<unsigned>(grid), kBsBlock, smem, st, a);
     return cudaGetLastError();
 }
 
@@ -2725,11 +2848,12 @@ cudaError_t launch_wlp_walk_bs_pipe(const RepArgs& a, uint32_t* bseeds, const Pi
     if (a.count <= 0) return cudaSuccess;
     const int64_t groups = (a.count + 31) / 32;
     if (!planes_ready)  // else the seeding kernel wrote them (SeedArgs::planes)
-        k_bs_seeds<<<static_cast<unsigned>((groups + kBsBlock - 1) / kBsBlock), kBsBlock, 0, st>>>(a, groups, bseeds);
+        launch_ex(k_bs_seeds, static_cast<unsigned>((groups + kBsBlock - 1) / kBsBlock), kBsBlock, 0, st, a, groups,
+                  bseeds);
     if (wrap_tab)
-        k_wlp_walk_bs_pipe<true><<<grid, kBsPipeBlock, 0, st>>>(a, bseeds, groups, s, wrap_tab);
+        launch_ex(k_wlp_walk_bs_pipe<true>, grid, kBsPipeBlock, 0, st, a, bseeds, groups, s, wrap_tab);
     else
-        k_wlp_walk_bs_pipe<false><<<grid, kBsPipeBlock, 0, st>>>(a, bseeds, groups, s, wrap_tab);
+        launch_ex(k_wlp_walk_bs_pipe<false>, grid, kBsPipeBlock, 0, st, a, bseeds, groups, s, wrap_tab);
     return cudaGetLastError();
 }
 
@@ -2737,7 +2861,7 @@ cudaError_t launch_wlp_walk_bs_lanes(const RepArgs& a, const uint32_t* lane_tab,
                                      cudaStream_t st) {
     if (a.count <= 0) return cudaSuccess;
     allow_smem(k_wlp_walk_bs_lanes, kLaneTabWords * 4);
-    k_wlp_walk_bs_lanes<<<grid, kBsLanesBlock, kLaneTabWords * 4, st>>>(a, lane_tab, K);
+    launch_ex(k_wlp_walk_bs_lanes, grid, kBsLanesBlock, kLaneTabWords * 4, st, a, lane_tab, K);
     return cudaGetLastError();
 }
 

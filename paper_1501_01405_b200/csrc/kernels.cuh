@@ -112,6 +112,16 @@ struct SeedArgs {
     // optional: the walk's bit planes of each group of 32 slots (88 live words per group,
     // the layout k_bs_seeds writes), so the bitsliced pipeline needs no separate pass
     uint32_t* planes = nullptr;
+    // optional words the seeding zeroes (block 0, before the model launch that follows):
+    // the next run's specials count and the model's work counter (no memset launches)
+    unsigned long long* zero_a = nullptr;
+    unsigned long long* zero_b = nullptr;
+    int stage_powers = 0;  // (set by launch_seed) binary powers staged in shared memory
+    // optional: the last block to finish stores the final specials count to `report`
+    // (mapped pinned host memory: the host reads it after a stream sync, no copy launch)
+    // and rearms `done` (a block counter, zero between launches)
+    unsigned int* done = nullptr;
+    unsigned long long* report = nullptr;
 };
 
 // Experimental plan (BASELINE config 5): many factor-level sets in one launch.
@@ -164,6 +174,9 @@ int wlp_blocks_per_sm(int model);
 int tlp_blocks_per_sm(int model, int block);
 
 cudaError_t launch_seed(const SeedArgs& a, cudaStream_t st);
+// Model launches on this thread use programmatic dependent launch (overlap with the
+// seeding kernel they follow) while set; off for launches bracketed by timing events.
+void set_pdl_launch(bool on);
 cudaError_t launch_neg_log1m(const uint32_t* k, int64_t n, double* out, cudaStream_t st);
 cudaError_t launch_taus_stream(const uint32_t* powers, Taus seed, int64_t n, uint32_t* out,
                                cudaStream_t st);

@@ -112,9 +112,20 @@ struct DevCtx {
     DevBuf<double> outs, partials, stats_in;
     DevBuf<SpecialRec> specials;
     DevBuf<unsigned long long> counter;  // [0] special candidates of the last seeding, [1] its grab counter
-    bool work_zeroed = false;            // counter[1] was cleared with counter[0] by seed_async
+    // counter[0], [1]: the specials counts of alternate seedings (each seeding zeroes the
+    // other for the next one, so no memset precedes it); [2]: the grab counter of the model
+    // launch behind a seeding (zeroed by that seeding); [3], [4]: the plan's specials count
+    // and grab counter (memset per plan)
+    int spec_slot = 0;                   // the next seeding counts its specials in counter[spec_slot]
+    int spec_read = 0;                   // the slot read_specials reads
+    bool work_zeroed = false;            // counter[2] was cleared by the seeding just launched
+    bool pdl_next = false;               // the next model launch directly follows a seeding kernel
     bool time_model = false;  // model_async records ev0 right before its launch
     unsigned long long* h_counter = nullptr;  // pinned host word for the specials count readback
+    unsigned long long* h_mapped = nullptr;   // mapped pinned word the seeding stores the count to
+    unsigned long long* d_mapped = nullptr;   // (its device alias)
+    bool spec_mapped = false;                 // the last seeding reports through h_mapped
+    DevBuf<unsigned int> seed_done;           // the seeding's finished-block counter
     unsigned char* h_stage = nullptr;         // pinned staging of small uploads (plan tables)
     size_t h_stage_cap = 0;
     DevBuf<unsigned char> plan_blob;          // the plan's SeedJob[] then SetParam[]
@@ -157,9 +168,14 @@ int ctx_init(DevCtx& c) {
         c.plan_bps[m] = plan_blocks_per_sm(m);
     }
     WLP_CUDA(c.specials.ensure(kSpecialCap));
-    WLP_CUDA(c.counter.ensure(2));
+    WLP_CUDA(c.counter.ensure(5));
+    WLP_CUDA(cudaMemset(c.counter.p, 0, 5 * sizeof(unsigned long long)));
     WLP_CUDA(c.work.ensure(1));
     WLP_CUDA(cudaMallocHost(&c.h_counter, sizeof(unsigned long long)));
+    WLP_CUDA(cudaHostAlloc(&c.h_mapped, sizeof(unsigned long long), cudaHostAllocMapped));
+    WLP_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c.d_mapped), c.h_mapped, 0));
+    WLP_CUDA(c.seed_done.ensure(1));
+    WLP_CUDA(cudaMemset(c.seed_done.p, 0, sizeof(unsigned int)));
     WLP_CUDA(c.hw.ensure(kHwWords));
     WLP_CUDA(cudaEventCreate(&c.ev0));
     WLP_CUDA(cudaEventCreate(&c.ev1));
@@ -432,8 +448,11 @@ int seed_async(DevCtx& c, Taus master, int64_t slot_begin, int64_t count, const 
         WLP_CUDA(c.rejected.ensure(static_cast<int64_t>(rej.size())));
         WLP_CUDA(cudaMemcpyAsync(c.rejected.p, rej.data(), rej.size() * 8, cudaMemcpyHostToDevice, st));
     }
-    // the specials count and the model launch's grab counter (counter[1]) in one memset
-    WLP_CUDA(cudaMemsetAsync(c.counter.p, 0, 16, st));
+    // counter[spec_slot] is zero (the previous seeding cleared it); this seeding clears the
+    // other slot and the grab counter of the model launch behind it
+    const int slot = c.spec_slot;
+    c.spec_slot = 1 - slot;
+    c.spec_read = slot;
     c.work_zeroed = true;
     SeedArgs a;
     a.powers = c.powers.p;
@@ -445,7 +464,12 @@ int seed_async(DevCtx& c, Taus master, int64_t slot_begin, int64_t count, const 
     a.out = d_out;
     a.specials = c.specials.p;
     a.special_cap = kSpecialCap;
-    a.n_special = c.counter.p;
+    a.n_special = c.counter.p + slot;
+    a.zero_a = c.counter.p + (1 - slot);
+    a.zero_b = c.counter.p + 2;
+    a.done = c.seed_done.p;
+    a.report = c.d_mapped;
+    c.spec_mapped = true;
     c.planes_of = nullptr;
     c.planes_count = -1;
     if (planes) {  // the walk's bitsliced pipeline follows: write its bit planes as well
@@ -455,15 +479,22 @@ int seed_async(DevCtx& c, Taus master, int64_t slot_begin, int64_t count, const 
         c.planes_count = count;
     }
     WLP_CUDA(launch_seed(a, st));
+    c.pdl_next = true;
     return WLP_OK;
 }
 
 // Specials of the last seed_async (synchronises the stream).
 int read_specials(DevCtx& c, cudaStream_t st, std::vector<SpecialRec>& sp, int64_t& n_total) {
     c.work_zeroed = false;
-    WLP_CUDA(cudaMemcpyAsync(c.h_counter, c.counter.p, 8, cudaMemcpyDeviceToHost, st));
-    WLP_CUDA(cudaStreamSynchronize(st));
-    const unsigned long long n = *c.h_counter;
+    unsigned long long n = 0;
+    if (c.spec_mapped) {  // the seeding's last block stored it in mapped host memory
+        WLP_CUDA(cudaStreamSynchronize(st));
+        n = *reinterpret_cast<volatile unsigned long long*>(c.h_mapped);
+    } else {
+        WLP_CUDA(cudaMemcpyAsync(c.h_counter, c.counter.p + c.spec_read, 8, cudaMemcpyDeviceToHost, st));
+        WLP_CUDA(cudaStreamSynchronize(st));
+        n = *c.h_counter;
+    }
     n_total = static_cast<int64_t>(n);
     if (n_total > kSpecialCap) return fail(WLP_EINTERNAL, "random_spacing: too many special candidates");
     sp.resize(static_cast<size_t>(n_total));
@@ -505,6 +536,8 @@ bool walk_planes(const DevCtx& c, int model, int mode, const wlp_params& p, int6
 // any host-side preparation (lane tables are built on first use), when c.time_model is set.
 int mark_model_start(DevCtx& c, cudaStream_t st) {
     if (c.time_model) WLP_CUDA(cudaEventRecord(c.ev0, st));
+    // the model kernel may overlap the seeding's tail (PDL) unless events bracket it
+    set_pdl_launch(c.pdl_next && !c.time_model);
     return WLP_OK;
 }
 
@@ -514,6 +547,14 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
                 int64_t count, double* o0, double* o1, double* o2, cudaStream_t st, int& grid_out) {
     const bool zeroed = c.work_zeroed;  // valid only for the launch right after seed_async
     c.work_zeroed = false;
+    struct PdlReset {  // PDL only for the launch right after seed_async, never past this call
+        DevCtx& c;
+        ~PdlReset() {
+            c.pdl_next = false;
+            set_pdl_launch(false);
+        }
+    } pdl_reset{c};
+    if (!zeroed || g_hw_counters) c.pdl_next = false;  // memsets would sit between seeding and model
     RepArgs a;
     a.seeds = d_seeds;
     a.count = count;
@@ -561,7 +602,7 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
     const int64_t warps = static_cast<int64_t>(grid_out) * ((model == WLP_MODEL_MM1 ? kMm1Block : kWlpBlock) / 32);
     a.grab = static_cast<int>(std::clamp<int64_t>(count / (warps * 32), 1, 32));  // ~32 grabs per warp
     if (zeroed) {  // seed_async just cleared counter[1] on this stream
-        a.next = c.counter.p + 1;
+        a.next = c.counter.p + 2;
     } else {
         a.next = c.work.p;
         WLP_CUDA(cudaMemsetAsync(c.work.p, 0, sizeof(unsigned long long), st));
@@ -1585,9 +1626,11 @@ int wlp_run_plan(int model, const wlp_params* sets, const uint64_t* master_seeds
     }
     // one batched seeding launch for all sets, and the model right behind it; the spacing
     // check below re-runs the model only when two special candidates share a key
-    WLP_CUDA(cudaMemsetAsync(c->counter.p, 0, 16, st));  // specials count and the grab counter
+    WLP_CUDA(cudaMemsetAsync(c->counter.p + 3, 0, 16, st));  // the plan's specials count and grab counter
+    c->spec_read = 3;
+    c->spec_mapped = false;
     WLP_CUDA(launch_seed_jobs(c->powers.p, d_jobs, n_sets, blocks, R, c->seeds.p, c->specials.p, kSpecialCap,
-                              c->counter.p, st));
+                              c->counter.p + 3, st));
     PlanArgs pa;
     pa.serial_rho = mm1_serial_rho();
     pa.tlp_div = all_rcp ? kDivRcp : kDivIeee;
@@ -1598,7 +1641,7 @@ int wlp_run_plan(int model, const wlp_params* sets, const uint64_t* master_seeds
     pa.out0 = o0;
     pa.out1 = o1;
     pa.out2 = o2;
-    pa.next = c->counter.p + 1;
+    pa.next = c->counter.p + 4;
     const int wpb = (model == WLP_MODEL_MM1 ? kMm1Block : kWlpBlock) / 32;
     const int grid = static_cast<int>(
         std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(c->sms) * c->plan_bps[model], (R + wpb - 1) / wpb)));
@@ -1631,7 +1674,9 @@ int wlp_run_plan(int model, const wlp_params* sets, const uint64_t* master_seeds
             rej.swap(next);
             WLP_CUDA(c->rejected.ensure(static_cast<int64_t>(rej.size())));
             WLP_CUDA(cudaMemcpyAsync(c->rejected.p, rej.data(), rej.size() * 8, cudaMemcpyHostToDevice, st));
-            WLP_CUDA(cudaMemsetAsync(c->counter.p, 0, 8, st));
+            WLP_CUDA(cudaMemsetAsync(c->counter.p + 3, 0, 8, st));
+            c->spec_read = 3;
+            c->spec_mapped = false;
             SeedArgs a{};
             a.powers = c->powers.p;
             a.master = jobs[k].master;
@@ -1644,7 +1689,7 @@ int wlp_run_plan(int model, const wlp_params* sets, const uint64_t* master_seeds
             a.stride = R;
             a.specials = c->specials.p;
             a.special_cap = kSpecialCap;
-            a.n_special = c->counter.p;
+            a.n_special = c->counter.p + 3;
             WLP_CUDA(launch_seed(a, st));
             std::vector<SpecialRec> sp2;
             int64_t n2 = 0;
@@ -2069,6 +2114,9 @@ int wlp_shutdown(void) {
     c.work.release();
     if (c.h_counter) cudaFreeHost(c.h_counter);
     c.h_counter = nullptr;
+    if (c.h_mapped) cudaFreeHost(c.h_mapped);
+    c.h_mapped = nullptr;
+    c.seed_done.release();
     if (c.h_stage) cudaFreeHost(c.h_stage);
     c.h_stage = nullptr;
     c.h_stage_cap = 0;

@@ -61,3 +61,23 @@ timed("wlp_run_shard, args pre-marshalled (report)", lambda: w._lib.wlp_run_shar
 timed("wlp_run_shard, args pre-marshalled (no report)", lambda: w._lib.wlp_run_shard(
     int(model), w.C.byref(pp), 2, 42, 256, 0, R, None, 0, o[0], o[1], o[2], 1, None, sp, 4096, w.C.byref(nsp),
     None))
+
+# host-side issue cost per call (no synchronisation inside the loop: the launch queue
+# absorbs the GPU work, so wall / call is the host's own overhead)
+def host_cost(label, fn, iters=200):
+    for _ in range(5):
+        fn()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        fn()
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    print(f"{label:44s} host issue {(t1 - t0) * 1e3 / iters:8.4f} ms / call", flush=True)
+
+
+host_cost("wlp_run_shard pre-marshalled (no report)", lambda: w._lib.wlp_run_shard(
+    int(model), w.C.byref(pp), 2, 42, 256, 0, R, None, 0, o[0], o[1], o[2], 1, None, None, 0, None, None))
+host_cost("wlp_run_streams pre-marshalled", lambda: w._lib.wlp_run_streams(
+    int(model), w.C.byref(pp), 2, seeds.data_ptr(), R, 1, *o, 1, None, None))
+host_cost("torch empty-kernel baseline (x.add_(1))", lambda: outs[0].add_(1.0))
