@@ -717,7 +717,7 @@ __device__ __forceinline__ Taus lane_jump_g(const uint32_t* __restrict__ tab, in
 }
 
 #ifndef WLP_PIPE_MINB
-#define WLP_PIPE_MINB 4
+#define WLP_PIPE_MINB 3
 #endif
 template <int MODEL, bool WIDE, int S, bool WRAP>
 __global__ void __launch_bounds__(kWlpBlock, WLP_PIPE_MINB) k_wlp_pipe(RepArgs a, PipeSched ps,
@@ -2718,7 +2718,9 @@ cudaError_t launch_wlp(int model, const RepArgs& a, const uint32_t* lane_tab, co
 template <int MODEL, bool WIDE>
 void launch_wlp_pipe_m(const RepArgs& a, const PipeSched& s, const uint32_t* wrap_tab, int grid, cudaStream_t st) {
     auto go = [&](auto kernel) { launch_ex(kernel, grid, kWlpBlock, 0, st, a, s, wrap_tab); };
-    if (s.S == 8)
+    if (s.S == 4)
+        go(k_wlp_pipe<MODEL, WIDE, 4, true>);
+    else if (s.S == 8)
         go(k_wlp_pipe<MODEL, WIDE, 8, true>);
     else if (s.S == 16)
         go(k_wlp_pipe<MODEL, WIDE, 16, true>);
@@ -2731,7 +2733,7 @@ void launch_wlp_pipe_m(const RepArgs& a, const PipeSched& s, const uint32_t* wra
 cudaError_t launch_wlp_pipe(int model, const RepArgs& a, const PipeSched& s, const uint32_t* wrap_tab, int grid,
                             cudaStream_t st) {
     if (a.count <= 0) return cudaSuccess;
-    if (s.S != 32 && (!wrap_tab || (s.S != 16 && s.S != 8))) return cudaErrorInvalidValue;
+    if (s.S != 32 && (!wrap_tab || (s.S != 16 && s.S != 8 && s.S != 4))) return cudaErrorInvalidValue;
     // 32-bit sums hold pi's hits (< n) and the walk's raw q sum (|sum| <= 12 n)
     const bool wide = a.n >= (int64_t(1) << 27) || a.count >= (int64_t(1) << 31);
     if (model == 0)

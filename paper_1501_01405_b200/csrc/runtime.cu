@@ -625,6 +625,7 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
             // lane's chunk is long at 32 (each step then interleaves more panels)
             int S = g_pipe_lanes;
             if (S == 0) S = a.n >= 32 * kMm1PanelT * 8 ? 32 : 8;
+            if (S < 8) S = 8;  // (the mm1 pipeline comes in 8, 16 and 32 lanes)
             int G = kMm1PanelT;
             if (a.n % kMm1PanelT != 0 || a.n < static_cast<int64_t>(S) * kMm1PanelT) {  // the ragged kernel
                 S = 32;
@@ -845,8 +846,8 @@ int wlp_debug_set_near_cap(int cap) {
 }
 
 int wlp_set_pipe_lanes(int lanes) {
-    if (lanes != 0 && lanes != 8 && lanes != 16 && lanes != 32)
-        return fail(WLP_EDOMAIN, "pipeline lanes per replication must be 0 (auto), 8, 16 or 32");
+    if (lanes != 0 && lanes != 4 && lanes != 8 && lanes != 16 && lanes != 32)
+        return fail(WLP_EDOMAIN, "pipeline lanes per replication must be 0 (auto), 4, 8, 16 or 32");
     g_pipe_lanes = lanes;
     return WLP_OK;
 }

@@ -391,7 +391,7 @@ def test_mm1_pipeline_lanes_and_division_modes(gpu, port, lanes, lam, mu, n):
 @pytest.mark.parametrize("model", [0, 2])
 @pytest.mark.parametrize("R,n", [(992, 1), (1000, 5), (2500, 257), (2500, 999), (3001, 1000), (1500, 10_000),
                                  (4000, 63), (993, 2049)])
-@pytest.mark.parametrize("lanes", [32, 16, 8])
+@pytest.mark.parametrize("lanes", [32, 16, 8, 4])
 def test_wrapped_pipeline_rotating_chunks_vs_oracle(gpu, port, model, R, n, lanes):
     # the pi / walk warp pipeline with rotating chunk lengths (PipeSched: G-unit blocks, a
     # remainder of blocks spread over the phases, a sub-block tail at phase 31) and the wrap
