@@ -1442,19 +1442,30 @@ __device__ __forceinline__ void bs_walk_exact(BsTaus& t, BsCount& P, BsCount& Q,
     }
 }
 
+template <int P>
 struct BsPipeWarp {
     uint32_t cnt[32][33];   // finished groups: P digits 0..15, Q digits 16..31 (+1 pad)
     long long grp[32];
-    uint32_t late[32][33];  // wrap groups' late-chunk counters, by wrap index k (P 0..15, Q 16..31)
-    __align__(16) uint32_t seed[2][kBsLive];  // next groups' bit planes, fetched a step ahead
+    uint32_t late[32][33];  // wrap groups' late-chunk counters, by pipeline * S + wrap index
+    __align__(16) uint32_t seed[2][P][kBsLive];  // the pipelines' next groups' bit planes, a step ahead
 };
 
-// Lanes 0..21 copy one 16-byte piece each of a group's 352-byte bit planes into shared
-// memory, asynchronously (cp.async), so lane 0's feed never waits on global memory.
-__device__ __forceinline__ void bs_prefetch(uint32_t* dst, const uint32_t* src, int lane) {
-    if (lane < kBsLive / 4) {
-        const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst + 4 * lane));
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + 4 * lane) : "memory");
+// cp.async of the next groups' 352-byte bit planes (22 pieces of 16 B per group) into
+// shared memory: piece c of the warp's 22 * P goes to lane c % 32; gidx of pipeline j
+// comes from its first lane.
+template <int S>
+__device__ __forceinline__ void bs_prefetch(uint32_t (*dst)[kBsLive], const uint32_t* __restrict__ bseeds,
+                                            int64_t gidx, int lane) {
+    constexpr int P = 32 / S, kPieces = kBsLive / 4;
+#pragma unroll
+    for (int c0 = 0; c0 < kPieces * P; c0 += 32) {
+        const int c = c0 + lane, j = c / kPieces, k = c % kPieces;
+        const int64_t gj = __shfl_sync(kFull, gidx, (j < P ? j : 0) * S);
+        if (c < kPieces * P && gj >= 0) {
+            const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst[j] + 4 * k));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(bseeds + gj * kBsLive + 4 * k)
+                         : "memory");
+        }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -1490,48 +1501,58 @@ __device__ __forceinline__ void bs_dx_store(const uint32_t (&d)[32], const uint3
     for (int j = 0; j < 32; ++j) out[j] = dx[j];
 }
 
-// Walk WLP, bitsliced warp pipeline on the rotating schedule (PipeSched, S = 32: L(t)
-// steps per lane per pipeline step, any 32 consecutive L summing to n, chunk lengths not
-// tied to 16-step blocks: bs_walk_exact advances the planes exactly) with the wrap of
-// k_wlp_pipe: warp w owns groups [31w, 31w + 31) besides the ones it grabs; at step 0
-// lane l >= 1 starts wrap group l at its chunk l (its 32 seeds jumped by a lane table and
-// transposed into planes), and after the grabbed groups lane 0 is fed wrap groups 31..1,
-// whose early chunks end at the warp's last step; each wrap group's dx is the sum of its
-// early and late counters. (WRAP = false: a straight pipeline, for runs too small to give
-// every warp its wrap groups.)
-template <bool WRAP>
-__global__ void __launch_bounds__(kBsPipeBlock, 6) k_wlp_walk_bs_pipe(RepArgs a, const uint32_t* __restrict__ bseeds,
+// Walk WLP, bitsliced warp pipeline on the rotating schedule (PipeSched: L(t) steps per
+// lane per pipeline step, any S consecutive L summing to n; bs_walk_exact advances the
+// planes exactly, so chunks need not be whole 16-step blocks), S lanes per group of 32
+// replications (32/S pipelines side by side in the warp: with S = 8 a step carries 125
+// walk steps of 1,000 instead of 31, so the per-step hand-over of 120 words and the
+// feed / emit bookkeeping cost a quarter as much), with the wrap of k_wlp_pipe: each
+// pipeline owns S - 1 wrap groups besides the ones its warp grabs; at step 0 its lane p
+// >= 1 starts wrap group p at its chunk p (the 32 seeds jumped by a lane table and
+// transposed into planes), and after the grabbed groups its lane 0 is fed wrap groups
+// S-1..1, whose early chunks end at the pipeline's last step; each wrap group's dx is the
+// sum of its early and late counters. Feeding: the last lane of each pipeline, whose
+// group has just been emitted, loads the next group's planes (prefetched into shared
+// memory a step ahead by cp.async) and the hand-over rotates them to lane 0.
+// (WRAP = false: straight pipelines, for runs too small to give every pipeline its wrap
+// groups.)
+#ifndef WLP_BS_MINB
+#define WLP_BS_MINB 4  // 255 registers: no spills (6 blocks spilled ~700 B: 0.96 vs 0.92 ms at config 4)
+#endif
+template <int S, bool WRAP>
+__global__ void __launch_bounds__(kBsPipeBlock, WLP_BS_MINB) k_wlp_walk_bs_pipe(RepArgs a, const uint32_t* __restrict__ bseeds,
                                                                     int64_t groups, PipeSched ps,
                                                                     const uint32_t* __restrict__ wtab) {
-    constexpr int kW = kBsPipeBlock / 32;
-    __shared__ BsPipeWarp sh[kW];
-    BsPipeWarp& E = sh[threadIdx.x >> 5];
+    constexpr int kW = kBsPipeBlock / 32, P = 32 / S, kWr = S - 1;
+    __shared__ BsPipeWarp<P> sh[kW];
+    BsPipeWarp<P>& E = sh[threadIdx.x >> 5];
     pdl_wait();
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, g = lane / S, pos = lane % S;
+    const int src = g * S + (pos + S - 1) % S;  // rotation within the pipeline: pos - 1, pos 0 <- pos S-1
     const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * kW + (threadIdx.x >> 5);
-    const int64_t wrap0 = gwarp * kWrap;  // wrap group k is wrap0 + k - 1
-    const int64_t pool0 = WRAP ? static_cast<int64_t>(gridDim.x) * kW * kWrap : 0;
+    const int64_t wrap0 = gwarp * (P * kWr) + g * kWr;  // wrap group k of this pipeline: wrap0 + k - 1
+    const int64_t pool0 = WRAP ? static_cast<int64_t>(gridDim.x) * kW * (P * kWr) : 0;
     RepArgs ga = a;  // the grab scheduler hands out groups
     ga.count = groups;
     BsTaus t;
-    BsCount P, Q;
+    BsCount Pc, Qc;
 #pragma unroll
     for (int i = 0; i < 32; ++i) t.b1[i] = t.b2[i] = t.b3[i] = 0u;
-    bs_count_init(P);
-    bs_count_init(Q);
+    bs_count_init(Pc);
+    bs_count_init(Qc);
     // item codes: g >= 0 a grabbed group, -1 idle, -1-k the late chunks of wrap group k,
     // -33-k its early chunks
     long long grp = -1;
     int left = 0;
-    if (WRAP) {  // lane l >= 1: wrap group l's 32 seeds jumped to chunk l, as bit planes
+    if (WRAP) {  // lane p >= 1: wrap group p's 32 seeds jumped to chunk p, as bit planes,
         // one component at a time through the lane's row of the (still unused) result
         // buffer, in loops that are not unrolled: the prologue stays small
-        const int64_t r0 = (wrap0 + lane - 1) * 32;
+        const int64_t r0 = (wrap0 + pos - 1) * 32;
         uint32_t* row = E.cnt[lane];
         const uint32_t fill[3] = {kMin1, kMin2, kMin3};
 #pragma unroll 1
         for (int comp = 0; comp < 3; ++comp) {
-            if (lane > 0) {
+            if (pos > 0) {
                 const uint32_t* tab = wtab + comp * 4096 + lane;
 #pragma unroll 1
                 for (int j = 0; j < 32; ++j) {
@@ -1552,35 +1573,38 @@ __global__ void __launch_bounds__(kBsPipeBlock, 6) k_wlp_walk_bs_pipe(RepArgs a,
             }
             __syncwarp();
         }
-        if (lane > 0) {
-            grp = -1 - lane;
+        if (pos > 0) {
+            grp = -1 - pos;
         } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i) t.b1[i] = t.b2[i] = t.b3[i] = 0u;
         }
     }
     int64_t cur = 0, cend = 0;
-    bool more = true;
-    int wraps = kWrap, nemit = 0, phase = 0;
+    bool more = true;   // the warp still grabs (warp-uniform)
+    bool drain = false;  // this lane's pipeline takes no more grabbed groups
+    bool fin = false;    // this lane's pipeline has run its last step
+    int wraps = kWr, nemit = 0, phase = 0;
     auto flush = [&](int cnt) {
         __syncwarp();
         if (lane < cnt) {
-            const long long g = E.grp[lane];
+            const long long gg = E.grp[lane];
             uint32_t d[32];
 #pragma unroll
             for (int w = 0; w < 32; ++w) d[w] = E.cnt[lane][w];
             int32_t* dx = reinterpret_cast<int32_t*>(E.cnt[lane]);  // the slot's own row
             bs_dx_store(d, nullptr, dx);
             for (int j = 0; j < 32; ++j) {  // not unrolled: one copy of fmod's code
-                const int64_t r = g * 32 + j;
+                const int64_t r = gg * 32 + j;
                 if (r < a.count) a.out0[r] = walk_fold(dx[j], a.chunks);
             }
         }
         __syncwarp();
     };
-    // the item lane 0 takes next, decided a step ahead so its planes can be prefetched:
-    // a grabbed group, then (WRAP) the early chunks of wrap groups 31..1, then idle
-    auto next_item = [&](long long& code, int64_t& gidx) {  // warp-uniform
+    // the item this lane's pipeline takes next (decided a step ahead, so its planes can
+    // be prefetched): a grabbed group, then (WRAP) the early chunks of its wrap groups
+    // S-1..1, then idle. The grab is warp-uniform; P groups per step.
+    auto decide = [&](long long& code, int64_t& gidx) {
         if (more && cur >= cend) {
             const int64_t base = pool0 + grab_take(grab_issue(ga, lane));
             if (base >= groups) {
@@ -1590,33 +1614,31 @@ __global__ void __launch_bounds__(kBsPipeBlock, 6) k_wlp_walk_bs_pipe(RepArgs a,
                 cend = base + a.grab < groups ? base + a.grab : groups;
             }
         }
-        if (more) {
-            code = gidx = cur++;
-        } else if (WRAP && wraps > 0) {
+        code = gidx = -1;
+        if (!drain) {
+            const int64_t r = cur + g;
+            if (more && r < cend)
+                code = gidx = r;
+            else
+                drain = true;
+        }
+        if (drain && WRAP && wraps > 0) {
             code = -33 - wraps;
             gidx = wrap0 + wraps - 1;
             --wraps;
-        } else {
-            code = gidx = -1;
         }
+        if (more) cur += P;
     };
-    long long feed;
-    int64_t fidx;
-    next_item(feed, fidx);
-    int buf = 0;
-    if (fidx >= 0) bs_prefetch(E.seed[buf], bseeds + fidx * kBsLive, lane);
-    for (;;) {
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncwarp();
-        const bool last = WRAP && feed == -34;  // lane 0 takes wrap group 1: the warp's last step
-        if (lane == 0) {  // feed the item fetched last step
-            grp = feed;
-            if (fidx >= 0) {
-                const uint4* src = reinterpret_cast<const uint4*>(E.seed[buf]);
+    // lane `who` takes item (code, gidx) from the prefetch buffer, with fresh counters
+    auto take = [&](bool who, long long code, int64_t gidx, const uint32_t* planes) {
+        if (who) {
+            grp = code;
+            if (gidx >= 0) {
+                const uint4* q = reinterpret_cast<const uint4*>(planes);
                 uint32_t w[kBsLive];
 #pragma unroll
                 for (int k = 0; k < kBsLive / 4; ++k) {
-                    const uint4 v = src[k];
+                    const uint4 v = q[k];
                     w[4 * k] = v.x;
                     w[4 * k + 1] = v.y;
                     w[4 * k + 2] = v.z;
@@ -1628,83 +1650,108 @@ __global__ void __launch_bounds__(kBsPipeBlock, 6) k_wlp_walk_bs_pipe(RepArgs a,
                 for (int i = 3; i < 32; ++i) t.b2[i] = w[31 + i - 3];
 #pragma unroll
                 for (int i = 4; i < 32; ++i) t.b3[i] = w[60 + i - 4];
-                bs_count_init(P);
-                bs_count_init(Q);
-                if (WRAP && feed < -1) left = static_cast<int>(pipe_wrap_units(ps, static_cast<int>(-33 - feed)));
+                bs_count_init(Pc);
+                bs_count_init(Qc);
+                if (WRAP && code < -1) left = static_cast<int>(pipe_wrap_units(ps, static_cast<int>(-33 - code)));
             }
         }
-        __syncwarp();
-        if (!last) {
-            next_item(feed, fidx);
-            buf ^= 1;
-            if (fidx >= 0) bs_prefetch(E.seed[buf], bseeds + fidx * kBsLive, lane);
-        }
-        if (!WRAP && !__any_sync(kFull, grp != -1)) break;
+    };
+    long long feed, cur_feed;
+    int64_t fidx;
+    decide(feed, fidx);
+    int buf = 0;
+    bs_prefetch<S>(E.seed[buf], bseeds, fidx, lane);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    take(pos == 0, feed, fidx, E.seed[buf][g]);  // step 0: the first lanes take their items directly
+    cur_feed = feed;
+    for (;;) {
+        decide(feed, fidx);  // next step's items, prefetched while this step walks
+        buf ^= 1;
+        bs_prefetch<S>(E.seed[buf], bseeds, fidx, lane);
         uint32_t units = static_cast<uint32_t>(pipe_units(ps, phase));
-        if (WRAP && grp <= -34) {  // early chunk `lane` of wrap group k: stop exactly at its late part
+        if (WRAP && grp <= -34) {  // early chunk `pos` of wrap group k: stop exactly at its late part
             const int k = static_cast<int>(-33 - grp);
-            const int u = lane == k - 1 ? left : (left < static_cast<int>(units) ? left : static_cast<int>(units));
+            const int u = pos == k - 1 ? left : (left < static_cast<int>(units) ? left : static_cast<int>(units));
             left -= u;
             units = static_cast<uint32_t>(u);
         }
-        if (grp != -1) bs_walk_exact(t, P, Q, units);
-        const long long g31 = __shfl_sync(kFull, grp, 31);
-        if (g31 >= 0) {  // lane 31 finished a group
-            if (lane == 31) {
-#pragma unroll
-                for (int w = 0; w < 16; ++w) {
-                    E.cnt[nemit][w] = P.c[w];
-                    E.cnt[nemit][16 + w] = Q.c[w];
-                }
-                E.grp[nemit] = grp;
-            }
-            if (++nemit == 32) {
-                flush(32);
-                nemit = 0;
-            }
-        } else if (WRAP && g31 < -1 && lane == 31) {  // the late chunks of wrap group -1-g31
-            const int k = static_cast<int>(-1 - g31);
+        if (grp != -1) bs_walk_exact(t, Pc, Qc, units);
+        // the pipelines' last lanes: finished groups to the result buffer, late wrap chunks
+        // to their counters
+        const bool done = pos == S - 1 && grp >= 0;
+        const unsigned dm = __ballot_sync(kFull, done);
+        if (done) {
+            const int slot = nemit + __popc(dm & ((1u << lane) - 1u));
 #pragma unroll
             for (int w = 0; w < 16; ++w) {
-                E.late[k][w] = P.c[w];
-                E.late[k][16 + w] = Q.c[w];
+                E.cnt[slot][w] = Pc.c[w];
+                E.cnt[slot][16 + w] = Qc.c[w];
+            }
+            E.grp[slot] = grp;
+        } else if (WRAP && pos == S - 1 && grp < -1 && grp >= -32) {
+            const int k = static_cast<int>(-1 - grp);
+#pragma unroll
+            for (int w = 0; w < 16; ++w) {
+                E.late[g * S + k][w] = Pc.c[w];
+                E.late[g * S + k][16 + w] = Qc.c[w];
             }
         }
-        if (last) break;  // lanes 0..30 hold the early chunks of wrap groups 1..31
+        nemit += __popc(dm);
+        if (nemit > 32 - P) {
+            flush(nemit);
+            nemit = 0;
+        }
+        if (WRAP) {
+            const bool last = cur_feed == -34;  // this pipeline's step ends its wrap groups' early chunks
+            if (__any_sync(kFull, last)) {
+                __syncwarp();
+                if (last && pos < S - 1) {  // early counters (registers) + late counters (shared)
+                    uint32_t d[32];
 #pragma unroll
-        for (int i = 1; i < 32; ++i) t.b1[i] = __shfl_up_sync(kFull, t.b1[i], 1);
+                    for (int w = 0; w < 16; ++w) {
+                        d[w] = Pc.c[w];
+                        d[16 + w] = Qc.c[w];
+                    }
+                    int32_t* dx = reinterpret_cast<int32_t*>(E.late[g * S + pos + 1]);
+                    bs_dx_store(d, E.late[g * S + pos + 1], dx);
+                    const int64_t gg = wrap0 + pos;
+                    for (int j = 0; j < 32; ++j) {
+                        const int64_t r = gg * 32 + j;
+                        if (r < a.count) a.out0[r] = walk_fold(dx[j], a.chunks);
+                    }
+                }
+                if (last) {
+                    fin = true;
+                    grp = -1;
+                }
+                __syncwarp();
+            }
+            if (__all_sync(kFull, fin)) break;
+        }
+        // feed: the last lane of each pipeline (its group emitted) takes the next item, and
+        // the hand-over rotates it to the first lane
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+        take(pos == S - 1 && !fin, feed, fidx, E.seed[buf][g]);
+        cur_feed = fin ? -1 : feed;
 #pragma unroll
-        for (int i = 3; i < 32; ++i) t.b2[i] = __shfl_up_sync(kFull, t.b2[i], 1);
+        for (int i = 1; i < 32; ++i) t.b1[i] = __shfl_sync(kFull, t.b1[i], src);
 #pragma unroll
-        for (int i = 4; i < 32; ++i) t.b3[i] = __shfl_up_sync(kFull, t.b3[i], 1);
+        for (int i = 3; i < 32; ++i) t.b2[i] = __shfl_sync(kFull, t.b2[i], src);
+#pragma unroll
+        for (int i = 4; i < 32; ++i) t.b3[i] = __shfl_sync(kFull, t.b3[i], src);
 #pragma unroll
         for (int w = 0; w < 16; ++w) {
-            P.c[w] = __shfl_up_sync(kFull, P.c[w], 1);
-            Q.c[w] = __shfl_up_sync(kFull, Q.c[w], 1);
+            Pc.c[w] = __shfl_sync(kFull, Pc.c[w], src);
+            Qc.c[w] = __shfl_sync(kFull, Qc.c[w], src);
         }
-        grp = __shfl_up_sync(kFull, grp, 1);
-        if (WRAP) left = __shfl_up_sync(kFull, left, 1);
-        phase = (phase + 1) & 31;
+        grp = __shfl_sync(kFull, grp, src);
+        if (WRAP) left = __shfl_sync(kFull, left, src);
+        if (!WRAP && !more && !__any_sync(kFull, grp != -1)) break;
+        phase = phase == S - 1 ? 0 : phase + 1;
     }
     flush(nemit);
-    if (WRAP) {  // the wrap groups: early counters (registers) + late counters (shared)
-        __syncwarp();
-        if (lane < kWrap) {
-            uint32_t d[32];
-#pragma unroll
-            for (int w = 0; w < 16; ++w) {
-                d[w] = P.c[w];
-                d[16 + w] = Q.c[w];
-            }
-            int32_t* dx = reinterpret_cast<int32_t*>(E.late[lane + 1]);
-            bs_dx_store(d, E.late[lane + 1], dx);
-            const int64_t g = wrap0 + lane;
-            for (int j = 0; j < 32; ++j) {
-                const int64_t r = g * 32 + j;
-                if (r < a.count) a.out0[r] = walk_fold(dx[j], a.chunks);
-            }
-        }
-    }
 }
 
 // ---------------------------------------------------------------------------------
@@ -2848,14 +2895,31 @@ cudaError_t launch_tlp_walk_bs(const RepArgs& a, cudaStream_t st) {
 cudaError_t launch_wlp_walk_bs_pipe(const RepArgs& a, uint32_t* bseeds, const PipeSched& s, const uint32_t* wrap_tab,
                                     int grid, cudaStream_t st, bool planes_ready) {
     if (a.count <= 0) return cudaSuccess;
+    if (s.S != 32 && s.S != 16 && s.S != 8 && s.S != 4) return cudaErrorInvalidValue;
     const int64_t groups = (a.count + 31) / 32;
     if (!planes_ready)  // else the seeding kernel wrote them (SeedArgs::planes)
         launch_ex(k_bs_seeds, static_cast<unsigned>((groups + kBsBlock - 1) / kBsBlock), kBsBlock, 0, st, a, groups,
                   bseeds);
-    if (wrap_tab)
-        launch_ex(k_wlp_walk_bs_pipe<true>, grid, kBsPipeBlock, 0, st, a, bseeds, groups, s, wrap_tab);
-    else
-        launch_ex(k_wlp_walk_bs_pipe<false>, grid, kBsPipeBlock, 0, st, a, bseeds, groups, s, wrap_tab);
+    auto go = [&](auto kernel) { launch_ex(kernel, grid, kBsPipeBlock, 0, st, a, bseeds, groups, s, wrap_tab); };
+    if (wrap_tab) {
+        if (s.S == 4)
+            go(k_wlp_walk_bs_pipe<4, true>);
+        else if (s.S == 8)
+            go(k_wlp_walk_bs_pipe<8, true>);
+        else if (s.S == 16)
+            go(k_wlp_walk_bs_pipe<16, true>);
+        else
+            go(k_wlp_walk_bs_pipe<32, true>);
+    } else {
+        if (s.S == 4)
+            go(k_wlp_walk_bs_pipe<4, false>);
+        else if (s.S == 8)
+            go(k_wlp_walk_bs_pipe<8, false>);
+        else if (s.S == 16)
+            go(k_wlp_walk_bs_pipe<16, false>);
+        else
+            go(k_wlp_walk_bs_pipe<32, false>);
+    }
     return cudaGetLastError();
 }
 
@@ -2869,7 +2933,7 @@ cudaError_t launch_wlp_walk_bs_lanes(const RepArgs& a, const uint32_t* lane_tab,
 
 int wlp_walk_bs_pipe_blocks_per_sm() {
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_walk_bs_pipe<true>, kBsPipeBlock, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wlp_walk_bs_pipe<8, true>, kBsPipeBlock, 0);
     return nb < 1 ? 1 : nb;
 }
 

@@ -658,12 +658,19 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
         const int64_t groups = (count + 31) / 32;
         const int64_t cap = static_cast<int64_t>(c.sms) * c.bs_pipe_bps;
         constexpr int64_t kBsW = kBsPipeBlock / 32;
+        // S lanes per group: the most lanes that still give every lane >= 250 walk steps
+        // per pipeline step (config 4, 1,000 steps: S = 4, eight pipelines per warp; the
+        // hand-over of 120 words per step then costs ~1 % instead of ~9 % at S = 32)
+        int S = g_pipe_lanes;
+        if (S == 0) S = a.n >= 32 * 250 ? 32 : (a.n >= 16 * 250 ? 16 : (a.n >= 8 * 250 ? 8 : 4));
         const int64_t blocks = std::clamp<int64_t>((std::max<int64_t>(1, groups / 64) + 1) / 2, 1, cap);
-        const bool wrap = groups >= kWrap * kBsW * blocks;
+        const int64_t wpw = pipe_wrap_per_warp(S);
+        const bool wrap = groups >= wpw * kBsW * blocks;
         grid_out = static_cast<int>(blocks);
-        const int64_t pool = groups - (wrap ? kWrap * kBsW * blocks : 0);
-        a.grab = static_cast<int>(std::clamp<int64_t>(pool / (kBsW * blocks * 32), 1, 32));
-        const PipeSched ps = pipe_sched(a.n, a.n >= 512 ? 16 : 1);
+        const int64_t pool = groups - (wrap ? wpw * kBsW * blocks : 0);
+        const int64_t P = 32 / S;
+        a.grab = static_cast<int>(P * std::clamp<int64_t>(pool / (kBsW * blocks * 32 * P), 1, 32));
+        const PipeSched ps = pipe_sched(a.n, a.n >= 16 * S ? 16 : 1, S);
         const uint32_t* wtab = nullptr;
         if (wrap) WLP_TRY(wrap_table(c, ps, wtab));
         g_last_kernel = "k_wlp_walk_bs_pipe";

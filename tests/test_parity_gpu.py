@@ -164,6 +164,20 @@ def test_walk_bitsliced_wlp_matches_oracle(gpu, port, R, steps, variant):
     assert np.array_equal(run.outputs["out"], want["out"])
 
 
+@pytest.mark.parametrize("lanes", [4, 8, 16, 32])
+@pytest.mark.parametrize("R,steps", [(2000, 1), (2048, 37), (5000, 1000), (70_000, 999), (3000, 5003), (2100, 16)])
+def test_walk_bitsliced_pipeline_lanes_wrap_vs_oracle(gpu, port, R, steps, lanes):
+    # S lanes per group of 32 replications (32/S pipelines per warp), rotating chunks not
+    # tied to 16-step blocks, wrap groups (jumped seeds as planes at step 0, early and late
+    # counters summed), the rotation feed; ragged last group
+    p = gpu.ModelParams(replications=R, steps=steps, chunks=3 + R % 31)
+    want = port.run_model(2, oracle.params_from(p), 99 + R)
+    with gpu.wlp_variant(3), gpu.pipe_lanes(lanes):
+        run = gpu.run_model(gpu.ModelKind.Walk, p, gpu.ExecutionMode.Wlp, master_seed=99 + R)
+    assert gpu.last_kernel() == "k_wlp_walk_bs_pipe"
+    assert np.array_equal(run.outputs["out"], want["out"])
+
+
 def test_walk_wlp_auto_picks_the_bitsliced_pipeline_at_large_R(gpu, port):
     # R = 6e5: above the automatic threshold; the result is still the reference's
     p = gpu.ModelParams(replications=600_000, steps=100, chunks=30)
