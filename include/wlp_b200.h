@@ -132,18 +132,20 @@ int wlp_set_hw_counters(int enable);
  * 0 = automatic (default); 1 = lane jumps (pi / walk: each lane jumps its stream to its
  * chunk; mm1: segment chaining by fixed-point rounds); 2 = warp pipeline (replications
  * move lane to lane, each lane runs its segment in order from the state its neighbour
- * hands over; a 31-step drain per warp); 3 = walk: bitsliced warp pipeline (each pipeline
+ * hands over; rotating chunk lengths, fill and drain covered by wrap replications); 3 = walk: bitsliced warp pipeline (each pipeline
  * slot carries 32 replications as bit planes); 4 = walk: bitsliced lane chunks (a warp per
  * group of 32 replications, each lane jumps all 32 to its chunk). The walk picks 3 / 4 /
  * per-replication automatically by R; pi and mm1 treat 3 and 4 as 0. Outputs are
  * identical; only speed differs. */
 int wlp_set_wlp_variant(int variant);
 
-/* Tuning / test hook for later calls on this thread: lanes per replication of the pi /
- * walk warp pipeline (wlp variant 2, automatic at large R). 32 = the whole warp is one
- * pipeline; 16 or 8 = 32/S pipelines side by side in the warp, each replication split into
- * S chunks (longer steps for the same hand-over work); 0 = automatic (32 when n >= 3840,
- * else 16 when n >= 1920, else 8). Outputs are identical. */
+/* Tuning / test hook for later calls on this thread: lanes per replication S of the warp
+ * pipelines (pi / walk per replication: variant 2, automatic at large R; walk bitsliced:
+ * lanes per group of 32 replications; mm1: 8, 16 or 32). 32 = the whole warp is one
+ * pipeline; 16, 8 or 4 = 32/S pipelines side by side in the warp, every replication still
+ * passing through lanes of one warp only, split into S chunks (longer steps for the same
+ * hand-over work). 0 = automatic: pi / walk the most lanes that give every lane >= 250
+ * units per step; mm1 8 below 2,048 clients, else 32. Outputs are identical. */
 int wlp_set_pipe_lanes(int lanes);
 
 /* Test hook (this thread): near-one list entries per panel of the mm1 warp pipeline, a

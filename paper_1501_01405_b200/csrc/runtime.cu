@@ -685,7 +685,7 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
         // replications beyond the ones its warp grabs) it has no fill or drain either;
         // without it a 31-step triangle per warp idles.
         int S = g_pipe_lanes;
-        if (S == 0) S = a.n >= 32 * 120 ? 32 : (a.n >= 16 * 120 ? 16 : 8);
+        if (S == 0) S = a.n >= 32 * 250 ? 32 : (a.n >= 16 * 250 ? 16 : (a.n >= 8 * 250 ? 8 : 4));
         const int64_t wpw = pipe_wrap_per_warp(S);
         int pgrid = static_cast<int>(std::min<int64_t>(grid_out, static_cast<int64_t>(c.sms) * c.pipe_bps));
         bool wrap = count >= 2 * wpw * static_cast<int64_t>(pgrid) * (kWlpBlock / 32);
