@@ -719,6 +719,17 @@ __device__ __forceinline__ Taus lane_jump_g(const uint32_t* __restrict__ tab, in
 #ifndef WLP_PIPE_MINB
 #define WLP_PIPE_MINB 3
 #endif
+// The pipeline's bookkeeping lives in shared memory (volatile: re-read each step), so
+// none of it is live across the unit loop; the loop then runs in 32 registers and the
+// kernel fits 4 blocks (64 warps) per SM like the thread-per-replication kernel.
+struct PipeCtl {
+    long long cur, cend;  // the warp's current group of replications
+    int more;             // the warp still grabs
+    int nemit;            // finished replications waiting in the result buffer
+    int drain[8];         // per pipeline: takes no more grabbed replications
+    int wraps[8];         // per pipeline: wrap replications still to feed
+};
+
 template <int MODEL, bool WIDE, int S, bool WRAP>
 __global__ void __launch_bounds__(kWlpBlock, WLP_PIPE_MINB) k_wlp_pipe(RepArgs a, PipeSched ps,
                                                            const uint32_t* __restrict__ wtab) {
@@ -729,24 +740,34 @@ __global__ void __launch_bounds__(kWlpBlock, WLP_PIPE_MINB) k_wlp_pipe(RepArgs a
     __shared__ I emit_rep[kW][32];
     __shared__ I emit_sum[kW][32];
     __shared__ I late_sum[kW][32];
+    __shared__ PipeCtl ctl[kW];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int g = lane / S, pos = lane % S;  // pipeline of the lane, stage in it
-    const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * kW + wid;
-    // wrap replication k (1..S-1) of pipeline g: wrap0 + g*(S-1) + k - 1
-    const int64_t wrap0 = gwarp * (P * kWr) + g * kWr;
-    const int64_t pool0 = WRAP ? static_cast<int64_t>(gridDim.x) * kW * (P * kWr) : 0;
+    volatile PipeCtl& C = ctl[wid];
+    // wrap replication k (1..S-1) of pipeline g: wrap_first() + k - 1
+    auto wrap_first = [&]() {
+        return (static_cast<int64_t>(blockIdx.x) * kW + wid) * (P * kWr) + g * kWr;
+    };
     // item codes: r >= 0 a grabbed replication, -1 idle, -1-k the late chunks of wrap k,
     // -33-k its early chunks
     Taus st{kMin1, kMin2, kMin3};
     I sum = 0, rep = -1, left = 0;
     if (WRAP && pos > 0) {
-        st = lane_jump_g(wtab, lane, load_seed(a, wrap0 + pos - 1));
+        st = lane_jump_g(wtab, lane, load_seed(a, wrap_first() + pos - 1));
         rep = static_cast<I>(-1 - pos);
     }
-    int64_t cur = 0, cend = 0;  // the warp's current group of replications (warp-uniform)
-    bool more = true;           // the warp still grabs
-    bool drain = false;         // this lane's pipeline takes no more grabbed replications
-    int wraps = kWr, nemit = 0, phase = 0;
+    if (lane == 0) {
+        C.cur = 0;
+        C.cend = 0;
+        C.more = 1;
+        C.nemit = 0;
+    }
+    if (pos == 0) {
+        C.drain[g] = 0;
+        C.wraps[g] = kWr;
+    }
+    __syncwarp();
+    int phase = 0;
     auto value = [&](I c) {  // pi: hits; walk: the raw q sum, dx = (sum + 6n) / 6
         return MODEL == 0 ? __ddiv_rn(__dmul_rn(4.0, static_cast<double>(c)), static_cast<double>(a.n))
                           : walk_fold((static_cast<int64_t>(c) + 6 * a.n) / 6, a.chunks);
@@ -757,8 +778,12 @@ __global__ void __launch_bounds__(kWlpBlock, WLP_PIPE_MINB) k_wlp_pipe(RepArgs a
         __syncwarp();
     };
     for (;;) {
+        int64_t cur = C.cur, cend = C.cend;
+        bool more = C.more != 0, drain = C.drain[g] != 0;
+        int wraps = C.wraps[g];
         if (more && cur >= cend) {  // next group (a multiple of P replications)
-            const int64_t base = pool0 + grab_take(grab_issue(a, lane));
+            const int64_t base = (WRAP ? static_cast<int64_t>(gridDim.x) * kW * (P * kWr) : 0) +
+                                 grab_take(grab_issue(a, lane));
             if (base >= a.count) {
                 more = false;
             } else {
@@ -784,7 +809,7 @@ __global__ void __launch_bounds__(kWlpBlock, WLP_PIPE_MINB) k_wlp_pipe(RepArgs a
             if (WRAP && wraps > 0) {  // the early chunks of wrap replication `wraps`
                 if (pos == 0) {
                     rep = static_cast<I>(-33 - wraps);
-                    st = load_seed(a, wrap0 + wraps - 1);
+                    st = load_seed(a, wrap_first() + wraps - 1);
                     sum = 0;
                     left = static_cast<I>(pipe_wrap_units(ps, wraps));
                 }
@@ -796,6 +821,16 @@ __global__ void __launch_bounds__(kWlpBlock, WLP_PIPE_MINB) k_wlp_pipe(RepArgs a
                 rep = -1;  // finished pipeline
             }
         }
+        __syncwarp();
+        if (lane == 0) {
+            C.cur = cur;
+            C.cend = cend;
+            C.more = more ? 1 : 0;
+        }
+        if (pos == 0) {
+            C.drain[g] = drain ? 1 : 0;
+            C.wraps[g] = wraps;
+        }
         if (!more && !__any_sync(kFull, rep != -1)) break;
         uint32_t units = static_cast<uint32_t>(pipe_units(ps, phase));
         if (WRAP && rep <= -34) {  // early chunk pos of wrap k: stop exactly at its late part
@@ -805,6 +840,7 @@ __global__ void __launch_bounds__(kWlpBlock, WLP_PIPE_MINB) k_wlp_pipe(RepArgs a
             units = static_cast<uint32_t>(u);
         }
         if (rep != -1) sum += MODEL == 0 ? static_cast<I>(pi_hits(st, units)) : static_cast<I>(walk_q(st, units));
+        int nemit = C.nemit;
         if (S == 32) {
             const I r31 = __shfl_sync(kFull, rep, 31);
             if (r31 >= 0) {  // lane 31 finished a replication
@@ -835,9 +871,11 @@ __global__ void __launch_bounds__(kWlpBlock, WLP_PIPE_MINB) k_wlp_pipe(RepArgs a
                 nemit = 0;
             }
         }
+        __syncwarp();
+        if (lane == 0) C.nemit = nemit;
         if (WRAP && __any_sync(kFull, last)) {  // early chunks of wraps 1..S-1 end here
             __syncwarp();
-            if (last && pos < S - 1) a.out0[wrap0 + pos] = value(sum + late_sum[wid][g * S + pos + 1]);
+            if (last && pos < S - 1) a.out0[wrap_first() + pos] = value(sum + late_sum[wid][g * S + pos + 1]);
             if (last) rep = -1;
             if (S == 32) break;
         }
@@ -848,8 +886,10 @@ __global__ void __launch_bounds__(kWlpBlock, WLP_PIPE_MINB) k_wlp_pipe(RepArgs a
         rep = __shfl_up_sync(kFull, rep, 1, S);
         if (WRAP) left = __shfl_up_sync(kFull, left, 1, S);
         phase = phase == S - 1 ? 0 : phase + 1;
+        __syncwarp();
     }
-    flush(nemit);
+    __syncwarp();
+    flush(C.nemit);
 }
 
 // mm1 WLP shared memory: lane-start tables, panel-skip table, log table, then per warp
