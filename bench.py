@@ -209,14 +209,16 @@ def measured_peaks() -> dict:
         return {}
 
 
-def ncu_capture(kernel: str) -> dict:
-    """The latest committed ncu summary of `kernel` (profiles/ncu_summary.json, keyed by the
-    kernel's demangled name as wlp_last_kernel reports it)."""
+def ncu_capture(kernel: str, config: str = "") -> dict:
+    """The committed ncu summary of `kernel` (profiles/ncu_summary.json, keyed by the name
+    wlp_last_kernel reports) for this configuration: the capture whose label ends with
+    `config` (e.g. "cfg4_pi_wlp", tools/prof_round2.sh), else none."""
     try:
         caps = json.loads((ROOT / "profiles" / "ncu_summary.json").read_text()).get(kernel, {})
     except Exception:
         return {}
-    return caps[sorted(caps)[-1]] if caps else {}
+    keys = sorted(k for k in caps if config and k.endswith(config))
+    return caps[keys[-1]] if keys else {}
 
 
 def barrier(world):
@@ -392,7 +394,8 @@ def run_reference_arm(args):
 # ---- GPU arm -----------------------------------------------------------------------------------
 
 
-def roofline_of(model: int, kernel: str, units: int, kernel_ms: float, sms: int, fmax: float) -> dict:
+def roofline_of(model: int, kernel: str, units: int, kernel_ms: float, sms: int, fmax: float,
+                capture: str = "") -> dict:
     """The roofline that bounds `kernel`: issue slots (pi, per-replication
     walk), the ALU pipe (bitsliced walk: LOP3) or the FP64 pipe (mm1). No tensor-core or
     HBM roofline applies (integer / FP64 ALU work, ~20 B of HBM per replication)."""
@@ -409,7 +412,7 @@ def roofline_of(model: int, kernel: str, units: int, kernel_ms: float, sms: int,
         achieved = units * INSTR_PER_UNIT[model] / 32 / t / 1e9
         peak, bound = 4 * sms * fmax * 1e-3, "issue"
         algo = f"{INSTR_PER_UNIT[model]} lane-instr per unit x {units:.0e} units / 32"
-    cap = ncu_capture(kernel)
+    cap = ncu_capture(kernel, capture)
     return {"bound": bound, "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s",
             "frac": achieved / peak, "traffic": cap.get("dram_bytes_per_launch"), "algorithmic": algo,
             "kernel_ms": kernel_ms,
@@ -484,7 +487,8 @@ def sharded_record(w, D, model: int, p, world: int, comm, stats, stream, steps: 
                     "h2d_bytes_per_step": 64 * world, "d2h_bytes_per_step": 8 * nout * R,
                     "call": "wlp_run (run_model) into pinned host arrays" if e2e_single_call
                     else "wlp_run_shard per rank into pinned host arrays + statistics exchange"},
-            "roofline": roofline_of(model, kernel, units, kernel_avg, sms, fmax),
+            "roofline": roofline_of(model, kernel, units, kernel_avg, sms, fmax,
+                                    capture=f"cfg4_{w.model_name(w.ModelKind(model))}_wlp"),
             "result": {"mean": ci.mean, "half_width": ci.halfWidth, "n": ci.n},
             "gpu_launches_per_step": 2 + 2 * nout}
 
@@ -515,7 +519,8 @@ def extras_single_gpu(w, sms, fmax, peak_issue) -> dict:
             with w.wlp_variant(wv), w.tlp_variant(tv), w.pipe_lanes(lanes):
                 r = model_rate(w, m, pp, md)
             units_ = pp.replications * pp.units(m)
-            rl = roofline_of(int(m), r["kernel"], units_, r["kernel_ms"], sms, fmax)
+            rl = roofline_of(int(m), r["kernel"], units_, r["kernel_ms"], sms, fmax,
+                             capture=f"{name[:4]}_{w.model_name(m)}_{label}")
             r[{"issue": "issue_frac", "alu_pipe": "alu_frac", "fp64_pipe": "fp64_frac"}[rl["bound"]]] = rl["frac"]
             extras[name][label] = r
     # measured warp-execution evidence (paper Table 1 / Fig. 7 analogue): divergence events
@@ -627,7 +632,7 @@ def main():
     peaks = measured_peaks()
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     fmax = float(peaks.get("sm_max_mhz", 1965.0))
-    roofline = roofline_of(0, kernel, R_PER_GPU * DRAWS, kernel_avg, sms, fmax)
+    roofline = roofline_of(0, kernel, R_PER_GPU * DRAWS, kernel_avg, sms, fmax, capture="cfg2_pi_wlp")
     roofline["frac_at_measured_clock"] = (roofline["achieved"] / (4 * sms * clk["sm_mhz"] * 1e-3)
                                           if clk.get("sm_mhz") else None)
     roofline["hbm_gbs_output_writeout"] = (R_PER_GPU * 8 + 3 * 4 * R_PER_GPU) / (kernel_avg * 1e-3) / 1e9

@@ -38,6 +38,23 @@ sets = [w.ModelParams(replications=3 + k, clients=100 + 37 * k, lambda_=0.2 + 0.
 for mode in (E.Tlp, E.Wlp):
     w.run_plan(M.Mm1, sets, list(range(6)), mode)
     w.run_plan(M.Walk, [w.ModelParams(replications=4, steps=50 + 90 * k) for k in range(5)], list(range(5)), mode)
+# round 2: the wrapped pipelines at every lanes-per-replication S (forced at small R: fewer
+# warps, each with its wrap replications), the single-pass mm1 pipeline (mu = 1 and a
+# general rate; its near-one overflow redo forced by a small list capacity), the bitsliced
+# walk pipeline with wrap groups at S = 4 / 8 / 32
+for lanes in (4, 8, 16, 32):
+    with w.wlp_variant(2), w.pipe_lanes(lanes):
+        for model in (M.Pi, M.Walk):
+            w.run_model(model, w.ModelParams(replications=1100, draws=999, steps=999), E.Wlp, master_seed=11)
+for lanes in (8, 32):
+    for cap in (128, 4):
+        with w.wlp_variant(2), w.pipe_lanes(lanes), w.near_cap(cap):
+            w.run_model(M.Mm1, w.ModelParams(replications=1100, clients=512), E.Wlp, master_seed=11)
+            w.run_model(M.Mm1, w.ModelParams(replications=1100, clients=520, lambda_=0.3, mu=0.9), E.Wlp,
+                        master_seed=12)
+for lanes in (4, 8, 32):
+    with w.wlp_variant(3), w.pipe_lanes(lanes):
+        w.run_model(M.Walk, w.ModelParams(replications=70_000, steps=300), E.Wlp, master_seed=13)
 w.confidence_interval(list(np.linspace(0.0, 1.0, 1000)), 0.95)
 for jit in (False, True):
     w.run_model(M.Walk, w.ModelParams(replications=64, steps=100), E.Tlp, master_seed=3,
