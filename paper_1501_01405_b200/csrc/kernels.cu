@@ -2199,86 +2199,100 @@ constexpr size_t kMm1PipeSmem = 256 * 8 + (kMm1Block / 32) * sizeof(PanelWarp);
 // no wrap, its queue state is sequential, so the S-1 step drain remains: ~1 % at config 4).
 // ---------------------------------------------------------------------------------
 constexpr int kNearCap2 = 128;  // list entries per panel (expected 32 of 512 draws)
-static_assert((kNearCap2 & (kNearCap2 - 1)) == 0, "the list index wraps with a mask");
 
 struct Mm1Pan {
-    double2 v[kPanT][32];  // (a, s) of client c of lane l
-    uint2 nl[kNearCap2];   // near list: {draw, slot (double index into v)}
-    Taus save[32];         // each lane's stream state before the panel being filled
-    uint32_t cnt;          // near-list claims of the panel
-    uint32_t pad[3];
+    double2 v[kPanT][32];     // (a, s) of client c of lane l
+    uint4 dr[kPanD / 4][32];  // the panel's draws: draws 4q..4q+3 of lane l at dr[q][l]
+    uint2 nl[kNearCap2];      // near list: {draw, slot (double index into v)}
 };
 constexpr size_t kMm1Pipe2Smem = 256 * 8 + (kMm1Block / 32) * sizeof(Mm1Pan);
 
-// Client c of a panel: two draws, their table-path exponentials, near-ones listed (a
-// shared-memory atomic claims the list entry; the claim counter runs past the capacity on
-// overflow, the index wraps, and fix_near redoes such a panel).
+// Clients c, c+1 of a panel: four draws, their table-path exponentials to the slots, the
+// draws to the staging rows (one STS.128), their near-one flags into the lane's mask m
+// (bit 15 - j for draw j: two integer ops per draw, no branch).
 template <int DIV>
-__device__ __forceinline__ void fill_client(Taus& st, int c, int lane, bool on, double lambda, double mu, double inv_l,
-                                            double inv_m, const double* tab, Mm1Pan& W, uint32_t cap) {
-    uint32_t x, y;
-    taus_next2(st, x, y);
-    const double a = scale<DIV>(neg_log1m_table_dev(x, tab), lambda, inv_l);
-    const double sv = scale_mu<DIV>(neg_log1m_table_dev(y, tab), mu, inv_m);
-    W.v[c][lane] = make_double2(a, sv);
-    const uint32_t slot = static_cast<uint32_t>(pan_slot(2 * c, lane));
-    if (on && x <= kNearMax) W.nl[atomicAdd(&W.cnt, 1u) & (cap - 1)] = make_uint2(x, slot);
-    if (on && y <= kNearMax) W.nl[atomicAdd(&W.cnt, 1u) & (cap - 1)] = make_uint2(y, slot + 1);
+__device__ __forceinline__ void fill_pair(Taus& st, int c, int lane, uint32_t& m, double lambda, double mu,
+                                          double inv_l, double inv_m, const double* tab, Mm1Pan& W) {
+    uint4 q4;
+    taus_next2(st, q4.x, q4.y);
+    taus_next2(st, q4.z, q4.w);
+    near_bit(m, q4.x);
+    near_bit(m, q4.y);
+    near_bit(m, q4.z);
+    near_bit(m, q4.w);
+    W.dr[c / 2][lane] = q4;
+    W.v[c][lane] = make_double2(scale<DIV>(neg_log1m_table_dev(q4.x, tab), lambda, inv_l),
+                                scale_mu<DIV>(neg_log1m_table_dev(q4.y, tab), mu, inv_m));
+    W.v[c + 1][lane] = make_double2(scale<DIV>(neg_log1m_table_dev(q4.z, tab), lambda, inv_l),
+                                    scale_mu<DIV>(neg_log1m_table_dev(q4.w, tab), mu, inv_m));
 }
 
-// The listed near-ones of the panel just filled, into their slots; on overflow every lane
-// redraws its panel from the saved state and fixes its own near-ones.
+// The near-one draws of the panel just filled, into their slots. Each lane's flag mask m
+// (~1 set bit of 16) is turned into list entries at the lane's place from one lane scan
+// of the counts (a loop over the set bits only); the warp then evaluates the list in one
+// pass across the lanes. More than `cap` near-ones (never at random draws: 128 of 512)
+// fall back to each lane fixing its own from the staged draws. Idle lanes (on = false)
+// list nothing.
 template <int DIV>
-__device__ __forceinline__ void fix_near(Mm1Pan& W, int lane, bool on, double lambda, double mu, double inv_l,
-                                         double inv_m, uint32_t cap) {
-    __syncwarp();
-    const uint32_t total = W.cnt;
-    __syncwarp();
-    if (lane == 0) W.cnt = 0;
+__device__ __forceinline__ void fix_near(Mm1Pan& W, int lane, bool on, uint32_t m, double lambda, double mu,
+                                         double inv_l, double inv_m, uint32_t cap) {
+    if (!on) m = 0u;
+    const int c = __popc(m);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const uint32_t total = static_cast<uint32_t>(__shfl_sync(kFull, incl, 31));
     double* v = reinterpret_cast<double*>(&W.v[0][0]);
+    const uint32_t* dr = reinterpret_cast<const uint32_t*>(&W.dr[0][0]);
+    __syncwarp();
     if (total <= cap) {
+        int pos = incl - c;
+        while (m) {  // this lane's near draws (bit 15 - j: draw j)
+            const int j = __clz(m) - 16;
+            m &= ~(0x8000u >> j);
+            W.nl[pos++] = make_uint2(dr[(j >> 2) * 128 + lane * 4 + (j & 3)], static_cast<uint32_t>(pan_slot(j, lane)));
+        }
+        __syncwarp();
         for (uint32_t k = lane; k < total; k += 32) {
             const uint2 it = W.nl[k];
             const double e = it.x == 0u ? -0.0 : -log_near_one_dev(one_minus_u32_dev(it.x));
             v[it.y] = scale_slot<DIV>(e, it.y & 1u, lambda, mu, inv_l, inv_m);
         }
-    } else if (on) {
-        Taus t = W.save[lane];
-        for (int j = 0; j < kPanD; ++j) {
-            const uint32_t n = taus_next(t);
-            if (n <= kNearMax) {
-                const double e = n == 0u ? -0.0 : -log_near_one_dev(one_minus_u32_dev(n));
-                v[pan_slot(j, lane)] = scale_slot<DIV>(e, j & 1, lambda, mu, inv_l, inv_m);
-            }
+    } else {
+        while (m) {
+            const int j = __clz(m) - 16;
+            m &= ~(0x8000u >> j);
+            const uint32_t n = dr[(j >> 2) * 128 + lane * 4 + (j & 3)];
+            const double e = n == 0u ? -0.0 : -log_near_one_dev(one_minus_u32_dev(n));
+            v[pan_slot(j, lane)] = scale_slot<DIV>(e, j & 1, lambda, mu, inv_l, inv_m);
         }
     }
     __syncwarp();
 }
 
-template <int DIV>
-__device__ __forceinline__ void fill_panel(Taus& st, int lane, bool on, double lambda, double mu, double inv_l,
-                                           double inv_m, const double* tab, Mm1Pan& W, uint32_t cap) {
-    W.save[lane] = st;
-#pragma unroll
-    for (int c = 0; c < kPanT; ++c) fill_client<DIV>(st, c, lane, on, lambda, mu, inv_l, inv_m, tab, W, cap);
-    fix_near<DIV>(W, lane, on, lambda, mu, inv_l, inv_m, cap);
-}
-
 // One pipeline step of a lane: np panels of its chunk (np >= 1, warp-uniform). Panel p's
-// recursion runs client by client interleaved with the fill of panel p + 1.
+// recursion runs two clients at a time interleaved with the fill of panel p + 1 into the
+// same slots (each slot is read by the recursion before its own lane overwrites it).
 template <int DIV>
 __device__ __forceinline__ void mm1_chunk(Taus& st, Queue& q, int np, int lane, bool on, double lambda, double mu,
                                           double inv_l, double inv_m, const double* tab, Mm1Pan& W, uint32_t cap) {
-    fill_panel<DIV>(st, lane, on, lambda, mu, inv_l, inv_m, tab, W, cap);
-    for (int p = 1; p < np; ++p) {
-        W.save[lane] = st;
+    uint32_t m = 0;
 #pragma unroll
-        for (int c = 0; c < kPanT; ++c) {
-            const double2 v = W.v[c][lane];  // panel p-1's client c, then its slot is refilled
-            q.client(v.x, v.y);
-            fill_client<DIV>(st, c, lane, on, lambda, mu, inv_l, inv_m, tab, W, cap);
+    for (int c = 0; c < kPanT; c += 2) fill_pair<DIV>(st, c, lane, m, lambda, mu, inv_l, inv_m, tab, W);
+    fix_near<DIV>(W, lane, on, m, lambda, mu, inv_l, inv_m, cap);
+    for (int p = 1; p < np; ++p) {
+        m = 0;
+#pragma unroll
+        for (int c = 0; c < kPanT; c += 2) {
+            const double2 v0 = W.v[c][lane], v1 = W.v[c + 1][lane];  // panel p-1's clients c, c+1
+            q.client(v0.x, v0.y);
+            q.client(v1.x, v1.y);
+            fill_pair<DIV>(st, c, lane, m, lambda, mu, inv_l, inv_m, tab, W);
         }
-        fix_near<DIV>(W, lane, on, lambda, mu, inv_l, inv_m, cap);
+        fix_near<DIV>(W, lane, on, m, lambda, mu, inv_l, inv_m, cap);
     }
 #pragma unroll
     for (int c = 0; c < kPanT; ++c) {
@@ -2294,7 +2308,6 @@ __global__ void __launch_bounds__(kMm1Block, WLP_MM1_MINB) k_wlp_mm1_pipe(RepArg
     double* logtab = reinterpret_cast<double*>(smraw);
     Mm1Pan& W = reinterpret_cast<Mm1Pan*>(logtab + 256)[threadIdx.x >> 5];
     stage_log_table(logtab);
-    if ((threadIdx.x & 31) == 0) W.cnt = 0;
     __syncthreads();
     pdl_wait();
     const int lane = threadIdx.x & 31, g = lane / S, pos = lane % S;
