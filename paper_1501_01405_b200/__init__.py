@@ -798,12 +798,13 @@ def run_shard(model: ModelKind, p: ModelParams, mode: ExecutionMode, master_seed
     special seeding candidates. If `report` is given it is filled
     with the model kernel's measured time (CUDA events on the launching stream)."""
     o = [_ptr(x) for x in outs] + [None] * (3 - len(outs))
-    rej = np.asarray(sorted(rejected), dtype=np.int64)
+    rej = np.asarray(sorted(rejected), dtype=np.int64) if len(rejected) else None  # (usually empty)
     sp = _special_buffer(special_cap)
     nsp = C.c_int64()
     rep = _Report() if report is not None else None
     _check(_lib.wlp_run_shard(int(model), C.byref(_params(p)), int(mode), master_seed & (2**64 - 1),
-                              int(tlp_block_size), r_begin, r_count, _ptr(rej) if len(rej) else None, len(rej),
+                              int(tlp_block_size), r_begin, r_count, _ptr(rej) if rej is not None else None,
+                              len(rej) if rej is not None else 0,
                               o[0], o[1], o[2], 1 if on_device else 0, stream, sp, special_cap, C.byref(nsp),
                               C.byref(rep) if rep is not None else None))
     if rep is not None:

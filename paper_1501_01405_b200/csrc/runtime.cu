@@ -187,13 +187,17 @@ int ctx_init(DevCtx& c) {
 
 // Context of the calling thread's current device, locked.
 int acquire(DevCtx*& out, std::unique_lock<std::mutex>& lk) {
+    // the device count is asked once per process (the call costs ~1 us on every run)
+    static const std::pair<cudaError_t, int> count = [] {
+        int n = 0;
+        const cudaError_t e = cudaGetDeviceCount(&n);
+        return std::make_pair(e, n);
+    }();
+    if (count.first != cudaSuccess || count.second == 0)
+        return fail(WLP_ECUDA, std::string("no CUDA device: ") + cudaGetErrorString(count.first));
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return fail(WLP_ECUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
-    int n = 0;
-    e = cudaGetDeviceCount(&n);
-    if (e != cudaSuccess || n == 0)
-        return fail(WLP_ECUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
     DevCtx* c;
     {
         std::lock_guard<std::mutex> g(g_ctx_mu);
@@ -213,6 +217,9 @@ int acquire(DevCtx*& out, std::unique_lock<std::mutex>& lk) {
 // The device scratch (seed keys, work counter, specials) is shared by every call on a
 // device. Calls on one stream are ordered by the stream; a call on a different stream
 // first waits for the last library work, and every call records its end.
+// (The event is recorded at the end of every call, on that call's stream: recording it
+// lazily on the previous stream when the stream changes would touch streams callers may
+// have destroyed meanwhile, as wlp_run_devices' worker streams are.)
 struct StreamOrder {
     DevCtx& c;
     cudaStream_t st;

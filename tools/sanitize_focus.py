@@ -1,6 +1,13 @@
+"""Focused compute-sanitizer driver for one round-2 kernel family (run on the GPU box):
+
+    compute-sanitizer --tool racecheck python tools/sanitize_focus.py pipe|mm1|bs|seed
+"""
 import sys
-sys.path.insert(0, '.')
-import paper_1501_01405_b200 as w
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import paper_1501_01405_b200 as w  # noqa: E402
 M, E = w.ModelKind, w.ExecutionMode
 which = sys.argv[1]
 if which == "pipe":
