@@ -124,6 +124,23 @@ __device__ __forceinline__ Taus uni_jump(const uint32_t* tab, Taus t) {
     return t;
 }
 
+// Output stores: the device arrays, and the host mirrors when the run writes the host's
+// pinned buffers directly (RepArgs::h0..h2).
+__device__ __forceinline__ void put1(const RepArgs& a, int64_t r, double v) {
+    a.out0[r] = v;
+    if (a.h0) a.h0[r] = v;
+}
+__device__ __forceinline__ void put3(const RepArgs& a, int64_t r, double v0, double v1, double v2) {
+    a.out0[r] = v0;
+    a.out1[r] = v1;
+    a.out2[r] = v2;
+    if (a.h0) {
+        a.h0[r] = v0;
+        a.h1[r] = v1;
+        a.h2[r] = v2;
+    }
+}
+
 __device__ __forceinline__ Taus load_seed(const RepArgs& a, int64_t r) {
     return Taus{__ldg(a.seeds + r), __ldg(a.seeds + a.count + r), __ldg(a.seeds + 2 * a.count + r)};
 }
@@ -671,7 +688,7 @@ __global__ void __launch_bounds__(kWlpBlock, 4) k_wlp_lanes(RepArgs a, const uin
             }
             if (lane == static_cast<int>(r - base)) keep = val;
         }
-        if (lane < end - base) a.out0[base + lane] = keep;
+        if (lane < end - base) put1(a, base + lane, keep);
         if (COUNT) {
             hw.ld += 3 * static_cast<unsigned>(end - base);
             hw.st += 1;
@@ -774,7 +791,7 @@ __global__ void __launch_bounds__(kWlpBlock, WLP_PIPE_MINB) k_wlp_pipe(RepArgs a
     };
     auto flush = [&](int cnt) {
         __syncwarp();
-        if (lane < cnt) a.out0[emit_rep[wid][lane]] = value(emit_sum[wid][lane]);
+        if (lane < cnt) put1(a, emit_rep[wid][lane], value(emit_sum[wid][lane]));
         __syncwarp();
     };
     for (;;) {
@@ -875,7 +892,7 @@ __global__ void __launch_bounds__(kWlpBlock, WLP_PIPE_MINB) k_wlp_pipe(RepArgs a
         if (lane == 0) C.nemit = nemit;
         if (WRAP && __any_sync(kFull, last)) {  // early chunks of wraps 1..S-1 end here
             __syncwarp();
-            if (last && pos < S - 1) a.out0[wrap_first() + pos] = value(sum + late_sum[wid][g * S + pos + 1]);
+            if (last && pos < S - 1) put1(a, wrap_first() + pos, value(sum + late_sum[wid][g * S + pos + 1]));
             if (last) rep = -1;
             if (S == 32) break;
         }
@@ -1157,9 +1174,7 @@ __global__ void __launch_bounds__(kMm1Block, 3) k_wlp_mm1(RepArgs a, const uint3
             }
         }
         if (lane < end - base) {
-            a.out0[base + lane] = k0;
-            a.out1[base + lane] = k1;
-            a.out2[base + lane] = k2;
+            put3(a, base + lane, k0, k1, k2);
         }
         if (COUNT) {
             hw.ld += (3 + 24) * static_cast<unsigned>(end - base);  // seed words, lane-jump table reads
@@ -1244,11 +1259,11 @@ __global__ void k_tlp(RepArgs a) {
     HwTally hw;
     if (COUNT) hw.t0 = hw_clock();
     if (MODEL == 0) {
-        a.out0[r] = pi_rep_tlp(st, a.n);  // no data-dependent branch: no events
+        put1(a, r, pi_rep_tlp(st, a.n));  // no data-dependent branch: no events
     } else if (COUNT) {
-        a.out0[r] = walk_rep_tlp_counted(st, a.n, a.chunks, hw.div);
+        put1(a, r, walk_rep_tlp_counted(st, a.n, a.chunks, hw.div));
     } else {
-        a.out0[r] = walk_rep_tlp(st, a.n, a.chunks);
+        put1(a, r, walk_rep_tlp(st, a.n, a.chunks));
     }
     if (COUNT) {
         hw.ld = 3;  // the seed words
@@ -1399,7 +1414,7 @@ __global__ void __launch_bounds__(kBsBlock) k_tlp_walk_bs(RepArgs a) {
     for (int j = 0; j < 32; ++j) {
         if (r0 + j >= a.count) break;
         const int64_t dx = static_cast<int64_t>(pv[j]) - static_cast<int64_t>(qv[j]) + (flushing ? acc[j] : 0);
-        a.out0[r0 + j] = walk_fold(dx, a.chunks);
+        put1(a, r0 + j, walk_fold(dx, a.chunks));
     }
 }
 
@@ -1625,20 +1640,23 @@ __global__ void __launch_bounds__(kBsPipeBlock, WLP_BS_MINB) k_wlp_walk_bs_pipe(
     bool drain = false;  // this lane's pipeline takes no more grabbed groups
     bool fin = false;    // this lane's pipeline has run its last step
     int wraps = kWr, nemit = 0, phase = 0;
+    // Stores group gg's 32 folded results from the dx row `row`: lane j writes element j,
+    // so each store instruction covers 256 consecutive bytes (with a lane per group and 32
+    // strided stores, the host-mirror writes over PCIe were 8-byte transactions).
+    auto store_group = [&](long long gg, const uint32_t* row) {
+        const int64_t r = gg * 32 + lane;
+        if (r < a.count) put1(a, r, walk_fold(static_cast<int32_t>(row[lane]), a.chunks));
+    };
     auto flush = [&](int cnt) {
         __syncwarp();
         if (lane < cnt) {
-            const long long gg = E.grp[lane];
             uint32_t d[32];
 #pragma unroll
             for (int w = 0; w < 32; ++w) d[w] = E.cnt[lane][w];
-            int32_t* dx = reinterpret_cast<int32_t*>(E.cnt[lane]);  // the slot's own row
-            bs_dx_store(d, nullptr, dx);
-            for (int j = 0; j < 32; ++j) {  // not unrolled: one copy of fmod's code
-                const int64_t r = gg * 32 + j;
-                if (r < a.count) a.out0[r] = walk_fold(dx[j], a.chunks);
-            }
+            bs_dx_store(d, nullptr, reinterpret_cast<int32_t*>(E.cnt[lane]));  // the slot's own row
         }
+        __syncwarp();
+        for (int sl = 0; sl < cnt; ++sl) store_group(E.grp[sl], E.cnt[sl]);
         __syncwarp();
     };
     // the item this lane's pipeline takes next (decided a step ahead, so its planes can
@@ -1746,6 +1764,7 @@ __global__ void __launch_bounds__(kBsPipeBlock, WLP_BS_MINB) k_wlp_walk_bs_pipe(
             const bool last = cur_feed == -34;  // this pipeline's step ends its wrap groups' early chunks
             if (__any_sync(kFull, last)) {
                 __syncwarp();
+                const unsigned fm = __ballot_sync(kFull, last && pos < S - 1);
                 if (last && pos < S - 1) {  // early counters (registers) + late counters (shared)
                     uint32_t d[32];
 #pragma unroll
@@ -1753,13 +1772,12 @@ __global__ void __launch_bounds__(kBsPipeBlock, WLP_BS_MINB) k_wlp_walk_bs_pipe(
                         d[w] = Pc.c[w];
                         d[16 + w] = Qc.c[w];
                     }
-                    int32_t* dx = reinterpret_cast<int32_t*>(E.late[g * S + pos + 1]);
-                    bs_dx_store(d, E.late[g * S + pos + 1], dx);
-                    const int64_t gg = wrap0 + pos;
-                    for (int j = 0; j < 32; ++j) {
-                        const int64_t r = gg * 32 + j;
-                        if (r < a.count) a.out0[r] = walk_fold(dx[j], a.chunks);
-                    }
+                    bs_dx_store(d, E.late[g * S + pos + 1], reinterpret_cast<int32_t*>(E.late[g * S + pos + 1]));
+                }
+                __syncwarp();
+                for (unsigned mm = fm; mm; mm &= mm - 1) {  // wrap group of lane l: (l / S, l % S)
+                    const int l = __ffs(static_cast<int>(mm)) - 1;
+                    store_group(gwarp * (P * kWr) + (l / S) * kWr + l % S, E.late[l + 1]);
                 }
                 if (last) {
                     fin = true;
@@ -1871,7 +1889,7 @@ __global__ void __launch_bounds__(kBsLanesBlock, 2) k_wlp_walk_bs_lanes(RepArgs 
             for (int w = 0; w < kD; ++w) dx |= static_cast<int32_t>((D[w] >> lane) & 1u) << w;
             dx = static_cast<int32_t>(static_cast<uint32_t>(dx) << (32 - kD)) >> (32 - kD);  // sign-extend from digit 21
             const int64_t r = g * 32 + lane;
-            if (r < a.count) a.out0[r] = walk_fold(dx, a.chunks);
+            if (r < a.count) put1(a, r, walk_fold(dx, a.chunks));
         }
         g = grab_take(ticket);
     }
@@ -2163,9 +2181,7 @@ __global__ void __launch_bounds__(kMm1Block, WLP_MM1_MINB) k_wlp_mm1_pipe_ragged
             panel_clients(q, P, cnt, lane);
         }
         if (lane == 31 && rep >= 0) {  // lane 31 finished a replication
-            a.out0[rep] = __ddiv_rn(q.idle, nd);
-            a.out1[rep] = __ddiv_rn(q.sumw, nd);
-            a.out2[rep] = __ddiv_rn(q.sums, nd);
+            put3(a, rep, __ddiv_rn(q.idle, nd), __ddiv_rn(q.sumw, nd), __ddiv_rn(q.sums, nd));
         }
         st.s1 = __shfl_up_sync(kFull, st.s1, 1);
         st.s2 = __shfl_up_sync(kFull, st.s2, 1);
@@ -2342,9 +2358,7 @@ __global__ void __launch_bounds__(kMm1Block, WLP_MM1_MINB) k_wlp_mm1_pipe(RepArg
         if (np > 0)
             mm1_chunk<DIV>(st, q, np, lane, rep >= 0, a.lambda, a.mu, a.inv_lambda, a.inv_mu, logtab, W, a.near_cap);
         if (pos == S - 1 && rep >= 0) {  // the pipeline's last lane finished a replication
-            a.out0[rep] = __ddiv_rn(q.idle, nd);
-            a.out1[rep] = __ddiv_rn(q.sumw, nd);
-            a.out2[rep] = __ddiv_rn(q.sums, nd);
+            put3(a, rep, __ddiv_rn(q.idle, nd), __ddiv_rn(q.sumw, nd), __ddiv_rn(q.sums, nd));
         }
         st.s1 = __shfl_up_sync(kFull, st.s1, 1, S);
         st.s2 = __shfl_up_sync(kFull, st.s2, 1, S);
@@ -2405,9 +2419,7 @@ __global__ void __launch_bounds__(SMALL ? 256 : 1024, SMALL ? WLP_TLP_MM1_MINB :
     }
     if (!live) return;
     const double nd = static_cast<double>(a.n);
-    a.out0[r] = __ddiv_rn(q.idle, nd);
-    a.out1[r] = __ddiv_rn(q.sumw, nd);
-    a.out2[r] = __ddiv_rn(q.sums, nd);
+    put3(a, r, __ddiv_rn(q.idle, nd), __ddiv_rn(q.sumw, nd), __ddiv_rn(q.sums, nd));
 }
 
 // ---------------------------------------------------------------------------------

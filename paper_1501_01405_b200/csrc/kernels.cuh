@@ -27,6 +27,12 @@ struct RepArgs {
     double* out0;
     double* out1;
     double* out2;
+    // optional host mirrors (mapped pinned host memory, device-accessible): every output
+    // is also stored there as it is produced, so results reach the host during the run
+    // instead of by a copy after it (the device arrays still feed the statistics)
+    double* h0 = nullptr;
+    double* h1 = nullptr;
+    double* h2 = nullptr;
     // WLP: warps take `grab` consecutive replications at a time from *next (zeroed
     // before launch), so warps the arbiter favours do not leave a tail behind them
     unsigned long long* next = nullptr;

@@ -120,6 +120,7 @@ struct DevCtx {
     int spec_read = 0;                   // the slot read_specials reads
     bool work_zeroed = false;            // counter[2] was cleared by the seeding just launched
     bool pdl_next = false;               // the next model launch directly follows a seeding kernel
+    double* hm[3] = {nullptr, nullptr, nullptr};  // host mirrors for the next model launch
     bool time_model = false;  // model_async records ev0 right before its launch
     unsigned long long* h_counter = nullptr;  // pinned host word for the specials count readback
     unsigned long long* h_mapped = nullptr;   // mapped pinned word the seeding stores the count to
@@ -539,6 +540,25 @@ bool walk_planes(const DevCtx& c, int model, int mode, const wlp_params& p, int6
     return model == WLP_MODEL_WALK && mode != WLP_MODE_TLP && !g_hw_counters && walk_bs_choice(c, count, p.steps) == 3;
 }
 
+// Device aliases of the caller's host output arrays when they are pinned and mapped into
+// this device's address space (cudaHostAlloc, cudaHostRegister; torch pin_memory): the
+// model kernel then stores every output there as well, as it is produced, and no copy
+// follows the run. Pageable arrays keep the device buffer and the copy.
+bool host_mirrors(DevCtx& c, int model, double* h0, double* h1, double* h2, double* (&out)[3]) {
+    double* hs[3] = {h0, h1, h2};
+    out[0] = out[1] = out[2] = nullptr;
+    for (int k = 0; k < (model == WLP_MODEL_MM1 ? 3 : 1); ++k) {
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, hs[k]) != cudaSuccess) {
+            cudaGetLastError();  // (an unregistered pointer is not an error for the run)
+            return false;
+        }
+        if (at.type != cudaMemoryTypeHost || at.devicePointer == nullptr || at.device != c.dev) return false;
+        out[k] = static_cast<double*>(at.devicePointer);
+    }
+    return true;
+}
+
 // The model kernel's start event: recorded by model_async right before its launch, after
 // any host-side preparation (lane tables are built on first use), when c.time_model is set.
 int mark_model_start(DevCtx& c, cudaStream_t st) {
@@ -580,6 +600,10 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
     a.out0 = o0;
     a.out1 = o1;
     a.out2 = o2;
+    a.h0 = c.hm[0];  // (set by the caller for this launch only)
+    a.h1 = c.hm[1];
+    a.h2 = c.hm[2];
+    c.hm[0] = c.hm[1] = c.hm[2] = nullptr;
     a.serial_rho = mm1_serial_rho();
     a.near_cap = g_near_cap;
     if (g_hw_counters) {
@@ -1169,15 +1193,18 @@ int wlp_run_shard(int model, const wlp_params* p, int mode, uint64_t master_seed
         o1 = c->outs.p + r_count;
         o2 = c->outs.p + 2 * r_count;
     }
+    double* mirror[3];
+    const bool mirrored = !out_on_device && host_mirrors(*c, model, out0, out1, out2, mirror);
     std::vector<int64_t> rej(rejected, rejected + n_rejected);
     WLP_TRY(seed_async(*c, master_from_seed(master_seed), r_begin, r_count, rej, c->seeds.p, st,
                        walk_planes(*c, model, mode, *p, r_count)));
     int grid = 0;
     c->time_model = report != nullptr;
+    if (mirrored) std::copy(mirror, mirror + 3, c->hm);
     WLP_TRY(model_async(*c, model, *p, mode, tlp_block_size, c->seeds.p, r_count, o0, o1, o2, st, grid));
     c->time_model = false;
     if (report) WLP_CUDA(cudaEventRecord(c->ev1, st));
-    if (!out_on_device) {
+    if (!out_on_device && !mirrored) {
         WLP_CUDA(cudaMemcpyAsync(out0, o0, r_count * 8, cudaMemcpyDeviceToHost, st));
         if (model == WLP_MODEL_MM1) {
             WLP_CUDA(cudaMemcpyAsync(out1, o1, r_count * 8, cudaMemcpyDeviceToHost, st));
@@ -1223,6 +1250,8 @@ int wlp_run(int model, const wlp_params* p, int mode, uint64_t master_seed, int 
         o2 = c->outs.p + 2 * R;
     }
     const Taus master = master_from_seed(master_seed);
+    double* mirror[3];
+    const bool mirrored = !out_on_device && host_mirrors(*c, model, out0, out1, out2, mirror);
     std::vector<int64_t> rej;
     int grid = 0;
     for (;;) {
@@ -1230,6 +1259,7 @@ int wlp_run(int model, const wlp_params* p, int mode, uint64_t master_seed, int 
         // re-run when two special candidates actually share a key.
         WLP_TRY(seed_async(*c, master, 0, R, rej, c->seeds.p, st, walk_planes(*c, model, mode, *p, R)));
         c->time_model = report != nullptr;
+        if (mirrored) std::copy(mirror, mirror + 3, c->hm);
         WLP_TRY(model_async(*c, model, *p, mode, tlp_block_size, c->seeds.p, R, o0, o1, o2, st, grid));
         c->time_model = false;
         if (report) WLP_CUDA(cudaEventRecord(c->ev1, st));
@@ -1248,7 +1278,7 @@ int wlp_run(int model, const wlp_params* p, int mode, uint64_t master_seed, int 
             WLP_TRY(ci_device(*c, d, R, level, &ci[k], st));
         }
     }
-    if (!out_on_device) {
+    if (!out_on_device && !mirrored) {
         WLP_CUDA(cudaMemcpyAsync(out0, o0, R * 8, cudaMemcpyDeviceToHost, st));
         if (model == WLP_MODEL_MM1) {
             WLP_CUDA(cudaMemcpyAsync(out1, o1, R * 8, cudaMemcpyDeviceToHost, st));

@@ -402,6 +402,35 @@ def test_mm1_pipeline_lanes_and_division_modes(gpu, port, lanes, lam, mu, n):
         assert np.array_equal(run.outputs[name], want[name]), name
 
 
+@pytest.mark.parametrize("model,kw", [(0, dict(replications=300_000, draws=100)),
+                                      (1, dict(replications=200_000, clients=64)),
+                                      (2, dict(replications=500_000, steps=100, chunks=9)),
+                                      (2, dict(replications=50_000, steps=100, chunks=9)),
+                                      (1, dict(replications=700, clients=300))])
+@pytest.mark.parametrize("mode", [1, 2])
+def test_host_outputs_pinned_mirrors_and_pageable_copies(gpu, port, model, kw, mode):
+    # outputs into pinned host memory are stored there by the model kernel as they are
+    # produced (no copy after the run); pageable host arrays keep the device buffer and the
+    # copy. Both equal the reference, through run_model (wlp_run) and run_shard.
+    import torch
+
+    p = gpu.ModelParams(**kw)
+    want = port.run_model(model, oracle.params_from(p), 404)
+    names = oracle.OUTPUTS[model]
+    pinned = [torch.zeros(p.replications, dtype=torch.float64, pin_memory=True) for _ in names]
+    gpu.run_model_into(gpu.ModelKind(model), p, gpu.ExecutionMode(mode), 404, [t.numpy() for t in pinned],
+                       on_device=False)
+    pageable = [np.zeros(p.replications) for _ in names]
+    gpu.run_model_into(gpu.ModelKind(model), p, gpu.ExecutionMode(mode), 404, pageable, on_device=False)
+    shard = [torch.zeros(p.replications, dtype=torch.float64, pin_memory=True) for _ in names]
+    gpu.run_shard(gpu.ModelKind(model), p, gpu.ExecutionMode(mode), 404, 0, p.replications,
+                  [t.numpy() for t in shard], on_device=False)
+    for k, name in enumerate(names):
+        assert np.array_equal(pinned[k].numpy(), want[name]), ("pinned", name)
+        assert np.array_equal(pageable[k], want[name]), ("pageable", name)
+        assert np.array_equal(shard[k].numpy(), want[name]), ("shard", name)
+
+
 @pytest.mark.parametrize("model", [0, 2])
 @pytest.mark.parametrize("R,n", [(992, 1), (1000, 5), (2500, 257), (2500, 999), (3001, 1000), (1500, 10_000),
                                  (4000, 63), (993, 2049)])
