@@ -764,16 +764,20 @@ def run_devices(model: ModelKind, p: ModelParams, mode: ExecutionMode, master_se
 
 def run_model_into(model: ModelKind, p: ModelParams, mode: ExecutionMode, master_seed: int, outs, *,
                    on_device: bool, stream: Optional[int] = None, tlp_block_size: int = 256,
-                   ci_level: Optional[float] = None):
+                   ci_level: Optional[float] = None, report: Optional[SimReport] = None):
     """Low-level run_model writing into caller buffers (device pointers / torch CUDA tensors
-    when on_device, else host arrays). Returns the list of ConfidenceIntervals when
-    ci_level is given (device reduction), else None."""
+    when on_device, else host arrays; pinned host arrays are written by the kernels
+    directly). Returns the list of ConfidenceIntervals when ci_level is given (device
+    reduction, one synchronisation for the run and every CI), else None."""
     o = [_ptr(x) for x in outs] + [None] * (3 - len(outs))
     nci = len(OUTPUT_NAMES[ModelKind(model)])
     cis = (_CI * nci)() if ci_level is not None else None
+    rep = _Report() if report is not None else None
     _check(_lib.wlp_run(int(model), C.byref(_params(p)), int(mode), master_seed & (2**64 - 1), int(tlp_block_size),
-                        o[0], o[1], o[2], 1 if on_device else 0, stream, None, cis,
-                        float(ci_level or 0.95), None, 0))
+                        o[0], o[1], o[2], 1 if on_device else 0, stream, C.byref(rep) if rep is not None else None,
+                        cis, float(ci_level or 0.95), None, 0))
+    if rep is not None:
+        report.__dict__.update(vars(_report(rep)))
     if cis is None:
         return None
     return [ConfidenceInterval(c.mean, c.half_width, c.level, c.n, bool(c.warn_small_sample)) for c in cis]

@@ -2569,7 +2569,9 @@ constexpr int kStatsBlock = 256;
 constexpr int64_t kStatsSeqMax = 256;
 
 __global__ void __launch_bounds__(kStatsBlock) k_stats(const double* __restrict__ x, int64_t n, int pass,
-                                                       double center, double* __restrict__ partials) {
+                                                       double center, double* __restrict__ partials,
+                                                       const double* __restrict__ center_dev) {
+    if (center_dev) center = *center_dev;  // pass 2 chained on the device (k_stats_fold's mean)
     if (n <= kStatsSeqMax) {  // the reference's naive sequential loop, bit for bit
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             double s = 0.0;
@@ -2613,7 +2615,9 @@ __global__ void __launch_bounds__(kStatsBlock) k_stats(const double* __restrict_
 // chain (~8 cycles per sample) is the cost: ~4 ns per sample (opt-in, wlp_set_stats_order).
 constexpr int kSeqTile = 2048;
 __global__ void __launch_bounds__(kStatsBlock) k_stats_seq(const double* __restrict__ x, int64_t n, int pass,
-                                                           double center, double* __restrict__ partials) {
+                                                           double center, double* __restrict__ partials,
+                                                           const double* __restrict__ center_dev) {
+    if (center_dev) center = *center_dev;
     __shared__ double tile[2][kSeqTile];
     const int64_t tiles = (n + kSeqTile - 1) / kSeqTile;
     double s = 0.0;
@@ -2653,6 +2657,30 @@ __global__ void __launch_bounds__(kStatsBlock) k_stats_seq(const double* __restr
         partials[0] = s;
         partials[1] = 0.0;
     }
+}
+
+// Pass 1's block partials [used][2] folded in block order into (hi, lo) and the mean, on
+// the device (one thread): the same double-double merge, renormalisation and division the
+// host does in stats_device, operation for operation, so pass 2 can follow without a round
+// trip through the host (meta = {hi, lo, mean}).
+__global__ void k_stats_fold(const double* __restrict__ partials, int used, int64_t n, double* __restrict__ meta) {
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    double hi = 0.0, lo = 0.0;
+    for (int b = 0; b < used; ++b) {
+        const double v = partials[2 * b];
+        const double sm = __dadd_rn(hi, v);
+        const double bb = __dsub_rn(sm, hi);
+        const double err = __dadd_rn(__dsub_rn(hi, __dsub_rn(sm, bb)), __dsub_rn(v, bb));
+        hi = sm;
+        lo = __dadd_rn(lo, err);
+        lo = __dadd_rn(lo, partials[2 * b + 1]);
+    }
+    const double t = __dadd_rn(hi, lo);
+    lo = __dsub_rn(lo, __dsub_rn(t, hi));
+    hi = t;
+    meta[0] = hi;
+    meta[1] = lo;
+    meta[2] = __ddiv_rn(__dadd_rn(hi, lo), static_cast<double>(n));
 }
 
 size_t tlp_mm1_smem(int block) { return 256 * 8 + static_cast<size_t>((block + 31) / 32) * sizeof(TlpMm1Warp); }
@@ -3058,13 +3086,18 @@ cudaError_t launch_plan(int model, int mode, const PlanArgs& a, const uint32_t* 
 }
 
 cudaError_t launch_stats(const double* x, int64_t n, int pass, double center, double* partials, int grid,
-                         cudaStream_t st, bool reference_order) {
+                         cudaStream_t st, bool reference_order, const double* center_dev) {
     if (reference_order && n > kStatsSeqMax) {
-        k_stats_seq<<<1, kStatsBlock, 0, st>>>(x, n, pass, center, partials);
+        k_stats_seq<<<1, kStatsBlock, 0, st>>>(x, n, pass, center, partials, center_dev);
         return cudaGetLastError();
     }
     if (n <= kStatsSeqMax) grid = 1;
-    k_stats<<<grid, kStatsBlock, 0, st>>>(x, n, pass, center, partials);
+    k_stats<<<grid, kStatsBlock, 0, st>>>(x, n, pass, center, partials, center_dev);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stats_fold(const double* partials, int used, int64_t n, double* meta, cudaStream_t st) {
+    k_stats_fold<<<1, 32, 0, st>>>(partials, used, n, meta);
     return cudaGetLastError();
 }
 

@@ -246,6 +246,10 @@ cudaError_t launch_exponentials(const double* u, int64_t n, double rate, double*
 // about 0, pass 2 about `center`). n <= 256 or reference_order: one partial, the
 // reference's sequential sum (models.cpp:104-109) bit for bit.
 cudaError_t launch_stats(const double* x, int64_t n, int pass, double center, double* partials,
-                         int grid, cudaStream_t st, bool reference_order = false);
+                         int grid, cudaStream_t st, bool reference_order = false,
+                         const double* center_dev = nullptr);
+// Folds pass-1 partials [used][2] into meta = {hi, lo, mean} on the device (the host's
+// stats_device merge, bit for bit), so pass 2 (center_dev = meta + 2) needs no round trip.
+cudaError_t launch_stats_fold(const double* partials, int used, int64_t n, double* meta, cudaStream_t st);
 
 }  // namespace wlp

@@ -849,6 +849,68 @@ int ci_device(DevCtx& c, const double* d_x, int64_t n, double level, wlp_ci* ci,
     return ci_from_stats(&s, level, ci);
 }
 
+// All outputs' confidence intervals with one host synchronisation: per output, pass 1, the
+// device fold of its partials (mean on the device), pass 2 about that mean; one copy of
+// every output's {hi, lo, mean} and pass-2 partials; then the host merge of pass 2 as in
+// stats_device. Same numbers as ci_device, bit for bit. ci_enqueue launches; the caller
+// synchronises the stream (e.g. with the specials read-back) and calls ci_finish.
+struct CiPlan {
+    int nout = 0, grid = 1, used = 1;
+    int64_t n = 0;
+    double level = 0.95;
+    std::vector<double> host;  // per output: meta[4] then pass-2 partials [2 * grid]
+};
+
+int ci_enqueue(DevCtx& c, const double* const* d_x, int nout, int64_t n, double level, CiPlan& plan,
+               cudaStream_t st) {
+    if (n < 2) return fail(WLP_EDOMAIN, "confidence_interval: need at least 2 samples");
+    if (!(level > 0.0 && level < 1.0)) return fail(WLP_EDOMAIN, "confidence_interval: level outside (0,1)");
+    plan.nout = nout;
+    plan.n = n;
+    plan.level = level;
+    plan.grid = std::max(1, std::min<int>(c.sms * 4, static_cast<int>((n + 255) / 256)));
+    const bool seq = g_stats_order == 1;
+    plan.used = n <= 256 || seq ? 1 : plan.grid;
+    const int64_t per = 4 + 4 * static_cast<int64_t>(plan.grid);  // meta[4], pass 1 [2g], pass 2 [2g]
+    WLP_CUDA(c.partials.ensure(per * nout));
+    for (int k = 0; k < nout; ++k) {
+        double* base = c.partials.p + k * per;
+        double* p1 = base + 4;
+        double* p2 = base + 4 + 2 * plan.grid;
+        WLP_CUDA(launch_stats(d_x[k], n, 1, 0.0, p1, plan.grid, st, seq));
+        WLP_CUDA(launch_stats_fold(p1, plan.used, n, base, st));
+        WLP_CUDA(launch_stats(d_x[k], n, 2, 0.0, p2, plan.grid, st, seq, base + 2));
+    }
+    plan.host.resize(static_cast<size_t>(per * nout));
+    WLP_CUDA(cudaMemcpyAsync(plan.host.data(), c.partials.p, plan.host.size() * 8, cudaMemcpyDeviceToHost, st));
+    return WLP_OK;
+}
+
+int ci_finish(const CiPlan& plan, wlp_ci* ci) {  // after the stream is synchronised
+    const int64_t per = 4 + 4 * static_cast<int64_t>(plan.grid);
+    for (int k = 0; k < plan.nout; ++k) {
+        const double* base = plan.host.data() + k * per;
+        const double* p2 = base + 4 + 2 * plan.grid;
+        wlp_stats s{};
+        s.n = plan.n;
+        s.sum_hi = base[0];
+        s.sum_lo = base[1];
+        s.center = base[2];
+        double hi = 0.0, lo = 0.0;
+        for (int b = 0; b < plan.used; ++b) {
+            dd_add(hi, lo, p2[2 * b]);
+            lo += p2[2 * b + 1];
+        }
+        const double t = hi + lo;
+        lo = lo - (t - hi);
+        hi = t;
+        s.ss_hi = hi;
+        s.ss_lo = lo;
+        WLP_TRY(ci_from_stats(&s, plan.level, &ci[k]));
+    }
+    return WLP_OK;
+}
+
 void copy_warning(const std::string& w, char* buf, int cap) {
     if (!buf || cap <= 0) return;
     const size_t n = std::min<size_t>(w.size(), static_cast<size_t>(cap - 1));
@@ -1254,6 +1316,7 @@ int wlp_run(int model, const wlp_params* p, int mode, uint64_t master_seed, int 
     const bool mirrored = !out_on_device && host_mirrors(*c, model, out0, out1, out2, mirror);
     std::vector<int64_t> rej;
     int grid = 0;
+    CiPlan plan;
     for (;;) {
         // Seeding and the model run back to back; the spacing check below only forces a
         // re-run when two special candidates actually share a key.
@@ -1263,6 +1326,10 @@ int wlp_run(int model, const wlp_params* p, int mode, uint64_t master_seed, int 
         WLP_TRY(model_async(*c, model, *p, mode, tlp_block_size, c->seeds.p, R, o0, o1, o2, st, grid));
         c->time_model = false;
         if (report) WLP_CUDA(cudaEventRecord(c->ev1, st));
+        if (ci) {  // both statistics passes of every output, behind the model, before the sync
+            const double* d[3] = {o0, o1, o2};
+            WLP_TRY(ci_enqueue(*c, d, n_outputs(model), R, level, plan, st));
+        }
         std::vector<SpecialRec> sp;
         int64_t nt = 0;
         WLP_TRY(read_specials(*c, st, sp, nt));
@@ -1272,12 +1339,7 @@ int wlp_run(int model, const wlp_params* p, int mode, uint64_t master_seed, int 
         if (next == rej) break;
         rej.swap(next);
     }
-    if (ci) {
-        for (int k = 0; k < n_outputs(model); ++k) {
-            const double* d = k == 0 ? o0 : k == 1 ? o1 : o2;
-            WLP_TRY(ci_device(*c, d, R, level, &ci[k], st));
-        }
-    }
+    if (ci) WLP_TRY(ci_finish(plan, ci));
     if (!out_on_device && !mirrored) {
         WLP_CUDA(cudaMemcpyAsync(out0, o0, R * 8, cudaMemcpyDeviceToHost, st));
         if (model == WLP_MODEL_MM1) {

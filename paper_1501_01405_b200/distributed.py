@@ -119,6 +119,11 @@ def run_sharded(model: ModelKind, R: int, runner: Callable, stats: Callable, *, 
       (pass 1: n and sum; pass 2: centred sum of squares about `center`).
     """
     comm = comm or _Comm()
+    if comm.world == 1 and getattr(runner, "whole", None) is not None:
+        # one rank: the whole run and every CI in one call (one synchronisation; the
+        # statistics' second pass follows the first on the device)
+        outputs, cis = runner.whole(level)
+        return ShardResult(outputs, 0, R, cis, [], 1)
     begin, count = shard_range(R, comm.world, comm.rank)
     nout = len(OUTPUT_NAMES[ModelKind(model)])
     rejected: List[int] = []
@@ -195,6 +200,19 @@ def gpu_runner(model: ModelKind, p, mode, master_seed: int, stream: Optional[int
             kernel_ms.append(rep.kernel_ms)
         return [o[:count] for o in outs], specials
 
+    def whole(level: float):  # single-rank run (run_sharded's shortcut)
+        from . import run_model_into
+
+        outs = cache.setdefault(p.replications, [torch.empty(max(p.replications, 1), dtype=torch.float64,
+                                                             device="cuda") for _ in OUTPUT_NAMES[ModelKind(model)]])
+        rep = SimReport() if kernel_ms is not None else None
+        cis = run_model_into(model, p, mode, master_seed, outs, on_device=True, stream=stream, ci_level=level,
+                             report=rep)
+        if rep is not None:
+            kernel_ms.append(rep.kernel_ms)
+        return [o[: p.replications] for o in outs], cis
+
+    run.whole = whole
     return run
 
 
