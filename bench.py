@@ -504,10 +504,25 @@ def sharded_record(w, D, model: int, p, world: int, comm, stats, stream, steps: 
             "gpu_launches_per_step": 2 + (3 if world == 1 else 2) * nout}
 
 
+def ncu_warp_efficiency() -> dict:
+    """Warp-execution evidence per configuration and mapping from the committed ncu
+    captures of the same kernels (profiles/round2_ncu.json, tools/prof_round2.sh): branch
+    uniformity (smsp__sass_average_branch_targets_threads_uniform.pct) and active threads
+    per warp-instruction. Captured on the B200 with ncu; not measured by this run (ncu
+    replays each kernel ~40 times)."""
+    try:
+        caps = json.loads((ROOT / "profiles" / "round2_ncu.json").read_text())
+    except Exception:
+        return {}
+    return {label: {"kernel": c.get("kernel"), "branch_uniform_pct": c.get("branch_uniform_pct"),
+                    "threads_per_warp_instr": c.get("threads_per_warp_instr"), "issue_pct": c.get("issue_pct")}
+            for label, c in caps.items() if label != "cfg3_seed"}
+
+
 def extras_single_gpu(w, sms, fmax, peak_issue) -> dict:
     import torch
 
-    extras = {}
+    extras = {"ncu_warp_efficiency": ncu_warp_efficiency()}
     cfgs = [("cfg2_pi_1e6x1e4", w.ModelKind.Pi, dict(replications=1_000_000, draws=10_000)),
             ("cfg3_walk_1e5x1e3", w.ModelKind.Walk, dict(replications=100_000, steps=1000, chunks=30)),
             ("cfg4_pi_1e7x1e3", w.ModelKind.Pi, dict(replications=R_CFG4, draws=1000)),
