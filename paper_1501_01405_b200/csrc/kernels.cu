@@ -215,8 +215,8 @@ __device__ __forceinline__ void pi_count(uint32_t& hits, uint32_t a, uint32_t b)
 
 // Hits among `units` consecutive points of a stream (main loop unrolled by 8).
 __device__ __forceinline__ uint32_t pi_hits(Taus& st, uint32_t units) {
-    uint32_t hits = 0, u = 0;
-    for (; u + 8 <= units; u += 8) {
+    uint32_t hits = 0;
+    for (uint32_t it = units >> 3; it; --it) {  // (a count-down: one counter, no bound)
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             uint32_t x, y;
@@ -224,7 +224,7 @@ __device__ __forceinline__ uint32_t pi_hits(Taus& st, uint32_t units) {
             pi_count(hits, x, y);
         }
     }
-    for (; u < units; ++u) {
+    for (uint32_t u = units & 7u; u; --u) {
         uint32_t x, y;
         taus_next2(st, x, y);
         pi_count(hits, x, y);
@@ -240,15 +240,14 @@ __device__ __forceinline__ uint32_t pi_hits(Taus& st, uint32_t units) {
 // The raw sum of q over `units` steps (units < 2^27); dx = (sum + 6*units) / 6.
 __device__ __forceinline__ int walk_q(Taus& st, uint32_t units) {
     int acc = 0;
-    uint32_t u = 0;
-    for (; u + 8 <= units; u += 8) {
+    for (uint32_t it = units >> 3; it; --it) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const int d = static_cast<int>(taus_next_skip1(st) >> 30);
             acc += (((21 - 4 * d) * d) - 29) * d;
         }
     }
-    for (; u < units; ++u) {
+    for (uint32_t u = units & 7u; u; --u) {
         const int d = static_cast<int>(taus_next_skip1(st) >> 30);
         acc += (((21 - 4 * d) * d) - 29) * d;
     }
