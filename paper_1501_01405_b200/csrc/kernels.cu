@@ -2134,8 +2134,10 @@ __device__ __forceinline__ void panel_clients(Queue& q, const PanelWarp& P, int 
 // EXACT: some chunk has a partial panel (n % kPanT != 0), whose draws are predicated so
 // the hand-over state is exact; otherwise lanes draw whole panels unpredicated.
 template <int DIV, bool EXACT>
+// 4 blocks of 8 warps per SM (64 registers, no spills; the compact near list keeps the
+// panel kernel's block at 54 KB of shared memory): config 4 42.4 -> 41.7 ms against 3.
 #ifndef WLP_MM1_MINB
-#define WLP_MM1_MINB 3
+#define WLP_MM1_MINB 4
 #endif
 __global__ void __launch_bounds__(kMm1Block, WLP_MM1_MINB) k_wlp_mm1_pipe_ragged(RepArgs a, PipeSched ps) {
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -2200,16 +2202,14 @@ constexpr size_t kMm1PipeSmem = 256 * 8 + (kMm1Block / 32) * sizeof(PanelWarp);
 // mm1 WLP warp pipeline, single-pass panels with the recursion interleaved (the default
 // for n % 8 == 0). Per lane and panel of kPanT clients:
 // * one pass draws, evaluates the branch-free table path of every exponential and stores
-//   the (a, s) pairs column-major; a near-one draw (1 in 16) also claims a list entry
-//   with a shared-memory atomic (ATOMS) and records {draw, slot}. No per-lane flag masks,
-//   no lane scan, no draw staging: ~4 instructions per draw of bookkeeping instead of ~8;
-// * the warp then evaluates the list (one pass of the near-one polynomial across the
-//   lanes, straight into the slots). More than kNearCap near-ones (never at random draws)
-//   redo the panel from the stream state saved before it, each lane fixing its own;
-// * the Lindley recursion of panel p runs client by client interleaved with the fill of
-//   panel p + 1 into the same slots (each slot is read by the recursion before its own
-//   lane overwrites it), so the recursion's dependent DADD chain overlaps independent
-//   draw / log work instead of idling the warp.
+//   the (a, s) pairs column-major; the draws go to a staging row (one STS.128 per two
+//   clients) and their near-one flags into a per-lane bit mask (two integer ops a draw);
+// * each lane claims room for its near-ones (1 in 16) in the panel's list with one
+//   shared-memory atomic and writes one compact entry {lane, bit} per near draw (a loop
+//   over the set bits of its mask only); the warp then evaluates the
+//   list (one pass of the near-one polynomial across the lanes, straight into the slots).
+//   More than the list capacity (never at random draws) makes each lane fix its own from
+//   the staged draws;
 // S lanes per replication (32, or 8: four pipelines per warp, 4x longer steps; mm1 has
 // no wrap, its queue state is sequential, so the S-1 step drain remains: ~1 % at config 4).
 // ---------------------------------------------------------------------------------
@@ -2218,7 +2218,8 @@ constexpr int kNearCap2 = 128;  // list entries per panel (expected 32 of 512 dr
 struct Mm1Pan {
     double2 v[kPanT][32];     // (a, s) of client c of lane l
     uint4 dr[kPanD / 4][32];  // the panel's draws: draws 4q..4q+3 of lane l at dr[q][l]
-    uint2 nl[kNearCap2];      // near list: {draw, slot (double index into v)}
+    uint32_t nl[kNearCap2];   // near list: lane << 5 | mask bit (draw 15 - bit of that lane)
+    uint32_t cnt, pad_[3];    // list entries claimed (zero between panels)
 };
 constexpr size_t kMm1Pipe2Smem = 256 * 8 + (kMm1Block / 32) * sizeof(Mm1Pan);
 
@@ -2243,40 +2244,68 @@ __device__ __forceinline__ void fill_pair(Taus& st, int c, int lane, uint32_t& m
 }
 
 // The near-one draws of the panel just filled, into their slots. Each lane's flag mask m
-// (~1 set bit of 16) is turned into list entries at the lane's place from one lane scan
-// of the counts (a loop over the set bits only); the warp then evaluates the list in one
-// pass across the lanes. More than `cap` near-ones (never at random draws: 128 of 512)
+// (~1 set bit of 16) is turned into list entries at the place one atomic on the panel's
+// counter gives the lane (WLP_NEAR_ATOMS=0: a lane scan of the counts; config 4 42.14 vs
+// 41.83 ms); the warp then evaluates the list in one pass across the lanes. More than `cap` near-ones (never at random draws: 128 of 512)
 // fall back to each lane fixing its own from the staged draws. Idle lanes (on = false)
 // list nothing.
+#ifndef WLP_NEAR_ATOMS
+#define WLP_NEAR_ATOMS 1
+#endif
 template <int DIV>
 __device__ __forceinline__ void fix_near(Mm1Pan& W, int lane, bool on, uint32_t m, double lambda, double mu,
                                          double inv_l, double inv_m, uint32_t cap) {
     if (!on) m = 0u;
-    const int c = __popc(m);
-    int incl = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += v;
-    }
-    const uint32_t total = static_cast<uint32_t>(__shfl_sync(kFull, incl, 31));
+    const uint32_t c = static_cast<uint32_t>(__popc(m));
     double* v = reinterpret_cast<double*>(&W.v[0][0]);
     const uint32_t* dr = reinterpret_cast<const uint32_t*>(&W.dr[0][0]);
+#if WLP_NEAR_ATOMS
+    // Each lane claims its c entries with one shared-memory atomic on the panel counter
+    // (lanes with no near-one skip it); the entries' order depends on the atomics' order,
+    // the values do not. Five dependent shuffles of a lane scan cost more.
+    __syncwarp();  // the previous panel's list reads and counter reset are done
+    uint32_t pos = 0;
+    if (c) pos = atomicAdd(&W.cnt, c);
+    const bool fits = pos + c <= cap;  // (false on some lane => the total is over cap)
+#else
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += t;
+    }
+    const uint32_t pos = incl - c;
+    const bool fits = incl <= cap;
     __syncwarp();
+#endif
+    const uint32_t m0 = m;
+    if (fits) {
+        // the set-bit loop runs as often as the lane with the most near-ones (~3 times a
+        // panel), so each pass is kept to FLO, the bit clear, the entry and its store
+        uint32_t* e = W.nl + pos;
+        const uint32_t tag = static_cast<uint32_t>(lane) << 5;
+        while (m) {
+            const uint32_t b = 31u - static_cast<uint32_t>(__clz(m));
+            m ^= 1u << b;
+            *e++ = tag | b;
+        }
+    }
+    __syncwarp();
+#if WLP_NEAR_ATOMS
+    const uint32_t total = W.cnt;
+#else
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+#endif
     if (total <= cap) {
-        int pos = incl - c;
-        while (m) {  // this lane's near draws (bit 15 - j: draw j)
-            const int j = __clz(m) - 16;
-            m &= ~(0x8000u >> j);
-            W.nl[pos++] = make_uint2(dr[(j >> 2) * 128 + lane * 4 + (j & 3)], static_cast<uint32_t>(pan_slot(j, lane)));
-        }
-        __syncwarp();
         for (uint32_t k = lane; k < total; k += 32) {
-            const uint2 it = W.nl[k];
-            const double e = it.x == 0u ? -0.0 : -log_near_one_dev(one_minus_u32_dev(it.x));
-            v[it.y] = scale_slot<DIV>(e, it.y & 1u, lambda, mu, inv_l, inv_m);
+            const uint32_t it = W.nl[k], l = it >> 5, j = 15u - (it & 31u);
+            const uint32_t n = dr[(j >> 2) * 128 + l * 4 + (j & 3)];
+            const uint32_t slot = static_cast<uint32_t>(pan_slot(static_cast<int>(j), static_cast<int>(l)));
+            const double e = n == 0u ? -0.0 : -log_near_one_dev(one_minus_u32_dev(n));
+            v[slot] = scale_slot<DIV>(e, slot & 1u, lambda, mu, inv_l, inv_m);
         }
-    } else {
+    } else {  // (never at random draws) each lane fixes its own near-ones from the staging rows
+        m = m0;
         while (m) {
             const int j = __clz(m) - 16;
             m &= ~(0x8000u >> j);
@@ -2286,6 +2315,9 @@ __device__ __forceinline__ void fix_near(Mm1Pan& W, int lane, bool on, uint32_t 
         }
     }
     __syncwarp();
+#if WLP_NEAR_ATOMS
+    if (lane == 0) W.cnt = 0u;  // (ordered before the next panel's atomics by its first sync)
+#endif
 }
 
 // One pipeline step of a lane: np panels of its chunk (np >= 1, warp-uniform). Panel p's
@@ -2323,6 +2355,7 @@ __global__ void __launch_bounds__(kMm1Block, WLP_MM1_MINB) k_wlp_mm1_pipe(RepArg
     double* logtab = reinterpret_cast<double*>(smraw);
     Mm1Pan& W = reinterpret_cast<Mm1Pan*>(logtab + 256)[threadIdx.x >> 5];
     stage_log_table(logtab);
+    if ((threadIdx.x & 31) == 0) W.cnt = 0u;
     __syncthreads();
     pdl_wait();
     const int lane = threadIdx.x & 31, g = lane / S, pos = lane % S;
