@@ -140,12 +140,15 @@ int wlp_set_hw_counters(int enable);
 int wlp_set_wlp_variant(int variant);
 
 /* Tuning / test hook for later calls on this thread: lanes per replication S of the warp
- * pipelines (pi / walk per replication: variant 2, automatic at large R; walk bitsliced:
- * lanes per group of 32 replications; mm1: 8, 16 or 32). 32 = the whole warp is one
- * pipeline; 16, 8 or 4 = 32/S pipelines side by side in the warp, every replication still
- * passing through lanes of one warp only, split into S chunks (longer steps for the same
- * hand-over work). 0 = automatic: pi / walk the most lanes that give every lane >= 250
- * units per step; mm1 8 below 2,048 clients, else 32. Outputs are identical. */
+ * pipelines (pi / walk per replication: 2, 4, 8, 16 or 32; walk bitsliced: lanes per
+ * group of 32 replications, 4 to 32; mm1: 2 to 32). 32 = the whole warp is one pipeline;
+ * 16 .. 2 = 32/S pipelines side by side in the warp, every replication still passing
+ * through lanes of one warp only, split into S chunks (longer steps for the same
+ * hand-over work). 0 = automatic: S = 2 when the run fills the grid with two-lane
+ * pipelines (pi / walk with their wrap replications; mm1 >= 4 replications a pipeline);
+ * else pi / walk the most lanes that give every lane >= 250 units per step, mm1 8 below
+ * 2,048 clients and 32 above; the bitsliced walk the >= 250-steps rule with S >= 4.
+ * Outputs are identical. */
 int wlp_set_pipe_lanes(int lanes);
 
 /* Test hook (this thread): near-one list entries per panel of the mm1 warp pipeline, a

@@ -622,7 +622,7 @@ class wlp_variant:
 
 
 class pipe_lanes:
-    """Context manager: lanes per replication of the pi / walk warp pipeline (8, 16, 32;
+    """Context manager: lanes per replication of the warp pipelines (2, 4, 8, 16, 32;
     0 automatic) for calls on this thread (wlp_set_pipe_lanes)."""
 
     def __init__(self, lanes: int):

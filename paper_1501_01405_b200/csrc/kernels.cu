@@ -742,8 +742,8 @@ struct PipeCtl {
     long long cur, cend;  // the warp's current group of replications
     int more;             // the warp still grabs
     int nemit;            // finished replications waiting in the result buffer
-    int drain[8];         // per pipeline: takes no more grabbed replications
-    int wraps[8];         // per pipeline: wrap replications still to feed
+    int drain[16];        // per pipeline: takes no more grabbed replications
+    int wraps[16];        // per pipeline: wrap replications still to feed
 };
 
 template <int MODEL, bool WIDE, int S, bool WRAP>
@@ -2890,7 +2890,9 @@ cudaError_t launch_wlp(int model, const RepArgs& a, const uint32_t* lane_tab, co
 template <int MODEL, bool WIDE>
 void launch_wlp_pipe_m(const RepArgs& a, const PipeSched& s, const uint32_t* wrap_tab, int grid, cudaStream_t st) {
     auto go = [&](auto kernel) { launch_ex(kernel, grid, kWlpBlock, 0, st, a, s, wrap_tab); };
-    if (s.S == 4)
+    if (s.S == 2)
+        go(k_wlp_pipe<MODEL, WIDE, 2, true>);
+    else if (s.S == 4)
         go(k_wlp_pipe<MODEL, WIDE, 4, true>);
     else if (s.S == 8)
         go(k_wlp_pipe<MODEL, WIDE, 8, true>);
@@ -2905,7 +2907,7 @@ void launch_wlp_pipe_m(const RepArgs& a, const PipeSched& s, const uint32_t* wra
 cudaError_t launch_wlp_pipe(int model, const RepArgs& a, const PipeSched& s, const uint32_t* wrap_tab, int grid,
                             cudaStream_t st) {
     if (a.count <= 0) return cudaSuccess;
-    if (s.S != 32 && (!wrap_tab || (s.S != 16 && s.S != 8 && s.S != 4))) return cudaErrorInvalidValue;
+    if (s.S != 32 && (!wrap_tab || (s.S != 16 && s.S != 8 && s.S != 4 && s.S != 2))) return cudaErrorInvalidValue;
     // 32-bit sums hold pi's hits (< n) and the walk's raw q sum (|sum| <= 12 n)
     const bool wide = a.n >= (int64_t(1) << 27) || a.count >= (int64_t(1) << 31);
     if (model == 0)
@@ -2925,7 +2927,11 @@ cudaError_t launch_wlp_mm1_pipe(const RepArgs& a, const PipeSched& ps, int grid,
         };
         auto by_s = [&](auto d) {
             constexpr int D = decltype(d)::value;
-            if (ps.S == 8)
+            if (ps.S == 2)
+                go(k_wlp_mm1_pipe<D, 2>);
+            else if (ps.S == 4)
+                go(k_wlp_mm1_pipe<D, 4>);
+            else if (ps.S == 8)
                 go(k_wlp_mm1_pipe<D, 8>);
             else if (ps.S == 16)
                 go(k_wlp_mm1_pipe<D, 16>);

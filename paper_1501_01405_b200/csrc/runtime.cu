@@ -652,11 +652,15 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
                 std::clamp<int64_t>(count / (static_cast<int64_t>(grid_out) * (kMm1Block / 32) * 32), 1, 32));
             g_last_kernel = "k_wlp_mm1_pipe";
             WLP_TRY(mark_model_start(c, st));
-            // whole panels at every step (n % 8 == 0): S lanes per replication, 8 unless a
-            // lane's chunk is long at 32 (each step then interleaves more panels)
+            // whole panels at every step (n % 8 == 0). S lanes per replication: 2 when
+            // every pipeline of the grid gets >= 4 replications (one drain step instead of
+            // S - 1, and the least hand-over: config 4 41.87 ms at S = 8, 41.31 at S = 2);
+            // on smaller runs 8, or 32 when a lane's chunk is long (more panels a step)
             int S = g_pipe_lanes;
-            if (S == 0) S = a.n >= 32 * kMm1PanelT * 8 ? 32 : 8;
-            if (S < 8) S = 8;  // (the mm1 pipeline comes in 8, 16 and 32 lanes)
+            if (S == 0) {
+                const int64_t pipes2 = static_cast<int64_t>(grid_out) * (kMm1Block / 32) * 16;
+                S = count >= 4 * pipes2 ? 2 : (a.n >= 32 * kMm1PanelT * 8 ? 32 : 8);
+            }
             int G = kMm1PanelT;
             if (a.n % kMm1PanelT != 0 || a.n < static_cast<int64_t>(S) * kMm1PanelT) {  // the ragged kernel
                 S = 32;
@@ -694,6 +698,7 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
         // hand-over of 120 words per step then costs ~1 % instead of ~9 % at S = 32)
         int S = g_pipe_lanes;
         if (S == 0) S = a.n >= 32 * 250 ? 32 : (a.n >= 16 * 250 ? 16 : (a.n >= 8 * 250 ? 8 : 4));
+        if (S < 4) S = 4;  // (the bitsliced pipeline comes in 4, 8, 16 and 32 lanes)
         const int64_t blocks = std::clamp<int64_t>((std::max<int64_t>(1, groups / 64) + 1) / 2, 1, cap);
         const int64_t wpw = pipe_wrap_per_warp(S);
         const bool wrap = groups >= wpw * kBsW * blocks;
@@ -715,10 +720,17 @@ int model_async(DevCtx& c, int model, const wlp_params& p, int mode, int tlp_blo
         // ~31-39. The pipeline has none; with the wrap (every S-lane pipeline owns S - 1
         // replications beyond the ones its warp grabs) it has no fill or drain either;
         // without it a 31-step triangle per warp idles.
-        int S = g_pipe_lanes;
-        if (S == 0) S = a.n >= 32 * 250 ? 32 : (a.n >= 16 * 250 ? 16 : (a.n >= 8 * 250 ? 8 : 4));
-        const int64_t wpw = pipe_wrap_per_warp(S);
         int pgrid = static_cast<int>(std::min<int64_t>(grid_out, static_cast<int64_t>(c.sms) * c.pipe_bps));
+        // S lanes per replication: 2 (each replication two chunks, one hand-over; config 4
+        // pi 10.89 ms vs 11.06 at S = 4, config 2 10.81 vs 11.18 at S = 32) when the run
+        // fills the grid with wrapped two-lane pipelines; on smaller runs the most lanes that
+        // give every lane >= 250 units per step
+        int S = g_pipe_lanes;
+        if (S == 0) {
+            S = a.n >= 32 * 250 ? 32 : (a.n >= 16 * 250 ? 16 : (a.n >= 8 * 250 ? 8 : 4));
+            if (count >= 2 * pipe_wrap_per_warp(2) * static_cast<int64_t>(pgrid) * (kWlpBlock / 32)) S = 2;
+        }
+        const int64_t wpw = pipe_wrap_per_warp(S);
         bool wrap = count >= 2 * wpw * static_cast<int64_t>(pgrid) * (kWlpBlock / 32);
         if (!wrap && (g_wlp_variant == 2 || S < 32) && count >= 2 * wpw * (kWlpBlock / 32)) {
             // fewer warps, each with its wrap replications (a forced pipeline on a small run)
@@ -946,8 +958,8 @@ int wlp_debug_set_near_cap(int cap) {
 }
 
 int wlp_set_pipe_lanes(int lanes) {
-    if (lanes != 0 && lanes != 4 && lanes != 8 && lanes != 16 && lanes != 32)
-        return fail(WLP_EDOMAIN, "pipeline lanes per replication must be 0 (auto), 4, 8, 16 or 32");
+    if (lanes != 0 && lanes != 2 && lanes != 4 && lanes != 8 && lanes != 16 && lanes != 32)
+        return fail(WLP_EDOMAIN, "pipeline lanes per replication must be 0 (auto), 2, 4, 8, 16 or 32");
     g_pipe_lanes = lanes;
     return WLP_OK;
 }

@@ -54,7 +54,7 @@ def test_kernel_variant_knobs_and_last_kernel():
         with pytest.raises(w.DomainError):
             with w.tlp_variant(bad):
                 pass
-    for bad in (-1, 2, 12, 64):
+    for bad in (-1, 1, 3, 12, 64):
         with pytest.raises(w.DomainError):
             with w.pipe_lanes(bad):
                 pass

@@ -388,7 +388,7 @@ def test_mm1_pipeline_near_list_overflow_redo(gpu, port, cap, lanes):
         assert np.array_equal(run.outputs[name], want[name]), name
 
 
-@pytest.mark.parametrize("lanes", [8, 16, 32])
+@pytest.mark.parametrize("lanes", [2, 4, 8, 16, 32])
 @pytest.mark.parametrize("lam,mu,n", [(0.5, 1.0, 1000), (0.3, 0.9, 512), (0.9, 1.0, 2048), (1.7, 1.0, 64),
                                       (0.4, 0.4, 800), (0.1, 1e-3, 96)])
 def test_mm1_pipeline_lanes_and_division_modes(gpu, port, lanes, lam, mu, n):
@@ -434,7 +434,7 @@ def test_host_outputs_pinned_mirrors_and_pageable_copies(gpu, port, model, kw, m
 @pytest.mark.parametrize("model", [0, 2])
 @pytest.mark.parametrize("R,n", [(992, 1), (1000, 5), (2500, 257), (2500, 999), (3001, 1000), (1500, 10_000),
                                  (4000, 63), (993, 2049)])
-@pytest.mark.parametrize("lanes", [32, 16, 8, 4])
+@pytest.mark.parametrize("lanes", [32, 16, 8, 4, 2])
 def test_wrapped_pipeline_rotating_chunks_vs_oracle(gpu, port, model, R, n, lanes):
     # the pi / walk warp pipeline with rotating chunk lengths (PipeSched: G-unit blocks, a
     # remainder of blocks spread over the phases, a sub-block tail at phase 31) and the wrap
