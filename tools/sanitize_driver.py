@@ -41,12 +41,12 @@ for mode in (E.Tlp, E.Wlp):
 # round 2: the wrapped pipelines at every lanes-per-replication S (forced at small R: fewer
 # warps, each with its wrap replications), the single-pass mm1 pipeline (mu = 1 and a
 # general rate; its near-one overflow redo forced by a small list capacity), the bitsliced
-# walk pipeline with wrap groups at S = 4 / 8 / 32
-for lanes in (4, 8, 16, 32):
+# walk pipeline with wrap groups at S = 4 / 8 / 32; the two-lane pipelines (S = 2)
+for lanes in (2, 4, 8, 16, 32):
     with w.wlp_variant(2), w.pipe_lanes(lanes):
         for model in (M.Pi, M.Walk):
             w.run_model(model, w.ModelParams(replications=1100, draws=999, steps=999), E.Wlp, master_seed=11)
-for lanes in (8, 32):
+for lanes in (2, 8, 32):
     for cap in (128, 4):
         with w.wlp_variant(2), w.pipe_lanes(lanes), w.near_cap(cap):
             w.run_model(M.Mm1, w.ModelParams(replications=1100, clients=512), E.Wlp, master_seed=11)
