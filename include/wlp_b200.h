@@ -264,7 +264,9 @@ int wlp_run_streams(int model, const wlp_params* p, int mode, const uint32_t* s,
  * wlp_seed_streams), runs the model in `mode`, writes per-replication outputs.
  * Reports the shard's special candidates so the caller can check spacing collisions
  * across shards and re-run with a rejection list in the (astronomically rare) case of
- * one. Outputs on device: asynchronous unless report/specials are requested. */
+ * one. Outputs on device without a report: the call returns once the seeding has
+ * reported its special candidates, with the model kernel still running on `stream`
+ * (stream-ordered like any CUDA call: read the outputs on `stream` or after syncing it). */
 int wlp_run_shard(int model, const wlp_params* p, int mode, uint64_t master_seed,
                   int tlp_block_size, int64_t r_begin, int64_t r_count, const int64_t* rejected,
                   int64_t n_rejected, double* out0, double* out1, double* out2,
@@ -275,7 +277,8 @@ int wlp_run_shard(int model, const wlp_params* p, int mode, uint64_t master_seed
  * outputs, optional report, and optional device-side confidence intervals of every
  * output (ci array of 1 or 3 entries, NULL to skip) at `level`. The outputs-on-host
  * form is the reference-facing call (e2e); warning text as in build_kernel
- * (models.cpp:294-299). */
+ * (models.cpp:294-299). Outputs on device without report or ci: returns once the seeding
+ * has reported, the model kernel still running on `stream` (as wlp_run_shard). */
 int wlp_run(int model, const wlp_params* p, int mode, uint64_t master_seed, int tlp_block_size,
             double* out0, double* out1, double* out2, int out_on_device, void* stream,
             wlp_report* report, wlp_ci* ci, double level, char* warn, int warn_cap);

@@ -558,9 +558,9 @@ __global__ void __launch_bounds__(kSeedBlock) k_seed(SeedArgs a) {
         if (threadIdx.x == 0) {
             __threadfence();
             if (atomicAdd(a.done, 1u) == gridDim.x - 1) {
-                __threadfence();
-                *reinterpret_cast<volatile unsigned long long*>(a.report) = atomicAdd(a.n_special, 0ull);
+                __threadfence_system();  // the specials list before the count the host polls
                 *a.done = 0u;
+                *reinterpret_cast<volatile unsigned long long*>(a.report) = atomicAdd(a.n_special, 0ull);
             }
         }
     }

@@ -93,6 +93,8 @@ struct DevBuf {
 constexpr int64_t kSpecialCap = 4096;
 constexpr int kMaxLaneTabs = 64;
 
+constexpr unsigned long long kCountPending = ~0ull;  // mapped count word before the seeding stores it
+
 struct DevCtx {
     int dev = 0;
     int sms = 0;
@@ -478,6 +480,7 @@ int seed_async(DevCtx& c, Taus master, int64_t slot_begin, int64_t count, const 
     a.done = c.seed_done.p;
     a.report = c.d_mapped;
     c.spec_mapped = true;
+    *reinterpret_cast<volatile unsigned long long*>(c.h_mapped) = kCountPending;  // (no seeding in flight writes it)
     c.planes_of = nullptr;
     c.planes_count = -1;
     if (planes) {  // the walk's bitsliced pipeline follows: write its bit planes as well
@@ -492,12 +495,31 @@ int seed_async(DevCtx& c, Taus master, int64_t slot_begin, int64_t count, const 
 }
 
 // Specials of the last seed_async (synchronises the stream).
-int read_specials(DevCtx& c, cudaStream_t st, std::vector<SpecialRec>& sp, int64_t& n_total) {
+// seed_only: wait for the seeding alone (its last block stores the count to mapped host
+// memory) and leave the model running on the stream: a run into device buffers then
+// returns while its model kernel works, and the caller's next launches queue behind it.
+int read_specials(DevCtx& c, cudaStream_t st, std::vector<SpecialRec>& sp, int64_t& n_total, bool seed_only = false) {
     c.work_zeroed = false;
     unsigned long long n = 0;
     if (c.spec_mapped) {  // the seeding's last block stored it in mapped host memory
-        WLP_CUDA(cudaStreamSynchronize(st));
-        n = *reinterpret_cast<volatile unsigned long long*>(c.h_mapped);
+        volatile unsigned long long* v = reinterpret_cast<volatile unsigned long long*>(c.h_mapped);
+        bool synced = !seed_only;
+        if (seed_only) {
+            // spin on the word; every ~4k polls ask the stream, so a failed launch or a
+            // finished stream (the count then must be there) ends the wait
+            for (unsigned it = 1; *v == kCountPending; ++it) {
+                if ((it & 4095u) == 0u) {
+                    const cudaError_t q = cudaStreamQuery(st);
+                    if (q != cudaErrorNotReady) {
+                        synced = true;
+                        break;
+                    }
+                }
+            }
+        }
+        if (synced) WLP_CUDA(cudaStreamSynchronize(st));
+        n = *v;
+        if (n == kCountPending) return fail(WLP_EINTERNAL, "random_spacing: the seeding did not report its count");
     } else {
         WLP_CUDA(cudaMemcpyAsync(c.h_counter, c.counter.p + c.spec_read, 8, cudaMemcpyDeviceToHost, st));
         WLP_CUDA(cudaStreamSynchronize(st));
@@ -1288,7 +1310,7 @@ int wlp_run_shard(int model, const wlp_params* p, int mode, uint64_t master_seed
     if (specials || n_special || report || !out_on_device) {
         std::vector<SpecialRec> sp;
         int64_t nt = 0;
-        WLP_TRY(read_specials(*c, st, sp, nt));
+        WLP_TRY(read_specials(*c, st, sp, nt, out_on_device && !report));
         if (n_special) *n_special = nt;
         if (specials) std::memcpy(specials, sp.data(), std::min<int64_t>(nt, special_cap) * sizeof(SpecialRec));
     }
@@ -1344,7 +1366,7 @@ int wlp_run(int model, const wlp_params* p, int mode, uint64_t master_seed, int 
         }
         std::vector<SpecialRec> sp;
         int64_t nt = 0;
-        WLP_TRY(read_specials(*c, st, sp, nt));
+        WLP_TRY(read_specials(*c, st, sp, nt, out_on_device && !report && !ci));
         if (nt < 2) break;
         std::vector<int64_t> next;
         WLP_TRY(spacing_rejections(sp, rej, next));
