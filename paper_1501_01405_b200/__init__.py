@@ -800,7 +800,9 @@ def run_shard(model: ModelKind, p: ModelParams, mode: ExecutionMode, master_seed
               tlp_block_size: int = 256, special_cap: int = 4096, report: Optional[SimReport] = None):
     """Shard [r_begin, r_begin + r_count) of a run of p.replications; returns the shard's
     special seeding candidates. If `report` is given it is filled
-    with the model kernel's measured time (CUDA events on the launching stream)."""
+    with the model kernel's measured time (CUDA events on the launching stream). With
+    on_device and no report the call returns once the seeding has reported, the model
+    still running on `stream` (None: the legacy default stream, torch's default)."""
     o = [_ptr(x) for x in outs] + [None] * (3 - len(outs))
     rej = np.asarray(sorted(rejected), dtype=np.int64) if len(rejected) else None  # (usually empty)
     sp = _special_buffer(special_cap)
