@@ -142,4 +142,19 @@ TAUS_HD void bs_count_values(const BsCount& k, uint32_t (&v)[32]) {
     transpose32(v);
 }
 
+// Per-stream P - Q of two 16-digit counters with one transpose: row w < 16 holds P's
+// digit w, row 16 + w Q's digit w, so column j is stream j's P count in bits 0..15 and
+// its Q count in bits 16..31.
+TAUS_HD void bs_count_diff(const BsCount& P, const BsCount& Q, int32_t (&dx)[32]) {
+    uint32_t v[32];
+#pragma unroll
+    for (int w = 0; w < 16; ++w) {
+        v[w] = P.c[w];
+        v[16 + w] = Q.c[w];
+    }
+    transpose32(v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) dx[j] = static_cast<int32_t>(v[j] & 0xFFFFu) - static_cast<int32_t>(v[j] >> 16);
+}
+
 }  // namespace wlp

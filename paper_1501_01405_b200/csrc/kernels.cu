@@ -1381,11 +1381,10 @@ __global__ void __launch_bounds__(kBsBlock) k_tlp_walk_bs(RepArgs a) {
     if (flushing)
         for (int j = 0; j < 32; ++j) acc[j] = 0;
     auto flush = [&]() {
-        uint32_t pv[32], qv[32];
-        bs_count_values(P, pv);
-        bs_count_values(Q, qv);
+        int32_t d[32];
+        bs_count_diff(P, Q, d);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) acc[j] += static_cast<int32_t>(pv[j]) - static_cast<int32_t>(qv[j]);
+        for (int j = 0; j < 32; ++j) acc[j] += d[j];
         bs_count_init(P);
         bs_count_init(Q);
     };
@@ -1406,13 +1405,12 @@ __global__ void __launch_bounds__(kBsBlock) k_tlp_walk_bs(RepArgs a) {
         bs_count_add1(P, pl);
         bs_count_add1(Q, mi);
     }
-    uint32_t pv[32], qv[32];
-    bs_count_values(P, pv);
-    bs_count_values(Q, qv);
+    int32_t d[32];
+    bs_count_diff(P, Q, d);
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
         if (r0 + j >= a.count) break;
-        const int64_t dx = static_cast<int64_t>(pv[j]) - static_cast<int64_t>(qv[j]) + (flushing ? acc[j] : 0);
+        const int64_t dx = static_cast<int64_t>(d[j]) + (flushing ? acc[j] : 0);
         put1(a, r0 + j, walk_fold(dx, a.chunks));
     }
 }
@@ -1529,27 +1527,22 @@ __device__ __forceinline__ void bs_prefetch(uint32_t (*dst)[kBsLive], const uint
 // wrap group), written to out[0..31] (shared memory; out may alias d2, which is read
 // first).
 __device__ __forceinline__ void bs_dx_store(const uint32_t (&d)[32], const uint32_t* d2, int32_t* out) {
-    uint32_t pv[32], qv[32];
+    // One transpose of both counters at once: row w < 16 holds P's digit w, row 16 + w Q's,
+    // so column j comes out as stream j's P count in bits 0..15 and its Q count above
+    // (half the transposes and the live registers of two separate ones).
+    uint32_t v[32];
 #pragma unroll
-    for (int w = 0; w < 32; ++w) {
-        pv[w] = w < 16 ? d[w] : 0u;
-        qv[w] = w < 16 ? d[16 + w] : 0u;
-    }
-    transpose32(pv);
-    transpose32(qv);
+    for (int w = 0; w < 32; ++w) v[w] = d[w];
+    transpose32(v);
     int32_t dx[32];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) dx[j] = static_cast<int32_t>(pv[j]) - static_cast<int32_t>(qv[j]);
+    for (int j = 0; j < 32; ++j) dx[j] = static_cast<int32_t>(v[j] & 0xFFFFu) - static_cast<int32_t>(v[j] >> 16);
     if (d2) {
 #pragma unroll
-        for (int w = 0; w < 32; ++w) {
-            pv[w] = w < 16 ? d2[w] : 0u;
-            qv[w] = w < 16 ? d2[16 + w] : 0u;
-        }
-        transpose32(pv);
-        transpose32(qv);
+        for (int w = 0; w < 32; ++w) v[w] = d2[w];
+        transpose32(v);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) dx[j] += static_cast<int32_t>(pv[j]) - static_cast<int32_t>(qv[j]);
+        for (int j = 0; j < 32; ++j) dx[j] += static_cast<int32_t>(v[j] & 0xFFFFu) - static_cast<int32_t>(v[j] >> 16);
     }
 #pragma unroll
     for (int j = 0; j < 32; ++j) out[j] = dx[j];

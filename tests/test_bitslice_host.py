@@ -1,6 +1,7 @@
 """Bitsliced taus88 / walk algebra (csrc/bitslice.cuh) on the host: the 32x32 transpose,
 32 streams stepped bit-plane-wise against taus_next, and the carry-save walk counters
-against the scalar walk (models.hpp:86-108). Compiled with g++ from the same header the
+against the scalar walk (models.hpp:86-108), also read out through the one-transpose
+difference the kernels use. Compiled with g++ from the same header the
 kernel uses; no GPU."""
 import subprocess
 
@@ -46,6 +47,9 @@ int main() {
         uint32_t pv[32], qv[32];
         bs_count_values(P, pv); bs_count_values(Q, qv);
         for (int j = 0; j < 32; ++j) if ((long)pv[j] - (long)qv[j] != dx[j]) return 3;
+        int32_t dd[32];  // both counters through one transpose (the kernels' form)
+        bs_count_diff(P, Q, dd);
+        for (int j = 0; j < 32; ++j) if (dd[j] != dx[j]) return 6;
         transpose32(t.b1); transpose32(t.b2); transpose32(t.b3);
         for (int j = 0; j < 32; ++j)  // live bits (the top k of each component)
             if ((t.b1[j] ^ s[j].s1) & ~1u || (t.b2[j] ^ s[j].s2) & ~7u || (t.b3[j] ^ s[j].s3) & ~15u) return 4;
