@@ -32,9 +32,33 @@ TAUS_HD void transpose32_stage(uint32_t (&a)[32]) {
     }
 }
 
+#if defined(__CUDA_ARCH__)
+// The 16- and 8-bit stages move whole bytes: two PRMTs per row pair instead of the
+// shift/mask/xor swap (five instructions).
+__device__ __forceinline__ void transpose32_bytes(uint32_t (&a)[32]) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {  // (a[r], a[r+16]): low halves to a[r], high halves to a[r+16]
+        const uint32_t x = a[r], y = a[r + 16];
+        a[r] = __byte_perm(x, y, 0x5410);
+        a[r + 16] = __byte_perm(x, y, 0x7632);
+    }
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {  // (a[r], a[r+8]): even bytes to a[r], odd bytes to a[r+8]
+        if (r & 8) continue;
+        const uint32_t x = a[r], y = a[r + 8];
+        a[r] = __byte_perm(x, y, 0x6240);
+        a[r + 8] = __byte_perm(x, y, 0x7351);
+    }
+}
+#endif
+
 TAUS_HD void transpose32(uint32_t (&a)[32]) {
+#if defined(__CUDA_ARCH__)
+    transpose32_bytes(a);
+#else
     transpose32_stage<16, 0x0000FFFFu>(a);
     transpose32_stage<8, 0x00FF00FFu>(a);
+#endif
     transpose32_stage<4, 0x0F0F0F0Fu>(a);
     transpose32_stage<2, 0x33333333u>(a);
     transpose32_stage<1, 0x55555555u>(a);

@@ -428,9 +428,25 @@ struct Queue {
 // Seeding
 // ---------------------------------------------------------------------------------
 
+// Shared-memory staging of the seeding: slots are produced and written out in batches of
+// kB = min(PER, 32) slots per thread, 3 x [kSeedBlock][kRow] words. A batch of 32 uses
+// an XOR swizzle (word j of row r at r*32 + (j ^ r)) instead of a padded row: 12 KB per
+// block, so a whole 1e7-stream run (2,442 blocks of 32 threads at 128 slots) is resident
+// in one wave (17 blocks per SM) where the 128-slot padded staging (49.5 KB) allowed 4.
+__host__ __device__ constexpr int seed_batch(int per) { return per < 32 ? per : 32; }
+__host__ __device__ constexpr int seed_row(int per) { return seed_batch(per) == 32 ? 32 : seed_batch(per) + 1; }
+__host__ __device__ constexpr int seed_stage_words(int per) { return 3 * kSeedBlock * seed_row(per); }
+template <int PER>
+__device__ __forceinline__ int seed_sidx(int r, int j) {
+    return r * seed_row(PER) + (seed_batch(PER) == 32 ? (j ^ r) : j);
+}
+
 // One block of stream slots of one random_spacing run: slots [blk*B, (blk+1)*B) of
 // `count` (B = kSeedBlock * PER), slot i = candidate c(slot_begin + i) after
-// the sorted rejection list; keys land SoA at out[plane*stride + out_off + i].
+// the sorted rejection list; keys land SoA at out[plane*stride + out_off + i]. Thread t
+// walks the master stream over slots [t*PER, (t+1)*PER) of the block (one jump-ahead),
+// staging kB slots at a time; each batch is written out as kSeedBlock runs of kB
+// consecutive slots (coalesced), and for the walk as one bit-plane group per thread.
 template <int PER, bool STAGED = false>
 __device__ __forceinline__ void seed_block(const uint32_t* __restrict__ pw, Taus master, int64_t slot_begin,
                                            int64_t count, int64_t blk, const int64_t* __restrict__ rejected,
@@ -438,81 +454,136 @@ __device__ __forceinline__ void seed_block(const uint32_t* __restrict__ pw, Taus
                                            int64_t stride, SpecialRec* specials, int64_t special_cap,
                                            unsigned long long* n_special, uint32_t job,
                                            uint32_t* __restrict__ planes = nullptr, const uint32_t* spw = nullptr) {
-    extern __shared__ uint32_t sh[];  // 3 x [kSeedBlock][PER + 1] (padded: conflict-free)
-    constexpr int kRow = PER + 1;
-    constexpr int kPlane = kSeedBlock * kRow;
+    extern __shared__ uint32_t sh[];  // 3 x [kSeedBlock][kRow] (padded or swizzled: conflict-free)
+    constexpr int kB = seed_batch(PER);
+    constexpr int kPlane = kSeedBlock * seed_row(PER);
+    static_assert(PER % kB == 0, "whole batches");
     const int tid = threadIdx.x;
     const int64_t blk0 = blk * kSeedBlock * PER;
     const int64_t my0 = blk0 + static_cast<int64_t>(tid) * PER;
     const int64_t left = count - my0;
     const int nmine = left <= 0 ? 0 : (left < PER ? static_cast<int>(left) : PER);
+    int64_t c = slot_begin + my0;  // candidate index of my next slot
+    int64_t ri = 0;
+    Taus m{};
     if (nmine > 0) {
-        int64_t c = slot_begin + my0;  // candidate index of my first slot
-        int64_t ri = 0;
         while (ri < n_rejected && rejected[ri] <= c) {
             ++c;
             ++ri;
         }
-        Taus m = STAGED ? jump_pow_s(spw, master, 3ull * static_cast<uint64_t>(c))
-                        : jump_pow(pw, master, 3ull * static_cast<uint64_t>(c));
-        for (int j = 0; j < nmine; ++j) {
-            Taus key;
-            for (;;) {
-                const uint32_t x = taus_next(m), y = taus_next(m), z = taus_next(m);
-                key = make_state(x, y, z);
-                if (ri < n_rejected && rejected[ri] == c) {  // a redrawn candidate
-                    ++ri;
-                    ++c;
-                    continue;
-                }
-                break;
-            }
-            if (is_special_key(key)) {
-                const unsigned long long pos = atomicAdd(n_special, 1ull);
-                if (static_cast<int64_t>(pos) < special_cap) {
-                    SpecialRec* sp = specials + pos;
-                    sp->index = c;
-                    sp->s1 = key.s1;
-                    sp->s2 = key.s2;
-                    sp->s3 = key.s3;
-                    sp->pad = job;
-                }
-            }
-            ++c;
-            sh[tid * kRow + j] = key.s1;
-            sh[kPlane + tid * kRow + j] = key.s2;
-            sh[2 * kPlane + tid * kRow + j] = key.s3;
-        }
-    }
-    __syncthreads();
-    if (PER >= 32 && planes != nullptr) {  // the walk's bit planes, group by group (PER % 32 == 0)
-        for (int q = 0; q < PER / 32; ++q) {
-            const int64_t s0 = my0 + 32 * q;
-            if (s0 >= count) break;
-            BsTaus t;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const bool in = s0 + j < count;
-                const int si = tid * kRow + 32 * q + j;
-                t.b1[j] = in ? sh[si] : kMin1;
-                t.b2[j] = in ? sh[kPlane + si] : kMin2;
-                t.b3[j] = in ? sh[2 * kPlane + si] : kMin3;
-            }
-            bs_store_planes(t, planes + (s0 / 32) * kBsLive);
-        }
+        m = STAGED ? jump_pow_s(spw, master, 3ull * static_cast<uint64_t>(c))
+                   : jump_pow(pw, master, 3ull * static_cast<uint64_t>(c));
     }
     int64_t nblk = count - blk0;
     if (nblk > kSeedBlock * PER) nblk = kSeedBlock * PER;
-    for (int i = tid; i < nblk; i += kSeedBlock) {
-        const int si = (i / PER) * kRow + (i % PER);
-        out[out_off + blk0 + i] = sh[si];
-        out[stride + out_off + blk0 + i] = sh[kPlane + si];
-        out[2 * stride + out_off + blk0 + i] = sh[2 * kPlane + si];
+    // no redrawn candidate among my slots (the rule: rejections are rare collisions), so
+    // the slot loop needs no rejection test
+    const bool clean = ri >= n_rejected || rejected[ri] >= c + nmine;
+    const bool full_blk = nblk == kSeedBlock * PER;
+    auto special = [&](const Taus& key) {
+        if (is_special_key(key)) {
+            const unsigned long long pos = atomicAdd(n_special, 1ull);
+            if (static_cast<int64_t>(pos) < special_cap) {
+                SpecialRec* sp = specials + pos;
+                sp->index = c;
+                sp->s1 = key.s1;
+                sp->s2 = key.s2;
+                sp->s3 = key.s3;
+                sp->pad = job;
+            }
+        }
+    };
+    auto stage = [&](int j, const Taus& key) {
+        const int si = seed_sidx<PER>(tid, j);
+        sh[si] = key.s1;
+        sh[kPlane + si] = key.s2;
+        sh[2 * kPlane + si] = key.s3;
+    };
+#pragma unroll 1
+    for (int b0 = 0; b0 < PER && b0 < nblk; b0 += kB) {
+        const int nb = nmine - b0 < 0 ? 0 : (nmine - b0 < kB ? nmine - b0 : kB);
+        if (clean) {
+            for (int j = 0; j < nb; ++j) {
+                uint32_t x, y;
+                taus_next2(m, x, y);
+                const uint32_t z = taus_next(m);
+                const Taus key = make_state(x, y, z);
+                special(key);
+                ++c;
+                stage(j, key);
+            }
+        } else {
+            for (int j = 0; j < nb; ++j) {
+                Taus key;
+                for (;;) {
+                    const uint32_t x = taus_next(m), y = taus_next(m), z = taus_next(m);
+                    key = make_state(x, y, z);
+                    if (ri < n_rejected && rejected[ri] == c) {  // a redrawn candidate
+                        ++ri;
+                        ++c;
+                        continue;
+                    }
+                    break;
+                }
+                special(key);
+                ++c;
+                stage(j, key);
+            }
+        }
+        __syncthreads();
+        if (kB == 32 && planes != nullptr) {  // the walk's bit planes: this batch is one group
+            const int64_t s0 = my0 + b0;
+            if (s0 < count) {
+                BsTaus t;
+                if (s0 + 32 <= count) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int si = seed_sidx<PER>(tid, j);
+                        t.b1[j] = sh[si];
+                        t.b2[j] = sh[kPlane + si];
+                        t.b3[j] = sh[2 * kPlane + si];
+                    }
+                } else {  // a ragged last group: idle streams at the minimum state
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const bool in = s0 + j < count;
+                        const int si = seed_sidx<PER>(tid, j);
+                        t.b1[j] = in ? sh[si] : kMin1;
+                        t.b2[j] = in ? sh[kPlane + si] : kMin2;
+                        t.b3[j] = in ? sh[2 * kPlane + si] : kMin3;
+                    }
+                }
+                bs_store_planes(t, planes + (s0 / 32) * kBsLive);
+            }
+        }
+        if (kB == 32 && full_blk) {  // row r's batch is 32 consecutive slots: lane k stores slot k
+            uint32_t* o = out + out_off + blk0 + b0 + tid;
+#pragma unroll 8
+            for (int r = 0; r < kSeedBlock; ++r) {
+                const int si = seed_sidx<PER>(r, tid);
+                o[r * PER] = sh[si];
+                o[stride + r * PER] = sh[kPlane + si];
+                o[2 * stride + r * PER] = sh[2 * kPlane + si];
+            }
+        } else {
+            for (int i = tid; i < kSeedBlock * kB; i += kSeedBlock) {
+                const int r = i / kB, k = i % kB;
+                const int64_t g = blk0 + static_cast<int64_t>(r) * PER + b0 + k;  // (row r's slots are consecutive)
+                if (g < count) {
+                    const int si = seed_sidx<PER>(r, k);
+                    out[out_off + g] = sh[si];
+                    out[stride + out_off + g] = sh[kPlane + si];
+                    out[2 * stride + out_off + g] = sh[2 * kPlane + si];
+                }
+            }
+        }
+        __syncthreads();  // (the next batch overwrites the staging)
     }
 }
 
+// (at most 120 registers: 17 blocks of a 1e7-stream run per SM, its 2,442 blocks in one wave)
 template <int PER>
-__global__ void __launch_bounds__(kSeedBlock) k_seed(SeedArgs a) {
+__global__ void __maxnreg__(120) k_seed(SeedArgs a) {
     pdl_wait();     // (launched early behind the previous run's kernels: they read what this writes)
     pdl_trigger();  // the model kernel may launch now; it waits for this grid to complete
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -528,7 +599,7 @@ __global__ void __launch_bounds__(kSeedBlock) k_seed(SeedArgs a) {
         // flight and cost ~10 us of this ~10 us kernel.
         extern __shared__ __align__(16) uint32_t sh[];
         __shared__ __align__(8) uint64_t bar;
-        uint32_t* spw = sh + 3 * kSeedBlock * (PER + 1);
+        uint32_t* spw = sh + seed_stage_words(PER);
         const uint32_t bytes = static_cast<uint32_t>(a.stage_powers) * kUniTabWords * 4;
         const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bar));
         if (threadIdx.x == 0) {
@@ -2823,13 +2894,13 @@ cudaError_t launch_seed_per(const SeedArgs& a, cudaStream_t st) {
     const int64_t per_block = static_cast<int64_t>(kSeedBlock) * PER;
     const int64_t grid = (a.count + per_block - 1) / per_block;
     SeedArgs b = a;
-    size_t smem = 3 * kSeedBlock * (PER + 1) * 4;
+    size_t smem = seed_stage_words(PER) * 4;
     if (PER == 8) {  // stage the binary powers up to the largest jump (3 x the last candidate)
         const uint64_t last = 3ull * static_cast<uint64_t>(a.slot_begin + a.count + a.n_rejected);
         b.stage_powers = 64 - __builtin_clzll(last | 1ull);
         smem += static_cast<size_t>(b.stage_powers) * kUniTabWords * 4;
     }
-    allow_smem(k_seed<PER>, 3 * kSeedBlock * (PER + 1) * 4 + 64 * kUniTabWords * 4);
+    allow_smem(k_seed<PER>, seed_stage_words(PER) * 4 + 64 * kUniTabWords * 4);
     // PDL: the seeding may launch while the previous run's kernels drain (it waits for them
     // before touching memory), so the launch latency overlaps their tail
     const bool prev = t_pdl;
@@ -3092,7 +3163,7 @@ cudaError_t launch_seed_jobs(const uint32_t* powers, const SeedJob* d_jobs, int 
                              int64_t total_slots, uint32_t* out, void* specials, int64_t special_cap,
                              unsigned long long* n_special, cudaStream_t st) {
     if (total_blocks <= 0) return cudaSuccess;
-    const size_t smem = 3 * kSeedBlock * (kSeedJobPer + 1) * 4;
+    const size_t smem = seed_stage_words(kSeedJobPer) * 4;
     allow_smem(k_seed_jobs, smem);
     k_seed_jobs<<<static_cast<unsigned>(total_blocks), kSeedBlock, smem, st>>>(
         powers, d_jobs, n_jobs, out, total_slots, static_cast<SpecialRec*>(specials), special_cap, n_special);

@@ -74,6 +74,31 @@ def test_seed_shards_and_rejection_remap(gpu, port):
     assert np.array_equal(keys2, whole[:, keep[12_345:12_445]])
 
 
+def test_seed_batches_large_ragged(gpu, port):
+    # runs of >= 2^22 streams seed 128 slots per thread in batches of 32 (swizzled staging):
+    # a ragged count, a shard offset and rejections in the first and last batches
+    R = (1 << 22) + 1_000 + 17
+    whole = port.random_spacing(9, R + 520)
+    keys, _ = gpu.seed_streams(9, 0, R)
+    assert np.array_equal(keys, whole[:, :R])
+    rej = [3, 31, 32, 33, 127, 128, 4_096, R - 40, R - 1]
+    keep = np.array([i for i in range(R + 520) if i not in set(rej)])
+    keys, _ = gpu.seed_streams(9, 0, R, rejected=rej)
+    assert np.array_equal(keys, whole[:, keep[:R]])
+    keys, _ = gpu.seed_streams(9, 77, R - 500, rejected=rej)
+    assert np.array_equal(keys, whole[:, keep[77:77 + R - 500]])
+
+
+def test_walk_planes_from_batched_seeding(gpu, port):
+    # the bitsliced walk pipeline reads the bit planes the 128-slot seeding writes, one
+    # group per batch; a ragged last group (37 of 32 * k + 37 replications)
+    p = gpu.ModelParams(replications=(1 << 22) + 37, steps=48, chunks=7)
+    run = gpu.run_model(gpu.ModelKind.Walk, p, gpu.ExecutionMode.Wlp, master_seed=31337)
+    want = port.run_model(2, oracle.params_from(p), 31337)
+    assert np.array_equal(run.outputs["out"], want["out"]), \
+        gpu.last_kernel()
+
+
 def test_special_candidates_reported(gpu):
     # over many candidates some key component falls below twice its minimum
     keys, specials = gpu.seed_streams(11, 0, 3_000_000)
