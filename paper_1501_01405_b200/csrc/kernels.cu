@@ -581,6 +581,24 @@ __device__ __forceinline__ void seed_block(const uint32_t* __restrict__ pw, Taus
     }
 }
 
+// The last block of a seeding grid to finish stores the final specials count to `report`
+// (mapped pinned host memory: the host polls it, no copy launch) and rearms `done`;
+// `rearm_count` also clears the count (all other blocks' atomics are done by then).
+__device__ __forceinline__ void seed_report(unsigned int* done, unsigned long long* report,
+                                            unsigned long long* n_special, bool rearm_count) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(done, 1u) == gridDim.x - 1) {
+            __threadfence_system();  // the specials list before the count the host polls
+            *done = 0u;
+            const unsigned long long n = atomicAdd(n_special, 0ull);
+            if (rearm_count) *n_special = 0ull;
+            *reinterpret_cast<volatile unsigned long long*>(report) = n;
+        }
+    }
+}
+
 // (at most 120 registers: 17 blocks of a 1e7-stream run per SM, its 2,442 blocks in one wave)
 template <int PER>
 __global__ void __maxnreg__(120) k_seed(SeedArgs a) {
@@ -624,17 +642,7 @@ __global__ void __maxnreg__(120) k_seed(SeedArgs a) {
                         a.out_off, a.stride ? a.stride : a.count, static_cast<SpecialRec*>(a.specials),
                         a.special_cap, a.n_special, 0u, a.planes);
     }
-    if (a.report) {  // the last block reports the specials count to the host
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            if (atomicAdd(a.done, 1u) == gridDim.x - 1) {
-                __threadfence_system();  // the specials list before the count the host polls
-                *a.done = 0u;
-                *reinterpret_cast<volatile unsigned long long*>(a.report) = atomicAdd(a.n_special, 0ull);
-            }
-        }
-    }
+    if (a.report) seed_report(a.done, a.report, a.n_special, false);
 }
 
 // Many independent runs (one per plan set) in one launch; block -> job by binary search.
@@ -642,7 +650,12 @@ __global__ void __launch_bounds__(kSeedBlock) k_seed_jobs(const uint32_t* __rest
                                                           const SeedJob* __restrict__ jobs, int n_jobs,
                                                           uint32_t* __restrict__ out, int64_t total,
                                                           SpecialRec* specials, int64_t special_cap,
-                                                          unsigned long long* n_special) {
+                                                          unsigned long long* n_special,
+                                                          unsigned long long* zero_a, unsigned int* done,
+                                                          unsigned long long* report) {
+    pdl_wait();     // (may launch behind the previous plan's model, which reads the seeds)
+    pdl_trigger();  // the plan's model may launch now; it waits for this grid to complete
+    if (zero_a && blockIdx.x == 0 && threadIdx.x == 0) *zero_a = 0ull;  // the model's grab counter
     int lo = 0, hi = n_jobs - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -654,6 +667,7 @@ __global__ void __launch_bounds__(kSeedBlock) k_seed_jobs(const uint32_t* __rest
     const SeedJob& J = jobs[lo];
     seed_block<kSeedJobPer>(pw, J.master, 0, J.count, blockIdx.x - J.block0, nullptr, 0, out, J.out_off, total, specials,
                special_cap, n_special, static_cast<uint32_t>(lo));
+    if (report) seed_report(done, report, n_special, true);
 }
 
 constexpr int kTausPerThread = 64;
@@ -2555,6 +2569,7 @@ __global__ void __launch_bounds__(kWlpBlock, 3) k_plan_lanes(PlanArgs a, const u
     stage_u32<kLaneTabWords>(tab, gtab);
     for (int i = threadIdx.x; i < kUniTabWords; i += blockDim.x) skip[i] = __ldg(gskip + i);
     __syncthreads();
+    pdl_wait();  // (the seeding behind which it may launch: seeds and the grab counter)
     const int lane = threadIdx.x & 31;
     constexpr int64_t P = 32 * kPlanT;
     for (int64_t r = next_rep(a, lane); r < a.count; r = next_rep(a, lane)) {
@@ -2580,6 +2595,7 @@ __global__ void __launch_bounds__(kWlpBlock, 3) k_plan_lanes(PlanArgs a, const u
 __global__ void __launch_bounds__(kMm1Block) k_plan_mm1(PlanArgs a, const uint32_t* __restrict__ gtab,
                                                          const uint32_t* __restrict__ gskip) {
     const Mm1Smem m = mm1_stage(gtab, gskip);
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     for (int64_t r = next_rep(a, lane); r < a.count; r = next_rep(a, lane)) {
         const SetParam S = a.sets[find_set(a.sets, a.n_sets, r)];
@@ -2604,6 +2620,7 @@ __global__ void __launch_bounds__(kMm1Block) k_plan_mm1(PlanArgs a, const uint32
 
 template <int MODEL>
 __global__ void k_plan_tlp(PlanArgs a) {
+    pdl_wait();
     const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (r >= a.count) return;
     const SetParam S = a.sets[find_set(a.sets, a.n_sets, r)];
@@ -2617,6 +2634,7 @@ __global__ void k_plan_tlp_mm1(PlanArgs a) {
     TlpMm1Warp& W = reinterpret_cast<TlpMm1Warp*>(logtab + 256)[threadIdx.x >> 5];
     stage_log_table(logtab);
     __syncthreads();
+    pdl_wait();
     const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const unsigned mask = block_lane_mask();
@@ -3161,12 +3179,18 @@ int plan_blocks_per_sm(int model) {
 
 cudaError_t launch_seed_jobs(const uint32_t* powers, const SeedJob* d_jobs, int n_jobs, int64_t total_blocks,
                              int64_t total_slots, uint32_t* out, void* specials, int64_t special_cap,
-                             unsigned long long* n_special, cudaStream_t st) {
+                             unsigned long long* n_special, cudaStream_t st, unsigned long long* zero_a,
+                             unsigned int* done, unsigned long long* report) {
     if (total_blocks <= 0) return cudaSuccess;
     const size_t smem = seed_stage_words(kSeedJobPer) * 4;
     allow_smem(k_seed_jobs, smem);
-    k_seed_jobs<<<static_cast<unsigned>(total_blocks), kSeedBlock, smem, st>>>(
-        powers, d_jobs, n_jobs, out, total_slots, static_cast<SpecialRec*>(specials), special_cap, n_special);
+    const bool prev = t_pdl;
+    t_pdl = true;  // (as launch_seed_per: it waits for the previous kernels before touching memory)
+    const cudaError_t e = launch_ex(k_seed_jobs, static_cast<unsigned>(total_blocks), kSeedBlock, smem, st, powers,
+                                    d_jobs, n_jobs, out, total_slots, static_cast<SpecialRec*>(specials), special_cap,
+                                    n_special, zero_a, done, report);
+    t_pdl = prev;
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
@@ -3180,22 +3204,22 @@ cudaError_t launch_plan(int model, int mode, const PlanArgs& a, const uint32_t* 
         if (model == 1) {
             const size_t smem = tlp_mm1_smem(static_cast<int>(block));
             allow_smem(k_plan_tlp_mm1, smem);
-            k_plan_tlp_mm1<<<g, b, smem, st>>>(a);
+            launch_ex(k_plan_tlp_mm1, g, b, smem, st, a);
         } else if (model == 0) {
-            k_plan_tlp<0><<<g, b, 0, st>>>(a);
+            launch_ex(k_plan_tlp<0>, g, b, 0, st, a);
         } else {
-            k_plan_tlp<2><<<g, b, 0, st>>>(a);
+            launch_ex(k_plan_tlp<2>, g, b, 0, st, a);
         }
         return cudaGetLastError();
     }
     if (model == 1) {
-        k_plan_mm1<<<grid, kMm1Block, kMm1Smem, st>>>(a, mm1_lane, mm1_skip);
+        launch_ex(k_plan_mm1, grid, kMm1Block, kMm1Smem, st, a, mm1_lane, mm1_skip);
     } else {
         const size_t smem = (kLaneTabWords + kUniTabWords) * 4;
         if (model == 0)
-            k_plan_lanes<0><<<grid, kWlpBlock, smem, st>>>(a, lane_tab, uni_tab);
+            launch_ex(k_plan_lanes<0>, grid, kWlpBlock, smem, st, a, lane_tab, uni_tab);
         else
-            k_plan_lanes<2><<<grid, kWlpBlock, smem, st>>>(a, lane_tab, uni_tab);
+            launch_ex(k_plan_lanes<2>, grid, kWlpBlock, smem, st, a, lane_tab, uni_tab);
     }
     return cudaGetLastError();
 }

@@ -218,7 +218,8 @@ constexpr int kBsPipeBlock = 64;  // threads per block of the bitsliced walk pip
 // Plan: batched seeding (specials carry the job index in `pad`), then one model launch.
 cudaError_t launch_seed_jobs(const uint32_t* powers, const SeedJob* d_jobs, int n_jobs, int64_t total_blocks,
                              int64_t total_slots, uint32_t* out, void* specials, int64_t special_cap,
-                             unsigned long long* n_special, cudaStream_t st);
+                             unsigned long long* n_special, cudaStream_t st, unsigned long long* zero_a = nullptr,
+                             unsigned int* done = nullptr, unsigned long long* report = nullptr);
 // grid: persistent blocks for WLP; TLP uses `tlp_block` threads per block over all replications.
 cudaError_t launch_plan(int model, int mode, const PlanArgs& a, const uint32_t* lane_tab, const uint32_t* uni_tab,
                         const uint32_t* mm1_lane, const uint32_t* mm1_skip, int grid, int tlp_block,

@@ -117,7 +117,7 @@ struct DevCtx {
     // counter[0], [1]: the specials counts of alternate seedings (each seeding zeroes the
     // other for the next one, so no memset precedes it); [2]: the grab counter of the model
     // launch behind a seeding (zeroed by that seeding); [3], [4]: the plan's specials count
-    // and grab counter (memset per plan)
+    // (cleared by the plan seeding's last block) and grab counter (zeroed by the seeding)
     int spec_slot = 0;                   // the next seeding counts its specials in counter[spec_slot]
     int spec_read = 0;                   // the slot read_specials reads
     bool work_zeroed = false;            // counter[2] was cleared by the seeding just launched
@@ -132,6 +132,8 @@ struct DevCtx {
     unsigned char* h_stage = nullptr;         // pinned staging of small uploads (plan tables)
     size_t h_stage_cap = 0;
     DevBuf<unsigned char> plan_blob;          // the plan's SeedJob[] then SetParam[]
+    std::vector<unsigned char> plan_blob_host;  // ... as last uploaded (skip re-uploads of the same plan)
+    const unsigned char* plan_blob_dev = nullptr;
     DevBuf<int64_t> rejected;
     DevBuf<unsigned long long> work;
     DevBuf<unsigned long long> hw;  // instrumentation tallies [div, ld, st]
@@ -1755,7 +1757,13 @@ int wlp_run_plan(int model, const wlp_params* sets, const uint64_t* master_seeds
     std::memcpy(c->h_stage, jobs.data(), n_sets * sizeof(SeedJob));
     std::memcpy(c->h_stage + jobs_bytes, sp.data(), n_sets * sizeof(SetParam));
     WLP_CUDA(c->plan_blob.ensure(static_cast<int64_t>(blob)));
-    WLP_CUDA(cudaMemcpyAsync(c->plan_blob.p, c->h_stage, blob, cudaMemcpyHostToDevice, st));
+    // a plan re-run with the same sets (the usual sweep loop) finds its tables on the device
+    if (c->plan_blob_dev != c->plan_blob.p || c->plan_blob_host.size() != blob ||
+        std::memcmp(c->plan_blob_host.data(), c->h_stage, blob) != 0) {
+        WLP_CUDA(cudaMemcpyAsync(c->plan_blob.p, c->h_stage, blob, cudaMemcpyHostToDevice, st));
+        c->plan_blob_host.assign(c->h_stage, c->h_stage + blob);
+        c->plan_blob_dev = c->plan_blob.p;
+    }
     const SeedJob* d_jobs = reinterpret_cast<const SeedJob*>(c->plan_blob.p);
     const SetParam* d_setp = reinterpret_cast<const SetParam*>(c->plan_blob.p + jobs_bytes);
     double *o0 = out0, *o1 = out1, *o2 = out2;
@@ -1765,13 +1773,16 @@ int wlp_run_plan(int model, const wlp_params* sets, const uint64_t* master_seeds
         o1 = c->outs.p + R;
         o2 = c->outs.p + 2 * R;
     }
-    // one batched seeding launch for all sets, and the model right behind it; the spacing
-    // check below re-runs the model only when two special candidates share a key
-    WLP_CUDA(cudaMemsetAsync(c->counter.p + 3, 0, 16, st));  // the plan's specials count and grab counter
+    // one batched seeding launch for all sets, and the model right behind it (PDL: its
+    // prologue overlaps the seeding); the spacing check below re-runs the model only when
+    // two special candidates share a key. The seeding zeroes the model's grab counter
+    // (counter[4]), reports the specials count through mapped host memory and clears
+    // counter[3] behind it, so no memset or copy launch brackets the plan.
     c->spec_read = 3;
-    c->spec_mapped = false;
+    c->spec_mapped = true;
+    *reinterpret_cast<volatile unsigned long long*>(c->h_mapped) = kCountPending;
     WLP_CUDA(launch_seed_jobs(c->powers.p, d_jobs, n_sets, blocks, R, c->seeds.p, c->specials.p, kSpecialCap,
-                              c->counter.p + 3, st));
+                              c->counter.p + 3, st, c->counter.p + 4, c->seed_done.p, c->d_mapped));
     PlanArgs pa;
     pa.serial_rho = mm1_serial_rho();
     pa.tlp_div = all_rcp ? kDivRcp : kDivIeee;
@@ -1786,20 +1797,26 @@ int wlp_run_plan(int model, const wlp_params* sets, const uint64_t* master_seeds
     const int wpb = (model == WLP_MODEL_MM1 ? kMm1Block : kWlpBlock) / 32;
     const int grid = static_cast<int>(
         std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(c->sms) * c->plan_bps[model], (R + wpb - 1) / wpb)));
-    bool first = true;
+    bool first = true, first_pdl = true;
     auto run_model_launch = [&]() -> int {
         if (!first) WLP_CUDA(cudaMemsetAsync(pa.next, 0, 8, st));  // (the first was cleared with the count)
         first = false;
         if (report) WLP_CUDA(cudaEventRecord(c->ev0, st));
-        WLP_CUDA(launch_plan(model, mode, pa, c->plan_lane.p, c->plan_skip.p, c->mm1_lane.p, c->mm1_skip.p, grid,
-                             tlp_block_size, st));
+        set_pdl_launch(!report && first_pdl);  // (directly behind the seeding, not timed)
+        const cudaError_t e = launch_plan(model, mode, pa, c->plan_lane.p, c->plan_skip.p, c->mm1_lane.p,
+                                          c->mm1_skip.p, grid, tlp_block_size, st);
+        set_pdl_launch(false);
+        first_pdl = false;
+        WLP_CUDA(e);
         if (report) WLP_CUDA(cudaEventRecord(c->ev1, st));
         return WLP_OK;
     };
     WLP_TRY(run_model_launch());
     std::vector<SpecialRec> specials;
     int64_t nt = 0;
-    WLP_TRY(read_specials(*c, st, specials, nt));
+    // into device buffers without a report the call returns once the seeding has reported
+    // its specials count; the model keeps running on the stream
+    WLP_TRY(read_specials(*c, st, specials, nt, out_on_device && !report));
     // per set, a key collision (only ever between special candidates) re-seeds that set
     // exactly with its rejection list
     std::map<uint32_t, std::vector<SpecialRec>> by_job;
@@ -1838,7 +1855,10 @@ int wlp_run_plan(int model, const wlp_params* sets, const uint64_t* master_seeds
             WLP_TRY(spacing_rejections(sp2, rej, next));
         }
     }
-    if (reseeded) WLP_TRY(run_model_launch());
+    if (reseeded) {
+        WLP_CUDA(cudaMemsetAsync(c->counter.p + 3, 0, 8, st));  // (the plan seeding expects it zero)
+        WLP_TRY(run_model_launch());
+    }
     if (!out_on_device) {
         WLP_CUDA(cudaMemcpyAsync(out0, o0, R * 8, cudaMemcpyDeviceToHost, st));
         if (model == WLP_MODEL_MM1) {
