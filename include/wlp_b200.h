@@ -318,7 +318,9 @@ int wlp_exponentials(const double* u, int64_t n, double rate, double* out, int o
  * count and master seed — executed as ONE batched seeding launch and ONE model launch
  * (WLP: warps take replications from a global counter; TLP: thread per replication).
  * Outputs are concatenated in set order (set k starts at sum_{j<k} sets[j].replications)
- * and bit-identical to the n_sets separate runs. Units per replication < 2^32. */
+ * and bit-identical to the n_sets separate runs. Units per replication < 2^32. Into device
+ * buffers without a report it returns once the seeding has reported its specials count,
+ * the model still running on `stream`; host outputs or a report synchronise. */
 int wlp_run_plan(int model, const wlp_params* sets, const uint64_t* master_seeds, int n_sets, int mode,
                  int tlp_block_size, double* out0, double* out1, double* out2, int out_on_device,
                  void* stream, wlp_report* report);

@@ -68,8 +68,10 @@ def main():
             print("skip", raw, e)
             continue
         out = (src / f"{label}.stdout")
-        m = re.search(r"kernel (\S+)", out.read_text()) if out.exists() else None
+        m = re.search(r"\bkernel (k_\S+)", out.read_text()) if out.exists() else None
         d["kernel"] = m.group(1) if m else d["kernel_demangled"]
+        if "k_seed" in d["kernel_demangled"] or not m:  # (the seeding, or a plan: the name ncu reports)
+            d["kernel"] = re.sub(r"^(?:void )?(?:\w+>)?::(k_\w+(<[^>]*>)?).*$", r"\1", d["kernel_demangled"])
         res[label] = d
     lines = ["| capture | kernel (wlp_last_kernel) | ms | issue % | ALU % | FMA % | FP64 % | XU % | threads/warp-instr | "
              "branch uniform % | warps/SM | regs | warp-instr | DRAM MB | top stalls (per issue) |",
