@@ -556,7 +556,9 @@ __device__ __forceinline__ void seed_block(const uint32_t* __restrict__ pw, Taus
                 bs_store_planes(t, planes + (s0 / 32) * kBsLive);
             }
         }
-        if (kB == 32 && full_blk) {  // row r's batch is 32 consecutive slots: lane k stores slot k
+        if (kB == 32 && planes != nullptr) {
+            // the bitsliced walk pipeline reads the planes alone (its wrap groups' seeds too)
+        } else if (kB == 32 && full_blk) {  // row r's batch is 32 consecutive slots: lane k stores slot k
             uint32_t* o = out + out_off + blk0 + b0 + tid;
 #pragma unroll 8
             for (int r = 0; r < kSeedBlock; ++r) {
@@ -1678,19 +1680,25 @@ __global__ void __launch_bounds__(kBsPipeBlock, WLP_BS_MINB) k_wlp_walk_bs_pipe(
     int left = 0;
     if (WRAP) {  // lane p >= 1: wrap group p's 32 seeds jumped to chunk p, as bit planes,
         // one component at a time through the lane's row of the (still unused) result
-        // buffer, in loops that are not unrolled: the prologue stays small
-        const int64_t r0 = (wrap0 + pos - 1) * 32;
+        // buffer, in loops that are not unrolled: the prologue stays small. The seeds come
+        // from the group's bit planes (transposed back; the dead low bits read as 0 and
+        // never reach a live bit), so the seeding writes no SoA keys for this kernel.
+        const uint32_t* gpl = bseeds + (wrap0 + pos - 1) * kBsLive;
         uint32_t* row = E.cnt[lane];
-        const uint32_t fill[3] = {kMin1, kMin2, kMin3};
 #pragma unroll 1
         for (int comp = 0; comp < 3; ++comp) {
             if (pos > 0) {
+                const int dead = comp == 0 ? 1 : (comp == 1 ? 3 : 4);  // rows below the live bits
+                const int off = comp == 0 ? -1 : (comp == 1 ? 31 - 3 : 60 - 4);
+                uint32_t k[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) k[i] = i < dead ? 0u : __ldg(gpl + off + i);
+                transpose32(k);  // k[j]: stream j's component
+#pragma unroll
+                for (int j = 0; j < 32; ++j) row[j] = k[j];
                 const uint32_t* tab = wtab + comp * 4096 + lane;
 #pragma unroll 1
-                for (int j = 0; j < 32; ++j) {
-                    const int64_t r = r0 + j;
-                    row[j] = nib_apply_g32(tab, r < a.count ? __ldg(a.seeds + comp * a.count + r) : fill[comp]);
-                }
+                for (int j = 0; j < 32; ++j) row[j] = nib_apply_g32(tab, row[j]);
             }
             __syncwarp();
             uint32_t w[32];

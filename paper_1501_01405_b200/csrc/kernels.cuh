@@ -117,7 +117,7 @@ struct SeedArgs {
     int64_t stride = 0;  // 0: count
     // optional: the walk's bit planes of each group of 32 slots (88 live words per group,
     // the layout k_bs_seeds writes), so the bitsliced pipeline needs no separate pass
-    uint32_t* planes = nullptr;
+    uint32_t* planes = nullptr;  // (when set, the SoA keys are not written: the pipeline reads the planes alone)
     // optional words the seeding zeroes (block 0, before the model launch that follows):
     // the next run's specials count and the model's work counter (no memset launches)
     unsigned long long* zero_a = nullptr;
