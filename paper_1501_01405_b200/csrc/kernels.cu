@@ -2687,7 +2687,10 @@ __device__ __forceinline__ double stat_term(double x, int pass, double center) {
     return __dmul_rn(d, d);
 }
 
-constexpr int kStatsBlock = 256;
+// One 1024-thread block per SM for pass 1 and 2 (the same threads in flight as 4 blocks of
+// 256): 148 block partials, so the ordered device fold and the host merge of pass 2 walk
+// a quarter of the entries (fold ~17 -> ~5 us).
+constexpr int kStatsBlock = 1024;
 constexpr int64_t kStatsSeqMax = 256;
 
 __global__ void __launch_bounds__(kStatsBlock) k_stats(const double* __restrict__ x, int64_t n, int pass,
@@ -2788,7 +2791,7 @@ __global__ void __launch_bounds__(kStatsBlock) k_stats_seq(const double* __restr
 // The merge is one thread's ordered loop (the host's order, bit for bit); the warp first
 // stages the partials in shared memory, so the loop waits on DADD latencies only, not on
 // a global load per partial (headline step: ~53 -> ~10 us under ncu).
-constexpr int kFoldStage = 1024;  // partials staged (the stats grids have <= 4 per SM)
+constexpr int kFoldStage = 1024;  // partials staged (the stats grids have one block per SM)
 __global__ void k_stats_fold(const double* __restrict__ partials, int used, int64_t n, double* __restrict__ meta) {
     __shared__ double sp[2 * kFoldStage];
     if (blockIdx.x != 0) return;

@@ -830,7 +830,7 @@ void fill_report(DevCtx& c, int model, int mode, int tlp_block, int64_t count, i
 }
 
 int stats_device(DevCtx& c, const double* x, int64_t n, int pass, wlp_stats* s, cudaStream_t st) {
-    const int grid = std::max(1, std::min<int>(c.sms * 4, static_cast<int>((n + 255) / 256)));
+    const int grid = std::max(1, std::min<int>(c.sms, static_cast<int>((n + 1023) / 1024)));
     WLP_CUDA(c.partials.ensure(2 * grid));
     const double center = pass == 1 ? 0.0 : s->center;
     const bool seq = g_stats_order == 1;
@@ -904,7 +904,7 @@ int ci_enqueue(DevCtx& c, const double* const* d_x, int nout, int64_t n, double 
     plan.nout = nout;
     plan.n = n;
     plan.level = level;
-    plan.grid = std::max(1, std::min<int>(c.sms * 4, static_cast<int>((n + 255) / 256)));
+    plan.grid = std::max(1, std::min<int>(c.sms, static_cast<int>((n + 1023) / 1024)));
     const bool seq = g_stats_order == 1;
     plan.used = n <= 256 || seq ? 1 : plan.grid;
     const int64_t per = 4 + 4 * static_cast<int64_t>(plan.grid);  // meta[4], pass 1 [2g], pass 2 [2g]
