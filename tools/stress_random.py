@@ -23,7 +23,7 @@ t0, n, bad = time.time(), 0, 0
 while time.time() - t0 < budget:
     model = int(rng.integers(0, 3))
     if rng.random() < LARGE:  # large R with few units: the walk's pipeline / lane-chunk switch
-        R = int(rng.choice([100_000, 150_001, 400_000, 700_003, 1_000_000]))
+        R = int(rng.choice([100_000, 150_001, 400_000, 700_003, 1_000_000, 4_194_305, 5_000_003]))
         N = int(rng.choice([1, 16, 17, 33, 64, 100]))
     else:
         R = int(rng.choice([1, 7, 31, 32, 33, 63, 64, 65, 97, 128, 500, 1000, 4097, 6000]))
